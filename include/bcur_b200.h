@@ -1,0 +1,208 @@
+/*
+ * bcur_b200.h — C ABI of the B200-native Block-CUR hot path.
+ *
+ * Drop-in boundary for the reference's hot path (/root/reference/proj/include/bcur):
+ * every entry point below names the reference interface it replaces.  Plain
+ * pointers and sizes only; host arrays are caller-owned, device objects
+ * (bcur_ctx, bcur_dmat) are library-owned and released with *_destroy.
+ * A context is used by one host thread at a time.  All compute runs on the
+ * GPU (sm_100a); there is no CPU fallback — without a usable device every
+ * compute call returns BCUR_E_CUDA.
+ *
+ * Matrices are column-major with a leading dimension (Eigen's default,
+ * matcore.hpp:10), fp32 or fp64.  Block partitions are passed as G+1 strictly
+ * increasing column offsets covering [0, n) (BlockPartition, leverage.hpp:18-48).
+ */
+#ifndef BCUR_B200_H
+#define BCUR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:9-57 → status codes (C++ mirror maps them back to exceptions). */
+typedef enum {
+    BCUR_OK = 0,
+    BCUR_E_INVALID_ARGUMENT = 1,   /* std::invalid_argument */
+    BCUR_E_OUT_OF_RANGE = 2,       /* std::out_of_range */
+    BCUR_E_DIMENSION_MISMATCH = 3, /* DimensionMismatch */
+    BCUR_E_INVALID_BASIS = 4,      /* InvalidBasis */
+    BCUR_E_ZERO_BLOCK = 5,         /* ZeroBlock */
+    BCUR_E_ZERO_MATRIX = 6,        /* ZeroMatrix */
+    BCUR_E_DISTRIBUTION_INVALID = 7,
+    BCUR_E_NOT_ENOUGH_BLOCKS = 8,
+    BCUR_E_DEGENERATE_R = 9,
+    BCUR_E_ITERATION_FAILURE = 10,
+    BCUR_E_PARSE = 11,
+    BCUR_E_CUDA = 12,              /* device error / no device */
+    BCUR_E_COMM = 13               /* collective callback failed */
+} bcur_status;
+
+typedef enum { BCUR_F32 = 0, BCUR_F64 = 1 } bcur_dtype;
+
+/* sampler.hpp:11 SamplingMode */
+typedef enum { BCUR_WITH_REPLACEMENT = 0, BCUR_WITHOUT_REPLACEMENT = 1 } bcur_sampling_mode;
+
+typedef enum { BCUR_RESID_AUTO = -1, BCUR_RESID_PYTHAGORAS = 0, BCUR_RESID_EXPLICIT = 1 } bcur_residual_mode;
+
+typedef struct bcur_ctx_s* bcur_ctx;
+typedef struct bcur_dmat_s* bcur_dmat;
+typedef struct bcur_rng_s* bcur_rng;
+
+/* sampler.hpp:17-21 BlockDraw */
+typedef struct {
+    int64_t block;
+    double probability; /* original p_j */
+    double scale;       /* 1/sqrt(g·p_j) */
+} bcur_block_draw;
+
+/* ---------------------------------------------------------------- context */
+bcur_status bcur_ctx_create(int device, bcur_ctx* out);
+bcur_status bcur_ctx_destroy(bcur_ctx ctx);
+/* Run on a caller-owned cudaStream_t (NULL → library-owned stream). */
+bcur_status bcur_ctx_set_stream(bcur_ctx ctx, void* cuda_stream);
+void* bcur_ctx_stream(bcur_ctx ctx);
+bcur_status bcur_ctx_synchronize(bcur_ctx ctx);
+/* Number of kernels this context has launched so far (bench evidence). */
+int64_t bcur_ctx_launch_count(bcur_ctx ctx);
+
+/* Multi-GPU plumbing: one process (context) per GPU; the host supplies the
+ * collectives (e.g. torch.distributed over NCCL).  Callbacks run on the
+ * calling thread and must enqueue on `stream` (or complete before returning). */
+typedef struct {
+    int rank;
+    int world;
+    void* user;
+    /* in-place sum of `count` doubles at device pointer `buf` */
+    int (*allreduce_f64)(void* user, double* buf, int64_t count, void* stream);
+} bcur_comm;
+bcur_status bcur_ctx_set_comm(bcur_ctx ctx, const bcur_comm* comm); /* NULL → single rank */
+
+/* --------------------------------------------------------------- matrices */
+bcur_status bcur_dmat_create(bcur_ctx ctx, int dtype, int64_t m, int64_t n, bcur_dmat* out);
+/* Copies m×n column-major host data (leading dimension ld_host ≥ m). */
+bcur_status bcur_dmat_upload(bcur_ctx ctx, bcur_dmat a, const void* host, int64_t ld_host);
+bcur_status bcur_dmat_download(bcur_ctx ctx, bcur_dmat a, void* host, int64_t ld_host);
+/* Wraps caller-owned device memory (no copy, not freed by destroy). */
+bcur_status bcur_dmat_wrap(bcur_ctx ctx, int dtype, int64_t m, int64_t n, void* dev_ptr, int64_t ld,
+                           bcur_dmat* out);
+bcur_status bcur_dmat_info(bcur_dmat a, int* dtype, int64_t* m, int64_t* n, int64_t* ld, void** dev_ptr);
+/* Column shard: this matrix holds global columns [col0, col0+n) of an n_global-column matrix. */
+bcur_status bcur_dmat_set_shard(bcur_dmat a, int64_t col0, int64_t n_global);
+bcur_status bcur_dmat_destroy(bcur_dmat a);
+
+/* ------------------------------------------------------- synthetic inputs */
+typedef enum { BCUR_GEN_LOWRANK = 0, BCUR_GEN_BIOMETRIC = 1 } bcur_gen_kind;
+typedef struct {
+    int kind;            /* bcur_gen_kind */
+    int dtype;           /* bcur_dtype */
+    int64_t m, n;
+    int64_t rank;        /* LOWRANK: number of singular triples */
+    const double* sigma; /* LOWRANK: rank values */
+    double noise;        /* LOWRANK: iid N(0, noise²) */
+    uint64_t seed;
+    int64_t col0;        /* first global column to generate (column shards) */
+    int64_t n_global;    /* global column count (0 → n) */
+} bcur_gen_spec;
+/* A = U·diag(σ)·Vᵀ + ν·E (U, V Gaussian-then-orthonormalised) or the config-2
+ * biometric surrogate; Philox counters, so shards are independent of the split. */
+bcur_status bcur_dmat_generate(bcur_ctx ctx, const bcur_gen_spec* spec, bcur_dmat* out);
+
+/* ------------------------------------------------------------------- Rng */
+/* rng.hpp:13-63 (std::mt19937_64 + the reference's hand-written conversions). */
+bcur_status bcur_rng_create(uint64_t seed, bcur_rng* out);
+bcur_status bcur_rng_destroy(bcur_rng r);
+uint64_t bcur_rng_seed(bcur_rng r);
+uint64_t bcur_rng_next_u64(bcur_rng r);
+double bcur_rng_uniform01(bcur_rng r);
+uint64_t bcur_rng_below(bcur_rng r, uint64_t bound);
+double bcur_rng_normal(bcur_rng r);
+uint64_t bcur_rng_split_seed(bcur_rng r, uint64_t stream);
+/* Sketch key used by the pipelines: Rng(seed).split(0x6F6D656761).seed(). */
+uint64_t bcur_omega_key(uint64_t seed);
+
+/* ------------------------------------------------------ hot-path kernels */
+/* matcore.cpp:93-95 frobenius_norm */
+bcur_status bcur_frobenius_norm(bcur_ctx ctx, bcur_dmat a, double* out);
+/* per-block ‖A_g‖_F² (sketch.cpp:21-26 middleCols(..).squaredNorm()) */
+bcur_status bcur_block_sq_norms(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, double* out);
+/* leverage.cpp:108-121 block_leverage (+ require_orthonormal, leverage.cpp:11-23;
+ * tol < 0 → 1e-8 for fp64 input, 1e-4 for fp32). */
+bcur_status bcur_block_leverage(bcur_ctx ctx, bcur_dmat v_k, const int64_t* offsets, int64_t G, double tol,
+                                double* scores, double* normalizer);
+/* leverage.cpp:100-106 column_leverage */
+bcur_status bcur_column_leverage(bcur_ctx ctx, bcur_dmat v_k, double tol, double* scores, double* normalizer);
+/* N1: randomized range finder replacing truncate(svd(a), k) (matcore.cpp:39-69).
+ * Returns V_k (n×k_eff) and U_k (m×k_eff) fp64 device matrices (either out may be NULL),
+ * sigma (k_eff values, host, nullable). */
+bcur_status bcur_range_finder(bcur_ctx ctx, bcur_dmat a, int64_t k, int64_t p, int64_t q, uint64_t key,
+                              bcur_dmat* v_out, bcur_dmat* u_out, double* sigma_out, int64_t* k_eff);
+/* sampler.cpp:116-146 draw_blocks (probabilities on the host, one uniform per draw
+ * drawn by the caller from its Rng; margins_out[t] = distance of u_t to the nearest
+ * CDF edge, nullable). */
+bcur_status bcur_draw_blocks(bcur_ctx ctx, const double* probs, int64_t G, int64_t g, int mode,
+                             const double* uniforms, uint64_t seed, bcur_block_draw* out, double* margins_out);
+/* sampler.cpp:161-184 materialize_columns; row blocks = column blocks of Aᵀ. */
+bcur_status bcur_materialize_columns(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G,
+                                     const bcur_block_draw* draws, int64_t ndraws, bcur_dmat* out);
+bcur_status bcur_materialize_row_blocks(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G,
+                                        const bcur_block_draw* draws, int64_t ndraws, bcur_dmat* out);
+/* blockcur.cpp:33-52 error_report: abs_err = ‖A − C(UR)‖_F, a_norm = ‖A‖_F. */
+bcur_status bcur_error_report(bcur_ctx ctx, bcur_dmat a, bcur_dmat c, bcur_dmat u, bcur_dmat r, double* abs_err,
+                              double* a_norm);
+
+/* ------------------------------------------------------- whole pipelines */
+typedef struct {
+    int64_t k, p, q;    /* range finder: rank, oversampling, power iterations */
+    int64_t g;          /* blocks to select (column blocks for CUR) */
+    int64_t g_rows;     /* CUR: row blocks to select */
+    int mode;           /* bcur_sampling_mode */
+    int residual;       /* bcur_residual_mode */
+    uint64_t seed;      /* Rng seed: sketch key = bcur_omega_key(seed) */
+} bcur_options;
+
+typedef struct {
+    double abs_err;     /* ‖A − C C⁺ A‖_F  (CUR: ‖A − C U R‖_F) */
+    double a_norm;      /* ‖A‖_F */
+    double rel_err;     /* abs_err / a_norm */
+    int64_t k_eff;      /* rank of the subspace used for scores */
+    int64_t rank_c;     /* numerical rank of C (CUR: of C) */
+    int64_t rank_r;     /* CUR: numerical rank of R */
+    int residual_path;  /* 0 Pythagoras, 1 explicit */
+    double orth_dev;    /* max |V_kᵀV_k − I| (require_orthonormal evidence) */
+} bcur_report;
+
+/* R15 block_css (sketch.cpp:68-82): scores → draws (uniforms[g] from the caller's
+ * Rng) → C → ‖A − CC⁺A‖_F.  scores_out[G], draws_out[g], margins_out[g] nullable. */
+bcur_status bcur_block_css(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, const bcur_options* opt,
+                           const double* uniforms, double* scores_out, double* normalizer_out,
+                           bcur_block_draw* draws_out, double* margins_out, bcur_report* rep);
+
+/* N3 greedy deterministic selection. */
+typedef struct {
+    int64_t block;
+    double score;       /* residual ‖(I−P_C)A_g‖² at pick time (or leverage if saturated) */
+    double margin;      /* top1 − top2 of the criterion */
+    int saturated;
+    int64_t rank_added;
+} bcur_greedy_step;
+bcur_status bcur_greedy_select(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, const bcur_options* opt,
+                               bcur_greedy_step* steps_out, double* residuals_out, bcur_report* rep);
+
+/* N4 block CUR with row and column blocks, U = C⁺AR⁺ (uniforms: g column draws
+ * then g_rows row draws).  u_out (c×r column-major, ldu) nullable. */
+bcur_status bcur_block_cur(bcur_ctx ctx, bcur_dmat a, const int64_t* col_offsets, int64_t Gc,
+                           const int64_t* row_offsets, int64_t Gr, const bcur_options* opt, const double* uniforms,
+                           double* col_scores, double* row_scores, bcur_block_draw* col_draws,
+                           bcur_block_draw* row_draws, double* u_out, int64_t ldu, bcur_report* rep);
+
+/* Thread-local message of the last failing call. */
+const char* bcur_last_error(void);
+const char* bcur_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BCUR_B200_H */

@@ -1,0 +1,597 @@
+// capi.cu — the C ABI (include/bcur_b200.h).  Validates arguments with the
+// reference's error semantics (errors.hpp:9-57, sampler.cpp, leverage.cpp,
+// blockcur.cpp), converts exceptions to bcur_status + a thread-local message,
+// and forwards to the device pipeline.
+#include <cmath>
+#include <cstring>
+#include <random>
+#include <string>
+
+#include "pipeline.h"
+
+using namespace bcur_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+bcur_status set_error(bcur_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define API_BEGIN try {
+#define API_END                                                                  \
+    return BCUR_OK;                                                              \
+    }                                                                            \
+    catch (const Failure& f) { return set_error(f.status, f.what()); }           \
+    catch (const std::bad_alloc&) { return set_error(BCUR_E_CUDA, "host allocation failed"); } \
+    catch (const std::exception& e) { return set_error(BCUR_E_INVALID_ARGUMENT, e.what()); }
+
+Ctx* C(bcur_ctx c) {
+    if (!c) fail(BCUR_E_INVALID_ARGUMENT, "null context");
+    CUDA_CHECK(cudaSetDevice(c->device));
+    return c;
+}
+DMat* M(bcur_dmat a) {
+    if (!a) fail(BCUR_E_INVALID_ARGUMENT, "null matrix");
+    return a;
+}
+
+void check_dtype(int dt) {
+    if (dt != BCUR_F32 && dt != BCUR_F64) fail(BCUR_E_INVALID_ARGUMENT, "dtype must be BCUR_F32 or BCUR_F64");
+}
+
+void check_partition(const int64_t* off, int64_t G, int64_t n, const char* what) {
+    if (!off || G < 1) fail(BCUR_E_INVALID_ARGUMENT, std::string(what) + ": at least one block required");
+    if (off[0] != 0) fail(BCUR_E_INVALID_ARGUMENT, std::string(what) + ": ranges must start at 0");
+    for (int64_t g = 0; g < G; ++g)
+        if (off[g + 1] <= off[g])
+            fail(BCUR_E_INVALID_ARGUMENT, std::string(what) + ": ranges must be contiguous, non-empty, and ordered");
+    if (n >= 0 && off[G] != n) fail(BCUR_E_DIMENSION_MISMATCH, std::string(what) + ": partition does not match matrix");
+}
+
+bcur_dmat new_dmat(Ctx* c, int dt, int64_t m, int64_t n) {
+    auto* d = new bcur_dmat_s();
+    d->ctx = c;
+    d->dtype = dt;
+    d->m = m;
+    d->n = n;
+    d->ld = std::max<int64_t>(m, 1);
+    d->owned = true;
+    const size_t bytes = (size_t)d->ld * (size_t)std::max<int64_t>(n, 1) * dtype_size(dt);
+    cudaError_t e = cudaMalloc(&d->ptr, bytes);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        c->trim();
+        e = cudaMalloc(&d->ptr, bytes);
+        if (e != cudaSuccess) {
+            delete d;
+            fail(BCUR_E_CUDA, std::string("cudaMalloc of matrix failed: ") + cudaGetErrorString(e));
+        }
+    }
+    return d;
+}
+
+bcur_dmat from_mat64(Ctx* c, const Mat64& x, int64_t m, int64_t n) {
+    bcur_dmat d = new_dmat(c, BCUR_F64, m, n);
+    if (m * n > 0)
+        CUDA_CHECK(cudaMemcpy2DAsync(d->ptr, d->ld * 8, x.p(), x.ld * 8, m * 8, n, cudaMemcpyDeviceToDevice, c->stream));
+    c->sync();
+    return d;
+}
+
+double sumsq(Ctx* c, const DMat* a) {
+    if (a->m * a->n == 0) return 0.0;
+    const int64_t off[2] = {0, a->n};
+    DevBuf d_off(c, sizeof off), out(c, sizeof(double));
+    CUDA_CHECK(cudaMemcpyAsync(d_off.ptr, off, sizeof off, cudaMemcpyHostToDevice, c->stream));
+    ops::block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, d_off.as<int64_t>(), 1, out.as<double>());
+    if (a->n_global > a->n) allreduce(c, out.as<double>(), 1);
+    double h = 0.0;
+    CUDA_CHECK(cudaMemcpyAsync(&h, out.ptr, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return h;
+}
+
+// require_orthonormal (leverage.cpp:11-23) on the device Gram VᵀV.
+void require_orthonormal(Ctx* c, const DMat* v, double tol, const char* what) {
+    if (v->m < 1 || v->n < 1) fail(BCUR_E_INVALID_BASIS, std::string(what) + ": basis must be non-empty");
+    if (v->m < v->n) fail(BCUR_E_INVALID_BASIS, std::string(what) + ": more columns than rows cannot be orthonormal");
+    if (tol < 0) tol = v->dtype == BCUR_F32 ? 1e-4 : 1e-8;
+    Mat64 g(c, v->n, v->n), dev(c, 1, 1);
+    ops::gemm(c, ops::OP_T, ops::OP_N, v->n, v->n, v->m, 1.0, v->ptr, v->dtype, v->ld, v->ptr, v->dtype, v->ld, 0.0,
+              g.p(), g.ld);
+    ops::max_dev_identity(c, g.p(), v->n, g.ld, dev.p());
+    double h = 0.0;
+    CUDA_CHECK(cudaMemcpyAsync(&h, dev.p(), sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (!(h <= tol))
+        fail(BCUR_E_INVALID_BASIS, std::string(what) + ": column Gram deviates from identity by " + std::to_string(h));
+}
+
+void upload_draws(Ctx* c, const bcur_block_draw* draws, int64_t nd, const int64_t* off, int64_t G, int64_t* total,
+                  DevBuf* d_draws, DevBuf* d_dst, DevBuf* d_off) {
+    std::vector<int64_t> dst(nd);
+    int64_t t = 0;
+    for (int64_t i = 0; i < nd; ++i) {
+        if (draws[i].block < 0 || draws[i].block >= G)
+            fail(BCUR_E_DIMENSION_MISMATCH, "materialize: plan references block " + std::to_string(draws[i].block) +
+                                                " outside the partition");
+        dst[i] = t;
+        t += off[draws[i].block + 1] - off[draws[i].block];
+    }
+    *total = t;
+    *d_draws = DevBuf(c, nd * sizeof(bcur_block_draw));
+    *d_dst = DevBuf(c, nd * sizeof(int64_t));
+    *d_off = DevBuf(c, (G + 1) * sizeof(int64_t));
+    CUDA_CHECK(cudaMemcpyAsync(d_draws->ptr, draws, nd * sizeof(bcur_block_draw), cudaMemcpyHostToDevice, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_dst->ptr, dst.data(), nd * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(d_off->ptr, off, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    c->sync();
+}
+
+}  // namespace
+
+struct bcur_rng_s {
+    uint64_t seed;
+    std::mt19937_64 engine;
+    double spare = 0.0;
+    bool has_spare = false;
+    explicit bcur_rng_s(uint64_t s) : seed(s), engine(s) {}
+    double uniform01() { return (double)(engine() >> 11) * 0x1.0p-53; }  // rng.hpp:22
+};
+
+extern "C" {
+
+const char* bcur_last_error(void) { return g_last_error.c_str(); }
+const char* bcur_version(void) { return "bcur_b200 0.1.0 (sm_100a)"; }
+
+// ------------------------------------------------------------- context
+bcur_status bcur_ctx_create(int device, bcur_ctx* out) {
+    API_BEGIN
+    if (!out) fail(BCUR_E_INVALID_ARGUMENT, "null output");
+    int count = 0;
+    cudaError_t e = cudaGetDeviceCount(&count);
+    if (e != cudaSuccess || count == 0) {
+        (void)cudaGetLastError();
+        fail(BCUR_E_CUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) fail(BCUR_E_INVALID_ARGUMENT, "device index out of range");
+    CUDA_CHECK(cudaSetDevice(device));
+    auto* c = new bcur_ctx_s();
+    c->device = device;
+    CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    c->own_stream = true;
+    CUDA_CHECK(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    *out = c;
+    API_END
+}
+
+bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
+    API_BEGIN
+    if (!ctx) return BCUR_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->trim();
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    API_END
+}
+
+bcur_status bcur_ctx_set_stream(bcur_ctx ctx, void* s) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    c->sync();
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (s) {
+        c->stream = (cudaStream_t)s;
+        c->own_stream = false;
+    } else {
+        CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    API_END
+}
+
+void* bcur_ctx_stream(bcur_ctx ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+bcur_status bcur_ctx_synchronize(bcur_ctx ctx) {
+    API_BEGIN
+    C(ctx)->sync();
+    API_END
+}
+
+int64_t bcur_ctx_launch_count(bcur_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+bcur_status bcur_ctx_set_comm(bcur_ctx ctx, const bcur_comm* comm) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    if (!comm) {
+        c->comm = bcur_comm{0, 1, nullptr, nullptr};
+    } else {
+        if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world)
+            fail(BCUR_E_INVALID_ARGUMENT, "bcur_comm: invalid rank/world");
+        if (comm->world > 1 && !comm->allreduce_f64) fail(BCUR_E_INVALID_ARGUMENT, "bcur_comm: allreduce_f64 required");
+        c->comm = *comm;
+    }
+    API_END
+}
+
+// -------------------------------------------------------------- matrices
+bcur_status bcur_dmat_create(bcur_ctx ctx, int dtype, int64_t m, int64_t n, bcur_dmat* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    check_dtype(dtype);
+    if (m < 0 || n < 0 || !out) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_create: bad shape");
+    *out = new_dmat(c, dtype, m, n);
+    API_END
+}
+
+bcur_status bcur_dmat_upload(bcur_ctx ctx, bcur_dmat a, const void* host, int64_t ld_host) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (ld_host < d->m) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_upload: ld_host < m");
+    const size_t es = dtype_size(d->dtype);
+    if (d->m * d->n > 0)
+        CUDA_CHECK(cudaMemcpy2DAsync(d->ptr, d->ld * es, host, ld_host * es, d->m * es, d->n, cudaMemcpyHostToDevice,
+                                     c->stream));
+    c->sync();
+    API_END
+}
+
+bcur_status bcur_dmat_download(bcur_ctx ctx, bcur_dmat a, void* host, int64_t ld_host) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (ld_host < d->m) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_download: ld_host < m");
+    const size_t es = dtype_size(d->dtype);
+    if (d->m * d->n > 0)
+        CUDA_CHECK(cudaMemcpy2DAsync(host, ld_host * es, d->ptr, d->ld * es, d->m * es, d->n, cudaMemcpyDeviceToHost,
+                                     c->stream));
+    c->sync();
+    API_END
+}
+
+bcur_status bcur_dmat_wrap(bcur_ctx ctx, int dtype, int64_t m, int64_t n, void* dev_ptr, int64_t ld, bcur_dmat* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    check_dtype(dtype);
+    if (m < 0 || n < 0 || ld < std::max<int64_t>(m, 1) || !out) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_wrap: bad shape");
+    auto* d = new bcur_dmat_s();
+    d->ctx = c;
+    d->dtype = dtype;
+    d->m = m;
+    d->n = n;
+    d->ld = ld;
+    d->ptr = dev_ptr;
+    d->owned = false;
+    *out = d;
+    API_END
+}
+
+bcur_status bcur_dmat_info(bcur_dmat a, int* dtype, int64_t* m, int64_t* n, int64_t* ld, void** dev_ptr) {
+    API_BEGIN
+    DMat* d = M(a);
+    if (dtype) *dtype = d->dtype;
+    if (m) *m = d->m;
+    if (n) *n = d->n;
+    if (ld) *ld = d->ld;
+    if (dev_ptr) *dev_ptr = d->ptr;
+    API_END
+}
+
+bcur_status bcur_dmat_set_shard(bcur_dmat a, int64_t col0, int64_t n_global) {
+    API_BEGIN
+    DMat* d = M(a);
+    if (col0 < 0 || n_global < col0 + d->n) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_set_shard: bad shard");
+    d->col0 = col0;
+    d->n_global = n_global;
+    API_END
+}
+
+bcur_status bcur_dmat_destroy(bcur_dmat a) {
+    API_BEGIN
+    if (!a) return BCUR_OK;
+    if (a->owned && a->ptr) {
+        cudaSetDevice(a->ctx->device);
+        cudaStreamSynchronize(a->ctx->stream);
+        cudaFree(a->ptr);
+    }
+    delete a;
+    API_END
+}
+
+bcur_status bcur_dmat_generate(bcur_ctx ctx, const bcur_gen_spec* spec, bcur_dmat* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    if (!spec || !out) fail(BCUR_E_INVALID_ARGUMENT, "null spec/output");
+    check_dtype(spec->dtype);
+    const int64_t m = spec->m, n = spec->n;
+    const int64_t ng = spec->n_global > 0 ? spec->n_global : n;
+    if (m < 1 || n < 1 || spec->col0 < 0 || spec->col0 + n > ng) fail(BCUR_E_INVALID_ARGUMENT, "generate: bad shape");
+    bcur_dmat d = new_dmat(c, spec->dtype, m, n);
+    try {
+        if (spec->kind == BCUR_GEN_LOWRANK) {
+            const int64_t r = spec->rank;
+            if (r < 1 || r > std::min(m, ng) || !spec->sigma) fail(BCUR_E_INVALID_ARGUMENT, "generate: need 1 <= rank <= min(m, n)");
+            // Gaussian factors → orthonormal (positive-diagonal CholQR2), U scaled by σ
+            Mat64 U0(c, m, r), V0(c, ng, r), U(c, m, r), V(c, ng, r), sg(c, r, 1);
+            ops::gaussian_matrix(c, spec->seed, 1, m, r, U0.p(), U0.ld);
+            ops::gaussian_matrix(c, spec->seed, 2, ng, r, V0.p(), V0.ld);
+            if (orth(c, U0.p(), m, r, U0.ld, -1.0, BCUR_F64, U.p(), U.ld, false, nullptr, nullptr) != r ||
+                orth(c, V0.p(), ng, r, V0.ld, -1.0, BCUR_F64, V.p(), V.ld, false, nullptr, nullptr) != r)
+                fail(BCUR_E_ITERATION_FAILURE, "generate: factor orthonormalisation lost rank");
+            CUDA_CHECK(cudaMemcpyAsync(sg.p(), spec->sigma, r * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+            ops::scale_columns(c, U.p(), m, r, U.ld, sg.p());
+            ops::lowrank_assemble(c, U.p(), V.p(), m, n, r, spec->col0, ng, spec->noise, spec->seed, d->ptr, d->dtype,
+                                  d->ld);
+        } else if (spec->kind == BCUR_GEN_BIOMETRIC) {
+            ops::biometric(c, m, n, spec->col0, ng, spec->seed, d->ptr, d->dtype, d->ld);
+        } else {
+            fail(BCUR_E_INVALID_ARGUMENT, "generate: unknown kind");
+        }
+        c->sync();
+    } catch (...) {
+        bcur_dmat_destroy(d);
+        throw;
+    }
+    d->col0 = spec->col0;
+    d->n_global = ng;
+    *out = d;
+    API_END
+}
+
+// ------------------------------------------------------------------- Rng
+bcur_status bcur_rng_create(uint64_t seed, bcur_rng* out) {
+    API_BEGIN
+    if (!out) fail(BCUR_E_INVALID_ARGUMENT, "null output");
+    *out = new bcur_rng_s(seed);
+    API_END
+}
+bcur_status bcur_rng_destroy(bcur_rng r) {
+    delete r;
+    return BCUR_OK;
+}
+uint64_t bcur_rng_seed(bcur_rng r) { return r->seed; }
+uint64_t bcur_rng_next_u64(bcur_rng r) { return r->engine(); }
+double bcur_rng_uniform01(bcur_rng r) { return r->uniform01(); }
+uint64_t bcur_rng_below(bcur_rng r, uint64_t bound) {  // rng.hpp:25-32
+    const uint64_t limit = bound * (UINT64_MAX / bound);
+    uint64_t x = r->engine();
+    while (x >= limit) x = r->engine();
+    return x % bound;
+}
+double bcur_rng_normal(bcur_rng r) {  // rng.hpp:35-47
+    if (r->has_spare) {
+        r->has_spare = false;
+        return r->spare;
+    }
+    const double u1 = 1.0 - r->uniform01();
+    const double u2 = r->uniform01();
+    const double radius = std::sqrt(-2.0 * std::log(u1));
+    const double angle = 2.0 * 3.14159265358979323846 * u2;
+    r->spare = radius * std::sin(angle);
+    r->has_spare = true;
+    return radius * std::cos(angle);
+}
+static uint64_t split_seed(uint64_t seed, uint64_t stream) {  // rng.hpp:51-56
+    uint64_t z = seed + 0x9e3779b97f4a7c15ULL * (stream + 1);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+uint64_t bcur_rng_split_seed(bcur_rng r, uint64_t stream) { return split_seed(r->seed, stream); }
+uint64_t bcur_omega_key(uint64_t seed) { return split_seed(seed, 0x6F6D656761ULL); }
+
+// ---------------------------------------------------------------- kernels
+bcur_status bcur_frobenius_norm(bcur_ctx ctx, bcur_dmat a, double* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (!out) fail(BCUR_E_INVALID_ARGUMENT, "null output");
+    *out = std::sqrt(sumsq(c, d));
+    API_END
+}
+
+bcur_status bcur_block_sq_norms(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, double* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    check_partition(offsets, G, d->n, "block_sq_norms");
+    DevBuf off(c, (G + 1) * sizeof(int64_t)), res(c, G * sizeof(double));
+    CUDA_CHECK(cudaMemcpyAsync(off.ptr, offsets, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    ops::block_sumsq(c, d->ptr, d->dtype, d->m, d->ld, off.as<int64_t>(), G, res.as<double>());
+    CUDA_CHECK(cudaMemcpyAsync(out, res.ptr, G * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    API_END
+}
+
+bcur_status bcur_block_leverage(bcur_ctx ctx, bcur_dmat v_k, const int64_t* offsets, int64_t G, double tol,
+                                double* scores, double* normalizer) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* v = M(v_k);
+    require_orthonormal(c, v, tol, "block_leverage");
+    check_partition(offsets, G, -1, "block_leverage");
+    if (offsets[G] != v->m) fail(BCUR_E_DIMENSION_MISMATCH, "block_leverage: partition size does not match V_k rows");
+    DevBuf off(c, (G + 1) * sizeof(int64_t)), res(c, G * sizeof(double));
+    CUDA_CHECK(cudaMemcpyAsync(off.ptr, offsets, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    ops::row_sumsq_blocks(c, v->ptr, v->dtype, v->m, v->n, v->ld, off.as<int64_t>(), G, nullptr, res.as<double>());
+    CUDA_CHECK(cudaMemcpyAsync(scores, res.ptr, G * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (normalizer) *normalizer = (double)v->n;
+    API_END
+}
+
+bcur_status bcur_column_leverage(bcur_ctx ctx, bcur_dmat v_k, double tol, double* scores, double* normalizer) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* v = M(v_k);
+    require_orthonormal(c, v, tol, "column_leverage");
+    DevBuf res(c, v->m * sizeof(double));
+    ops::row_sumsq_blocks(c, v->ptr, v->dtype, v->m, v->n, v->ld, nullptr, 0, res.as<double>(), nullptr);
+    CUDA_CHECK(cudaMemcpyAsync(scores, res.ptr, v->m * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (normalizer) *normalizer = (double)v->n;
+    API_END
+}
+
+bcur_status bcur_range_finder(bcur_ctx ctx, bcur_dmat a, int64_t k, int64_t p, int64_t q, uint64_t key,
+                              bcur_dmat* v_out, bcur_dmat* u_out, double* sigma_out, int64_t* k_eff) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (d->m < 1 || d->n < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: matrix must be non-empty");
+    Subspace s;
+    range_finder(c, d, k, p, q, key, &s);
+    if (v_out) *v_out = from_mat64(c, s.v, d->n, s.k_eff);
+    if (u_out) *u_out = from_mat64(c, s.u, d->m, s.k_eff);
+    if (sigma_out) std::memcpy(sigma_out, s.sigma.data(), s.k_eff * sizeof(double));
+    if (k_eff) *k_eff = s.k_eff;
+    API_END
+}
+
+bcur_status bcur_draw_blocks(bcur_ctx ctx, const double* probs, int64_t G, int64_t g, int mode, const double* uniforms,
+                             uint64_t seed, bcur_block_draw* out, double* margins_out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    (void)seed;
+    if (g < 1) fail(BCUR_E_INVALID_ARGUMENT, "draw_blocks: g must be >= 1");
+    if (G < 1 || !probs) fail(BCUR_E_DISTRIBUTION_INVALID, "empty probability vector");
+    if (mode != BCUR_WITH_REPLACEMENT && mode != BCUR_WITHOUT_REPLACEMENT) fail(BCUR_E_INVALID_ARGUMENT, "bad mode");
+    DevBuf dp(c, G * sizeof(double)), du(c, g * sizeof(double)), dd(c, g * sizeof(bcur_block_draw)),
+        dm(c, g * sizeof(double)), st(c, 16);
+    CUDA_CHECK(cudaMemcpyAsync(dp.ptr, probs, G * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(du.ptr, uniforms, g * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    ops::distribution_draw(c, dp.as<double>(), G, 0, g, mode, du.as<double>(), dd.as<bcur_block_draw>(), dm.as<double>(),
+                           st.as<int>());
+    int status = 0;
+    CUDA_CHECK(cudaMemcpyAsync(&status, st.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (status == BCUR_E_DISTRIBUTION_INVALID) fail(BCUR_E_DISTRIBUTION_INVALID, "draw_blocks: probabilities invalid or do not sum to 1");
+    if (status == BCUR_E_NOT_ENOUGH_BLOCKS)
+        fail(BCUR_E_NOT_ENOUGH_BLOCKS, "draw_blocks: asked for " + std::to_string(g) + " distinct blocks but too few have positive probability");
+    if (status != BCUR_OK) fail((bcur_status)status, "draw_blocks failed");
+    CUDA_CHECK(cudaMemcpyAsync(out, dd.ptr, g * sizeof(bcur_block_draw), cudaMemcpyDeviceToHost, c->stream));
+    if (margins_out)
+        CUDA_CHECK(cudaMemcpyAsync(margins_out, dm.ptr, g * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    API_END
+}
+
+static bcur_status materialize(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G,
+                               const bcur_block_draw* draws, int64_t nd, int rows, bcur_dmat* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    const int64_t dim = rows ? d->m : d->n;
+    check_partition(offsets, G, -1, "materialize");
+    if (offsets[G] != dim)
+        fail(BCUR_E_DIMENSION_MISMATCH, rows ? "materialize_rows: A rows do not match partition"
+                                             : "materialize_columns: A columns do not match partition");
+    if (nd < 1 || !draws) fail(BCUR_E_INVALID_ARGUMENT, "materialize: empty plan");
+    int64_t total = 0;
+    DevBuf dd, dst, doff;
+    upload_draws(c, draws, nd, offsets, G, &total, &dd, &dst, &doff);
+    bcur_dmat o = rows ? new_dmat(c, d->dtype, total, d->n) : new_dmat(c, d->dtype, d->m, total);
+    ops::gather_blocks(c, d->ptr, d->dtype, d->m, d->n, d->ld, doff.as<int64_t>(), dd.as<bcur_block_draw>(),
+                       dst.as<int64_t>(), nd, rows, 1, o->ptr, o->dtype, o->ld);
+    c->sync();
+    *out = o;
+    API_END
+}
+
+bcur_status bcur_materialize_columns(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G,
+                                     const bcur_block_draw* draws, int64_t nd, bcur_dmat* out) {
+    return materialize(ctx, a, offsets, G, draws, nd, 0, out);
+}
+bcur_status bcur_materialize_row_blocks(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G,
+                                        const bcur_block_draw* draws, int64_t nd, bcur_dmat* out) {
+    return materialize(ctx, a, offsets, G, draws, nd, 1, out);
+}
+
+bcur_status bcur_error_report(bcur_ctx ctx, bcur_dmat a, bcur_dmat cm, bcur_dmat um, bcur_dmat rm, double* abs_err,
+                              double* a_norm) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat *A = M(a), *Cm = M(cm), *U = M(um), *R = M(rm);
+    if (Cm->m != A->m || R->n != A->n || U->m != Cm->n || U->n != R->m)
+        fail(BCUR_E_DIMENSION_MISMATCH, "error_report: C U R shapes do not compose to the shape of A");
+    // UR (c × n) then Σ (A − C·UR)²
+    Mat64 UR(c, U->m, A->n), tot(c, 1, 1);
+    ops::gemm(c, ops::OP_N, ops::OP_N, U->m, A->n, U->n, 1.0, U->ptr, U->dtype, U->ld, R->ptr, R->dtype, R->ld, 0.0,
+              UR.p(), UR.ld);
+    ops::gemm_resid_sumsq(c, ops::OP_N, ops::OP_N, A->m, A->n, Cm->n, Cm->ptr, Cm->dtype, Cm->ld, UR.p(), BCUR_F64,
+                          UR.ld, A->ptr, A->dtype, A->ld, tot.p());
+    double h = 0.0;
+    CUDA_CHECK(cudaMemcpyAsync(&h, tot.p(), sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (abs_err) *abs_err = std::sqrt(std::max(h, 0.0));
+    if (a_norm) *a_norm = std::sqrt(sumsq(c, A));
+    API_END
+}
+
+// --------------------------------------------------------------- pipelines
+bcur_status bcur_block_css(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, const bcur_options* opt,
+                           const double* uniforms, double* scores_out, double* normalizer_out,
+                           bcur_block_draw* draws_out, double* margins_out, bcur_report* rep) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (!opt || !uniforms) fail(BCUR_E_INVALID_ARGUMENT, "block_css: null options/uniforms");
+    if (opt->mode != BCUR_WITH_REPLACEMENT && opt->mode != BCUR_WITHOUT_REPLACEMENT) fail(BCUR_E_INVALID_ARGUMENT, "bad mode");
+    check_partition(offsets, G, -1, "block_css");
+    CssOut o;
+    block_css(c, d, offsets, G, *opt, uniforms, &o);
+    if (scores_out) std::memcpy(scores_out, o.scores.data(), G * sizeof(double));
+    if (normalizer_out) *normalizer_out = o.normalizer;
+    if (draws_out) std::memcpy(draws_out, o.draws.data(), o.draws.size() * sizeof(bcur_block_draw));
+    if (margins_out) std::memcpy(margins_out, o.margins.data(), o.margins.size() * sizeof(double));
+    if (rep) *rep = o.rep;
+    API_END
+}
+
+bcur_status bcur_greedy_select(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, const bcur_options* opt,
+                               bcur_greedy_step* steps_out, double* residuals_out, bcur_report* rep) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (!opt) fail(BCUR_E_INVALID_ARGUMENT, "greedy_select: null options");
+    check_partition(offsets, G, -1, "greedy_select");
+    GreedyOut o;
+    greedy_select(c, d, offsets, G, *opt, &o);
+    if (steps_out) std::memcpy(steps_out, o.steps.data(), o.steps.size() * sizeof(bcur_greedy_step));
+    if (residuals_out) std::memcpy(residuals_out, o.residuals.data(), G * sizeof(double));
+    if (rep) *rep = o.rep;
+    API_END
+}
+
+bcur_status bcur_block_cur(bcur_ctx ctx, bcur_dmat a, const int64_t* col_offsets, int64_t Gc,
+                           const int64_t* row_offsets, int64_t Gr, const bcur_options* opt, const double* uniforms,
+                           double* col_scores, double* row_scores, bcur_block_draw* col_draws,
+                           bcur_block_draw* row_draws, double* u_out, int64_t ldu, bcur_report* rep) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (!opt || !uniforms) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: null options/uniforms");
+    check_partition(col_offsets, Gc, -1, "block_cur columns");
+    check_partition(row_offsets, Gr, d->m, "block_cur rows");
+    CurOut o;
+    block_cur(c, d, col_offsets, Gc, row_offsets, Gr, *opt, uniforms, u_out != nullptr, &o);
+    if (col_scores) std::memcpy(col_scores, o.col_scores.data(), Gc * sizeof(double));
+    if (row_scores) std::memcpy(row_scores, o.row_scores.data(), Gr * sizeof(double));
+    if (col_draws) std::memcpy(col_draws, o.col_draws.data(), o.col_draws.size() * sizeof(bcur_block_draw));
+    if (row_draws) std::memcpy(row_draws, o.row_draws.data(), o.row_draws.size() * sizeof(bcur_block_draw));
+    if (u_out && o.u_valid) {
+        if (ldu < o.u.m) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: ldu < c");
+        CUDA_CHECK(cudaMemcpy2DAsync(u_out, ldu * 8, o.u.p(), o.u.ld * 8, o.u.m * 8, o.u.n, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+    }
+    if (rep) *rep = o.rep;
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,155 @@
+// common.cuh — runtime core shared by every translation unit of libbcur_b200.so:
+// error model (errors.hpp:9-57 → bcur_status), device context (stream, pooled
+// workspace, collective plumbing), device matrix handle (column-major + ld).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bcur_b200.h"
+
+namespace bcur_b200 {
+
+// ------------------------------------------------------------------ errors
+struct Failure : std::runtime_error {
+    bcur_status status;
+    Failure(bcur_status s, const std::string& msg) : std::runtime_error(msg), status(s) {}
+};
+
+[[noreturn]] inline void fail(bcur_status s, const std::string& msg) { throw Failure(s, msg); }
+
+inline void check_cuda(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess) {
+        fail(BCUR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" + std::to_string(line) + ")");
+    }
+}
+#define CUDA_CHECK(x) ::bcur_b200::check_cuda((x), #x, __FILE__, __LINE__)
+#define LAUNCH_CHECK(ctx) do { (ctx)->launches++; ::bcur_b200::check_cuda(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); } while (0)
+
+inline size_t dtype_size(int dt) { return dt == BCUR_F32 ? 4 : 8; }
+
+// ---------------------------------------------------------------- context
+struct Ctx;
+
+// Pooled device allocation (returned to the context's free list on release).
+struct DevBuf {
+    Ctx* ctx = nullptr;
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(Ctx* c, size_t b);
+    ~DevBuf();
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), ptr(o.ptr), bytes(o.bytes) { o.ptr = nullptr; o.ctx = nullptr; }
+    DevBuf& operator=(DevBuf&& o) noexcept;
+    template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 148;
+    int64_t launches = 0;
+    bcur_comm comm{0, 1, nullptr, nullptr};
+    std::multimap<size_t, void*> free_list;
+    size_t pooled_bytes = 0;
+    // pinned host staging for small device→host reads
+    void* pinned = nullptr;
+    size_t pinned_bytes = 0;
+
+    void* acquire(size_t bytes) {
+        size_t want = round(bytes);
+        auto it = free_list.lower_bound(want);
+        if (it != free_list.end() && it->first <= want + want / 2 + (1 << 20)) {
+            void* p = it->second;
+            free_list.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) {
+            (void)cudaGetLastError();
+            trim();
+            CUDA_CHECK(cudaMalloc(&p, want));
+        }
+        sizes[p] = want;
+        return p;
+    }
+    void release(void* p) {
+        if (!p) return;
+        free_list.emplace(sizes[p], p);
+    }
+    void trim() {
+        cudaStreamSynchronize(stream);
+        for (auto& kv : free_list) {
+            cudaFree(kv.second);
+            sizes.erase(kv.second);
+        }
+        free_list.clear();
+    }
+    static size_t round(size_t b) {
+        if (b < 256) return 256;
+        const size_t g = b < (1u << 20) ? 256 : (1u << 20);
+        return (b + g - 1) / g * g;
+    }
+    void* host_stage(size_t bytes) {
+        if (bytes > pinned_bytes) {
+            if (pinned) cudaFreeHost(pinned);
+            pinned_bytes = bytes < (1u << 20) ? (1u << 20) : bytes;
+            CUDA_CHECK(cudaMallocHost(&pinned, pinned_bytes));
+        }
+        return pinned;
+    }
+    void sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
+    std::map<void*, size_t> sizes;
+};
+
+inline DevBuf::DevBuf(Ctx* c, size_t b) : ctx(c), bytes(b) { ptr = b ? c->acquire(b) : nullptr; }
+inline DevBuf::~DevBuf() {
+    if (ctx && ptr) ctx->release(ptr);
+}
+inline DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+        if (ctx && ptr) ctx->release(ptr);
+        ctx = o.ctx; ptr = o.ptr; bytes = o.bytes;
+        o.ptr = nullptr; o.ctx = nullptr;
+    }
+    return *this;
+}
+
+// Device matrix: column-major, leading dimension ld (elements).
+struct DMat {
+    Ctx* ctx = nullptr;
+    int dtype = BCUR_F64;
+    int64_t m = 0, n = 0, ld = 0;
+    void* ptr = nullptr;
+    bool owned = false;
+    int64_t col0 = 0, n_global = 0;  // column shard
+    size_t bytes() const { return (size_t)ld * (size_t)n * dtype_size(dtype); }
+};
+
+// Lightweight non-owning view used by kernels wrappers.
+template <class T>
+struct View {
+    T* p;
+    int64_t m, n, ld;
+    __host__ __device__ T& operator()(int64_t i, int64_t j) const { return p[i + j * ld]; }
+};
+
+}  // namespace bcur_b200
+
+// Opaque handle types of the C ABI.
+struct bcur_ctx_s : bcur_b200::Ctx {};
+struct bcur_dmat_s : bcur_b200::DMat {};
+
+__host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }

@@ -1,0 +1,108 @@
+// kernels_misc.cu — layout/elementwise helpers (dtype conversion, scaling, copies).
+#include "ops.h"
+
+namespace bcur_b200 {
+namespace {
+
+template <class T>
+__global__ void k_convert(const T* __restrict__ src, int64_t m, int64_t n, int64_t lds, double* __restrict__ dst,
+                          int64_t ldd) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m * n) return;
+    const int64_t i = e % m, j = e / m;
+    dst[i + j * ldd] = (double)src[i + j * lds];
+}
+
+template <class T>
+__global__ void k_transpose(const T* __restrict__ src, int64_t m, int64_t n, int64_t lds, double* __restrict__ dst,
+                            int64_t ldd) {
+    __shared__ double tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + threadIdx.x, j = j0 + r;
+        if (i < m && j < n) tile[r][threadIdx.x] = (double)src[i + j * lds];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + threadIdx.x, i = i0 + r;  // dst(j, i) = src(i, j)
+        if (i < m && j < n) dst[j + i * ldd] = tile[threadIdx.x][r];
+    }
+}
+
+__global__ void k_fill(double* p, int64_t count, double v) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < count) p[e] = v;
+}
+
+__global__ void k_scale_columns(double* x, int64_t m, int64_t n, int64_t ld, const double* __restrict__ s) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m * n) return;
+    const int64_t i = e % m, j = e / m;
+    x[i + j * ld] *= s[j];
+}
+
+__global__ void k_copy(const double* __restrict__ src, int64_t m, int64_t n, int64_t lds, double* __restrict__ dst,
+                       int64_t ldd) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m * n) return;
+    const int64_t i = e % m, j = e / m;
+    dst[i + j * ldd] = src[i + j * lds];
+}
+
+__global__ void k_axpy_neg(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) y[e] -= x[e];
+}
+
+inline unsigned nblk(int64_t count) { return (unsigned)((count + 255) / 256); }
+
+}  // namespace
+
+namespace ops {
+
+void axpy_neg(Ctx* c, const double* x, double* y, int64_t n) {
+    if (n <= 0) return;
+    k_axpy_neg<<<nblk(n), 256, 0, c->stream>>>(x, y, n);
+    LAUNCH_CHECK(c);
+}
+
+void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
+    if (m * n == 0) return;
+    if (dt == BCUR_F32)
+        k_convert<float><<<nblk(m * n), 256, 0, c->stream>>>((const float*)src, m, n, lds, dst, ldd);
+    else
+        k_convert<double><<<nblk(m * n), 256, 0, c->stream>>>((const double*)src, m, n, lds, dst, ldd);
+    LAUNCH_CHECK(c);
+}
+
+void transpose_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
+    if (m * n == 0) return;
+    dim3 grid((unsigned)((m + 31) / 32), (unsigned)((n + 31) / 32));
+    dim3 block(32, 8);
+    if (dt == BCUR_F32)
+        k_transpose<float><<<grid, block, 0, c->stream>>>((const float*)src, m, n, lds, dst, ldd);
+    else
+        k_transpose<double><<<grid, block, 0, c->stream>>>((const double*)src, m, n, lds, dst, ldd);
+    LAUNCH_CHECK(c);
+}
+
+void fill_f64(Ctx* c, double* p, int64_t count, double v) {
+    if (count <= 0) return;
+    k_fill<<<nblk(count), 256, 0, c->stream>>>(p, count, v);
+    LAUNCH_CHECK(c);
+}
+
+void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale) {
+    if (m * n == 0) return;
+    k_scale_columns<<<nblk(m * n), 256, 0, c->stream>>>(x, m, n, ld, d_scale);
+    LAUNCH_CHECK(c);
+}
+
+void copy_f64(Ctx* c, const double* src, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
+    if (m * n == 0) return;
+    k_copy<<<nblk(m * n), 256, 0, c->stream>>>(src, m, n, lds, dst, ldd);
+    LAUNCH_CHECK(c);
+}
+
+}  // namespace ops
+}  // namespace bcur_b200

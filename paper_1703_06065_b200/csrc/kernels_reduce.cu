@@ -1,0 +1,203 @@
+// kernels_reduce.cu — HBM-streaming reductions with fp64 accumulation.
+//
+//  * block_sumsq      ‖A_g‖_F² per column block (sketch.cpp:21-26), whose sum is
+//                     ‖A‖_F² (matcore.cpp:93-95).  Pure streaming pass over A.
+//  * row_sumsq_blocks block leverage ℓ_g = Σ_{j∈g} ‖V_k[j,:]‖² (leverage.cpp:108-121),
+//                     coalesced along the rows of column-major V_k.
+// All sums are deterministic (fixed-order partials, no floating atomics), so a
+// rerun with the same inputs reproduces results bit-for-bit.
+#include "ops.h"
+
+namespace bcur_b200 {
+namespace {
+
+constexpr int RT = 256;
+
+__device__ __forceinline__ double warp_sum(double s) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// Fixed-order block reduction of one value per thread (RT threads).
+__device__ double block_sum(double s) {
+    __shared__ double red[32];
+    s = warp_sum(s);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[w] = s;
+    __syncthreads();
+    double t = 0.0;
+    if (w == 0) {
+        t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+        t = warp_sum(t);
+    }
+    return t;  // valid in thread 0
+}
+
+template <class T>
+__device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, bool vec) {
+    double s0 = 0.0, s1 = 0.0;
+    if (vec && sizeof(T) == 4) {
+        const float4* c4 = reinterpret_cast<const float4*>(col);
+        const int64_t m4 = m >> 2;
+        for (int64_t i = threadIdx.x; i < m4; i += RT) {
+            const float4 v = __ldcs(c4 + i);
+            s0 = fma((double)v.x, (double)v.x, s0);
+            s1 = fma((double)v.y, (double)v.y, s1);
+            s0 = fma((double)v.z, (double)v.z, s0);
+            s1 = fma((double)v.w, (double)v.w, s1);
+        }
+        for (int64_t i = (m4 << 2) + threadIdx.x; i < m; i += RT) {
+            const double v = (double)col[i];
+            s0 = fma(v, v, s0);
+        }
+    } else if (vec) {
+        const double2* c2 = reinterpret_cast<const double2*>(col);
+        const int64_t m2 = m >> 1;
+        for (int64_t i = threadIdx.x; i < m2; i += RT) {
+            const double2 v = __ldcs(c2 + i);
+            s0 = fma(v.x, v.x, s0);
+            s1 = fma(v.y, v.y, s1);
+        }
+        for (int64_t i = (m2 << 1) + threadIdx.x; i < m; i += RT) {
+            const double v = (double)col[i];
+            s0 = fma(v, v, s0);
+        }
+    } else {
+        for (int64_t i = threadIdx.x; i < m; i += RT) {
+            const double v = (double)col[i];
+            s0 = fma(v, v, s0);
+        }
+    }
+    return s0 + s1;
+}
+
+// grid (G, Z): CTA (g, z) sums columns off[g]+z, off[g]+z+Z, ...
+template <class T>
+__global__ void __launch_bounds__(RT) k_block_sumsq(const T* __restrict__ a, int64_t m, int64_t ld,
+                                                    const int64_t* __restrict__ off, int Z, bool vec,
+                                                    double* __restrict__ partial) {
+    const int64_t g = blockIdx.x;
+    const int z = blockIdx.y;
+    double s = 0.0;
+    for (int64_t j = off[g] + z; j < off[g + 1]; j += Z) s += sq_col(a + j * ld, m, vec);
+    s = block_sum(s);
+    if (threadIdx.x == 0) partial[g * Z + z] = s;
+}
+
+__global__ void k_segment_rows(const double* __restrict__ partial, int Z, int64_t G, double* __restrict__ out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    double s = 0.0;
+    for (int z = 0; z < Z; ++z) s += partial[g * Z + z];
+    out[g] = s;
+}
+
+template <class T>
+__global__ void k_row_sumsq(const T* __restrict__ v, int64_t n, int64_t k, int64_t ld, double* __restrict__ rows) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    double s = 0.0;
+    for (int64_t c = 0; c < k; ++c) {
+        const double x = (double)v[j + c * ld];
+        s = fma(x, x, s);
+    }
+    rows[j] = s;
+}
+
+// one warp per segment
+__global__ void k_segment_sum(const double* __restrict__ x, const int64_t* __restrict__ off, int64_t G,
+                              double* __restrict__ out) {
+    const int64_t g = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (g >= G) return;
+    double s = 0.0;
+    for (int64_t j = off[g] + lane; j < off[g + 1]; j += 32) s += x[j];
+    s = warp_sum(s);
+    if (lane == 0) out[g] = s;
+}
+
+__global__ void k_sum_vector(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) s += x[i];
+    s = block_sum(s);
+    if (threadIdx.x == 0) out[0] = s;
+}
+
+__global__ void k_max_dev_identity(const double* __restrict__ g, int64_t w, int64_t ld, double* __restrict__ out) {
+    double mx = 0.0;
+    for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
+        const int64_t i = e % w, j = e / w;
+        const double d = fabs(g[i + j * ld] - (i == j ? 1.0 : 0.0));
+        mx = d > mx || d != d ? d : mx;  // NaN propagates
+    }
+    __shared__ double red[RT];
+    red[threadIdx.x] = mx;
+    __syncthreads();
+    for (int s = RT / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) {
+            const double o = red[threadIdx.x + s];
+            if (o > red[threadIdx.x] || o != o) red[threadIdx.x] = o;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = red[0];
+}
+
+}  // namespace
+
+namespace ops {
+
+void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
+                 double* d_out) {
+    if (G <= 0) return;
+    // enough CTAs to fill the machine several times over
+    int Z = (int)std::max<int64_t>(1, std::min<int64_t>(64, (8LL * c->sm_count + G - 1) / G));
+    const size_t es = dtype_size(dt);
+    const bool vec = ((ld * es) % 16 == 0) && (((uintptr_t)a) % 16 == 0);
+    DevBuf part(c, (size_t)G * Z * sizeof(double));
+    dim3 grid((unsigned)G, (unsigned)Z);
+    if (dt == BCUR_F32)
+        k_block_sumsq<float><<<grid, RT, 0, c->stream>>>((const float*)a, m, ld, d_offsets, Z, vec, part.as<double>());
+    else
+        k_block_sumsq<double><<<grid, RT, 0, c->stream>>>((const double*)a, m, ld, d_offsets, Z, vec, part.as<double>());
+    LAUNCH_CHECK(c);
+    k_segment_rows<<<(unsigned)((G + 255) / 256), 256, 0, c->stream>>>(part.as<double>(), Z, G, d_out);
+    LAUNCH_CHECK(c);
+}
+
+void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64_t ld, const int64_t* d_offsets,
+                      int64_t G, double* d_rows, double* d_blocks) {
+    DevBuf tmp;
+    if (!d_rows) {
+        tmp = DevBuf(c, (size_t)n * sizeof(double));
+        d_rows = tmp.as<double>();
+    }
+    if (dt == BCUR_F32)
+        k_row_sumsq<float><<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>((const float*)v, n, k, ld, d_rows);
+    else
+        k_row_sumsq<double><<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>((const double*)v, n, k, ld, d_rows);
+    LAUNCH_CHECK(c);
+    if (d_blocks) segment_sum(c, d_rows, d_offsets, G, d_blocks);
+}
+
+void segment_sum(Ctx* c, const double* x, const int64_t* d_offsets, int64_t G, double* d_out) {
+    if (G <= 0) return;
+    const int64_t threads = G * 32;
+    k_segment_sum<<<(unsigned)((threads + 255) / 256), 256, 0, c->stream>>>(x, d_offsets, G, d_out);
+    LAUNCH_CHECK(c);
+}
+
+void max_dev_identity(Ctx* c, const double* g, int64_t w, int64_t ld, double* d_out) {
+    k_max_dev_identity<<<1, RT, 0, c->stream>>>(g, w, ld, d_out);
+    LAUNCH_CHECK(c);
+}
+
+void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out) {
+    k_sum_vector<<<1, 1024, 0, c->stream>>>(x, n, d_out);
+    LAUNCH_CHECK(c);
+}
+
+}  // namespace ops
+}  // namespace bcur_b200

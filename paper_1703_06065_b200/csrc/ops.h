@@ -1,0 +1,76 @@
+// ops.h — host-side launchers for every device kernel of the hot path.
+// Everything takes the context (stream, workspace pool) and raw device pointers.
+#pragma once
+
+#include "common.cuh"
+
+namespace bcur_b200 {
+namespace ops {
+
+enum Op { OP_N = 0, OP_T = 1 };
+
+// ---- reductions (kernels_reduce.cu) --------------------------------------
+// out[g] = Σ_{j∈block g} Σ_i a(i,j)²  (fp64; offsets are device, relative to a's first column)
+void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
+                 double* d_out);
+// out[j] = Σ_c v(j,c)²   then segmented into blocks: out_blocks[g]
+void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64_t ld, const int64_t* d_offsets,
+                      int64_t G, double* d_rows /*nullable*/, double* d_blocks);
+// segmented sum of a fp64 vector over block offsets
+void segment_sum(Ctx* c, const double* x, const int64_t* d_offsets, int64_t G, double* d_out);
+// max |G - I| over a w×w fp64 matrix → d_out[0]
+void max_dev_identity(Ctx* c, const double* g, int64_t w, int64_t ld, double* d_out);
+// ordered sum of x[0..n) → d_out[0]
+void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out);
+
+// ---- dense products (kernels_gemm.cu), fp64 accumulation ------------------
+// C(M×N fp64) = alpha·op(A)·op(B) + beta·C
+void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
+          const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc);
+// rowsq[i] = Σ_j (op(A)·op(B))(i,j)²   (product never stored)
+void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
+                   const void* B, int dtb, int64_t ldb, double* rowsq);
+// out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
+void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
+                      const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
+
+// ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
+// R upper with G = RᵀR; info[0] = 0 ok / j+1 failed pivot;
+// diag[0] = min diag(R), diag[1] = max diag(G) (input)
+void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int* info, double* diag);
+// X = R⁻¹ (upper triangular, w×w, ld w)
+void tri_inv_upper(Ctx* c, const double* r, int64_t w, double* x);
+// symmetric eig, eigenvalues descending in lam, eigenvectors in columns of V (w×w)
+void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, double* v);
+
+// ---- elementwise / layout (kernels_misc.cu) -------------------------------
+void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
+void fill_f64(Ctx* c, double* p, int64_t count, double v);
+void axpy_neg(Ctx* c, const double* x, double* y, int64_t n);  // y -= x
+void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*n*/);
+void copy_f64(Ctx* c, const double* src, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
+void transpose_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
+
+// ---- generators (kernels_gen.cu) ------------------------------------------
+void omega(Ctx* c, uint64_t key, int64_t n_rows, int64_t row0, int64_t l, double* out, int64_t ld);
+void gaussian_matrix(Ctx* c, uint64_t key, uint32_t stream, int64_t m, int64_t n, double* out, int64_t ld);
+void lowrank_assemble(Ctx* c, const double* us /*m×r*/, const double* v /*n_global×r*/, int64_t m, int64_t n,
+                      int64_t r, int64_t col0, int64_t n_global, double noise, uint64_t seed, void* a, int dt,
+                      int64_t lda);
+void biometric(Ctx* c, int64_t m, int64_t n, int64_t col0, int64_t n_global, uint64_t seed, void* a, int dt,
+               int64_t lda);
+
+// ---- sampling (kernels_sample.cu) -----------------------------------------
+// scores (G) → distribution → draws with the given uniforms.  status[0] = bcur_status.
+void distribution_draw(Ctx* c, const double* d_scores, int64_t G, int normalize, int64_t g, int mode,
+                       const double* d_uniforms, bcur_block_draw* d_draws, double* d_margins, int* d_status);
+// C[:, dst cols of draw t] = scale_t · A[:, block_t]  (or rows when rows=1: gathers row blocks into R)
+void gather_blocks(Ctx* c, const void* a, int dt, int64_t m, int64_t n, int64_t lda, const int64_t* d_offsets,
+                   const bcur_block_draw* d_draws, const int64_t* d_dst_off, int64_t ndraws, int rows, int scaled,
+                   void* out, int dto, int64_t ldo);
+// argmax over unselected entries (ties → lowest index); out_vals = {top1, top2}
+void argmax_masked(Ctx* c, const double* x, const unsigned char* mask_selected, int64_t G, int64_t* out_idx,
+                   double* out_vals);
+
+}  // namespace ops
+}  // namespace bcur_b200

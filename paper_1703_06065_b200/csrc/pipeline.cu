@@ -1,0 +1,667 @@
+// pipeline.cu — host orchestration of the Block-CUR hot path on one GPU (one
+// column shard of A per rank; collectives through the context's bcur_comm).
+//
+//   range_finder   N1  (replaces truncate(svd(a),k), matcore.cpp:39-69)
+//   block_css      R15 (sketch.cpp:68-82)
+//   greedy_select  N3
+//   block_cur      N4  (U = C⁺AR⁺; reference U = W⁺, blockcur.cpp:103)
+//
+// The numerical definitions (thresholds, orthonormalisation paths, residual
+// rule) are shared with the oracle (oracle/bcur_oracle.py) and documented in
+// DESIGN.md §Numerics.  Every floating-point operation runs on the device; the
+// host only moves O(G)-sized decision data (draws, argmax, ranks).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "pipeline.h"
+
+namespace bcur_b200 {
+
+using namespace ops;
+
+// ------------------------------------------------------------- utilities
+Mat64::Mat64(Ctx* c, int64_t m_, int64_t n_)
+    : buf(c, (size_t)std::max<int64_t>(1, m_) * std::max<int64_t>(1, n_) * sizeof(double)),
+      m(m_), n(n_), ld(std::max<int64_t>(1, m_)) {}
+
+template <class T>
+static void d2h(Ctx* c, T* host, const T* dev, size_t count) {
+    if (!count) return;
+    CUDA_CHECK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+}
+template <class T>
+static void h2d(Ctx* c, T* dev, const T* host, size_t count) {
+    if (!count) return;
+    CUDA_CHECK(cudaMemcpyAsync(dev, host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    c->sync();  // host buffers may be stack-owned by the caller
+}
+
+void allreduce(Ctx* c, double* d, int64_t count) {
+    if (c->comm.world <= 1 || count <= 0) return;
+    if (!c->comm.allreduce_f64) fail(BCUR_E_COMM, "allreduce requested but no callback installed");
+    const int rc = c->comm.allreduce_f64(c->comm.user, d, count, c->stream);
+    if (rc != 0) fail(BCUR_E_COMM, "allreduce callback failed with code " + std::to_string(rc));
+}
+
+double tau_chol(int dt) { return dt == BCUR_F32 ? 1e-2 : 1e-5; }
+double tau_rank(int dt) { return dt == BCUR_F32 ? 3e-4 : 1e-7; }
+double theta_explicit(int dt) { return dt == BCUR_F32 ? 0.1 : 1e-6; }
+double tau_saturate(int dt) { return dt == BCUR_F32 ? 1e-6 : 1e-12; }
+
+Shard shard_of(const DMat* a, const int64_t* offsets, int64_t G) {
+    Shard s;
+    s.G = G;
+    s.n_global = a->n_global > 0 ? a->n_global : a->n;
+    s.col0 = a->col0;
+    if (G < 1) fail(BCUR_E_INVALID_ARGUMENT, "partition must have at least one block");
+    if (offsets[0] != 0 || offsets[G] != s.n_global)
+        fail(BCUR_E_DIMENSION_MISMATCH, "partition does not cover the columns of A");
+    for (int64_t g = 0; g < G; ++g)
+        if (offsets[g + 1] <= offsets[g]) fail(BCUR_E_INVALID_ARGUMENT, "partition blocks must be non-empty and ordered");
+    s.g0 = -1;
+    s.g1 = -1;
+    for (int64_t g = 0; g <= G; ++g) {
+        if (offsets[g] == s.col0) s.g0 = g;
+        if (offsets[g] == s.col0 + a->n) s.g1 = g;
+    }
+    if (s.g0 < 0 || s.g1 < 0 || s.g1 < s.g0)
+        fail(BCUR_E_DIMENSION_MISMATCH, "column shard is not aligned to block boundaries");
+    s.off_global.assign(offsets, offsets + G + 1);
+    std::vector<int64_t> local(s.g1 - s.g0 + 1);
+    for (int64_t g = s.g0; g <= s.g1; ++g) local[g - s.g0] = offsets[g] - s.col0;
+    s.d_local = DevBuf(a->ctx, local.size() * sizeof(int64_t));
+    h2d(a->ctx, s.d_local.as<int64_t>(), local.data(), local.size());
+    return s;
+}
+
+// Gather a G-vector whose shard-local part [g0, g1) lives on each rank (zero-padded allreduce).
+static void gather_blocks_vec(Ctx* c, const Shard& s, const double* d_local, double* d_global) {
+    if (c->comm.world <= 1) {
+        CUDA_CHECK(cudaMemcpyAsync(d_global, d_local, s.G * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    fill_f64(c, d_global, s.G, 0.0);
+    CUDA_CHECK(cudaMemcpyAsync(d_global + s.g0, d_local, (s.g1 - s.g0) * sizeof(double), cudaMemcpyDeviceToDevice,
+                               c->stream));
+    allreduce(c, d_global, s.G);
+}
+
+// ------------------------------------------------------------------ orth
+// X (rows × w, fp64) → Q (rows × r) with X ≈ Q·T.  Grams allreduced when dist.
+// ref < 0 → ref = max column norm of X.  Mirrors oracle.orth.
+int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
+             int64_t ldq, bool dist, Mat64* T_out, int* path_out) {
+    if (w == 0) return 0;
+    Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w);
+    DevBuf st(c, 64);
+    int* d_info = st.as<int>();
+    double* d_diag = st.as<double>() + 1;
+    gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld);
+    if (dist) allreduce(c, G.p(), w * w);
+    cholesky_upper(c, G.p(), w, G.ld, R.p(), d_info, d_diag);
+    struct { int info; int pad; double mindiag, maxdiag; } hs;
+    d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
+    if (ref < 0) ref = std::sqrt(std::max(hs.maxdiag, 0.0));
+    int64_t r = w;
+    const bool chol_ok = hs.info == 0 && std::isfinite(hs.mindiag) && hs.mindiag > tau_chol(dt) * ref;
+    Mat64 Wr, sig;
+    std::vector<double> sig_h;
+    if (chol_ok) {
+        tri_inv_upper(c, R.p(), w, Ri.p());
+        gemm(c, OP_N, OP_N, rows, w, w, 1.0, X, BCUR_F64, ldx, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
+    } else {
+        Mat64 lam(c, w, 1), V(c, w, w);
+        sym_eig(c, G.p(), w, G.ld, lam.p(), V.p());
+        std::vector<double> lh(w);
+        d2h(c, lh.data(), lam.p(), w);
+        r = 0;
+        for (int64_t i = 0; i < w; ++i) {
+            const double s = std::sqrt(std::max(lh[i], 0.0));
+            if (s > tau_rank(dt) * ref) ++r;
+        }
+        if (r == 0) {
+            if (path_out) *path_out = 1;
+            if (T_out) *T_out = Mat64(c, 0, w);
+            return 0;
+        }
+        sig_h.resize(r);
+        std::vector<double> inv(r);
+        for (int64_t i = 0; i < r; ++i) {
+            sig_h[i] = std::sqrt(lh[i]);
+            inv[i] = 1.0 / sig_h[i];
+        }
+        Wr = Mat64(c, w, r);
+        copy_f64(c, V.p(), w, r, V.ld, Wr.p(), Wr.ld);
+        Mat64 dinv(c, r, 1);
+        h2d(c, dinv.p(), inv.data(), r);
+        Mat64 F(c, w, r);
+        copy_f64(c, Wr.p(), w, r, Wr.ld, F.p(), F.ld);
+        scale_columns(c, F.p(), w, r, F.ld, dinv.p());
+        gemm(c, OP_N, OP_N, rows, r, w, 1.0, X, BCUR_F64, ldx, F.p(), BCUR_F64, F.ld, 0.0, Q1.p(), Q1.ld);
+        sig = Mat64(c, r, 1);
+        h2d(c, sig.p(), sig_h.data(), r);
+    }
+    // second pass: CholQR of the well-conditioned Q1
+    Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
+    gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
+    if (dist) allreduce(c, G2.p(), r * r);
+    cholesky_upper(c, G2.p(), r, G2.ld, R2.p(), d_info, d_diag);
+    d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
+    if (hs.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
+    tri_inv_upper(c, R2.p(), r, R2i.p());
+    gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
+    if (T_out) {
+        Mat64 T(c, r, w);
+        if (chol_ok) {
+            gemm(c, OP_N, OP_N, r, w, r, 1.0, R2.p(), BCUR_F64, R2.ld, R.p(), BCUR_F64, R.ld, 0.0, T.p(), T.ld);
+        } else {
+            // T = R2·diag(σ)·Wrᵀ
+            Mat64 R2s(c, r, r);
+            copy_f64(c, R2.p(), r, r, R2.ld, R2s.p(), R2s.ld);
+            scale_columns(c, R2s.p(), r, r, R2s.ld, sig.p());
+            gemm(c, OP_N, OP_T, r, w, r, 1.0, R2s.p(), BCUR_F64, R2s.ld, Wr.p(), BCUR_F64, Wr.ld, 0.0, T.p(), T.ld);
+        }
+        *T_out = std::move(T);
+    }
+    if (path_out) *path_out = chol_ok ? 0 : 1;
+    return r;
+}
+
+// Block CGS2 of panel P (rows × w) against Q (rows × cur); P is overwritten.
+// New orthonormal columns are written at Q(:, cur..cur+r).  Returns r.
+int64_t cgs2_append(Ctx* c, double* Qbase, int64_t ldq, int64_t rows, int64_t cur, double* P, int64_t w, int64_t ldp,
+                    double ref, int dt, bool dist) {
+    if (cur > 0) {
+        Mat64 X(c, cur, w);
+        for (int pass = 0; pass < 2; ++pass) {
+            gemm(c, OP_T, OP_N, cur, w, rows, 1.0, Qbase, BCUR_F64, ldq, P, BCUR_F64, ldp, 0.0, X.p(), X.ld);
+            if (dist) allreduce(c, X.p(), cur * w);
+            gemm(c, OP_N, OP_N, rows, w, cur, -1.0, Qbase, BCUR_F64, ldq, X.p(), BCUR_F64, X.ld, 1.0, P, ldp);
+        }
+    }
+    return orth(c, P, rows, w, ldp, ref, dt, Qbase + cur * ldq, ldq, dist, nullptr, nullptr);
+}
+
+// ---------------------------------------------------------- range finder
+void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out) {
+    const int64_t m = a->m, nl = a->n;
+    const int64_t ng = a->n_global > 0 ? a->n_global : a->n;
+    if (k < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: k must be >= 1");
+    if (p < 0 || q < 0) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: p and q must be >= 0");
+    const int64_t l = std::min(k + p, std::min(m, ng));
+    const int dt = a->dtype;
+    Mat64 Om(c, nl, l), Y(c, m, l);
+    omega(c, key, nl, a->col0, l, Om.p(), Om.ld);
+    gemm(c, OP_N, OP_N, m, l, nl, 1.0, a->ptr, dt, a->ld, Om.p(), BCUR_F64, Om.ld, 0.0, Y.p(), Y.ld);
+    allreduce(c, Y.p(), m * l);
+    Mat64 Qy(c, m, l);
+    int64_t r = l;
+    for (int64_t it = 0; it < q; ++it) {
+        r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
+        if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
+        Mat64 Z(c, nl, r), Qz(c, nl, r);
+        gemm(c, OP_T, OP_N, nl, r, m, 1.0, a->ptr, dt, a->ld, Qy.p(), BCUR_F64, Qy.ld, 0.0, Z.p(), Z.ld);
+        r = orth(c, Z.p(), nl, r, Z.ld, -1.0, dt, Qz.p(), Qz.ld, true, nullptr, nullptr);
+        if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
+        gemm(c, OP_N, OP_N, m, r, nl, 1.0, a->ptr, dt, a->ld, Qz.p(), BCUR_F64, Qz.ld, 0.0, Y.p(), Y.ld);
+        allreduce(c, Y.p(), m * r);
+    }
+    r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
+    if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
+    // Bᵀ = Aᵀ·Q (n_local × r); B·Bᵀ = Σ_ranks Bᵀ_sᵀ Bᵀ_s
+    Mat64 Bt(c, nl, r), Gb(c, r, r), lam(c, r, 1), Ut(c, r, r);
+    gemm(c, OP_T, OP_N, nl, r, m, 1.0, a->ptr, dt, a->ld, Qy.p(), BCUR_F64, Qy.ld, 0.0, Bt.p(), Bt.ld);
+    gemm(c, OP_T, OP_N, r, r, nl, 1.0, Bt.p(), BCUR_F64, Bt.ld, Bt.p(), BCUR_F64, Bt.ld, 0.0, Gb.p(), Gb.ld);
+    allreduce(c, Gb.p(), r * r);
+    sym_eig(c, Gb.p(), r, Gb.ld, lam.p(), Ut.p());
+    std::vector<double> lh(r);
+    d2h(c, lh.data(), lam.p(), r);
+    std::vector<double> sg(r);
+    for (int64_t i = 0; i < r; ++i) sg[i] = std::sqrt(std::max(lh[i], 0.0));
+    if (!(sg[0] > 0.0)) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
+    const double tol = std::max(1e-12 * (double)std::max(m, ng) * sg[0], tau_rank(dt) * sg[0]);
+    int64_t rank = 0;
+    while (rank < r && sg[rank] > tol) ++rank;
+    const int64_t ke = std::min(k, rank);
+    std::vector<double> inv(ke);
+    for (int64_t i = 0; i < ke; ++i) inv[i] = 1.0 / sg[i];
+    Mat64 Wm(c, r, ke), dinv(c, ke, 1);
+    copy_f64(c, Ut.p(), r, ke, Ut.ld, Wm.p(), Wm.ld);
+    h2d(c, dinv.p(), inv.data(), ke);
+    scale_columns(c, Wm.p(), r, ke, Wm.ld, dinv.p());
+    out->v = Mat64(c, nl, ke);
+    gemm(c, OP_N, OP_N, nl, ke, r, 1.0, Bt.p(), BCUR_F64, Bt.ld, Wm.p(), BCUR_F64, Wm.ld, 0.0, out->v.p(), out->v.ld);
+    out->u = Mat64(c, m, ke);
+    gemm(c, OP_N, OP_N, m, ke, r, 1.0, Qy.p(), BCUR_F64, Qy.ld, Ut.p(), BCUR_F64, Ut.ld, 0.0, out->u.p(), out->u.ld);
+    // require_orthonormal evidence: V_kᵀV_k = Wmᵀ (B Bᵀ) Wm
+    Mat64 T1(c, r, ke), Vg(c, ke, ke), dev(c, 1, 1);
+    gemm(c, OP_N, OP_N, r, ke, r, 1.0, Gb.p(), BCUR_F64, Gb.ld, Wm.p(), BCUR_F64, Wm.ld, 0.0, T1.p(), T1.ld);
+    gemm(c, OP_T, OP_N, ke, ke, r, 1.0, Wm.p(), BCUR_F64, Wm.ld, T1.p(), BCUR_F64, T1.ld, 0.0, Vg.p(), Vg.ld);
+    max_dev_identity(c, Vg.p(), ke, Vg.ld, dev.p());
+    d2h(c, &out->orth_dev, dev.p(), 1);
+    out->k_eff = ke;
+    out->l = l;
+    out->sigma.assign(sg.begin(), sg.begin() + rank);
+}
+
+// ------------------------------------------------------------- block CSS
+struct Basis {
+    Mat64 q;         // rows × capacity
+    int64_t rank = 0;
+};
+
+// Build the orthonormal basis of the selected (unique, in order) column blocks of A.
+static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vector<int64_t>& blocks,
+                         const std::vector<double>& bn2, Basis* out) {
+    const int64_t m = a->m;
+    int64_t cap = 0;
+    for (int64_t b : blocks) cap += s.off_global[b + 1] - s.off_global[b];
+    out->q = Mat64(c, m, std::max<int64_t>(cap, 1));
+    out->rank = 0;
+    for (int64_t b : blocks) {
+        const int64_t w = s.off_global[b + 1] - s.off_global[b];
+        Mat64 P(c, m, w);
+        const bool mine = b >= s.g0 && b < s.g1;
+        if (mine) {
+            const int64_t lc = s.off_global[b] - s.col0;
+            const size_t es = dtype_size(a->dtype);
+            convert_to_f64(c, (const char*)a->ptr + (size_t)lc * a->ld * es, a->dtype, m, w, a->ld, P.p(), P.ld);
+        } else {
+            fill_f64(c, P.p(), m * w, 0.0);
+        }
+        allreduce(c, P.p(), m * w);  // broadcast from the owner
+        const double ref = std::sqrt(std::max(bn2[b], 0.0));
+        const int64_t r = cgs2_append(c, out->q.p(), out->q.ld, m, out->rank, P.p(), w, P.ld, ref, a->dtype, false);
+        out->rank += r;
+    }
+}
+
+// res2 = ‖A‖² − Σ_g ‖Qᵀ A_g‖²  (shard-local per-block values in d_blk, allreduced total)
+static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const double* Q, int64_t ldq, int64_t r,
+                             double* d_blk_local) {
+    const int64_t nl = a->n;
+    Mat64 rows(c, nl, 1), tot(c, 1, 1);
+    gemm_rowsumsq(c, OP_T, OP_N, nl, r, a->m, a->ptr, a->dtype, a->ld, Q, BCUR_F64, ldq, rows.p());
+    Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
+    double* b = d_blk_local ? d_blk_local : blk.p();
+    segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
+    sum_vector(c, b, s.g1 - s.g0, tot.p());
+    allreduce(c, tot.p(), 1);
+    double h = 0.0;
+    d2h(c, &h, tot.p(), 1);
+    return h;
+}
+
+static double explicit_residual(Ctx* c, const DMat* a, const double* Q, int64_t ldq, int64_t r) {
+    const int64_t m = a->m, nl = a->n;
+    Mat64 tot(c, 1, 1);
+    if (r == 0) {
+        // ‖A‖² of the shard
+        Mat64 one(c, 1, 1);
+        fill_f64(c, one.p(), 1, 0.0);
+        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, 1, one.p(), BCUR_F64, m, one.p(), BCUR_F64, 1, a->ptr, a->dtype, a->ld,
+                         tot.p());
+    } else {
+        Mat64 X(c, r, nl);
+        gemm(c, OP_T, OP_N, r, nl, m, 1.0, Q, BCUR_F64, ldq, a->ptr, a->dtype, a->ld, 0.0, X.p(), X.ld);
+        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, r, Q, BCUR_F64, ldq, X.p(), BCUR_F64, X.ld, a->ptr, a->dtype, a->ld,
+                         tot.p());
+    }
+    allreduce(c, tot.p(), 1);
+    double h = 0.0;
+    d2h(c, &h, tot.p(), 1);
+    return h;
+}
+
+// global per-block ‖A_g‖² (host copy) and ‖A‖²
+static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global) {
+    Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
+    *d_global = Mat64(c, s.G, 1);
+    block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
+    gather_blocks_vec(c, s, loc.p(), d_global->p());
+    bn2->assign(s.G, 0.0);
+    d2h(c, bn2->data(), d_global->p(), s.G);
+    Mat64 tot(c, 1, 1);
+    sum_vector(c, d_global->p(), s.G, tot.p());
+    double h = 0.0;
+    d2h(c, &h, tot.p(), 1);
+    return h;
+}
+
+static std::vector<int64_t> unique_in_order(const std::vector<int64_t>& v) {
+    std::vector<int64_t> out;
+    for (int64_t b : v)
+        if (std::find(out.begin(), out.end(), b) == out.end()) out.push_back(b);
+    return out;
+}
+
+// scores (global G, device) from the shard-local rows of V
+static void block_scores(Ctx* c, const Shard& s, const Mat64& v, int64_t nl, double* d_global) {
+    Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
+    row_sumsq_blocks(c, v.p(), BCUR_F64, nl, v.n, v.ld, s.d_local.as<int64_t>(), s.g1 - s.g0, nullptr, loc.p());
+    gather_blocks_vec(c, s, loc.p(), d_global);
+}
+
+static void draw_on_device(Ctx* c, const double* d_scores, int64_t G, int64_t g, int mode, const double* uniforms,
+                           std::vector<bcur_block_draw>* draws, std::vector<double>* margins) {
+    Mat64 du(c, std::max<int64_t>(g, 1), 1), dm(c, std::max<int64_t>(g, 1), 1);
+    DevBuf dd(c, (size_t)std::max<int64_t>(g, 1) * sizeof(bcur_block_draw)), st(c, 16);
+    h2d(c, du.p(), uniforms, g);
+    distribution_draw(c, d_scores, G, 1, g, mode, du.p(), dd.as<bcur_block_draw>(), dm.p(), st.as<int>());
+    int status = 0;
+    d2h(c, &status, st.as<int>(), 1);
+    if (status == BCUR_E_ZERO_MATRIX) fail(BCUR_E_ZERO_MATRIX, "ScoreVector::distribution: scores sum to zero");
+    if (status == BCUR_E_DISTRIBUTION_INVALID) fail(BCUR_E_DISTRIBUTION_INVALID, "draw_blocks: invalid distribution");
+    if (status == BCUR_E_NOT_ENOUGH_BLOCKS)
+        fail(BCUR_E_NOT_ENOUGH_BLOCKS, "draw_blocks: more distinct blocks requested than have positive probability");
+    if (status != BCUR_OK) fail(BCUR_E_CUDA, "draw_blocks: kernel status " + std::to_string(status));
+    draws->resize(g);
+    margins->resize(g);
+    d2h(c, draws->data(), dd.as<bcur_block_draw>(), g);
+    d2h(c, margins->data(), dm.p(), g);
+}
+
+void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, const double* uniforms,
+               CssOut* out) {
+    if (o.k < 1) fail(BCUR_E_INVALID_ARGUMENT, "block_css: k must be >= 1");
+    if (o.g < 1) fail(BCUR_E_INVALID_ARGUMENT, "draw_blocks: g must be >= 1");
+    Shard s = shard_of(a, offsets, G);
+    std::vector<double> bn2;
+    Mat64 dbn;
+    const double a2 = block_norms(c, a, s, &bn2, &dbn);
+    if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
+    Subspace sub;
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);
+    Mat64 sc(c, G, 1);
+    block_scores(c, s, sub.v, a->n, sc.p());
+    out->scores.resize(G);
+    d2h(c, out->scores.data(), sc.p(), G);
+    out->normalizer = (double)sub.k_eff;
+    draw_on_device(c, sc.p(), G, o.g, o.mode, uniforms, &out->draws, &out->margins);
+    std::vector<int64_t> blocks;
+    for (auto& d : out->draws) blocks.push_back(d.block);
+    Basis B;
+    column_basis(c, a, s, unique_in_order(blocks), bn2, &B);
+    double res2 = a2 - projected_mass(c, a, s, B.q.p(), B.q.ld, B.rank, nullptr);
+    int path = 0;
+    if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(a->dtype) * a2)) {
+        res2 = explicit_residual(c, a, B.q.p(), B.q.ld, B.rank);
+        path = 1;
+    }
+    out->rep = bcur_report{};
+    out->rep.abs_err = std::sqrt(std::max(res2, 0.0));
+    out->rep.a_norm = std::sqrt(a2);
+    out->rep.rel_err = out->rep.abs_err / out->rep.a_norm;
+    out->rep.k_eff = sub.k_eff;
+    out->rep.rank_c = B.rank;
+    out->rep.residual_path = path;
+    out->rep.orth_dev = sub.orth_dev;
+}
+
+// ---------------------------------------------------------------- greedy
+void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, GreedyOut* out) {
+    if (o.g < 1 || o.g > G) fail(BCUR_E_INVALID_ARGUMENT, "greedy_select: need 1 <= g <= number of blocks");
+    Shard s = shard_of(a, offsets, G);
+    std::vector<double> bn2;
+    Mat64 res;
+    const double a2 = block_norms(c, a, s, &bn2, &res);  // res starts as ‖A_g‖²
+    if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "greedy_select: A is identically zero");
+    const int dt = a->dtype;
+    const int64_t m = a->m;
+    int64_t cap = 0;
+    {
+        std::vector<int64_t> w(G);
+        for (int64_t g = 0; g < G; ++g) w[g] = offsets[g + 1] - offsets[g];
+        std::sort(w.begin(), w.end(), std::greater<int64_t>());
+        for (int64_t t = 0; t < o.g; ++t) cap += w[t];
+    }
+    Basis B;
+    B.q = Mat64(c, m, std::max<int64_t>(cap, 1));
+    DevBuf sel(c, (size_t)G);
+    CUDA_CHECK(cudaMemsetAsync(sel.ptr, 0, G, c->stream));
+    DevBuf didx(c, 64);
+    Mat64 lev;
+    bool have_lev = false;
+    Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1), upd(c, G, 1), rows(c, a->n, 1);
+    out->steps.clear();
+    for (int64_t t = 0; t < o.g; ++t) {
+        argmax_masked(c, res.p(), sel.as<unsigned char>(), G, didx.as<int64_t>(), didx.as<double>() + 1);
+        struct { int64_t idx; double v1, v2; } hm;
+        d2h(c, reinterpret_cast<char*>(&hm), reinterpret_cast<const char*>(didx.ptr), 24);
+        bcur_greedy_step st{};
+        st.block = hm.idx;
+        st.score = hm.v1;
+        st.margin = hm.v1 - hm.v2;
+        st.saturated = hm.v1 <= tau_saturate(dt) * a2 ? 1 : 0;
+        if (st.saturated) {
+            if (!have_lev) {
+                Subspace sub;
+                range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);
+                lev = Mat64(c, G, 1);
+                block_scores(c, s, sub.v, a->n, lev.p());
+                have_lev = true;
+            }
+            argmax_masked(c, lev.p(), sel.as<unsigned char>(), G, didx.as<int64_t>(), didx.as<double>() + 1);
+            d2h(c, reinterpret_cast<char*>(&hm), reinterpret_cast<const char*>(didx.ptr), 24);
+            st.block = hm.idx;
+            st.margin = hm.v1 - hm.v2;
+            double rv = 0.0;
+            d2h(c, &rv, res.p() + hm.idx, 1);
+            st.score = rv;
+        }
+        const int64_t b = st.block;
+        const unsigned char one = 1;
+        h2d(c, sel.as<unsigned char>() + b, &one, 1);
+        // panel = block b (broadcast from its owner)
+        const int64_t w = offsets[b + 1] - offsets[b];
+        Mat64 P(c, m, w);
+        if (b >= s.g0 && b < s.g1) {
+            const size_t es = dtype_size(dt);
+            convert_to_f64(c, (const char*)a->ptr + (size_t)(offsets[b] - s.col0) * a->ld * es, dt, m, w, a->ld,
+                           P.p(), P.ld);
+        } else {
+            fill_f64(c, P.p(), m * w, 0.0);
+        }
+        allreduce(c, P.p(), m * w);
+        const int64_t r = cgs2_append(c, B.q.p(), B.q.ld, m, B.rank, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)),
+                                      dt, false);
+        if (r > 0) {
+            // res_g −= ‖Q_newᵀ A_g‖²
+            gemm_rowsumsq(c, OP_T, OP_N, a->n, r, m, a->ptr, dt, a->ld, B.q.p() + B.rank * B.q.ld, BCUR_F64, B.q.ld,
+                          rows.p());
+            segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
+            gather_blocks_vec(c, s, loc.p(), upd.p());
+            axpy_neg(c, upd.p(), res.p(), G);
+        }
+        B.rank += r;
+        st.rank_added = r;
+        out->steps.push_back(st);
+    }
+    out->residuals.resize(G);
+    d2h(c, out->residuals.data(), res.p(), G);
+    Mat64 tot(c, 1, 1);
+    sum_vector(c, res.p(), G, tot.p());
+    double res2 = 0.0;
+    d2h(c, &res2, tot.p(), 1);
+    int path = 0;
+    if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(dt) * a2)) {
+        res2 = explicit_residual(c, a, B.q.p(), B.q.ld, B.rank);
+        path = 1;
+    }
+    out->rep = bcur_report{};
+    out->rep.abs_err = std::sqrt(std::max(res2, 0.0));
+    out->rep.a_norm = std::sqrt(a2);
+    out->rep.rel_err = out->rep.abs_err / out->rep.a_norm;
+    out->rep.rank_c = B.rank;
+    out->rep.residual_path = path;
+}
+
+// ------------------------------------------------------------ block CUR
+void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int64_t* roff, int64_t Gr,
+               const bcur_options& o, const double* uniforms, bool want_u, CurOut* out) {
+    const int64_t m = a->m, nl = a->n;
+    const int dt = a->dtype;
+    if (o.g < 1 || o.g_rows < 1) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: g and g_rows must be >= 1");
+    if (Gr < 1 || roff[0] != 0 || roff[Gr] != m) fail(BCUR_E_DIMENSION_MISMATCH, "block_cur: row partition does not match A");
+    Shard s = shard_of(a, coff, Gc);
+    std::vector<double> bn2;
+    Mat64 dbn;
+    const double a2 = block_norms(c, a, s, &bn2, &dbn);
+    if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_cur: A is identically zero");
+    Subspace sub;
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);
+    Mat64 csc(c, Gc, 1), rsc(c, Gr, 1);
+    block_scores(c, s, sub.v, nl, csc.p());
+    DevBuf droff(c, (Gr + 1) * sizeof(int64_t));
+    h2d(c, droff.as<int64_t>(), roff, Gr + 1);
+    row_sumsq_blocks(c, sub.u.p(), BCUR_F64, m, sub.u.n, sub.u.ld, droff.as<int64_t>(), Gr, nullptr, rsc.p());
+    out->col_scores.resize(Gc);
+    out->row_scores.resize(Gr);
+    d2h(c, out->col_scores.data(), csc.p(), Gc);
+    d2h(c, out->row_scores.data(), rsc.p(), Gr);
+    std::vector<double> mc, mr;
+    draw_on_device(c, csc.p(), Gc, o.g, o.mode, uniforms, &out->col_draws, &mc);
+    draw_on_device(c, rsc.p(), Gr, o.g_rows, o.mode, uniforms + o.g, &out->row_draws, &mr);
+    std::vector<int64_t> cb, rb;
+    for (auto& d : out->col_draws) cb.push_back(d.block);
+    for (auto& d : out->row_draws) rb.push_back(d.block);
+    cb = unique_in_order(cb);
+    rb = unique_in_order(rb);
+    // Q_C (m × rc), replicated
+    Basis QC;
+    column_basis(c, a, s, cb, bn2, &QC);
+    // Q_R (n × rr): basis of the selected row blocks of A, i.e. column blocks of Aᵀ (row-distributed over ranks)
+    std::vector<double> rbn2(Gr, 0.0);
+    {
+        // ‖A_{h,:}‖² per row block = per-column-block sums of Aᵀ (n_local × m), allreduced
+        Mat64 tmp(c, Gr, 1);
+        Mat64 at(c, nl, m);
+        transpose_to_f64(c, a->ptr, dt, m, nl, a->ld, at.p(), at.ld);
+        block_sumsq(c, at.p(), BCUR_F64, nl, at.ld, droff.as<int64_t>(), Gr, tmp.p());
+        allreduce(c, tmp.p(), Gr);
+        d2h(c, rbn2.data(), tmp.p(), Gr);
+        int64_t cap = 0;
+        for (int64_t h : rb) cap += roff[h + 1] - roff[h];
+        out->qr = Mat64(c, nl, std::max<int64_t>(cap, 1));
+        out->rank_r = 0;
+        for (int64_t h : rb) {
+            const int64_t w = roff[h + 1] - roff[h];
+            Mat64 P(c, nl, w);  // rows [roff[h], roff[h+1]) of A, transposed: nl × w
+            copy_f64(c, at.p() + roff[h] * at.ld, nl, w, at.ld, P.p(), P.ld);
+            const int64_t r = cgs2_append(c, out->qr.p(), out->qr.ld, nl, out->rank_r, P.p(), w, P.ld,
+                                          std::sqrt(std::max(rbn2[h], 0.0)), dt, true);
+            out->rank_r += r;
+        }
+    }
+    const int64_t rc = QC.rank, rr = out->rank_r;
+    // M = Q_Cᵀ A Q_R = Σ_s (Q_Cᵀ A_s) Q_R,s
+    Mat64 X(c, std::max<int64_t>(rc, 1), nl), M(c, std::max<int64_t>(rc, 1), std::max<int64_t>(rr, 1));
+    gemm(c, OP_T, OP_N, rc, nl, m, 1.0, QC.q.p(), BCUR_F64, QC.q.ld, a->ptr, dt, a->ld, 0.0, X.p(), X.ld);
+    gemm(c, OP_N, OP_N, rc, rr, nl, 1.0, X.p(), BCUR_F64, X.ld, out->qr.p(), BCUR_F64, out->qr.ld, 0.0, M.p(), M.ld);
+    allreduce(c, M.p(), rc * rr);
+    Mat64 tot(c, 1, 1);
+    {
+        // ‖M‖²
+        Mat64 rows2(c, std::max<int64_t>(rc, 1), 1);
+        row_sumsq_blocks(c, M.p(), BCUR_F64, rc, rr, M.ld, nullptr, 0, rows2.p(), nullptr);
+        sum_vector(c, rows2.p(), rc, tot.p());
+    }
+    double mm = 0.0;
+    d2h(c, &mm, tot.p(), 1);
+    double res2 = a2 - mm;
+    int path = 0;
+    if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(dt) * a2)) {
+        // Σ (A_s − Q_C (M Q_R,sᵀ))²
+        Mat64 Bm(c, std::max<int64_t>(rc, 1), nl);
+        gemm(c, OP_N, OP_T, rc, nl, rr, 1.0, M.p(), BCUR_F64, M.ld, out->qr.p(), BCUR_F64, out->qr.ld, 0.0, Bm.p(), Bm.ld);
+        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, rc, QC.q.p(), BCUR_F64, QC.q.ld, Bm.p(), BCUR_F64, Bm.ld, a->ptr, dt,
+                         a->ld, tot.p());
+        allreduce(c, tot.p(), 1);
+        d2h(c, &res2, tot.p(), 1);
+        path = 1;
+    }
+    out->u_valid = false;
+    if (want_u && rc > 0 && rr > 0) {
+        // C (m × cc) and Rᵀ (n_local × cr) with their sampling scales
+        int64_t cc = 0, cr = 0;
+        std::vector<int64_t> dco, dro;
+        for (auto& d : out->col_draws) { dco.push_back(cc); cc += coff[d.block + 1] - coff[d.block]; }
+        for (auto& d : out->row_draws) { dro.push_back(cr); cr += roff[d.block + 1] - roff[d.block]; }
+        Mat64 Cm(c, m, cc), Rt(c, nl, cr);
+        // columns: gather from each owner and broadcast via allreduce (zero elsewhere)
+        fill_f64(c, Cm.p(), m * cc, 0.0);
+        {
+            std::vector<bcur_block_draw> mine;
+            std::vector<int64_t> dst;
+            for (size_t t = 0; t < out->col_draws.size(); ++t) {
+                const int64_t b = out->col_draws[t].block;
+                if (b >= s.g0 && b < s.g1) {
+                    bcur_block_draw d = out->col_draws[t];
+                    d.block = b - s.g0;
+                    mine.push_back(d);
+                    dst.push_back(dco[t]);
+                }
+            }
+            if (!mine.empty()) {
+                DevBuf dd(c, mine.size() * sizeof(bcur_block_draw)), ddst(c, dst.size() * sizeof(int64_t));
+                h2d(c, dd.as<bcur_block_draw>(), mine.data(), mine.size());
+                h2d(c, ddst.as<int64_t>(), dst.data(), dst.size());
+                gather_blocks(c, a->ptr, dt, m, nl, a->ld, s.d_local.as<int64_t>(), dd.as<bcur_block_draw>(),
+                              ddst.as<int64_t>(), (int64_t)mine.size(), 0, 1, Cm.p(), BCUR_F64, Cm.ld);
+            }
+            allreduce(c, Cm.p(), m * cc);
+        }
+        {
+            DevBuf dd(c, out->row_draws.size() * sizeof(bcur_block_draw)), ddst(c, dro.size() * sizeof(int64_t));
+            h2d(c, dd.as<bcur_block_draw>(), out->row_draws.data(), out->row_draws.size());
+            h2d(c, ddst.as<int64_t>(), dro.data(), dro.size());
+            // R (cr × nl) = scaled row blocks; Rᵀ = its transpose
+            Mat64 Rm(c, cr, nl);
+            gather_blocks(c, a->ptr, dt, m, nl, a->ld, droff.as<int64_t>(), dd.as<bcur_block_draw>(), ddst.as<int64_t>(),
+                          (int64_t)out->row_draws.size(), 1, 1, Rm.p(), BCUR_F64, Rm.ld);
+            transpose_to_f64(c, Rm.p(), BCUR_F64, cr, nl, Rm.ld, Rt.p(), Rt.ld);
+        }
+        // T_C = Q_Cᵀ C (rc × cc), T_R = Q_Rᵀ Rᵀ (rr × cr)
+        Mat64 TC(c, rc, cc), TR(c, rr, cr);
+        gemm(c, OP_T, OP_N, rc, cc, m, 1.0, QC.q.p(), BCUR_F64, QC.q.ld, Cm.p(), BCUR_F64, Cm.ld, 0.0, TC.p(), TC.ld);
+        gemm(c, OP_T, OP_N, rr, cr, nl, 1.0, out->qr.p(), BCUR_F64, out->qr.ld, Rt.p(), BCUR_F64, Rt.ld, 0.0, TR.p(), TR.ld);
+        allreduce(c, TR.p(), rr * cr);
+        // T⁺ = Tᵀ (T Tᵀ)⁻¹ ; (T Tᵀ)⁻¹ = R⁻¹ R⁻ᵀ with T Tᵀ = RᵀR
+        auto pinv_rows = [&](const Mat64& T, int64_t rk, int64_t cols, Mat64* out_p) {
+            Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk);
+            DevBuf st(c, 64);
+            gemm(c, OP_N, OP_T, rk, rk, cols, 1.0, T.p(), BCUR_F64, T.ld, T.p(), BCUR_F64, T.ld, 0.0, G.p(), G.ld);
+            cholesky_upper(c, G.p(), rk, G.ld, R.p(), st.as<int>(), st.as<double>() + 2);
+            int info = 0;
+            d2h(c, &info, st.as<int>(), 1);
+            if (info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
+            tri_inv_upper(c, R.p(), rk, Ri.p());
+            gemm(c, OP_N, OP_T, rk, rk, rk, 1.0, Ri.p(), BCUR_F64, Ri.ld, Ri.p(), BCUR_F64, Ri.ld, 0.0, Gi.p(), Gi.ld);
+            *out_p = Mat64(c, cols, rk);
+            gemm(c, OP_T, OP_N, cols, rk, rk, 1.0, T.p(), BCUR_F64, T.ld, Gi.p(), BCUR_F64, Gi.ld, 0.0, out_p->p(),
+                 out_p->ld);
+        };
+        Mat64 TCp, TRp;
+        pinv_rows(TC, rc, cc, &TCp);  // cc × rc
+        pinv_rows(TR, rr, cr, &TRp);  // cr × rr
+        Mat64 T2(c, cc, rr);
+        gemm(c, OP_N, OP_N, cc, rr, rc, 1.0, TCp.p(), BCUR_F64, TCp.ld, M.p(), BCUR_F64, M.ld, 0.0, T2.p(), T2.ld);
+        out->u = Mat64(c, cc, cr);
+        gemm(c, OP_N, OP_T, cc, cr, rr, 1.0, T2.p(), BCUR_F64, T2.ld, TRp.p(), BCUR_F64, TRp.ld, 0.0, out->u.p(),
+             out->u.ld);
+        out->u_valid = true;
+    }
+    out->rep = bcur_report{};
+    out->rep.abs_err = std::sqrt(std::max(res2, 0.0));
+    out->rep.a_norm = std::sqrt(a2);
+    out->rep.rel_err = out->rep.abs_err / out->rep.a_norm;
+    out->rep.k_eff = sub.k_eff;
+    out->rep.rank_c = rc;
+    out->rep.rank_r = rr;
+    out->rep.residual_path = path;
+    out->rep.orth_dev = sub.orth_dev;
+}
+
+}  // namespace bcur_b200
