@@ -1,0 +1,388 @@
+#!/usr/bin/env python
+"""Block-CUR decompositions/sec on B200 (BASELINE.json metric) — one JSON line.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl b200|reference]
+
+A step is one full decomposition of the workload: range finder → block leverage
+scores → seeded draws → C → ‖A − CC⁺A‖_F (or greedy / CUR for configs 2 / 4),
+with A resident in HBM (`value`), and through the public API with the input
+uploaded from pinned host memory every step (`e2e`).  Under torchrun each rank
+owns a contiguous column-block shard of A and the collectives go through NCCL
+(torch.distributed); the decomposition is the same job at every N (strong scaling).
+
+`--impl reference` times the reference algorithm on the host cores instead: the
+CPU oracle restatement (oracle/bcur_oracle.py, numpy/OpenBLAS with all threads),
+because the reference itself cannot be built here (Eigen3 and vendor/ are absent).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1703_06065_b200.configs import CONFIGS, spectrum  # noqa: E402
+
+METRIC = "Block-CUR decompositions/sec"
+UNIT = "decompositions/s"
+
+
+def env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                           "--format=csv,noheader,nounits", "-lms", "200"],
+                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except OSError:
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except Exception:
+                self._proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm": d.get("hbm_gbs", 6650.0), "tensor": d.get("bf16_tflops_sustained", d.get("bf16_tflops")),
+                "tensor_burst": d.get("bf16_tflops"), "source": "MEASURED_PEAKS.json"}
+    return {"hbm": 6650.0, "tensor": 1590.0, "tensor_burst": 1590.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------ GPU workload
+def block_offsets(n, s):
+    return np.array(list(range(0, n, s)) + [n], dtype=np.int64)
+
+
+def run_step(B, cfg, dm, part, rpart, ctx):
+    sel = cfg["select"]
+    if sel == "greedy":
+        r = B.greedy_select(dm, part, cfg["k"], cfg["g"], seed=cfg["seed"], p=cfg["p"], q=cfg["q"], ctx=ctx)
+        return r.rel_err, r.blocks()
+    if sel == "cur":
+        r = B.block_cur(dm, part, rpart, cfg["k"], cfg["g"], cfg["g_rows"], B.Rng(cfg["seed"]), p=cfg["p"],
+                        q=cfg["q"], mode=cfg["mode"], want_u=True, ctx=ctx)
+        return r.rel_err, r.col_plan.blocks() + r.row_plan.blocks()
+    r = B.block_css(dm, part, cfg["k"], cfg["g"], B.Rng(cfg["seed"]), p=cfg["p"], q=cfg["q"], mode=cfg["mode"],
+                    return_c=False, ctx=ctx)
+    out = (r.rel_err, r.plan.blocks())
+    if sel == "leverage+greedy":
+        gr = B.greedy_select(dm, part, cfg["k"], cfg["g"], seed=cfg["seed"], p=cfg["p"], q=cfg["q"], ctx=ctx)
+        out = (r.rel_err, r.plan.blocks() + gr.blocks())
+    return out
+
+
+def d2h_bytes(cfg, G):
+    g = cfg["g"] + cfg.get("g_rows", 0)
+    return 8 * G + 32 * g + 64
+
+
+def bench_b200(args, cfg, rank, world, local_rank):
+    import torch
+
+    from paper_1703_06065_b200 import bcur as B
+
+    torch.cuda.set_device(local_rank)
+    ctx = B.Context(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        class Cai:
+            def __init__(self, ptr, count):
+                self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
+                                                 "version": 3, "strides": None}
+
+        def allreduce(ptr, count, stream):
+            t = torch.as_tensor(Cai(ptr, count), device=f"cuda:{local_rank}")
+            with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=f"cuda:{local_rank}")):
+                dist.all_reduce(t)
+
+        ctx.set_comm(rank, world, allreduce)
+
+    m, n, s = cfg["m"], cfg["n"], cfg["s"]
+    G = n // s
+    if G % world:
+        raise SystemExit(f"{G} blocks do not split evenly over {world} ranks")
+    n_local = n // world
+    col0 = rank * n_local
+    dt = np.float32 if cfg["dtype"] == "f32" else np.float64
+    t0 = time.time()
+    if cfg["kind"] == "lowrank":
+        dm = B.DeviceMatrix.generate("lowrank", dt, m, n_local, seed=cfg["seed"],
+                                     sigma=spectrum(cfg["spectrum"], cfg["rank"]), noise=cfg["noise"], col0=col0,
+                                     n_global=n, ctx=ctx)
+    else:
+        dm = B.DeviceMatrix.generate("biometric", dt, m, n_local, seed=cfg["seed"], col0=col0, n_global=n, ctx=ctx)
+    gen_s = time.time() - t0
+    part = B.BlockPartition.equal_blocks(n, s)
+    rpart = B.BlockPartition.equal_blocks(m, s)
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local_rank}")
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def timed(fn, steps, profile=False):
+        barrier()
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        l0 = ctx.launch_count
+        if profile:
+            ctx.profile(True)
+        e0.record(stream)
+        res = None
+        for _ in range(steps):
+            res = fn()
+        e1.record(stream)
+        ctx.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        prof = ctx.profile_report() if profile else None
+        if profile:
+            ctx.profile(False)
+        launches = ctx.launch_count - l0
+        if dist is not None:
+            t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{local_rank}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, res, prof, launches
+
+    for _ in range(args.warmup):
+        run_step(B, cfg, dm, part, rpart, ctx)
+    with ClockSampler(local_rank) as clk:
+        ms, res, prof, launches = timed(lambda: run_step(B, cfg, dm, part, rpart, ctx), args.steps, profile=True)
+    rel_err, blocks = res
+
+    # e2e: the public API with host buffers — pinned A shard uploaded every step
+    host = torch.empty((n_local, m), dtype=torch.float32 if dt == np.float32 else torch.float64, pin_memory=True)
+    import ctypes
+    B._check(B.L.lib.bcur_dmat_download(ctx.handle, dm.handle, ctypes.c_void_p(host.data_ptr()), m))
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    hptr = ctypes.c_void_p(host.data_ptr())
+
+    def e2e_step():
+        B._check(B.L.lib.bcur_dmat_upload(ctx.handle, dm.handle, hptr, m))
+        return run_step(B, cfg, dm, part, rpart, ctx)
+
+    e2e_step()
+    ms_e2e, _, _, _ = timed(e2e_step, e2e_steps)
+
+    value = args.steps / (ms / 1e3)
+    e2e_value = e2e_steps / (ms_e2e / 1e3)
+    h2d = m * n_local * (4 if dt == np.float32 else 8)
+
+    line = None
+    if rank == 0:
+        peaks = measured_peaks()
+        roof = roofline(prof, peaks)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dt == np.float32 else "f64",
+            "data": "synthetic (Philox-generated on device; BASELINE.json config distribution)",
+            "config": {"workload": args.config, "m": m, "n": n, "block_width": s, "blocks": G, "k": cfg["k"],
+                       "p": cfg["p"], "q": cfg["q"], "g": cfg["g"], "select": cfg["select"], "mode": cfg["mode"],
+                       "parallelism": f"column-block shards x{world}" if world > 1 else "single GPU",
+                       "l2": "A is larger than L2 (126 MB), re-read every step"},
+            "rel_err": rel_err, "selected_blocks": blocks[:16],
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
+                    "d2h_bytes_per_step": d2h_bytes(cfg, G) * world, "ms_per_step": ms_e2e / e2e_steps},
+            "gpu_launches": launches, "roofline": roof, "kernels": prof,
+            "clocks": clk.summary(), "generate_s": gen_s,
+        }
+    return line
+
+
+def roofline(prof, peaks):
+    if not prof:
+        return None
+    tag, d = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    total = sum(v["ms"] for v in prof.values())
+    avg_ms = d["ms"] / max(d["scopes"], 1)
+    if d["flops"] > 0 and d["flops"] / max(d["bytes"], 1) > 60:
+        achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
+        return {"kernel": tag, "bound": "tensor", "achieved": achieved, "peak": peaks["tensor"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["tensor"], "traffic": None, "share_of_step": d["ms"] / total,
+                "avg_launch_ms": avg_ms, "peak_source": peaks["source"] + " bf16_tflops_sustained"}
+    achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
+    return {"kernel": tag, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm"], "traffic": None, "share_of_step": d["ms"] / total,
+            "avg_launch_ms": avg_ms, "peak_source": peaks["source"] + " hbm_gbs"}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if info:
+            return int(info[0]["num_threads"])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def cpu_sample_time(cfg, n_cols, seed=1):
+    """One oracle decomposition on the first n_cols columns (same m, s, k, p, q, g)."""
+    from oracle import bcur_oracle as O
+
+    rng = np.random.default_rng(seed)
+    dt = np.float32 if cfg["dtype"] == "f32" else np.float64
+    m = cfg["m"]
+    if cfg["kind"] == "lowrank":
+        r = cfg["rank"]
+        u, _ = np.linalg.qr(rng.standard_normal((m, r)))
+        v, _ = np.linalg.qr(rng.standard_normal((n_cols, r)))
+        a = (u * spectrum(cfg["spectrum"], r)) @ v.T + cfg["noise"] * rng.standard_normal((m, n_cols))
+    else:
+        a = O.gen_biometric(m, n_cols, cfg["seed"])
+    a = np.asfortranarray(a.astype(dt))
+    part = O.BlockPartition.equal_blocks(n_cols, cfg["s"])
+    g = min(cfg["g"], part.num_blocks())
+    t0 = time.perf_counter()
+    if cfg["select"] == "greedy":
+        O.greedy_select(a, part, cfg["k"], g, O.omega_key_from_seed(cfg["seed"]), p=cfg["p"], q=cfg["q"])
+    elif cfg["select"] == "cur":
+        rp = O.BlockPartition.equal_blocks(m, cfg["s"])
+        O.block_cur_rows_cols(a, part, rp, cfg["k"], g, min(cfg["g_rows"], rp.num_blocks()), O.Rng(cfg["seed"]),
+                              p=cfg["p"], q=cfg["q"], mode=cfg["mode"], want_u=True)
+    else:
+        O.block_css(a, part, cfg["k"], g, O.Rng(cfg["seed"]), p=cfg["p"], q=cfg["q"], mode=cfg["mode"])
+        if cfg["select"] == "leverage+greedy":
+            O.greedy_select(a, part, cfg["k"], g, O.omega_key_from_seed(cfg["seed"]), p=cfg["p"], q=cfg["q"])
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(cfg, budget_cols=None):
+    """Time the oracle on two column samples and extrapolate T(n) = a + b·n to the full n."""
+    n, s = cfg["n"], cfg["s"]
+    if n <= 20000 or cfg["m"] * n <= 4e7:
+        t = cpu_sample_time(cfg, n)
+        return {"value": 1.0 / t, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+                "sample": f"full {cfg['m']}x{n} workload, one decomposition ({t:.2f} s)"}
+    g = cfg["g"]
+    n1 = max(2 * g * s, budget_cols or 0)
+    n1 = min(n1, n // 4)
+    n2 = 2 * n1
+    t1 = cpu_sample_time(cfg, n1)
+    t2 = cpu_sample_time(cfg, n2)
+    b = max((t2 - t1) / (n2 - n1), 0.0)
+    a = max(t1 - b * n1, 0.0)
+    t_full = a + b * n
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+            "sample": (f"oracle on {cfg['m']}x{n1} ({t1:.2f} s) and {cfg['m']}x{n2} ({t2:.2f} s) column samples "
+                       f"(same m, s, k, p, q, g); T(n)=a+b*n extrapolated to n={n}: {t_full:.2f} s")}
+
+
+def bench_reference(args, cfg):
+    steps = []
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(cfg)
+        if i >= args.warmup:
+            steps.append(cb)
+    vals = [c["value"] for c in steps]
+    v = statistics.median(vals)
+    cb = dict(steps[-1])
+    cb["value"] = v
+    return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": cfg["dtype"], "data": "synthetic (numpy, same shapes/distribution)",
+            "config": {"workload": args.config, "m": cfg["m"], "n": cfg["n"], "block_width": cfg["s"],
+                       "k": cfg["k"], "p": cfg["p"], "q": cfg["q"], "g": cfg["g"], "select": cfg["select"]},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference (Eigen, vendor/) unbuildable here; CPU oracle restatement timed on host cores"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = dict(CONFIGS[args.config])
+    rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(bench_reference(args, cfg)), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    line = bench_b200(args, cfg, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(cfg)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -67,6 +67,12 @@ void* bcur_ctx_stream(bcur_ctx ctx);
 bcur_status bcur_ctx_synchronize(bcur_ctx ctx);
 /* Number of kernels this context has launched so far (bench evidence). */
 int64_t bcur_ctx_launch_count(bcur_ctx ctx);
+/* Per-kernel-class accounting with CUDA events on the context stream.
+ * enable=1 clears and starts recording; bcur_ctx_profile_dump synchronizes and
+ * writes JSON {"tag": {"scopes": n, "ms": t, "flops": f, "bytes": b}, ...}
+ * (algorithmic flops/bytes) into buf; returns the needed length. */
+bcur_status bcur_ctx_profile(bcur_ctx ctx, int enable);
+int64_t bcur_ctx_profile_dump(bcur_ctx ctx, char* buf, int64_t cap);
 
 /* Multi-GPU plumbing: one process (context) per GPU; the host supplies the
  * collectives (e.g. torch.distributed over NCCL).  Callbacks run on the

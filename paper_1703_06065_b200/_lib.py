@@ -64,6 +64,8 @@ SIGNATURES = {
     "bcur_ctx_stream": (vp, [vp]),
     "bcur_ctx_synchronize": (C.c_int, [vp]),
     "bcur_ctx_launch_count": (i64, [vp]),
+    "bcur_ctx_profile": (C.c_int, [vp, C.c_int]),
+    "bcur_ctx_profile_dump": (i64, [vp, C.c_char_p, i64]),
     "bcur_ctx_set_comm": (C.c_int, [vp, C.POINTER(CommC)]),
     "bcur_dmat_create": (C.c_int, [vp, C.c_int, i64, i64, C.POINTER(vp)]),
     "bcur_dmat_upload": (C.c_int, [vp, vp, vp, i64]),

@@ -124,6 +124,17 @@ class Context:
     def launch_count(self) -> int:
         return int(L.lib.bcur_ctx_launch_count(self.handle))
 
+    def profile(self, enable: bool = True):
+        """Start (clear) / stop per-kernel-class CUDA-event accounting."""
+        _check(L.lib.bcur_ctx_profile(self.handle, 1 if enable else 0))
+
+    def profile_report(self) -> dict:
+        import json
+        need = int(L.lib.bcur_ctx_profile_dump(self.handle, None, 0))
+        buf = C.create_string_buffer(max(need, 2))
+        L.lib.bcur_ctx_profile_dump(self.handle, buf, len(buf))
+        return json.loads(buf.value.decode())
+
     def set_comm(self, rank: int, world: int, allreduce_fn):
         """allreduce_fn(ptr:int, count:int, stream:int) -> None (in-place sum of fp64)."""
         if world <= 1:

@@ -3,6 +3,7 @@
 // blockcur.cpp), converts exceptions to bcur_status + a thread-local message,
 // and forwards to the device pipeline.
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <random>
 #include <string>
@@ -204,6 +205,55 @@ bcur_status bcur_ctx_synchronize(bcur_ctx ctx) {
 }
 
 int64_t bcur_ctx_launch_count(bcur_ctx ctx) { return ctx ? ctx->launches : 0; }
+
+bcur_status bcur_ctx_profile(bcur_ctx ctx, int enable) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    c->sync();
+    for (auto& r : c->prof_recs) {
+        c->ev_pool.push_back(r.e0);
+        c->ev_pool.push_back(r.e1);
+    }
+    c->prof_recs.clear();
+    c->prof = enable != 0;
+    API_END
+}
+
+int64_t bcur_ctx_profile_dump(bcur_ctx ctx, char* buf, int64_t cap) {
+    if (!ctx) return -1;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    struct Acc { int64_t n = 0; double ms = 0, flops = 0, bytes = 0; };
+    std::map<std::string, Acc> acc;
+    for (auto& r : ctx->prof_recs) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, r.e0, r.e1) != cudaSuccess) {
+            (void)cudaGetLastError();
+            continue;
+        }
+        Acc& a = acc[r.tag];
+        a.n++;
+        a.ms += ms;
+        a.flops += r.flops;
+        a.bytes += r.bytes;
+    }
+    std::string s = "{";
+    bool first = true;
+    char tmp[512];
+    for (auto& kv : acc) {
+        std::snprintf(tmp, sizeof tmp, "%s\"%s\": {\"scopes\": %lld, \"ms\": %.6f, \"flops\": %.6e, \"bytes\": %.6e}",
+                      first ? "" : ", ", kv.first.c_str(), (long long)kv.second.n, kv.second.ms, kv.second.flops,
+                      kv.second.bytes);
+        s += tmp;
+        first = false;
+    }
+    s += "}";
+    if (buf && cap > 0) {
+        std::strncpy(buf, s.c_str(), (size_t)cap - 1);
+        buf[cap - 1] = 0;
+    }
+    return (int64_t)s.size() + 1;
+}
 
 bcur_status bcur_ctx_set_comm(bcur_ctx ctx, const bcur_comm* comm) {
     API_BEGIN

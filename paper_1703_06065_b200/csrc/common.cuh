@@ -111,6 +111,42 @@ struct Ctx {
     }
     void sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
     std::map<void*, size_t> sizes;
+
+    // --- per-kernel accounting (CUDA events on this stream; bench roofline) ---
+    struct ProfRec {
+        std::string tag;
+        cudaEvent_t e0, e1;
+        double flops, bytes;
+    };
+    bool prof = false;
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t event() {
+        if (!ev_pool.empty()) {
+            cudaEvent_t e = ev_pool.back();
+            ev_pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        CUDA_CHECK(cudaEventCreate(&e));
+        return e;
+    }
+};
+
+// RAII: records [start, stop) events around the kernels launched in its scope.
+struct ProfScope {
+    Ctx* c;
+    size_t idx = (size_t)-1;
+    ProfScope(Ctx* ctx, const char* tag, double flops, double bytes) : c(ctx) {
+        if (!c->prof) return;
+        Ctx::ProfRec r{tag, c->event(), c->event(), flops, bytes};
+        CUDA_CHECK(cudaEventRecord(r.e0, c->stream));
+        c->prof_recs.push_back(r);
+        idx = c->prof_recs.size() - 1;
+    }
+    ~ProfScope() {
+        if (idx != (size_t)-1) cudaEventRecord(c->prof_recs[idx].e1, c->stream);
+    }
 };
 
 inline DevBuf::DevBuf(Ctx* c, size_t b) : ctx(c), bytes(b) { ptr = b ? c->acquire(b) : nullptr; }

@@ -215,6 +215,8 @@ namespace ops {
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (M <= 0 || N <= 0) return;
+    ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_store_f32" : "gemm_store_f64", 2.0 * M * N * K,
+                   (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M * N);
     if (K <= 0) {
         // C = beta·C
         if (beta == 0.0) {
@@ -254,6 +256,8 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                    const void* B, int dtb, int64_t ldb, double* rowsq) {
     if (M <= 0) return;
+    ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_rowsumsq_f32" : "gemm_rowsumsq_f64",
+                   2.0 * M * N * K, (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M);
     if (N <= 0) {
         CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
         return;
@@ -269,6 +273,8 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out) {
+    ProfScope prof(c, "gemm_resid", 2.0 * M * N * K,
+                   (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + (double)M * N * dtype_size(dtd));
     const int64_t mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
     DevBuf part(c, (size_t)mt * nt * sizeof(double));
     dim3 grid((unsigned)mt, (unsigned)nt, 1);

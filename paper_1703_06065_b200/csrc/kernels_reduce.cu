@@ -152,6 +152,7 @@ namespace ops {
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
                  double* d_out) {
     if (G <= 0) return;
+    ProfScope prof(c, "block_sumsq", 0.0, 0.0);
     // enough CTAs to fill the machine several times over
     int Z = (int)std::max<int64_t>(1, std::min<int64_t>(64, (8LL * c->sm_count + G - 1) / G));
     const size_t es = dtype_size(dt);
@@ -169,6 +170,7 @@ void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int
 
 void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64_t ld, const int64_t* d_offsets,
                       int64_t G, double* d_rows, double* d_blocks) {
+    ProfScope prof(c, "block_scores", 2.0 * n * k, (double)n * k * dtype_size(dt));
     DevBuf tmp;
     if (!d_rows) {
         tmp = DevBuf(c, (size_t)n * sizeof(double));

@@ -188,6 +188,7 @@ namespace ops {
 
 void distribution_draw(Ctx* c, const double* d_scores, int64_t G, int normalize, int64_t g, int mode,
                        const double* d_uniforms, bcur_block_draw* d_draws, double* d_margins, int* d_status) {
+    ProfScope prof(c, "draw", 0.0, 8.0 * G);
     DevBuf p(c, (size_t)G * sizeof(double)), act(c, (size_t)G);
     k_distribution_draw<<<1, 32, 0, c->stream>>>(d_scores, G, normalize, g, mode, d_uniforms, p.as<double>(),
                                                  act.as<unsigned char>(), d_draws, d_margins, d_status);
@@ -198,6 +199,7 @@ void gather_blocks(Ctx* c, const void* a, int dt, int64_t m, int64_t n, int64_t 
                    const bcur_block_draw* d_draws, const int64_t* d_dst_off, int64_t ndraws, int rows, int scaled,
                    void* out, int dto, int64_t ldo) {
     if (ndraws <= 0) return;
+    ProfScope prof(c, "gather", 0.0, 0.0);
     dim3 grid((unsigned)ndraws, rows ? 64u : 32u);
 #define BCUR_GATHER(TI, TO)                                                                                   \
     k_gather<TI, TO><<<grid, 256, 0, c->stream>>>((const TI*)a, m, n, lda, d_offsets, d_draws, d_dst_off, rows, \

@@ -102,6 +102,13 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
         V[e] = i == j ? 1.0 : 0.0;
     }
     for (int i = threadIdx.x; i < wp; i += ST) pos[i] = i;
+    // absolute floor: off-diagonal rounding noise of the input (≈ eps·‖G‖_F) is not rotated away
+    __shared__ double floor_abs;
+    if (threadIdx.x == 0) {
+        double f = 0.0;
+        for (int64_t j = 0; j < w; ++j) f = fmax(f, fabs(g[j + j * ldg]));
+        floor_abs = 1e-17 * f * (double)w;
+    }
     __syncthreads();
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
         if (threadIdx.x == 0) rotated = 0;
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                 if (q < w) {
                     const double apq = A[p + q * w];
                     const double app = A[p + p * w], aqq = A[q + q * w];
-                    if (fabs(apq) > 1e-300 && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
+                    if (fabs(apq) > floor_abs && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
                         const double tau = (aqq - app) / (2.0 * apq);
                         const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
                         c = 1.0 / sqrt(1.0 + t * t);
@@ -209,12 +216,14 @@ void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, 
         work = DevBuf(c, (size_t)w * w * sizeof(double));
     }
     ensure_attrs();
+    ProfScope prof(c, "cholesky", w * w * w / 3.0, 8.0 * w * w);
     k_cholesky<<<1, ST, smem, c->stream>>>(g, w, ldg, r, work.as<double>(), info, mindiag);
     LAUNCH_CHECK(c);
 }
 
 void tri_inv_upper(Ctx* c, const double* r, int64_t w, double* x) {
     ensure_attrs();
+    ProfScope prof(c, "tri_inv", w * w * w / 3.0, 8.0 * w * w);
     const bool use = w <= SMEM_MAX_W;
     k_tri_inv_upper<<<1, ST, use ? (size_t)w * w * sizeof(double) : 0, c->stream>>>(r, w, x, use);
     LAUNCH_CHECK(c);
@@ -223,6 +232,7 @@ void tri_inv_upper(Ctx* c, const double* r, int64_t w, double* x) {
 void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, double* v) {
     if (w > 512) fail(BCUR_E_INVALID_ARGUMENT, "sym_eig: w > 512 not supported");
     ensure_attrs();
+    ProfScope prof(c, "sym_eig", 0.0, 8.0 * w * w);
     DevBuf work, vtmp(c, (size_t)w * w * sizeof(double));
     size_t smem = 0;
     if (w <= SMEM_MAX_W) smem = (size_t)w * w * sizeof(double);
