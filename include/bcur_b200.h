@@ -145,6 +145,12 @@ bcur_status bcur_column_leverage(bcur_ctx ctx, bcur_dmat v_k, double tol, double
  * sigma (k_eff values, host, nullable). */
 bcur_status bcur_range_finder(bcur_ctx ctx, bcur_dmat a, int64_t k, int64_t p, int64_t q, uint64_t key,
                               bcur_dmat* v_out, bcur_dmat* u_out, double* sigma_out, int64_t* k_eff);
+/* The sketch products of the range finder on the hot-path kernels (tcgen05 3×TF32 for
+ * fp32 A, fp64 SIMT otherwise): out (fp64) = A·X (transpose=0, X n×N) or Aᵀ·X
+ * (transpose=1, X m×N).  X is fp64.  rows_out (nullable, host, length n) with
+ * transpose=1 receives Σ_c (AᵀX)_jc² instead of storing the product (out may be NULL). */
+bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, bcur_dmat out,
+                                double* rows_out);
 /* sampler.cpp:116-146 draw_blocks (probabilities on the host, one uniform per draw
  * drawn by the caller from its Rng; margins_out[t] = distance of u_t to the nearest
  * CDF edge, nullable). */

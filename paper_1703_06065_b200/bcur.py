@@ -435,6 +435,25 @@ def block_sq_norms(a, part: BlockPartition, ctx: Optional[Context] = None) -> np
     return out
 
 
+def sketch_product(a, x: np.ndarray, transpose: bool = False, row_sumsq: bool = False,
+                   ctx: Optional[Context] = None) -> np.ndarray:
+    """A·X (or Aᵀ·X) on the range finder's product kernels; ``row_sumsq`` returns
+    Σ_c (AᵀX)_jc² per row without storing the product (fused residual epilogue)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    xd = DeviceMatrix.from_host(np.asarray(x, dtype=np.float64), ctx)
+    rows = d.shape[1] if transpose else d.shape[0]
+    if row_sumsq:
+        out = np.empty(rows, dtype=np.float64)
+        _check(L.lib.bcur_sketch_product(ctx.handle, d.handle, xd.handle, 1, None, out.ctypes.data_as(L.P_dbl)))
+        return out
+    h = C.c_void_p()
+    _check(L.lib.bcur_dmat_create(ctx.handle, L.F64, rows, xd.shape[1], C.byref(h)))
+    o = DeviceMatrix(h, ctx)
+    _check(L.lib.bcur_sketch_product(ctx.handle, d.handle, xd.handle, 1 if transpose else 0, o.handle, None))
+    return o.to_host()
+
+
 @dataclass
 class Subspace:
     v_k: np.ndarray

@@ -504,6 +504,31 @@ bcur_status bcur_range_finder(bcur_ctx ctx, bcur_dmat a, int64_t k, int64_t p, i
     API_END
 }
 
+bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, bcur_dmat out,
+                                double* rows_out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat *A = M(a), *X = M(x);
+    if (X->dtype != BCUR_F64) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product: X must be fp64");
+    const int64_t K = transpose ? A->m : A->n, rows = transpose ? A->n : A->m;
+    if (X->m != K) fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product: inner dimensions differ");
+    if (rows_out) {
+        if (!transpose) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product: row sums need transpose=1");
+        Mat64 r(c, rows, 1);
+        ops::gemm_rowsumsq(c, ops::OP_T, ops::OP_N, rows, X->n, K, A->ptr, A->dtype, A->ld, X->ptr, BCUR_F64, X->ld,
+                           r.p());
+        CUDA_CHECK(cudaMemcpyAsync(rows_out, r.p(), rows * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    } else {
+        DMat* O = M(out);
+        if (O->dtype != BCUR_F64 || O->m != rows || O->n != X->n)
+            fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product: output must be fp64 rows × N");
+        ops::gemm(c, transpose ? ops::OP_T : ops::OP_N, ops::OP_N, rows, X->n, K, 1.0, A->ptr, A->dtype, A->ld,
+                  X->ptr, BCUR_F64, X->ld, 0.0, (double*)O->ptr, O->ld);
+    }
+    c->sync();
+    API_END
+}
+
 bcur_status bcur_draw_blocks(bcur_ctx ctx, const double* probs, int64_t G, int64_t g, int mode, const double* uniforms,
                              uint64_t seed, bcur_block_draw* out, double* margins_out) {
     API_BEGIN

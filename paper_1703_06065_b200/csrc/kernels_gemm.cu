@@ -215,6 +215,17 @@ namespace ops {
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (M <= 0 || N <= 0) return;
+    // fp32 A-passes → tcgen05 3×TF32 kernels
+    if (alpha == 1.0 && beta == 0.0 && dta == BCUR_F32 && dtb == BCUR_F64 && N <= 256 && K > 0) {
+        if (ta == OP_N && tb == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {
+            umma_ax(c, (const float*)A, M, K, lda, (const double*)B, N, ldb, C, ldc);
+            return;
+        }
+        if (ta == OP_T && tb == OP_N && umma_ok(dta, K, lda, A)) {
+            umma_atx(c, (const float*)A, K, M, lda, (const double*)B, N, ldb, C, ldc, nullptr);
+            return;
+        }
+    }
     ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_store_f32" : "gemm_store_f64", 2.0 * M * N * K,
                    (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M * N);
     if (K <= 0) {
@@ -256,6 +267,10 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                    const void* B, int dtb, int64_t ldb, double* rowsq) {
     if (M <= 0) return;
+    if (ta == OP_T && tb == OP_N && dta == BCUR_F32 && dtb == BCUR_F64 && N > 0 && K > 0 && umma_ok(dta, K, lda, A)) {
+        umma_atx(c, (const float*)A, K, M, lda, (const double*)B, N, ldb, nullptr, 0, rowsq);
+        return;
+    }
     ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_rowsumsq_f32" : "gemm_rowsumsq_f64",
                    2.0 * M * N * K, (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M);
     if (N <= 0) {

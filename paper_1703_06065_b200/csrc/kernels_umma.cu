@@ -1,0 +1,432 @@
+// kernels_umma.cu — the A-passes of the fp32 configs on 5th-gen tensor cores.
+//
+// fp32 accuracy from TF32 tensor cores with the 3×TF32 split (north star (1)):
+//   a = a_hi + a_lo, x = x_hi + x_lo (a_hi, x_hi exactly representable in TF32)
+//   a·x ≈ a_hi·x_hi + a_hi·x_lo + a_lo·x_hi          (3 tcgen05.mma kind::tf32)
+// accumulated in TMEM (fp32), epilogue in fp64.
+//
+//   AtX   Out(n×N) = Aᵀ·X   (Z = AᵀQ, Bᵀ = AᵀQ of the range finder; ‖Q_Cᵀ A_g‖² of the
+//                          residual / greedy score via the ROWSQ epilogue — never stored)
+//   AX    Out(m×N) = A·X    (Y = AΩ, Y = A·Z; split-K over the columns of A, fp64 partials)
+//
+// Per CTA: one 128-row output tile × BN columns; warp 0 issues TMA (A tile + x_hi/x_lo
+// tiles, 128B swizzle) into a multi-stage mbarrier ring; warps 2-5 form a_lo = a − trunc(a)
+// from the staged A tile (byte-image transform, swizzle-agnostic); warp 1 (one elected
+// lane) issues the 3×(BK/8) UMMAs per stage and commits to the ring's empty barriers;
+// after the last stage warps 2-5 drain the TMEM accumulator (tcgen05.ld 32x32b) into the
+// fused epilogue.  A (column-major) is a K-major operand for AtX and an MN-major operand
+// for AX; x_hi/x_lo are always K-major.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "ops.h"
+
+namespace bcur_b200 {
+namespace {
+
+constexpr int BM = 128, BK = 32, NTHREADS = 192;
+constexpr uint32_t A_TILE_BYTES = BM * BK * 4;  // 16 KB
+enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
+
+// ------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_u32(bar);
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, 0x989680;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}" ::"r"(a), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// SW128 shared-memory matrix descriptor (Blackwell version 1).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // version
+    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+#define TMEM_LD16(taddr, r)                                                                                        \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),         \
+                   "=r"(r[15])                                                                                     \
+                 : "r"(taddr))
+
+template <int BN>
+struct Smem {
+    static constexpr uint32_t X_TILE = BN * BK * 4;
+    static constexpr uint32_t STAGE = 2 * A_TILE_BYTES + 2 * X_TILE;
+    static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+    static constexpr uint32_t BYTES = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <bool A_MN, int BN, int EPI>
+__global__ void __launch_bounds__(NTHREADS, 1)
+k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
+       const __grid_constant__ CUtensorMap tmXl, int M, int N, int k_tiles, int k_tiles_per_split,
+       double* __restrict__ out, int64_t ldo, double* __restrict__ partial) {
+    using S = Smem<BN>;
+    constexpr int STAGES = S::STAGES;
+    constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                               ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * S::STAGE);
+    uint64_t* full = bars;
+    uint64_t* lo_ready = bars + STAGES;
+    uint64_t* empty = bars + 2 * STAGES;
+    uint64_t* tmem_full = bars + 3 * STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(bars + 3 * STAGES + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    int m_tile, n_tile, split;
+    if (A_MN) { m_tile = blockIdx.x; n_tile = blockIdx.y; split = blockIdx.z; }
+    else { n_tile = blockIdx.x; m_tile = blockIdx.y; split = 0; }
+    const int kt0 = split * k_tiles_per_split;
+    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
+    const int nk = kt1 - kt0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&lo_ready[s], 128);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXh) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXl) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto a_raw = [&](int s) { return smem + s * S::STAGE; };
+    auto a_lo = [&](int s) { return smem + s * S::STAGE + A_TILE_BYTES; };
+    auto x_hi = [&](int s) { return smem + s * S::STAGE + 2 * A_TILE_BYTES; };
+    auto x_lo = [&](int s) { return smem + s * S::STAGE + 2 * A_TILE_BYTES + S::X_TILE; };
+
+    if (warp == 0) {
+        // ------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % STAGES;
+                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_expect_tx(&full[s], A_TILE_BYTES + 2 * S::X_TILE);
+                const int k0 = (kt0 + i) * BK;
+                if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
+                else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
+                tma_load_2d(x_hi(s), &tmXh, &full[s], k0, n_tile * BN);
+                tma_load_2d(x_lo(s), &tmXl, &full[s], k0, n_tile * BN);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------ MMA issuer
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            mbar_wait(&lo_ready[s], ph);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
+                const uint32_t xh = smem_u32(x_hi(s)), xl = smem_u32(x_lo(s));
+#pragma unroll
+                for (int k8 = 0; k8 < BK / 8; ++k8) {
+                    uint64_t da_r, da_l;
+                    if (A_MN) {  // [4 MN atoms (LBO 4 KB)][32 K rows][128 B]; 8 K rows per MMA
+                        da_r = sdesc(ar + k8 * 1024, 4096, 1024);
+                        da_l = sdesc(al + k8 * 1024, 4096, 1024);
+                    } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
+                        da_r = sdesc(ar + k8 * 32, 16, 1024);
+                        da_l = sdesc(al + k8 * 32, 16, 1024);
+                    }
+                    const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024), dxl = sdesc(xl + k8 * 32, 16, 1024);
+                    const uint32_t acc0 = (i > 0 || k8 > 0) ? 1u : 0u;
+                    umma_tf32(tmem, da_r, dxh, IDESC, acc0);
+                    umma_tf32(tmem, da_r, dxl, IDESC, 1u);
+                    umma_tf32(tmem, da_l, dxh, IDESC, 1u);
+                }
+                umma_commit(&empty[s]);
+                if (i == nk - 1) umma_commit(tmem_full);
+            }
+            __syncwarp();
+        }
+        if (nk == 0 && lane == 0) mbar_arrive(tmem_full);
+    } else {
+        // ------------------------------------- a_lo transform, then epilogue
+        const int t = threadIdx.x - 64;  // 0..127
+        for (int i = 0; i < nk; ++i) {
+            const int s = i % STAGES;
+            const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+            mbar_wait(&full[s], ph);
+            const float4* src = (const float4*)a_raw(s);
+            float4* dst = (float4*)a_lo(s);
+#pragma unroll 4
+            for (int v = t; v < (int)(A_TILE_BYTES / 16); v += 128) {
+                const float4 a = src[v];
+                float4 l;
+                l.x = a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
+                l.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
+                l.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
+                l.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
+                dst[v] = l;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&lo_ready[s]);
+        }
+        // epilogue: warp w reads TMEM lanes 32·(w%4) .. +31 → tile rows
+        mbar_wait(tmem_full, 0);
+        tc_fence_after();
+        const int q = warp & 3;
+        const int row = m_tile * BM + q * 32 + lane;
+        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
+        double rowsq = 0.0;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            uint32_t r[16];
+            TMEM_LD16(tbase + c0, r);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (nk == 0) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) r[j] = 0u;
+            }
+            if (EPI == EPI_ROWSQ) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const double v = (double)__uint_as_float(r[j]);
+                    rowsq = fma(v, v, rowsq);
+                }
+            } else if (row < M) {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int col = n_tile * BN + c0 + j;
+                    if (col < N) {
+                        const double v = (double)__uint_as_float(r[j]);
+                        if (partial) partial[(int64_t)split * M * N + row + (int64_t)col * M] = v;
+                        else out[row + (int64_t)col * ldo] = v;
+                    }
+                }
+            }
+        }
+        if (EPI == EPI_ROWSQ && row < M) partial[(int64_t)n_tile * M + row] = rowsq;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    }
+}
+
+// ---------------------------------------------------------------- helpers
+__global__ void k_split_hilo(const double* __restrict__ x, int64_t K, int64_t N, int64_t ldx, float* __restrict__ hi,
+                             float* __restrict__ lo) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= K * N) return;
+    const int64_t i = e % K, j = e / K;
+    const float f = (float)x[i + j * ldx];
+    const float h = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+    hi[e] = h;
+    lo[e] = f - h;
+}
+
+__global__ void k_reduce_splits(int64_t M, int64_t N, int splits, const double* __restrict__ partial,
+                                double* __restrict__ out, int64_t ldo) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= M * N) return;
+    const int64_t i = e % M, j = e / M;
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * M * N + e];
+    out[i + j * ldo] = s;
+}
+
+__global__ void k_sum_tiles(int64_t M, int tiles, const double* __restrict__ partial, double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    double s = 0.0;
+    for (int t = 0; t < tiles; ++t) s += partial[(int64_t)t * M + i];
+    out[i] = s;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) fail(BCUR_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                     const uint32_t* box) {
+    CUtensorMap m;
+    uint32_t es[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides_bytes,
+                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(BCUR_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return m;
+}
+
+template <bool A_MN, int BN, int EPI>
+void launch_umma(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M, int N,
+                 int k_tiles, int kps, double* out, int64_t ldo, double* partial) {
+    auto kern = k_umma<A_MN, BN, EPI>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::BYTES));
+        attr = true;
+    }
+    kern<<<grid, NTHREADS, Smem<BN>::BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo, partial);
+    LAUNCH_CHECK(c);
+}
+
+int pick_bn(int64_t N) { return N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+
+// x (K × N fp64, ldx) → hi/lo fp32 (K × N, ld K)
+void split_x(Ctx* c, const double* x, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
+    *hi = DevBuf(c, (size_t)K * N * 4);
+    *lo = DevBuf(c, (size_t)K * N * 4);
+    k_split_hilo<<<(unsigned)((K * N + 255) / 256), 256, 0, c->stream>>>(x, K, N, ldx, hi->as<float>(), lo->as<float>());
+    LAUNCH_CHECK(c);
+}
+
+}  // namespace
+
+namespace ops {
+
+bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char* e = getenv("BCUR_DISABLE_UMMA");
+        enabled = (e && e[0] == '1') ? 0 : 1;
+    }
+    return enabled && dta == BCUR_F32 && m % 32 == 0 && (lda * 4) % 16 == 0 && ((uintptr_t)a % 16) == 0 && m > 0 &&
+           m < (1LL << 31);
+}
+
+// Out(n×N) = Aᵀ X  (A m×n fp32 col-major; X m×N fp64) → fp64 store, or per-row Σ² (rowsq != nullptr)
+void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
+              double* out, int64_t ldo, double* rowsq) {
+    if (n <= 0 || N <= 0) {
+        if (rowsq && n > 0) CUDA_CHECK(cudaMemsetAsync(rowsq, 0, n * sizeof(double), c->stream));
+        return;
+    }
+    ProfScope prof(c, rowsq ? "umma_atx_rowsq" : "umma_atx_store", 2.0 * n * N * m,
+                   4.0 * m * n + 8.0 * m * N + (rowsq ? 8.0 * n : 8.0 * n * N));
+    DevBuf xh, xl;
+    split_x(c, X, m, N, ldx, &xh, &xl);
+    const int bn = rowsq ? (N <= 128 ? pick_bn(N) : 256) : pick_bn(N);
+    if (!rowsq && N > 256) fail(BCUR_E_INVALID_ARGUMENT, "umma_atx: store epilogue supports N <= 256");
+    const uint64_t dA[2] = {(uint64_t)m, (uint64_t)n}, sA[1] = {(uint64_t)lda * 4};
+    const uint32_t bA[2] = {BK, BM};
+    const uint64_t dX[2] = {(uint64_t)m, (uint64_t)N}, sX[1] = {(uint64_t)m * 4};
+    const uint32_t bX[2] = {BK, (uint32_t)bn};
+    CUtensorMap ta = make_map(A, 2, dA, sA, bA);
+    CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX);
+    CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX);
+    const int k_tiles = (int)((m + BK - 1) / BK);
+    const int mt = (int)((n + BM - 1) / BM), nt = (int)((N + bn - 1) / bn);
+    dim3 grid(nt, mt, 1);
+    if (rowsq) {
+        DevBuf part(c, (size_t)nt * n * sizeof(double));
+        if (bn == 64) launch_umma<false, 64, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0, part.as<double>());
+        else if (bn == 128) launch_umma<false, 128, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0, part.as<double>());
+        else launch_umma<false, 256, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0, part.as<double>());
+        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt, part.as<double>(), rowsq);
+        LAUNCH_CHECK(c);
+    } else {
+        if (bn == 64) launch_umma<false, 64, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
+        else if (bn == 128) launch_umma<false, 128, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
+        else launch_umma<false, 256, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
+    }
+}
+
+// Out(m×N) = A X  (A m×n fp32; X n×N fp64), split-K over n with fp64 partials
+void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
+             double* out, int64_t ldo) {
+    if (m <= 0 || N <= 0) return;
+    if (N > 256) fail(BCUR_E_INVALID_ARGUMENT, "umma_ax supports N <= 256");
+    ProfScope prof(c, "umma_ax", 2.0 * m * n * N, 4.0 * m * n + 8.0 * n * N + 8.0 * m * N);
+    DevBuf xh, xl;
+    split_x(c, X, n, N, ldx, &xh, &xl);
+    const int bn = pick_bn(N);
+    // 3-D view of column-major A: (32 rows, n columns, m/32 row groups)
+    const uint64_t dA[3] = {32, (uint64_t)n, (uint64_t)(m / 32)}, sA[2] = {(uint64_t)lda * 4, 128};
+    const uint32_t bA[3] = {32, BK, BM / 32};
+    const uint64_t dX[2] = {(uint64_t)n, (uint64_t)N}, sX[1] = {(uint64_t)n * 4};
+    const uint32_t bX[2] = {BK, (uint32_t)bn};
+    CUtensorMap ta = make_map(A, 3, dA, sA, bA);
+    CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX);
+    CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX);
+    const int k_tiles = (int)((n + BK - 1) / BK);
+    const int mt = (int)((m + BM - 1) / BM);
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c->sm_count + mt - 1) / mt, k_tiles / 8));
+    const int kps = (k_tiles + splits - 1) / splits;
+    splits = (k_tiles + kps - 1) / kps;
+    DevBuf part(c, (size_t)splits * m * N * sizeof(double));
+    dim3 grid(mt, 1, splits);
+    if (bn == 64) launch_umma<true, 64, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
+    else if (bn == 128) launch_umma<true, 128, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
+    else launch_umma<true, 256, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
+    k_reduce_splits<<<(unsigned)((m * N + 255) / 256), 256, 0, c->stream>>>(m, N, splits, part.as<double>(), out, ldo);
+    LAUNCH_CHECK(c);
+}
+
+}  // namespace ops
+}  // namespace bcur_b200

@@ -34,6 +34,15 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
 
+// ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
+bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
+// Out(n×N) = Aᵀ X (fp64 store, N ≤ 256) or rowsq[j] = Σ_c (AᵀX)_jc² (any N)
+void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
+              double* out, int64_t ldo, double* rowsq);
+// Out(m×N) = A X (N ≤ 256)
+void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
+             double* out, int64_t ldo);
+
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
 // R upper with G = RᵀR; info[0] = 0 ok / j+1 failed pivot;
 // diag[0] = min diag(R), diag[1] = max diag(G) (input)

@@ -1,0 +1,56 @@
+"""tcgen05 3×TF32 sketch products vs exact fp64 products of the same fp32 A
+(the accuracy the range finder and residual passes rely on)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_1703_06065_b200 import bcur
+    return bcur
+
+
+def rel_fro(got, ref):
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+@pytest.mark.parametrize("m,n,N", [(512, 1024, 60), (1024, 768, 110), (256, 4096, 220), (2048, 512, 256),
+                                   (96, 1000, 17), (64, 200, 64)])
+def test_ax_and_atx(B, m, n, N):
+    gen = np.random.default_rng(m + n + N)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    a64 = a.astype(np.float64)
+    x = np.asfortranarray(gen.standard_normal((n, N)))
+    y = B.sketch_product(a, x)
+    assert rel_fro(y, a64 @ x) < 2e-6
+    q = np.asfortranarray(gen.standard_normal((m, N)))
+    z = B.sketch_product(a, q, transpose=True)
+    assert rel_fro(z, a64.T @ q) < 2e-6
+
+
+def test_low_mantissa_bits_are_kept(B):
+    """Inputs whose information sits below the TF32 mantissa: a plain TF32 product would
+    lose it (rel. error ~1e-3); the 3×TF32 split must keep fp32 accuracy."""
+    gen = np.random.default_rng(1)
+    m, n, N = 256, 512, 64
+    base = np.float32(1.0) + gen.integers(0, 1 << 13, size=(m, n)).astype(np.float32) * np.float32(2.0 ** -23)
+    a = np.asfortranarray(base * np.sign(gen.standard_normal((m, n))).astype(np.float32))
+    x = np.asfortranarray(gen.standard_normal((n, N)))
+    ref = a.astype(np.float64) @ x
+    assert rel_fro(B.sketch_product(a, x), ref) < 2e-6
+    q = np.asfortranarray(gen.standard_normal((m, N)))
+    assert rel_fro(B.sketch_product(a, q, transpose=True), a.astype(np.float64).T @ q) < 2e-6
+
+
+@pytest.mark.parametrize("N", [40, 128, 300, 1024])
+def test_fused_row_sumsq(B, N):
+    gen = np.random.default_rng(N)
+    m, n = 512, 1000
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    q = np.asfortranarray(gen.standard_normal((m, N)))
+    ref = np.sum((a.astype(np.float64).T @ q) ** 2, axis=1)
+    got = B.sketch_product(a, q, transpose=True, row_sumsq=True)
+    assert np.max(np.abs(got - ref) / ref) < 1e-5
+    assert abs(got.sum() - ref.sum()) / ref.sum() < 1e-7
