@@ -216,7 +216,7 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (M <= 0 || N <= 0) return;
     // fp32 A-passes → tcgen05 3×TF32 kernels
-    if (alpha == 1.0 && beta == 0.0 && dta == BCUR_F32 && dtb == BCUR_F64 && N <= 256 && K > 0) {
+    if (alpha == 1.0 && beta == 0.0 && dta == BCUR_F32 && dtb == BCUR_F64 && K > 0) {
         if (ta == OP_N && tb == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {
             umma_ax(c, (const float*)A, M, K, lda, (const double*)B, N, ldb, C, ldc);
             return;

@@ -2,20 +2,25 @@
 //
 // fp32 accuracy from TF32 tensor cores with the 3×TF32 split (north star (1)):
 //   a = a_hi + a_lo, x = x_hi + x_lo (a_hi, x_hi exactly representable in TF32)
-//   a·x ≈ a_hi·x_hi + a_hi·x_lo + a_lo·x_hi          (3 tcgen05.mma kind::tf32)
-// accumulated in TMEM (fp32), epilogue in fp64.
+//   a·x ≈ a_hi·x_hi + (a_hi·x_lo + a_lo·x_hi)          (3 tcgen05.mma kind::tf32)
 //
 //   AtX   Out(n×N) = Aᵀ·X   (Z = AᵀQ, Bᵀ = AᵀQ of the range finder; ‖Q_Cᵀ A_g‖² of the
 //                          residual / greedy score via the ROWSQ epilogue — never stored)
 //   AX    Out(m×N) = A·X    (Y = AΩ, Y = A·Z; split-K over the columns of A, fp64 partials)
 //
-// Per CTA: one 128-row output tile × BN columns; warp 0 issues TMA (A tile + x_hi/x_lo
-// tiles, 128B swizzle) into a multi-stage mbarrier ring; warps 2-5 form a_lo = a − trunc(a)
-// from the staged A tile (byte-image transform, swizzle-agnostic); warp 1 (one elected
-// lane) issues the 3×(BK/8) UMMAs per stage and commits to the ring's empty barriers;
-// after the last stage warps 2-5 drain the TMEM accumulator (tcgen05.ld 32x32b) into the
-// fused epilogue.  A (column-major) is a K-major operand for AtX and an MN-major operand
-// for AX; x_hi/x_lo are always K-major.
+// The tensor core's fp32 accumulate rounds toward zero at every MMA step (measured:
+// a bias of ≈ steps·2⁻²⁴ relative), so the accumulator is never long-lived: the hi·hi
+// and the small cross terms go to separate TMEM accumulators, which are double-buffered
+// and drained into fp64 registers every CH stages (K = CH·32) by the epilogue warps
+// while the MMA warp fills the other buffer.
+//
+// Warp roles (320 threads, 1 CTA/SM): warp 0 TMA producer (A tile + x_hi/x_lo tiles into
+// a 4-stage mbarrier ring); warp 1 TMEM allocator + single-lane UMMA issuer; warps 2,3,8,9
+// form a_lo = rn(a − trunc(a)) from the staged A tile (byte-image transform, swizzle-
+// agnostic — the tensor core truncates the raw fp32 tile to a_hi itself); warps 4-7 drain
+// TMEM (tcgen05.ld 32x32b, lane quarter = warp % 4) and run the fused epilogue.
+// A (column-major) is a K-major operand for AtX (SW128) and an MN-major operand for AX
+// (tf32 MN-major needs the 128B/32B-atom swizzle); x_hi/x_lo are K-major.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -24,9 +29,23 @@
 namespace bcur_b200 {
 namespace {
 
-constexpr int BM = 128, BK = 32, NTHREADS = 192;
-constexpr uint32_t A_TILE_BYTES = BM * BK * 4;  // 16 KB
+constexpr int BM = 128, BK = 32, BN = 64, CH = 2, STAGES = 4, NTHREADS = 320;
+constexpr uint32_t A_TILE = BM * BK * 4;            // 16 KB
+constexpr uint32_t X_TILE = BN * BK * 4;            // 8 KB
+constexpr uint32_t STAGE = 2 * A_TILE + 2 * X_TILE;  // 48 KB
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
+constexpr uint32_t TMEM_COLS = 4 * BN;               // 2 buffers × {hi, lo}
 enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
+
+// Round an fp32 value to the nearest TF32 (10-bit mantissa), ties to even.
+__device__ __forceinline__ float rn_tf32(float x) {
+    uint32_t u = __float_as_uint(x);
+    u += 0xFFFu + ((u >> 13) & 1u);
+    return __uint_as_float(u & 0xFFFFE000u);
+}
+// a_lo for a raw fp32 operand the tensor core truncates to TF32: the exact remainder,
+// itself rounded to TF32 so the hardware takes it unchanged.
+__device__ __forceinline__ float lo_of(float a) { return rn_tf32(a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u)); }
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -62,14 +81,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// SW128 shared-memory matrix descriptor (Blackwell version 1).
-__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+// Shared-memory matrix descriptor (Blackwell version 1).  layout: 2 = SWIZZLE_128B
+// (K-major operands), 1 = SWIZZLE_128B_BASE32B (MN-major 32-bit operands).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // version
-    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
     return d;
 }
 
@@ -93,33 +113,23 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    "=r"(r[15])                                                                                     \
                  : "r"(taddr))
 
-template <int BN>
-struct Smem {
-    static constexpr uint32_t X_TILE = BN * BK * 4;
-    static constexpr uint32_t STAGE = 2 * A_TILE_BYTES + 2 * X_TILE;
-    static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
-    static constexpr uint32_t BYTES = STAGES * STAGE + 1024 /*align*/ + 256 /*barriers*/;
-};
-
-template <bool A_MN, int BN, int EPI>
+template <bool A_MN, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
        const __grid_constant__ CUtensorMap tmXl, int M, int N, int k_tiles, int k_tiles_per_split,
        double* __restrict__ out, int64_t ldo, double* __restrict__ partial) {
-    using S = Smem<BN>;
-    constexpr int STAGES = S::STAGES;
-    constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* bars = (uint64_t*)(smem + STAGES * S::STAGE);
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE);
     uint64_t* full = bars;
     uint64_t* lo_ready = bars + STAGES;
     uint64_t* empty = bars + 2 * STAGES;
-    uint64_t* tmem_full = bars + 3 * STAGES;
-    uint32_t* tmem_slot = (uint32_t*)(bars + 3 * STAGES + 1);
+    uint64_t* tfull = bars + 3 * STAGES;       // [2]
+    uint64_t* tempty = bars + 3 * STAGES + 2;  // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 3 * STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     int m_tile, n_tile, split;
@@ -127,7 +137,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     else { n_tile = blockIdx.x; m_tile = blockIdx.y; split = 0; }
     const int kt0 = split * k_tiles_per_split;
     const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
-    const int nk = kt1 - kt0;
+    const int nk = max(kt1 - kt0, 0);
+    const int nchunks = (nk + CH - 1) / CH;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -135,7 +146,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             mbar_init(&lo_ready[s], 128);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXh) : "memory");
@@ -151,19 +165,18 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    auto a_raw = [&](int s) { return smem + s * S::STAGE; };
-    auto a_lo = [&](int s) { return smem + s * S::STAGE + A_TILE_BYTES; };
-    auto x_hi = [&](int s) { return smem + s * S::STAGE + 2 * A_TILE_BYTES; };
-    auto x_lo = [&](int s) { return smem + s * S::STAGE + 2 * A_TILE_BYTES + S::X_TILE; };
+    auto a_raw = [&](int s) { return smem + s * STAGE; };
+    auto a_lo = [&](int s) { return smem + s * STAGE + A_TILE; };
+    auto x_hi = [&](int s) { return smem + s * STAGE + 2 * A_TILE; };
+    auto x_lo = [&](int s) { return smem + s * STAGE + 2 * A_TILE + X_TILE; };
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         if (lane == 0) {
             for (int i = 0; i < nk; ++i) {
                 const int s = i % STAGES;
-                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                mbar_expect_tx(&full[s], A_TILE_BYTES + 2 * S::X_TILE);
+                mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
+                mbar_expect_tx(&full[s], A_TILE + 2 * X_TILE);
                 const int k0 = (kt0 + i) * BK;
                 if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
                 else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
@@ -175,92 +188,95 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         // ------------------------------------------------------ MMA issuer
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
+            const int c = i / CH, b = c & 1;
+            const bool first = (i % CH) == 0;
+            if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
             const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
             mbar_wait(&full[s], ph);
             mbar_wait(&lo_ready[s], ph);
             tc_fence_after();
             if (lane == 0) {
+                const uint32_t t_hi = tmem + (uint32_t)(b * 2 * BN), t_lo = t_hi + BN;
                 const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
                 const uint32_t xh = smem_u32(x_hi(s)), xl = smem_u32(x_lo(s));
 #pragma unroll
                 for (int k8 = 0; k8 < BK / 8; ++k8) {
                     uint64_t da_r, da_l;
-                    if (A_MN) {  // [4 MN atoms (LBO 4 KB)][32 K rows][128 B]; 8 K rows per MMA
-                        da_r = sdesc(ar + k8 * 1024, 4096, 1024);
-                        da_l = sdesc(al + k8 * 1024, 4096, 1024);
+                    if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
+                        da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
+                        da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
                     } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
-                        da_r = sdesc(ar + k8 * 32, 16, 1024);
-                        da_l = sdesc(al + k8 * 32, 16, 1024);
+                        da_r = sdesc(ar + k8 * 32, 16, 1024, 2);
+                        da_l = sdesc(al + k8 * 32, 16, 1024, 2);
                     }
-                    const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024), dxl = sdesc(xl + k8 * 32, 16, 1024);
-                    const uint32_t acc0 = (i > 0 || k8 > 0) ? 1u : 0u;
-                    umma_tf32(tmem, da_r, dxh, IDESC, acc0);
-                    umma_tf32(tmem, da_r, dxl, IDESC, 1u);
-                    umma_tf32(tmem, da_l, dxh, IDESC, 1u);
+                    const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2), dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
+                    const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                    umma_tf32(t_hi, da_r, dxh, IDESC, acc);
+                    umma_tf32(t_lo, da_r, dxl, IDESC, acc);
+                    umma_tf32(t_lo, da_l, dxh, IDESC, 1u);
                 }
                 umma_commit(&empty[s]);
-                if (i == nk - 1) umma_commit(tmem_full);
+                if ((i % CH) == CH - 1 || i == nk - 1) umma_commit(&tfull[b]);
             }
             __syncwarp();
         }
-        if (nk == 0 && lane == 0) mbar_arrive(tmem_full);
-    } else {
-        // ------------------------------------- a_lo transform, then epilogue
-        const int t = threadIdx.x - 64;  // 0..127
+    } else if (warp >= 4 && warp < 8) {
+        // ------------------------------------------- TMEM drain + epilogue
+        const int q = warp & 3;
+        const int row = m_tile * BM + q * 32 + lane;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        double acc[BN];
+#pragma unroll
+        for (int j = 0; j < BN; ++j) acc[j] = 0.0;
+        for (int c = 0; c < nchunks; ++c) {
+            const int b = c & 1;
+            mbar_wait(&tfull[b], (uint32_t)(c / 2) & 1u);
+            tc_fence_after();
+            const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * 2 * BN), t_lo = t_hi + BN;
+#pragma unroll
+            for (int j0 = 0; j0 < BN; j0 += 16) {
+                uint32_t h[16], l[16];
+                TMEM_LD16(t_hi + j0, h);
+                TMEM_LD16(t_lo + j0, l);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    acc[j0 + j] += (double)__uint_as_float(h[j]) + (double)__uint_as_float(l[j]);
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[b]);
+        }
+        if (EPI == EPI_ROWSQ) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < BN; ++j) s = fma(acc[j], acc[j], s);  // columns ≥ N are exact zeros
+            if (row < M) partial[(int64_t)n_tile * M + row] = s;
+        } else if (row < M) {
+#pragma unroll
+            for (int j = 0; j < BN; ++j) {
+                const int col = n_tile * BN + j;
+                if (col < N) {
+                    if (partial) partial[(int64_t)split * M * N + row + (int64_t)col * M] = acc[j];
+                    else out[row + (int64_t)col * ldo] = acc[j];
+                }
+            }
+        }
+    } else if (warp >= 2) {
+        // ------------------------------------------------ a_lo transform
+        const int t = (warp < 4 ? warp - 2 : warp - 6) * 32 + lane;  // 0..127
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
-            const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-            mbar_wait(&full[s], ph);
+            mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
             const float4* src = (const float4*)a_raw(s);
             float4* dst = (float4*)a_lo(s);
 #pragma unroll 4
-            for (int v = t; v < (int)(A_TILE_BYTES / 16); v += 128) {
+            for (int v = t; v < (int)(A_TILE / 16); v += 128) {
                 const float4 a = src[v];
-                float4 l;
-                l.x = a.x - __uint_as_float(__float_as_uint(a.x) & 0xFFFFE000u);
-                l.y = a.y - __uint_as_float(__float_as_uint(a.y) & 0xFFFFE000u);
-                l.z = a.z - __uint_as_float(__float_as_uint(a.z) & 0xFFFFE000u);
-                l.w = a.w - __uint_as_float(__float_as_uint(a.w) & 0xFFFFE000u);
-                dst[v] = l;
+                dst[v] = make_float4(lo_of(a.x), lo_of(a.y), lo_of(a.z), lo_of(a.w));
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&lo_ready[s]);
         }
-        // epilogue: warp w reads TMEM lanes 32·(w%4) .. +31 → tile rows
-        mbar_wait(tmem_full, 0);
-        tc_fence_after();
-        const int q = warp & 3;
-        const int row = m_tile * BM + q * 32 + lane;
-        const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
-        double rowsq = 0.0;
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-            uint32_t r[16];
-            TMEM_LD16(tbase + c0, r);
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            if (nk == 0) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) r[j] = 0u;
-            }
-            if (EPI == EPI_ROWSQ) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const double v = (double)__uint_as_float(r[j]);
-                    rowsq = fma(v, v, rowsq);
-                }
-            } else if (row < M) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int col = n_tile * BN + c0 + j;
-                    if (col < N) {
-                        const double v = (double)__uint_as_float(r[j]);
-                        if (partial) partial[(int64_t)split * M * N + row + (int64_t)col * M] = v;
-                        else out[row + (int64_t)col * ldo] = v;
-                    }
-                }
-            }
-        }
-        if (EPI == EPI_ROWSQ && row < M) partial[(int64_t)n_tile * M + row] = rowsq;
     }
     tc_fence_before();
     __syncthreads();
@@ -271,15 +287,17 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 }
 
 // ---------------------------------------------------------------- helpers
+// x (K × N fp64) → x_hi = rn_tf32(x), x_lo = rn_tf32(x − x_hi) (fp32, ld K).  x_hi = rn(x)
+// makes x_lo sign-symmetric, so the dropped a_lo·x_lo term carries no bias.
 __global__ void k_split_hilo(const double* __restrict__ x, int64_t K, int64_t N, int64_t ldx, float* __restrict__ hi,
                              float* __restrict__ lo) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= K * N) return;
     const int64_t i = e % K, j = e / K;
-    const float f = (float)x[i + j * ldx];
-    const float h = __uint_as_float(__float_as_uint(f) & 0xFFFFE000u);
+    const double xd = x[i + j * ldx];
+    const float h = rn_tf32((float)xd);
     hi[e] = h;
-    lo[e] = f - h;
+    lo[e] = rn_tf32((float)(xd - (double)h));
 }
 
 __global__ void k_reduce_splits(int64_t M, int64_t N, int splits, const double* __restrict__ partial,
@@ -313,30 +331,28 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                     const uint32_t* box) {
+                     const uint32_t* box, CUtensorMapSwizzle swz) {
     CUtensorMap m;
     uint32_t es[3] = {1, 1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides_bytes,
-                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(BCUR_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
 }
 
-template <bool A_MN, int BN, int EPI>
+template <bool A_MN, int EPI>
 void launch_umma(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M, int N,
                  int k_tiles, int kps, double* out, int64_t ldo, double* partial) {
-    auto kern = k_umma<A_MN, BN, EPI>;
+    auto kern = k_umma<A_MN, EPI>;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<BN>::BYTES));
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
         attr = true;
     }
-    kern<<<grid, NTHREADS, Smem<BN>::BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo, partial);
+    kern<<<grid, NTHREADS, SMEM_BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo, partial);
     LAUNCH_CHECK(c);
 }
-
-int pick_bn(int64_t N) { return N <= 64 ? 64 : N <= 128 ? 128 : 256; }
 
 // x (K × N fp64, ldx) → hi/lo fp32 (K × N, ld K)
 void split_x(Ctx* c, const double* x, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
@@ -371,29 +387,24 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const d
                    4.0 * m * n + 8.0 * m * N + (rowsq ? 8.0 * n : 8.0 * n * N));
     DevBuf xh, xl;
     split_x(c, X, m, N, ldx, &xh, &xl);
-    const int bn = rowsq ? (N <= 128 ? pick_bn(N) : 256) : pick_bn(N);
-    if (!rowsq && N > 256) fail(BCUR_E_INVALID_ARGUMENT, "umma_atx: store epilogue supports N <= 256");
     const uint64_t dA[2] = {(uint64_t)m, (uint64_t)n}, sA[1] = {(uint64_t)lda * 4};
     const uint32_t bA[2] = {BK, BM};
     const uint64_t dX[2] = {(uint64_t)m, (uint64_t)N}, sX[1] = {(uint64_t)m * 4};
-    const uint32_t bX[2] = {BK, (uint32_t)bn};
-    CUtensorMap ta = make_map(A, 2, dA, sA, bA);
-    CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX);
-    CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX);
+    const uint32_t bX[2] = {BK, BN};
+    CUtensorMap ta = make_map(A, 2, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B);
+    CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
+    CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     const int k_tiles = (int)((m + BK - 1) / BK);
-    const int mt = (int)((n + BM - 1) / BM), nt = (int)((N + bn - 1) / bn);
-    dim3 grid(nt, mt, 1);
+    const int mt = (int)((n + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    dim3 grid(nt, mt, 1);  // N tiles of one A row-tile run side by side and share it through L2
     if (rowsq) {
         DevBuf part(c, (size_t)nt * n * sizeof(double));
-        if (bn == 64) launch_umma<false, 64, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0, part.as<double>());
-        else if (bn == 128) launch_umma<false, 128, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0, part.as<double>());
-        else launch_umma<false, 256, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0, part.as<double>());
+        launch_umma<false, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0,
+                                      part.as<double>());
         k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt, part.as<double>(), rowsq);
         LAUNCH_CHECK(c);
     } else {
-        if (bn == 64) launch_umma<false, 64, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
-        else if (bn == 128) launch_umma<false, 128, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
-        else launch_umma<false, 256, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
+        launch_umma<false, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
     }
 }
 
@@ -401,29 +412,26 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const d
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
              double* out, int64_t ldo) {
     if (m <= 0 || N <= 0) return;
-    if (N > 256) fail(BCUR_E_INVALID_ARGUMENT, "umma_ax supports N <= 256");
     ProfScope prof(c, "umma_ax", 2.0 * m * n * N, 4.0 * m * n + 8.0 * n * N + 8.0 * m * N);
     DevBuf xh, xl;
     split_x(c, X, n, N, ldx, &xh, &xl);
-    const int bn = pick_bn(N);
     // 3-D view of column-major A: (32 rows, n columns, m/32 row groups)
     const uint64_t dA[3] = {32, (uint64_t)n, (uint64_t)(m / 32)}, sA[2] = {(uint64_t)lda * 4, 128};
     const uint32_t bA[3] = {32, BK, BM / 32};
     const uint64_t dX[2] = {(uint64_t)n, (uint64_t)N}, sX[1] = {(uint64_t)n * 4};
-    const uint32_t bX[2] = {BK, (uint32_t)bn};
-    CUtensorMap ta = make_map(A, 3, dA, sA, bA);
-    CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX);
-    CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX);
+    const uint32_t bX[2] = {BK, BN};
+    CUtensorMap ta = make_map(A, 3, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
+    CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     const int k_tiles = (int)((n + BK - 1) / BK);
-    const int mt = (int)((m + BM - 1) / BM);
-    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c->sm_count + mt - 1) / mt, k_tiles / 8));
+    const int mt = (int)((m + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c->sm_count + mt * nt - 1) / (mt * nt),
+                                                             k_tiles / 16));
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
     DevBuf part(c, (size_t)splits * m * N * sizeof(double));
-    dim3 grid(mt, 1, splits);
-    if (bn == 64) launch_umma<true, 64, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
-    else if (bn == 128) launch_umma<true, 128, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
-    else launch_umma<true, 256, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
+    dim3 grid(mt, nt, splits);
+    launch_umma<true, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
     k_reduce_splits<<<(unsigned)((m * N + 255) / 256), 256, 0, c->stream>>>(m, N, splits, part.as<double>(), out, ldo);
     LAUNCH_CHECK(c);
 }
