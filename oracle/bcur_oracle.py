@@ -646,13 +646,38 @@ def unique_in_order(blocks: Sequence[int]) -> List[int]:
     return out
 
 
+def cholqr2_whole(c: np.ndarray, dt) -> Optional[np.ndarray]:
+    """Whole-C CholQR2 when C is safely full rank: chol(CᵀC) succeeds with
+    min R_ii > τ_chol · max_j ‖c_j‖ (the same test the GPU applies before taking
+    its tensor-core path); None → fall back to block CGS2 panels."""
+    if c.shape[1] == 0:
+        return None
+    g = c.T @ c
+    r = chol_upper(g)
+    ref = float(np.sqrt(np.max(np.diag(g))))
+    if r is None or not np.all(np.isfinite(r)) or not np.min(np.diag(r)) > TAU_CHOL[np.dtype(dt)] * ref:
+        return None
+    q1 = np.linalg.solve(r.T, c.T).T
+    r2 = chol_upper(q1.T @ q1)
+    if r2 is None:
+        return None
+    return np.linalg.solve(r2.T, q1.T).T
+
+
 def column_basis(a64: np.ndarray, part: BlockPartition, blocks: Sequence[int], dt,
-                 block_norms: np.ndarray):
-    """Q_C for the unique selected blocks (draw order), block CGS2 panels."""
+                 block_norms: np.ndarray, allow_whole: bool = True):
+    """Q_C for the unique selected blocks (draw order): whole-C CholQR2 when safely
+    full rank, else block CGS2 panels with per-panel rank revealing."""
     m = a64.shape[0]
+    ub = unique_in_order(blocks)
+    if allow_whole and np.dtype(dt) == np.float32:
+        cols = np.concatenate([a64[:, part.ranges[b][0]:part.ranges[b][1]] for b in ub], axis=1)
+        q = cholqr2_whole(cols, dt)
+        if q is not None:
+            return q, ["whole"]
     qc = np.zeros((m, 0))
     paths = []
-    for bidx in unique_in_order(blocks):
+    for bidx in ub:
         b, e = part.ranges[bidx]
         ref = math.sqrt(block_norms[bidx])
         qn, _, _, path = cgs2_panel(qc, a64[:, b:e].copy(), ref, dt)

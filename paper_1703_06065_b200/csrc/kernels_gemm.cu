@@ -216,13 +216,13 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc) {
     if (M <= 0 || N <= 0) return;
     // fp32 A-passes → tcgen05 3×TF32 kernels
-    if (alpha == 1.0 && beta == 0.0 && dta == BCUR_F32 && dtb == BCUR_F64 && K > 0) {
-        if (ta == OP_N && tb == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {
-            umma_ax(c, (const float*)A, M, K, lda, (const double*)B, N, ldb, C, ldc);
+    if (dta == BCUR_F32 && K > 0 && tb == OP_N) {
+        if (ta == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {
+            umma_ax(c, (const float*)A, M, K, lda, B, dtb, N, ldb, alpha, beta, C, ldc);
             return;
         }
-        if (ta == OP_T && tb == OP_N && umma_ok(dta, K, lda, A)) {
-            umma_atx(c, (const float*)A, K, M, lda, (const double*)B, N, ldb, C, ldc, nullptr);
+        if (ta == OP_T && umma_ok(dta, K, lda, A)) {
+            umma_atx(c, (const float*)A, K, M, lda, B, dtb, N, ldb, alpha, beta, C, ldc, nullptr);
             return;
         }
     }
@@ -267,8 +267,8 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                    const void* B, int dtb, int64_t ldb, double* rowsq) {
     if (M <= 0) return;
-    if (ta == OP_T && tb == OP_N && dta == BCUR_F32 && dtb == BCUR_F64 && N > 0 && K > 0 && umma_ok(dta, K, lda, A)) {
-        umma_atx(c, (const float*)A, K, M, lda, (const double*)B, N, ldb, nullptr, 0, rowsq);
+    if (ta == OP_T && tb == OP_N && dta == BCUR_F32 && N > 0 && K > 0 && umma_ok(dta, K, lda, A)) {
+        umma_atx(c, (const float*)A, K, M, lda, B, dtb, N, ldb, 1.0, 0.0, nullptr, 0, rowsq);
         return;
     }
     ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_rowsumsq_f32" : "gemm_rowsumsq_f64",

@@ -1,20 +1,20 @@
-// kernels_misc.cu — layout/elementwise helpers (dtype conversion, scaling, copies).
+// kernels_misc.cu — layout/elementwise helpers (dtype conversion, transposes, scaling, copies).
 #include "ops.h"
 
 namespace bcur_b200 {
 namespace {
 
-template <class T>
-__global__ void k_convert(const T* __restrict__ src, int64_t m, int64_t n, int64_t lds, double* __restrict__ dst,
+template <class TS, class TD>
+__global__ void k_convert(const TS* __restrict__ src, int64_t m, int64_t n, int64_t lds, TD* __restrict__ dst,
                           int64_t ldd) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m * n) return;
     const int64_t i = e % m, j = e / m;
-    dst[i + j * ldd] = (double)src[i + j * lds];
+    dst[i + j * ldd] = (TD)src[i + j * lds];
 }
 
-template <class T>
-__global__ void k_transpose(const T* __restrict__ src, int64_t m, int64_t n, int64_t lds, double* __restrict__ dst,
+template <class TS, class TD>
+__global__ void k_transpose(const TS* __restrict__ src, int64_t m, int64_t n, int64_t lds, TD* __restrict__ dst,
                             int64_t ldd) {
     __shared__ double tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
@@ -25,7 +25,7 @@ __global__ void k_transpose(const T* __restrict__ src, int64_t m, int64_t n, int
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
         const int64_t j = j0 + threadIdx.x, i = i0 + r;  // dst(j, i) = src(i, j)
-        if (i < m && j < n) dst[j + i * ldd] = tile[threadIdx.x][r];
+        if (i < m && j < n) dst[j + i * ldd] = (TD)tile[threadIdx.x][r];
     }
 }
 
@@ -41,17 +41,16 @@ __global__ void k_scale_columns(double* x, int64_t m, int64_t n, int64_t ld, con
     x[i + j * ld] *= s[j];
 }
 
-__global__ void k_copy(const double* __restrict__ src, int64_t m, int64_t n, int64_t lds, double* __restrict__ dst,
-                       int64_t ldd) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= m * n) return;
-    const int64_t i = e % m, j = e / m;
-    dst[i + j * ldd] = src[i + j * lds];
-}
-
 __global__ void k_axpy_neg(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n) y[e] -= x[e];
+}
+
+__global__ void k_zero_lower(double* x, int64_t w, int64_t ld) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= w * w) return;
+    const int64_t i = e % w, j = e / w;
+    if (i > j) x[i + j * ld] = 0.0;
 }
 
 inline unsigned nblk(int64_t count) { return (unsigned)((count + 255) / 256); }
@@ -60,35 +59,52 @@ inline unsigned nblk(int64_t count) { return (unsigned)((count + 255) / 256); }
 
 namespace ops {
 
-void axpy_neg(Ctx* c, const double* x, double* y, int64_t n) {
-    if (n <= 0) return;
-    k_axpy_neg<<<nblk(n), 256, 0, c->stream>>>(x, y, n);
+void convert(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd) {
+    if (m * n == 0) return;
+    const unsigned g = nblk(m * n);
+    if (dts == BCUR_F32 && dtd == BCUR_F32)
+        k_convert<float, float><<<g, 256, 0, c->stream>>>((const float*)src, m, n, lds, (float*)dst, ldd);
+    else if (dts == BCUR_F32)
+        k_convert<float, double><<<g, 256, 0, c->stream>>>((const float*)src, m, n, lds, (double*)dst, ldd);
+    else if (dtd == BCUR_F32)
+        k_convert<double, float><<<g, 256, 0, c->stream>>>((const double*)src, m, n, lds, (float*)dst, ldd);
+    else
+        k_convert<double, double><<<g, 256, 0, c->stream>>>((const double*)src, m, n, lds, (double*)dst, ldd);
     LAUNCH_CHECK(c);
 }
 
 void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
+    convert(c, src, dt, m, n, lds, dst, BCUR_F64, ldd);
+}
+
+void transpose(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd) {
     if (m * n == 0) return;
-    if (dt == BCUR_F32)
-        k_convert<float><<<nblk(m * n), 256, 0, c->stream>>>((const float*)src, m, n, lds, dst, ldd);
+    dim3 grid((unsigned)((m + 31) / 32), (unsigned)((n + 31) / 32));
+    dim3 block(32, 8);
+    if (dts == BCUR_F32 && dtd == BCUR_F32)
+        k_transpose<float, float><<<grid, block, 0, c->stream>>>((const float*)src, m, n, lds, (float*)dst, ldd);
+    else if (dts == BCUR_F32)
+        k_transpose<float, double><<<grid, block, 0, c->stream>>>((const float*)src, m, n, lds, (double*)dst, ldd);
+    else if (dtd == BCUR_F32)
+        k_transpose<double, float><<<grid, block, 0, c->stream>>>((const double*)src, m, n, lds, (float*)dst, ldd);
     else
-        k_convert<double><<<nblk(m * n), 256, 0, c->stream>>>((const double*)src, m, n, lds, dst, ldd);
+        k_transpose<double, double><<<grid, block, 0, c->stream>>>((const double*)src, m, n, lds, (double*)dst, ldd);
     LAUNCH_CHECK(c);
 }
 
 void transpose_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
-    if (m * n == 0) return;
-    dim3 grid((unsigned)((m + 31) / 32), (unsigned)((n + 31) / 32));
-    dim3 block(32, 8);
-    if (dt == BCUR_F32)
-        k_transpose<float><<<grid, block, 0, c->stream>>>((const float*)src, m, n, lds, dst, ldd);
-    else
-        k_transpose<double><<<grid, block, 0, c->stream>>>((const double*)src, m, n, lds, dst, ldd);
-    LAUNCH_CHECK(c);
+    transpose(c, src, dt, m, n, lds, dst, BCUR_F64, ldd);
 }
 
 void fill_f64(Ctx* c, double* p, int64_t count, double v) {
     if (count <= 0) return;
     k_fill<<<nblk(count), 256, 0, c->stream>>>(p, count, v);
+    LAUNCH_CHECK(c);
+}
+
+void axpy_neg(Ctx* c, const double* x, double* y, int64_t n) {
+    if (n <= 0) return;
+    k_axpy_neg<<<nblk(n), 256, 0, c->stream>>>(x, y, n);
     LAUNCH_CHECK(c);
 }
 
@@ -99,8 +115,12 @@ void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const do
 }
 
 void copy_f64(Ctx* c, const double* src, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
-    if (m * n == 0) return;
-    k_copy<<<nblk(m * n), 256, 0, c->stream>>>(src, m, n, lds, dst, ldd);
+    convert(c, src, BCUR_F64, m, n, lds, dst, BCUR_F64, ldd);
+}
+
+void zero_lower(Ctx* c, double* x, int64_t w, int64_t ld) {
+    if (w <= 0) return;
+    k_zero_lower<<<nblk(w * w), 256, 0, c->stream>>>(x, w, ld);
     LAUNCH_CHECK(c);
 }
 

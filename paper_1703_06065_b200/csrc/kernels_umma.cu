@@ -29,12 +29,21 @@
 namespace bcur_b200 {
 namespace {
 
-constexpr int BM = 128, BK = 32, BN = 64, CH = 2, STAGES = 4, NTHREADS = 320;
-constexpr uint32_t A_TILE = BM * BK * 4;            // 16 KB
-constexpr uint32_t X_TILE = BN * BK * 4;            // 8 KB
-constexpr uint32_t STAGE = 2 * A_TILE + 2 * X_TILE;  // 48 KB
-constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
-constexpr uint32_t TMEM_COLS = 4 * BN;               // 2 buffers × {hi, lo}
+constexpr int BM = 128, BK = 32, BN = 64, CH = 2;
+constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
+constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
+
+// NT 64-column N tiles per CTA share every staged A tile (NT = 2 halves the L2 bytes
+// per MMA for wide products).  TMEM: NT tiles × {hi, lo} × 2 buffers × 64 columns.
+template <int NT>
+struct Cfg {
+    static constexpr uint32_t STAGE = 2 * A_TILE + 2 * NT * X_TILE;  // 48 KB / 64 KB
+    static constexpr int STAGES = NT == 1 ? 4 : 3;
+    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
+    static constexpr uint32_t TMEM_COLS = 4 * BN * NT;
+    static constexpr int NTRANSFORM = NT == 1 ? 4 : 2;                    // transform warps
+    static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + 4 * NT);       // 320 / 384
+};
 enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
 
 // Round an fp32 value to the nearest TF32 (10-bit mantissa), ties to even.
@@ -113,14 +122,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    "=r"(r[15])                                                                                     \
                  : "r"(taddr))
 
-template <bool A_MN, int EPI>
-__global__ void __launch_bounds__(NTHREADS, 1)
+template <bool A_MN, int EPI, int NT>
+__global__ void __launch_bounds__(Cfg<NT>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
        const __grid_constant__ CUtensorMap tmXl, int M, int N, int k_tiles, int k_tiles_per_split,
-       double* __restrict__ out, int64_t ldo, double* __restrict__ partial) {
+       double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta) {
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
+    using CF = Cfg<NT>;
+    constexpr int STAGES = CF::STAGES;
+    constexpr uint32_t STAGE = CF::STAGE, TMEM_COLS = CF::TMEM_COLS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE);
@@ -143,12 +155,12 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&lo_ready[s], 128);
+            mbar_init(&lo_ready[s], 32 * CF::NTRANSFORM);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128);
+            mbar_init(&tempty[b], 128 * NT);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -167,8 +179,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 
     auto a_raw = [&](int s) { return smem + s * STAGE; };
     auto a_lo = [&](int s) { return smem + s * STAGE + A_TILE; };
+    // per stage: [a_raw][a_lo][x_hi tile 0..NT-1][x_lo tile 0..NT-1]
     auto x_hi = [&](int s) { return smem + s * STAGE + 2 * A_TILE; };
-    auto x_lo = [&](int s) { return smem + s * STAGE + 2 * A_TILE + X_TILE; };
+    auto x_lo = [&](int s) { return smem + s * STAGE + 2 * A_TILE + NT * X_TILE; };
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -176,12 +189,15 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             for (int i = 0; i < nk; ++i) {
                 const int s = i % STAGES;
                 mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
-                mbar_expect_tx(&full[s], A_TILE + 2 * X_TILE);
+                mbar_expect_tx(&full[s], A_TILE + 2 * NT * X_TILE);
                 const int k0 = (kt0 + i) * BK;
                 if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
                 else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
-                tma_load_2d(x_hi(s), &tmXh, &full[s], k0, n_tile * BN);
-                tma_load_2d(x_lo(s), &tmXl, &full[s], k0, n_tile * BN);
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
+                    tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
+                }
             }
         }
     } else if (warp == 1) {
@@ -196,11 +212,14 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             mbar_wait(&lo_ready[s], ph);
             tc_fence_after();
             if (lane == 0) {
-                const uint32_t t_hi = tmem + (uint32_t)(b * 2 * BN), t_lo = t_hi + BN;
                 const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
-                const uint32_t xh = smem_u32(x_hi(s)), xl = smem_u32(x_lo(s));
 #pragma unroll
-                for (int k8 = 0; k8 < BK / 8; ++k8) {
+                for (int k8 = 0; k8 < BK / 8; ++k8)
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    // TMEM columns: [buffer b][tile nt][hi | lo]
+                    const uint32_t t_hi = tmem + (uint32_t)((b * NT + nt) * 2 * BN), t_lo = t_hi + BN;
+                    const uint32_t xh = smem_u32(x_hi(s)) + nt * X_TILE, xl = smem_u32(x_lo(s)) + nt * X_TILE;
                     uint64_t da_r, da_l;
                     if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
                         da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
@@ -220,10 +239,12 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             }
             __syncwarp();
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= 4 && warp < 4 + 4 * NT) {
         // ------------------------------------------- TMEM drain + epilogue
-        const int q = warp & 3;
+        const int q = warp & 3;                 // TMEM lane quarter (warp % 4)
+        const int nt = (warp - 4) >> 2;         // N tile drained by this warp
         const int row = m_tile * BM + q * 32 + lane;
+        const int col0 = (n_tile * NT + nt) * BN;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         double acc[BN];
 #pragma unroll
@@ -232,7 +253,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const int b = c & 1;
             mbar_wait(&tfull[b], (uint32_t)(c / 2) & 1u);
             tc_fence_after();
-            const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * 2 * BN), t_lo = t_hi + BN;
+            const uint32_t t_hi = tmem + lane_off + (uint32_t)((b * NT + nt) * 2 * BN), t_lo = t_hi + BN;
 #pragma unroll
             for (int j0 = 0; j0 < BN; j0 += 16) {
                 uint32_t h[16], l[16];
@@ -250,29 +271,36 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < BN; ++j) s = fma(acc[j], acc[j], s);  // columns ≥ N are exact zeros
-            if (row < M) partial[(int64_t)n_tile * M + row] = s;
+            if (row < M) partial[(int64_t)(n_tile * NT + nt) * M + row] = s;
         } else if (row < M) {
 #pragma unroll
             for (int j = 0; j < BN; ++j) {
-                const int col = n_tile * BN + j;
+                const int col = col0 + j;
                 if (col < N) {
-                    if (partial) partial[(int64_t)split * M * N + row + (int64_t)col * M] = acc[j];
-                    else out[row + (int64_t)col * ldo] = acc[j];
+                    if (partial) {
+                        partial[(int64_t)split * M * N + row + (int64_t)col * M] = acc[j];
+                    } else {
+                        double* o = out + row + (int64_t)col * ldo;
+                        *o = beta == 0.0 ? alpha * acc[j] : fma(beta, *o, alpha * acc[j]);
+                    }
                 }
             }
         }
     } else if (warp >= 2) {
         // ------------------------------------------------ a_lo transform
-        const int t = (warp < 4 ? warp - 2 : warp - 6) * 32 + lane;  // 0..127
+        constexpr int NTT = 32 * CF::NTRANSFORM;
+        const int t = (warp < 4 ? warp - 2 : warp - (4 + 4 * NT) + 2) * 32 + lane;  // 0..NTT-1
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
             mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
-            const float4* src = (const float4*)a_raw(s);
-            float4* dst = (float4*)a_lo(s);
+            const uint32_t src = smem_u32(a_raw(s)), dst = smem_u32(a_lo(s));
 #pragma unroll 4
-            for (int v = t; v < (int)(A_TILE / 16); v += 128) {
-                const float4 a = src[v];
-                dst[v] = make_float4(lo_of(a.x), lo_of(a.y), lo_of(a.z), lo_of(a.w));
+            for (int v = t; v < (int)(A_TILE / 16); v += NTT) {
+                float4 a;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                             : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(lo_of(a.x)),
+                             "f"(lo_of(a.y)), "f"(lo_of(a.z)), "f"(lo_of(a.w)) : "memory");
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&lo_ready[s]);
@@ -289,25 +317,27 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 // ---------------------------------------------------------------- helpers
 // x (K × N fp64) → x_hi = rn_tf32(x), x_lo = rn_tf32(x − x_hi) (fp32, ld K).  x_hi = rn(x)
 // makes x_lo sign-symmetric, so the dropped a_lo·x_lo term carries no bias.
-__global__ void k_split_hilo(const double* __restrict__ x, int64_t K, int64_t N, int64_t ldx, float* __restrict__ hi,
+template <class T>
+__global__ void k_split_hilo(const T* __restrict__ x, int64_t K, int64_t N, int64_t ldx, float* __restrict__ hi,
                              float* __restrict__ lo) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= K * N) return;
     const int64_t i = e % K, j = e / K;
-    const double xd = x[i + j * ldx];
+    const double xd = (double)x[i + j * ldx];
     const float h = rn_tf32((float)xd);
     hi[e] = h;
     lo[e] = rn_tf32((float)(xd - (double)h));
 }
 
 __global__ void k_reduce_splits(int64_t M, int64_t N, int splits, const double* __restrict__ partial,
-                                double* __restrict__ out, int64_t ldo) {
+                                double* __restrict__ out, int64_t ldo, double alpha, double beta) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= M * N) return;
     const int64_t i = e % M, j = e / M;
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * M * N + e];
-    out[i + j * ldo] = s;
+    double* o = out + i + j * ldo;
+    *o = beta == 0.0 ? alpha * s : fma(beta, *o, alpha * s);
 }
 
 __global__ void k_sum_tiles(int64_t M, int tiles, const double* __restrict__ partial, double* __restrict__ out) {
@@ -341,24 +371,40 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
     return m;
 }
 
-template <bool A_MN, int EPI>
-void launch_umma(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M, int N,
-                 int k_tiles, int kps, double* out, int64_t ldo, double* partial) {
-    auto kern = k_umma<A_MN, EPI>;
+template <bool A_MN, int EPI, int NT>
+void launch_umma_nt(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
+                    int N, int k_tiles, int kps, double* out, int64_t ldo, double* partial, double alpha,
+                    double beta) {
+    auto kern = k_umma<A_MN, EPI, NT>;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NT>::SMEM_BYTES));
         attr = true;
     }
-    kern<<<grid, NTHREADS, SMEM_BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo, partial);
+    kern<<<grid, Cfg<NT>::NTHREADS, Cfg<NT>::SMEM_BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo,
+                                                                      partial, alpha, beta);
     LAUNCH_CHECK(c);
 }
 
-// x (K × N fp64, ldx) → hi/lo fp32 (K × N, ld K)
-void split_x(Ctx* c, const double* x, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
+template <bool A_MN, int EPI>
+void launch_umma(Ctx* c, int nt_per_cta, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th,
+                 const CUtensorMap& tl, int M, int N, int k_tiles, int kps, double* out, int64_t ldo, double* partial,
+                 double alpha, double beta) {
+    if (nt_per_cta == 2)
+        launch_umma_nt<A_MN, EPI, 2>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
+    else
+        launch_umma_nt<A_MN, EPI, 1>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
+}
+
+// x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
+void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
     *hi = DevBuf(c, (size_t)K * N * 4);
     *lo = DevBuf(c, (size_t)K * N * 4);
-    k_split_hilo<<<(unsigned)((K * N + 255) / 256), 256, 0, c->stream>>>(x, K, N, ldx, hi->as<float>(), lo->as<float>());
+    const unsigned g = (unsigned)((K * N + 255) / 256);
+    if (dtx == BCUR_F32)
+        k_split_hilo<float><<<g, 256, 0, c->stream>>>((const float*)x, K, N, ldx, hi->as<float>(), lo->as<float>());
+    else
+        k_split_hilo<double><<<g, 256, 0, c->stream>>>((const double*)x, K, N, ldx, hi->as<float>(), lo->as<float>());
     LAUNCH_CHECK(c);
 }
 
@@ -376,17 +422,18 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
            m < (1LL << 31);
 }
 
-// Out(n×N) = Aᵀ X  (A m×n fp32 col-major; X m×N fp64) → fp64 store, or per-row Σ² (rowsq != nullptr)
-void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
-              double* out, int64_t ldo, double* rowsq) {
+// Out(n×N) = alpha·Aᵀ X + beta·Out  (A m×n fp32 col-major; X m×N fp32/fp64) → fp64 store,
+// or rowsq[j] = Σ_c (AᵀX)_jc² (rowsq != nullptr; product never stored)
+void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
+              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq) {
     if (n <= 0 || N <= 0) {
         if (rowsq && n > 0) CUDA_CHECK(cudaMemsetAsync(rowsq, 0, n * sizeof(double), c->stream));
         return;
     }
     ProfScope prof(c, rowsq ? "umma_atx_rowsq" : "umma_atx_store", 2.0 * n * N * m,
-                   4.0 * m * n + 8.0 * m * N + (rowsq ? 8.0 * n : 8.0 * n * N));
+                   4.0 * m * n + (double)dtype_size(dtx) * m * N + (rowsq ? 8.0 * n : 8.0 * n * N));
     DevBuf xh, xl;
-    split_x(c, X, m, N, ldx, &xh, &xl);
+    split_x(c, X, dtx, m, N, ldx, &xh, &xl);
     const uint64_t dA[2] = {(uint64_t)m, (uint64_t)n}, sA[1] = {(uint64_t)lda * 4};
     const uint32_t bA[2] = {BK, BM};
     const uint64_t dX[2] = {(uint64_t)m, (uint64_t)N}, sX[1] = {(uint64_t)m * 4};
@@ -395,26 +442,28 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const d
     CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     const int k_tiles = (int)((m + BK - 1) / BK);
-    const int mt = (int)((n + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    const int NT = N > BN ? 2 : 1;
+    const int mt = (int)((n + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
     dim3 grid(nt, mt, 1);  // N tiles of one A row-tile run side by side and share it through L2
     if (rowsq) {
-        DevBuf part(c, (size_t)nt * n * sizeof(double));
-        launch_umma<false, EPI_ROWSQ>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0,
-                                      part.as<double>());
-        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt, part.as<double>(), rowsq);
+        DevBuf part(c, (size_t)nt * NT * n * sizeof(double));
+        launch_umma<false, EPI_ROWSQ>(c, NT, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0,
+                                      part.as<double>(), 1.0, 0.0);
+        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt * NT, part.as<double>(), rowsq);
         LAUNCH_CHECK(c);
     } else {
-        launch_umma<false, EPI_STORE>(c, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr);
+        launch_umma<false, EPI_STORE>(c, NT, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr,
+                                      alpha, beta);
     }
 }
 
-// Out(m×N) = A X  (A m×n fp32; X n×N fp64), split-K over n with fp64 partials
-void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
-             double* out, int64_t ldo) {
+// Out(m×N) = alpha·A X + beta·Out  (A m×n fp32; X n×N fp32/fp64), split-K over n with fp64 partials
+void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
+             int64_t ldx, double alpha, double beta, double* out, int64_t ldo) {
     if (m <= 0 || N <= 0) return;
-    ProfScope prof(c, "umma_ax", 2.0 * m * n * N, 4.0 * m * n + 8.0 * n * N + 8.0 * m * N);
+    ProfScope prof(c, "umma_ax", 2.0 * m * n * N, 4.0 * m * n + (double)dtype_size(dtx) * n * N + 8.0 * m * N);
     DevBuf xh, xl;
-    split_x(c, X, n, N, ldx, &xh, &xl);
+    split_x(c, X, dtx, n, N, ldx, &xh, &xl);
     // 3-D view of column-major A: (32 rows, n columns, m/32 row groups)
     const uint64_t dA[3] = {32, (uint64_t)n, (uint64_t)(m / 32)}, sA[2] = {(uint64_t)lda * 4, 128};
     const uint32_t bA[3] = {32, BK, BM / 32};
@@ -424,15 +473,23 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const do
     CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     const int k_tiles = (int)((n + BK - 1) / BK);
-    const int mt = (int)((m + BM - 1) / BM), nt = (int)((N + BN - 1) / BN);
+    const int NT = N > BN ? 2 : 1;
+    const int mt = (int)((m + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c->sm_count + mt * nt - 1) / (mt * nt),
                                                              k_tiles / 16));
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
-    DevBuf part(c, (size_t)splits * m * N * sizeof(double));
     dim3 grid(mt, nt, splits);
-    launch_umma<true, EPI_STORE>(c, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0, part.as<double>());
-    k_reduce_splits<<<(unsigned)((m * N + 255) / 256), 256, 0, c->stream>>>(m, N, splits, part.as<double>(), out, ldo);
+    if (splits == 1) {
+        launch_umma<true, EPI_STORE>(c, NT, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, out, ldo, nullptr,
+                                     alpha, beta);
+        return;
+    }
+    DevBuf part(c, (size_t)splits * m * N * sizeof(double));
+    launch_umma<true, EPI_STORE>(c, NT, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0,
+                                 part.as<double>(), 1.0, 0.0);
+    k_reduce_splits<<<(unsigned)((m * N + 255) / 256), 256, 0, c->stream>>>(m, N, splits, part.as<double>(), out, ldo,
+                                                                            alpha, beta);
     LAUNCH_CHECK(c);
 }
 

@@ -36,12 +36,12 @@ void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, con
 
 // ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
 bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
-// Out(n×N) = Aᵀ X (fp64 store, N ≤ 256) or rowsq[j] = Σ_c (AᵀX)_jc² (any N)
-void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
-              double* out, int64_t ldo, double* rowsq);
-// Out(m×N) = A X (N ≤ 256)
-void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const double* X, int64_t N, int64_t ldx,
-             double* out, int64_t ldo);
+// Out(n×N) = alpha·Aᵀ X + beta·Out (fp64) or rowsq[j] = Σ_c (AᵀX)_jc²; X fp32 or fp64
+void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
+              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq);
+// Out(m×N) = alpha·A X + beta·Out (fp64); X fp32 or fp64
+void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
+             int64_t ldx, double alpha, double beta, double* out, int64_t ldo);
 
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
 // R upper with G = RᵀR; info[0] = 0 ok / j+1 failed pivot;
@@ -53,6 +53,9 @@ void tri_inv_upper(Ctx* c, const double* r, int64_t w, double* x);
 void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, double* v);
 
 // ---- elementwise / layout (kernels_misc.cu) -------------------------------
+void convert(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd);
+void transpose(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd);
+void zero_lower(Ctx* c, double* x, int64_t w, int64_t ld);
 void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
 void fill_f64(Ctx* c, double* p, int64_t count, double v);
 void axpy_neg(Ctx* c, const double* x, double* y, int64_t n);  // y -= x

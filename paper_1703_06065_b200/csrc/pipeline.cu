@@ -9,7 +9,9 @@
 // The numerical definitions (thresholds, orthonormalisation paths, residual
 // rule) are shared with the oracle (oracle/bcur_oracle.py) and documented in
 // DESIGN.md §Numerics.  Every floating-point operation runs on the device; the
-// host only moves O(G)-sized decision data (draws, argmax, ranks).
+// host only moves O(G)-sized decision data (draws, argmax, ranks, pivots).
+// For fp32 inputs the factor bases are kept in fp32 so that every product with
+// A or with a basis runs on the tcgen05 3×TF32 kernels (kernels_umma.cu).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -88,28 +90,102 @@ static void gather_blocks_vec(Ctx* c, const Shard& s, const double* d_local, dou
     allreduce(c, d_global, s.G);
 }
 
+// ------------------------------------------------- factorizations of any size
+struct CholInfo {
+    int info;
+    double mindiag, maxdiag;
+};
+
+static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X);
+
+// G (w×w SPD, fp64) → R upper (w×w, ld w) with G = RᵀR.  Single CTA up to 256,
+// blocked right-looking (128-wide diagonal blocks + fp64 product updates) beyond.
+static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R) {
+    DevBuf st(c, 64);
+    struct { int info; int pad; double mindiag, maxdiag; } hs;
+    if (w <= 256) {
+        cholesky_upper(c, G, w, ldg, R, st.as<int>(), st.as<double>() + 1);
+        d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
+        return {hs.info, hs.mindiag, hs.maxdiag};
+    }
+    constexpr int64_t B = 128;
+    copy_f64(c, G, w, w, ldg, R, w);
+    CholInfo out{0, INFINITY, 0.0};
+    {
+        std::vector<double> diag(w);
+        CUDA_CHECK(cudaMemcpy2DAsync(diag.data(), sizeof(double), G, (ldg + 1) * sizeof(double), sizeof(double), w,
+                                     cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        for (double d : diag) out.maxdiag = std::max(out.maxdiag, d);
+    }
+    Mat64 Rkk(c, B, B), Rinv(c, B, B), T1(c, B, w);
+    for (int64_t k = 0; k < w; k += B) {
+        const int64_t kb = std::min(B, w - k), rest = w - k - kb;
+        double* Dk = R + k + k * w;
+        cholesky_upper(c, Dk, kb, w, Rkk.p(), st.as<int>(), st.as<double>() + 1);
+        d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
+        if (hs.info != 0) {
+            out.info = (int)k + hs.info;
+            out.mindiag = 0.0;
+            return out;
+        }
+        out.mindiag = std::min(out.mindiag, hs.mindiag);
+        copy_f64(c, Rkk.p(), kb, kb, kb, Dk, w);  // Rkk / Rinv are packed kb×kb (ld kb)
+        if (rest > 0) {
+            tri_inv_any(c, Rkk.p(), kb, Rinv.p());
+            double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
+            gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Rinv.p(), BCUR_F64, kb, Pk, BCUR_F64, w, 0.0, T1.p(), B);
+            copy_f64(c, T1.p(), kb, rest, B, Pk, w);
+            double* Tr = R + (k + kb) + (k + kb) * w;
+            gemm(c, OP_T, OP_N, rest, rest, kb, -1.0, T1.p(), BCUR_F64, B, T1.p(), BCUR_F64, B, 1.0, Tr, w);
+        }
+    }
+    zero_lower(c, R, w, w);
+    return out;
+}
+
+// X = R⁻¹ for upper-triangular R (w×w, ld w).  Blocked back-substitution by block rows.
+static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X) {
+    constexpr int64_t B = 64;  // single-CTA shared-memory inverse of ≤64-wide diagonal blocks
+    if (w <= B) {
+        tri_inv_upper(c, R, w, X);
+        return;
+    }
+    fill_f64(c, X, w * w, 0.0);
+    Mat64 Rii(c, B, B), Ri(c, B, B), T(c, B, w);
+    const int64_t nb = (w + B - 1) / B;
+    for (int64_t bi = nb - 1; bi >= 0; --bi) {
+        const int64_t r0 = bi * B, rb = std::min(B, w - r0), c0 = r0 + rb, rest = w - c0;
+        copy_f64(c, R + r0 + r0 * w, rb, rb, w, Rii.p(), rb);  // packed rb×rb (ld rb)
+        tri_inv_upper(c, Rii.p(), rb, Ri.p());
+        copy_f64(c, Ri.p(), rb, rb, rb, X + r0 + r0 * w, w);
+        if (rest > 0) {
+            // X[r0, c0:] = −Rii⁻¹ · (R[r0, c0:] · X[c0:, c0:])
+            gemm(c, OP_N, OP_N, rb, rest, rest, 1.0, R + r0 + c0 * w, BCUR_F64, w, X + c0 + c0 * w, BCUR_F64, w, 0.0,
+                 T.p(), B);
+            gemm(c, OP_N, OP_N, rb, rest, rb, -1.0, Ri.p(), BCUR_F64, rb, T.p(), BCUR_F64, B, 0.0, X + r0 + c0 * w,
+                 w);
+        }
+    }
+}
+
 // ------------------------------------------------------------------ orth
-// X (rows × w, fp64) → Q (rows × r) with X ≈ Q·T.  Grams allreduced when dist.
+// X (rows × w, fp64) → Q (rows × r, fp64) with X ≈ Q·T.  Grams allreduced when dist.
 // ref < 0 → ref = max column norm of X.  Mirrors oracle.orth.
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
              int64_t ldq, bool dist, Mat64* T_out, int* path_out) {
     if (w == 0) return 0;
     Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w);
-    DevBuf st(c, 64);
-    int* d_info = st.as<int>();
-    double* d_diag = st.as<double>() + 1;
     gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld);
     if (dist) allreduce(c, G.p(), w * w);
-    cholesky_upper(c, G.p(), w, G.ld, R.p(), d_info, d_diag);
-    struct { int info; int pad; double mindiag, maxdiag; } hs;
-    d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
-    if (ref < 0) ref = std::sqrt(std::max(hs.maxdiag, 0.0));
+    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p());
+    if (ref < 0) ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     int64_t r = w;
-    const bool chol_ok = hs.info == 0 && std::isfinite(hs.mindiag) && hs.mindiag > tau_chol(dt) * ref;
+    const bool chol_ok = ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref;
     Mat64 Wr, sig;
     std::vector<double> sig_h;
     if (chol_ok) {
-        tri_inv_upper(c, R.p(), w, Ri.p());
+        tri_inv_any(c, R.p(), w, Ri.p());
         gemm(c, OP_N, OP_N, rows, w, w, 1.0, X, BCUR_F64, ldx, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
     } else {
         Mat64 lam(c, w, 1), V(c, w, w);
@@ -147,17 +223,15 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
     gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
     if (dist) allreduce(c, G2.p(), r * r);
-    cholesky_upper(c, G2.p(), r, G2.ld, R2.p(), d_info, d_diag);
-    d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
-    if (hs.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
-    tri_inv_upper(c, R2.p(), r, R2i.p());
+    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p());
+    if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
+    tri_inv_any(c, R2.p(), r, R2i.p());
     gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
     if (T_out) {
         Mat64 T(c, r, w);
         if (chol_ok) {
             gemm(c, OP_N, OP_N, r, w, r, 1.0, R2.p(), BCUR_F64, R2.ld, R.p(), BCUR_F64, R.ld, 0.0, T.p(), T.ld);
         } else {
-            // T = R2·diag(σ)·Wrᵀ
             Mat64 R2s(c, r, r);
             copy_f64(c, R2.p(), r, r, R2.ld, R2s.p(), R2s.ld);
             scale_columns(c, R2s.p(), r, r, R2s.ld, sig.p());
@@ -169,19 +243,72 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     return r;
 }
 
-// Block CGS2 of panel P (rows × w) against Q (rows × cur); P is overwritten.
-// New orthonormal columns are written at Q(:, cur..cur+r).  Returns r.
-int64_t cgs2_append(Ctx* c, double* Qbase, int64_t ldq, int64_t rows, int64_t cur, double* P, int64_t w, int64_t ldp,
-                    double ref, int dt, bool dist) {
+// ----------------------------------------------------------------- bases
+// Orthonormal basis kept in fp32 (fp32 inputs: every product with it runs on the
+// tensor cores) or fp64 (fp64 inputs).
+struct Basis {
+    DevBuf buf;
+    int dt = BCUR_F64;
+    int64_t rows = 0, cap = 0, rank = 0;
+    void init(Ctx* c, int dt_, int64_t rows_, int64_t cap_) {
+        dt = dt_;
+        rows = rows_;
+        cap = std::max<int64_t>(cap_, 1);
+        rank = 0;
+        buf = DevBuf(c, (size_t)std::max<int64_t>(rows, 1) * cap * dtype_size(dt));
+        CUDA_CHECK(cudaMemsetAsync(buf.ptr, 0, buf.bytes, c->stream));
+    }
+    void* col(int64_t j) const { return (char*)buf.ptr + (size_t)j * rows * dtype_size(dt); }
+};
+
+// Block CGS2 of panel P (rows × w, fp64, overwritten) against the basis; the new
+// orthonormal columns are appended to it.  Returns the rank added.
+static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, double ref, int dt, bool dist) {
+    const int64_t rows = B->rows, cur = B->rank;
     if (cur > 0) {
         Mat64 X(c, cur, w);
         for (int pass = 0; pass < 2; ++pass) {
-            gemm(c, OP_T, OP_N, cur, w, rows, 1.0, Qbase, BCUR_F64, ldq, P, BCUR_F64, ldp, 0.0, X.p(), X.ld);
+            gemm(c, OP_T, OP_N, cur, w, rows, 1.0, B->buf.ptr, B->dt, rows, P, BCUR_F64, ldp, 0.0, X.p(), X.ld);
             if (dist) allreduce(c, X.p(), cur * w);
-            gemm(c, OP_N, OP_N, rows, w, cur, -1.0, Qbase, BCUR_F64, ldq, X.p(), BCUR_F64, X.ld, 1.0, P, ldp);
+            gemm(c, OP_N, OP_N, rows, w, cur, -1.0, B->buf.ptr, B->dt, rows, X.p(), BCUR_F64, X.ld, 1.0, P, ldp);
         }
     }
-    return orth(c, P, rows, w, ldp, ref, dt, Qbase + cur * ldq, ldq, dist, nullptr, nullptr);
+    int64_t r;
+    if (B->dt == BCUR_F64) {
+        r = orth(c, P, rows, w, ldp, ref, dt, (double*)B->col(cur), rows, dist, nullptr, nullptr);
+    } else {
+        Mat64 Qn(c, rows, w);
+        r = orth(c, P, rows, w, ldp, ref, dt, Qn.p(), Qn.ld, dist, nullptr, nullptr);
+        convert(c, Qn.p(), BCUR_F64, rows, r, Qn.ld, B->col(cur), B->dt, rows);
+    }
+    B->rank += r;
+    return r;
+}
+
+// Whole-matrix CholQR2 of an fp32 C (rows × cc) on the tensor cores, written to B.
+// Returns false (B untouched) when C is not safely full rank (oracle.cholqr2_whole).
+static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
+    if (cc == 0 || rows < cc) return false;
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc);
+    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, BCUR_F32, rows, C, BCUR_F32, rows, 0.0, G.p(), G.ld);
+    if (dist) allreduce(c, G.p(), cc * cc);
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p());
+    const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
+    if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
+    tri_inv_any(c, R.p(), cc, Ri.p());
+    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
+    DevBuf q1f(c, (size_t)rows * cc * 4);
+    convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, q1f.ptr, BCUR_F32, rows);
+    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, q1f.ptr, BCUR_F32, rows, q1f.ptr, BCUR_F32, rows, 0.0, G.p(), G.ld);
+    if (dist) allreduce(c, G.p(), cc * cc);
+    const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p());
+    if (c2.info != 0) return false;
+    tri_inv_any(c, R.p(), cc, Ri.p());
+    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1f.ptr, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
+    B->init(c, BCUR_F32, rows, cc);
+    convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
+    B->rank = cc;
+    return true;
 }
 
 // ---------------------------------------------------------- range finder
@@ -246,44 +373,66 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
     out->sigma.assign(sg.begin(), sg.begin() + rank);
 }
 
-// ------------------------------------------------------------- block CSS
-struct Basis {
-    Mat64 q;         // rows × capacity
-    int64_t rank = 0;
-};
+// ------------------------------------------------------------- helpers
+static std::vector<int64_t> unique_in_order(const std::vector<int64_t>& v) {
+    std::vector<int64_t> out;
+    for (int64_t b : v)
+        if (std::find(out.begin(), out.end(), b) == out.end()) out.push_back(b);
+    return out;
+}
 
-// Build the orthonormal basis of the selected (unique, in order) column blocks of A.
+// Replicate column block b of A (owned by one rank) as an fp64 rows × w panel.
+static void block_panel(Ctx* c, const DMat* a, const Shard& s, int64_t b, double* P) {
+    const int64_t w = s.off_global[b + 1] - s.off_global[b];
+    if (b >= s.g0 && b < s.g1) {
+        const size_t es = dtype_size(a->dtype);
+        convert_to_f64(c, (const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * es, a->dtype, a->m, w,
+                       a->ld, P, a->m);
+    } else {
+        fill_f64(c, P, a->m * w, 0.0);
+    }
+    allreduce(c, P, a->m * w);  // broadcast from the owner
+}
+
+// Orthonormal basis of the selected (unique, in order) column blocks of A:
+// whole-C CholQR2 on the tensor cores for fp32 when safely full rank, else block
+// CGS2 panels with per-panel rank revealing (oracle.column_basis).
 static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vector<int64_t>& blocks,
-                         const std::vector<double>& bn2, Basis* out) {
+                         const std::vector<double>& bn2, Basis* B) {
     const int64_t m = a->m;
     int64_t cap = 0;
     for (int64_t b : blocks) cap += s.off_global[b + 1] - s.off_global[b];
-    out->q = Mat64(c, m, std::max<int64_t>(cap, 1));
-    out->rank = 0;
+    if (a->dtype == BCUR_F32 && cap > 0) {
+        DevBuf cf(c, (size_t)m * cap * 4);
+        int64_t at = 0;
+        for (int64_t b : blocks) {
+            const int64_t w = s.off_global[b + 1] - s.off_global[b];
+            if (c->comm.world <= 1) {
+                convert(c, (const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * 4, BCUR_F32, m, w, a->ld,
+                        (float*)cf.ptr + at * m, BCUR_F32, m);
+            } else {
+                Mat64 P(c, m, w);
+                block_panel(c, a, s, b, P.p());
+                convert(c, P.p(), BCUR_F64, m, w, m, (float*)cf.ptr + at * m, BCUR_F32, m);
+            }
+            at += w;
+        }
+        if (cholqr2_whole(c, cf.as<float>(), m, cap, false, a->dtype, B)) return;
+    }
+    B->init(c, a->dtype == BCUR_F32 ? BCUR_F32 : BCUR_F64, m, cap);
     for (int64_t b : blocks) {
         const int64_t w = s.off_global[b + 1] - s.off_global[b];
         Mat64 P(c, m, w);
-        const bool mine = b >= s.g0 && b < s.g1;
-        if (mine) {
-            const int64_t lc = s.off_global[b] - s.col0;
-            const size_t es = dtype_size(a->dtype);
-            convert_to_f64(c, (const char*)a->ptr + (size_t)lc * a->ld * es, a->dtype, m, w, a->ld, P.p(), P.ld);
-        } else {
-            fill_f64(c, P.p(), m * w, 0.0);
-        }
-        allreduce(c, P.p(), m * w);  // broadcast from the owner
-        const double ref = std::sqrt(std::max(bn2[b], 0.0));
-        const int64_t r = cgs2_append(c, out->q.p(), out->q.ld, m, out->rank, P.p(), w, P.ld, ref, a->dtype, false);
-        out->rank += r;
+        block_panel(c, a, s, b, P.p());
+        cgs2_append(c, B, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)), a->dtype, false);
     }
 }
 
-// res2 = ‖A‖² − Σ_g ‖Qᵀ A_g‖²  (shard-local per-block values in d_blk, allreduced total)
-static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const double* Q, int64_t ldq, int64_t r,
-                             double* d_blk_local) {
+// Σ_g ‖Qᵀ A_g‖² (shard-local per-block values in d_blk_local, allreduced total)
+static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local) {
     const int64_t nl = a->n;
     Mat64 rows(c, nl, 1), tot(c, 1, 1);
-    gemm_rowsumsq(c, OP_T, OP_N, nl, r, a->m, a->ptr, a->dtype, a->ld, Q, BCUR_F64, ldq, rows.p());
+    gemm_rowsumsq(c, OP_T, OP_N, nl, B.rank, a->m, a->ptr, a->dtype, a->ld, B.buf.ptr, B.dt, B.rows, rows.p());
     Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     double* b = d_blk_local ? d_blk_local : blk.p();
     segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
@@ -294,21 +443,17 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const double
     return h;
 }
 
-static double explicit_residual(Ctx* c, const DMat* a, const double* Q, int64_t ldq, int64_t r) {
-    const int64_t m = a->m, nl = a->n;
+// ‖A − Q Qᵀ A‖² (streamed: X = QᵀA, then Σ (A − Q X)² tile by tile)
+static double explicit_residual(Ctx* c, const DMat* a, const Basis& B) {
+    const int64_t m = a->m, nl = a->n, r = B.rank;
     Mat64 tot(c, 1, 1);
-    if (r == 0) {
-        // ‖A‖² of the shard
-        Mat64 one(c, 1, 1);
-        fill_f64(c, one.p(), 1, 0.0);
-        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, 1, one.p(), BCUR_F64, m, one.p(), BCUR_F64, 1, a->ptr, a->dtype, a->ld,
-                         tot.p());
-    } else {
-        Mat64 X(c, r, nl);
-        gemm(c, OP_T, OP_N, r, nl, m, 1.0, Q, BCUR_F64, ldq, a->ptr, a->dtype, a->ld, 0.0, X.p(), X.ld);
-        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, r, Q, BCUR_F64, ldq, X.p(), BCUR_F64, X.ld, a->ptr, a->dtype, a->ld,
-                         tot.p());
-    }
+    Mat64 X(c, std::max<int64_t>(r, 1), nl);
+    if (r > 0)
+        gemm(c, OP_T, OP_N, r, nl, m, 1.0, B.buf.ptr, B.dt, B.rows, a->ptr, a->dtype, a->ld, 0.0, X.p(), X.ld);
+    else
+        fill_f64(c, X.p(), nl, 0.0);
+    gemm_resid_sumsq(c, OP_N, OP_N, m, nl, std::max<int64_t>(r, 1), B.buf.ptr, B.dt, B.rows, X.p(), BCUR_F64, X.ld,
+                     a->ptr, a->dtype, a->ld, tot.p());
     allreduce(c, tot.p(), 1);
     double h = 0.0;
     d2h(c, &h, tot.p(), 1);
@@ -328,13 +473,6 @@ static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<dou
     double h = 0.0;
     d2h(c, &h, tot.p(), 1);
     return h;
-}
-
-static std::vector<int64_t> unique_in_order(const std::vector<int64_t>& v) {
-    std::vector<int64_t> out;
-    for (int64_t b : v)
-        if (std::find(out.begin(), out.end(), b) == out.end()) out.push_back(b);
-    return out;
 }
 
 // scores (global G, device) from the shard-local rows of V
@@ -363,6 +501,7 @@ static void draw_on_device(Ctx* c, const double* d_scores, int64_t G, int64_t g,
     d2h(c, margins->data(), dm.p(), g);
 }
 
+// ------------------------------------------------------------- block CSS
 void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, const double* uniforms,
                CssOut* out) {
     if (o.k < 1) fail(BCUR_E_INVALID_ARGUMENT, "block_css: k must be >= 1");
@@ -384,10 +523,10 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     for (auto& d : out->draws) blocks.push_back(d.block);
     Basis B;
     column_basis(c, a, s, unique_in_order(blocks), bn2, &B);
-    double res2 = a2 - projected_mass(c, a, s, B.q.p(), B.q.ld, B.rank, nullptr);
+    double res2 = a2 - projected_mass(c, a, s, B, nullptr);
     int path = 0;
     if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(a->dtype) * a2)) {
-        res2 = explicit_residual(c, a, B.q.p(), B.q.ld, B.rank);
+        res2 = explicit_residual(c, a, B);
         path = 1;
     }
     out->rep = bcur_report{};
@@ -418,7 +557,7 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
         for (int64_t t = 0; t < o.g; ++t) cap += w[t];
     }
     Basis B;
-    B.q = Mat64(c, m, std::max<int64_t>(cap, 1));
+    B.init(c, dt == BCUR_F32 ? BCUR_F32 : BCUR_F64, m, cap);
     DevBuf sel(c, (size_t)G);
     CUDA_CHECK(cudaMemsetAsync(sel.ptr, 0, G, c->stream));
     DevBuf didx(c, 64);
@@ -454,28 +593,18 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
         const int64_t b = st.block;
         const unsigned char one = 1;
         h2d(c, sel.as<unsigned char>() + b, &one, 1);
-        // panel = block b (broadcast from its owner)
         const int64_t w = offsets[b + 1] - offsets[b];
         Mat64 P(c, m, w);
-        if (b >= s.g0 && b < s.g1) {
-            const size_t es = dtype_size(dt);
-            convert_to_f64(c, (const char*)a->ptr + (size_t)(offsets[b] - s.col0) * a->ld * es, dt, m, w, a->ld,
-                           P.p(), P.ld);
-        } else {
-            fill_f64(c, P.p(), m * w, 0.0);
-        }
-        allreduce(c, P.p(), m * w);
-        const int64_t r = cgs2_append(c, B.q.p(), B.q.ld, m, B.rank, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)),
-                                      dt, false);
+        block_panel(c, a, s, b, P.p());
+        const int64_t cur = B.rank;
+        const int64_t r = cgs2_append(c, &B, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)), dt, false);
         if (r > 0) {
             // res_g −= ‖Q_newᵀ A_g‖²
-            gemm_rowsumsq(c, OP_T, OP_N, a->n, r, m, a->ptr, dt, a->ld, B.q.p() + B.rank * B.q.ld, BCUR_F64, B.q.ld,
-                          rows.p());
+            gemm_rowsumsq(c, OP_T, OP_N, a->n, r, m, a->ptr, dt, a->ld, B.col(cur), B.dt, B.rows, rows.p());
             segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
             gather_blocks_vec(c, s, loc.p(), upd.p());
             axpy_neg(c, upd.p(), res.p(), G);
         }
-        B.rank += r;
         st.rank_added = r;
         out->steps.push_back(st);
     }
@@ -487,7 +616,7 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     d2h(c, &res2, tot.p(), 1);
     int path = 0;
     if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(dt) * a2)) {
-        res2 = explicit_residual(c, a, B.q.p(), B.q.ld, B.rank);
+        res2 = explicit_residual(c, a, B);
         path = 1;
     }
     out->rep = bcur_report{};
@@ -503,6 +632,8 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
                const bcur_options& o, const double* uniforms, bool want_u, CurOut* out) {
     const int64_t m = a->m, nl = a->n;
     const int dt = a->dtype;
+    const int bdt = dt == BCUR_F32 ? BCUR_F32 : BCUR_F64;
+    const bool dist = c->comm.world > 1;
     if (o.g < 1 || o.g_rows < 1) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: g and g_rows must be >= 1");
     if (Gr < 1 || roff[0] != 0 || roff[Gr] != m) fail(BCUR_E_DIMENSION_MISMATCH, "block_cur: row partition does not match A");
     Shard s = shard_of(a, coff, Gc);
@@ -532,38 +663,61 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     // Q_C (m × rc), replicated
     Basis QC;
     column_basis(c, a, s, cb, bn2, &QC);
-    // Q_R (n × rr): basis of the selected row blocks of A, i.e. column blocks of Aᵀ (row-distributed over ranks)
+    // Q_R (n_local × rr): basis of the selected row blocks of A (column blocks of Aᵀ),
+    // row-distributed over ranks.  Rᵀ_u = unscaled selected rows, transposed.
+    int64_t ru = 0;
+    std::vector<int64_t> dst_u;
+    for (int64_t h : rb) { dst_u.push_back(ru); ru += roff[h + 1] - roff[h]; }
+    DevBuf rtu(c, (size_t)nl * std::max<int64_t>(ru, 1) * dtype_size(bdt));
+    {
+        std::vector<bcur_block_draw> dr;
+        for (int64_t h : rb) dr.push_back({h, 0.0, 1.0});
+        DevBuf dd(c, dr.size() * sizeof(bcur_block_draw)), dds(c, dst_u.size() * sizeof(int64_t));
+        h2d(c, dd.as<bcur_block_draw>(), dr.data(), dr.size());
+        h2d(c, dds.as<int64_t>(), dst_u.data(), dst_u.size());
+        DevBuf rr_(c, (size_t)std::max<int64_t>(ru, 1) * nl * dtype_size(bdt));
+        gather_blocks(c, a->ptr, dt, m, nl, a->ld, droff.as<int64_t>(), dd.as<bcur_block_draw>(), dds.as<int64_t>(),
+                      (int64_t)dr.size(), 1, 0, rr_.ptr, bdt, ru);
+        transpose(c, rr_.ptr, bdt, ru, nl, ru, rtu.ptr, bdt, nl);
+    }
     std::vector<double> rbn2(Gr, 0.0);
     {
-        // ‖A_{h,:}‖² per row block = per-column-block sums of Aᵀ (n_local × m), allreduced
-        Mat64 tmp(c, Gr, 1);
-        Mat64 at(c, nl, m);
-        transpose_to_f64(c, a->ptr, dt, m, nl, a->ld, at.p(), at.ld);
-        block_sumsq(c, at.p(), BCUR_F64, nl, at.ld, droff.as<int64_t>(), Gr, tmp.p());
-        allreduce(c, tmp.p(), Gr);
-        d2h(c, rbn2.data(), tmp.p(), Gr);
-        int64_t cap = 0;
-        for (int64_t h : rb) cap += roff[h + 1] - roff[h];
-        out->qr = Mat64(c, nl, std::max<int64_t>(cap, 1));
-        out->rank_r = 0;
-        for (int64_t h : rb) {
-            const int64_t w = roff[h + 1] - roff[h];
-            Mat64 P(c, nl, w);  // rows [roff[h], roff[h+1]) of A, transposed: nl × w
-            copy_f64(c, at.p() + roff[h] * at.ld, nl, w, at.ld, P.p(), P.ld);
-            const int64_t r = cgs2_append(c, out->qr.p(), out->qr.ld, nl, out->rank_r, P.p(), w, P.ld,
-                                          std::sqrt(std::max(rbn2[h], 0.0)), dt, true);
-            out->rank_r += r;
+        // ‖A_h‖² for the selected row blocks, from the columns of Rᵀ_u (allreduced over shards)
+        std::vector<int64_t> lo(dst_u);
+        lo.push_back(ru);
+        DevBuf dlo(c, lo.size() * sizeof(int64_t));
+        h2d(c, dlo.as<int64_t>(), lo.data(), lo.size());
+        Mat64 t(c, std::max<int64_t>((int64_t)rb.size(), 1), 1);
+        block_sumsq(c, rtu.ptr, bdt, nl, nl, dlo.as<int64_t>(), (int64_t)rb.size(), t.p());
+        allreduce(c, t.p(), (int64_t)rb.size());
+        std::vector<double> th(rb.size());
+        d2h(c, th.data(), t.p(), rb.size());
+        for (size_t i = 0; i < rb.size(); ++i) rbn2[rb[i]] = th[i];
+    }
+    Basis QR;
+    bool whole = false;
+    if (bdt == BCUR_F32 && ru > 0) whole = cholqr2_whole(c, rtu.as<float>(), nl, ru, dist, dt, &QR);
+    if (!whole) {
+        QR.init(c, bdt, nl, ru);
+        for (size_t i = 0; i < rb.size(); ++i) {
+            const int64_t h = rb[i], w = roff[h + 1] - roff[h];
+            Mat64 P(c, nl, w);
+            convert(c, (const char*)rtu.ptr + (size_t)dst_u[i] * nl * dtype_size(bdt), bdt, nl, w, nl, P.p(),
+                    BCUR_F64, P.ld);
+            cgs2_append(c, &QR, P.p(), w, P.ld, std::sqrt(std::max(rbn2[h], 0.0)), dt, dist);
         }
     }
-    const int64_t rc = QC.rank, rr = out->rank_r;
-    // M = Q_Cᵀ A Q_R = Σ_s (Q_Cᵀ A_s) Q_R,s
-    Mat64 X(c, std::max<int64_t>(rc, 1), nl), M(c, std::max<int64_t>(rc, 1), std::max<int64_t>(rr, 1));
-    gemm(c, OP_T, OP_N, rc, nl, m, 1.0, QC.q.p(), BCUR_F64, QC.q.ld, a->ptr, dt, a->ld, 0.0, X.p(), X.ld);
-    gemm(c, OP_N, OP_N, rc, rr, nl, 1.0, X.p(), BCUR_F64, X.ld, out->qr.p(), BCUR_F64, out->qr.ld, 0.0, M.p(), M.ld);
-    allreduce(c, M.p(), rc * rr);
+    out->rank_r = QR.rank;
+    const int64_t rc = QC.rank, rr = QR.rank;
+    // M = Q_Cᵀ A Q_R:  Xᵀ = A_sᵀ Q_C (n_local × rc), Mᵀ = Σ_s Q_R,sᵀ Xᵀ (rr × rc)
+    Mat64 Xt(c, nl, std::max<int64_t>(rc, 1)), Mt(c, std::max<int64_t>(rr, 1), std::max<int64_t>(rc, 1));
+    Mat64 M(c, std::max<int64_t>(rc, 1), std::max<int64_t>(rr, 1));
+    gemm(c, OP_T, OP_N, nl, rc, m, 1.0, a->ptr, dt, a->ld, QC.buf.ptr, QC.dt, QC.rows, 0.0, Xt.p(), Xt.ld);
+    gemm(c, OP_T, OP_N, rr, rc, nl, 1.0, QR.buf.ptr, QR.dt, QR.rows, Xt.p(), BCUR_F64, Xt.ld, 0.0, Mt.p(), Mt.ld);
+    allreduce(c, Mt.p(), rr * rc);
+    transpose(c, Mt.p(), BCUR_F64, rr, rc, Mt.ld, M.p(), BCUR_F64, M.ld);
     Mat64 tot(c, 1, 1);
     {
-        // ‖M‖²
         Mat64 rows2(c, std::max<int64_t>(rc, 1), 1);
         row_sumsq_blocks(c, M.p(), BCUR_F64, rc, rr, M.ld, nullptr, 0, rows2.p(), nullptr);
         sum_vector(c, rows2.p(), rc, tot.p());
@@ -575,8 +729,10 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(dt) * a2)) {
         // Σ (A_s − Q_C (M Q_R,sᵀ))²
         Mat64 Bm(c, std::max<int64_t>(rc, 1), nl);
-        gemm(c, OP_N, OP_T, rc, nl, rr, 1.0, M.p(), BCUR_F64, M.ld, out->qr.p(), BCUR_F64, out->qr.ld, 0.0, Bm.p(), Bm.ld);
-        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, rc, QC.q.p(), BCUR_F64, QC.q.ld, Bm.p(), BCUR_F64, Bm.ld, a->ptr, dt,
+        Mat64 qr64(c, nl, std::max<int64_t>(rr, 1));
+        convert(c, QR.buf.ptr, QR.dt, nl, rr, nl, qr64.p(), BCUR_F64, qr64.ld);
+        gemm(c, OP_N, OP_T, rc, nl, rr, 1.0, M.p(), BCUR_F64, M.ld, qr64.p(), BCUR_F64, qr64.ld, 0.0, Bm.p(), Bm.ld);
+        gemm_resid_sumsq(c, OP_N, OP_N, m, nl, rc, QC.buf.ptr, QC.dt, QC.rows, Bm.p(), BCUR_F64, Bm.ld, a->ptr, dt,
                          a->ld, tot.p());
         allreduce(c, tot.p(), 1);
         d2h(c, &res2, tot.p(), 1);
@@ -589,10 +745,10 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         std::vector<int64_t> dco, dro;
         for (auto& d : out->col_draws) { dco.push_back(cc); cc += coff[d.block + 1] - coff[d.block]; }
         for (auto& d : out->row_draws) { dro.push_back(cr); cr += roff[d.block + 1] - roff[d.block]; }
-        Mat64 Cm(c, m, cc), Rt(c, nl, cr);
-        // columns: gather from each owner and broadcast via allreduce (zero elsewhere)
-        fill_f64(c, Cm.p(), m * cc, 0.0);
+        DevBuf Cm(c, (size_t)m * cc * dtype_size(bdt)), Rt(c, (size_t)nl * cr * dtype_size(bdt));
         {
+            Mat64 C64(c, m, cc);
+            fill_f64(c, C64.p(), m * cc, 0.0);
             std::vector<bcur_block_draw> mine;
             std::vector<int64_t> dst;
             for (size_t t = 0; t < out->col_draws.size(); ++t) {
@@ -609,35 +765,32 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
                 h2d(c, dd.as<bcur_block_draw>(), mine.data(), mine.size());
                 h2d(c, ddst.as<int64_t>(), dst.data(), dst.size());
                 gather_blocks(c, a->ptr, dt, m, nl, a->ld, s.d_local.as<int64_t>(), dd.as<bcur_block_draw>(),
-                              ddst.as<int64_t>(), (int64_t)mine.size(), 0, 1, Cm.p(), BCUR_F64, Cm.ld);
+                              ddst.as<int64_t>(), (int64_t)mine.size(), 0, 1, C64.p(), BCUR_F64, C64.ld);
             }
-            allreduce(c, Cm.p(), m * cc);
+            allreduce(c, C64.p(), m * cc);
+            convert(c, C64.p(), BCUR_F64, m, cc, C64.ld, Cm.ptr, bdt, m);
         }
         {
             DevBuf dd(c, out->row_draws.size() * sizeof(bcur_block_draw)), ddst(c, dro.size() * sizeof(int64_t));
             h2d(c, dd.as<bcur_block_draw>(), out->row_draws.data(), out->row_draws.size());
             h2d(c, ddst.as<int64_t>(), dro.data(), dro.size());
-            // R (cr × nl) = scaled row blocks; Rᵀ = its transpose
-            Mat64 Rm(c, cr, nl);
+            DevBuf Rm(c, (size_t)cr * nl * dtype_size(bdt));
             gather_blocks(c, a->ptr, dt, m, nl, a->ld, droff.as<int64_t>(), dd.as<bcur_block_draw>(), ddst.as<int64_t>(),
-                          (int64_t)out->row_draws.size(), 1, 1, Rm.p(), BCUR_F64, Rm.ld);
-            transpose_to_f64(c, Rm.p(), BCUR_F64, cr, nl, Rm.ld, Rt.p(), Rt.ld);
+                          (int64_t)out->row_draws.size(), 1, 1, Rm.ptr, bdt, cr);
+            transpose(c, Rm.ptr, bdt, cr, nl, cr, Rt.ptr, bdt, nl);
         }
         // T_C = Q_Cᵀ C (rc × cc), T_R = Q_Rᵀ Rᵀ (rr × cr)
         Mat64 TC(c, rc, cc), TR(c, rr, cr);
-        gemm(c, OP_T, OP_N, rc, cc, m, 1.0, QC.q.p(), BCUR_F64, QC.q.ld, Cm.p(), BCUR_F64, Cm.ld, 0.0, TC.p(), TC.ld);
-        gemm(c, OP_T, OP_N, rr, cr, nl, 1.0, out->qr.p(), BCUR_F64, out->qr.ld, Rt.p(), BCUR_F64, Rt.ld, 0.0, TR.p(), TR.ld);
+        gemm(c, OP_T, OP_N, rc, cc, m, 1.0, QC.buf.ptr, QC.dt, QC.rows, Cm.ptr, bdt, m, 0.0, TC.p(), TC.ld);
+        gemm(c, OP_T, OP_N, rr, cr, nl, 1.0, QR.buf.ptr, QR.dt, QR.rows, Rt.ptr, bdt, nl, 0.0, TR.p(), TR.ld);
         allreduce(c, TR.p(), rr * cr);
         // T⁺ = Tᵀ (T Tᵀ)⁻¹ ; (T Tᵀ)⁻¹ = R⁻¹ R⁻ᵀ with T Tᵀ = RᵀR
         auto pinv_rows = [&](const Mat64& T, int64_t rk, int64_t cols, Mat64* out_p) {
             Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk);
-            DevBuf st(c, 64);
             gemm(c, OP_N, OP_T, rk, rk, cols, 1.0, T.p(), BCUR_F64, T.ld, T.p(), BCUR_F64, T.ld, 0.0, G.p(), G.ld);
-            cholesky_upper(c, G.p(), rk, G.ld, R.p(), st.as<int>(), st.as<double>() + 2);
-            int info = 0;
-            d2h(c, &info, st.as<int>(), 1);
-            if (info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
-            tri_inv_upper(c, R.p(), rk, Ri.p());
+            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p());
+            if (ci.info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
+            tri_inv_any(c, R.p(), rk, Ri.p());
             gemm(c, OP_N, OP_T, rk, rk, rk, 1.0, Ri.p(), BCUR_F64, Ri.ld, Ri.p(), BCUR_F64, Ri.ld, 0.0, Gi.p(), Gi.ld);
             *out_p = Mat64(c, cols, rk);
             gemm(c, OP_T, OP_N, cols, rk, rk, 1.0, T.p(), BCUR_F64, T.ld, Gi.p(), BCUR_F64, Gi.ld, 0.0, out_p->p(),
