@@ -33,16 +33,26 @@ constexpr int BM = 128, BK = 32, BN = 64, CH = 2;
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 
-// NT 64-column N tiles per CTA share every staged A tile (NT = 2 halves the L2 bytes
-// per MMA for wide products).  TMEM: NT tiles × {hi, lo} × 2 buffers × 64 columns.
-template <int NT>
+// NT 64-column N tiles per CTA share every staged A tile (more N per CTA = fewer L2
+// bytes per MMA).  Two precisions:
+//  X3 (3×TF32): stage = {a_raw, a_lo, x_hi[NT], x_lo[NT]}; per tile a hi and a cross-term
+//      accumulator, double-buffered in TMEM; drained into fp64 registers (1 tile/warp).
+//  X1 (1×TF32, both operands rounded to nearest): stage = {rn(a) in place, x[NT]}; one
+//      accumulator per tile; drained into fp32 (round-to-nearest) registers.
+//      Only for sums of squared projections (ROWSQ): the unbiased rounding errors cancel
+//      to ~1e-8 relative over the ~10⁸ terms.
+template <int NT, bool X3>
 struct Cfg {
-    static constexpr uint32_t STAGE = 2 * A_TILE + 2 * NT * X_TILE;  // 48 KB / 64 KB
-    static constexpr int STAGES = NT == 1 ? 4 : 3;
+    static constexpr int NACC = X3 ? 2 : 1;                                  // accumulators per tile
+    static constexpr int TPW = 1;                                            // tiles per drain warp
+    static constexpr uint32_t STAGE = (X3 ? 2 : 1) * A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
+    static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 4 * BN * NT;
-    static constexpr int NTRANSFORM = NT == 1 ? 4 : 2;                    // transform warps
-    static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + 4 * NT);       // 320 / 384
+    static constexpr uint32_t TMEM_COLS = 2 * NACC * BN * NT;               // ≤ 512
+    static constexpr int NDRAIN = 4 * NT / TPW;                              // drain warps
+    static constexpr int NTRANSFORM = (2 + NDRAIN) >= 10 ? 2 : 4;           // transform warps
+    static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
+    static_assert(TMEM_COLS <= 512, "TMEM budget");
 };
 enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
 
@@ -122,15 +132,17 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    "=r"(r[15])                                                                                     \
                  : "r"(taddr))
 
-template <bool A_MN, int EPI, int NT>
-__global__ void __launch_bounds__(Cfg<NT>::NTHREADS, 1)
+template <bool A_MN, int EPI, int NT, bool X3>
+__global__ void __launch_bounds__(Cfg<NT, X3>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
        const __grid_constant__ CUtensorMap tmXl, int M, int N, int k_tiles, int k_tiles_per_split,
        double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta) {
     constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
                                ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
 
-    using CF = Cfg<NT>;
+    using CF = Cfg<NT, X3>;
+    constexpr int NACC = CF::NACC, TPW = CF::TPW;
+    using AccT = typename std::conditional<X3, double, float>::type;
     constexpr int STAGES = CF::STAGES;
     constexpr uint32_t STAGE = CF::STAGE, TMEM_COLS = CF::TMEM_COLS;
     extern __shared__ uint8_t smem_raw[];
@@ -160,7 +172,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 128 * NT);
+            mbar_init(&tempty[b], 32 * CF::NDRAIN);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
@@ -177,11 +189,12 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
+    // per stage: [a_raw][a_lo (X3)][x_hi tile 0..NT-1][x_lo tile 0..NT-1 (X3)]
+    constexpr uint32_t A_BYTES = (X3 ? 2 : 1) * A_TILE;
     auto a_raw = [&](int s) { return smem + s * STAGE; };
     auto a_lo = [&](int s) { return smem + s * STAGE + A_TILE; };
-    // per stage: [a_raw][a_lo][x_hi tile 0..NT-1][x_lo tile 0..NT-1]
-    auto x_hi = [&](int s) { return smem + s * STAGE + 2 * A_TILE; };
-    auto x_lo = [&](int s) { return smem + s * STAGE + 2 * A_TILE + NT * X_TILE; };
+    auto x_hi = [&](int s) { return smem + s * STAGE + A_BYTES; };
+    auto x_lo = [&](int s) { return smem + s * STAGE + A_BYTES + NT * X_TILE; };
 
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
@@ -189,14 +202,14 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             for (int i = 0; i < nk; ++i) {
                 const int s = i % STAGES;
                 mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
-                mbar_expect_tx(&full[s], A_TILE + 2 * NT * X_TILE);
+                mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
                 const int k0 = (kt0 + i) * BK;
                 if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
                 else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
                     tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
-                    tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
+                    if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
                 }
             }
         }
@@ -217,8 +230,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                 for (int k8 = 0; k8 < BK / 8; ++k8)
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
-                    // TMEM columns: [buffer b][tile nt][hi | lo]
-                    const uint32_t t_hi = tmem + (uint32_t)((b * NT + nt) * 2 * BN), t_lo = t_hi + BN;
+                    // TMEM columns: [buffer b][tile nt][hi | lo (X3)]
+                    const uint32_t t_hi = tmem + (uint32_t)((b * NT + nt) * NACC * BN), t_lo = t_hi + BN;
                     const uint32_t xh = smem_u32(x_hi(s)) + nt * X_TILE, xl = smem_u32(x_lo(s)) + nt * X_TILE;
                     uint64_t da_r, da_l;
                     if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
@@ -231,76 +244,96 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2), dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
                     const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
                     umma_tf32(t_hi, da_r, dxh, IDESC, acc);
-                    umma_tf32(t_lo, da_r, dxl, IDESC, acc);
-                    umma_tf32(t_lo, da_l, dxh, IDESC, 1u);
+                    if (X3) {
+                        umma_tf32(t_lo, da_r, dxl, IDESC, acc);
+                        umma_tf32(t_lo, da_l, dxh, IDESC, 1u);
+                    }
                 }
                 umma_commit(&empty[s]);
                 if ((i % CH) == CH - 1 || i == nk - 1) umma_commit(&tfull[b]);
             }
             __syncwarp();
         }
-    } else if (warp >= 4 && warp < 4 + 4 * NT) {
+    } else if (warp >= 4 && warp < 4 + CF::NDRAIN) {
         // ------------------------------------------- TMEM drain + epilogue
-        const int q = warp & 3;                 // TMEM lane quarter (warp % 4)
-        const int nt = (warp - 4) >> 2;         // N tile drained by this warp
+        const int q = warp & 3;                     // TMEM lane quarter (warp % 4)
+        const int nt0 = ((warp - 4) >> 2) * TPW;    // first N tile drained by this warp
         const int row = m_tile * BM + q * 32 + lane;
-        const int col0 = (n_tile * NT + nt) * BN;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        double acc[BN];
+        AccT acc[TPW * BN];
 #pragma unroll
-        for (int j = 0; j < BN; ++j) acc[j] = 0.0;
+        for (int j = 0; j < TPW * BN; ++j) acc[j] = (AccT)0;
         for (int c = 0; c < nchunks; ++c) {
             const int b = c & 1;
             mbar_wait(&tfull[b], (uint32_t)(c / 2) & 1u);
             tc_fence_after();
-            const uint32_t t_hi = tmem + lane_off + (uint32_t)((b * NT + nt) * 2 * BN), t_lo = t_hi + BN;
 #pragma unroll
-            for (int j0 = 0; j0 < BN; j0 += 16) {
-                uint32_t h[16], l[16];
-                TMEM_LD16(t_hi + j0, h);
-                TMEM_LD16(t_lo + j0, l);
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int tt = 0; tt < TPW; ++tt) {
+                const uint32_t t_hi = tmem + lane_off + (uint32_t)((b * NT + nt0 + tt) * NACC * BN), t_lo = t_hi + BN;
 #pragma unroll
-                for (int j = 0; j < 16; ++j)
-                    acc[j0 + j] += (double)__uint_as_float(h[j]) + (double)__uint_as_float(l[j]);
+                for (int j0 = 0; j0 < BN; j0 += 16) {
+                    uint32_t h[16], l[16];
+                    TMEM_LD16(t_hi + j0, h);
+                    if (X3) TMEM_LD16(t_lo + j0, l);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        if (X3) acc[tt * BN + j0 + j] += (double)__uint_as_float(h[j]) + (double)__uint_as_float(l[j]);
+                        else acc[tt * BN + j0 + j] += __uint_as_float(h[j]);
+                    }
+                }
             }
             tc_fence_before();
             mbar_arrive(&tempty[b]);
         }
-        if (EPI == EPI_ROWSQ) {
-            double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < BN; ++j) s = fma(acc[j], acc[j], s);  // columns ≥ N are exact zeros
-            if (row < M) partial[(int64_t)(n_tile * NT + nt) * M + row] = s;
-        } else if (row < M) {
+        for (int tt = 0; tt < TPW; ++tt) {
+            const int nt = nt0 + tt;
+            const int col0 = (n_tile * NT + nt) * BN;
+            if (EPI == EPI_ROWSQ) {
+                double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < BN; ++j) {
-                const int col = col0 + j;
-                if (col < N) {
-                    if (partial) {
-                        partial[(int64_t)split * M * N + row + (int64_t)col * M] = acc[j];
-                    } else {
-                        double* o = out + row + (int64_t)col * ldo;
-                        *o = beta == 0.0 ? alpha * acc[j] : fma(beta, *o, alpha * acc[j]);
+                for (int j = 0; j < BN; ++j) {
+                    const double v = (double)acc[tt * BN + j];
+                    s = fma(v, v, s);  // columns ≥ N are exact zeros
+                }
+                if (row < M) partial[(int64_t)(n_tile * NT + nt) * M + row] = s;
+            } else if (row < M) {
+#pragma unroll
+                for (int j = 0; j < BN; ++j) {
+                    const int col = col0 + j;
+                    if (col < N) {
+                        const double v = (double)acc[tt * BN + j];
+                        if (partial) {
+                            partial[(int64_t)split * M * N + row + (int64_t)col * M] = v;
+                        } else {
+                            double* o = out + row + (int64_t)col * ldo;
+                            *o = beta == 0.0 ? alpha * v : fma(beta, *o, alpha * v);
+                        }
                     }
                 }
             }
         }
     } else if (warp >= 2) {
-        // ------------------------------------------------ a_lo transform
+        // ------------------------- a_lo transform (X3) / in-place rn_tf32 (X1)
         constexpr int NTT = 32 * CF::NTRANSFORM;
-        const int t = (warp < 4 ? warp - 2 : warp - (4 + 4 * NT) + 2) * 32 + lane;  // 0..NTT-1
+        const int t = (warp < 4 ? warp - 2 : warp - (4 + CF::NDRAIN) + 2) * 32 + lane;  // 0..NTT-1
         for (int i = 0; i < nk; ++i) {
             const int s = i % STAGES;
             mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
-            const uint32_t src = smem_u32(a_raw(s)), dst = smem_u32(a_lo(s));
+            const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(s)) : src;
 #pragma unroll 4
             for (int v = t; v < (int)(A_TILE / 16); v += NTT) {
                 float4 a;
                 asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                              : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
-                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(lo_of(a.x)),
-                             "f"(lo_of(a.y)), "f"(lo_of(a.z)), "f"(lo_of(a.w)) : "memory");
+                if (X3) {
+                    a.x = lo_of(a.x); a.y = lo_of(a.y); a.z = lo_of(a.z); a.w = lo_of(a.w);
+                } else {
+                    a.x = rn_tf32(a.x); a.y = rn_tf32(a.y); a.z = rn_tf32(a.z); a.w = rn_tf32(a.w);
+                }
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(a.x), "f"(a.y),
+                             "f"(a.z), "f"(a.w) : "memory");
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&lo_ready[s]);
@@ -371,29 +404,31 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
     return m;
 }
 
-template <bool A_MN, int EPI, int NT>
+template <bool A_MN, int EPI, int NT, bool X3>
 void launch_umma_nt(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
                     int N, int k_tiles, int kps, double* out, int64_t ldo, double* partial, double alpha,
                     double beta) {
-    auto kern = k_umma<A_MN, EPI, NT>;
+    using CF = Cfg<NT, X3>;
+    auto kern = k_umma<A_MN, EPI, NT, X3>;
     static bool attr = false;
     if (!attr) {
-        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<NT>::SMEM_BYTES));
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         attr = true;
     }
-    kern<<<grid, Cfg<NT>::NTHREADS, Cfg<NT>::SMEM_BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo,
-                                                                      partial, alpha, beta);
+    kern<<<grid, CF::NTHREADS, CF::SMEM_BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha,
+                                                            beta);
     LAUNCH_CHECK(c);
 }
 
+// 3×TF32 with 1 or 2 N tiles per CTA
 template <bool A_MN, int EPI>
 void launch_umma(Ctx* c, int nt_per_cta, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th,
                  const CUtensorMap& tl, int M, int N, int k_tiles, int kps, double* out, int64_t ldo, double* partial,
                  double alpha, double beta) {
     if (nt_per_cta == 2)
-        launch_umma_nt<A_MN, EPI, 2>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
+        launch_umma_nt<A_MN, EPI, 2, true>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
     else
-        launch_umma_nt<A_MN, EPI, 1>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
+        launch_umma_nt<A_MN, EPI, 1, true>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
 }
 
 // x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
@@ -442,16 +477,24 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
     CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     const int k_tiles = (int)((m + BK - 1) / BK);
-    const int NT = N > BN ? 2 : 1;
-    const int mt = (int)((n + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
-    dim3 grid(nt, mt, 1);  // N tiles of one A row-tile run side by side and share it through L2
+    const int mt = (int)((n + BM - 1) / BM);
     if (rowsq) {
-        DevBuf part(c, (size_t)nt * NT * n * sizeof(double));
-        launch_umma<false, EPI_ROWSQ>(c, NT, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, nullptr, 0,
-                                      part.as<double>(), 1.0, 0.0);
-        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt * NT, part.as<double>(), rowsq);
+        // Σ of squared projections: 1×TF32 with both operands rounded to nearest (unbiased),
+        // 4 N tiles (256 columns) per CTA sharing each A tile.
+        constexpr int NT4 = 4;
+        const int nt = (int)((N + NT4 * BN - 1) / (NT4 * BN));
+        dim3 grid(nt, mt, 1);
+        DevBuf part(c, (size_t)nt * NT4 * n * sizeof(double));
+        launch_umma_nt<false, EPI_ROWSQ, NT4, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles, nullptr,
+                                                     0, part.as<double>(), 1.0, 0.0);
+        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt * NT4, part.as<double>(), rowsq);
         LAUNCH_CHECK(c);
-    } else {
+        return;
+    }
+    const int NT = N > BN ? 2 : 1;
+    const int nt = (int)((N + NT * BN - 1) / (NT * BN));
+    dim3 grid(nt, mt, 1);  // N tiles of one A row-tile run side by side and share it through L2
+    {
         launch_umma<false, EPI_STORE>(c, NT, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr,
                                       alpha, beta);
     }

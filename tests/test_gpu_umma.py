@@ -52,6 +52,8 @@ def test_fused_row_sumsq(B, N):
     q = np.asfortranarray(gen.standard_normal((m, N)))
     ref = np.sum((a.astype(np.float64).T @ q) ** 2, axis=1)
     got = B.sketch_product(a, q, transpose=True, row_sumsq=True)
-    assert np.max(np.abs(got - ref) / ref) < 1e-5
+    # 1×TF32 with both operands rounded to nearest: unbiased per-element errors ~2⁻¹² that
+    # average out — a row (N·K terms) is good to ~1e-4, the grand total to ~1e-7
+    assert np.max(np.abs(got - ref) / ref) < 5e-4
     # tensor-core accumulate rounds toward zero: bounded by chunked fp64 draining
     assert abs(got.sum() - ref.sum()) / ref.sum() < 1e-6
