@@ -250,7 +250,12 @@ def bench_b200(args, cfg, rank, world, local_rank):
     return line
 
 
+def kernel_tags(prof):
+    return {t: v for t, v in (prof or {}).items() if not t.startswith(("phase:", "_"))}
+
+
 def roofline(prof, peaks):
+    prof = kernel_tags(prof)
     if not prof:
         return None
     tag, d = max(prof.items(), key=lambda kv: kv[1]["ms"])

@@ -216,6 +216,7 @@ bcur_status bcur_ctx_profile(bcur_ctx ctx, int enable) {
     }
     c->prof_recs.clear();
     c->prof = enable != 0;
+    c->allocs_mark = c->allocs;
     API_END
 }
 
@@ -247,6 +248,9 @@ int64_t bcur_ctx_profile_dump(bcur_ctx ctx, char* buf, int64_t cap) {
         s += tmp;
         first = false;
     }
+    std::snprintf(tmp, sizeof tmp, "%s\"_cudaMalloc\": {\"scopes\": %lld, \"ms\": 0, \"flops\": 0, \"bytes\": 0}",
+                  first ? "" : ", ", (long long)(ctx->allocs - ctx->allocs_mark));
+    s += tmp;
     s += "}";
     if (buf && cap > 0) {
         std::strncpy(buf, s.c_str(), (size_t)cap - 1);

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -66,10 +67,15 @@ struct Ctx {
     void* pinned = nullptr;
     size_t pinned_bytes = 0;
 
+    // Workspace cache over cudaMalloc (large pages, TMA-friendly): blocks are kept in exact
+    // size classes (≤ 12.5% rounding), so a repeated decomposition reuses every block and
+    // never calls cudaMalloc in steady state.  Reuse is safe in stream order: a block is
+    // released only after its last use has been enqueued on this context's stream.
+    int64_t allocs = 0, allocs_mark = 0;
     void* acquire(size_t bytes) {
-        size_t want = round(bytes);
-        auto it = free_list.lower_bound(want);
-        if (it != free_list.end() && it->first <= want + want / 2 + (1 << 20)) {
+        const size_t want = round(bytes);
+        auto it = free_list.find(want);
+        if (it != free_list.end()) {
             void* p = it->second;
             free_list.erase(it);
             return p;
@@ -81,6 +87,7 @@ struct Ctx {
             trim();
             CUDA_CHECK(cudaMalloc(&p, want));
         }
+        ++allocs;
         sizes[p] = want;
         return p;
     }
@@ -97,8 +104,13 @@ struct Ctx {
         free_list.clear();
     }
     static size_t round(size_t b) {
-        if (b < 256) return 256;
-        const size_t g = b < (1u << 20) ? 256 : (1u << 20);
+        if (b <= 256) return 256;
+        size_t p = 256;
+        while (p < b && p < (1u << 20)) p <<= 1;
+        if (b <= (1u << 20)) return p;
+        size_t top = 1;
+        while ((top << 1) <= b) top <<= 1;
+        const size_t g = std::max<size_t>(top >> 3, 2u << 20);
         return (b + g - 1) / g * g;
     }
     void* host_stage(size_t bytes) {

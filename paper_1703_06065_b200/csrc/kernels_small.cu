@@ -17,23 +17,30 @@ constexpr int SMEM_MAX_W = 144;
 
 // --------------------------------------------------------------- Cholesky
 // Right-looking, upper: M (w×w, column-major, ld w) → R with G = RᵀR.
+// Chained use (blocked factorization): a nonzero *info on entry means an earlier block
+// failed — return untouched; on failure write info = info_offset + j + 1.  diag[0]
+// accumulates min diag(R) across the chain (caller initialises it), diag[1] = max diag(G).
 __global__ void __launch_bounds__(ST) k_cholesky(const double* __restrict__ g, int w, int64_t ldg,
                                                  double* __restrict__ r, double* __restrict__ work, int* info,
-                                                 double* diag) {
+                                                 double* diag, int info_offset, int chained) {
     extern __shared__ double sm[];
+    if (chained && *info != 0) return;
     double* M = work ? work : sm;
+    double* rowj = work ? work + (size_t)w * w : sm + (size_t)w * w;  // w doubles after M
     __shared__ int stop;
     __shared__ double rdiag;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int k = warp; k < w; k += NW)
         for (int i = lane; i < w; i += 32) M[i + k * w] = g[i + k * ldg];
-    if (threadIdx.x == 0) {
-        stop = 0;
-        double mx = 0.0;
-        for (int j = 0; j < w; ++j) mx = fmax(mx, g[j + j * ldg]);
-        diag[1] = mx;
-    }
+    if (threadIdx.x == 0) stop = 0;
     __syncthreads();
+    if (warp == 0) {
+        double mx = 0.0;
+        for (int j = lane; j < w; j += 32) mx = fmax(mx, M[j + j * w]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && !chained) diag[1] = mx;
+    }
     double mn = INFINITY;
     for (int j = 0; j < w; ++j) {
         if (threadIdx.x == 0) {
@@ -50,20 +57,29 @@ __global__ void __launch_bounds__(ST) k_cholesky(const double* __restrict__ g, i
         const double rj = rdiag;
         mn = fmin(mn, rj);
         const double inv = 1.0 / rj;
-        for (int k = j + 1 + threadIdx.x; k < w; k += ST) M[j + k * w] *= inv;
+        for (int k = j + 1 + threadIdx.x; k < w; k += ST) {
+            const double v = M[j + k * w] * inv;
+            M[j + k * w] = v;
+            rowj[k] = v;  // contiguous copy of row j: the update below reads it conflict-free
+        }
         __syncthreads();
-        // trailing update of the upper triangle: M[i,k] -= M[j,i]·M[j,k], j < i ≤ k
+        // trailing update of the upper triangle: M[i,k] -= R[j,i]·R[j,k], j < i ≤ k
         for (int k = j + 1 + warp; k < w; k += NW) {
-            const double rk = M[j + k * w];
-            for (int i = j + 1 + lane; i <= k; i += 32) M[i + k * w] = fma(-M[j + i * w], rk, M[i + k * w]);
+            const double rk = rowj[k];
+            for (int i = j + 1 + lane; i <= k; i += 32) M[i + k * w] = fma(-rowj[i], rk, M[i + k * w]);
         }
         __syncthreads();
     }
     for (int k = warp; k < w; k += NW)
         for (int i = lane; i < w; i += 32) r[i + k * w] = i <= k ? M[i + k * w] : 0.0;
     if (threadIdx.x == 0) {
-        *info = stop;
-        diag[0] = stop ? 0.0 : mn;
+        if (chained) {
+            if (stop) *info = info_offset + stop;
+            diag[0] = stop ? 0.0 : fmin(diag[0], mn);
+        } else {
+            *info = stop;
+            diag[0] = stop ? 0.0 : mn;
+        }
     }
 }
 
@@ -218,15 +234,17 @@ void ensure_attrs() {
 
 namespace ops {
 
-void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int* info, double* diag) {
+void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int* info, double* diag,
+                    int64_t info_offset, bool chained) {
     if (w > 4096) fail(BCUR_E_INVALID_ARGUMENT, "cholesky_upper: single-CTA path limited to w <= 4096");
     ensure_attrs();
     ProfScope prof(c, "cholesky", w * w * w / 3.0, 8.0 * w * w);
     DevBuf work;
     size_t smem = 0;
-    if (w <= SMEM_MAX_W) smem = (size_t)w * w * sizeof(double);
-    else work = DevBuf(c, (size_t)w * w * sizeof(double));
-    k_cholesky<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, r, work.as<double>(), info, diag);
+    if (w <= SMEM_MAX_W) smem = (size_t)(w * w + w) * sizeof(double);
+    else work = DevBuf(c, (size_t)(w * w + w) * sizeof(double));
+    k_cholesky<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, r, work.as<double>(), info, diag, (int)info_offset,
+                                           chained ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
