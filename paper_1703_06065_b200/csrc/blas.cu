@@ -1,0 +1,37 @@
+// blas.cu — cuBLAS DGEMM for the plain fp64 products of the small factorizations
+// (the task rules allow a library for plain GEMMs; every fused hot-path product is a
+// hand-written tcgen05 kernel in kernels_umma.cu).
+#include <cublas_v2.h>
+
+#include "ops.h"
+
+namespace bcur_b200 {
+namespace ops {
+
+namespace {
+struct Handle {
+    cublasHandle_t h = nullptr;
+    ~Handle() {
+        if (h) cublasDestroy(h);
+    }
+};
+thread_local std::map<int, Handle> g_handles;  // per device, per host thread
+}  // namespace
+
+void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+    Handle& hd = g_handles[c->device];
+    if (!hd.h) {
+        if (cublasCreate(&hd.h) != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasCreate failed");
+        cublasSetPointerMode(hd.h, CUBLAS_POINTER_MODE_HOST);
+    }
+    cublasSetStream(hd.h, c->stream);
+    const cublasStatus_t st =
+        cublasDgemm(hd.h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, (int)M, (int)N, (int)K,
+                    &alpha, A, (int)lda, B, (int)ldb, &beta, C, (int)ldc);
+    if (st != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasDgemm failed (" + std::to_string((int)st) + ")");
+    c->launches++;
+}
+
+}  // namespace ops
+}  // namespace bcur_b200

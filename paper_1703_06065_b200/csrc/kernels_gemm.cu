@@ -226,6 +226,14 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
             return;
         }
     }
+    // plain fp64 GEMMs of the small factorizations (Grams, Cholesky/inverse updates, factor
+    // products) → cuBLAS DGEMM (DMMA tensor cores); deterministic for a fixed device.
+    if (dta == BCUR_F64 && dtb == BCUR_F64 && K > 0 && (double)M * N * K >= 32768.0) {
+        ProfScope prof(c, "dgemm_cublas", 2.0 * M * N * K, 8.0 * ((double)M * K + (double)K * N + (double)M * N));
+        cublas_dgemm(c, ta == OP_T, tb == OP_T, M, N, K, alpha, (const double*)A, lda, (const double*)B, ldb, beta,
+                     C, ldc);
+        return;
+    }
     ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_store_f32" : "gemm_store_f64", 2.0 * M * N * K,
                    (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M * N);
     if (K <= 0) {

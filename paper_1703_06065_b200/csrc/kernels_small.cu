@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
     extern __shared__ double sm[];
     double* A = Aglob ? Aglob : sm;
     __shared__ int pos[512];
-    __shared__ double cs[256], sn[256];
+    __shared__ double cs[256], sn[256], np_[256], nq_[256];
     __shared__ int pp[256], qq[256];
     __shared__ int rotated;
     __shared__ double floor_abs;
@@ -147,7 +147,10 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
         __syncthreads();
         for (int round = 0; round < wp - 1; ++round) {
             for (int i = threadIdx.x; i < half; i += ST) {
-                int p = pos[i], q = pos[wp - 1 - i];
+                // circle method: player wp-1 fixed, the others rotate (all pairs in wp-1 rounds)
+                const int mrot = wp - 1;
+                int p = i == 0 ? round : (round + i) % mrot;
+                int q = i == 0 ? wp - 1 : (round - i + mrot) % mrot;
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, s = 0.0;
                 if (q < w) {
@@ -158,6 +161,8 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                         const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
                         c = 1.0 / sqrt(1.0 + t * t);
                         s = t * c;
+                        np_[i] = app - t * apq;  // exact post-rotation diagonal (Golub–Van Loan 8.4)
+                        nq_[i] = aqq + t * apq;
                         rotated = 1;
                     }
                 }
@@ -194,10 +199,14 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                 }
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                const int last = pos[wp - 1];
-                for (int i = wp - 1; i > 1; --i) pos[i] = pos[i - 1];
-                pos[1] = last;
+            // the rotated pair is annihilated exactly (rounding noise would retrigger rotations)
+            for (int i = threadIdx.x; i < half; i += ST) {
+                const int p = pp[i], q = qq[i];
+                if (q >= w || sn[i] == 0.0) continue;
+                A[p + q * w] = 0.0;
+                A[q + p * w] = 0.0;
+                A[p + p * w] = np_[i];
+                A[q + q * w] = nq_[i];
             }
             __syncthreads();
         }

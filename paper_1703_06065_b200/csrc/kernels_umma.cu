@@ -30,6 +30,7 @@ namespace bcur_b200 {
 namespace {
 
 constexpr int BM = 128, BK = 32, BN = 64, CH = 2;
+__device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, bit 1 skip drain (timing experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 
@@ -46,7 +47,7 @@ struct Cfg {
     static constexpr int NACC = X3 ? 2 : 1;                                  // accumulators per tile
     static constexpr int TPW = 1;                                            // tiles per drain warp
     static constexpr uint32_t STAGE = (X3 ? 2 : 1) * A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
-    static constexpr int STAGES = (200 * 1024) / STAGE > 6 ? 6 : (200 * 1024) / STAGE;
+    static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * NACC * BN * NT;               // ≤ 512
     static constexpr int NDRAIN = 4 * NT / TPW;                              // drain warps
@@ -96,6 +97,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
         ::"r"(smem_u32(dst)), "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+}
+// L2 prefetch of a future A tile (no shared memory, no barrier): hides DRAM latency
+// beyond what the shared-memory stage ring can keep in flight.
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tm), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(tm), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -199,8 +209,16 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     if (warp == 0) {
         // ------------------------------------------------------ TMA producer
         if (lane == 0) {
+            constexpr int PF = 12;  // A-tile L2 prefetch distance (stages)
+            auto prefetch_a = [&](int i) {
+                const int k0 = (kt0 + i) * BK;
+                if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
+                else tma_prefetch_2d(&tmA, k0, m_tile * BM);
+            };
+            for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
             for (int i = 0; i < nk; ++i) {
                 const int s = i % STAGES;
+                if (i + PF < nk) prefetch_a(i + PF);
                 mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
                 mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
                 const int k0 = (kt0 + i) * BK;
@@ -267,6 +285,11 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const int b = c & 1;
             mbar_wait(&tfull[b], (uint32_t)(c / 2) & 1u);
             tc_fence_after();
+            if (g_dbg_flags & 2) {  // experiment switch: skip the drain (wrong results)
+                tc_fence_before();
+                mbar_arrive(&tempty[b]);
+                continue;
+            }
 #pragma unroll
             for (int tt = 0; tt < TPW; ++tt) {
                 const uint32_t t_hi = tmem + lane_off + (uint32_t)((b * NT + nt0 + tt) * NACC * BN), t_lo = t_hi + BN;
@@ -322,6 +345,11 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const int s = i % STAGES;
             mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
             const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(s)) : src;
+            if (g_dbg_flags & 1) {  // experiment switch: skip the transform (wrong results)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive(&lo_ready[s]);
+                continue;
+            }
 #pragma unroll 4
             for (int v = t; v < (int)(A_TILE / 16); v += NTT) {
                 float4 a;
@@ -452,6 +480,11 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
     if (enabled < 0) {
         const char* e = getenv("BCUR_DISABLE_UMMA");
         enabled = (e && e[0] == '1') ? 0 : 1;
+        const char* d = getenv("BCUR_UMMA_DEBUG");
+        if (d) {
+            const int f = atoi(d);
+            CUDA_CHECK(cudaMemcpyToSymbol(g_dbg_flags, &f, sizeof f));
+        }
     }
     return enabled && dta == BCUR_F32 && m % 32 == 0 && (lda * 4) % 16 == 0 && ((uintptr_t)a % 16) == 0 && m > 0 &&
            m < (1LL << 31);
@@ -479,15 +512,23 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
     const int k_tiles = (int)((m + BK - 1) / BK);
     const int mt = (int)((n + BM - 1) / BM);
     if (rowsq) {
-        // Σ of squared projections: 1×TF32 with both operands rounded to nearest (unbiased),
-        // 4 N tiles (256 columns) per CTA sharing each A tile.
-        constexpr int NT4 = 4;
-        const int nt = (int)((N + NT4 * BN - 1) / (NT4 * BN));
+        // Σ of squared projections: 1×TF32 with both operands rounded to nearest (unbiased);
+        // up to 4 N tiles (256 columns) per CTA share each A tile; narrow panels (greedy
+        // steps) use fewer tiles and a deeper stage ring (HBM-bound regime).
+        const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
+        const int nt = (int)((N + NTX * BN - 1) / (NTX * BN));
         dim3 grid(nt, mt, 1);
-        DevBuf part(c, (size_t)nt * NT4 * n * sizeof(double));
-        launch_umma_nt<false, EPI_ROWSQ, NT4, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles, nullptr,
-                                                     0, part.as<double>(), 1.0, 0.0);
-        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt * NT4, part.as<double>(), rowsq);
+        DevBuf part(c, (size_t)nt * NTX * n * sizeof(double));
+        if (NTX == 1)
+            launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles,
+                                                       nullptr, 0, part.as<double>(), 1.0, 0.0);
+        else if (NTX == 2)
+            launch_umma_nt<false, EPI_ROWSQ, 2, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles,
+                                                       nullptr, 0, part.as<double>(), 1.0, 0.0);
+        else
+            launch_umma_nt<false, EPI_ROWSQ, 4, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles,
+                                                       nullptr, 0, part.as<double>(), 1.0, 0.0);
+        k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt * NTX, part.as<double>(), rowsq);
         LAUNCH_CHECK(c);
         return;
     }

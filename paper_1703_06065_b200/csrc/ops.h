@@ -34,6 +34,10 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
 
+// ---- cuBLAS DGEMM for plain fp64 products (blas.cu) -----------------------
+void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
+
 // ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
 bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
 // Out(n×N) = alpha·Aᵀ X + beta·Out (fp64) or rowsq[j] = Σ_c (AᵀX)_jc²; X fp32 or fp64

@@ -185,6 +185,13 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
         tri_inv_any(c, R.p(), w, Ri.p());
         gemm(c, OP_N, OP_N, rows, w, w, 1.0, X, BCUR_F64, ldx, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
     } else {
+        // σ_max(X) ≤ ‖X‖_F ≤ sqrt(w·max diag G): below the rank cut every σ is, so the
+        // eig path would keep nothing — skip the eigensolver (e.g. a panel already in span).
+        if (std::sqrt((double)w * std::max(ci.maxdiag, 0.0)) <= tau_rank(dt) * ref) {
+            if (path_out) *path_out = 1;
+            if (T_out) *T_out = Mat64(c, 0, w);
+            return 0;
+        }
         Mat64 lam(c, w, 1), V(c, w, w);
         sym_eig(c, G.p(), w, G.ld, lam.p(), V.p());
         std::vector<double> lh(w);
