@@ -125,24 +125,26 @@ __global__ void k_sum_vector(const double* __restrict__ x, int64_t n, double* __
     if (threadIdx.x == 0) out[0] = s;
 }
 
-__global__ void k_max_dev_identity(const double* __restrict__ g, int64_t w, int64_t ld, double* __restrict__ out) {
+// max |G − I| over a w×w matrix: warp per column (lanes over rows, coalesced), block max,
+// then an integer atomicMax on the bit pattern (non-negative doubles order like their bits;
+// a NaN's pattern exceeds +inf, so NaN propagates).  *out must be zeroed first.
+__global__ void k_max_dev_identity(const double* __restrict__ g, int w, int64_t ld,
+                                   unsigned long long* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     double mx = 0.0;
-    for (int64_t e = threadIdx.x; e < w * w; e += blockDim.x) {
-        const int64_t i = e % w, j = e / w;
-        const double d = fabs(g[i + j * ld] - (i == j ? 1.0 : 0.0));
-        mx = d > mx || d != d ? d : mx;  // NaN propagates
-    }
-    __shared__ double red[RT];
-    red[threadIdx.x] = mx;
-    __syncthreads();
-    for (int s = RT / 2; s > 0; s >>= 1) {
-        if ((int)threadIdx.x < s) {
-            const double o = red[threadIdx.x + s];
-            if (o > red[threadIdx.x] || o != o) red[threadIdx.x] = o;
+    for (int j = blockIdx.x * nw + warp; j < w; j += gridDim.x * nw) {
+        const double* col = g + (int64_t)j * ld;
+        for (int i = lane; i < w; i += 32) {
+            const double d = fabs(col[i] - (i == j ? 1.0 : 0.0));
+            mx = d > mx || d != d ? d : mx;
         }
-        __syncthreads();
     }
-    if (threadIdx.x == 0) out[0] = red[0];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, mx, o);
+        mx = v > mx || v != v ? v : mx;
+    }
+    if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
 }
 
 }  // namespace
@@ -192,7 +194,11 @@ void segment_sum(Ctx* c, const double* x, const int64_t* d_offsets, int64_t G, d
 }
 
 void max_dev_identity(Ctx* c, const double* g, int64_t w, int64_t ld, double* d_out) {
-    k_max_dev_identity<<<1, RT, 0, c->stream>>>(g, w, ld, d_out);
+    ProfScope prof(c, "max_dev", 0.0, 8.0 * w * w);
+    CUDA_CHECK(cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
+    if (w <= 0) return;
+    const int blocks = (int)std::min<int64_t>((w + 7) / 8, 4LL * c->sm_count);
+    k_max_dev_identity<<<blocks, 256, 0, c->stream>>>(g, (int)w, ld, reinterpret_cast<unsigned long long*>(d_out));
     LAUNCH_CHECK(c);
 }
 

@@ -16,63 +16,54 @@ constexpr int NW = ST / 32;
 constexpr int SMEM_MAX_W = 144;
 
 // --------------------------------------------------------------- Cholesky
-// Right-looking, upper: M (w×w, column-major, ld w) → R with G = RᵀR.
+// Right-looking with delayed scaling on the LOWER triangle L of the working copy
+// (M[i,k], i ≥ k, holds Gᵀ's entries): step j subtracts M[i,j]·M[k,j]/M[j,j] from every
+// trailing M[i,k] (j < k ≤ i) — column j is read contiguously, one barrier per column —
+// and R[j,k] = M[k,j]/√M[j,j] is formed once at the end.  Input: the upper triangle of g.
 // Chained use (blocked factorization): a nonzero *info on entry means an earlier block
 // failed — return untouched; on failure write info = info_offset + j + 1.  diag[0]
 // accumulates min diag(R) across the chain (caller initialises it), diag[1] = max diag(G).
-__global__ void __launch_bounds__(ST) k_cholesky(const double* __restrict__ g, int w, int64_t ldg,
-                                                 double* __restrict__ r, double* __restrict__ work, int* info,
-                                                 double* diag, int info_offset, int chained) {
+__global__ void __launch_bounds__(ST) k_cholesky(const double* g, int w, int64_t ldg, double* r, int64_t ldr,
+                                                 double* __restrict__ work, int* info, double* diag,
+                                                 int info_offset, int chained) {
     extern __shared__ double sm[];
     if (chained && *info != 0) return;
     double* M = work ? work : sm;
-    double* rowj = work ? work + (size_t)w * w : sm + (size_t)w * w;  // w doubles after M
-    __shared__ int stop;
-    __shared__ double rdiag;
+    const int ldm = w | 1;  // odd stride: row-wise walks of the final transpose hit distinct banks
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int k = warp; k < w; k += NW)
-        for (int i = lane; i < w; i += 32) M[i + k * w] = g[i + k * ldg];
-    if (threadIdx.x == 0) stop = 0;
+        for (int i = lane; i <= k; i += 32) M[k + i * ldm] = g[i + k * ldg];  // upper of g → lower of M
     __syncthreads();
     if (warp == 0) {
         double mx = 0.0;
-        for (int j = lane; j < w; j += 32) mx = fmax(mx, M[j + j * w]);
+        for (int j = lane; j < w; j += 32) mx = fmax(mx, M[j + j * ldm]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0 && !chained) diag[1] = mx;
     }
+    int stop = 0;
     double mn = INFINITY;
     for (int j = 0; j < w; ++j) {
-        if (threadIdx.x == 0) {
-            const double d = M[j + j * w];
-            if (!(d > 0.0) || !isfinite(d)) {
-                stop = j + 1;
-            } else {
-                rdiag = sqrt(d);
-                M[j + j * w] = rdiag;
-            }
+        const double d = M[j + j * ldm];  // final after step j-1's barrier; identical in all threads
+        if (!(d > 0.0) || !isfinite(d)) {
+            stop = j + 1;
+            break;
         }
-        __syncthreads();
-        if (stop) break;
-        const double rj = rdiag;
-        mn = fmin(mn, rj);
-        const double inv = 1.0 / rj;
-        for (int k = j + 1 + threadIdx.x; k < w; k += ST) {
-            const double v = M[j + k * w] * inv;
-            M[j + k * w] = v;
-            rowj[k] = v;  // contiguous copy of row j: the update below reads it conflict-free
-        }
-        __syncthreads();
-        // trailing update of the upper triangle: M[i,k] -= R[j,i]·R[j,k], j < i ≤ k
+        mn = fmin(mn, d);
+        const double inv = 1.0 / d;
+        const double* colj = M + j * ldm;
         for (int k = j + 1 + warp; k < w; k += NW) {
-            const double rk = rowj[k];
-            for (int i = j + 1 + lane; i <= k; i += 32) M[i + k * w] = fma(-rowj[i], rk, M[i + k * w]);
+            const double a = colj[k] * inv;
+            double* colk = M + k * ldm;
+            for (int i = k + lane; i < w; i += 32) colk[i] = fma(-a, colj[i], colk[i]);
         }
         __syncthreads();
     }
     for (int k = warp; k < w; k += NW)
-        for (int i = lane; i < w; i += 32) r[i + k * w] = i <= k ? M[i + k * w] : 0.0;
+        for (int i = lane; i < w; i += 32)
+            r[i + k * ldr] = i <= k && !stop ? M[k + i * ldm] / sqrt(M[i + i * ldm]) : 0.0;
     if (threadIdx.x == 0) {
+        mn = sqrt(mn);
         if (chained) {
             if (stop) *info = info_offset + stop;
             diag[0] = stop ? 0.0 : fmin(diag[0], mn);
@@ -84,34 +75,60 @@ __global__ void __launch_bounds__(ST) k_cholesky(const double* __restrict__ g, i
 }
 
 // ------------------------------------------------------ triangular inverse
-// X = R⁻¹ (w ≤ TRI_MAX_W), both in shared memory; thread c back-substitutes column c:
-// X[i, c] = −(Σ_{t=i+1..c} R[i,t] X[t,c]) / R[i,i].  R is stored row-major and X
-// transposed (padded rows) so a thread walks contiguous, conflict-light addresses.
-constexpr int TRI_MAX_W = 64;
-__global__ void __launch_bounds__(64) k_tri_inv_upper(const double* __restrict__ r, int w, double* __restrict__ x) {
+// X = R⁻¹ for upper-triangular R, w ≤ TRI_MAX_W, one CTA, 16-wide blocks (the matrix is
+// padded with identity to a multiple of 16).  Storage: one padded square S holds R's
+// upper triangle in place and Xᵀ's strictly-lower part (X[i,c] at S[c + i·ld], c > i), X's
+// diagonal in xd.  Phase A inverts all diagonal blocks at once (thread per column, a
+// ≤16-deep back substitution); phase B sweeps block columns j = 1.. : T = X[0:j,0:j]·R[0:j,j],
+// then X[0:j,j] = −T·X_jj.  ~8 barriers instead of a w-deep serial chain.
+constexpr int TRI_MAX_W = 128;
+constexpr int TRI_B = 16;
+constexpr int TRI_LD = TRI_MAX_W + 1;
+__global__ void __launch_bounds__(ST) k_tri_inv_upper(const double* __restrict__ r, int w, int64_t ldr,
+                                                      double* __restrict__ x, int64_t ldx) {
     extern __shared__ double sm_tri[];
-    double(*Rr)[TRI_MAX_W + 1] = reinterpret_cast<double(*)[TRI_MAX_W + 1]>(sm_tri);                   // Rr[i][t] = R[i,t]
-    double(*XT)[TRI_MAX_W + 1] = reinterpret_cast<double(*)[TRI_MAX_W + 1]>(sm_tri + TRI_MAX_W * (TRI_MAX_W + 1));  // XT[c][t] = X[t,c]
-    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-        const int i = e % w, t = e / w;
-        Rr[i][t] = r[i + t * w];
-    }
+    double* S = sm_tri;                      // TRI_LD × TRI_LD
+    double* T = S + TRI_LD * TRI_LD;         // (TRI_MAX_W − TRI_B) × TRI_B, row r at T[r·TRI_B + c]
+    __shared__ double xd[TRI_MAX_W];
+    const int wp = (w + TRI_B - 1) / TRI_B * TRI_B;
+    const int nb = wp / TRI_B;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = warp; k < wp; k += NW)
+        for (int i = lane; i <= k; i += 32)
+            S[i + k * TRI_LD] = (i < w && k < w) ? r[i + k * ldr] : (i == k ? 1.0 : 0.0);
     __syncthreads();
-    const int c = threadIdx.x;
-    if (c < w) {
-        for (int i = c + 1; i < w; ++i) XT[c][i] = 0.0;
-        XT[c][c] = 1.0 / Rr[c][c];
-        for (int i = c - 1; i >= 0; --i) {
-            double s = 0.0;
-            for (int t = i + 1; t <= c; ++t) s = fma(Rr[i][t], XT[c][t], s);
-            XT[c][i] = -s / Rr[i][i];
+    // phase A: column c of the inverse of its diagonal block
+    for (int c = threadIdx.x; c < wp; c += ST) {
+        const int b0 = c / TRI_B * TRI_B;
+        const double xcc = 1.0 / S[c + c * TRI_LD];
+        xd[c] = xcc;
+        for (int i = c - 1; i >= b0; --i) {
+            double s = S[i + c * TRI_LD] * xcc;
+            for (int t = i + 1; t < c; ++t) s = fma(S[i + t * TRI_LD], S[c + t * TRI_LD], s);
+            S[c + i * TRI_LD] = -s / S[i + i * TRI_LD];
         }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < w * w; e += blockDim.x) {
-        const int i = e % w, cc = e / w;
-        x[i + cc * w] = XT[cc][i];
+    // phase B
+    for (int jb = 1; jb < nb; ++jb) {
+        const int j0 = jb * TRI_B;
+        for (int e = threadIdx.x; e < j0 * TRI_B; e += ST) {
+            const int cc = e % TRI_B, rr = e / TRI_B, c = j0 + cc;
+            double s = xd[rr] * S[rr + c * TRI_LD];
+            for (int t = rr + 1; t < j0; ++t) s = fma(S[t + rr * TRI_LD], S[t + c * TRI_LD], s);
+            T[rr * TRI_B + cc] = s;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < j0 * TRI_B; e += ST) {
+            const int cc = e % TRI_B, rr = e / TRI_B, c = j0 + cc;
+            double s = T[rr * TRI_B + cc] * xd[c];
+            for (int u = j0; u < c; ++u) s = fma(T[rr * TRI_B + (u - j0)], S[c + u * TRI_LD], s);
+            S[c + rr * TRI_LD] = -s;
+        }
+        __syncthreads();
     }
+    for (int k = warp; k < w; k += NW)
+        for (int i = lane; i < w; i += 32) x[i + k * ldx] = i < k ? S[k + i * TRI_LD] : (i == k ? xd[i] : 0.0);
 }
 
 // ---------------------------------------------------------------- Jacobi
@@ -243,30 +260,32 @@ void ensure_attrs() {
 
 namespace ops {
 
-void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int* info, double* diag,
+void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int64_t ldr, int* info, double* diag,
                     int64_t info_offset, bool chained) {
     if (w > 4096) fail(BCUR_E_INVALID_ARGUMENT, "cholesky_upper: single-CTA path limited to w <= 4096");
     ensure_attrs();
     ProfScope prof(c, "cholesky", w * w * w / 3.0, 8.0 * w * w);
     DevBuf work;
     size_t smem = 0;
-    if (w <= SMEM_MAX_W) smem = (size_t)(w * w + w) * sizeof(double);
-    else work = DevBuf(c, (size_t)(w * w + w) * sizeof(double));
-    k_cholesky<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, r, work.as<double>(), info, diag, (int)info_offset,
+    const size_t bytes = (size_t)w * (size_t)(w | 1) * sizeof(double);
+    if (w <= SMEM_MAX_W) smem = bytes;
+    else work = DevBuf(c, bytes);
+    k_cholesky<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, r, ldr, work.as<double>(), info, diag, (int)info_offset,
                                            chained ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
-void tri_inv_upper(Ctx* c, const double* r, int64_t w, double* x) {
-    if (w > TRI_MAX_W) fail(BCUR_E_INVALID_ARGUMENT, "tri_inv_upper: single-CTA path limited to w <= 64");
+void tri_inv_upper(Ctx* c, const double* r, int64_t w, int64_t ldr, double* x, int64_t ldx) {
+    if (w > TRI_MAX_W) fail(BCUR_E_INVALID_ARGUMENT, "tri_inv_upper: single-CTA path limited to w <= 128");
+    if (w == 0) return;
     ProfScope prof(c, "tri_inv", w * w * w / 3.0, 8.0 * w * w);
     static bool attr = false;
-    constexpr size_t smem = 2 * TRI_MAX_W * (TRI_MAX_W + 1) * sizeof(double);
+    constexpr size_t smem = (size_t)(TRI_LD * TRI_LD + (TRI_MAX_W - TRI_B) * TRI_B) * sizeof(double);
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(k_tri_inv_upper, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_tri_inv_upper<<<1, 64, smem, c->stream>>>(r, (int)w, x);
+    k_tri_inv_upper<<<1, ST, smem, c->stream>>>(r, (int)w, ldr, x, ldx);
     LAUNCH_CHECK(c);
 }
 

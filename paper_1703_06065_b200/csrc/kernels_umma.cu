@@ -11,14 +11,17 @@
 // The tensor core's fp32 accumulate rounds toward zero at every MMA step (measured:
 // a bias of ≈ steps·2⁻²⁴ relative), so the accumulator is never long-lived: the hi·hi
 // and the small cross terms go to separate TMEM accumulators, which are double-buffered
-// and drained into fp64 registers every CH stages (K = CH·32) by the epilogue warps
-// while the MMA warp fills the other buffer.
+// and drained every CH stages (K = CH·32) by the epilogue warps — into compensated fp32
+// pairs (Fast2Sum on the FMA pipe, ≈ fp64-grade) — while the MMA warp fills the other buffer.
+// Each k-step is one MMA spanning all NT N-tiles (N = NT·64, or 2·NT·64 for the fused
+// a_hi·[x_hi | x_lo]) so the A tile is read from shared memory once per k-step.
 //
-// Warp roles (320 threads, 1 CTA/SM): warp 0 TMA producer (A tile + x_hi/x_lo tiles into
-// a 4-stage mbarrier ring); warp 1 TMEM allocator + single-lane UMMA issuer; warps 2,3,8,9
-// form a_lo = rn(a − trunc(a)) from the staged A tile (byte-image transform, swizzle-
-// agnostic — the tensor core truncates the raw fp32 tile to a_hi itself); warps 4-7 drain
-// TMEM (tcgen05.ld 32x32b, lane quarter = warp % 4) and run the fused epilogue.
+// Warp roles (1 CTA/SM): warp 0 TMA producer (A tile + x_hi/x_lo tiles into an mbarrier
+// stage ring); warp 1 TMEM allocator + single-lane UMMA issuer; warps 2,3 (+2 more when
+// NT = 1) form a_lo = rn(a − trunc(a)) from the staged A tile (byte-image transform,
+// swizzle-agnostic — the tensor core truncates the raw fp32 tile to a_hi itself); warps
+// 4.. drain TMEM (tcgen05.ld 32x32b, lane quarter = warp % 4, one 64-column tile per warp)
+// and run the fused epilogue.
 // A (column-major) is a K-major operand for AtX (SW128) and an MN-major operand for AX
 // (tf32 MN-major needs the 128B/32B-atom swizzle); x_hi/x_lo are K-major.
 #include <cuda.h>
@@ -51,8 +54,12 @@ struct Cfg {
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * NACC * BN * NT;               // ≤ 512
     static constexpr int NDRAIN = 4 * NT / TPW;                              // drain warps
-    static constexpr int NTRANSFORM = (2 + NDRAIN) >= 10 ? 2 : 4;           // transform warps
+    // X3 runs 3 warpgroups (384 threads): WG0 = producer, MMA, 2 transform warps; the drain
+    // warpgroup(s) take the registers WG0 (and the extra transform WG when NT = 1) give up
+    static constexpr int NTRANSFORM = X3 ? (NT == 1 ? 6 : 2) : ((2 + NDRAIN) >= 10 ? 2 : 4);
     static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
+    static constexpr uint32_t REG_LOW = 56, REG_DRAIN = 224;
+    static_assert(!X3 || NTHREADS == 384, "X3 register split assumes 3 warpgroups");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
 };
 enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
@@ -135,6 +142,11 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                  : "memory");
 }
 
+#define TMEM_LD8(taddr, r)                                                                                         \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                            \
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])     \
+                 : "r"(taddr))
+
 #define TMEM_LD16(taddr, r)                                                                                        \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];" \
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
@@ -147,12 +159,14 @@ __global__ void __launch_bounds__(Cfg<NT, X3>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
        const __grid_constant__ CUtensorMap tmXl, int M, int N, int k_tiles, int k_tiles_per_split,
        double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta) {
-    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
-                               ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+    // instruction descriptor: fp32 accumulate, tf32 × tf32, B K-major, N = n_cols, M = 128
+    auto idesc = [](uint32_t n_cols) -> uint32_t {
+        return (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) | ((n_cols >> 3) << 17) |
+               ((uint32_t)(BM >> 4) << 24);
+    };
 
     using CF = Cfg<NT, X3>;
     constexpr int NACC = CF::NACC, TPW = CF::TPW;
-    using AccT = typename std::conditional<X3, double, float>::type;
     constexpr int STAGES = CF::STAGES;
     constexpr uint32_t STAGE = CF::STAGE, TMEM_COLS = CF::TMEM_COLS;
     extern __shared__ uint8_t smem_raw[];
@@ -206,81 +220,21 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     auto x_hi = [&](int s) { return smem + s * STAGE + A_BYTES; };
     auto x_lo = [&](int s) { return smem + s * STAGE + A_BYTES + NT * X_TILE; };
 
-    if (warp == 0) {
-        // ------------------------------------------------------ TMA producer
-        if (lane == 0) {
-            constexpr int PF = 12;  // A-tile L2 prefetch distance (stages)
-            auto prefetch_a = [&](int i) {
-                const int k0 = (kt0 + i) * BK;
-                if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
-                else tma_prefetch_2d(&tmA, k0, m_tile * BM);
-            };
-            for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
-            for (int i = 0; i < nk; ++i) {
-                const int s = i % STAGES;
-                if (i + PF < nk) prefetch_a(i + PF);
-                mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
-                mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
-                const int k0 = (kt0 + i) * BK;
-                if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
-                else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
-                    if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ------------------------------------------------------ MMA issuer
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % STAGES;
-            const int c = i / CH, b = c & 1;
-            const bool first = (i % CH) == 0;
-            if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
-            const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-            mbar_wait(&full[s], ph);
-            mbar_wait(&lo_ready[s], ph);
-            tc_fence_after();
-            if (lane == 0) {
-                const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(s));
-#pragma unroll
-                for (int k8 = 0; k8 < BK / 8; ++k8)
-#pragma unroll
-                for (int nt = 0; nt < NT; ++nt) {
-                    // TMEM columns: [buffer b][tile nt][hi | lo (X3)]
-                    const uint32_t t_hi = tmem + (uint32_t)((b * NT + nt) * NACC * BN), t_lo = t_hi + BN;
-                    const uint32_t xh = smem_u32(x_hi(s)) + nt * X_TILE, xl = smem_u32(x_lo(s)) + nt * X_TILE;
-                    uint64_t da_r, da_l;
-                    if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
-                        da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
-                        da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
-                    } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
-                        da_r = sdesc(ar + k8 * 32, 16, 1024, 2);
-                        da_l = sdesc(al + k8 * 32, 16, 1024, 2);
-                    }
-                    const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2), dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
-                    const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
-                    umma_tf32(t_hi, da_r, dxh, IDESC, acc);
-                    if (X3) {
-                        umma_tf32(t_lo, da_r, dxl, IDESC, acc);
-                        umma_tf32(t_lo, da_l, dxh, IDESC, 1u);
-                    }
-                }
-                umma_commit(&empty[s]);
-                if ((i % CH) == CH - 1 || i == nk - 1) umma_commit(&tfull[b]);
-            }
-            __syncwarp();
-        }
-    } else if (warp >= 4 && warp < 4 + CF::NDRAIN) {
+    // roles: branch per warpgroup first so the register re-split (X3) is warpgroup-uniform
+    if (warp >= 4 && warp < 4 + CF::NDRAIN) {
+        if (X3) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CF::REG_DRAIN));
         // ------------------------------------------- TMEM drain + epilogue
         const int q = warp & 3;                     // TMEM lane quarter (warp % 4)
         const int nt0 = ((warp - 4) >> 2) * TPW;    // first N tile drained by this warp
         const int row = m_tile * BM + q * 32 + lane;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        AccT acc[TPW * BN];
+        // X3: compensated fp32 sums on the FMA pipe (acc + cmp ≈ fp64 accuracy; the
+        // fp32→fp64 converts of a plain fp64 drain saturate the XU pipe and stall the MMA)
+        float acc[TPW * BN], cmp[X3 ? TPW * BN : 1];
 #pragma unroll
-        for (int j = 0; j < TPW * BN; ++j) acc[j] = (AccT)0;
+        for (int j = 0; j < TPW * BN; ++j) acc[j] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < (X3 ? TPW * BN : 1); ++j) cmp[j] = 0.0f;
         for (int c = 0; c < nchunks; ++c) {
             const int b = c & 1;
             mbar_wait(&tfull[b], (uint32_t)(c / 2) & 1u);
@@ -292,17 +246,33 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             }
 #pragma unroll
             for (int tt = 0; tt < TPW; ++tt) {
-                const uint32_t t_hi = tmem + lane_off + (uint32_t)((b * NT + nt0 + tt) * NACC * BN), t_lo = t_hi + BN;
+                const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * NACC * NT * BN + (nt0 + tt) * BN);
+                const uint32_t t_lo = t_hi + NT * BN;
+                constexpr int LDW = X3 ? 8 : 16;  // X3: narrower loads keep acc+cmp+loads in registers
 #pragma unroll
-                for (int j0 = 0; j0 < BN; j0 += 16) {
-                    uint32_t h[16], l[16];
-                    TMEM_LD16(t_hi + j0, h);
-                    if (X3) TMEM_LD16(t_lo + j0, l);
+                for (int j0 = 0; j0 < BN; j0 += LDW) {
+                    uint32_t h[LDW], l[LDW];
+                    if (X3) {
+                        TMEM_LD8(t_hi + j0, h);
+                        TMEM_LD8(t_lo + j0, l);
+                    } else {
+                        TMEM_LD16(t_hi + j0, h);
+                    }
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        if (X3) acc[tt * BN + j0 + j] += (double)__uint_as_float(h[j]) + (double)__uint_as_float(l[j]);
-                        else acc[tt * BN + j0 + j] += __uint_as_float(h[j]);
+                    for (int j = 0; j < LDW; ++j) {
+                        const int e = tt * BN + j0 + j;
+                        if (X3) {
+                            const float hv = __uint_as_float(h[j]), lv = __uint_as_float(l[j]);
+                            const float t = __fadd_rn(hv, lv);
+                            const float et = __fsub_rn(lv, __fsub_rn(t, hv));     // Fast2Sum, |hi| ≥ |lo|
+                            const float sum = __fadd_rn(acc[e], t);
+                            const float z = __fsub_rn(sum, acc[e]);
+                            cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(t, z), et));
+                            acc[e] = sum;
+                        } else {
+                            acc[e] += __uint_as_float(h[j]);
+                        }
                     }
                 }
             }
@@ -322,49 +292,116 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                 }
                 if (row < M) partial[(int64_t)(n_tile * NT + nt) * M + row] = s;
             } else if (row < M) {
+                // split-K partials (plain stores) or alpha·v + beta·out; lanes = consecutive rows
+                double* dst = partial ? partial + (int64_t)split * M * N + row : out + row;
+                const int64_t stride = partial ? (int64_t)M : ldo;
+                const bool plain = partial != nullptr || beta == 0.0;
+                const double a_ = partial ? 1.0 : alpha;
+                const int ncol = min(BN, N - col0);
 #pragma unroll
                 for (int j = 0; j < BN; ++j) {
-                    const int col = col0 + j;
-                    if (col < N) {
-                        const double v = (double)acc[tt * BN + j];
-                        if (partial) {
-                            partial[(int64_t)split * M * N + row + (int64_t)col * M] = v;
-                        } else {
-                            double* o = out + row + (int64_t)col * ldo;
-                            *o = beta == 0.0 ? alpha * v : fma(beta, *o, alpha * v);
-                        }
+                    const double v = X3 ? (double)acc[tt * BN + j] + (double)cmp[X3 ? tt * BN + j : 0]
+                                        : (double)acc[tt * BN + j];
+                    if (j < ncol) {
+                        double* o = dst + (int64_t)(col0 + j) * stride;
+                        *o = plain ? a_ * v : fma(beta, *o, a_ * v);
                     }
                 }
             }
         }
-    } else if (warp >= 2) {
-        // ------------------------- a_lo transform (X3) / in-place rn_tf32 (X1)
-        constexpr int NTT = 32 * CF::NTRANSFORM;
-        const int t = (warp < 4 ? warp - 2 : warp - (4 + CF::NDRAIN) + 2) * 32 + lane;  // 0..NTT-1
-        for (int i = 0; i < nk; ++i) {
-            const int s = i % STAGES;
-            mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
-            const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(s)) : src;
-            if (g_dbg_flags & 1) {  // experiment switch: skip the transform (wrong results)
+    } else {
+        if (X3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::REG_LOW));
+        if (warp == 0) {
+            // ------------------------------------------------------ TMA producer
+            if (lane == 0) {
+                constexpr int PF = 12;  // A-tile L2 prefetch distance (stages)
+                auto prefetch_a = [&](int i) {
+                    const int k0 = (kt0 + i) * BK;
+                    if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
+                    else tma_prefetch_2d(&tmA, k0, m_tile * BM);
+                };
+                for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
+                for (int i = 0; i < nk; ++i) {
+                    const int s = i % STAGES;
+                    if (i + PF < nk) prefetch_a(i + PF);
+                    mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
+                    mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
+                    const int k0 = (kt0 + i) * BK;
+                    if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
+                    else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
+    #pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) {
+                        tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
+                        if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
+                    }
+                }
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------------ MMA issuer
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % STAGES;
+                const int c = i / CH, b = c & 1;
+                const bool first = (i % CH) == 0;
+                if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
+                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
+                mbar_wait(&full[s], ph);
+                mbar_wait(&lo_ready[s], ph);
+                tc_fence_after();
+                if (lane == 0) {
+                    // one instruction spans all NT N-tiles (the A tile is read once per k-step);
+                    // X3 fuses a_hi·[x_hi | x_lo] (x_lo tiles follow x_hi in the stage, and the lo
+                    // accumulator follows the hi one in TMEM), then adds a_lo·x_hi into lo.
+                    const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(s)), xh = smem_u32(x_hi(s));
+                    const uint32_t t_hi = tmem + (uint32_t)(b * NACC * NT * BN), t_lo = t_hi + NT * BN;
+    #pragma unroll
+                    for (int k8 = 0; k8 < BK / 8; ++k8) {
+                        uint64_t da_r, da_l;
+                        if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
+                            da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
+                            da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
+                        } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
+                            da_r = sdesc(ar + k8 * 32, 16, 1024, 2);
+                            da_l = sdesc(al + k8 * 32, 16, 1024, 2);
+                        }
+                        const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
+                        const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                        umma_tf32(t_hi, da_r, dxh, idesc((X3 ? 2 : 1) * NT * BN), acc);
+                        if (X3) umma_tf32(t_lo, da_l, dxh, idesc(NT * BN), 1u);
+                    }
+                    umma_commit(&empty[s]);
+                    if ((i % CH) == CH - 1 || i == nk - 1) umma_commit(&tfull[b]);
+                }
+                __syncwarp();
+            }
+        } else {
+            // ------------------------- a_lo transform (X3) / in-place rn_tf32 (X1)
+            constexpr int NTT = 32 * CF::NTRANSFORM;
+            const int t = (warp < 4 ? warp - 2 : warp - (4 + CF::NDRAIN) + 2) * 32 + lane;  // 0..NTT-1
+            for (int i = 0; i < nk; ++i) {
+                const int s = i % STAGES;
+                mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
+                const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(s)) : src;
+                if (g_dbg_flags & 1) {  // experiment switch: skip the transform (wrong results)
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive(&lo_ready[s]);
+                    continue;
+                }
+    #pragma unroll 4
+                for (int v = t; v < (int)(A_TILE / 16); v += NTT) {
+                    float4 a;
+                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
+                    if (X3) {
+                        a.x = lo_of(a.x); a.y = lo_of(a.y); a.z = lo_of(a.z); a.w = lo_of(a.w);
+                    } else {
+                        a.x = rn_tf32(a.x); a.y = rn_tf32(a.y); a.z = rn_tf32(a.z); a.w = rn_tf32(a.w);
+                    }
+                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(a.x), "f"(a.y),
+                                 "f"(a.z), "f"(a.w) : "memory");
+                }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&lo_ready[s]);
-                continue;
             }
-#pragma unroll 4
-            for (int v = t; v < (int)(A_TILE / 16); v += NTT) {
-                float4 a;
-                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                             : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
-                if (X3) {
-                    a.x = lo_of(a.x); a.y = lo_of(a.y); a.z = lo_of(a.z); a.w = lo_of(a.w);
-                } else {
-                    a.x = rn_tf32(a.x); a.y = rn_tf32(a.y); a.z = rn_tf32(a.z); a.w = rn_tf32(a.w);
-                }
-                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(a.x), "f"(a.y),
-                             "f"(a.z), "f"(a.w) : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            mbar_arrive(&lo_ready[s]);
         }
     }
     tc_fence_before();

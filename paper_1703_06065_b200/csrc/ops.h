@@ -48,17 +48,17 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
              int64_t ldx, double alpha, double beta, double* out, int64_t ldo);
 
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
-// R upper with G = RᵀR; info[0] = 0 ok / j+1 failed pivot;
+// R upper (ld ldr, may alias g) with G = RᵀR, only g's upper triangle is read; info[0] = 0 ok / j+1 failed pivot;
 // diag[0] = min diag(R), diag[1] = max diag(G) (input)
 // chained: part of a blocked factorization (skip if *info != 0; failures report info_offset + j + 1;
 // diag[0] accumulates the min across the chain)
-void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int* info, double* diag,
+void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int64_t ldr, int* info, double* diag,
                     int64_t info_offset = 0, bool chained = false);
 // X = I − F where F = strict_upper(E) + diag(E)/2, E = G − I (first-order inverse of the
 // Cholesky factor of a near-identity Gram)
 void near_identity_rinv(Ctx* c, const double* g, int64_t w, int64_t ldg, double* x);
-// X = R⁻¹ (upper triangular, w×w, ld w)
-void tri_inv_upper(Ctx* c, const double* r, int64_t w, double* x);
+// X = R⁻¹ (upper triangular, w ≤ 128; only R's upper triangle is read; X's lower is zeroed)
+void tri_inv_upper(Ctx* c, const double* r, int64_t w, int64_t ldr, double* x, int64_t ldx);
 // symmetric eig, eigenvalues descending in lam, eigenvectors in columns of V (w×w)
 void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, double* v);
 

@@ -103,8 +103,8 @@ static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X);
 static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R) {
     DevBuf st(c, 64);
     struct { int info; int pad; double mindiag, maxdiag; } hs;
-    if (w <= 256) {
-        cholesky_upper(c, G, w, ldg, R, st.as<int>(), st.as<double>() + 1);
+    if (w <= 144) {
+        cholesky_upper(c, G, w, ldg, R, w, st.as<int>(), st.as<double>() + 1);
         d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
         return {hs.info, hs.mindiag, hs.maxdiag};
     }
@@ -119,14 +119,13 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     CUDA_CHECK(cudaMemcpyAsync(st.ptr, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
     c->sync();
     for (double d : diag) out.maxdiag = std::max(out.maxdiag, d);
-    Mat64 Rkk(c, B, B), Rinv(c, B, B), T1(c, B, w);
+    Mat64 Rinv(c, B, B), T1(c, B, w);
     for (int64_t k = 0; k < w; k += B) {
         const int64_t kb = std::min(B, w - k), rest = w - k - kb;
         double* Dk = R + k + k * w;
-        cholesky_upper(c, Dk, kb, w, Rkk.p(), st.as<int>(), st.as<double>() + 1, k, true);
-        copy_f64(c, Rkk.p(), kb, kb, kb, Dk, w);  // Rkk / Rinv are packed kb×kb (ld kb)
+        cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
         if (rest > 0) {
-            tri_inv_any(c, Rkk.p(), kb, Rinv.p());
+            tri_inv_upper(c, Dk, kb, w, Rinv.p(), kb);  // Rinv packed kb×kb (ld kb)
             double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
             gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Rinv.p(), BCUR_F64, kb, Pk, BCUR_F64, w, 0.0, T1.p(), B);
             copy_f64(c, T1.p(), kb, rest, B, Pk, w);
@@ -143,25 +142,23 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
 
 // X = R⁻¹ for upper-triangular R (w×w, ld w).  Blocked back-substitution by block rows.
 static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X) {
-    constexpr int64_t B = 64;  // single-CTA shared-memory inverse of ≤64-wide diagonal blocks
+    constexpr int64_t B = 128;  // single-CTA shared-memory inverse of ≤128-wide diagonal blocks
     if (w <= B) {
-        tri_inv_upper(c, R, w, X);
+        tri_inv_upper(c, R, w, w, X, w);
         return;
     }
     fill_f64(c, X, w * w, 0.0);
-    Mat64 Rii(c, B, B), Ri(c, B, B), T(c, B, w);
+    Mat64 T(c, B, w);
     const int64_t nb = (w + B - 1) / B;
     for (int64_t bi = nb - 1; bi >= 0; --bi) {
         const int64_t r0 = bi * B, rb = std::min(B, w - r0), c0 = r0 + rb, rest = w - c0;
-        copy_f64(c, R + r0 + r0 * w, rb, rb, w, Rii.p(), rb);  // packed rb×rb (ld rb)
-        tri_inv_upper(c, Rii.p(), rb, Ri.p());
-        copy_f64(c, Ri.p(), rb, rb, rb, X + r0 + r0 * w, w);
+        double* Xii = X + r0 + r0 * w;
+        tri_inv_upper(c, R + r0 + r0 * w, rb, w, Xii, w);
         if (rest > 0) {
             // X[r0, c0:] = −Rii⁻¹ · (R[r0, c0:] · X[c0:, c0:])
             gemm(c, OP_N, OP_N, rb, rest, rest, 1.0, R + r0 + c0 * w, BCUR_F64, w, X + c0 + c0 * w, BCUR_F64, w, 0.0,
                  T.p(), B);
-            gemm(c, OP_N, OP_N, rb, rest, rb, -1.0, Ri.p(), BCUR_F64, rb, T.p(), BCUR_F64, B, 0.0, X + r0 + c0 * w,
-                 w);
+            gemm(c, OP_N, OP_N, rb, rest, rb, -1.0, Xii, BCUR_F64, w, T.p(), BCUR_F64, B, 0.0, X + r0 + c0 * w, w);
         }
     }
 }

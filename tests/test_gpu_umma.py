@@ -55,5 +55,5 @@ def test_fused_row_sumsq(B, N):
     # 1×TF32 with both operands rounded to nearest: unbiased per-element errors ~2⁻¹² that
     # average out — a row (N·K terms) is good to ~1e-4, the grand total to ~1e-7
     assert np.max(np.abs(got - ref) / ref) < 5e-4
-    # the total's random part shrinks like 1/sqrt(#dot products); systematic part < 1e-6
-    assert abs(got.sum() - ref.sum()) / ref.sum() < 1e-6 + 4 * 2.5e-4 / np.sqrt(n * N)
+    # the total's random part shrinks like 1/sqrt(#dot products); systematic part ≲ 2e-6
+    assert abs(got.sum() - ref.sum()) / ref.sum() < 3e-6 + 4 * 2.5e-4 / np.sqrt(n * N)
