@@ -54,12 +54,16 @@ struct Cfg {
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
     static constexpr uint32_t TMEM_COLS = 2 * NACC * BN * NT;               // ≤ 512
     static constexpr int NDRAIN = 4 * NT / TPW;                              // drain warps
-    // X3 runs 3 warpgroups (384 threads): WG0 = producer, MMA, 2 transform warps; the drain
-    // warpgroup(s) take the registers WG0 (and the extra transform WG when NT = 1) give up
-    static constexpr int NTRANSFORM = X3 ? (NT == 1 ? 6 : 2) : ((2 + NDRAIN) >= 10 ? 2 : 4);
+    // X3 runs whole warpgroups: WG0 = producer, MMA, 2 transform warps; NT drain warpgroups;
+    // one more transform warpgroup (the a_lo split is the MMA's feeder).  The drain
+    // warpgroups take the registers the others give up (setmaxnreg).
+    static constexpr int NTRANSFORM = X3 ? 6 : ((2 + NDRAIN) >= 10 ? 2 : 4);
     static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
-    static constexpr uint32_t REG_LOW = 56, REG_DRAIN = 224;
-    static_assert(!X3 || NTHREADS == 384, "X3 register split assumes 3 warpgroups");
+    static constexpr uint32_t REG_LOW = 56;
+    static constexpr uint32_t REG_DRAIN = NT == 1 ? 224 : 200;
+    static_assert(!X3 || (NTHREADS % 128 == 0 &&
+                          (NTHREADS - 32 * NDRAIN) * REG_LOW + 32 * NDRAIN * REG_DRAIN <= 65536),
+                  "X3 register split");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
 };
 enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
