@@ -137,28 +137,16 @@ def bench_b200(args, cfg, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     ctx = B.Context(local_rank)
+    from paper_1703_06065_b200 import dist as BD
+
     dist = None
     if world > 1:
         import torch.distributed as dist
-
-        class Cai:
-            def __init__(self, ptr, count):
-                self.__cuda_array_interface__ = {"shape": (count,), "typestr": "<f8", "data": (ptr, False),
-                                                 "version": 3, "strides": None}
-
-        def allreduce(ptr, count, stream):
-            t = torch.as_tensor(Cai(ptr, count), device=f"cuda:{local_rank}")
-            with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=f"cuda:{local_rank}")):
-                dist.all_reduce(t)
-
-        ctx.set_comm(rank, world, allreduce)
+        BD.attach(ctx, rank, world, device=f"cuda:{local_rank}")
 
     m, n, s = cfg["m"], cfg["n"], cfg["s"]
     G = n // s
-    if G % world:
-        raise SystemExit(f"{G} blocks do not split evenly over {world} ranks")
-    n_local = n // world
-    col0 = rank * n_local
+    col0, n_local, _, _ = BD.shard_columns(np.arange(G + 1, dtype=np.int64) * s, rank, world)
     dt = np.float32 if cfg["dtype"] == "f32" else np.float64
     t0 = time.time()
     if cfg["kind"] == "lowrank":
@@ -207,8 +195,14 @@ def bench_b200(args, cfg, rank, world, local_rank):
     for _ in range(args.warmup):
         run_step(B, cfg, dm, part, rpart, ctx)
     with ClockSampler(local_rank) as clk:
-        ms, res, prof, launches = timed(lambda: run_step(B, cfg, dm, part, rpart, ctx), args.steps, profile=True)
+        ms, res, _, launches = timed(lambda: run_step(B, cfg, dm, part, rpart, ctx), args.steps)
     rel_err, blocks = res
+    # per-kernel-class breakdown (CUDA events on the library stream) in a separate pass,
+    # so the event records do not perturb the headline timing
+    prof_steps = max(1, min(2, args.steps))
+    _, _, prof, _ = timed(lambda: run_step(B, cfg, dm, part, rpart, ctx), prof_steps, profile=True)
+    prof = {t: dict(v, ms=v["ms"] / prof_steps, scopes=v["scopes"] / prof_steps, flops=v["flops"] / prof_steps,
+                    bytes=v["bytes"] / prof_steps) for t, v in (prof or {}).items()}
 
     # e2e: the public API with host buffers — pinned A shard uploaded every step
     host = torch.empty((n_local, m), dtype=torch.float32 if dt == np.float32 else torch.float64, pin_memory=True)
@@ -231,7 +225,7 @@ def bench_b200(args, cfg, rank, world, local_rank):
     line = None
     if rank == 0:
         peaks = measured_peaks()
-        roof = roofline(prof, peaks)
+        roof = roofline(prof, peaks, ncu_traffic(args.config))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -244,7 +238,7 @@ def bench_b200(args, cfg, rank, world, local_rank):
             "rel_err": rel_err, "selected_blocks": blocks[:16],
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h_bytes(cfg, G) * world, "ms_per_step": ms_e2e / e2e_steps},
-            "gpu_launches": launches, "roofline": roof, "kernels": prof,
+            "gpu_launches": launches, "roofline": roof, "kernels_per_step": prof,
             "clocks": clk.summary(), "generate_s": gen_s,
         }
     return line
@@ -254,22 +248,42 @@ def kernel_tags(prof):
     return {t: v for t, v in (prof or {}).items() if not t.startswith(("phase:", "_"))}
 
 
-def roofline(prof, peaks):
+def ncu_traffic(workload):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of each
+    kernel class from the latest committed `ncu --set full` capture, if any."""
+    import glob
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
+        with open(path) as f:
+            d = json.load(f)
+        return {t: v for t, v in d.get(workload, {}).items()}, os.path.relpath(path, ROOT)
+    return {}, None
+
+
+def roofline(prof, peaks, traffic=({}, None)):
+    """Dominant kernel class of the step: algorithmic work per launch ÷ its mean launch
+    time (CUDA events on the launching stream), against the measured peak."""
     prof = kernel_tags(prof)
     if not prof:
         return None
     tag, d = max(prof.items(), key=lambda kv: kv[1]["ms"])
     total = sum(v["ms"] for v in prof.values())
-    avg_ms = d["ms"] / max(d["scopes"], 1)
+    launches = max(d["scopes"], 1)
+    avg_ms = d["ms"] / launches
+    tr, tr_src = traffic
+    common = {"kernel": tag, "share_of_step": d["ms"] / total, "avg_launch_ms": avg_ms,
+              "launches_per_step": d["scopes"], "traffic_source": tr_src,
+              "algorithmic_bytes_per_launch": d["bytes"] / launches,
+              "algorithmic_flops_per_launch": d["flops"] / launches}
     if d["flops"] > 0 and d["flops"] / max(d["bytes"], 1) > 60:
         achieved = d["flops"] / (d["ms"] / 1e3) / 1e12
-        return {"kernel": tag, "bound": "tensor", "achieved": achieved, "peak": peaks["tensor"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["tensor"], "traffic": None, "share_of_step": d["ms"] / total,
-                "avg_launch_ms": avg_ms, "peak_source": peaks["source"] + " bf16_tflops_sustained"}
+        return dict(common, bound="tensor", achieved=achieved, peak=peaks["tensor"], unit="TFLOP/s",
+                    frac=achieved / peaks["tensor"], traffic=tr.get(tag),
+                    frac_of_tf32_peak=achieved / (peaks["tensor"] / 2.0),
+                    peak_source=peaks["source"] + " bf16_tflops_sustained (the kernel computes in TF32: "
+                                                  "dense TF32 rate = bf16/2, reported as frac_of_tf32_peak)")
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
-    return {"kernel": tag, "bound": "hbm", "achieved": achieved, "peak": peaks["hbm"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm"], "traffic": None, "share_of_step": d["ms"] / total,
-            "avg_launch_ms": avg_ms, "peak_source": peaks["source"] + " hbm_gbs"}
+    return dict(common, bound="hbm", achieved=achieved, peak=peaks["hbm"], unit="GB/s",
+                frac=achieved / peaks["hbm"], traffic=tr.get(tag), peak_source=peaks["source"] + " hbm_gbs")
 
 
 # ------------------------------------------------------------ CPU baseline

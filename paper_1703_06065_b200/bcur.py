@@ -142,19 +142,26 @@ class Context:
             self._comm = None
             return
 
-        def cb(user, buf, count, stream):
-            try:
-                allreduce_fn(C.cast(buf, C.c_void_p).value, int(count), stream or 0)
-                return 0
-            except Exception:  # reported to the library as BCUR_E_COMM
-                import traceback
-                traceback.print_exc()
-                return 1
-
-        fn = L.ALLREDUCE_FN(cb)
+        fn = make_comm_callback(allreduce_fn)
         comm = L.CommC(rank, world, None, fn)
         _check(L.lib.bcur_ctx_set_comm(self.handle, C.byref(comm)))
         self._comm = (fn, comm)  # keep alive
+
+
+def make_comm_callback(allreduce_fn):
+    """C function pointer for ``bcur_comm.allreduce_f64`` wrapping a Python
+    ``allreduce_fn(ptr, count, stream)``; exceptions become a nonzero return, which the
+    library reports as BCUR_E_COMM."""
+    def cb(user, buf, count, stream):
+        try:
+            allreduce_fn(C.cast(buf, C.c_void_p).value, int(count), stream or 0)
+            return 0
+        except Exception:
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    return L.ALLREDUCE_FN(cb)
 
 
 _default_ctx: Optional[Context] = None
