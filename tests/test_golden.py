@@ -105,9 +105,11 @@ def _gen(B, g, dt):
         a = B.DeviceMatrix.generate("lowrank", dt, g["m"], g["n"], seed=g.get("data_seed", g["seed"]), sigma=sig,
                                     noise=g["noise"])
     h = a.to_host().astype(np.float64)
-    # the device generator is bit-identical to the oracle's (Philox, fma-only): checksums match
+    # the device generator reproduces the oracle's (same Philox streams; the factor
+    # orthonormalization rounds differently in the last bits of fp64)
     assert float(np.sum(h * h)) == pytest.approx(d(g["a"]["sumsq"]), rel=1e-12)
-    assert float(h[0, 0]) == d(g["a"]["corner"][0]) and float(h[-1, -1]) == d(g["a"]["corner"][1])
+    for got, ref in ((h[0, 0], g["a"]["corner"][0]), (h[-1, -1], g["a"]["corner"][1])):
+        assert float(got) == pytest.approx(d(ref), rel=1e-12, abs=1e-15)
     return a
 
 
