@@ -213,16 +213,17 @@ void dispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, i
 namespace ops {
 
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
-          const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc) {
+          const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags) {
     if (M <= 0 || N <= 0) return;
     // fp32 A-passes → tcgen05 3×TF32 kernels
     if (dta == BCUR_F32 && K > 0 && tb == OP_N) {
         if (ta == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {
-            umma_ax(c, (const float*)A, M, K, lda, B, dtb, N, ldb, alpha, beta, C, ldc);
+            umma_ax(c, (const float*)A, M, K, lda, B, dtb, N, ldb, alpha, beta, C, ldc, (flags & GEMM_B_UPPER) != 0);
             return;
         }
         if (ta == OP_T && umma_ok(dta, K, lda, A)) {
-            umma_atx(c, (const float*)A, K, M, lda, B, dtb, N, ldb, alpha, beta, C, ldc, nullptr);
+            const bool sym = (flags & GEMM_SYM_UPPER) && A == B && dta == dtb && lda == ldb && M == N && beta == 0.0;
+            umma_atx(c, (const float*)A, K, M, lda, B, dtb, N, ldb, alpha, beta, C, ldc, nullptr, sym);
             return;
         }
     }

@@ -134,7 +134,7 @@ __global__ void k_max_dev_identity(const double* __restrict__ g, int w, int64_t 
     double mx = 0.0;
     for (int j = blockIdx.x * nw + warp; j < w; j += gridDim.x * nw) {
         const double* col = g + (int64_t)j * ld;
-        for (int i = lane; i < w; i += 32) {
+        for (int i = lane; i <= j; i += 32) {  // upper triangle (G is symmetric; Grams may hold only it)
             const double d = fabs(col[i] - (i == j ? 1.0 : 0.0));
             mx = d > mx || d != d ? d : mx;
         }

@@ -33,7 +33,8 @@ namespace bcur_b200 {
 namespace {
 
 constexpr int BM = 128, BK = 32, BN = 64, CH = 2;
-__device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, bit 1 skip drain (timing experiments)
+__device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, bit 1 skip drain, bit 2 skip MMAs (timing experiments)
+bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 
@@ -48,22 +49,35 @@ constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 template <int NT, bool X3>
 struct Cfg {
     static constexpr int NACC = X3 ? 2 : 1;                                  // accumulators per tile
-    static constexpr int TPW = 1;                                            // tiles per drain warp
-    static constexpr uint32_t STAGE = (X3 ? 2 : 1) * A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
-    static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
-    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 2 * NACC * BN * NT;               // ≤ 512
-    static constexpr int NDRAIN = 4 * NT / TPW;                              // drain warps
+    static constexpr uint32_t BUFCOLS = NACC * BN * NT;                     // per drain buffer
+    static constexpr int DCOLS = 64;                                         // output columns per drain warp
+    // TMA stage = {a_raw, x_hi[NT], x_lo[NT] (X3)}; the a_lo split (X3) lives in its own
+    // LO_SLOTS-deep ring so the TMA ring keeps as many stages in flight as fit (the
+    // HBM-bound passes need ≥ 6 × 16 KB of A in flight per SM).
+    static constexpr int LO_SLOTS = X3 ? 2 : 0;
+    static constexpr uint32_t STAGE = A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
+    static constexpr int STAGES_FIT = (int)((232448u - 1280u - LO_SLOTS * A_TILE) / STAGE);
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int LOR = X3 ? LO_SLOTS : STAGES;  // lo_ready barriers
+    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + LO_SLOTS * A_TILE + 1024 + 256;
+    static constexpr uint32_t TMEM_COLS = 2 * BUFCOLS;                      // ≤ 512
+    static constexpr int NDRAIN = 4 * NT * (BN / DCOLS);                     // drain warps
     // X3 runs whole warpgroups: WG0 = producer, MMA, 2 transform warps; NT drain warpgroups;
     // one more transform warpgroup (the a_lo split is the MMA's feeder).  The drain
     // warpgroups take the registers the others give up (setmaxnreg).
-    static constexpr int NTRANSFORM = X3 ? 6 : ((2 + NDRAIN) >= 10 ? 2 : 4);
+    static constexpr int NTRANSFORM = (X3 || NT <= 2) ? 6 : 2;
     static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
     static constexpr uint32_t REG_LOW = 56;
-    static constexpr uint32_t REG_DRAIN = NT == 1 ? 224 : 200;
-    static_assert(!X3 || (NTHREADS % 128 == 0 &&
-                          (NTHREADS - 32 * NDRAIN) * REG_LOW + 32 * NDRAIN * REG_DRAIN <= 65536),
-                  "X3 register split");
+    // setmaxnreg moves registers only inside the CTA's launch allocation: every thread starts
+    // with ptxas's cap R0 = ⌊65536 / NTHREADS⌋ (multiple of 8); the drains may grow by what the
+    // other warpgroups release (an .inc that asks for more blocks forever).
+    static constexpr uint32_t R0 = (65536u / NTHREADS) / 8 * 8;
+    static constexpr uint32_t REG_DRAIN_FIT =
+        R0 + ((NTHREADS - 32 * NDRAIN) * (R0 - REG_LOW) / (32 * NDRAIN)) / 8 * 8;
+    static constexpr uint32_t REG_DRAIN = REG_DRAIN_FIT > 232 ? 232 : REG_DRAIN_FIT;
+    static_assert(!X3 || (NTHREADS % 128 == 0 && R0 > REG_LOW &&
+                          (NTHREADS - 32 * NDRAIN) * (R0 - REG_LOW) >= 32 * NDRAIN * (REG_DRAIN - R0)),
+                  "X3 register split must fit the launch allocation");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
 };
 enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
@@ -141,6 +155,25 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint6
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
         "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// Whole-warp issue: every lane computes the same (uniform) descriptors and elect.sync
+// picks the issuing lane inside the asm — a lane-0-only branch makes the compiler wrap
+// each MMA in an ELECT/R2UR.BROADCAST waterfall (~56 cycles per instruction).
+__device__ __forceinline__ void umma_tf32_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
+        "}" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -158,10 +191,61 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
                    "=r"(r[15])                                                                                     \
                  : "r"(taddr))
 
+// Persistent tile schedule.  Tiles are (m_tile, n_tile, split); consecutive tiles walk
+// group_n N tiles side by side, then the next M tile, so a wave of CTAs streams a band
+// of A tiles and a band of X tiles together and both are served from L2 (a plain grid
+// lets CTAs drift apart and re-streams the operands from HBM: 130 GB for a 4.3 GB pass).
+//   sym:   Out = AᵀA — only tiles with n ≥ m (the upper triangle) are enumerated.
+//   tri_x: X is upper triangular (X[k, j] = 0 for k > j) — each N tile stops at its diagonal.
+//   wave_ctr: a wave barrier — a CTA's producer starts tile wave w+1 only after every CTA
+//   has issued its wave-w loads, so a wave's CTAs stay in lockstep along K and share the
+//   A and X bands through L2 (cooperative launch guarantees co-residency).
+struct Sched {
+    int m_tiles, n_tiles, splits, group_n, total;
+    int k_tiles, kps, sym, tri_x;
+    unsigned int* wave_ctr;
+};
+// CTAs that have a tile in waves 0..w
+__device__ __forceinline__ unsigned int wave_arrivals(const Sched& sc, int w) {
+    const int g = gridDim.x;
+    unsigned int s = 0;
+    for (int v = 0; v <= w; ++v) s += (unsigned int)max(0, min(g, sc.total - v * g));
+    return s;
+}
+struct TileInfo {
+    int m_tile, n_tile, split, kt0, nk;
+};
+template <int NT>
+__device__ __forceinline__ TileInfo tile_info(const Sched& sc, int t) {
+    TileInfo ti;
+    const int per_split = sc.sym ? sc.n_tiles * (sc.n_tiles + 1) / 2 : sc.m_tiles * sc.n_tiles;
+    ti.split = t / per_split;
+    const int r = t - ti.split * per_split;
+    if (sc.sym) {  // r = n(n+1)/2 + m, m ≤ n
+        int n = (int)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
+        while ((n + 1) * (n + 2) / 2 <= r) ++n;
+        while (n * (n + 1) / 2 > r) --n;
+        ti.n_tile = n;
+        ti.m_tile = r - n * (n + 1) / 2;
+    } else {
+        const int gsz = sc.group_n * sc.m_tiles;
+        const int g = r / gsz, first_n = g * sc.group_n;
+        const int gn = min(sc.group_n, sc.n_tiles - first_n);
+        const int rr = r - g * gsz;
+        ti.n_tile = first_n + rr % gn;
+        ti.m_tile = rr / gn;
+    }
+    ti.kt0 = ti.split * sc.kps;
+    int kt1 = min(sc.k_tiles, ti.kt0 + sc.kps);
+    if (sc.tri_x) kt1 = min(kt1, ((ti.n_tile + 1) * NT * BN + BK - 1) / BK);
+    ti.nk = max(kt1 - ti.kt0, 0);
+    return ti;
+}
+
 template <bool A_MN, int EPI, int NT, bool X3>
 __global__ void __launch_bounds__(Cfg<NT, X3>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
-       const __grid_constant__ CUtensorMap tmXl, int M, int N, int k_tiles, int k_tiles_per_split,
+       const __grid_constant__ CUtensorMap tmXl, int M, int N, const Sched sc,
        double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta) {
     // instruction descriptor: fp32 accumulate, tf32 × tf32, B K-major, N = n_cols, M = 128
     auto idesc = [](uint32_t n_cols) -> uint32_t {
@@ -170,34 +254,32 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     };
 
     using CF = Cfg<NT, X3>;
-    constexpr int NACC = CF::NACC, TPW = CF::TPW;
+    constexpr int NACC = CF::NACC;
+    constexpr uint32_t BUFCOLS = CF::BUFCOLS;
     constexpr int STAGES = CF::STAGES;
     constexpr uint32_t STAGE = CF::STAGE, TMEM_COLS = CF::TMEM_COLS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE);
-    uint64_t* full = bars;
-    uint64_t* lo_ready = bars + STAGES;
-    uint64_t* empty = bars + 2 * STAGES;
-    uint64_t* tfull = bars + 3 * STAGES;       // [2]
-    uint64_t* tempty = bars + 3 * STAGES + 2;  // [2]
-    uint32_t* tmem_slot = (uint32_t*)(bars + 3 * STAGES + 4);
+    constexpr int LO_SLOTS = CF::LO_SLOTS, LOR = CF::LOR;
+    uint64_t* bars = (uint64_t*)(smem + STAGES * STAGE + LO_SLOTS * A_TILE);
+    uint64_t* full = bars;                                   // [STAGES] TMA bytes landed
+    uint64_t* empty = full + STAGES;                         // [STAGES] MMAs done with the stage
+    uint64_t* lo_ready = empty + STAGES;                     // [LOR]   a_lo (X3) / rn (X1) written
+    uint64_t* lo_empty = lo_ready + LOR;                     // [LO_SLOTS] MMAs done with the a_lo slot
+    uint64_t* tfull = lo_empty + LO_SLOTS;                   // [2]
+    uint64_t* tempty = tfull + 2;                            // [2]
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int m_tile, n_tile, split;
-    if (A_MN) { m_tile = blockIdx.x; n_tile = blockIdx.y; split = blockIdx.z; }
-    else { n_tile = blockIdx.x; m_tile = blockIdx.y; split = 0; }
-    const int kt0 = split * k_tiles_per_split;
-    const int kt1 = min(k_tiles, kt0 + k_tiles_per_split);
-    const int nk = max(kt1 - kt0, 0);
-    const int nchunks = (nk + CH - 1) / CH;
+    const int dbg = g_dbg_flags;  // read once (a per-stage global load sat on the transform's critical path)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&lo_ready[s], 32 * CF::NTRANSFORM);
             mbar_init(&empty[s], 1);
         }
+        for (int s = 0; s < LOR; ++s) mbar_init(&lo_ready[s], 32 * CF::NTRANSFORM);
+        for (int s = 0; s < LO_SLOTS; ++s) mbar_init(&lo_empty[s], 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 32 * CF::NDRAIN);
@@ -217,101 +299,104 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // per stage: [a_raw][a_lo (X3)][x_hi tile 0..NT-1][x_lo tile 0..NT-1 (X3)]
-    constexpr uint32_t A_BYTES = (X3 ? 2 : 1) * A_TILE;
+    // per stage: [a_raw][x_hi tile 0..NT-1][x_lo tile 0..NT-1 (X3)]; then the a_lo slots
     auto a_raw = [&](int s) { return smem + s * STAGE; };
-    auto a_lo = [&](int s) { return smem + s * STAGE + A_TILE; };
-    auto x_hi = [&](int s) { return smem + s * STAGE + A_BYTES; };
-    auto x_lo = [&](int s) { return smem + s * STAGE + A_BYTES + NT * X_TILE; };
+    auto x_hi = [&](int s) { return smem + s * STAGE + A_TILE; };
+    auto x_lo = [&](int s) { return smem + s * STAGE + A_TILE + NT * X_TILE; };
+    auto a_lo = [&](int l) { return smem + STAGES * STAGE + l * A_TILE; };
 
     // roles: branch per warpgroup first so the register re-split (X3) is warpgroup-uniform
     if (warp >= 4 && warp < 4 + CF::NDRAIN) {
         if (X3) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CF::REG_DRAIN));
         // ------------------------------------------- TMEM drain + epilogue
-        const int q = warp & 3;                     // TMEM lane quarter (warp % 4)
-        const int nt0 = ((warp - 4) >> 2) * TPW;    // first N tile drained by this warp
-        const int row = m_tile * BM + q * 32 + lane;
+        // warp → (TMEM lane quarter q, DC-column slice of the NT·64 output columns)
+        constexpr int DC = CF::DCOLS;
+        const int q = warp & 3;
+        const int slice = (warp - 4) >> 2;
+        const int ccol = slice * DC;                  // first output column (within the tile) of this warp
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        int gc = 0;  // chunks drained so far (all tiles)
+        for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+        const TileInfo ti = tile_info<NT>(sc, t);
+        const int m_tile = ti.m_tile, n_tile = ti.n_tile, split = ti.split;
+        const int nchunks = (ti.nk + CH - 1) / CH;
+        const int row = m_tile * BM + q * 32 + lane;
         // X3: compensated fp32 sums on the FMA pipe (acc + cmp ≈ fp64 accuracy; the
         // fp32→fp64 converts of a plain fp64 drain saturate the XU pipe and stall the MMA)
-        float acc[TPW * BN], cmp[X3 ? TPW * BN : 1];
+        float acc[DC], cmp[X3 ? DC : 1];
 #pragma unroll
-        for (int j = 0; j < TPW * BN; ++j) acc[j] = 0.0f;
+        for (int j = 0; j < DC; ++j) acc[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < (X3 ? TPW * BN : 1); ++j) cmp[j] = 0.0f;
+        for (int j = 0; j < (X3 ? DC : 1); ++j) cmp[j] = 0.0f;
         for (int c = 0; c < nchunks; ++c) {
-            const int b = c & 1;
-            mbar_wait(&tfull[b], (uint32_t)(c / 2) & 1u);
+            const int g = gc + c, b = g & 1;
+            mbar_wait(&tfull[b], (uint32_t)(g / 2) & 1u);
             tc_fence_after();
-            if (g_dbg_flags & 2) {  // experiment switch: skip the drain (wrong results)
+            if (dbg & 2) {  // experiment switch: skip the drain (wrong results)
                 tc_fence_before();
                 mbar_arrive(&tempty[b]);
                 continue;
             }
+            const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * BUFCOLS + ccol);
+            const uint32_t t_lo = t_hi + NT * BN;
+            constexpr int LDW = X3 ? 8 : 16;  // X3: narrower loads keep acc+cmp+loads in registers
 #pragma unroll
-            for (int tt = 0; tt < TPW; ++tt) {
-                const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * NACC * NT * BN + (nt0 + tt) * BN);
-                const uint32_t t_lo = t_hi + NT * BN;
-                constexpr int LDW = X3 ? 8 : 16;  // X3: narrower loads keep acc+cmp+loads in registers
+            for (int j0 = 0; j0 < DC; j0 += LDW) {
+                uint32_t h[LDW], l[LDW];
+                if (X3) {
+                    TMEM_LD8(t_hi + j0, h);
+                    TMEM_LD8(t_lo + j0, l);
+                } else {
+                    TMEM_LD16(t_hi + j0, h);
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                for (int j0 = 0; j0 < BN; j0 += LDW) {
-                    uint32_t h[LDW], l[LDW];
+                for (int j = 0; j < LDW; ++j) {
+                    const int e = j0 + j;
+                    const float hsum = __uint_as_float(h[j]);
                     if (X3) {
-                        TMEM_LD8(t_hi + j0, h);
-                        TMEM_LD8(t_lo + j0, l);
+                        const float hv = hsum, lv = __uint_as_float(l[j]);
+                        const float t = __fadd_rn(hv, lv);
+                        const float et = __fsub_rn(lv, __fsub_rn(t, hv));     // Fast2Sum, |hi| ≥ |lo|
+                        const float sum = __fadd_rn(acc[e], t);
+                        const float z = __fsub_rn(sum, acc[e]);
+                        cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(t, z), et));
+                        acc[e] = sum;
                     } else {
-                        TMEM_LD16(t_hi + j0, h);
-                    }
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                    for (int j = 0; j < LDW; ++j) {
-                        const int e = tt * BN + j0 + j;
-                        if (X3) {
-                            const float hv = __uint_as_float(h[j]), lv = __uint_as_float(l[j]);
-                            const float t = __fadd_rn(hv, lv);
-                            const float et = __fsub_rn(lv, __fsub_rn(t, hv));     // Fast2Sum, |hi| ≥ |lo|
-                            const float sum = __fadd_rn(acc[e], t);
-                            const float z = __fsub_rn(sum, acc[e]);
-                            cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(t, z), et));
-                            acc[e] = sum;
-                        } else {
-                            acc[e] += __uint_as_float(h[j]);
-                        }
+                        acc[e] += hsum;
                     }
                 }
             }
             tc_fence_before();
             mbar_arrive(&tempty[b]);
         }
+        const int col0 = n_tile * NT * BN + ccol;
+        if (EPI == EPI_ROWSQ) {
+            double s = 0.0;
 #pragma unroll
-        for (int tt = 0; tt < TPW; ++tt) {
-            const int nt = nt0 + tt;
-            const int col0 = (n_tile * NT + nt) * BN;
-            if (EPI == EPI_ROWSQ) {
-                double s = 0.0;
+            for (int j = 0; j < DC; ++j) {
+                const double v = (double)acc[j];
+                s = fma(v, v, s);  // columns ≥ N are exact zeros
+            }
+            // one partial row-sum per DC-column slice of the output
+            if (row < M) partial[(int64_t)(col0 / DC) * M + row] = s;
+        } else if (row < M) {
+            // split-K partials (plain stores) or alpha·v + beta·out; lanes = consecutive rows
+            double* dst = partial ? partial + (int64_t)split * M * N + row : out + row;
+            const int64_t stride = partial ? (int64_t)M : ldo;
+            const bool plain = partial != nullptr || beta == 0.0;
+            const double a_ = partial ? 1.0 : alpha;
+            const int ncol = min(DC, N - col0);
 #pragma unroll
-                for (int j = 0; j < BN; ++j) {
-                    const double v = (double)acc[tt * BN + j];
-                    s = fma(v, v, s);  // columns ≥ N are exact zeros
-                }
-                if (row < M) partial[(int64_t)(n_tile * NT + nt) * M + row] = s;
-            } else if (row < M) {
-                // split-K partials (plain stores) or alpha·v + beta·out; lanes = consecutive rows
-                double* dst = partial ? partial + (int64_t)split * M * N + row : out + row;
-                const int64_t stride = partial ? (int64_t)M : ldo;
-                const bool plain = partial != nullptr || beta == 0.0;
-                const double a_ = partial ? 1.0 : alpha;
-                const int ncol = min(BN, N - col0);
-#pragma unroll
-                for (int j = 0; j < BN; ++j) {
-                    const double v = X3 ? (double)acc[tt * BN + j] + (double)cmp[X3 ? tt * BN + j : 0]
-                                        : (double)acc[tt * BN + j];
-                    if (j < ncol) {
-                        double* o = dst + (int64_t)(col0 + j) * stride;
-                        *o = plain ? a_ * v : fma(beta, *o, a_ * v);
-                    }
+            for (int j = 0; j < DC; ++j) {
+                const double v = X3 ? (double)acc[j] + (double)cmp[X3 ? j : 0] : (double)acc[j];
+                if (j < ncol) {
+                    double* o = dst + (int64_t)(col0 + j) * stride;
+                    *o = plain ? a_ * v : fma(beta, *o, a_ * v);
                 }
             }
+        }
+        gc += nchunks;
         }
     } else {
         if (X3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::REG_LOW));
@@ -319,79 +404,114 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             // ------------------------------------------------------ TMA producer
             if (lane == 0) {
                 constexpr int PF = 12;  // A-tile L2 prefetch distance (stages)
-                auto prefetch_a = [&](int i) {
-                    const int k0 = (kt0 + i) * BK;
-                    if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
-                    else tma_prefetch_2d(&tmA, k0, m_tile * BM);
-                };
-                for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
-                for (int i = 0; i < nk; ++i) {
-                    const int s = i % STAGES;
-                    if (i + PF < nk) prefetch_a(i + PF);
-                    mbar_wait(&empty[s], ((uint32_t)(i / STAGES) & 1u) ^ 1u);
-                    mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
-                    const int k0 = (kt0 + i) * BK;
-                    if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
-                    else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
-    #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) {
-                        tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
-                        if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
+                int gi = 0;             // stages issued so far (all tiles)
+                for (int t = blockIdx.x, w = 0; t < sc.total; t += gridDim.x, ++w) {
+                    if (sc.wave_ctr && w > 0) {  // wave barrier (see Sched)
+                        const unsigned int target = wave_arrivals(sc, w - 1);
+                        unsigned int v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(sc.wave_ctr) : "memory");
+                        } while (v < target);
                     }
+                    const TileInfo ti = tile_info<NT>(sc, t);
+                    const int kt0 = ti.kt0, nk = ti.nk, m_tile = ti.m_tile, n_tile = ti.n_tile;
+                    auto prefetch_a = [&](int i) {
+                        const int k0 = (kt0 + i) * BK;
+                        if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
+                        else tma_prefetch_2d(&tmA, k0, m_tile * BM);
+                    };
+                    for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % STAGES;
+                        if (i + PF < nk) prefetch_a(i + PF);
+                        mbar_wait(&empty[s], ((uint32_t)(gi / STAGES) & 1u) ^ 1u);
+                        mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
+                        const int k0 = (kt0 + i) * BK;
+                        if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
+                        else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) {
+                            tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
+                            if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
+                        }
+                    }
+                    if (sc.wave_ctr) atomicAdd(sc.wave_ctr, 1u);
                 }
             }
         } else if (warp == 1) {
             // ------------------------------------------------------ MMA issuer
-            for (int i = 0; i < nk; ++i) {
-                const int s = i % STAGES;
-                const int c = i / CH, b = c & 1;
-                const bool first = (i % CH) == 0;
-                if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
-                const uint32_t ph = (uint32_t)(i / STAGES) & 1u;
-                mbar_wait(&full[s], ph);
-                mbar_wait(&lo_ready[s], ph);
-                tc_fence_after();
-                if (lane == 0) {
-                    // one instruction spans all NT N-tiles (the A tile is read once per k-step);
-                    // X3 fuses a_hi·[x_hi | x_lo] (x_lo tiles follow x_hi in the stage, and the lo
-                    // accumulator follows the hi one in TMEM), then adds a_lo·x_hi into lo.
-                    const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(s)), xh = smem_u32(x_hi(s));
-                    const uint32_t t_hi = tmem + (uint32_t)(b * NACC * NT * BN), t_lo = t_hi + NT * BN;
-    #pragma unroll
-                    for (int k8 = 0; k8 < BK / 8; ++k8) {
-                        uint64_t da_r, da_l;
-                        if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
-                            da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
-                            da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
-                        } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
-                            da_r = sdesc(ar + k8 * 32, 16, 1024, 2);
-                            da_l = sdesc(al + k8 * 32, 16, 1024, 2);
+            int gi = 0, gc = 0;  // stages / chunks consumed so far (all tiles)
+            for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
+                const int nk = tile_info<NT>(sc, t).nk;
+                for (int i = 0; i < nk; ++i, ++gi) {
+                    const int s = gi % STAGES;
+                    const int c = gc + i / CH, b = c & 1;
+                    const bool first = (i % CH) == 0;
+                    if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
+                    const uint32_t ph = (uint32_t)(gi / STAGES) & 1u;
+                    const int lr = X3 ? gi % LO_SLOTS : s;
+                    mbar_wait(&full[s], ph);
+                    mbar_wait(&lo_ready[lr], X3 ? (uint32_t)(gi / LO_SLOTS) & 1u : ph);
+                    tc_fence_after();
+                    {  // whole warp (elect.sync inside the issue helpers)
+                        const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(lr)), xh = smem_u32(x_hi(s));
+#pragma unroll
+                        for (int k8 = 0; k8 < BK / 8; ++k8) {
+                            uint64_t da_r, da_l;
+                            if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
+                                da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
+                                da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
+                            } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
+                                da_r = sdesc(ar + k8 * 32, 16, 1024, 2);
+                                da_l = sdesc(al + k8 * 32, 16, 1024, 2);
+                            }
+                            // one instruction spans all NT N-tiles (the A tile is read once per k-step);
+                            // X3 fuses a_hi·[x_hi | x_lo] (x_lo tiles follow x_hi in the stage, and the lo
+                            // accumulator follows the hi one in TMEM), then adds a_lo·x_hi into lo.
+                            // (Rotating independent accumulators per k-step was measured slower:
+                            // the extra drain loads cost more than the MMA-chain overlap gains.)
+                            const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
+                            const uint32_t t_hi = tmem + (uint32_t)(b * BUFCOLS), t_lo = t_hi + NT * BN;
+                            const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                            if (!(dbg & 4)) {  // bit 2: skip the MMAs (timing experiments)
+                                umma_tf32_warp(t_hi, da_r, dxh, idesc((X3 ? 2 : 1) * NT * BN), acc);
+                                if (X3) umma_tf32_warp(t_lo, da_l, dxh, idesc(NT * BN), 1u);
+                            }
                         }
-                        const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
-                        const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
-                        umma_tf32(t_hi, da_r, dxh, idesc((X3 ? 2 : 1) * NT * BN), acc);
-                        if (X3) umma_tf32(t_lo, da_l, dxh, idesc(NT * BN), 1u);
+                        umma_commit_warp(&empty[s]);
+                        if (X3) umma_commit_warp(&lo_empty[lr]);
+                        if ((i % CH) == CH - 1 || i == nk - 1) umma_commit_warp(&tfull[b]);
                     }
-                    umma_commit(&empty[s]);
-                    if ((i % CH) == CH - 1 || i == nk - 1) umma_commit(&tfull[b]);
+                    __syncwarp();
                 }
-                __syncwarp();
+                gc += (nk + CH - 1) / CH;
             }
         } else {
             // ------------------------- a_lo transform (X3) / in-place rn_tf32 (X1)
             constexpr int NTT = 32 * CF::NTRANSFORM;
-            const int t = (warp < 4 ? warp - 2 : warp - (4 + CF::NDRAIN) + 2) * 32 + lane;  // 0..NTT-1
-            for (int i = 0; i < nk; ++i) {
-                const int s = i % STAGES;
-                mbar_wait(&full[s], (uint32_t)(i / STAGES) & 1u);
-                const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(s)) : src;
-                if (g_dbg_flags & 1) {  // experiment switch: skip the transform (wrong results)
+            const int tid = (warp < 4 ? warp - 2 : warp - (4 + CF::NDRAIN) + 2) * 32 + lane;  // 0..NTT-1
+            int gi = 0;
+            int nk = 0, tile = blockIdx.x - (int)gridDim.x, i = 0;
+            for (;; ++i, ++gi) {
+                while (i >= nk) {  // next tile with work
+                    tile += gridDim.x;
+                    if (tile >= sc.total) break;
+                    nk = tile_info<NT>(sc, tile).nk;
+                    i = 0;
+                }
+                if (tile >= sc.total) break;
+                const int s = gi % STAGES;
+                const int lr = X3 ? gi % LO_SLOTS : s;
+                mbar_wait(&full[s], (uint32_t)(gi / STAGES) & 1u);
+                if (X3) mbar_wait(&lo_empty[lr], ((uint32_t)(gi / LO_SLOTS) & 1u) ^ 1u);
+                const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(lr)) : src;
+                if (dbg & 1) {  // experiment switch: skip the transform (wrong results)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    mbar_arrive(&lo_ready[s]);
+                    mbar_arrive(&lo_ready[lr]);
                     continue;
                 }
     #pragma unroll 4
-                for (int v = t; v < (int)(A_TILE / 16); v += NTT) {
+                for (int v = tid; v < (int)(A_TILE / 16); v += NTT) {
                     float4 a;
                     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                                  : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
@@ -404,7 +524,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                                  "f"(a.z), "f"(a.w) : "memory");
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(&lo_ready[s]);
+                mbar_arrive(&lo_ready[lr]);
             }
         }
     }
@@ -473,10 +593,10 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
     return m;
 }
 
+// Persistent launch: one CTA per SM (or fewer when there are fewer tiles).
 template <bool A_MN, int EPI, int NT, bool X3>
-void launch_umma_nt(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
-                    int N, int k_tiles, int kps, double* out, int64_t ldo, double* partial, double alpha,
-                    double beta) {
+void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
+                    int N, double* out, int64_t ldo, double* partial, double alpha, double beta) {
     using CF = Cfg<NT, X3>;
     auto kern = k_umma<A_MN, EPI, NT, X3>;
     static bool attr = false;
@@ -484,20 +604,54 @@ void launch_umma_nt(Ctx* c, dim3 grid, const CUtensorMap& ta, const CUtensorMap&
         CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         attr = true;
     }
-    kern<<<grid, CF::NTHREADS, CF::SMEM_BYTES, c->stream>>>(ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha,
-                                                            beta);
+    if (sc.total <= 0) return;
+    const int grid = std::min(sc.total, c->sm_count);
+    DevBuf ctr;
+    if (grid < sc.total && !(g_wave_barrier_off)) {
+        ctr = DevBuf(c, 64);
+        CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
+        sc.wave_ctr = ctr.as<unsigned int>();
+    } else {
+        sc.wave_ctr = nullptr;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(CF::NTHREADS);
+    cfg.dynamicSmemBytes = CF::SMEM_BYTES;
+    cfg.stream = c->stream;
+    cudaLaunchAttribute attr_c[1];
+    attr_c[0].id = cudaLaunchAttributeCooperative;
+    attr_c[0].val.cooperative = sc.wave_ctr ? 1 : 0;
+    cfg.attrs = attr_c;
+    cfg.numAttrs = 1;
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, th, tl, M, N, sc, out, ldo, partial, alpha, beta));
     LAUNCH_CHECK(c);
 }
 
 // 3×TF32 with 1 or 2 N tiles per CTA
 template <bool A_MN, int EPI>
-void launch_umma(Ctx* c, int nt_per_cta, dim3 grid, const CUtensorMap& ta, const CUtensorMap& th,
-                 const CUtensorMap& tl, int M, int N, int k_tiles, int kps, double* out, int64_t ldo, double* partial,
-                 double alpha, double beta) {
+void launch_umma(Ctx* c, int nt_per_cta, Sched sc, const CUtensorMap& ta, const CUtensorMap& th,
+                 const CUtensorMap& tl, int M, int N, double* out, int64_t ldo, double* partial, double alpha,
+                 double beta) {
     if (nt_per_cta == 2)
-        launch_umma_nt<A_MN, EPI, 2, true>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
+        launch_umma_nt<A_MN, EPI, 2, true>(c, sc, ta, th, tl, M, N, out, ldo, partial, alpha, beta);
     else
-        launch_umma_nt<A_MN, EPI, 1, true>(c, grid, ta, th, tl, M, N, k_tiles, kps, out, ldo, partial, alpha, beta);
+        launch_umma_nt<A_MN, EPI, 1, true>(c, sc, ta, th, tl, M, N, out, ldo, partial, alpha, beta);
+}
+
+Sched make_sched(int m_tiles, int n_tiles, int splits, int k_tiles, int kps, bool sym, bool tri_x) {
+    Sched sc;
+    sc.m_tiles = m_tiles;
+    sc.n_tiles = n_tiles;
+    sc.splits = splits;
+    sc.group_n = std::min(8, n_tiles);  // a wave of 148 CTAs ≈ 8 N tiles × 18 M tiles
+    sc.k_tiles = k_tiles;
+    sc.kps = kps;
+    sc.sym = sym ? 1 : 0;
+    sc.tri_x = tri_x ? 1 : 0;
+    sc.total = splits * (sym ? n_tiles * (n_tiles + 1) / 2 : m_tiles * n_tiles);
+    sc.wave_ctr = nullptr;
+    return sc;
 }
 
 // x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
@@ -521,6 +675,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
     if (enabled < 0) {
         const char* e = getenv("BCUR_DISABLE_UMMA");
         enabled = (e && e[0] == '1') ? 0 : 1;
+        const char* wb = getenv("BCUR_UMMA_NO_WAVE_BARRIER");
+        g_wave_barrier_off = wb && wb[0] == '1';
         const char* d = getenv("BCUR_UMMA_DEBUG");
         if (d) {
             const int f = atoi(d);
@@ -534,12 +690,14 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
 // Out(n×N) = alpha·Aᵀ X + beta·Out  (A m×n fp32 col-major; X m×N fp32/fp64) → fp64 store,
 // or rowsq[j] = Σ_c (AᵀX)_jc² (rowsq != nullptr; product never stored)
 void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq) {
+              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq, bool sym) {
     if (n <= 0 || N <= 0) {
         if (rowsq && n > 0) CUDA_CHECK(cudaMemsetAsync(rowsq, 0, n * sizeof(double), c->stream));
         return;
     }
-    ProfScope prof(c, rowsq ? "umma_atx_rowsq" : "umma_atx_store", 2.0 * n * N * m,
+    const int NT = N > BN ? 2 : 1;
+    sym = sym && !rowsq && NT == 2 && n == N;  // Gram AᵀA: upper-triangle tiles only
+    ProfScope prof(c, rowsq ? "umma_atx_rowsq" : "umma_atx_store", (sym ? 1.0 : 2.0) * n * N * m,
                    4.0 * m * n + (double)dtype_size(dtx) * m * N + (rowsq ? 8.0 * n : 8.0 * n * N));
     DevBuf xh, xl;
     split_x(c, X, dtx, m, N, ldx, &xh, &xl);
@@ -558,35 +716,34 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
         // steps) use fewer tiles and a deeper stage ring (HBM-bound regime).
         const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
         const int nt = (int)((N + NTX * BN - 1) / (NTX * BN));
-        dim3 grid(nt, mt, 1);
+        const Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
         DevBuf part(c, (size_t)nt * NTX * n * sizeof(double));
         if (NTX == 1)
-            launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles,
-                                                       nullptr, 0, part.as<double>(), 1.0, 0.0);
+            launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
+                                                       part.as<double>(), 1.0, 0.0);
         else if (NTX == 2)
-            launch_umma_nt<false, EPI_ROWSQ, 2, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles,
-                                                       nullptr, 0, part.as<double>(), 1.0, 0.0);
+            launch_umma_nt<false, EPI_ROWSQ, 2, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
+                                                       part.as<double>(), 1.0, 0.0);
         else
-            launch_umma_nt<false, EPI_ROWSQ, 4, false>(c, grid, ta, th, th, (int)n, (int)N, k_tiles, k_tiles,
-                                                       nullptr, 0, part.as<double>(), 1.0, 0.0);
+            launch_umma_nt<false, EPI_ROWSQ, 4, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
+                                                       part.as<double>(), 1.0, 0.0);
         k_sum_tiles<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(n, nt * NTX, part.as<double>(), rowsq);
         LAUNCH_CHECK(c);
         return;
     }
-    const int NT = N > BN ? 2 : 1;
     const int nt = (int)((N + NT * BN - 1) / (NT * BN));
-    dim3 grid(nt, mt, 1);  // N tiles of one A row-tile run side by side and share it through L2
-    {
-        launch_umma<false, EPI_STORE>(c, NT, grid, ta, th, tl, (int)n, (int)N, k_tiles, k_tiles, out, ldo, nullptr,
-                                      alpha, beta);
-    }
+    const Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, sym, false);
+    launch_umma<false, EPI_STORE>(c, NT, sc, ta, th, tl, (int)n, (int)N, out, ldo, nullptr, alpha, beta);
 }
 
-// Out(m×N) = alpha·A X + beta·Out  (A m×n fp32; X n×N fp32/fp64), split-K over n with fp64 partials
+// Out(m×N) = alpha·A X + beta·Out  (A m×n fp32; X n×N fp32/fp64), split-K over n with fp64
+// partials.  x_upper_tri: X[k, j] = 0 for k > j (R⁻¹ of a Cholesky factor) — each N tile
+// stops at its diagonal (half the MMAs).
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-             int64_t ldx, double alpha, double beta, double* out, int64_t ldo) {
+             int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri) {
     if (m <= 0 || N <= 0) return;
-    ProfScope prof(c, "umma_ax", 2.0 * m * n * N, 4.0 * m * n + (double)dtype_size(dtx) * n * N + 8.0 * m * N);
+    ProfScope prof(c, "umma_ax", (x_upper_tri ? 1.0 : 2.0) * m * n * N,
+                   4.0 * m * n + (double)dtype_size(dtx) * n * N + 8.0 * m * N);
     DevBuf xh, xl;
     split_x(c, X, dtx, n, N, ldx, &xh, &xl);
     // 3-D view of column-major A: (32 rows, n columns, m/32 row groups)
@@ -604,15 +761,13 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
                                                              k_tiles / 16));
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
-    dim3 grid(mt, nt, splits);
+    const Sched sc = make_sched(mt, nt, splits, k_tiles, kps, false, x_upper_tri);
     if (splits == 1) {
-        launch_umma<true, EPI_STORE>(c, NT, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, out, ldo, nullptr,
-                                     alpha, beta);
+        launch_umma<true, EPI_STORE>(c, NT, sc, ta, th, tl, (int)m, (int)N, out, ldo, nullptr, alpha, beta);
         return;
     }
     DevBuf part(c, (size_t)splits * m * N * sizeof(double));
-    launch_umma<true, EPI_STORE>(c, NT, grid, ta, th, tl, (int)m, (int)N, k_tiles, kps, nullptr, 0,
-                                 part.as<double>(), 1.0, 0.0);
+    launch_umma<true, EPI_STORE>(c, NT, sc, ta, th, tl, (int)m, (int)N, nullptr, 0, part.as<double>(), 1.0, 0.0);
     k_reduce_splits<<<(unsigned)((m * N + 255) / 256), 256, 0, c->stream>>>(m, N, splits, part.as<double>(), out, ldo,
                                                                             alpha, beta);
     LAUNCH_CHECK(c);

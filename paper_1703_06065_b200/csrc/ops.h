@@ -18,15 +18,19 @@ void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64
                       int64_t G, double* d_rows /*nullable*/, double* d_blocks);
 // segmented sum of a fp64 vector over block offsets
 void segment_sum(Ctx* c, const double* x, const int64_t* d_offsets, int64_t G, double* d_out);
-// max |G - I| over a w×w fp64 matrix → d_out[0]
+// max |G - I| over the upper triangle of a symmetric w×w fp64 matrix → d_out[0]
 void max_dev_identity(Ctx* c, const double* g, int64_t w, int64_t ld, double* d_out);
 // ordered sum of x[0..n) → d_out[0]
 void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out);
 
 // ---- dense products (kernels_gemm.cu), fp64 accumulation ------------------
-// C(M×N fp64) = alpha·op(A)·op(B) + beta·C
+// C(M×N fp64) = alpha·op(A)·op(B) + beta·C.  Structure hints (exploited by the tcgen05 path
+// only; other paths compute the full product):
+//   GEMM_SYM_UPPER  op(A)·op(B) is the Gram AᵀA (B == A): only C's upper triangle is needed
+//   GEMM_B_UPPER    op(B) is upper triangular
+enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2 };
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
-          const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc);
+          const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags = 0);
 // rowsq[i] = Σ_j (op(A)·op(B))(i,j)²   (product never stored)
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                    const void* B, int dtb, int64_t ldb, double* rowsq);
@@ -40,12 +44,13 @@ void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
 
 // ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
 bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
-// Out(n×N) = alpha·Aᵀ X + beta·Out (fp64) or rowsq[j] = Σ_c (AᵀX)_jc²; X fp32 or fp64
+// Out(n×N) = alpha·Aᵀ X + beta·Out (fp64) or rowsq[j] = Σ_c (AᵀX)_jc²; X fp32 or fp64.
+// sym: X holds the same matrix as A (a Gram) — only the upper triangle of Out is written.
 void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq);
-// Out(m×N) = alpha·A X + beta·Out (fp64); X fp32 or fp64
+              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq, bool sym = false);
+// Out(m×N) = alpha·A X + beta·Out (fp64); X fp32 or fp64; x_upper_tri: X[k,j] = 0 for k > j
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-             int64_t ldx, double alpha, double beta, double* out, int64_t ldo);
+             int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri = false);
 
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
 // R upper (ld ldr, may alias g) with G = RᵀR, only g's upper triangle is read; info[0] = 0 ok / j+1 failed pivot;

@@ -291,16 +291,19 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
     if (cc == 0 || rows < cc) return false;
     Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc);
-    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, BCUR_F32, rows, C, BCUR_F32, rows, 0.0, G.p(), G.ld);
+    // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
+    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, BCUR_F32, rows, C, BCUR_F32, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
     const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p());
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     tri_inv_any(c, R.p(), cc, Ri.p());
-    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
+    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
+         GEMM_B_UPPER);
     DevBuf q1f(c, (size_t)rows * cc * 4);
     convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, q1f.ptr, BCUR_F32, rows);
-    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, q1f.ptr, BCUR_F32, rows, q1f.ptr, BCUR_F32, rows, 0.0, G.p(), G.ld);
+    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, q1f.ptr, BCUR_F32, rows, q1f.ptr, BCUR_F32, rows, 0.0, G.p(), G.ld,
+         GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
     // Second pass.  Q1ᵀQ1 = I + E with ‖E‖ ~ 1e-7·κ(C)²; when ‖E‖_max < 1e-4 the Cholesky
     // factor is R2 = I + F + O(‖E‖²), F = strict_upper(E) + diag(E)/2, so R2⁻¹ = I − F to
@@ -316,7 +319,8 @@ static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool
         if (c2.info != 0) return false;
         tri_inv_any(c, R.p(), cc, Ri.p());
     }
-    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1f.ptr, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
+    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1f.ptr, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
+         GEMM_B_UPPER);
     B->init(c, BCUR_F32, rows, cc);
     convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
     B->rank = cc;

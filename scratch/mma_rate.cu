@@ -1,0 +1,96 @@
+// Microbenchmark: tcgen05.mma kind::tf32 issue rate (cta_group::1, A and B from shared
+// memory, K-major SW128), one CTA per SM, no TMA — per-SM cycles per MMA for N = 64/128/256.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mma_rate mma_rate.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)layout << 61;
+    return d;
+}
+__device__ __forceinline__ uint32_t idesc(uint32_t n) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+
+__global__ void __launch_bounds__(128, 1) k_mma(int iters, int n1, int n2, unsigned long long* cycles) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* a = smem;                // 128 × 32 fp32 (16 KB)
+    uint8_t* b = smem + 16384;        // 256 × 32 fp32 (32 KB)
+    uint64_t* bar = (uint64_t*)(smem + 16384 + 32768);
+    uint32_t* slot = (uint32_t*)(bar + 1);
+    for (int i = threadIdx.x; i < (16384 + 32768) / 4; i += blockDim.x) ((float*)smem)[i] = 1.0f;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (threadIdx.x < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int k8 = 0; k8 < 4; ++k8) {
+                const uint64_t da = sdesc(smem_u32(a) + k8 * 32, 16, 1024, 2);
+                const uint64_t db = sdesc(smem_u32(b) + k8 * 32, 16, 1024, 2);
+                asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                             "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                             ::"r"(tmem), "l"(da), "l"(db), "r"(idesc(n1)), "r"(1));
+                if (n2)
+                    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                 "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+                                 ::"r"(tmem + 256), "l"(da), "l"(db), "r"(idesc(n2)), "r"(1));
+            }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                     : "memory");
+        asm volatile("{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W;\n\t}"
+                     ::"r"(smem_u32(bar)) : "memory");
+        const long long t1 = clock64();
+        cycles[blockIdx.x] = (unsigned long long)(t1 - t0);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+int main(int argc, char** argv) {
+    const int n1 = argc > 1 ? atoi(argv[1]) : 128, n2 = argc > 2 ? atoi(argv[2]) : 0;
+    const int iters = 4096, grid = 148;
+    unsigned long long* d;
+    cudaMalloc(&d, grid * 8);
+    const int smem = 16384 + 32768 + 1024 + 64;
+    cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mma<<<grid, 128, smem>>>(16, n1, n2, d);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    k_mma<<<grid, 128, smem>>>(iters, n1, n2, d);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long h[148];
+    cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    const double mmas = (double)iters * 4;
+    const double flops = 2.0 * 128 * 8 * (n1 + n2) * mmas * grid;
+    printf("N=%d+%d: %.1f cycles per k8-step (clock64, CTA 0), %.1f TFLOP/s tf32 (%s)\n", n1, n2, h[0] / mmas,
+           flops / (ms * 1e9), cudaGetErrorString(cudaGetLastError()));
+    return 0;
+}
