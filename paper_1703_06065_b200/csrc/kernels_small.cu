@@ -12,6 +12,17 @@ namespace bcur_b200 {
 namespace {
 
 constexpr int ST = 1024;
+
+// 1/x to full double precision from the hardware approximation + two Newton steps (the
+// IEEE-exact division is a long software sequence that sat on the factorizations'
+// serial critical paths).
+__device__ __forceinline__ double fast_rcp(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    r = fma(r, fma(-x, r, 1.0), r);
+    r = fma(r, fma(-x, r, 1.0), r);
+    return r;
+}
 constexpr int NW = ST / 32;
 constexpr int SMEM_MAX_W = 144;
 
@@ -50,7 +61,7 @@ __global__ void __launch_bounds__(ST) k_cholesky(const double* g, int w, int64_t
             break;
         }
         mn = fmin(mn, d);
-        const double inv = 1.0 / d;
+        const double inv = fast_rcp(d);
         const double* colj = M + j * ldm;
         for (int k = j + 1 + warp; k < w; k += NW) {
             const double a = colj[k] * inv;
@@ -70,6 +81,139 @@ __global__ void __launch_bounds__(ST) k_cholesky(const double* g, int w, int64_t
         } else {
             *info = stop;
             diag[0] = stop ? 0.0 : mn;
+        }
+    }
+}
+
+// ------------------------------------------------- panel Cholesky (w ≤ 128)
+// Same contract as k_cholesky, for the diagonal blocks of the blocked factorization.
+// 32-column panels: (1) one warp factors the 32×32 diagonal block in registers (lane i
+// holds row i; pivots and multipliers move by shuffles — no barriers), (2) one thread per
+// remaining row forward-substitutes its 32 panel entries (TRSM), (3) all 8 warps apply the
+// rank-32 SYRK update to the trailing lower triangle with 6×6 register tiles.  Three
+// barriers per panel instead of one per column; ~5× fewer instructions than k_cholesky.
+constexpr int CP_T = 256, CP_MAX = 128, CP_LD = CP_MAX + 1;
+__global__ void __launch_bounds__(CP_T) k_chol_panel(const double* g, int w, int64_t ldg, double* r, int64_t ldr,
+                                                     int* info, double* diag, int info_offset, int chained) {
+    extern __shared__ double smc[];
+    double* M = smc;                    // lower triangle, M[i + k·LD] (i ≥ k), padded with identity
+    __shared__ double invd[CP_MAX];
+    __shared__ int stop_sh;
+    __shared__ double mn_sh;
+    if (chained && *info != 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wp = (w + 31) & ~31;
+    for (int k = warp; k < wp; k += CP_T / 32)
+        for (int i = lane; i <= k; i += 32)
+            M[k + i * CP_LD] = (i < w && k < w) ? g[i + (int64_t)k * ldg] : (i == k ? 1.0 : 0.0);
+    if (tid == 0) {
+        stop_sh = 0;
+        mn_sh = INFINITY;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        double mx = 0.0;
+        for (int j = lane; j < w; j += 32) mx = fmax(mx, M[j + j * CP_LD]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0 && !chained) diag[1] = mx;
+    }
+    for (int c0 = 0; c0 < wp; c0 += 32) {
+        // (1) 32×32 diagonal block, warp 0, registers
+        if (warp == 0) {
+            double a[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) a[k] = k <= lane ? M[(c0 + lane) + (c0 + k) * CP_LD] : 0.0;
+            int bad = 0;
+            double mn = INFINITY, dl = 1.0;  // dl: this lane's 1/r_ii
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {  // fully unrolled: a[] stays in registers (no break)
+                const double d = __shfl_sync(0xffffffffu, a[j], j);
+                if (!bad && (!(d > 0.0) || !isfinite(d))) bad = c0 + j + 1;
+                if (bad) continue;
+                const double ri = rsqrt(d), rj = d * ri;
+                if (c0 + j < w) mn = fmin(mn, rj);  // padding pivots are 1
+                if (lane == j) dl = ri;
+                const double lij = a[j] * ri;  // l(lane, j) for lane > j
+                a[j] = lane == j ? rj : (lane > j ? lij : 0.0);
+#pragma unroll
+                for (int k = j + 1; k < 32; ++k) {
+                    const double lkj = __shfl_sync(0xffffffffu, lij, k);
+                    if (lane >= k) a[k] = fma(-lij, lkj, a[k]);
+                }
+            }
+            if (!bad) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k <= lane) M[(c0 + lane) + (c0 + k) * CP_LD] = a[k];
+                invd[c0 + lane] = dl;
+            }
+            if (lane == 0) {
+                if (bad) stop_sh = bad;
+                mn_sh = fmin(mn_sh, mn);
+            }
+        }
+        __syncthreads();
+        if (stop_sh) break;
+        const int base = c0 + 32, nr = wp - base;
+        if (nr <= 0) break;
+        // (2) TRSM: row i of the panel below the diagonal block, x = m · L_ppᵀ⁻¹
+        if (tid < nr) {
+            const int i = base + tid;
+            double x[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) {
+                double s = M[i + (c0 + c) * CP_LD];
+#pragma unroll
+                for (int cc = 0; cc < c; ++cc) s = fma(-x[cc], M[(c0 + c) + (c0 + cc) * CP_LD], s);
+                x[c] = s * invd[c0 + c];
+            }
+#pragma unroll
+            for (int c = 0; c < 32; ++c) M[i + (c0 + c) * CP_LD] = x[c];
+        }
+        __syncthreads();
+        // (3) SYRK: M[i,k] -= Σ_c L[i,c]·L[k,c] over the trailing lower triangle
+        {
+            const int ty = tid >> 4, tx = tid & 15;
+            double acc[6][6];
+#pragma unroll
+            for (int u = 0; u < 6; ++u)
+#pragma unroll
+                for (int v = 0; v < 6; ++v) acc[u][v] = 0.0;
+#pragma unroll 4
+            for (int c = 0; c < 32; ++c) {
+                const double* col = M + (c0 + c) * CP_LD + base;
+                double li[6], lk[6];
+#pragma unroll
+                for (int u = 0; u < 6; ++u) {
+                    li[u] = (ty + 16 * u) < nr ? col[ty + 16 * u] : 0.0;
+                    lk[u] = (tx + 16 * u) < nr ? col[tx + 16 * u] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+#pragma unroll
+                    for (int v = 0; v < 6; ++v) acc[u][v] = fma(li[u], lk[v], acc[u][v]);
+            }
+#pragma unroll
+            for (int u = 0; u < 6; ++u)
+#pragma unroll
+                for (int v = 0; v < 6; ++v) {
+                    const int i = ty + 16 * u, k = tx + 16 * v;
+                    if (i < nr && k <= i) M[(base + i) + (base + k) * CP_LD] -= acc[u][v];
+                }
+        }
+        __syncthreads();
+    }
+    const int stop = stop_sh;
+    for (int k = warp; k < w; k += CP_T / 32)
+        for (int i = lane; i < w; i += 32) r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * CP_LD] : 0.0;
+    if (tid == 0) {
+        if (chained) {
+            if (stop) *info = info_offset + stop;
+            diag[0] = stop ? 0.0 : fmin(diag[0], mn_sh);
+        } else {
+            *info = stop;
+            diag[0] = stop ? 0.0 : mn_sh;
         }
     }
 }
@@ -97,15 +241,16 @@ __global__ void __launch_bounds__(ST) k_tri_inv_upper(const double* __restrict__
         for (int i = lane; i <= k; i += 32)
             S[i + k * TRI_LD] = (i < w && k < w) ? r[i + k * ldr] : (i == k ? 1.0 : 0.0);
     __syncthreads();
+    for (int c = threadIdx.x; c < wp; c += ST) xd[c] = fast_rcp(S[c + c * TRI_LD]);
+    __syncthreads();
     // phase A: column c of the inverse of its diagonal block
     for (int c = threadIdx.x; c < wp; c += ST) {
         const int b0 = c / TRI_B * TRI_B;
-        const double xcc = 1.0 / S[c + c * TRI_LD];
-        xd[c] = xcc;
+        const double xcc = xd[c];
         for (int i = c - 1; i >= b0; --i) {
             double s = S[i + c * TRI_LD] * xcc;
             for (int t = i + 1; t < c; ++t) s = fma(S[i + t * TRI_LD], S[c + t * TRI_LD], s);
-            S[c + i * TRI_LD] = -s / S[i + i * TRI_LD];
+            S[c + i * TRI_LD] = -s * xd[i];
         }
     }
     __syncthreads();
@@ -173,10 +318,14 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                 if (q < w) {
                     const double apq = A[p + q * w];
                     const double app = A[p + p * w], aqq = A[q + q * w];
-                    if (fabs(apq) > floor_abs && fabs(apq) > 1e-16 * sqrt(fabs(app * aqq))) {
-                        const double tau = (aqq - app) / (2.0 * apq);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
-                        c = 1.0 / sqrt(1.0 + t * t);
+                    if (fabs(apq) > floor_abs && apq * apq > 1e-32 * fabs(app * aqq)) {
+                        // rotation from rsqrt/rcp approximations refined to ~1 ulp (the
+                        // IEEE sqrt/div sequences made each round a long serial chain)
+                        const double tau = (aqq - app) * fast_rcp(2.0 * apq);
+                        const double q2 = fma(tau, tau, 1.0);
+                        const double root = q2 * rsqrt(q2);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(tau) + root);
+                        c = rsqrt(fma(t, t, 1.0));
                         s = t * c;
                         np_[i] = app - t * apq;  // exact post-rotation diagonal (Golub–Van Loan 8.4)
                         nq_[i] = aqq + t * apq;
@@ -265,6 +414,18 @@ void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, 
     if (w > 4096) fail(BCUR_E_INVALID_ARGUMENT, "cholesky_upper: single-CTA path limited to w <= 4096");
     ensure_attrs();
     ProfScope prof(c, "cholesky", w * w * w / 3.0, 8.0 * w * w);
+    if (w <= CP_MAX) {
+        static bool attr_p = false;
+        constexpr size_t smem_p = (size_t)CP_MAX * CP_LD * sizeof(double);
+        if (!attr_p) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_chol_panel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
+            attr_p = true;
+        }
+        k_chol_panel<<<1, CP_T, smem_p, c->stream>>>(g, (int)w, ldg, r, ldr, info, diag, (int)info_offset,
+                                                     chained ? 1 : 0);
+        LAUNCH_CHECK(c);
+        return;
+    }
     DevBuf work;
     size_t smem = 0;
     const size_t bytes = (size_t)w * (size_t)(w | 1) * sizeof(double);

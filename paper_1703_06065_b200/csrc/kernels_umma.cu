@@ -54,7 +54,7 @@ struct Cfg {
     // TMA stage = {a_raw, x_hi[NT], x_lo[NT] (X3)}; the a_lo split (X3) lives in its own
     // LO_SLOTS-deep ring so the TMA ring keeps as many stages in flight as fit (the
     // HBM-bound passes need ≥ 6 × 16 KB of A in flight per SM).
-    static constexpr int LO_SLOTS = X3 ? 2 : 0;
+    static constexpr int LO_SLOTS = X3 ? 3 : 0;
     static constexpr uint32_t STAGE = A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
     static constexpr int STAGES_FIT = (int)((232448u - 1280u - LO_SLOTS * A_TILE) / STAGE);
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
@@ -65,7 +65,9 @@ struct Cfg {
     // X3 runs whole warpgroups: WG0 = producer, MMA, 2 transform warps; NT drain warpgroups;
     // one more transform warpgroup (the a_lo split is the MMA's feeder).  The drain
     // warpgroups take the registers the others give up (setmaxnreg).
-    static constexpr int NTRANSFORM = (X3 || NT <= 2) ? 6 : 2;
+    static constexpr int NTRANSFORM = 6;
+    // register re-split (setmaxnreg) whenever the launch cap is below what the drains need
+    static constexpr bool RESPLIT = X3 || NT == 4;
     static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
     static constexpr uint32_t REG_LOW = 56;
     // setmaxnreg moves registers only inside the CTA's launch allocation: every thread starts
@@ -75,7 +77,7 @@ struct Cfg {
     static constexpr uint32_t REG_DRAIN_FIT =
         R0 + ((NTHREADS - 32 * NDRAIN) * (R0 - REG_LOW) / (32 * NDRAIN)) / 8 * 8;
     static constexpr uint32_t REG_DRAIN = REG_DRAIN_FIT > 232 ? 232 : REG_DRAIN_FIT;
-    static_assert(!X3 || (NTHREADS % 128 == 0 && R0 > REG_LOW &&
+    static_assert(!RESPLIT || (NTHREADS % 128 == 0 && R0 > REG_LOW &&
                           (NTHREADS - 32 * NDRAIN) * (R0 - REG_LOW) >= 32 * NDRAIN * (REG_DRAIN - R0)),
                   "X3 register split must fit the launch allocation");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
@@ -307,7 +309,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 
     // roles: branch per warpgroup first so the register re-split (X3) is warpgroup-uniform
     if (warp >= 4 && warp < 4 + CF::NDRAIN) {
-        if (X3) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CF::REG_DRAIN));
+        if (CF::RESPLIT) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CF::REG_DRAIN));
         // ------------------------------------------- TMEM drain + epilogue
         // warp → (TMEM lane quarter q, DC-column slice of the NT·64 output columns)
         constexpr int DC = CF::DCOLS;
@@ -339,13 +341,13 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             }
             const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * BUFCOLS + ccol);
             const uint32_t t_lo = t_hi + NT * BN;
-            constexpr int LDW = X3 ? 8 : 16;  // X3: narrower loads keep acc+cmp+loads in registers
+            constexpr int LDW = (X3 || NT == 4) ? 8 : 16;  // narrower loads keep acc(+cmp)+loads in registers
 #pragma unroll
             for (int j0 = 0; j0 < DC; j0 += LDW) {
                 uint32_t h[LDW], l[LDW];
-                if (X3) {
+                if (LDW == 8) {
                     TMEM_LD8(t_hi + j0, h);
-                    TMEM_LD8(t_lo + j0, l);
+                    if (X3) TMEM_LD8(t_lo + j0, l);
                 } else {
                     TMEM_LD16(t_hi + j0, h);
                 }
@@ -399,7 +401,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         gc += nchunks;
         }
     } else {
-        if (X3) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::REG_LOW));
+        if (CF::RESPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::REG_LOW));
         if (warp == 0) {
             // ------------------------------------------------------ TMA producer
             if (lane == 0) {

@@ -96,11 +96,13 @@ struct CholInfo {
     double mindiag, maxdiag;
 };
 
-static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X);
+static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X, const double* dinv = nullptr);
 
-// G (w×w SPD, fp64) → R upper (w×w, ld w) with G = RᵀR.  Single CTA up to 256,
+// G (w×w SPD, fp64) → R upper (w×w, ld w) with G = RᵀR.  Single CTA up to 144,
 // blocked right-looking (128-wide diagonal blocks + fp64 product updates) beyond.
-static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R) {
+// dinv (nullable, 128 × w, ld 128): receives the inverses of the diagonal blocks, which
+// the panel updates need anyway and tri_inv_any can reuse.
+static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* dinv = nullptr) {
     DevBuf st(c, 64);
     struct { int info; int pad; double mindiag, maxdiag; } hs;
     if (w <= 144) {
@@ -124,10 +126,11 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         const int64_t kb = std::min(B, w - k), rest = w - k - kb;
         double* Dk = R + k + k * w;
         cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
+        double* Ri = dinv ? dinv + k * B : Rinv.p();  // inverse of the diagonal block (ld B)
+        if (rest > 0 || dinv) tri_inv_upper(c, Dk, kb, w, Ri, B);
         if (rest > 0) {
-            tri_inv_upper(c, Dk, kb, w, Rinv.p(), kb);  // Rinv packed kb×kb (ld kb)
             double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
-            gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Rinv.p(), BCUR_F64, kb, Pk, BCUR_F64, w, 0.0, T1.p(), B);
+            gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Ri, BCUR_F64, B, Pk, BCUR_F64, w, 0.0, T1.p(), B);
             copy_f64(c, T1.p(), kb, rest, B, Pk, w);
             double* Tr = R + (k + kb) + (k + kb) * w;
             gemm(c, OP_T, OP_N, rest, rest, kb, -1.0, T1.p(), BCUR_F64, B, T1.p(), BCUR_F64, B, 1.0, Tr, w);
@@ -141,19 +144,21 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
 }
 
 // X = R⁻¹ for upper-triangular R (w×w, ld w).  Blocked back-substitution by block rows.
-static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X) {
+static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X, const double* dinv) {
     constexpr int64_t B = 128;  // single-CTA shared-memory inverse of ≤128-wide diagonal blocks
     if (w <= B) {
         tri_inv_upper(c, R, w, w, X, w);
         return;
     }
+    if (w <= 144) dinv = nullptr;  // chol_any factored it in one piece (no blocks kept)
     fill_f64(c, X, w * w, 0.0);
     Mat64 T(c, B, w);
     const int64_t nb = (w + B - 1) / B;
     for (int64_t bi = nb - 1; bi >= 0; --bi) {
         const int64_t r0 = bi * B, rb = std::min(B, w - r0), c0 = r0 + rb, rest = w - c0;
         double* Xii = X + r0 + r0 * w;
-        tri_inv_upper(c, R + r0 + r0 * w, rb, w, Xii, w);
+        if (dinv) copy_f64(c, dinv + r0 * B, rb, rb, B, Xii, w);
+        else tri_inv_upper(c, R + r0 + r0 * w, rb, w, Xii, w);
         if (rest > 0) {
             // X[r0, c0:] = −Rii⁻¹ · (R[r0, c0:] · X[c0:, c0:])
             gemm(c, OP_N, OP_N, rb, rest, rest, 1.0, R + r0 + c0 * w, BCUR_F64, w, X + c0 + c0 * w, BCUR_F64, w, 0.0,
@@ -169,17 +174,17 @@ static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X) {
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
              int64_t ldq, bool dist, Mat64* T_out, int* path_out) {
     if (w == 0) return 0;
-    Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w);
+    Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w), Dv(c, 128, w);
     gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld);
     if (dist) allreduce(c, G.p(), w * w);
-    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p());
+    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Dv.p());
     if (ref < 0) ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     int64_t r = w;
     const bool chol_ok = ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref;
     Mat64 Wr, sig;
     std::vector<double> sig_h;
     if (chol_ok) {
-        tri_inv_any(c, R.p(), w, Ri.p());
+        tri_inv_any(c, R.p(), w, Ri.p(), Dv.p());
         gemm(c, OP_N, OP_N, rows, w, w, 1.0, X, BCUR_F64, ldx, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
     } else {
         // σ_max(X) ≤ ‖X‖_F ≤ sqrt(w·max diag G): below the rank cut every σ is, so the
@@ -224,9 +229,9 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
     gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
     if (dist) allreduce(c, G2.p(), r * r);
-    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p());
+    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p());
     if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
-    tri_inv_any(c, R2.p(), r, R2i.p());
+    tri_inv_any(c, R2.p(), r, R2i.p(), Dv.p());
     gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
     if (T_out) {
         Mat64 T(c, r, w);
@@ -290,14 +295,14 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 // Returns false (B untouched) when C is not safely full rank (oracle.cholqr2_whole).
 static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
     if (cc == 0 || rows < cc) return false;
-    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc);
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
     gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, BCUR_F32, rows, C, BCUR_F32, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p());
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p());
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
-    tri_inv_any(c, R.p(), cc, Ri.p());
+    tri_inv_any(c, R.p(), cc, Ri.p(), Dv.p());
     gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
          GEMM_B_UPPER);
     DevBuf q1f(c, (size_t)rows * cc * 4);
@@ -315,9 +320,9 @@ static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool
     if (hdev < 1e-4) {
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p());
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p());
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p());
         if (c2.info != 0) return false;
-        tri_inv_any(c, R.p(), cc, Ri.p());
+        tri_inv_any(c, R.p(), cc, Ri.p(), Dv.p());
     }
     gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1f.ptr, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
          GEMM_B_UPPER);
@@ -808,11 +813,11 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         allreduce(c, TR.p(), rr * cr);
         // T⁺ = Tᵀ (T Tᵀ)⁻¹ ; (T Tᵀ)⁻¹ = R⁻¹ R⁻ᵀ with T Tᵀ = RᵀR
         auto pinv_rows = [&](const Mat64& T, int64_t rk, int64_t cols, Mat64* out_p) {
-            Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk);
+            Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk), Dv(c, 128, rk);
             gemm(c, OP_N, OP_T, rk, rk, cols, 1.0, T.p(), BCUR_F64, T.ld, T.p(), BCUR_F64, T.ld, 0.0, G.p(), G.ld);
-            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p());
+            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Dv.p());
             if (ci.info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
-            tri_inv_any(c, R.p(), rk, Ri.p());
+            tri_inv_any(c, R.p(), rk, Ri.p(), Dv.p());
             gemm(c, OP_N, OP_T, rk, rk, rk, 1.0, Ri.p(), BCUR_F64, Ri.ld, Ri.p(), BCUR_F64, Ri.ld, 0.0, Gi.p(), Gi.ld);
             *out_p = Mat64(c, cols, rk);
             gemm(c, OP_T, OP_N, cols, rk, rk, 1.0, T.p(), BCUR_F64, T.ld, Gi.p(), BCUR_F64, Gi.ld, 0.0, out_p->p(),
