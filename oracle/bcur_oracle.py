@@ -541,7 +541,8 @@ def orth(x: np.ndarray, ref: float, dt) -> Tuple[np.ndarray, np.ndarray, str]:
     """Rank-revealing orthonormalisation X ≈ Q·T (Q: m×r orthonormal, T: r×w).
 
     Path "chol": CholQR2 if chol(XᵀX) succeeds with min R_ii > τ_chol·ref.
-    Path "eig":  SVQB (eig of XᵀX, keep σ_i > τ_rank·ref) then one CholQR pass.
+    Path "eig":  SVQB (eig of XᵀX — or of X·Xᵀ for a wide panel, rows < w — keep
+                 σ_i > τ_rank·ref) then one CholQR pass.
     Replaces the reference's SVD-based pinv/rank cut (matcore.cpp:39-56,85-91).
     """
     dt = np.dtype(dt)
@@ -556,6 +557,23 @@ def orth(x: np.ndarray, ref: float, dt) -> Tuple[np.ndarray, np.ndarray, str]:
         r2 = chol_upper(q1.T @ q1)
         q = np.linalg.solve(r2.T, q1.T).T
         return q, r2 @ r, "chol"
+    if x.shape[0] < w:
+        # wide panel: decide on the smaller row Gram X·Xᵀ.  Safely full row rank (its
+        # Cholesky passes the same τ_chol test) → range(X) = ℝ^rows, Q = I, T = X;
+        # otherwise its eigenvectors are the orthonormal basis directly.
+        gr = x @ x.T
+        rr = chol_upper(gr)
+        if rr is not None and np.all(np.isfinite(rr)) and np.min(np.diag(rr)) > TAU_CHOL[dt] * ref:
+            return np.eye(x.shape[0]), x.copy(), "eig"
+        lam, u = eig_desc(gr)
+        sig = np.sqrt(np.maximum(lam, 0.0))
+        keep = int(np.sum(sig > TAU_RANK[dt] * ref))
+        if keep == 0:
+            return np.zeros((x.shape[0], 0)), np.zeros((0, w)), "eig"
+        q1 = u[:, :keep]
+        r2 = chol_upper(q1.T @ q1)
+        q = np.linalg.solve(r2.T, q1.T).T
+        return q, r2 @ (q1.T @ x), "eig"
     lam, wv = eig_desc(g)
     sig = np.sqrt(np.maximum(lam, 0.0))
     keep = int(np.sum(sig > TAU_RANK[dt] * ref))

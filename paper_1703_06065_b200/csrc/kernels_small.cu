@@ -279,10 +279,12 @@ __global__ void __launch_bounds__(ST) k_tri_inv_upper(const double* __restrict__
 // ---------------------------------------------------------------- Jacobi
 // Parallel (round-robin) cyclic Jacobi; A (w×w, column-major) in `A`, V (w×w) in `V`.
 __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int w, int64_t ldg,
-                                               double* __restrict__ Aglob, double* __restrict__ V,
+                                               double* __restrict__ Aglob, double* V,
                                                double* __restrict__ lam, double* __restrict__ vout, int max_sweeps) {
     extern __shared__ double sm[];
+    const int la = w | 1;  // odd leading dimension: row rotations (stride la) hit distinct banks
     double* A = Aglob ? Aglob : sm;
+    if (!V) V = sm + w * la;  // V in shared memory after A (sym_eig sizes the allocation)
     __shared__ int pos[512];
     __shared__ double cs[256], sn[256], np_[256], nq_[256];
     __shared__ int pp[256], qq[256];
@@ -293,18 +295,19 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
     const int half = wp / 2;
     for (int j = warp; j < w; j += NW)
         for (int i = lane; i < w; i += 32) {
-            A[i + j * w] = g[i + j * ldg];
-            V[i + j * w] = i == j ? 1.0 : 0.0;
+            A[i + j * la] = g[i + j * ldg];
+            V[i + j * la] = i == j ? 1.0 : 0.0;
         }
     for (int i = threadIdx.x; i < wp; i += ST) pos[i] = i;
     // absolute floor: off-diagonal rounding noise of the input (≈ eps·‖G‖) is not rotated away
     if (threadIdx.x == 0) {
         double f = 0.0;
         for (int j = 0; j < w; ++j) f = fmax(f, fabs(g[j + j * ldg]));
-        floor_abs = 1e-17 * f * (double)w;
+        floor_abs = 1e-16 * f * (double)w;
     }
     __syncthreads();
-    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    const int msw = max_sweeps < 0 ? -max_sweeps : max_sweeps;
+    for (int sweep = 0; sweep < msw; ++sweep) {
         if (threadIdx.x == 0) rotated = 0;
         __syncthreads();
         for (int round = 0; round < wp - 1; ++round) {
@@ -316,9 +319,9 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, s = 0.0;
                 if (q < w) {
-                    const double apq = A[p + q * w];
-                    const double app = A[p + p * w], aqq = A[q + q * w];
-                    if (fabs(apq) > floor_abs && apq * apq > 1e-32 * fabs(app * aqq)) {
+                    const double apq = A[p + q * la];
+                    const double app = A[p + p * la], aqq = A[q + q * la];
+                    if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(app * aqq)) {  // |apq| > 1e-15·√|app·aqq|
                         // rotation from rsqrt/rcp approximations refined to ~1 ulp (the
                         // IEEE sqrt/div sequences made each round a long serial chain)
                         const double tau = (aqq - app) * fast_rcp(2.0 * apq);
@@ -344,9 +347,9 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                 if (q >= w || sn[i] == 0.0) continue;
                 const double c = cs[i], s = sn[i];
                 for (int k = lane; k < w; k += 32) {
-                    const double ap = A[p + k * w], aq = A[q + k * w];
-                    A[p + k * w] = c * ap - s * aq;
-                    A[q + k * w] = s * ap + c * aq;
+                    const double ap = A[p + k * la], aq = A[q + k * la];
+                    A[p + k * la] = c * ap - s * aq;
+                    A[q + k * la] = s * ap + c * aq;
                 }
             }
             __syncthreads();
@@ -356,27 +359,29 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
                 if (q >= w || sn[i] == 0.0) continue;
                 const double c = cs[i], s = sn[i];
                 for (int k = lane; k < w; k += 32) {
-                    const double ap = A[k + p * w], aq = A[k + q * w];
-                    A[k + p * w] = c * ap - s * aq;
-                    A[k + q * w] = s * ap + c * aq;
-                    const double vp = V[k + p * w], vq = V[k + q * w];
-                    V[k + p * w] = c * vp - s * vq;
-                    V[k + q * w] = s * vp + c * vq;
+                    const double ap = A[k + p * la], aq = A[k + q * la];
+                    A[k + p * la] = c * ap - s * aq;
+                    A[k + q * la] = s * ap + c * aq;
+                    const double vp = V[k + p * la], vq = V[k + q * la];
+                    V[k + p * la] = c * vp - s * vq;
+                    V[k + q * la] = s * vp + c * vq;
+                }
+                // the rotated pair is annihilated exactly (rounding noise would retrigger
+                // rotations); columns p and q belong to this warp alone in this phase
+                __syncwarp();
+                if (lane == 0) {
+                    A[p + q * la] = 0.0;
+                    A[q + p * la] = 0.0;
+                    A[p + p * la] = np_[i];
+                    A[q + q * la] = nq_[i];
                 }
             }
             __syncthreads();
-            // the rotated pair is annihilated exactly (rounding noise would retrigger rotations)
-            for (int i = threadIdx.x; i < half; i += ST) {
-                const int p = pp[i], q = qq[i];
-                if (q >= w || sn[i] == 0.0) continue;
-                A[p + q * w] = 0.0;
-                A[q + p * w] = 0.0;
-                A[p + p * w] = np_[i];
-                A[q + q * w] = nq_[i];
-            }
-            __syncthreads();
         }
-        if (!rotated) break;
+        if (!rotated) {
+            if (threadIdx.x == 0 && max_sweeps < 0) printf("jacobi w=%d sweeps=%d\n", w, sweep + 1);
+            break;
+        }
         __syncthreads();
     }
     // sort eigenvalues descending (stable selection on indices), permute V
@@ -386,14 +391,14 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
         for (int i = 0; i < w; ++i) {
             int best = i;
             for (int j = i + 1; j < w; ++j)
-                if (A[order[j] + order[j] * w] > A[order[best] + order[best] * w]) best = j;
+                if (A[order[j] + order[j] * la] > A[order[best] + order[best] * la]) best = j;
             const int t = order[i]; order[i] = order[best]; order[best] = t;
         }
     }
     __syncthreads();
     for (int j = warp; j < w; j += NW)
-        for (int i = lane; i < w; i += 32) vout[i + j * w] = V[i + order[j] * w];
-    for (int j = threadIdx.x; j < w; j += ST) lam[j] = A[order[j] + order[j] * w];
+        for (int i = lane; i < w; i += 32) vout[i + j * w] = V[i + order[j] * la];
+    for (int j = threadIdx.x; j < w; j += ST) lam[j] = A[order[j] + order[j] * la];
 }
 
 void ensure_attrs() {
@@ -454,11 +459,20 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
     if (w > 512) fail(BCUR_E_INVALID_ARGUMENT, "sym_eig: w > 512 not supported");
     ensure_attrs();
     ProfScope prof(c, "sym_eig", 0.0, 8.0 * w * w);
-    DevBuf work, vtmp(c, (size_t)w * w * sizeof(double));
+    // A and V both in shared memory when they fit (every rotation updates two rows and
+    // two columns of each; a global V made a 64×64 solve take 3.4 ms)
+    const size_t mat = (size_t)w * (size_t)(w | 1) * sizeof(double);
+    DevBuf work, vtmp;
     size_t smem = 0;
-    if (w <= SMEM_MAX_W) smem = (size_t)w * w * sizeof(double);
-    else work = DevBuf(c, (size_t)w * w * sizeof(double));
-    k_jacobi<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, work.as<double>(), vtmp.as<double>(), lam, v, 40);
+    if (2 * mat <= 200 * 1024) {
+        smem = 2 * mat;
+    } else {
+        vtmp = DevBuf(c, mat);
+        if (w <= SMEM_MAX_W) smem = mat;
+        else work = DevBuf(c, mat);
+    }
+    static const int dbg = getenv("BCUR_JACOBI_DEBUG") ? -1 : 1;
+    k_jacobi<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, work.as<double>(), vtmp.as<double>(), lam, v, 40 * dbg);
     LAUNCH_CHECK(c);
 }
 

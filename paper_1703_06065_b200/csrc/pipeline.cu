@@ -194,6 +194,57 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
             if (T_out) *T_out = Mat64(c, 0, w);
             return 0;
         }
+        if (!dist && rows < w) {
+            // wide panel (e.g. 64 × 100 biometric blocks): the same nonzero spectrum from the
+            // rows × rows Gram X·Xᵀ, whose eigenvectors are the orthonormal basis directly
+            Mat64 Gr(c, rows, rows), lam(c, rows, 1), U(c, rows, rows);
+            gemm(c, OP_N, OP_T, rows, rows, w, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, Gr.p(), Gr.ld);
+            {   // safely full row rank → range(X) = ℝ^rows: Q = I, T = X (no eigensolve)
+                Mat64 Rr(c, rows, rows);
+                const CholInfo cr = chol_any(c, Gr.p(), rows, Gr.ld, Rr.p(), Dv.p());
+                if (cr.info == 0 && std::isfinite(cr.mindiag) && cr.mindiag > tau_chol(dt) * ref) {
+                    fill_f64(c, Q1.p(), rows * rows, 0.0);
+                    Mat64 one(c, rows, 1);
+                    fill_f64(c, one.p(), rows, 1.0);
+                    CUDA_CHECK(cudaMemcpy2DAsync(Q1.p(), (Q1.ld + 1) * sizeof(double), one.p(), sizeof(double),
+                                                 sizeof(double), rows, cudaMemcpyDeviceToDevice, c->stream));
+                    copy_f64(c, Q1.p(), rows, rows, Q1.ld, Q, ldq);
+                    if (T_out) {
+                        Mat64 T(c, rows, w);
+                        copy_f64(c, X, rows, w, ldx, T.p(), T.ld);
+                        *T_out = std::move(T);
+                    }
+                    if (path_out) *path_out = 1;
+                    return rows;
+                }
+            }
+            sym_eig(c, Gr.p(), rows, Gr.ld, lam.p(), U.p());
+            std::vector<double> lh(rows);
+            d2h(c, lh.data(), lam.p(), rows);
+            r = 0;
+            for (int64_t i = 0; i < rows; ++i)
+                if (std::sqrt(std::max(lh[i], 0.0)) > tau_rank(dt) * ref) ++r;
+            if (r == 0) {
+                if (path_out) *path_out = 1;
+                if (T_out) *T_out = Mat64(c, 0, w);
+                return 0;
+            }
+            copy_f64(c, U.p(), rows, r, U.ld, Q1.p(), Q1.ld);
+            Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
+            gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
+            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p());
+            if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
+            tri_inv_any(c, R2.p(), r, R2i.p(), Dv.p());
+            gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
+            if (T_out) {  // T = R2 · (Q1ᵀ X)
+                Mat64 QX(c, r, w), T(c, r, w);
+                gemm(c, OP_T, OP_N, r, w, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, X, BCUR_F64, ldx, 0.0, QX.p(), QX.ld);
+                gemm(c, OP_N, OP_N, r, w, r, 1.0, R2.p(), BCUR_F64, R2.ld, QX.p(), BCUR_F64, QX.ld, 0.0, T.p(), T.ld);
+                *T_out = std::move(T);
+            }
+            if (path_out) *path_out = 1;
+            return r;
+        }
         Mat64 lam(c, w, 1), V(c, w, w);
         sym_eig(c, G.p(), w, G.ld, lam.p(), V.p());
         std::vector<double> lh(w);
