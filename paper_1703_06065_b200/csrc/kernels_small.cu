@@ -401,6 +401,98 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
     for (int j = threadIdx.x; j < w; j += ST) lam[j] = A[order[j] + order[j] * la];
 }
 
+// ------------------------------------------------ one-sided Jacobi (large w)
+// Hestenes one-sided Jacobi on a symmetric PSD G (its singular values are its
+// eigenvalues): column pairs of W = G·V are orthogonalised in the same circle-method
+// rounds; only column operations (coalesced, in an L2-resident global scratch), one
+// barrier per round.  λ_i = ‖W e_i‖, eigenvectors = V e_i.  Used when G does not fit in
+// shared memory (the two-sided rotations' row updates would be uncoalesced there).
+__global__ void __launch_bounds__(ST) k_jacobi1s(const double* __restrict__ g, int w, int64_t ldg,
+                                                 double* __restrict__ W, double* __restrict__ V,
+                                                 double* __restrict__ lam, double* __restrict__ vout, int max_sweeps) {
+    __shared__ int rotated;
+    __shared__ int order[512];
+    __shared__ double nrm[512];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wp = (w + 1) & ~1, half = wp / 2, mrot = wp - 1;
+    for (int j = warp; j < w; j += NW)
+        for (int i = lane; i < w; i += 32) {
+            W[i + (int64_t)j * w] = g[i + (int64_t)j * ldg];
+            V[i + (int64_t)j * w] = i == j ? 1.0 : 0.0;
+        }
+    __syncthreads();
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        if (threadIdx.x == 0) rotated = 0;
+        __syncthreads();
+        for (int round = 0; round < mrot; ++round) {
+            for (int i = warp; i < half; i += NW) {
+                int p = i == 0 ? round : (round + i) % mrot;
+                int q = i == 0 ? mrot : (round - i + mrot) % mrot;
+                if (p > q) { const int t = p; p = q; q = t; }
+                if (q >= w) continue;
+                double* wp_ = W + (int64_t)p * w;
+                double* wq_ = W + (int64_t)q * w;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int k = lane; k < w; k += 32) {
+                    const double x = wp_[k], y = wq_[k];
+                    al = fma(x, x, al);
+                    be = fma(y, y, be);
+                    ga = fma(x, y, ga);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    al += __shfl_xor_sync(0xffffffffu, al, o);
+                    be += __shfl_xor_sync(0xffffffffu, be, o);
+                    ga += __shfl_xor_sync(0xffffffffu, ga, o);
+                }
+                if (!(ga * ga > 1e-30 * al * be) || ga == 0.0) continue;  // |γ| ≤ 1e-15·√(αβ): orthogonal
+                const double zeta = (be - al) * fast_rcp(2.0 * ga);
+                const double q2 = fma(zeta, zeta, 1.0);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(zeta) + q2 * rsqrt(q2));
+                const double c = rsqrt(fma(t, t, 1.0)), s = t * c;
+                double* vp = V + (int64_t)p * w;
+                double* vq = V + (int64_t)q * w;
+                for (int k = lane; k < w; k += 32) {
+                    const double x = wp_[k], y = wq_[k];
+                    wp_[k] = c * x - s * y;
+                    wq_[k] = s * x + c * y;
+                    const double a = vp[k], b = vq[k];
+                    vp[k] = c * a - s * b;
+                    vq[k] = s * a + c * b;
+                }
+                if (lane == 0) rotated = 1;
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+        __syncthreads();
+    }
+    for (int j = warp; j < w; j += NW) {
+        double s = 0.0;
+        for (int k = lane; k < w; k += 32) {
+            const double x = W[k + (int64_t)j * w];
+            s = fma(x, x, s);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) nrm[j] = sqrt(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < w; ++i) order[i] = i;
+        for (int i = 0; i < w; ++i) {
+            int best = i;
+            for (int j = i + 1; j < w; ++j)
+                if (nrm[order[j]] > nrm[order[best]]) best = j;
+            const int t = order[i]; order[i] = order[best]; order[best] = t;
+        }
+    }
+    __syncthreads();
+    for (int j = warp; j < w; j += NW)
+        for (int i = lane; i < w; i += 32) vout[i + (int64_t)j * w] = V[i + (int64_t)order[j] * w];
+    for (int j = threadIdx.x; j < w; j += ST) lam[j] = nrm[order[j]];
+}
+
 void ensure_attrs() {
     static bool attr = false;
     if (!attr) {
@@ -464,13 +556,14 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
     const size_t mat = (size_t)w * (size_t)(w | 1) * sizeof(double);
     DevBuf work, vtmp;
     size_t smem = 0;
-    if (2 * mat <= 200 * 1024) {
-        smem = 2 * mat;
-    } else {
-        vtmp = DevBuf(c, mat);
-        if (w <= SMEM_MAX_W) smem = mat;
-        else work = DevBuf(c, mat);
+    if (2 * mat > 200 * 1024) {  // too big for shared memory: one-sided, column-coalesced
+        work = DevBuf(c, (size_t)w * w * sizeof(double));
+        vtmp = DevBuf(c, (size_t)w * w * sizeof(double));
+        k_jacobi1s<<<1, ST, 0, c->stream>>>(g, (int)w, ldg, work.as<double>(), vtmp.as<double>(), lam, v, 40);
+        LAUNCH_CHECK(c);
+        return;
     }
+    smem = 2 * mat;
     static const int dbg = getenv("BCUR_JACOBI_DEBUG") ? -1 : 1;
     k_jacobi<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, work.as<double>(), vtmp.as<double>(), lam, v, 40 * dbg);
     LAUNCH_CHECK(c);

@@ -734,8 +734,23 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
         return;
     }
     const int nt = (int)((N + NT * BN - 1) / (NT * BN));
-    const Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, sym, false);
-    launch_umma<false, EPI_STORE>(c, NT, sc, ta, th, tl, (int)n, (int)N, out, ldo, nullptr, alpha, beta);
+    // split K (the m rows) when there are fewer output tiles than SMs (a thin Q_Cᵀ·P of
+    // the greedy CGS2 has ≤ 64 tiles of 2048 stages each); fp64 partials, ordered reduce
+    const int tiles = sym ? nt * (nt + 1) / 2 : mt * nt;
+    int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c->sm_count + tiles - 1) / tiles, k_tiles / 32));
+    const int kps = (k_tiles + splits - 1) / splits;
+    splits = (k_tiles + kps - 1) / kps;
+    const Sched sc = make_sched(mt, nt, splits, k_tiles, kps, sym, false);
+    if (splits == 1) {
+        launch_umma<false, EPI_STORE>(c, NT, sc, ta, th, tl, (int)n, (int)N, out, ldo, nullptr, alpha, beta);
+        return;
+    }
+    DevBuf part(c, (size_t)splits * n * N * sizeof(double));
+    if (sym) CUDA_CHECK(cudaMemsetAsync(part.ptr, 0, part.bytes, c->stream));  // skipped lower tiles
+    launch_umma<false, EPI_STORE>(c, NT, sc, ta, th, tl, (int)n, (int)N, nullptr, 0, part.as<double>(), 1.0, 0.0);
+    k_reduce_splits<<<(unsigned)((n * N + 255) / 256), 256, 0, c->stream>>>(n, N, splits, part.as<double>(), out, ldo,
+                                                                            alpha, beta);
+    LAUNCH_CHECK(c);
 }
 
 // Out(m×N) = alpha·A X + beta·Out  (A m×n fp32; X n×N fp32/fp64), split-K over n with fp64

@@ -94,6 +94,21 @@ def test_range_finder_matches_oracle(B, dt):
                      O.block_sums(np.sum(ref.v_k ** 2, axis=1), part), dt)
 
 
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_range_finder_wide_sketch_one_sided_jacobi(B, dt):
+    # ℓ = k + p = 130: the ℓ×ℓ eigenproblem no longer fits shared memory and runs on the
+    # one-sided (column-coalesced) Jacobi — same subspace, same σ as the oracle
+    a = lowrank(700, 2400, 150, "pow:1", 1e-4, 5, dt)
+    key = O.omega_key_from_seed(6)
+    got = B.range_finder(a, 120, 10, 1, key)
+    ref = O.range_finder(a, 120, 10, 1, key)
+    assert got.k_eff == ref.k_eff
+    np.testing.assert_allclose(got.sigma, ref.sigma[:got.k_eff], rtol=1e-9 if dt == np.float64 else 1e-5)
+    part = O.BlockPartition.equal_blocks(2400, 40)
+    check_scores(O.block_sums(np.sum(got.v_k ** 2, axis=1), part),
+                 O.block_sums(np.sum(ref.v_k ** 2, axis=1), part), dt)
+
+
 def test_config1_full(B):
     c = O.CONFIGS["c1"]
     a = lowrank(c["m"], c["n"], c["rank"], c["spectrum"], c["noise"], c["seed"], np.float64)
