@@ -16,6 +16,15 @@ constexpr int ST = 1024;
 // 1/x to full double precision from the hardware approximation + two Newton steps (the
 // IEEE-exact division is a long software sequence that sat on the factorizations'
 // serial critical paths).
+// 1/√x to full double precision: hardware approximation + two Newton steps (4 DFMA deep)
+__device__ __forceinline__ double fast_rsqrt(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double hx = 0.5 * x;
+    r = r * fma(-hx * r, r, 1.5);
+    r = r * fma(-hx * r, r, 1.5);
+    return r;
+}
 __device__ __forceinline__ double fast_rcp(double x) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
@@ -98,6 +107,7 @@ __global__ void __launch_bounds__(CP_T) k_chol_panel(const double* g, int w, int
     extern __shared__ double smc[];
     double* M = smc;                    // lower triangle, M[i + k·LD] (i ≥ k), padded with identity
     __shared__ double invd[CP_MAX];
+    __shared__ double xch[32];
     __shared__ int stop_sh;
     __shared__ double mn_sh;
     if (chained && *info != 0) return;
@@ -123,7 +133,10 @@ __global__ void __launch_bounds__(CP_T) k_chol_panel(const double* g, int w, int
         if (warp == 0) {
             double a[32];
 #pragma unroll
-            for (int k = 0; k < 32; ++k) a[k] = k <= lane ? M[(c0 + lane) + (c0 + k) * CP_LD] : 0.0;
+            // row `lane` of the block; entries k > lane are upper-triangle garbage that is
+            // updated harmlessly and never stored or read for a lower entry (no per-lane
+            // predicates in the step: they cost more than the arithmetic)
+            for (int k = 0; k < 32; ++k) a[k] = M[(c0 + lane) + (c0 + k) * CP_LD];
             int bad = 0;
             double mn = INFINITY, dl = 1.0;  // dl: this lane's 1/r_ii
 #pragma unroll
@@ -131,16 +144,18 @@ __global__ void __launch_bounds__(CP_T) k_chol_panel(const double* g, int w, int
                 const double d = __shfl_sync(0xffffffffu, a[j], j);
                 if (!bad && (!(d > 0.0) || !isfinite(d))) bad = c0 + j + 1;
                 if (bad) continue;
-                const double ri = rsqrt(d), rj = d * ri;
+                const double ri = fast_rsqrt(d), rj = d * ri;
                 if (c0 + j < w) mn = fmin(mn, rj);  // padding pivots are 1
                 if (lane == j) dl = ri;
-                const double lij = a[j] * ri;  // l(lane, j) for lane > j
-                a[j] = lane == j ? rj : (lane > j ? lij : 0.0);
+                const double lij = a[j] * ri;  // l(lane, j) for lane > j (garbage above)
+                a[j] = lane == j ? rj : lij;
+                // multipliers exchanged through shared memory (broadcast loads pipeline;
+                // 31 dependent-issue double shuffles per step dominated the step time)
+                xch[lane] = lij;
+                __syncwarp();
 #pragma unroll
-                for (int k = j + 1; k < 32; ++k) {
-                    const double lkj = __shfl_sync(0xffffffffu, lij, k);
-                    if (lane >= k) a[k] = fma(-lij, lkj, a[k]);
-                }
+                for (int k = j + 1; k < 32; ++k) a[k] = fma(-lij, xch[k], a[k]);
+                __syncwarp();
             }
             if (!bad) {
 #pragma unroll
@@ -159,14 +174,17 @@ __global__ void __launch_bounds__(CP_T) k_chol_panel(const double* g, int w, int
         if (nr <= 0) break;
         // (2) TRSM: row i of the panel below the diagonal block, x = m · L_ppᵀ⁻¹
         if (tid < nr) {
+            // right-looking: each solved x_c immediately updates every later entry, so the
+            // dependent chain is 2 ops per column (a dot-product form is a 528-deep chain)
             const int i = base + tid;
             double x[32];
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-                double s = M[i + (c0 + c) * CP_LD];
+            for (int c = 0; c < 32; ++c) x[c] = M[i + (c0 + c) * CP_LD];
 #pragma unroll
-                for (int cc = 0; cc < c; ++cc) s = fma(-x[cc], M[(c0 + c) + (c0 + cc) * CP_LD], s);
-                x[c] = s * invd[c0 + c];
+            for (int c = 0; c < 32; ++c) {
+                x[c] *= invd[c0 + c];
+#pragma unroll
+                for (int cc = c + 1; cc < 32; ++cc) x[cc] = fma(-x[c], M[(c0 + cc) + (c0 + c) * CP_LD], x[cc]);
             }
 #pragma unroll
             for (int c = 0; c < 32; ++c) M[i + (c0 + c) * CP_LD] = x[c];
