@@ -688,7 +688,7 @@ def column_basis(a64: np.ndarray, part: BlockPartition, blocks: Sequence[int], d
     full rank, else block CGS2 panels with per-panel rank revealing."""
     m = a64.shape[0]
     ub = unique_in_order(blocks)
-    if allow_whole and np.dtype(dt) == np.float32:
+    if allow_whole:
         cols = np.concatenate([a64[:, part.ranges[b][0]:part.ranges[b][1]] for b in ub], axis=1)
         q = cholqr2_whole(cols, dt)
         if q is not None:

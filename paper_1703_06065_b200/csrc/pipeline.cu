@@ -342,24 +342,29 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
     return r;
 }
 
-// Whole-matrix CholQR2 of an fp32 C (rows × cc) on the tensor cores, written to B.
-// Returns false (B untouched) when C is not safely full rank (oracle.cholqr2_whole).
-static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
+// Whole-matrix CholQR2 of C (rows × cc; fp32 on the tensor cores, fp64 on DGEMM), written
+// to B.  Returns false (B untouched) when C is not safely full rank (oracle.cholqr2_whole).
+static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
     if (cc == 0 || rows < cc) return false;
     Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
-    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, BCUR_F32, rows, C, BCUR_F32, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
+    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, cdt, rows, C, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
     const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p());
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     tri_inv_any(c, R.p(), cc, Ri.p(), Dv.p());
-    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
+    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
          GEMM_B_UPPER);
-    DevBuf q1f(c, (size_t)rows * cc * 4);
-    convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, q1f.ptr, BCUR_F32, rows);
-    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, q1f.ptr, BCUR_F32, rows, q1f.ptr, BCUR_F32, rows, 0.0, G.p(), G.ld,
-         GEMM_SYM_UPPER);
+    // Q1 in the basis dtype (fp32 → every later product with it runs on the tensor cores)
+    DevBuf q1f;
+    const void* q1 = Q1.p();
+    if (cdt == BCUR_F32) {
+        q1f = DevBuf(c, (size_t)rows * cc * 4);
+        convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, q1f.ptr, BCUR_F32, rows);
+        q1 = q1f.ptr;
+    }
+    gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, q1, cdt, rows, q1, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
     // Second pass.  Q1ᵀQ1 = I + E with ‖E‖ ~ 1e-7·κ(C)²; when ‖E‖_max < 1e-4 the Cholesky
     // factor is R2 = I + F + O(‖E‖²), F = strict_upper(E) + diag(E)/2, so R2⁻¹ = I − F to
@@ -375,10 +380,15 @@ static bool cholqr2_whole(Ctx* c, const float* C, int64_t rows, int64_t cc, bool
         if (c2.info != 0) return false;
         tri_inv_any(c, R.p(), cc, Ri.p(), Dv.p());
     }
-    gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1f.ptr, BCUR_F32, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
-         GEMM_B_UPPER);
-    B->init(c, BCUR_F32, rows, cc);
-    convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
+    B->init(c, cdt, rows, cc);
+    if (cdt == BCUR_F32) {
+        gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
+             GEMM_B_UPPER);
+        convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
+    } else {
+        gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, (double*)B->buf.ptr,
+             rows, GEMM_B_UPPER);
+    }
     B->rank = cc;
     return true;
 }
@@ -474,22 +484,25 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
     const int64_t m = a->m;
     int64_t cap = 0;
     for (int64_t b : blocks) cap += s.off_global[b + 1] - s.off_global[b];
-    if (a->dtype == BCUR_F32 && cap > 0) {
-        DevBuf cf(c, (size_t)m * cap * 4);
+    if (cap > 0 && cap <= m) {  // whole-C CholQR2 first (oracle.column_basis)
+        const int cdt = a->dtype;
+        const size_t es = dtype_size(cdt);
+        DevBuf cf(c, (size_t)m * cap * es);
         int64_t at = 0;
         for (int64_t b : blocks) {
             const int64_t w = s.off_global[b + 1] - s.off_global[b];
+            char* dst = (char*)cf.ptr + (size_t)at * m * es;
             if (c->comm.world <= 1) {
-                convert(c, (const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * 4, BCUR_F32, m, w, a->ld,
-                        (float*)cf.ptr + at * m, BCUR_F32, m);
+                convert(c, (const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * es, cdt, m, w, a->ld, dst,
+                        cdt, m);
             } else {
                 Mat64 P(c, m, w);
                 block_panel(c, a, s, b, P.p());
-                convert(c, P.p(), BCUR_F64, m, w, m, (float*)cf.ptr + at * m, BCUR_F32, m);
+                convert(c, P.p(), BCUR_F64, m, w, m, dst, cdt, m);
             }
             at += w;
         }
-        if (cholqr2_whole(c, cf.as<float>(), m, cap, false, a->dtype, B)) return;
+        if (cholqr2_whole(c, cf.ptr, cdt, m, cap, false, a->dtype, B)) return;
     }
     B->init(c, a->dtype == BCUR_F32 ? BCUR_F32 : BCUR_F64, m, cap);
     for (int64_t b : blocks) {
@@ -774,7 +787,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     }
     Basis QR;
     bool whole = false;
-    if (bdt == BCUR_F32 && ru > 0) whole = cholqr2_whole(c, rtu.as<float>(), nl, ru, dist, dt, &QR);
+    if (ru > 0) whole = cholqr2_whole(c, rtu.ptr, bdt, nl, ru, dist, dt, &QR);
     if (!whole) {
         QR.init(c, bdt, nl, ru);
         for (size_t i = 0; i < rb.size(); ++i) {
