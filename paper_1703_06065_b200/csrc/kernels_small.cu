@@ -309,14 +309,15 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
     __shared__ int rotated;
     __shared__ double floor_abs;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int NWB = blockDim.x >> 5, NTB = blockDim.x;  // (256 threads measured slower for w = 64)
     const int wp = (w + 1) & ~1;  // even number of players (w..wp-1 is a bye)
     const int half = wp / 2;
-    for (int j = warp; j < w; j += NW)
+    for (int j = warp; j < w; j += NWB)
         for (int i = lane; i < w; i += 32) {
             A[i + j * la] = g[i + j * ldg];
             V[i + j * la] = i == j ? 1.0 : 0.0;
         }
-    for (int i = threadIdx.x; i < wp; i += ST) pos[i] = i;
+    for (int i = threadIdx.x; i < wp; i += NTB) pos[i] = i;
     // absolute floor: off-diagonal rounding noise of the input (≈ eps·‖G‖) is not rotated away
     if (threadIdx.x == 0) {
         double f = 0.0;
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
         if (threadIdx.x == 0) rotated = 0;
         __syncthreads();
         for (int round = 0; round < wp - 1; ++round) {
-            for (int i = threadIdx.x; i < half; i += ST) {
+            for (int i = threadIdx.x; i < half; i += NTB) {
                 // circle method: player wp-1 fixed, the others rotate (all pairs in wp-1 rounds)
                 const int mrot = wp - 1;
                 int p = i == 0 ? round : (round + i) % mrot;
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
             }
             __syncthreads();
             // rows: A ← Jᵀ A   (warp per pair, lanes over columns)
-            for (int i = warp; i < half; i += NW) {
+            for (int i = warp; i < half; i += NWB) {
                 const int p = pp[i], q = qq[i];
                 if (q >= w || sn[i] == 0.0) continue;
                 const double c = cs[i], s = sn[i];
@@ -372,7 +373,7 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
             }
             __syncthreads();
             // columns: A ← A J, V ← V J   (coalesced along the column)
-            for (int i = warp; i < half; i += NW) {
+            for (int i = warp; i < half; i += NWB) {
                 const int p = pp[i], q = qq[i];
                 if (q >= w || sn[i] == 0.0) continue;
                 const double c = cs[i], s = sn[i];
@@ -414,9 +415,9 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
         }
     }
     __syncthreads();
-    for (int j = warp; j < w; j += NW)
+    for (int j = warp; j < w; j += NWB)
         for (int i = lane; i < w; i += 32) vout[i + j * w] = V[i + order[j] * la];
-    for (int j = threadIdx.x; j < w; j += ST) lam[j] = A[order[j] + order[j] * la];
+    for (int j = threadIdx.x; j < w; j += NTB) lam[j] = A[order[j] + order[j] * la];
 }
 
 // ------------------------------------------------ one-sided Jacobi (large w)
