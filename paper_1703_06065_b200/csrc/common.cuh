@@ -78,6 +78,7 @@ struct Ctx {
         if (it != free_list.end()) {
             void* p = it->second;
             free_list.erase(it);
+            pooled_bytes -= want;
             return p;
         }
         void* p = nullptr;
@@ -94,6 +95,7 @@ struct Ctx {
     void release(void* p) {
         if (!p) return;
         free_list.emplace(sizes[p], p);
+        pooled_bytes += sizes[p];
     }
     void trim() {
         cudaStreamSynchronize(stream);
@@ -102,7 +104,9 @@ struct Ctx {
             sizes.erase(kv.second);
         }
         free_list.clear();
+        pooled_bytes = 0;
     }
+    bool cached(size_t bytes) const { return free_list.count(round(bytes)) > 0; }
     static size_t round(size_t b) {
         if (b <= 256) return 256;
         size_t p = 256;
@@ -184,6 +188,14 @@ struct DMat {
     int64_t col0 = 0, n_global = 0;  // column shard
     size_t bytes() const { return (size_t)ld * (size_t)n * dtype_size(dtype); }
 };
+
+// Round an fp32 value to the nearest TF32 (10-bit mantissa), ties to even — the rounding
+// of the X1 (1×TF32) tensor-core passes, shared by the kernels that pre-round A.
+__device__ __forceinline__ float rn_tf32_dev(float x) {
+    uint32_t u = __float_as_uint(x);
+    u += 0xFFFu + ((u >> 13) & 1u);
+    return __uint_as_float(u & 0xFFFFE000u);
+}
 
 // Lightweight non-owning view used by kernels wrappers.
 template <class T>

@@ -274,10 +274,10 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
 }
 
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
-                   const void* B, int dtb, int64_t ldb, double* rowsq) {
+                   const void* B, int dtb, int64_t ldb, double* rowsq, bool a_rounded) {
     if (M <= 0) return;
     if (ta == OP_T && tb == OP_N && dta == BCUR_F32 && N > 0 && K > 0 && umma_ok(dta, K, lda, A)) {
-        umma_atx(c, (const float*)A, K, M, lda, B, dtb, N, ldb, 1.0, 0.0, nullptr, 0, rowsq);
+        umma_atx(c, (const float*)A, K, M, lda, B, dtb, N, ldb, 1.0, 0.0, nullptr, 0, rowsq, false, a_rounded);
         return;
     }
     ProfScope prof(c, (dta == BCUR_F32 || dtb == BCUR_F32) ? "gemm_rowsumsq_f32" : "gemm_rowsumsq_f64",

@@ -35,11 +35,14 @@ __device__ double block_sum(double s) {
     return t;  // valid in thread 0
 }
 
+// Σ col[i]²; fp32 columns optionally also write their TF32-rounded copy to `shadow`
+// (one read of A serves the norms and the pre-rounded operand of the X1 passes).
 template <class T>
-__device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, bool vec) {
+__device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, bool vec, float* __restrict__ shadow) {
     double s0 = 0.0, s1 = 0.0;
     if (vec && sizeof(T) == 4) {
         const float4* c4 = reinterpret_cast<const float4*>(col);
+        float4* sh4 = reinterpret_cast<float4*>(shadow);
         const int64_t m4 = m >> 2;
         for (int64_t i = threadIdx.x; i < m4; i += RT) {
             const float4 v = __ldcs(c4 + i);
@@ -47,10 +50,13 @@ __device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, b
             s1 = fma((double)v.y, (double)v.y, s1);
             s0 = fma((double)v.z, (double)v.z, s0);
             s1 = fma((double)v.w, (double)v.w, s1);
+            if (shadow)
+                __stcs(sh4 + i, make_float4(rn_tf32_dev(v.x), rn_tf32_dev(v.y), rn_tf32_dev(v.z), rn_tf32_dev(v.w)));
         }
         for (int64_t i = (m4 << 2) + threadIdx.x; i < m; i += RT) {
             const double v = (double)col[i];
             s0 = fma(v, v, s0);
+            if (shadow) shadow[i] = rn_tf32_dev((float)v);
         }
     } else if (vec) {
         const double2* c2 = reinterpret_cast<const double2*>(col);
@@ -68,6 +74,7 @@ __device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, b
         for (int64_t i = threadIdx.x; i < m; i += RT) {
             const double v = (double)col[i];
             s0 = fma(v, v, s0);
+            if (shadow) shadow[i] = rn_tf32_dev((float)v);
         }
     }
     return s0 + s1;
@@ -77,11 +84,13 @@ __device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, b
 template <class T>
 __global__ void __launch_bounds__(RT) k_block_sumsq(const T* __restrict__ a, int64_t m, int64_t ld,
                                                     const int64_t* __restrict__ off, int Z, bool vec,
-                                                    double* __restrict__ partial) {
+                                                    double* __restrict__ partial, float* __restrict__ shadow,
+                                                    int64_t lds) {
     const int64_t g = blockIdx.x;
     const int z = blockIdx.y;
     double s = 0.0;
-    for (int64_t j = off[g] + z; j < off[g + 1]; j += Z) s += sq_col(a + j * ld, m, vec);
+    for (int64_t j = off[g] + z; j < off[g + 1]; j += Z)
+        s += sq_col(a + j * ld, m, vec, shadow ? shadow + j * lds : nullptr);
     s = block_sum(s);
     if (threadIdx.x == 0) partial[g * Z + z] = s;
 }
@@ -152,7 +161,7 @@ __global__ void k_max_dev_identity(const double* __restrict__ g, int w, int64_t 
 namespace ops {
 
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
-                 double* d_out) {
+                 double* d_out, float* shadow, int64_t lds) {
     if (G <= 0) return;
     ProfScope prof(c, "block_sumsq", 0.0, 0.0);
     // enough CTAs to fill the machine several times over
@@ -162,9 +171,12 @@ void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int
     DevBuf part(c, (size_t)G * Z * sizeof(double));
     dim3 grid((unsigned)G, (unsigned)Z);
     if (dt == BCUR_F32)
-        k_block_sumsq<float><<<grid, RT, 0, c->stream>>>((const float*)a, m, ld, d_offsets, Z, vec, part.as<double>());
+        k_block_sumsq<float><<<grid, RT, 0, c->stream>>>((const float*)a, m, ld, d_offsets, Z,
+                                                         vec && (shadow == nullptr || (lds % 4 == 0)),
+                                                         part.as<double>(), shadow, lds);
     else
-        k_block_sumsq<double><<<grid, RT, 0, c->stream>>>((const double*)a, m, ld, d_offsets, Z, vec, part.as<double>());
+        k_block_sumsq<double><<<grid, RT, 0, c->stream>>>((const double*)a, m, ld, d_offsets, Z, vec, part.as<double>(),
+                                                          nullptr, 0);
     LAUNCH_CHECK(c);
     k_segment_rows<<<(unsigned)((G + 255) / 256), 256, 0, c->stream>>>(part.as<double>(), Z, G, d_out);
     LAUNCH_CHECK(c);

@@ -206,6 +206,7 @@ struct Sched {
     int m_tiles, n_tiles, splits, group_n, total;
     int k_tiles, kps, sym, tri_x;
     unsigned int* wave_ctr;
+    int a_rn;  // X1: A already rounded to TF32 (no transform)
 };
 // CTAs that have a tile in waves 0..w
 __device__ __forceinline__ unsigned int wave_arrivals(const Sched& sc, int w) {
@@ -507,7 +508,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                 mbar_wait(&full[s], (uint32_t)(gi / STAGES) & 1u);
                 if (X3) mbar_wait(&lo_empty[lr], ((uint32_t)(gi / LO_SLOTS) & 1u) ^ 1u);
                 const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(lr)) : src;
-                if (dbg & 1) {  // experiment switch: skip the transform (wrong results)
+                if ((dbg & 1) || (!X3 && sc.a_rn)) {  // pre-rounded A (or the experiment switch)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_arrive(&lo_ready[lr]);
                     continue;
@@ -653,6 +654,7 @@ Sched make_sched(int m_tiles, int n_tiles, int splits, int k_tiles, int kps, boo
     sc.tri_x = tri_x ? 1 : 0;
     sc.total = splits * (sym ? n_tiles * (n_tiles + 1) / 2 : m_tiles * n_tiles);
     sc.wave_ctr = nullptr;
+    sc.a_rn = 0;
     return sc;
 }
 
@@ -692,7 +694,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
 // Out(n×N) = alpha·Aᵀ X + beta·Out  (A m×n fp32 col-major; X m×N fp32/fp64) → fp64 store,
 // or rowsq[j] = Σ_c (AᵀX)_jc² (rowsq != nullptr; product never stored)
 void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq, bool sym) {
+              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq, bool sym,
+              bool a_rounded) {
     if (n <= 0 || N <= 0) {
         if (rowsq && n > 0) CUDA_CHECK(cudaMemsetAsync(rowsq, 0, n * sizeof(double), c->stream));
         return;
@@ -718,7 +721,8 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
         // steps) use fewer tiles and a deeper stage ring (HBM-bound regime).
         const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
         const int nt = (int)((N + NTX * BN - 1) / (NTX * BN));
-        const Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
+        Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
+        sc.a_rn = a_rounded ? 1 : 0;
         DevBuf part(c, (size_t)nt * NTX * n * sizeof(double));
         if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,

@@ -11,8 +11,9 @@ enum Op { OP_N = 0, OP_T = 1 };
 
 // ---- reductions (kernels_reduce.cu) --------------------------------------
 // out[g] = Σ_{j∈block g} Σ_i a(i,j)²  (fp64; offsets are device, relative to a's first column)
+// shadow (nullable, fp32 A only): also write the TF32-rounded copy of A (ld lds)
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
-                 double* d_out);
+                 double* d_out, float* shadow = nullptr, int64_t lds = 0);
 // out[j] = Σ_c v(j,c)²   then segmented into blocks: out_blocks[g]
 void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64_t ld, const int64_t* d_offsets,
                       int64_t G, double* d_rows /*nullable*/, double* d_blocks);
@@ -32,8 +33,9 @@ enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2 };
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags = 0);
 // rowsq[i] = Σ_j (op(A)·op(B))(i,j)²   (product never stored)
+// a_rounded: A is already rounded to TF32 (block_sumsq's shadow) — the X1 pass skips its transform
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
-                   const void* B, int dtb, int64_t ldb, double* rowsq);
+                   const void* B, int dtb, int64_t ldb, double* rowsq, bool a_rounded = false);
 // out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
@@ -47,7 +49,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
 // Out(n×N) = alpha·Aᵀ X + beta·Out (fp64) or rowsq[j] = Σ_c (AᵀX)_jc²; X fp32 or fp64.
 // sym: X holds the same matrix as A (a Gram) — only the upper triangle of Out is written.
 void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq, bool sym = false);
+              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, double* rowsq, bool sym = false,
+              bool a_rounded = false);
 // Out(m×N) = alpha·A X + beta·Out (fp64); X fp32 or fp64; x_upper_tri: X[k,j] = 0 for k > j
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri = false);

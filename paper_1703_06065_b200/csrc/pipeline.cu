@@ -513,11 +513,44 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
     }
 }
 
+// TF32-rounded copy of an fp32 A (ld m), written by the norms pass: the X1 row-Σ² passes
+// (residual, greedy scores) read it and skip their in-kernel rounding (shared-memory
+// bound).  Empty when A is fp64 or the copy does not fit in device memory.
+struct RoundedA {
+    DevBuf buf;
+    const float* ptr() const { return buf.as<float>(); }
+};
+static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra) {
+    if (a->dtype != BCUR_F32 || a->m % 4 != 0 || a->m <= 0 || a->n <= 0) return;
+    size_t freeb = 0, totalb = 0;
+    CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
+    const size_t need = (size_t)a->m * (size_t)a->n * 4;
+    const size_t headroom = (size_t)8 << 30;  // the rest of the pipeline's workspace
+    if (!c->cached(need)) {
+        if (need + headroom > freeb + c->pooled_bytes) return;  // does not fit: in-kernel rounding
+        if (need + headroom > freeb) c->trim();                  // make room from the workspace cache
+    }
+    ra->buf = DevBuf(c, need);
+}
+// A operand of the row-Σ² passes: the rounded copy when present
+static const void* rowsq_a(const DMat* a, const RoundedA* ra, int64_t* ld) {
+    if (ra && ra->buf.ptr) {
+        *ld = a->m;
+        return ra->buf.ptr;
+    }
+    *ld = a->ld;
+    return a->ptr;
+}
+
 // Σ_g ‖Qᵀ A_g‖² (shard-local per-block values in d_blk_local, allreduced total)
-static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local) {
+static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local,
+                             const RoundedA* ra = nullptr) {
     const int64_t nl = a->n;
     Mat64 rows(c, nl, 1), tot(c, 1, 1);
-    gemm_rowsumsq(c, OP_T, OP_N, nl, B.rank, a->m, a->ptr, a->dtype, a->ld, B.buf.ptr, B.dt, B.rows, rows.p());
+    int64_t lda = 0;
+    const void* ap = rowsq_a(a, ra, &lda);
+    gemm_rowsumsq(c, OP_T, OP_N, nl, B.rank, a->m, ap, a->dtype, lda, B.buf.ptr, B.dt, B.rows, rows.p(),
+                  ap != a->ptr);
     Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     double* b = d_blk_local ? d_blk_local : blk.p();
     segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
@@ -546,10 +579,13 @@ static double explicit_residual(Ctx* c, const DMat* a, const Basis& B) {
 }
 
 // global per-block ‖A_g‖² (host copy) and ‖A‖²
-static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global) {
+static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global,
+                          RoundedA* ra = nullptr) {
     Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     *d_global = Mat64(c, s.G, 1);
-    block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
+    if (ra) make_rounded(c, a, ra);
+    block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p(),
+                ra ? ra->buf.as<float>() : nullptr, a->m);
     gather_blocks_vec(c, s, loc.p(), d_global->p());
     bn2->assign(s.G, 0.0);
     d2h(c, bn2->data(), d_global->p(), s.G);
@@ -595,7 +631,8 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     Shard s = shard_of(a, offsets, G);
     std::vector<double> bn2;
     Mat64 dbn;
-    const double a2 = block_norms(c, a, s, &bn2, &dbn);
+    RoundedA ra;
+    const double a2 = block_norms(c, a, s, &bn2, &dbn, &ra);
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
     ph.reset(new ProfScope(c, "phase:2 range_finder", 0, 0));
     Subspace sub;
@@ -613,7 +650,7 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     Basis B;
     column_basis(c, a, s, unique_in_order(blocks), bn2, &B);
     ph.reset(new ProfScope(c, "phase:5 residual", 0, 0));
-    double res2 = a2 - projected_mass(c, a, s, B, nullptr);
+    double res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra);
     ph.reset();
     int path = 0;
     if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(a->dtype) * a2)) {
@@ -636,7 +673,8 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     Shard s = shard_of(a, offsets, G);
     std::vector<double> bn2;
     Mat64 res;
-    const double a2 = block_norms(c, a, s, &bn2, &res);  // res starts as ‖A_g‖²
+    RoundedA ra;
+    const double a2 = block_norms(c, a, s, &bn2, &res, &ra);  // res starts as ‖A_g‖²
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "greedy_select: A is identically zero");
     const int dt = a->dtype;
     const int64_t m = a->m;
@@ -691,7 +729,9 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
         const int64_t r = cgs2_append(c, &B, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)), dt, false);
         if (r > 0) {
             // res_g −= ‖Q_newᵀ A_g‖²
-            gemm_rowsumsq(c, OP_T, OP_N, a->n, r, m, a->ptr, dt, a->ld, B.col(cur), B.dt, B.rows, rows.p());
+            int64_t lda = 0;
+            const void* ap = rowsq_a(a, &ra, &lda);
+            gemm_rowsumsq(c, OP_T, OP_N, a->n, r, m, ap, dt, lda, B.col(cur), B.dt, B.rows, rows.p(), ap != a->ptr);
             segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
             gather_blocks_vec(c, s, loc.p(), upd.p());
             axpy_neg(c, upd.p(), res.p(), G);
