@@ -522,11 +522,11 @@ struct RoundedA {
 };
 static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra) {
     if (a->dtype != BCUR_F32 || a->m % 4 != 0 || a->m <= 0 || a->n <= 0) return;
-    size_t freeb = 0, totalb = 0;
-    CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
     const size_t need = (size_t)a->m * (size_t)a->n * 4;
     const size_t headroom = (size_t)8 << 30;  // the rest of the pipeline's workspace
-    if (!c->cached(need)) {
+    if (!c->cached(need)) {  // first call for this shape (cudaMemGetInfo is not free: not per step)
+        size_t freeb = 0, totalb = 0;
+        CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
         if (need + headroom > freeb + c->pooled_bytes) return;  // does not fit: in-kernel rounding
         if (need + headroom > freeb) c->trim();                  // make room from the workspace cache
     }
