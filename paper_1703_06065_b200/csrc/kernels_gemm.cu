@@ -218,7 +218,8 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
     // fp32 A-passes → tcgen05 3×TF32 kernels
     if (dta == BCUR_F32 && K > 0 && tb == OP_N) {
         if (ta == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {
-            umma_ax(c, (const float*)A, M, K, lda, B, dtb, N, ldb, alpha, beta, C, ldc, (flags & GEMM_B_UPPER) != 0);
+            umma_ax(c, (const float*)A, M, K, lda, B, dtb, N, ldb, alpha, beta, C, ldc, (flags & GEMM_B_UPPER) != 0,
+                    (flags & GEMM_X1) != 0);
             return;
         }
         if (ta == OP_T && umma_ok(dta, K, lda, A)) {

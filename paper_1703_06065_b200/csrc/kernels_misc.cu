@@ -53,12 +53,13 @@ __global__ void k_zero_lower(double* x, int64_t w, int64_t ld) {
     if (i > j) x[i + j * ld] = 0.0;
 }
 
-__global__ void k_near_identity_rinv(const double* __restrict__ g, int64_t w, int64_t ldg, double* __restrict__ x) {
+__global__ void k_near_identity_rinv(const double* __restrict__ g, int64_t w, int64_t ldg, double* __restrict__ x,
+                                     double one) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= w * w) return;
     const int64_t i = e % w, j = e / w;
     double v = 0.0;
-    if (i == j) v = 1.0 - 0.5 * (g[i + j * ldg] - 1.0);
+    if (i == j) v = one - 0.5 * (g[i + j * ldg] - 1.0);
     else if (i < j) v = -g[i + j * ldg];
     x[i + j * w] = v;
 }
@@ -128,9 +129,9 @@ void copy_f64(Ctx* c, const double* src, int64_t m, int64_t n, int64_t lds, doub
     convert(c, src, BCUR_F64, m, n, lds, dst, BCUR_F64, ldd);
 }
 
-void near_identity_rinv(Ctx* c, const double* g, int64_t w, int64_t ldg, double* x) {
+void near_identity_rinv(Ctx* c, const double* g, int64_t w, int64_t ldg, double* x, bool minus_identity) {
     if (w <= 0) return;
-    k_near_identity_rinv<<<nblk(w * w), 256, 0, c->stream>>>(g, w, ldg, x);
+    k_near_identity_rinv<<<nblk(w * w), 256, 0, c->stream>>>(g, w, ldg, x, minus_identity ? 0.0 : 1.0);
     LAUNCH_CHECK(c);
 }
 

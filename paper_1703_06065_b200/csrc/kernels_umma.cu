@@ -761,9 +761,9 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
 // partials.  x_upper_tri: X[k, j] = 0 for k > j (R⁻¹ of a Cholesky factor) — each N tile
 // stops at its diagonal (half the MMAs).
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-             int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri) {
+             int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri, bool x1) {
     if (m <= 0 || N <= 0) return;
-    ProfScope prof(c, "umma_ax", (x_upper_tri ? 1.0 : 2.0) * m * n * N,
+    ProfScope prof(c, x1 ? "umma_ax_x1" : "umma_ax", (x_upper_tri ? 1.0 : 2.0) * m * n * N,
                    4.0 * m * n + (double)dtype_size(dtx) * n * N + 8.0 * m * N);
     DevBuf xh, xl;
     split_x(c, X, dtx, n, N, ldx, &xh, &xl);
@@ -776,19 +776,31 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
     CUtensorMap th = make_map(xh.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     CUtensorMap tl = make_map(xl.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B);
     const int k_tiles = (int)((n + BK - 1) / BK);
-    const int NT = N > BN ? 2 : 1;
+    const int NT = x1 ? (N > 2 * BN ? 4 : N > BN ? 2 : 1) : (N > BN ? 2 : 1);
     const int mt = (int)((m + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
     int splits = (int)std::max<int64_t>(1, std::min<int64_t>((2LL * c->sm_count + mt * nt - 1) / (mt * nt),
                                                              k_tiles / 16));
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
     const Sched sc = make_sched(mt, nt, splits, k_tiles, kps, false, x_upper_tri);
+    // 1×TF32 (both operands rounded to nearest) for small corrections: up to 4 N tiles per CTA
+    auto launch = [&](double* o, int64_t lo, double* prt, double al, double be) {
+        if (!x1) {
+            launch_umma<true, EPI_STORE>(c, NT, sc, ta, th, tl, (int)m, (int)N, o, lo, prt, al, be);
+        } else if (NT == 4) {
+            launch_umma_nt<true, EPI_STORE, 4, false>(c, sc, ta, th, th, (int)m, (int)N, o, lo, prt, al, be);
+        } else if (NT == 2) {
+            launch_umma_nt<true, EPI_STORE, 2, false>(c, sc, ta, th, th, (int)m, (int)N, o, lo, prt, al, be);
+        } else {
+            launch_umma_nt<true, EPI_STORE, 1, false>(c, sc, ta, th, th, (int)m, (int)N, o, lo, prt, al, be);
+        }
+    };
     if (splits == 1) {
-        launch_umma<true, EPI_STORE>(c, NT, sc, ta, th, tl, (int)m, (int)N, out, ldo, nullptr, alpha, beta);
+        launch(out, ldo, nullptr, alpha, beta);
         return;
     }
     DevBuf part(c, (size_t)splits * m * N * sizeof(double));
-    launch_umma<true, EPI_STORE>(c, NT, sc, ta, th, tl, (int)m, (int)N, nullptr, 0, part.as<double>(), 1.0, 0.0);
+    launch(nullptr, 0, part.as<double>(), 1.0, 0.0);
     k_reduce_splits<<<(unsigned)((m * N + 255) / 256), 256, 0, c->stream>>>(m, N, splits, part.as<double>(), out, ldo,
                                                                             alpha, beta);
     LAUNCH_CHECK(c);

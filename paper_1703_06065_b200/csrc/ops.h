@@ -29,7 +29,9 @@ void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out);
 // only; other paths compute the full product):
 //   GEMM_SYM_UPPER  op(A)·op(B) is the Gram AᵀA (B == A): only C's upper triangle is needed
 //   GEMM_B_UPPER    op(B) is upper triangular
-enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2 };
+//   GEMM_X1         the product is a small correction (‖op(B)‖ ≲ 1e-4): one round-to-nearest
+//                   TF32 pass suffices (errors ~1e-4 × the correction)
+enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2, GEMM_X1 = 4 };
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags = 0);
 // rowsq[i] = Σ_j (op(A)·op(B))(i,j)²   (product never stored)
@@ -53,7 +55,8 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
               bool a_rounded = false);
 // Out(m×N) = alpha·A X + beta·Out (fp64); X fp32 or fp64; x_upper_tri: X[k,j] = 0 for k > j
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
-             int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri = false);
+             int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri = false,
+             bool x1 = false);
 
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
 // R upper (ld ldr, may alias g) with G = RᵀR, only g's upper triangle is read; info[0] = 0 ok / j+1 failed pivot;
@@ -64,7 +67,8 @@ void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, 
                     int64_t info_offset = 0, bool chained = false);
 // X = I − F where F = strict_upper(E) + diag(E)/2, E = G − I (first-order inverse of the
 // Cholesky factor of a near-identity Gram)
-void near_identity_rinv(Ctx* c, const double* g, int64_t w, int64_t ldg, double* x);
+// minus_identity: return −F instead (the correction of Q = Q1·(I − F) = Q1 + Q1·(−F))
+void near_identity_rinv(Ctx* c, const double* g, int64_t w, int64_t ldg, double* x, bool minus_identity = false);
 // X = R⁻¹ (upper triangular, w ≤ 128; only R's upper triangle is read; X's lower is zeroed)
 void tri_inv_upper(Ctx* c, const double* r, int64_t w, int64_t ldr, double* x, int64_t ldx);
 // symmetric eig, eigenvalues descending in lam, eigenvectors in columns of V (w×w)

@@ -373,8 +373,11 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
     max_dev_identity(c, G.p(), cc, G.ld, dev.p());
     double hdev = 1.0;
     d2h(c, &hdev, dev.p(), 1);
-    if (hdev < 1e-4) {
-        near_identity_rinv(c, G.p(), cc, G.ld, Ri.p());
+    const bool near = hdev < 1e-4;
+    if (near) {
+        // fp32: Q = Q1 + Q1·(−F) — the product is a ~1e-7-sized correction, so one rounded TF32
+        // pass is exact to ~1e-11; fp64: Q = Q1·(I − F) on DGEMM
+        near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), cdt == BCUR_F32);
     } else {
         const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p());
         if (c2.info != 0) return false;
@@ -382,8 +385,12 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
     }
     B->init(c, cdt, rows, cc);
     if (cdt == BCUR_F32) {
-        gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
-             GEMM_B_UPPER);
+        if (near)
+            gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 1.0, Q1.p(), Q1.ld,
+                 GEMM_B_UPPER | GEMM_X1);
+        else
+            gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
+                 GEMM_B_UPPER);
         convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
     } else {
         gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, q1, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, (double*)B->buf.ptr,
