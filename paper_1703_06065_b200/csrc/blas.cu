@@ -33,5 +33,22 @@ void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
     c->launches++;
 }
 
+// C(upper) = alpha·AᵀA + beta·C(upper), A k×n (ld lda): the symmetric GEMM of the blocked
+// Cholesky's trailing update (half the flops of the full product; only the upper
+// triangle is ever read)
+void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
+                          double* C, int64_t ldc) {
+    Handle& hd = g_handles[c->device];
+    if (!hd.h) {
+        if (cublasCreate(&hd.h) != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasCreate failed");
+        cublasSetPointerMode(hd.h, CUBLAS_POINTER_MODE_HOST);
+    }
+    cublasSetStream(hd.h, c->stream);
+    const cublasStatus_t st = cublasDsyrk(hd.h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, (int)n, (int)k, &alpha, A,
+                                          (int)lda, &beta, C, (int)ldc);
+    if (st != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasDsyrk failed (" + std::to_string((int)st) + ")");
+    c->launches++;
+}
+
 }  // namespace ops
 }  // namespace bcur_b200

@@ -46,6 +46,10 @@ void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, con
 void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 
+// C(upper) = alpha·AᵀA + beta·C(upper)  (A k×n)
+void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
+                          double* C, int64_t ldc);
+
 // ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
 bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
 // Out(n×N) = alpha·Aᵀ X + beta·Out (fp64) or rowsq[j] = Σ_c (AᵀX)_jc²; X fp32 or fp64.

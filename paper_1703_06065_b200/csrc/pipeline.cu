@@ -133,7 +133,10 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
             gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Ri, BCUR_F64, B, Pk, BCUR_F64, w, 0.0, T1.p(), B);
             copy_f64(c, T1.p(), kb, rest, B, Pk, w);
             double* Tr = R + (k + kb) + (k + kb) * w;
-            gemm(c, OP_T, OP_N, rest, rest, kb, -1.0, T1.p(), BCUR_F64, B, T1.p(), BCUR_F64, B, 1.0, Tr, w);
+            {  // trailing update, upper triangle only (everything downstream reads the upper)
+                ProfScope prof(c, "dsyrk_cublas", 1.0 * rest * rest * kb, 8.0 * (kb * rest + rest * rest / 2.0));
+                cublas_dsyrk_upper_t(c, rest, kb, -1.0, T1.p(), B, 1.0, Tr, w);
+            }
         }
     }
     zero_lower(c, R, w, w);
