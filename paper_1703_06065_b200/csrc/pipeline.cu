@@ -643,6 +643,7 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     Mat64 dbn;
     RoundedA ra;
     const double a2 = block_norms(c, a, s, &bn2, &dbn, &ra);
+    if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_css: matrix contains NaN or Inf");  // require_finite
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
     ph.reset(new ProfScope(c, "phase:2 range_finder", 0, 0));
     Subspace sub;
@@ -685,6 +686,7 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     Mat64 res;
     RoundedA ra;
     const double a2 = block_norms(c, a, s, &bn2, &res, &ra);  // res starts as ‖A_g‖²
+    if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "greedy_select: matrix contains NaN or Inf");  // require_finite
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "greedy_select: A is identically zero");
     const int dt = a->dtype;
     const int64_t m = a->m;
@@ -781,6 +783,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     std::vector<double> bn2;
     Mat64 dbn;
     const double a2 = block_norms(c, a, s, &bn2, &dbn);
+    if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: matrix contains NaN or Inf");  // require_finite
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_cur: A is identically zero");
     Subspace sub;
     range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);

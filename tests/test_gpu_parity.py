@@ -194,6 +194,14 @@ def test_errors(B):
         B.block_css(sparse, part, 1, 3, B.Rng(0), mode=B.SamplingMode.without_replacement)
     with pytest.raises(B.DimensionMismatch):
         B.block_css(np.ones((10, 41)), part, 2, 2, B.Rng(0))
+    # require_finite (matcore.cpp:26-33): NaN / Inf inputs are rejected, not propagated
+    for bad in (np.nan, np.inf):
+        a = np.random.default_rng(1).standard_normal((10, 40))
+        a[3, 17] = bad
+        with pytest.raises(ValueError):
+            B.block_css(a, part, 2, 2, B.Rng(0))
+        with pytest.raises(ValueError):
+            B.greedy_select(a, part, 2, 2, seed=0)
 
 
 def test_bitwise_rerun_determinism(B):
