@@ -35,6 +35,7 @@ namespace {
 constexpr int BM = 128, BK = 32, BN = 64, CH = 2;
 __device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, bit 1 skip drain, bit 2 skip MMAs (timing experiments)
 bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
+bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 
@@ -658,6 +659,213 @@ Sched make_sched(int m_tiles, int n_tiles, int splits, int k_tiles, int kps, boo
     return sc;
 }
 
+// ------------------------------------------------ CTA-pair row-Σ² (cta_group::2)
+// rowsq[j] = Σ_c (AᵀX)_jc² on a pre-rounded A (1×TF32), one CTA pair per 256 A columns ×
+// 256 X columns.  Each CTA TMA-loads its own 128-column A tile and HALF of the X tile
+// (the 2-SM TMA form signals the leader's barrier); the leader issues M=256 × N=256 MMAs
+// (tcgen05.mma.cta_group::2) that read A from each CTA's shared memory and B split across
+// the two; each CTA's TMEM holds its 128 rows.  Per SM and stage this moves 32 KB into
+// shared memory and 32 KB out to the tensor core, against 48 + 48 KB for a single-CTA
+// N=256 tile — the single-CTA pass is bound by shared-memory bandwidth.
+constexpr int P2_NDRAIN = 16;                                   // 4 lane quarters × 4 64-column tiles
+constexpr int P2_THREADS = 32 * (4 + P2_NDRAIN);               // producer, MMA, 2 idle, drains
+constexpr uint32_t P2_STAGE = A_TILE + 2 * X_TILE;              // own A tile + half of the X tile
+constexpr int P2_STAGES = 6;
+constexpr uint32_t P2_SMEM = P2_STAGES * P2_STAGE + 1024 + 256;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t smem_addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// pair tile t → (A column pair mp, X tile nt): groups of 8 X tiles × all pairs, so a wave
+// of pairs shares A and X bands through L2 (as make_sched's raster)
+__device__ __forceinline__ void pair_tile(int t, int m_pairs, int n_tiles, int* mp, int* nt) {
+    const int gn0 = n_tiles < 8 ? n_tiles : 8, gsz = gn0 * m_pairs;
+    const int g = t / gsz, first = g * gn0, gn = min(gn0, n_tiles - first), r = t - g * gsz;
+    *nt = first + r % gn;
+    *mp = r / gn;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2_THREADS, 1)
+k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int M, int m_pairs,
+              int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + P2_STAGES * P2_STAGE);
+    uint64_t* full = bars;                     // [STAGES] leader: both CTAs' bytes
+    uint64_t* empty = full + P2_STAGES;        // [STAGES] each CTA: multicast MMA commit
+    uint64_t* tfull = empty + P2_STAGES;       // [2]      each CTA: multicast MMA commit
+    uint64_t* tempty = tfull + 2;              // [2]      leader: both CTAs' drains
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int total = m_pairs * n_tiles;
+    constexpr int NTP = 4;                     // N tiles (of 64) per pair tile = 256 columns
+    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((NTP * BN) >> 3) << 17) |
+                               ((uint32_t)(2 * BM >> 4) << 24);   // M = 256, N = 256
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < P2_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * P2_NDRAIN);  // one (remote) arrive per drain warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmX) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int dbg = g_dbg_flags;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- producer
+        if (lane == 0) {
+            const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);  // leader's barriers
+            int gi = 0;
+            for (int t = pair, w = 0; t < total; t += npairs, ++w) {
+                if (wave_ctr && w > 0) {  // wave barrier: every CTA issued wave w-1 (lockstep along K)
+                    unsigned int target = 0;
+                    for (int v = 0; v < w; ++v) target += 2u * (unsigned int)max(0, min(npairs, total - v * npairs));
+                    unsigned int val;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(val) : "l"(wave_ctr) : "memory");
+                    } while (val < target);
+                }
+                int mp, nt;
+                pair_tile(t, m_pairs, n_tiles, &mp, &nt);
+                const int m_tile = 2 * mp + (int)rank;
+                for (int i = 0; i < k_tiles; ++i, ++gi) {
+                    const int s = gi % P2_STAGES;
+                    mbar_wait(&empty[s], ((uint32_t)(gi / P2_STAGES) & 1u) ^ 1u);
+                    if (rank == 0) mbar_expect_tx(&full[s], 2 * P2_STAGE);
+                    const uint32_t fb = full0 + s * 8;
+                    const int k0 = i * BK;
+                    uint8_t* st = smem + s * P2_STAGE;
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(k0),
+                        "r"(m_tile * BM) : "memory");
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st + A_TILE + h * X_TILE)), "l"(&tmX),
+                            "r"(fb), "r"(k0), "r"((nt * NTP + (int)rank * 2 + h) * BN) : "memory");
+                }
+                if (wave_ctr) atomicAdd(wave_ctr, 1u);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------- MMA issuer (leader only)
+        if (rank == 0) {
+            int gi = 0, gc = 0;
+            for (int t = pair; t < total; t += npairs) {
+                for (int i = 0; i < k_tiles; ++i, ++gi) {
+                    const int s = gi % P2_STAGES;
+                    const int c = gc + i / CH, b = c & 1;
+                    const bool first = (i % CH) == 0;
+                    if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
+                    mbar_wait(&full[s], (uint32_t)(gi / P2_STAGES) & 1u);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(smem + s * P2_STAGE), x0 = a0 + A_TILE;
+                    const uint32_t d = tmem + (uint32_t)(b * NTP * BN);
+#pragma unroll
+                    for (int k8 = 0; k8 < BK / 8; ++k8) {
+                        const uint64_t da = sdesc(a0 + k8 * 32, 16, 1024, 2);
+                        const uint64_t dx = sdesc(x0 + k8 * 32, 16, 1024, 2);
+                        const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                        if (!(dbg & 4))
+                            asm volatile(
+                                "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(da),
+                                "l"(dx), "r"(IDESC), "r"(acc));
+                    }
+                    asm volatile(
+                        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                        " [%0], %1;\n\t}" ::"r"(smem_u32(&empty[s])), "h"((uint16_t)3) : "memory");
+                    if ((i % CH) == CH - 1 || i == k_tiles - 1)
+                        asm volatile(
+                            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                            " [%0], %1;\n\t}" ::"r"(smem_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+                    __syncwarp();
+                }
+                gc += (k_tiles + CH - 1) / CH;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------- drain (both CTAs, own TMEM rows)
+        const int q = warp & 3, tile = (warp - 4) >> 2;   // lane quarter, 64-column tile
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t tempty0 = map_to_rank(smem_u32(&tempty[0]), 0);
+        int gc = 0;
+        const int nchunks = (k_tiles + CH - 1) / CH;
+        for (int t = pair; t < total; t += npairs) {
+            int mp, nt;
+            pair_tile(t, m_pairs, n_tiles, &mp, &nt);
+            const int row = (2 * mp + (int)rank) * BM + q * 32 + lane;
+            float acc[BN];
+#pragma unroll
+            for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+            for (int c = 0; c < nchunks; ++c) {
+                const int g = gc + c, b = g & 1;
+                mbar_wait(&tfull[b], (uint32_t)(g / 2) & 1u);
+                tc_fence_after();
+                if (!(dbg & 2)) {
+                    const uint32_t t0 = tmem + lane_off + (uint32_t)(b * NTP * BN + tile * BN);
+#pragma unroll
+                    for (int j0 = 0; j0 < BN; j0 += 16) {
+                        uint32_t h[16];
+                        TMEM_LD16(t0 + j0, h);
+                        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) acc[j0 + j] += __uint_as_float(h[j]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)  // default (cta-scope release) form: a .cluster-scope release is a GPU-wide MEMBAR
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+            }
+            gc += nchunks;
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < BN; ++j) {
+                const double v = (double)acc[j];
+                s = fma(v, v, s);  // columns ≥ N are exact zeros (TMA zero fill)
+            }
+            if (row < M) partial[(int64_t)(nt * NTP + tile) * M + row] = s;
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
 // x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
 void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
     *hi = DevBuf(c, (size_t)K * N * 4);
@@ -681,6 +889,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         enabled = (e && e[0] == '1') ? 0 : 1;
         const char* wb = getenv("BCUR_UMMA_NO_WAVE_BARRIER");
         g_wave_barrier_off = wb && wb[0] == '1';
+        const char* np_ = getenv("BCUR_UMMA_NO_PAIR");
+        g_no_pair = np_ && np_[0] == '1';
         const char* d = getenv("BCUR_UMMA_DEBUG");
         if (d) {
             const int f = atoi(d);
@@ -724,7 +934,26 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
         Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
         sc.a_rn = a_rounded ? 1 : 0;
         DevBuf part(c, (size_t)nt * NTX * n * sizeof(double));
-        if (NTX == 1)
+        if (NTX == 4 && a_rounded && mt >= 2 && !g_no_pair) {
+            // CTA pairs: 256 A columns × 256 X columns per pair (see k_umma2_rowsq)
+            static bool attr = false;
+            if (!attr) {
+                CUDA_CHECK(cudaFuncSetAttribute(k_umma2_rowsq, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+                attr = true;
+            }
+            const int m_pairs = (mt + 1) / 2;
+            const int pairs = std::min(m_pairs * nt, c->sm_count / 2);
+            DevBuf ctr;
+            unsigned int* wc = nullptr;
+            if (pairs < m_pairs * nt && !g_wave_barrier_off) {  // ≤ 1 CTA per SM: all co-resident
+                ctr = DevBuf(c, 64);
+                CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
+                wc = ctr.as<unsigned int>();
+            }
+            k_umma2_rowsq<<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, th, (int)n, m_pairs, nt, k_tiles,
+                                                                         part.as<double>(), wc);
+            LAUNCH_CHECK(c);
+        } else if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
                                                        part.as<double>(), 1.0, 0.0);
         else if (NTX == 2)
