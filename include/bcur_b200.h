@@ -151,6 +151,13 @@ bcur_status bcur_range_finder(bcur_ctx ctx, bcur_dmat a, int64_t k, int64_t p, i
  * transpose=1 receives Σ_c (AᵀX)_jc² instead of storing the product (out may be NULL). */
 bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, bcur_dmat out,
                                 double* rows_out);
+/* Structured forms of the same products (diagnostics and tests; the pipelines use them for
+ * the basis Grams and Q = C·R⁻¹):
+ *   BCUR_PRODUCT_GRAM      out = AᵀA, upper triangle only (x must be NULL, transpose = 1)
+ *   BCUR_PRODUCT_X_UPPER   X is upper triangular (zero below its diagonal; the tcgen05 path
+ *                          skips that part of the product) */
+enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2 };
+bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
 /* sampler.cpp:116-146 draw_blocks (probabilities on the host, one uniform per draw
  * drawn by the caller from its Rng; margins_out[t] = distance of u_t to the nearest
  * CDF edge, nullable). */

@@ -90,6 +90,7 @@ SIGNATURES = {
     "bcur_column_leverage": (C.c_int, [vp, vp, dbl, P_dbl, P_dbl]),
     "bcur_range_finder": (C.c_int, [vp, vp, i64, i64, i64, u64, C.POINTER(vp), C.POINTER(vp), P_dbl, P_i64]),
     "bcur_sketch_product": (C.c_int, [vp, vp, vp, C.c_int, vp, P_dbl]),
+    "bcur_sketch_product_ex": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
     "bcur_draw_blocks": (C.c_int, [vp, P_dbl, i64, i64, C.c_int, P_dbl, u64, C.POINTER(BlockDrawC), P_dbl]),
     "bcur_materialize_columns": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(BlockDrawC), i64, C.POINTER(vp)]),
     "bcur_materialize_row_blocks": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(BlockDrawC), i64, C.POINTER(vp)]),

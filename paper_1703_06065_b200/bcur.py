@@ -461,6 +461,24 @@ def sketch_product(a, x: np.ndarray, transpose: bool = False, row_sumsq: bool = 
     return o.to_host()
 
 
+def structured_product(a, x: Optional[np.ndarray] = None, transpose: bool = False, gram: bool = False,
+                       x_upper: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
+    """bcur_sketch_product_ex: ``gram`` → AᵀA (upper triangle valid, ``x`` None);
+    ``x_upper`` → A·X or Aᵀ·X with an upper-triangular X (the pipelines' Q = C·R⁻¹)."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    flags = (1 if gram else 0) | (2 if x_upper else 0)
+    xd = None if x is None else DeviceMatrix.from_host(np.asarray(x, dtype=np.float64), ctx)
+    rows = d.shape[1] if (transpose or gram) else d.shape[0]
+    cols = d.shape[1] if gram else xd.shape[1]
+    h = C.c_void_p()
+    _check(L.lib.bcur_dmat_create(ctx.handle, L.F64, rows, cols, C.byref(h)))
+    o = DeviceMatrix(h, ctx)
+    _check(L.lib.bcur_sketch_product_ex(ctx.handle, d.handle, None if xd is None else xd.handle,
+                                        1 if (transpose or gram) else 0, flags, o.handle))
+    return o.to_host()
+
+
 @dataclass
 class Subspace:
     v_k: np.ndarray

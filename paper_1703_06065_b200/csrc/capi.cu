@@ -177,6 +177,11 @@ bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
     ctx->trim();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+        for (auto e : ctx->side_ev) cudaEventDestroy(e);
+    }
     delete ctx;
     API_END
 }
@@ -528,6 +533,34 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
             fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product: output must be fp64 rows × N");
         ops::gemm(c, transpose ? ops::OP_T : ops::OP_N, ops::OP_N, rows, X->n, K, 1.0, A->ptr, A->dtype, A->ld,
                   X->ptr, BCUR_F64, X->ld, 0.0, (double*)O->ptr, O->ld);
+    }
+    c->sync();
+    API_END
+}
+
+bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat *A = M(a), *O = M(out);
+    if (flags & ~(BCUR_PRODUCT_GRAM | BCUR_PRODUCT_X_UPPER)) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: bad flags");
+    if (flags & BCUR_PRODUCT_GRAM) {
+        if (x || !transpose || (flags & BCUR_PRODUCT_X_UPPER))
+            fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the Gram form takes x = NULL and transpose = 1");
+        if (O->dtype != BCUR_F64 || O->m != A->n || O->n != A->n)
+            fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: Gram output must be fp64 n × n");
+        ops::gemm(c, ops::OP_T, ops::OP_N, A->n, A->n, A->m, 1.0, A->ptr, A->dtype, A->ld, A->ptr, A->dtype, A->ld, 0.0,
+                  (double*)O->ptr, O->ld, ops::GEMM_SYM_UPPER);
+    } else {
+        DMat* X = M(x);
+        if (X->dtype != BCUR_F64) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: X must be fp64");
+        const int64_t K = transpose ? A->m : A->n, rows = transpose ? A->n : A->m;
+        if (X->m != K) fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: inner dimensions differ");
+        if ((flags & BCUR_PRODUCT_X_UPPER) && X->m != X->n)
+            fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: an upper-triangular X is square");
+        if (O->dtype != BCUR_F64 || O->m != rows || O->n != X->n)
+            fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: output must be fp64 rows × N");
+        ops::gemm(c, transpose ? ops::OP_T : ops::OP_N, ops::OP_N, rows, X->n, K, 1.0, A->ptr, A->dtype, A->ld, X->ptr,
+                  BCUR_F64, X->ld, 0.0, (double*)O->ptr, O->ld, (flags & BCUR_PRODUCT_X_UPPER) ? ops::GEMM_B_UPPER : 0);
     }
     c->sync();
     API_END

@@ -128,6 +128,24 @@ struct Ctx {
     void sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
     std::map<void*, size_t> sizes;
 
+    // Second stream for overlapped work (the blocked Cholesky's look-ahead).  Work on it is
+    // forked from `stream` and joined back into it before any buffer it touches is released,
+    // so the workspace cache's stream-order reuse rule still holds.
+    cudaStream_t side = nullptr;
+    cudaEvent_t side_ev[2] = {nullptr, nullptr};
+    cudaStream_t side_stream() {
+        if (!side) {
+            CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            for (auto& e : side_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        return side;
+    }
+    // make `to` wait for everything enqueued so far on `from`
+    void order(cudaStream_t from, cudaStream_t to, int slot) {
+        CUDA_CHECK(cudaEventRecord(side_ev[slot], from));
+        CUDA_CHECK(cudaStreamWaitEvent(to, side_ev[slot], 0));
+    }
+
     // --- per-kernel accounting (CUDA events on this stream; bench roofline) ---
     struct ProfRec {
         std::string tag;

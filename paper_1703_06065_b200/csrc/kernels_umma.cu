@@ -36,6 +36,7 @@ constexpr int BM = 128, BK = 32, BN = 64, CH = 2;
 __device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, bit 1 skip drain, bit 2 skip MMAs (timing experiments)
 bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
 bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (experiments)
+bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 
@@ -66,7 +67,7 @@ struct Cfg {
     // X3 runs whole warpgroups: WG0 = producer, MMA, 2 transform warps; NT drain warpgroups;
     // one more transform warpgroup (the a_lo split is the MMA's feeder).  The drain
     // warpgroups take the registers the others give up (setmaxnreg).
-    static constexpr int NTRANSFORM = 6;
+    static constexpr int NTRANSFORM = (X3 && NT == 1) ? 10 : 6;
     // register re-split (setmaxnreg) whenever the launch cap is below what the drains need
     static constexpr bool RESPLIT = X3 || NT == 4;
     static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
@@ -92,10 +93,22 @@ __device__ __forceinline__ float rn_tf32(float x) {
     return __uint_as_float(u & 0xFFFFE000u);
 }
 // a_lo for a raw fp32 operand the tensor core truncates to TF32: the exact remainder,
-// itself rounded to TF32 so the hardware takes it unchanged.
-__device__ __forceinline__ float lo_of(float a) { return rn_tf32(a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u)); }
+// itself rounded to TF32 so the hardware takes it unchanged.  Ties round away from zero
+// (two integer ops instead of four for ties-to-even; a_lo is always finite, and a tie
+// needs the 12 low bits of the 13-bit remainder to be exactly 1000…0).  The transform
+// warps issue this for every A element of a 3×TF32 pass, so its op count sets the rate of
+// the HBM-bound range-finder passes.
+__device__ __forceinline__ float lo_of(float a) {
+    const float r = a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
+    return __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
+}
 
 // ------------------------------------------------------------- PTX helpers
+// Warp index broadcast from lane 0: ptxas then knows role branches on it are warp-uniform.
+// With plain threadIdx.x >> 5 it must assume a role branch may split a warp, and wraps every
+// tcgen05.mma in a BRA.DIV + ELECT + R2UR.BROADCAST waterfall (~24 SASS instructions per MMA,
+// which made the small-N passes MMA-issue bound).
+__device__ __forceinline__ int warp_index() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -225,10 +238,10 @@ __device__ __forceinline__ TileInfo tile_info(const Sched& sc, int t) {
     const int per_split = sc.sym ? sc.n_tiles * (sc.n_tiles + 1) / 2 : sc.m_tiles * sc.n_tiles;
     ti.split = t / per_split;
     const int r = t - ti.split * per_split;
-    if (sc.sym) {  // r = n(n+1)/2 + m, m ≤ n
-        int n = (int)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
+    if (sc.sym) {  // r = n(n+1)/2 + m, m ≤ n.  Integer search: a sqrtf (MUFU, vector
+        // registers) here made the schedule look non-uniform to ptxas (see warp_index)
+        int n = 0;
         while ((n + 1) * (n + 2) / 2 <= r) ++n;
-        while (n * (n + 1) / 2 > r) --n;
         ti.n_tile = n;
         ti.m_tile = r - n * (n + 1) / 2;
     } else {
@@ -274,8 +287,10 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     uint64_t* tempty = tfull + 2;                            // [2]
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int dbg = g_dbg_flags;  // read once (a per-stage global load sat on the transform's critical path)
+    const int warp = warp_index(), lane = threadIdx.x & 31;
+    // read once (a per-stage global load sat on the transform's critical path); broadcast so the
+    // MMA guard below stays provably warp-uniform (see warp_index)
+    const int dbg = __shfl_sync(0xffffffffu, g_dbg_flags, 0);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -707,7 +722,7 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     uint64_t* tfull = empty + P2_STAGES;       // [2]      each CTA: multicast MMA commit
     uint64_t* tempty = tfull + 2;              // [2]      leader: both CTAs' drains
     uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = warp_index(), lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int total = m_pairs * n_tiles;
@@ -735,7 +750,7 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int dbg = g_dbg_flags;
+    const int dbg = __shfl_sync(0xffffffffu, g_dbg_flags, 0);
 
     if (warp == 0) {
         // ---------------------------------------------------------------- producer
@@ -866,6 +881,333 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
 }
 
+// ------------------------------------------- CTA-pair 3×TF32 product (cta_group::2)
+// Out = alpha·op(A)·X + beta·Out with 3×TF32 operands (as k_umma X3), one CTA pair per
+// 256 output rows × 128 output columns.  Each CTA stages its own 128-row A tile and HALF
+// of x_hi and x_lo (32 KB per stage against 48 KB for a single-CTA N = 128 X3 stage), and
+// computes a_lo = a − trunc(a) into its own ring; the leader issues three M = 256 × N = 128
+// MMAs per k-step (a·x_hi → hi, a·x_lo → lo, a_lo·x_hi → lo) that read both CTAs' shared
+// memory.  (The single-CTA kernel fuses a·[x_hi | x_lo] into one N = 256 instruction; with
+// B split across the pair at equal offsets the lo half would not be contiguous.)
+// Hand-off: a CTA's transform warps meet at a named barrier after their a_lo stores and
+// one thread arrives (cluster-scope release) on the leader's lo_ready — that arrive also
+// vouches for the CTA's TMA bytes, which the transform waited for.
+struct PSched {
+    int m_pairs, n_tiles, total, k_tiles, sym, tri_x;
+    unsigned int* wave_ctr;
+};
+constexpr int X3P_NTRANSFORM = 6, X3P_NDRAIN = 8;
+constexpr int X3P_THREADS = 32 * (2 + X3P_NTRANSFORM + X3P_NDRAIN);        // 512
+constexpr uint32_t X3P_STAGE = A_TILE + 2 * X_TILE;                          // A + x_hi half + x_lo half
+constexpr int X3P_LO = 3;
+constexpr int X3P_STAGES = (int)((232448u - 1280u - X3P_LO * A_TILE) / X3P_STAGE);
+constexpr uint32_t X3P_SMEM = X3P_STAGES * X3P_STAGE + X3P_LO * A_TILE + 1024 + 256;
+constexpr uint32_t X3P_R0 = (65536u / X3P_THREADS) / 8 * 8;                  // 128
+constexpr uint32_t X3P_REG_LOW = 56;
+constexpr uint32_t X3P_REG_DRAIN_FIT =
+    X3P_R0 + ((X3P_THREADS - 32 * X3P_NDRAIN) * (X3P_R0 - X3P_REG_LOW) / (32 * X3P_NDRAIN)) / 8 * 8;
+constexpr uint32_t X3P_REG_DRAIN = X3P_REG_DRAIN_FIT > 232 ? 232 : X3P_REG_DRAIN_FIT;
+
+// pair tile t → (row pair mp, 128-column tile nt, k stages).  sym: only tiles touching the
+// upper triangle (256·mp ≤ 128·nt + 127), column by column.
+__device__ __forceinline__ void x3p_tile(const PSched& sc, int t, int* mp, int* nt, int* nk) {
+    if (sc.sym) {
+        int n = 0;
+        for (;; ++n) {
+            const int cnt = min(n / 2, sc.m_pairs - 1) + 1;
+            if (t < cnt) break;
+            t -= cnt;
+        }
+        *nt = n;
+        *mp = t;
+    } else {
+        pair_tile(t, sc.m_pairs, sc.n_tiles, mp, nt);
+    }
+    *nk = sc.tri_x ? min(sc.k_tiles, ((*nt + 1) * 2 * BN + BK - 1) / BK) : sc.k_tiles;
+}
+
+template <bool A_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(X3P_THREADS, 1)
+k_umma2_x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
+           const __grid_constant__ CUtensorMap tmXl, int M, int N, const PSched sc, double* __restrict__ out,
+           int64_t ldo, double alpha, double beta) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + X3P_STAGES * X3P_STAGE + X3P_LO * A_TILE);
+    uint64_t* full = bars;                       // [STAGES] own TMA bytes
+    uint64_t* empty = full + X3P_STAGES;         // [STAGES] multicast MMA commit
+    uint64_t* lo_ready = empty + X3P_STAGES;     // [LO]     leader: one arrive per CTA
+    uint64_t* lo_empty = lo_ready + X3P_LO;      // [LO]     multicast MMA commit
+    uint64_t* tfull = lo_empty + X3P_LO;         // [2]      multicast MMA commit
+    uint64_t* tempty = tfull + 2;                // [2]      leader: both CTAs' drain warps
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = warp_index(), lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    constexpr int NTP = 2;  // 64-column tiles per pair tile
+    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) |
+                               ((uint32_t)((NTP * BN) >> 3) << 17) | ((uint32_t)(2 * BM >> 4) << 24);
+    constexpr uint32_t BUF = 2 * NTP * BN;  // hi + lo columns per TMEM buffer
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < X3P_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int l = 0; l < X3P_LO; ++l) {
+            mbar_init(&lo_ready[l], 2);
+            mbar_init(&lo_empty[l], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * X3P_NDRAIN);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXh) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXl) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    auto a_raw = [&](int s) { return smem + s * X3P_STAGE; };
+    auto x_hi = [&](int s) { return smem + s * X3P_STAGE + A_TILE; };
+    auto x_lo = [&](int s) { return smem + s * X3P_STAGE + A_TILE + X_TILE; };
+    auto a_lo = [&](int l) { return smem + X3P_STAGES * X3P_STAGE + l * A_TILE; };
+
+    if (warp >= 4 && warp < 4 + X3P_NDRAIN) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(X3P_REG_DRAIN));
+        // ------------------------------------------- drain (both CTAs, own TMEM rows)
+        const int q = warp & 3, tile = (warp - 4) >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t tempty0 = map_to_rank(smem_u32(&tempty[0]), 0);
+        int gc = 0;
+        for (int t = pair; t < sc.total; t += npairs) {
+            int mp, nt, nk;
+            x3p_tile(sc, t, &mp, &nt, &nk);
+            const int nchunks = (nk + CH - 1) / CH;
+            const int row = (2 * mp + (int)rank) * BM + q * 32 + lane;
+            float acc[BN], cmp[BN];
+#pragma unroll
+            for (int j = 0; j < BN; ++j) acc[j] = cmp[j] = 0.0f;
+            for (int c = 0; c < nchunks; ++c) {
+                const int g = gc + c, b = g & 1;
+                mbar_wait(&tfull[b], (uint32_t)(g / 2) & 1u);
+                tc_fence_after();
+                const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * BUF + tile * BN), t_lo = t_hi + NTP * BN;
+#pragma unroll
+                for (int j0 = 0; j0 < BN; j0 += 8) {
+                    uint32_t h[8], l[8];
+                    TMEM_LD8(t_hi + j0, h);
+                    TMEM_LD8(t_lo + j0, l);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int e = j0 + j;
+                        const float hv = __uint_as_float(h[j]), lv = __uint_as_float(l[j]);
+                        const float tt = __fadd_rn(hv, lv);
+                        const float et = __fsub_rn(lv, __fsub_rn(tt, hv));  // Fast2Sum, |hi| ≥ |lo|
+                        const float sum = __fadd_rn(acc[e], tt);
+                        const float z = __fsub_rn(sum, acc[e]);
+                        cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(tt, z), et));
+                        acc[e] = sum;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)  // default (cta-scope) form, as k_umma2_rowsq
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+            }
+            gc += nchunks;
+            const int col0 = nt * NTP * BN + tile * BN;
+            if (row < M) {
+                const int ncol = min(BN, N - col0);
+                double* dst = out + row;
+#pragma unroll
+                for (int j = 0; j < BN; ++j) {
+                    const double v = (double)acc[j] + (double)cmp[j];
+                    if (j < ncol) {
+                        double* o = dst + (int64_t)(col0 + j) * ldo;
+                        *o = beta == 0.0 ? alpha * v : fma(beta, *o, alpha * v);
+                    }
+                }
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(X3P_REG_LOW));
+        if (warp == 0) {
+            // ---------------------------------------------------------------- producer
+            if (lane == 0) {
+                constexpr int PF = 12;
+                int gi = 0;
+                for (int t = pair, w = 0; t < sc.total; t += npairs, ++w) {
+                    if (sc.wave_ctr && w > 0) {
+                        unsigned int target = 0;
+                        for (int v = 0; v < w; ++v)
+                            target += 2u * (unsigned int)max(0, min(npairs, sc.total - v * npairs));
+                        unsigned int val;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(val) : "l"(sc.wave_ctr) : "memory");
+                        } while (val < target);
+                    }
+                    int mp, nt, nk;
+                    x3p_tile(sc, t, &mp, &nt, &nk);
+                    const int m_tile = 2 * mp + (int)rank, xc = (nt * NTP + (int)rank) * BN;
+                    auto prefetch_a = [&](int i) {
+                        if (A_MN) tma_prefetch_3d(&tmA, 0, i * BK, m_tile * (BM / 32));
+                        else tma_prefetch_2d(&tmA, i * BK, m_tile * BM);
+                    };
+                    for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % X3P_STAGES;
+                        if (i + PF < nk) prefetch_a(i + PF);
+                        mbar_wait(&empty[s], ((uint32_t)(gi / X3P_STAGES) & 1u) ^ 1u);
+                        mbar_expect_tx(&full[s], X3P_STAGE);
+                        const int k0 = i * BK;
+                        if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
+                        else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
+                        tma_load_2d(x_hi(s), &tmXh, &full[s], k0, xc);
+                        tma_load_2d(x_lo(s), &tmXl, &full[s], k0, xc);
+                    }
+                    if (sc.wave_ctr) atomicAdd(sc.wave_ctr, 1u);
+                }
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------- MMA issuer (leader only)
+            if (rank == 0) {
+                int gi = 0, gc = 0;
+                for (int t = pair; t < sc.total; t += npairs) {
+                    int mp, nt, nk;
+                    x3p_tile(sc, t, &mp, &nt, &nk);
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % X3P_STAGES, lr = gi % X3P_LO;
+                        const int c = gc + i / CH, b = c & 1;
+                        const bool first = (i % CH) == 0;
+                        if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
+                        mbar_wait(&lo_ready[lr], (uint32_t)(gi / X3P_LO) & 1u);
+                        tc_fence_after();
+                        const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(lr));
+                        const uint32_t xh = smem_u32(x_hi(s)), xl = smem_u32(x_lo(s));
+                        const uint32_t d_hi = tmem + (uint32_t)(b * BUF), d_lo = d_hi + NTP * BN;
+#pragma unroll
+                        for (int k8 = 0; k8 < BK / 8; ++k8) {
+                            uint64_t da_r, da_l;
+                            if (A_MN) {
+                                da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
+                                da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
+                            } else {
+                                da_r = sdesc(ar + k8 * 32, 16, 1024, 2);
+                                da_l = sdesc(al + k8 * 32, 16, 1024, 2);
+                            }
+                            const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
+                            const uint64_t dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
+                            const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n\t.reg .pred e, p, one;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                "setp.ne.b32 p, %7, 0;\n\tsetp.eq.b32 one, %7, %7;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %2, %3, %6, p;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], %2, %4, %6, p;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::tf32 [%1], %5, %3, %6, one;\n\t}" ::"r"(d_hi),
+                                "r"(d_lo), "l"(da_r), "l"(dxh), "l"(dxl), "l"(da_l), "r"(IDESC), "r"(acc));
+                        }
+                        asm volatile(
+                            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                            " [%0], %2;\n\t"
+                            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                            " [%1], %2;\n\t}" ::"r"(smem_u32(&empty[s])), "r"(smem_u32(&lo_empty[lr])),
+                            "h"((uint16_t)3) : "memory");
+                        if ((i % CH) == CH - 1 || i == nk - 1)
+                            asm volatile(
+                                "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                                " [%0], %1;\n\t}" ::"r"(smem_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+                        __syncwarp();
+                    }
+                    gc += (nk + CH - 1) / CH;
+                }
+            }
+        } else {
+            // ------------------------------------------- a_lo transform (both CTAs)
+            constexpr int NTT = 32 * X3P_NTRANSFORM;
+            const int tid = (warp < 4 ? warp - 2 : warp - (4 + X3P_NDRAIN) + 2) * 32 + lane;
+            const uint32_t lo_ready0 = map_to_rank(smem_u32(&lo_ready[0]), 0);
+            int gi = 0;
+            for (int t = pair; t < sc.total; t += npairs) {
+                int mp, nt, nk;
+                x3p_tile(sc, t, &mp, &nt, &nk);
+                for (int i = 0; i < nk; ++i, ++gi) {
+                    const int s = gi % X3P_STAGES, lr = gi % X3P_LO;
+                    mbar_wait(&full[s], (uint32_t)(gi / X3P_STAGES) & 1u);
+                    mbar_wait(&lo_empty[lr], ((uint32_t)(gi / X3P_LO) & 1u) ^ 1u);
+                    const uint32_t src = smem_u32(a_raw(s)), dst = smem_u32(a_lo(lr));
+#pragma unroll 4
+                    for (int v = tid; v < (int)(A_TILE / 16); v += NTT) {
+                        float4 a;
+                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                                     : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
+                        a.x = lo_of(a.x); a.y = lo_of(a.y); a.z = lo_of(a.z); a.w = lo_of(a.w);
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(a.x), "f"(a.y),
+                                     "f"(a.z), "f"(a.w) : "memory");
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    asm volatile("bar.sync 1, %0;" ::"n"(NTT) : "memory");
+                    if (tid == 0)
+                        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(lo_ready0 + lr * 8)
+                                     : "memory");
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <bool A_MN>
+void launch_umma2_x3(Ctx* c, PSched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
+                     int N, double* out, int64_t ldo, double alpha, double beta) {
+    auto kern = k_umma2_x3<A_MN>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, X3P_SMEM));
+        attr = true;
+    }
+    const int pairs = std::min(sc.total, c->sm_count / 2);
+    DevBuf ctr;
+    sc.wave_ctr = nullptr;
+    if (pairs < sc.total && !g_wave_barrier_off) {  // ≤ 1 CTA per SM: all co-resident
+        ctr = DevBuf(c, 64);
+        CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
+        sc.wave_ctr = ctr.as<unsigned int>();
+    }
+    kern<<<2 * pairs, X3P_THREADS, X3P_SMEM, c->stream>>>(ta, th, tl, M, N, sc, out, ldo, alpha, beta);
+    LAUNCH_CHECK(c);
+}
+PSched make_psched(int mt, int nt, int k_tiles, bool sym, bool tri_x) {
+    PSched sc;
+    sc.m_pairs = (mt + 1) / 2;
+    sc.n_tiles = nt;
+    sc.k_tiles = k_tiles;
+    sc.sym = sym ? 1 : 0;
+    sc.tri_x = tri_x ? 1 : 0;
+    sc.wave_ctr = nullptr;
+    if (sym) {
+        sc.total = 0;
+        for (int n = 0; n < nt; ++n) sc.total += std::min(n / 2, sc.m_pairs - 1) + 1;
+    } else {
+        sc.total = sc.m_pairs * nt;
+    }
+    return sc;
+}
+
 // x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
 void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
     *hi = DevBuf(c, (size_t)K * N * 4);
@@ -891,6 +1233,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         g_wave_barrier_off = wb && wb[0] == '1';
         const char* np_ = getenv("BCUR_UMMA_NO_PAIR");
         g_no_pair = np_ && np_[0] == '1';
+        const char* nx = getenv("BCUR_UMMA_X3_PAIR");
+        g_no_x3pair = !(nx && nx[0] == '1');
         const char* d = getenv("BCUR_UMMA_DEBUG");
         if (d) {
             const int f = atoi(d);
@@ -974,6 +1318,13 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
     const Sched sc = make_sched(mt, nt, splits, k_tiles, kps, sym, false);
+    if (splits == 1 && NT == 2 && mt >= 2 && !g_no_x3pair) {  // CTA pairs (see k_umma2_x3)
+        const PSched ps = make_psched(mt, nt, k_tiles, sym, false);
+        if (ps.total >= c->sm_count / 2) {
+            launch_umma2_x3<false>(c, ps, ta, th, tl, (int)n, (int)N, out, ldo, alpha, beta);
+            return;
+        }
+    }
     if (splits == 1) {
         launch_umma<false, EPI_STORE>(c, NT, sc, ta, th, tl, (int)n, (int)N, out, ldo, nullptr, alpha, beta);
         return;
@@ -1024,6 +1375,13 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
             launch_umma_nt<true, EPI_STORE, 1, false>(c, sc, ta, th, th, (int)m, (int)N, o, lo, prt, al, be);
         }
     };
+    if (splits == 1 && !x1 && NT == 2 && mt >= 2 && !g_no_x3pair) {  // CTA pairs (see k_umma2_x3)
+        const PSched ps = make_psched(mt, nt, k_tiles, false, x_upper_tri);
+        if (ps.total >= c->sm_count / 2) {
+            launch_umma2_x3<true>(c, ps, ta, th, tl, (int)m, (int)N, out, ldo, alpha, beta);
+            return;
+        }
+    }
     if (splits == 1) {
         launch(out, ldo, nullptr, alpha, beta);
         return;

@@ -121,24 +121,44 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     CUDA_CHECK(cudaMemcpyAsync(st.ptr, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
     c->sync();
     for (double d : diag) out.maxdiag = std::max(out.maxdiag, d);
-    Mat64 Rinv(c, B, B), T1(c, B, w);
-    for (int64_t k = 0; k < w; k += B) {
+    // Look-ahead: step k updates the next block row (rows of block k+1, which step k+1
+    // factors and reads as its panel) on the main stream, and the rest of the trailing
+    // matrix with DSYRK on the side stream, where it overlaps step k+1's diagonal
+    // factorization, inverse and panel product.  Step k+1's own block-row update, which
+    // touches rows the side DSYRK also updates, waits for it.  T1 is double-buffered: the
+    // side DSYRK of step k reads T1[k&1] while step k+1 writes T1[(k+1)&1].
+    Mat64 Rinv(c, B, B), T1a(c, B, w), T1b(c, B, w);
+    cudaStream_t main_s = c->stream, side_s = c->side_stream();
+    c->order(main_s, side_s, 0);  // the side stream starts after R's initial copy
+    int64_t step = 0;
+    for (int64_t k = 0; k < w; k += B, ++step) {
         const int64_t kb = std::min(B, w - k), rest = w - k - kb;
         double* Dk = R + k + k * w;
         cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
         double* Ri = dinv ? dinv + k * B : Rinv.p();  // inverse of the diagonal block (ld B)
         if (rest > 0 || dinv) tri_inv_upper(c, Dk, kb, w, Ri, B);
         if (rest > 0) {
+            double* T1 = (step & 1) ? T1b.p() : T1a.p();
             double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
-            gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Ri, BCUR_F64, B, Pk, BCUR_F64, w, 0.0, T1.p(), B);
-            copy_f64(c, T1.p(), kb, rest, B, Pk, w);
-            double* Tr = R + (k + kb) + (k + kb) * w;
-            {  // trailing update, upper triangle only (everything downstream reads the upper)
-                ProfScope prof(c, "dsyrk_cublas", 1.0 * rest * rest * kb, 8.0 * (kb * rest + rest * rest / 2.0));
-                cublas_dsyrk_upper_t(c, rest, kb, -1.0, T1.p(), B, 1.0, Tr, w);
+            gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Ri, BCUR_F64, B, Pk, BCUR_F64, w, 0.0, T1, B);
+            copy_f64(c, T1, kb, rest, B, Pk, w);
+            const int64_t n1 = std::min(B, rest), k1 = k + kb;
+            if (step > 0) c->order(side_s, main_s, 1);  // previous side DSYRK covered these rows
+            // next block row (upper part used downstream): R[k1:k1+n1, k1:] −= T1[:, :n1]ᵀ·T1
+            gemm(c, OP_T, OP_N, n1, rest, kb, -1.0, T1, BCUR_F64, B, T1, BCUR_F64, B, 1.0, R + k1 + k1 * w, w);
+            if (rest > n1) {
+                const int64_t k2 = k1 + n1, r2 = rest - n1;
+                c->order(main_s, side_s, 0);
+                c->stream = side_s;
+                {
+                    ProfScope prof(c, "dsyrk_cublas", 1.0 * r2 * r2 * kb, 8.0 * (kb * r2 + r2 * r2 / 2.0));
+                    cublas_dsyrk_upper_t(c, r2, kb, -1.0, T1 + n1 * B, B, 1.0, R + k2 + k2 * w, w);
+                }
+                c->stream = main_s;
             }
         }
     }
+    c->order(side_s, main_s, 1);  // join before any buffer is released
     zero_lower(c, R, w, w);
     d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
     out.info = hs.info;

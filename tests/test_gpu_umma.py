@@ -57,3 +57,40 @@ def test_fused_row_sumsq(B, N):
     assert np.max(np.abs(got - ref) / ref) < 5e-4
     # the total's random part shrinks like 1/sqrt(#dot products); systematic part ≲ 2e-6
     assert abs(got.sum() - ref.sum()) / ref.sum() < 3e-6 + 4 * 2.5e-4 / np.sqrt(n * N)
+
+
+# CTA-pair 3×TF32 path (k_umma2_x3): NT = 2 products with ≥ 74 pair tiles; odd tile counts
+# leave the last pair's second CTA on zero-filled A rows
+@pytest.mark.parametrize("m,n,N", [(8288, 256, 600), (8192, 96, 1000)])
+def test_pair_ax(B, m, n, N):
+    gen = np.random.default_rng(m + N)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    x = np.asfortranarray(gen.standard_normal((n, N)))
+    assert rel_fro(B.sketch_product(a, x), a.astype(np.float64) @ x) < 2e-6
+
+
+@pytest.mark.parametrize("m,n,N", [(512, 8288, 600), (224, 8192, 1000)])
+def test_pair_atx(B, m, n, N):
+    gen = np.random.default_rng(m + n + N)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    q = np.asfortranarray(gen.standard_normal((m, N)))
+    assert rel_fro(B.sketch_product(a, q, transpose=True), a.astype(np.float64).T @ q) < 2e-6
+
+
+@pytest.mark.parametrize("m,n", [(1024, 4224), (480, 2176)])
+def test_gram_upper(B, m, n):
+    gen = np.random.default_rng(m + n)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    a64 = a.astype(np.float64)
+    g = B.structured_product(a, gram=True)
+    ref = a64.T @ a64
+    iu = np.triu_indices(n)
+    assert rel_fro(g[iu], ref[iu]) < 2e-6
+
+
+@pytest.mark.parametrize("m,n", [(8192, 640), (4096, 200)])
+def test_x_upper(B, m, n):
+    gen = np.random.default_rng(m + n + 1)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    x = np.asfortranarray(np.triu(gen.standard_normal((n, n))))
+    assert rel_fro(B.structured_product(a, x, x_upper=True), a.astype(np.float64) @ x) < 2e-6
