@@ -62,7 +62,9 @@ struct Cfg {
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int LOR = X3 ? LO_SLOTS : STAGES;  // lo_ready barriers
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + LO_SLOTS * A_TILE + 1024 + 256;
-    static constexpr uint32_t TMEM_COLS = 2 * BUFCOLS;                      // ≤ 512
+    static constexpr uint32_t TMEM_USED = 2 * BUFCOLS;                      // ≤ 512
+    static constexpr uint32_t TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128
+                                        : TMEM_USED <= 256 ? 256 : 512;      // allocation: power of 2
     static constexpr int NDRAIN = 4 * NT * (BN / DCOLS);                     // drain warps
     // X3 runs whole warpgroups: WG0 = producer, MMA, 2 transform warps; NT drain warpgroups;
     // one more transform warpgroup (the a_lo split is the MMA's feeder).  The drain
@@ -93,15 +95,19 @@ __device__ __forceinline__ float rn_tf32(float x) {
     return __uint_as_float(u & 0xFFFFE000u);
 }
 // a_lo for a raw fp32 operand the tensor core truncates to TF32: the exact remainder,
-// itself rounded to TF32 so the hardware takes it unchanged.  Ties round away from zero
-// (two integer ops instead of four for ties-to-even; a_lo is always finite, and a tie
-// needs the 12 low bits of the 13-bit remainder to be exactly 1000…0).  The transform
-// warps issue this for every A element of a 3×TF32 pass, so its op count sets the rate of
-// the HBM-bound range-finder passes.
+// rounded to TF32 (ties away from zero) as the tensor core will read it.  The MMA ignores
+// the 13 low mantissa bits of a kind::tf32 operand, so adding half an ulp is enough — the
+// mask that would clear those bits is left to the hardware (a_lo is always finite).  Three
+// ops per element: the transform warps run this on every A element of a 3×TF32 pass, and
+// its op count sets the rate of the HBM-bound range-finder passes.
 __device__ __forceinline__ float lo_of(float a) {
     const float r = a - __uint_as_float(__float_as_uint(a) & 0xFFFFE000u);
-    return __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
+    return __uint_as_float(__float_as_uint(r) + 0x1000u);
 }
+
+// x rounded to the nearest TF32 (ties away) as the tensor core reads it: half an ulp added,
+// the low bits left for the MMA to ignore (one op; for operands only an MMA consumes)
+__device__ __forceinline__ float rn_mma(float x) { return __uint_as_float(__float_as_uint(x) + 0x1000u); }
 
 // ------------------------------------------------------------- PTX helpers
 // Warp index broadcast from lane 0: ptxas then knows role branches on it are warp-uniform.
@@ -150,6 +156,29 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int c0, i
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// One A tile (A_TILE bytes) through f, NTT threads: every load of a thread is issued before
+// its first store (the accesses are volatile asm, which the compiler keeps in order — a
+// load/compute/store loop left each warp waiting out one shared-memory latency per float4).
+template <int NTT, class F>
+__device__ __forceinline__ void transform_tile(uint32_t src, uint32_t dst, int tid, F f) {
+    constexpr int NV = (int)(A_TILE / 16), IT = (NV + NTT - 1) / NTT;
+    float4 a[IT];
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+        const int v = tid + j * NTT;
+        if (NV % NTT == 0 || v < NV)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(a[j].x), "=f"(a[j].y), "=f"(a[j].z), "=f"(a[j].w) : "r"(src + v * 16));
+    }
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+        const int v = tid + j * NTT;
+        if (NV % NTT == 0 || v < NV)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(f(a[j].x)),
+                         "f"(f(a[j].y)), "f"(f(a[j].z)), "f"(f(a[j].w)) : "memory");
+    }
+}
 
 // Shared-memory matrix descriptor (Blackwell version 1).  layout: 2 = SWIZZLE_128B
 // (K-major operands), 1 = SWIZZLE_128B_BASE32B (MN-major 32-bit operands).
@@ -374,12 +403,15 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     const int e = j0 + j;
                     const float hsum = __uint_as_float(h[j]);
                     if (X3) {
-                        const float hv = hsum, lv = __uint_as_float(l[j]);
-                        const float t = __fadd_rn(hv, lv);
-                        const float et = __fsub_rn(lv, __fsub_rn(t, hv));     // Fast2Sum, |hi| ≥ |lo|
-                        const float sum = __fadd_rn(acc[e], t);
+                        // hi chunks through a compensated (Fast2Sum) sum; the cross terms
+                        // (~2⁻¹¹ of hi) go straight into the compensation accumulator with the
+                        // rounding error — both are small, so one fp32 sum of them is exact to
+                        // ~2⁻³⁵ of the result: 5 FP ops per element (8 with the cross term
+                        // folded into hi by a second Fast2Sum first)
+                        const float hv = hsum;
+                        const float sum = __fadd_rn(acc[e], hv);
                         const float z = __fsub_rn(sum, acc[e]);
-                        cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(t, z), et));
+                        cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(hv, z), __uint_as_float(l[j])));
                         acc[e] = sum;
                     } else {
                         acc[e] += hsum;
@@ -529,19 +561,8 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     mbar_arrive(&lo_ready[lr]);
                     continue;
                 }
-    #pragma unroll 4
-                for (int v = tid; v < (int)(A_TILE / 16); v += NTT) {
-                    float4 a;
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
-                    if (X3) {
-                        a.x = lo_of(a.x); a.y = lo_of(a.y); a.z = lo_of(a.z); a.w = lo_of(a.w);
-                    } else {
-                        a.x = rn_tf32(a.x); a.y = rn_tf32(a.y); a.z = rn_tf32(a.z); a.w = rn_tf32(a.w);
-                    }
-                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(a.x), "f"(a.y),
-                                 "f"(a.z), "f"(a.w) : "memory");
-                }
+                if (X3) transform_tile<NTT>(src, dst, tid, lo_of);
+                else transform_tile<NTT>(src, dst, tid, rn_mma);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 mbar_arrive(&lo_ready[lr]);
             }
@@ -1145,15 +1166,7 @@ k_umma2_x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
                     mbar_wait(&full[s], (uint32_t)(gi / X3P_STAGES) & 1u);
                     mbar_wait(&lo_empty[lr], ((uint32_t)(gi / X3P_LO) & 1u) ^ 1u);
                     const uint32_t src = smem_u32(a_raw(s)), dst = smem_u32(a_lo(lr));
-#pragma unroll 4
-                    for (int v = tid; v < (int)(A_TILE / 16); v += NTT) {
-                        float4 a;
-                        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                     : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w) : "r"(src + v * 16));
-                        a.x = lo_of(a.x); a.y = lo_of(a.y); a.z = lo_of(a.z); a.w = lo_of(a.w);
-                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + v * 16), "f"(a.x), "f"(a.y),
-                                     "f"(a.z), "f"(a.w) : "memory");
-                    }
+                    transform_tile<NTT>(src, dst, tid, lo_of);
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     asm volatile("bar.sync 1, %0;" ::"n"(NTT) : "memory");
                     if (tid == 0)
