@@ -155,8 +155,10 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
  * the basis Grams and Q = C·R⁻¹):
  *   BCUR_PRODUCT_GRAM      out = AᵀA, upper triangle only (x must be NULL, transpose = 1)
  *   BCUR_PRODUCT_X_UPPER   X is upper triangular (zero below its diagonal; the tcgen05 path
- *                          skips that part of the product) */
-enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2 };
+ *                          skips that part of the product)
+ *   BCUR_PRODUCT_ROWSQ_F16 out (n × 1) = Σ_c (AᵀX)_jc² through the pipelines' fp16 path
+ *                          (fp32 A with m % 32 == 0; transpose = 1) */
+enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4 };
 bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
 /* sampler.cpp:116-146 draw_blocks (probabilities on the host, one uniform per draw
  * drawn by the caller from its Rng; margins_out[t] = distance of u_t to the nearest

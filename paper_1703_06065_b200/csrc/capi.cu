@@ -542,7 +542,28 @@ bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int t
     API_BEGIN
     Ctx* c = C(ctx);
     DMat *A = M(a), *O = M(out);
-    if (flags & ~(BCUR_PRODUCT_GRAM | BCUR_PRODUCT_X_UPPER)) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: bad flags");
+    if (flags & ~(BCUR_PRODUCT_GRAM | BCUR_PRODUCT_X_UPPER | BCUR_PRODUCT_ROWSQ_F16))
+        fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: bad flags");
+    if (flags & BCUR_PRODUCT_ROWSQ_F16) {
+        DMat* X = x ? M(x) : nullptr;
+        if (flags != BCUR_PRODUCT_ROWSQ_F16 || !X || !transpose)
+            fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the fp16 row-sum form takes X and transpose = 1");
+        if (A->dtype != BCUR_F32 || A->m % 32 != 0 || A->ld % 4 != 0 || ((uintptr_t)A->ptr % 16) != 0)
+            fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the fp16 row-sum form needs fp32 A with m % 32 == 0");
+        if (X->m != A->m) fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: inner dimensions differ");
+        if (O->dtype != BCUR_F64 || O->m != A->n || O->n != 1)
+            fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: row sums go to an fp64 n × 1 output");
+        DevBuf a16(c, (size_t)A->m * A->n * 2), exps(c, (size_t)A->n * sizeof(int)), off(c, 2 * sizeof(int64_t)),
+            tot(c, sizeof(double));
+        const int64_t h_off[2] = {0, A->n};
+        CUDA_CHECK(cudaMemcpyAsync(off.ptr, h_off, sizeof h_off, cudaMemcpyHostToDevice, c->stream));
+        ops::block_sumsq(c, A->ptr, A->dtype, A->m, A->ld, off.as<int64_t>(), 1, tot.as<double>(), nullptr, A->m,
+                         a16.as<uint16_t>(), exps.as<int>());
+        ops::gemm_rowsumsq_f16(c, A->n, X->n, A->m, a16.as<uint16_t>(), A->m, exps.as<int>(), X->ptr, X->dtype, X->ld,
+                               (double*)O->ptr);
+        c->sync();
+        return BCUR_OK;
+    }
     if (flags & BCUR_PRODUCT_GRAM) {
         if (x || !transpose || (flags & BCUR_PRODUCT_X_UPPER))
             fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the Gram form takes x = NULL and transpose = 1");

@@ -7,6 +7,7 @@
 // All sums are deterministic (fixed-order partials, no floating atomics), so a
 // rerun with the same inputs reproduces results bit-for-bit.
 #include "ops.h"
+#include <cuda_fp16.h>
 
 namespace bcur_b200 {
 namespace {
@@ -33,6 +34,32 @@ __device__ double block_sum(double s) {
         t = warp_sum(t);
     }
     return t;  // valid in thread 0
+}
+
+// Block-wide max of one non-negative value per thread, broadcast to every thread.
+__device__ float block_max_all(float v) {
+    __shared__ float red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    float t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0f;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmaxf(t, __shfl_xor_sync(0xffffffffu, t, o));
+    return t;
+}
+
+// Power-of-two scale exponent p for a column with max |value| mx: mx·2^p < 2^15, so the
+// scaled column fits fp16 (max 65504) with 29 binades of normal range below its largest
+// entry.  Scaling by 2^p is exact; fp16 round-to-nearest then keeps the same 11-bit
+// significand as a TF32 round-to-nearest of the unscaled value.
+__device__ __forceinline__ int f16_scale_exp(float mx) {
+    if (!(mx > 0.0f) || !isfinite(mx)) return 0;
+    int e;
+    frexpf(mx, &e);  // mx = f·2^e, f ∈ [0.5, 1)
+    return 15 - e;
 }
 
 // Σ col[i]²; fp32 columns optionally also write their TF32-rounded copy to `shadow`
@@ -80,17 +107,51 @@ __device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, b
     return s0 + s1;
 }
 
-// grid (G, Z): CTA (g, z) sums columns off[g]+z, off[g]+z+Z, ...
+// Σ col[i]² of an fp32 column (m % 4 == 0, 16-byte aligned) that also writes its fp16 copy
+// scaled by 2^p (p = f16_scale_exp(max |col|), stored in colexp[j]): the max pass reads the
+// column from HBM; the scaling pass re-reads it from L2.
+__device__ double sq_col_f16(const float* __restrict__ col, int64_t m, uint16_t* __restrict__ sh16, int* colexp_j) {
+    double s0 = 0.0, s1 = 0.0;
+    float mx = 0.0f;
+    const float4* c4 = reinterpret_cast<const float4*>(col);
+    const int64_t m4 = m >> 2;
+    for (int64_t i = threadIdx.x; i < m4; i += RT) {
+        const float4 v = c4[i];
+        s0 = fma((double)v.x, (double)v.x, s0);
+        s1 = fma((double)v.y, (double)v.y, s1);
+        s0 = fma((double)v.z, (double)v.z, s0);
+        s1 = fma((double)v.w, (double)v.w, s1);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    const int p = f16_scale_exp(block_max_all(mx));
+    if (threadIdx.x == 0) *colexp_j = p;
+    uint2* o4 = reinterpret_cast<uint2*>(sh16);
+    for (int64_t i = threadIdx.x; i < m4; i += RT) {
+        const float4 v = __ldcs(c4 + i);
+        const __half2 lo = __floats2half2_rn(ldexpf(v.x, p), ldexpf(v.y, p));
+        const __half2 hi = __floats2half2_rn(ldexpf(v.z, p), ldexpf(v.w, p));
+        __stcs(o4 + i, make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi)));
+    }
+    return s0 + s1;
+}
+
+// grid (G, Z): CTA (g, z) sums columns off[g]+z, off[g]+z+Z, ...  Optional copies of the
+// column: the TF32-rounded fp32 `shadow`, or the scaled fp16 `sh16` (+ per-column exponents).
 template <class T>
 __global__ void __launch_bounds__(RT) k_block_sumsq(const T* __restrict__ a, int64_t m, int64_t ld,
                                                     const int64_t* __restrict__ off, int Z, bool vec,
                                                     double* __restrict__ partial, float* __restrict__ shadow,
-                                                    int64_t lds) {
+                                                    int64_t lds, uint16_t* __restrict__ sh16,
+                                                    int* __restrict__ colexp) {
     const int64_t g = blockIdx.x;
     const int z = blockIdx.y;
     double s = 0.0;
-    for (int64_t j = off[g] + z; j < off[g + 1]; j += Z)
-        s += sq_col(a + j * ld, m, vec, shadow ? shadow + j * lds : nullptr);
+    for (int64_t j = off[g] + z; j < off[g + 1]; j += Z) {
+        if (sizeof(T) == 4 && sh16)
+            s += sq_col_f16(reinterpret_cast<const float*>(a + j * ld), m, sh16 + j * lds, colexp + j);
+        else
+            s += sq_col(a + j * ld, m, vec, shadow ? shadow + j * lds : nullptr);
+    }
     s = block_sum(s);
     if (threadIdx.x == 0) partial[g * Z + z] = s;
 }
@@ -161,7 +222,7 @@ __global__ void k_max_dev_identity(const double* __restrict__ g, int w, int64_t 
 namespace ops {
 
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
-                 double* d_out, float* shadow, int64_t lds) {
+                 double* d_out, float* shadow, int64_t lds, uint16_t* sh16, int* colexp) {
     if (G <= 0) return;
     ProfScope prof(c, "block_sumsq", 0.0, 0.0);
     // enough CTAs to fill the machine several times over
@@ -171,12 +232,15 @@ void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int
     DevBuf part(c, (size_t)G * Z * sizeof(double));
     dim3 grid((unsigned)G, (unsigned)Z);
     if (dt == BCUR_F32)
+    {
+        if (sh16 && !(vec && m % 4 == 0 && lds % 4 == 0))
+            fail(BCUR_E_INVALID_ARGUMENT, "block_sumsq: the fp16 copy needs aligned columns with m % 4 == 0");
         k_block_sumsq<float><<<grid, RT, 0, c->stream>>>((const float*)a, m, ld, d_offsets, Z,
                                                          vec && (shadow == nullptr || (lds % 4 == 0)),
-                                                         part.as<double>(), shadow, lds);
-    else
+                                                         part.as<double>(), shadow, lds, sh16, colexp);
+    } else
         k_block_sumsq<double><<<grid, RT, 0, c->stream>>>((const double*)a, m, ld, d_offsets, Z, vec, part.as<double>(),
-                                                          nullptr, 0);
+                                                          nullptr, 0, nullptr, nullptr);
     LAUNCH_CHECK(c);
     k_segment_rows<<<(unsigned)((G + 255) / 256), 256, 0, c->stream>>>(part.as<double>(), Z, G, d_out);
     LAUNCH_CHECK(c);

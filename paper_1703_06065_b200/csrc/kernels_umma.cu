@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include "ops.h"
+#include <cuda_fp16.h>
 
 namespace bcur_b200 {
 namespace {
@@ -39,6 +40,10 @@ bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (e
 bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
+// K elements per stage: tiles are 128-byte K rows (SWIZZLE_128B) — 32 tf32 or 64 fp16
+// elements; every MMA consumes 32 bytes of K (8 tf32 / 16 fp16), so the byte geometry of
+// stages, descriptors and tensor maps is the same for both kinds.
+template <bool H> constexpr int bke() { return H ? 2 * BK : BK; }
 
 // NT 64-column N tiles per CTA share every staged A tile (more N per CTA = fewer L2
 // bytes per MMA).  Two precisions:
@@ -212,6 +217,21 @@ __device__ __forceinline__ void umma_tf32_warp(uint32_t tmem_d, uint64_t adesc, 
         "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
         "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void umma_f16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t"
+        "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+template <bool H>
+__device__ __forceinline__ void umma_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t accumulate) {
+    if (H) umma_f16_warp(tmem_d, adesc, bdesc, idesc, accumulate);
+    else umma_tf32_warp(tmem_d, adesc, bdesc, idesc, accumulate);
+}
 __device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
@@ -288,14 +308,18 @@ __device__ __forceinline__ TileInfo tile_info(const Sched& sc, int t) {
     return ti;
 }
 
-template <bool A_MN, int EPI, int NT, bool X3>
+template <bool A_MN, int EPI, int NT, bool X3, bool H = false>
 __global__ void __launch_bounds__(Cfg<NT, X3>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
        const __grid_constant__ CUtensorMap tmXl, int M, int N, const Sched sc,
        double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta) {
-    // instruction descriptor: fp32 accumulate, tf32 × tf32, B K-major, N = n_cols, M = 128
+    // instruction descriptor: fp32 accumulate, tf32 × tf32 (H: f16 × f16), B K-major,
+    // N = n_cols, M = 128
+    static_assert(!H || (!X3 && EPI == EPI_ROWSQ && !A_MN), "fp16 operands: pre-converted row-sum-of-squares only");
+    constexpr uint32_t FMT = H ? 0u : 2u;
+    constexpr int BKE = bke<H>();
     auto idesc = [](uint32_t n_cols) -> uint32_t {
-        return (1u << 4) | (2u << 7) | (2u << 10) | ((A_MN ? 1u : 0u) << 15) | ((n_cols >> 3) << 17) |
+        return (1u << 4) | (FMT << 7) | (FMT << 10) | ((A_MN ? 1u : 0u) << 15) | ((n_cols >> 3) << 17) |
                ((uint32_t)(BM >> 4) << 24);
     };
 
@@ -467,7 +491,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     const TileInfo ti = tile_info<NT>(sc, t);
                     const int kt0 = ti.kt0, nk = ti.nk, m_tile = ti.m_tile, n_tile = ti.n_tile;
                     auto prefetch_a = [&](int i) {
-                        const int k0 = (kt0 + i) * BK;
+                        const int k0 = (kt0 + i) * BKE;
                         if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
                         else tma_prefetch_2d(&tmA, k0, m_tile * BM);
                     };
@@ -477,7 +501,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         if (i + PF < nk) prefetch_a(i + PF);
                         mbar_wait(&empty[s], ((uint32_t)(gi / STAGES) & 1u) ^ 1u);
                         mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
-                        const int k0 = (kt0 + i) * BK;
+                        const int k0 = (kt0 + i) * BKE;
                         if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
                         else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
 #pragma unroll
@@ -525,7 +549,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                             const uint32_t t_hi = tmem + (uint32_t)(b * BUFCOLS), t_lo = t_hi + NT * BN;
                             const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
                             if (!(dbg & 4)) {  // bit 2: skip the MMAs (timing experiments)
-                                umma_tf32_warp(t_hi, da_r, dxh, idesc((X3 ? 2 : 1) * NT * BN), acc);
+                                umma_warp<H>(t_hi, da_r, dxh, idesc((X3 ? 2 : 1) * NT * BN), acc);
                                 if (X3) umma_tf32_warp(t_lo, da_l, dxh, idesc(NT * BN), 1u);
                             }
                         }
@@ -623,10 +647,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
-                     const uint32_t* box, CUtensorMapSwizzle swz) {
+                     const uint32_t* box, CUtensorMapSwizzle swz,
+                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     CUtensorMap m;
     uint32_t es[3] = {1, 1, 1};
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(base), dims, strides_bytes,
+    CUresult r = encode_fn()(&m, dt, rank, const_cast<void*>(base), dims, strides_bytes,
                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(BCUR_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
@@ -634,11 +659,11 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 }
 
 // Persistent launch: one CTA per SM (or fewer when there are fewer tiles).
-template <bool A_MN, int EPI, int NT, bool X3>
+template <bool A_MN, int EPI, int NT, bool X3, bool H = false>
 void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
                     int N, double* out, int64_t ldo, double* partial, double alpha, double beta) {
     using CF = Cfg<NT, X3>;
-    auto kern = k_umma<A_MN, EPI, NT, X3>;
+    auto kern = k_umma<A_MN, EPI, NT, X3, H>;
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
@@ -732,6 +757,7 @@ __device__ __forceinline__ void pair_tile(int t, int m_pairs, int n_tiles, int* 
     *mp = r / gn;
 }
 
+template <bool H>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2_THREADS, 1)
 k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int M, int m_pairs,
               int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr) {
@@ -748,7 +774,9 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     const int total = m_pairs * n_tiles;
     constexpr int NTP = 4;                     // N tiles (of 64) per pair tile = 256 columns
-    constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((NTP * BN) >> 3) << 17) |
+    constexpr uint32_t FMT = H ? 0u : 2u;   // f16 / tf32 operands
+    constexpr int BKE = bke<H>();
+    constexpr uint32_t IDESC = (1u << 4) | (FMT << 7) | (FMT << 10) | ((uint32_t)((NTP * BN) >> 3) << 17) |
                                ((uint32_t)(2 * BM >> 4) << 24);   // M = 256, N = 256
     if (threadIdx.x == 0) {
         for (int s = 0; s < P2_STAGES; ++s) {
@@ -795,7 +823,7 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     mbar_wait(&empty[s], ((uint32_t)(gi / P2_STAGES) & 1u) ^ 1u);
                     if (rank == 0) mbar_expect_tx(&full[s], 2 * P2_STAGE);
                     const uint32_t fb = full0 + s * 8;
-                    const int k0 = i * BK;
+                    const int k0 = i * BKE;
                     uint8_t* st = smem + s * P2_STAGE;
                     asm volatile(
                         "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -830,7 +858,12 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                         const uint64_t da = sdesc(a0 + k8 * 32, 16, 1024, 2);
                         const uint64_t dx = sdesc(x0 + k8 * 32, 16, 1024, 2);
                         const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
-                        if (!(dbg & 4))
+                        if (!(dbg & 4) && H)
+                            asm volatile(
+                                "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(da),
+                                "l"(dx), "r"(IDESC), "r"(acc));
+                        else if (!(dbg & 4))
                             asm volatile(
                                 "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                                 "@e tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d), "l"(da),
@@ -1221,6 +1254,48 @@ PSched make_psched(int mt, int nt, int k_tiles, bool sym, bool tri_x) {
     return sc;
 }
 
+// ------------------------------------------------ fp16 operands (row-Σ² passes)
+// max |x| over a K × N matrix into *mx (float bits; non-negative floats order as integers)
+template <class T>
+__global__ void k_absmax(const T* __restrict__ x, int64_t K, int64_t N, int64_t ldx, unsigned int* __restrict__ mx) {
+    float m = 0.0f;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < K * N; e += (int64_t)gridDim.x * blockDim.x) {
+        const float v = fabsf((float)x[e % K + (e / K) * ldx]);
+        m = fmaxf(m, isfinite(v) ? v : 0.0f);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, __float_as_uint(m));
+}
+// scale exponent q with max·2^q < 2^15 (as block_sumsq's per-column exponents)
+__device__ __forceinline__ int f16_exp_of(unsigned int mxbits) {
+    const float mx = __uint_as_float(mxbits);
+    if (!(mx > 0.0f)) return 0;
+    int e;
+    frexpf(mx, &e);
+    return 15 - e;
+}
+// x → fp16(x·2^q), K × N, ld K; q = f16_exp_of(*mx), also stored to *qout
+template <class T>
+__global__ void k_to_f16(const T* __restrict__ x, int64_t K, int64_t N, int64_t ldx, const unsigned int* __restrict__ mx,
+                         uint16_t* __restrict__ out, int* __restrict__ qout) {
+    const int q = f16_exp_of(*mx);
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e == 0) *qout = q;
+    if (e >= K * N) return;
+    const __half h = __float2half_rn(ldexpf((float)x[e % K + (e / K) * ldx], q));
+    out[e] = *reinterpret_cast<const uint16_t*>(&h);
+}
+// out[i] = 2^(−2(colexp[i] + q)) · Σ_t partial[t·M + i]  (removes both exact scales)
+__global__ void k_sum_tiles_scaled(int64_t M, int tiles, const double* __restrict__ partial, const int* __restrict__ colexp,
+                                   const int* __restrict__ q, double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    double s = 0.0;
+    for (int t = 0; t < tiles; ++t) s += partial[(int64_t)t * M + i];
+    out[i] = ldexp(s, -2 * (colexp[i] + *q));
+}
+
 // x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
 void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, DevBuf* hi, DevBuf* lo) {
     *hi = DevBuf(c, (size_t)K * N * 4);
@@ -1295,7 +1370,7 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
             // CTA pairs: 256 A columns × 256 X columns per pair (see k_umma2_rowsq)
             static bool attr = false;
             if (!attr) {
-                CUDA_CHECK(cudaFuncSetAttribute(k_umma2_rowsq, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+                CUDA_CHECK(cudaFuncSetAttribute(k_umma2_rowsq<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
                 attr = true;
             }
             const int m_pairs = (mt + 1) / 2;
@@ -1307,7 +1382,7 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
                 CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
                 wc = ctr.as<unsigned int>();
             }
-            k_umma2_rowsq<<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, th, (int)n, m_pairs, nt, k_tiles,
+            k_umma2_rowsq<false><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, th, (int)n, m_pairs, nt, k_tiles,
                                                                          part.as<double>(), wc);
             LAUNCH_CHECK(c);
         } else if (NTX == 1)
@@ -1347,6 +1422,81 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
     launch_umma<false, EPI_STORE>(c, NT, sc, ta, th, tl, (int)n, (int)N, nullptr, 0, part.as<double>(), 1.0, 0.0);
     k_reduce_splits<<<(unsigned)((n * N + 255) / 256), 256, 0, c->stream>>>(n, N, splits, part.as<double>(), out, ldo,
                                                                             alpha, beta);
+    LAUNCH_CHECK(c);
+}
+
+void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
+                       const void* X, int dtx, int64_t ldx, double* rowsq) {
+    if (M <= 0) return;
+    if (N <= 0 || K <= 0) {
+        CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
+        return;
+    }
+    if (K % 8 != 0 || lda % 8 != 0 || ((uintptr_t)A16 % 16) != 0)
+        fail(BCUR_E_INVALID_ARGUMENT, "gemm_rowsumsq_f16: K and lda must be multiples of 8, A 16-byte aligned");
+    ProfScope prof(c, "umma_atx_rowsq", 2.0 * M * N * K, 2.0 * K * M + (double)dtype_size(dtx) * K * N + 8.0 * M);
+    (void)umma_ok(BCUR_F32, K, lda, A16);  // reads the environment switches once
+    // X → fp16 with one power-of-two scale from its max (device-side; no host sync)
+    DevBuf mx(c, 64), x16(c, (size_t)K * N * 2);
+    CUDA_CHECK(cudaMemsetAsync(mx.ptr, 0, 8, c->stream));
+    int* q = reinterpret_cast<int*>(mx.as<unsigned int>() + 1);
+    const unsigned gx = (unsigned)std::min<int64_t>((K * N + 255) / 256, 4LL * c->sm_count);
+    const unsigned gc = (unsigned)((K * N + 255) / 256);
+    if (dtx == BCUR_F32) {
+        k_absmax<float><<<gx, 256, 0, c->stream>>>((const float*)X, K, N, ldx, mx.as<unsigned int>());
+        k_to_f16<float><<<gc, 256, 0, c->stream>>>((const float*)X, K, N, ldx, mx.as<unsigned int>(),
+                                                   x16.as<uint16_t>(), q);
+    } else {
+        k_absmax<double><<<gx, 256, 0, c->stream>>>((const double*)X, K, N, ldx, mx.as<unsigned int>());
+        k_to_f16<double><<<gc, 256, 0, c->stream>>>((const double*)X, K, N, ldx, mx.as<unsigned int>(),
+                                                    x16.as<uint16_t>(), q);
+    }
+    LAUNCH_CHECK(c);
+    constexpr int BKH = bke<true>();
+    const uint64_t dA[2] = {(uint64_t)K, (uint64_t)M}, sA[1] = {(uint64_t)lda * 2};
+    const uint32_t bA[2] = {BKH, BM};
+    const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
+    const uint32_t bX[2] = {BKH, BN};
+    CUtensorMap ta = make_map(A16, 2, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap tx = make_map(x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    const int k_tiles = (int)((K + BKH - 1) / BKH);
+    const int mt = (int)((M + BM - 1) / BM);
+    const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
+    const int nt = (int)((N + NTX * BN - 1) / (NTX * BN));
+    DevBuf part(c, (size_t)nt * NTX * M * sizeof(double));
+    if (NTX == 4 && mt >= 2 && !g_no_pair) {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_umma2_rowsq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
+            attr = true;
+        }
+        const int m_pairs = (mt + 1) / 2;
+        const int pairs = std::min(m_pairs * nt, c->sm_count / 2);
+        DevBuf ctr;
+        unsigned int* wc = nullptr;
+        if (pairs < m_pairs * nt && !g_wave_barrier_off) {
+            ctr = DevBuf(c, 64);
+            CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
+            wc = ctr.as<unsigned int>();
+        }
+        k_umma2_rowsq<true><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, tx, (int)M, m_pairs, nt, k_tiles,
+                                                                           part.as<double>(), wc);
+        LAUNCH_CHECK(c);
+    } else {
+        Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
+        sc.a_rn = 1;  // converted operands: no transform
+        if (NTX == 1)
+            launch_umma_nt<false, EPI_ROWSQ, 1, false, true>(c, sc, ta, tx, tx, (int)M, (int)N, nullptr, 0,
+                                                             part.as<double>(), 1.0, 0.0);
+        else if (NTX == 2)
+            launch_umma_nt<false, EPI_ROWSQ, 2, false, true>(c, sc, ta, tx, tx, (int)M, (int)N, nullptr, 0,
+                                                             part.as<double>(), 1.0, 0.0);
+        else
+            launch_umma_nt<false, EPI_ROWSQ, 4, false, true>(c, sc, ta, tx, tx, (int)M, (int)N, nullptr, 0,
+                                                             part.as<double>(), 1.0, 0.0);
+    }
+    k_sum_tiles_scaled<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(M, nt * NTX, part.as<double>(), colexp, q,
+                                                                           rowsq);
     LAUNCH_CHECK(c);
 }
 

@@ -12,8 +12,11 @@ enum Op { OP_N = 0, OP_T = 1 };
 // ---- reductions (kernels_reduce.cu) --------------------------------------
 // out[g] = Σ_{j∈block g} Σ_i a(i,j)²  (fp64; offsets are device, relative to a's first column)
 // shadow (nullable, fp32 A only): also write the TF32-rounded copy of A (ld lds)
+// Optional copies written in the same pass (fp32 A): `shadow` = TF32-rounded fp32, or
+// `sh16` = fp16 scaled per column by 2^colexp[j] (exact; see gemm_rowsumsq_f16)
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
-                 double* d_out, float* shadow = nullptr, int64_t lds = 0);
+                 double* d_out, float* shadow = nullptr, int64_t lds = 0, uint16_t* sh16 = nullptr,
+                 int* colexp = nullptr);
 // out[j] = Σ_c v(j,c)²   then segmented into blocks: out_blocks[g]
 void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64_t ld, const int64_t* d_offsets,
                       int64_t G, double* d_rows /*nullable*/, double* d_blocks);
@@ -38,6 +41,13 @@ void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, c
 // a_rounded: A is already rounded to TF32 (block_sumsq's shadow) — the X1 pass skips its transform
 void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                    const void* B, int dtb, int64_t ldb, double* rowsq, bool a_rounded = false);
+// rowsq[j] = Σ_c (AᵀX)_jc² from block_sumsq's fp16 copy of A (K × M, ld lda, column j scaled
+// by 2^colexp[j]).  X (K × N, fp32/fp64) is converted to fp16 scaled by a power of two
+// from its max; the tensor cores run kind::f16 (same 11-bit significand as the
+// round-to-nearest 1×TF32 pass, twice the MMA rate, half the bytes) and the scales are
+// removed exactly in fp64.
+void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
+                       const void* B, int dtb, int64_t ldb, double* rowsq);
 // out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);

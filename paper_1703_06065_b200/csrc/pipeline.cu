@@ -546,13 +546,16 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
 // TF32-rounded copy of an fp32 A (ld m), written by the norms pass: the X1 row-Σ² passes
 // (residual, greedy scores) read it and skip their in-kernel rounding (shared-memory
 // bound).  Empty when A is fp64 or the copy does not fit in device memory.
+// block_sumsq's fp16 copy of an fp32 A for the row-Σ² passes: column j scaled by
+// 2^exps[j] (exact), rounded to nearest — the same 11-bit significands a round-to-nearest
+// TF32 copy holds, in half the bytes, for kind::f16 MMAs (twice the TF32 rate).
 struct RoundedA {
-    DevBuf buf;
-    const float* ptr() const { return buf.as<float>(); }
+    DevBuf buf, exps;
 };
 static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra) {
-    if (a->dtype != BCUR_F32 || a->m % 4 != 0 || a->m <= 0 || a->n <= 0) return;
-    const size_t need = (size_t)a->m * (size_t)a->n * 4;
+    if (a->dtype != BCUR_F32 || a->m % 32 != 0 || a->m <= 0 || a->n <= 0 || !umma_ok(a->dtype, a->m, a->ld, a->ptr))
+        return;
+    const size_t need = (size_t)a->m * (size_t)a->n * 2;
     const size_t headroom = (size_t)8 << 30;  // the rest of the pipeline's workspace
     if (!c->cached(need)) {  // first call for this shape (cudaMemGetInfo is not free: not per step)
         size_t freeb = 0, totalb = 0;
@@ -561,15 +564,15 @@ static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra) {
         if (need + headroom > freeb) c->trim();                  // make room from the workspace cache
     }
     ra->buf = DevBuf(c, need);
+    ra->exps = DevBuf(c, (size_t)a->n * sizeof(int));
 }
-// A operand of the row-Σ² passes: the rounded copy when present
-static const void* rowsq_a(const DMat* a, const RoundedA* ra, int64_t* ld) {
-    if (ra && ra->buf.ptr) {
-        *ld = a->m;
-        return ra->buf.ptr;
-    }
-    *ld = a->ld;
-    return a->ptr;
+// rows[j] = Σ_c (AᵀX)_jc² over the shard's columns: from the fp16 copy when present
+static void rowsq_pass(Ctx* c, const DMat* a, const RoundedA* ra, int64_t N, const void* X, int dtx, int64_t ldx,
+                       double* rows) {
+    if (ra && ra->buf.ptr)
+        gemm_rowsumsq_f16(c, a->n, N, a->m, ra->buf.as<uint16_t>(), a->m, ra->exps.as<int>(), X, dtx, ldx, rows);
+    else
+        gemm_rowsumsq(c, OP_T, OP_N, a->n, N, a->m, a->ptr, a->dtype, a->ld, X, dtx, ldx, rows);
 }
 
 // Σ_g ‖Qᵀ A_g‖² (shard-local per-block values in d_blk_local, allreduced total)
@@ -577,10 +580,7 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
                              const RoundedA* ra = nullptr) {
     const int64_t nl = a->n;
     Mat64 rows(c, nl, 1), tot(c, 1, 1);
-    int64_t lda = 0;
-    const void* ap = rowsq_a(a, ra, &lda);
-    gemm_rowsumsq(c, OP_T, OP_N, nl, B.rank, a->m, ap, a->dtype, lda, B.buf.ptr, B.dt, B.rows, rows.p(),
-                  ap != a->ptr);
+    rowsq_pass(c, a, ra, B.rank, B.buf.ptr, B.dt, B.rows, rows.p());
     Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     double* b = d_blk_local ? d_blk_local : blk.p();
     segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
@@ -614,8 +614,9 @@ static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<dou
     Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     *d_global = Mat64(c, s.G, 1);
     if (ra) make_rounded(c, a, ra);
-    block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p(),
-                ra ? ra->buf.as<float>() : nullptr, a->m);
+    const bool f16 = ra && ra->buf.ptr;
+    block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p(), nullptr, a->m,
+                f16 ? ra->buf.as<uint16_t>() : nullptr, f16 ? ra->exps.as<int>() : nullptr);
     gather_blocks_vec(c, s, loc.p(), d_global->p());
     bn2->assign(s.G, 0.0);
     d2h(c, bn2->data(), d_global->p(), s.G);
@@ -761,9 +762,7 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
         const int64_t r = cgs2_append(c, &B, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)), dt, false);
         if (r > 0) {
             // res_g −= ‖Q_newᵀ A_g‖²
-            int64_t lda = 0;
-            const void* ap = rowsq_a(a, &ra, &lda);
-            gemm_rowsumsq(c, OP_T, OP_N, a->n, r, m, ap, dt, lda, B.col(cur), B.dt, B.rows, rows.p(), ap != a->ptr);
+            rowsq_pass(c, a, &ra, r, B.col(cur), B.dt, B.rows, rows.p());
             segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
             gather_blocks_vec(c, s, loc.p(), upd.p());
             axpy_neg(c, upd.p(), res.p(), G);

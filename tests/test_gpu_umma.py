@@ -94,3 +94,21 @@ def test_x_upper(B, m, n):
     a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
     x = np.asfortranarray(np.triu(gen.standard_normal((n, n))))
     assert rel_fro(B.structured_product(a, x, x_upper=True), a.astype(np.float64) @ x) < 2e-6
+
+
+# fp16 row-Σ² path (kind::f16 on block_sumsq's per-column-scaled copy): single-CTA NT = 1/2/4
+# and the CTA-pair kernel; columns spanning many binades exercise the per-column scales
+@pytest.mark.parametrize("m,n,N", [(512, 1000, 40), (512, 1000, 128), (1024, 768, 300), (2048, 1024, 1024)])
+def test_rowsq_f16(B, m, n, N):
+    gen = np.random.default_rng(m + n + N)
+    a = gen.standard_normal((m, n)) * np.exp2(gen.integers(-40, 40, size=n))[None, :]
+    a = np.asfortranarray(a.astype(np.float32))
+    q = np.asfortranarray(gen.standard_normal((m, N)) * 1e-3)
+    ref = np.sum((a.astype(np.float64).T @ q) ** 2, axis=1)
+    got = B.structured_product(a, q, rowsq_f16=True)
+    # same rounding model as the 1×TF32 pass (11-bit significands, round to nearest)
+    rel = (got - ref) / ref
+    assert np.max(np.abs(rel)) < 5e-4
+    # unbiased: the per-row errors average out (column scales span 2^±40, so the plain
+    # total would be one column's error)
+    assert abs(rel.mean()) < 3e-6 + 4 * rel.std() / np.sqrt(n)
