@@ -157,8 +157,11 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
  *   BCUR_PRODUCT_X_UPPER   X is upper triangular (zero below its diagonal; the tcgen05 path
  *                          skips that part of the product)
  *   BCUR_PRODUCT_ROWSQ_F16 out (n × 1) = Σ_c (AᵀX)_jc² through the pipelines' fp16 path
- *                          (fp32 A with m % 32 == 0; transpose = 1) */
-enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4 };
+ *                          (fp32 A with m % 64 == 0; transpose = 1)
+ *   BCUR_PRODUCT_H3        A·X, AᵀX or (with GRAM) AᵀA through the pipelines' 3×FP16 form: A
+ *                          split into fp16 hi + lo by the norms pass (fp32 A; m % 64 == 0 for
+ *                          A·X, m % 8 == 0 for AᵀX) */
+enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4, BCUR_PRODUCT_H3 = 8 };
 bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
 /* sampler.cpp:116-146 draw_blocks (probabilities on the host, one uniform per draw
  * drawn by the caller from its Rng; margins_out[t] = distance of u_t to the nearest

@@ -542,23 +542,54 @@ bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int t
     API_BEGIN
     Ctx* c = C(ctx);
     DMat *A = M(a), *O = M(out);
-    if (flags & ~(BCUR_PRODUCT_GRAM | BCUR_PRODUCT_X_UPPER | BCUR_PRODUCT_ROWSQ_F16))
+    if (flags & ~(BCUR_PRODUCT_GRAM | BCUR_PRODUCT_X_UPPER | BCUR_PRODUCT_ROWSQ_F16 | BCUR_PRODUCT_H3))
         fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: bad flags");
+    if (flags & BCUR_PRODUCT_H3) {
+        // the pipelines' 3×FP16 form: A split once by the norms pass into fp16 hi + lo
+        DMat* X = x ? M(x) : nullptr;
+        const bool gram = (flags & BCUR_PRODUCT_GRAM) != 0;
+        if (flags & BCUR_PRODUCT_ROWSQ_F16) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: H3 has no row-sum form");
+        if (A->dtype != BCUR_F32 || A->ld % 4 != 0 || ((uintptr_t)A->ptr % 16) != 0 || !ops::h3_ok(A->m))
+            fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: H3 needs fp32 A with m % 64 == 0");
+        if (gram ? (x || !transpose) : !X) fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: bad H3 operands");
+        const int64_t K = transpose ? A->m : A->n, rows = transpose ? A->n : A->m, N = gram ? A->n : X->n;
+        if (!gram && (X->dtype != BCUR_F64 || X->m != K)) fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: bad X");
+        if (O->dtype != BCUR_F64 || O->m != rows || O->n != N)
+            fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: output must be fp64 rows × N");
+        DevBuf il(c, (size_t)A->m * A->n * 4), exps(c, (size_t)A->n * sizeof(int)),
+            off(c, 2 * sizeof(int64_t)), tot(c, sizeof(double));
+        const int64_t h_off[2] = {0, A->n};
+        CUDA_CHECK(cudaMemcpyAsync(off.ptr, h_off, sizeof h_off, cudaMemcpyHostToDevice, c->stream));
+        ops::block_sumsq(c, A->ptr, A->dtype, A->m, A->ld, off.as<int64_t>(), 1, tot.as<double>(), nullptr, A->m,
+                         nullptr, exps.as<int>(), il.as<uint16_t>());
+        const int fl = gram ? ops::GEMM_SYM_UPPER : (flags & BCUR_PRODUCT_X_UPPER) ? ops::GEMM_B_UPPER : 0;
+        if (gram) {  // X = the same matrix, split on its own (K-major X operand)
+            ops::SplitF16 xs;
+            ops::split_f16(c, A->ptr, A->dtype, A->m, A->n, A->ld, nullptr, &xs);
+            ops::umma_h3(c, false, il.as<uint16_t>(), exps.as<int>(), A->m, A->n, ops::view(xs), 1.0, 0.0,
+                         (double*)O->ptr, O->ld, fl);
+        } else {
+            ops::umma_h3(c, !transpose, il.as<uint16_t>(), exps.as<int>(), A->m, A->n, X->ptr, X->dtype, X->n, X->ld,
+                         1.0, 0.0, (double*)O->ptr, O->ld, fl);
+        }
+        c->sync();
+        return BCUR_OK;
+    }
     if (flags & BCUR_PRODUCT_ROWSQ_F16) {
         DMat* X = x ? M(x) : nullptr;
         if (flags != BCUR_PRODUCT_ROWSQ_F16 || !X || !transpose)
             fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the fp16 row-sum form takes X and transpose = 1");
-        if (A->dtype != BCUR_F32 || A->m % 32 != 0 || A->ld % 4 != 0 || ((uintptr_t)A->ptr % 16) != 0)
-            fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the fp16 row-sum form needs fp32 A with m % 32 == 0");
+        if (A->dtype != BCUR_F32 || A->m % 64 != 0 || A->ld % 4 != 0 || ((uintptr_t)A->ptr % 16) != 0)
+            fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: the fp16 row-sum form needs fp32 A with m % 64 == 0");
         if (X->m != A->m) fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: inner dimensions differ");
         if (O->dtype != BCUR_F64 || O->m != A->n || O->n != 1)
             fail(BCUR_E_DIMENSION_MISMATCH, "sketch_product_ex: row sums go to an fp64 n × 1 output");
-        DevBuf a16(c, (size_t)A->m * A->n * 2), exps(c, (size_t)A->n * sizeof(int)), off(c, 2 * sizeof(int64_t)),
+        DevBuf a16(c, (size_t)A->m * A->n * 4), exps(c, (size_t)A->n * sizeof(int)), off(c, 2 * sizeof(int64_t)),
             tot(c, sizeof(double));
         const int64_t h_off[2] = {0, A->n};
         CUDA_CHECK(cudaMemcpyAsync(off.ptr, h_off, sizeof h_off, cudaMemcpyHostToDevice, c->stream));
         ops::block_sumsq(c, A->ptr, A->dtype, A->m, A->ld, off.as<int64_t>(), 1, tot.as<double>(), nullptr, A->m,
-                         a16.as<uint16_t>(), exps.as<int>());
+                         nullptr, exps.as<int>(), a16.as<uint16_t>());
         ops::gemm_rowsumsq_f16(c, A->n, X->n, A->m, a16.as<uint16_t>(), A->m, exps.as<int>(), X->ptr, X->dtype, X->ld,
                                (double*)O->ptr);
         c->sync();

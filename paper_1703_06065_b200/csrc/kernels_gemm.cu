@@ -215,6 +215,19 @@ namespace ops {
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags) {
     if (M <= 0 || N <= 0) return;
+    // fp32 products wide enough to be tensor-bound (N ≥ 256, Grams) → 3×FP16 on operands split
+    // here (the split is one extra pass over A: worth it only where the MMAs dominate).  This
+    // includes the GEMM_X1 corrections: 3×FP16 is both faster than the 1×TF32 pass (no in-kernel
+    // rounding) and exact to ~2⁻²² instead of 2⁻¹¹ of the correction.
+    if (dta == BCUR_F32 && K > 0 && tb == OP_N && (N >= 256 || (flags & GEMM_SYM_UPPER)) &&
+        h3_ok(ta == OP_N ? M : K) && ((uintptr_t)A % 16) == 0) {
+        const bool sym = (flags & GEMM_SYM_UPPER) && A == B && dta == dtb && lda == ldb && M == N && beta == 0.0;
+        if (ta == OP_N)
+            gemm_h3(c, true, A, dta, M, K, lda, B, dtb, N, ldb, alpha, beta, C, ldc, flags & GEMM_B_UPPER);
+        else
+            gemm_h3(c, false, A, dta, K, M, lda, B, dtb, N, ldb, alpha, beta, C, ldc, sym ? GEMM_SYM_UPPER : 0);
+        return;
+    }
     // fp32 A-passes → tcgen05 3×TF32 kernels
     if (dta == BCUR_F32 && K > 0 && tb == OP_N) {
         if (ta == OP_N && K % 4 == 0 && umma_ok(dta, M, lda, A)) {

@@ -110,7 +110,12 @@ __device__ __forceinline__ double sq_col(const T* __restrict__ col, int64_t m, b
 // Σ col[i]² of an fp32 column (m % 4 == 0, 16-byte aligned) that also writes its fp16 copy
 // scaled by 2^p (p = f16_scale_exp(max |col|), stored in colexp[j]): the max pass reads the
 // column from HBM; the scaling pass re-reads it from L2.
-__device__ double sq_col_f16(const float* __restrict__ col, int64_t m, uint16_t* __restrict__ sh16, int* colexp_j) {
+// il16 (nullable, m % 64 == 0): also the 3×FP16 operand of the column (kernels_umma.cu, H3) —
+// hi and the fp16 remainder lo = rn(col·2^p − hi), interleaved per 64-row chunk
+// [hi 64 | lo 64] (2m halves per column), so a tile's hi and lo rows are one 256-byte run.
+// hi + lo carry 22 significant bits.
+__device__ double sq_col_f16(const float* __restrict__ col, int64_t m, uint16_t* __restrict__ sh16,
+                             uint16_t* __restrict__ sl16, int* colexp_j) {
     double s0 = 0.0, s1 = 0.0;
     float mx = 0.0f;
     const float4* c4 = reinterpret_cast<const float4*>(col);
@@ -126,11 +131,22 @@ __device__ double sq_col_f16(const float* __restrict__ col, int64_t m, uint16_t*
     const int p = f16_scale_exp(block_max_all(mx));
     if (threadIdx.x == 0) *colexp_j = p;
     uint2* o4 = reinterpret_cast<uint2*>(sh16);
+    uint2* l4 = reinterpret_cast<uint2*>(sl16);
     for (int64_t i = threadIdx.x; i < m4; i += RT) {
         const float4 v = __ldcs(c4 + i);
-        const __half2 lo = __floats2half2_rn(ldexpf(v.x, p), ldexpf(v.y, p));
-        const __half2 hi = __floats2half2_rn(ldexpf(v.z, p), ldexpf(v.w, p));
-        __stcs(o4 + i, make_uint2(*reinterpret_cast<const uint32_t*>(&lo), *reinterpret_cast<const uint32_t*>(&hi)));
+        const float x0 = ldexpf(v.x, p), x1 = ldexpf(v.y, p), x2 = ldexpf(v.z, p), x3 = ldexpf(v.w, p);
+        const __half2 h01 = __floats2half2_rn(x0, x1);
+        const __half2 h23 = __floats2half2_rn(x2, x3);
+        if (sh16)
+            __stcs(o4 + i, make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23)));
+        if (sl16) {  // exact fp32 remainders (x and hi share the binade), rounded to fp16
+            const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+            const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y);
+            const __half2 l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+            const int64_t r = i << 2, at = ((r >> 6) << 5) + ((r & 63) >> 2);  // uint2 units: chunk = 32
+            __stcs(l4 + at, make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23)));
+            __stcs(l4 + at + 16, make_uint2(*reinterpret_cast<const uint32_t*>(&l01), *reinterpret_cast<const uint32_t*>(&l23)));
+        }
     }
     return s0 + s1;
 }
@@ -142,13 +158,14 @@ __global__ void __launch_bounds__(RT) k_block_sumsq(const T* __restrict__ a, int
                                                     const int64_t* __restrict__ off, int Z, bool vec,
                                                     double* __restrict__ partial, float* __restrict__ shadow,
                                                     int64_t lds, uint16_t* __restrict__ sh16,
-                                                    int* __restrict__ colexp) {
+                                                    uint16_t* __restrict__ sl16, int* __restrict__ colexp) {
     const int64_t g = blockIdx.x;
     const int z = blockIdx.y;
     double s = 0.0;
     for (int64_t j = off[g] + z; j < off[g + 1]; j += Z) {
-        if (sizeof(T) == 4 && sh16)
-            s += sq_col_f16(reinterpret_cast<const float*>(a + j * ld), m, sh16 + j * lds, colexp + j);
+        if (sizeof(T) == 4 && (sh16 || sl16))
+            s += sq_col_f16(reinterpret_cast<const float*>(a + j * ld), m, sh16 ? sh16 + j * lds : nullptr,
+                            sl16 ? sl16 + 2 * j * m : nullptr, colexp + j);
         else
             s += sq_col(a + j * ld, m, vec, shadow ? shadow + j * lds : nullptr);
     }
@@ -222,7 +239,7 @@ __global__ void k_max_dev_identity(const double* __restrict__ g, int w, int64_t 
 namespace ops {
 
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
-                 double* d_out, float* shadow, int64_t lds, uint16_t* sh16, int* colexp) {
+                 double* d_out, float* shadow, int64_t lds, uint16_t* sh16, int* colexp, uint16_t* sl16) {
     if (G <= 0) return;
     ProfScope prof(c, "block_sumsq", 0.0, 0.0);
     // enough CTAs to fill the machine several times over
@@ -233,14 +250,15 @@ void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int
     dim3 grid((unsigned)G, (unsigned)Z);
     if (dt == BCUR_F32)
     {
-        if (sh16 && !(vec && m % 4 == 0 && lds % 4 == 0))
+        if ((sh16 || sl16) && !(vec && m % 4 == 0 && lds % 4 == 0))
             fail(BCUR_E_INVALID_ARGUMENT, "block_sumsq: the fp16 copy needs aligned columns with m % 4 == 0");
+        if (sl16 && m % 64 != 0) fail(BCUR_E_INVALID_ARGUMENT, "block_sumsq: the 3×FP16 copy needs m % 64 == 0");
         k_block_sumsq<float><<<grid, RT, 0, c->stream>>>((const float*)a, m, ld, d_offsets, Z,
                                                          vec && (shadow == nullptr || (lds % 4 == 0)),
-                                                         part.as<double>(), shadow, lds, sh16, colexp);
+                                                         part.as<double>(), shadow, lds, sh16, sl16, colexp);
     } else
         k_block_sumsq<double><<<grid, RT, 0, c->stream>>>((const double*)a, m, ld, d_offsets, Z, vec, part.as<double>(),
-                                                          nullptr, 0, nullptr, nullptr);
+                                                          nullptr, 0, nullptr, nullptr, nullptr);
     LAUNCH_CHECK(c);
     k_segment_rows<<<(unsigned)((G + 255) / 256), 256, 0, c->stream>>>(part.as<double>(), Z, G, d_out);
     LAUNCH_CHECK(c);

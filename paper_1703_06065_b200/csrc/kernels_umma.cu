@@ -38,6 +38,7 @@ __device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, 
 bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
 bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (experiments)
 bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
+int g_pf = -1;                    // BCUR_UMMA_PF: A-tile L2 prefetch distance in stages (experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
 // K elements per stage: tiles are 128-byte K rows (SWIZZLE_128B) — 32 tf32 or 64 fp16
@@ -53,19 +54,24 @@ template <bool H> constexpr int bke() { return H ? 2 * BK : BK; }
 //      accumulator per tile; drained into fp32 (round-to-nearest) registers.
 //      Only for sums of squared projections (ROWSQ): the unbiased rounding errors cancel
 //      to ~1e-8 relative over the ~10⁸ terms.
-template <int NT, bool X3>
+//  H3 (3×FP16, H && X3): A and x both pre-split into fp16 hi + lo (exact power-of-two
+//      scales per column, removed in the fp64 epilogue); stage = {a_hi, a_lo, x_hi[NT],
+//      x_lo[NT]} all by TMA — no transform warps, and each kind::f16 MMA runs at twice the
+//      TF32 rate.  hi + lo carry 22 significant bits, as the 3×TF32 split does.
+template <int NT, bool X3, bool H = false>
 struct Cfg {
+    static constexpr bool H3 = H && X3;
     static constexpr int NACC = X3 ? 2 : 1;                                  // accumulators per tile
     static constexpr uint32_t BUFCOLS = NACC * BN * NT;                     // per drain buffer
     static constexpr int DCOLS = 64;                                         // output columns per drain warp
-    // TMA stage = {a_raw, x_hi[NT], x_lo[NT] (X3)}; the a_lo split (X3) lives in its own
+    // TMA stage = {a_raw, x_hi[NT], x_lo[NT] (X3)}; the a_lo split (3×TF32) lives in its own
     // LO_SLOTS-deep ring so the TMA ring keeps as many stages in flight as fit (the
-    // HBM-bound passes need ≥ 6 × 16 KB of A in flight per SM).
-    static constexpr int LO_SLOTS = X3 ? 3 : 0;
-    static constexpr uint32_t STAGE = A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
+    // HBM-bound passes need ≥ 6 × 16 KB of A in flight per SM).  H3 stages a_lo by TMA.
+    static constexpr int LO_SLOTS = (X3 && !H3) ? 3 : 0;
+    static constexpr uint32_t STAGE = (H3 ? 2 : 1) * A_TILE + (X3 ? 2 : 1) * NT * X_TILE;
     static constexpr int STAGES_FIT = (int)((232448u - 1280u - LO_SLOTS * A_TILE) / STAGE);
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int LOR = X3 ? LO_SLOTS : STAGES;  // lo_ready barriers
+    static constexpr int LOR = H3 ? 0 : X3 ? LO_SLOTS : STAGES;  // lo_ready barriers
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE + LO_SLOTS * A_TILE + 1024 + 256;
     static constexpr uint32_t TMEM_USED = 2 * BUFCOLS;                      // ≤ 512
     static constexpr uint32_t TMEM_COLS = TMEM_USED <= 32 ? 32 : TMEM_USED <= 64 ? 64 : TMEM_USED <= 128 ? 128
@@ -73,10 +79,11 @@ struct Cfg {
     static constexpr int NDRAIN = 4 * NT * (BN / DCOLS);                     // drain warps
     // X3 runs whole warpgroups: WG0 = producer, MMA, 2 transform warps; NT drain warpgroups;
     // one more transform warpgroup (the a_lo split is the MMA's feeder).  The drain
-    // warpgroups take the registers the others give up (setmaxnreg).
-    static constexpr int NTRANSFORM = (X3 && NT == 1) ? 10 : 6;
+    // warpgroups take the registers the others give up (setmaxnreg).  H3 keeps only WG0
+    // (warps 2, 3 idle) and the drains.
+    static constexpr int NTRANSFORM = H3 ? 2 : (X3 && NT == 1) ? 10 : 6;
     // register re-split (setmaxnreg) whenever the launch cap is below what the drains need
-    static constexpr bool RESPLIT = X3 || NT == 4;
+    static constexpr bool RESPLIT = (X3 && !(H3 && NT == 1)) || NT == 4;
     static constexpr int NTHREADS = 32 * (2 + NTRANSFORM + NDRAIN);
     static constexpr uint32_t REG_LOW = 56;
     // setmaxnreg moves registers only inside the CTA's launch allocation: every thread starts
@@ -86,7 +93,7 @@ struct Cfg {
     static constexpr uint32_t REG_DRAIN_FIT =
         R0 + ((NTHREADS - 32 * NDRAIN) * (R0 - REG_LOW) / (32 * NDRAIN)) / 8 * 8;
     static constexpr uint32_t REG_DRAIN = REG_DRAIN_FIT > 232 ? 232 : REG_DRAIN_FIT;
-    static_assert(!RESPLIT || (NTHREADS % 128 == 0 && R0 > REG_LOW &&
+    static_assert(!RESPLIT || (NTHREADS % 128 == 0 && R0 > REG_LOW && REG_DRAIN > R0 &&
                           (NTHREADS - 32 * NDRAIN) * (R0 - REG_LOW) >= 32 * NDRAIN * (REG_DRAIN - R0)),
                   "X3 register split must fit the launch allocation");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
@@ -113,6 +120,9 @@ __device__ __forceinline__ float lo_of(float a) {
 // x rounded to the nearest TF32 (ties away) as the tensor core reads it: half an ulp added,
 // the low bits left for the MMA to ignore (one op; for operands only an MMA consumes)
 __device__ __forceinline__ float rn_mma(float x) { return __uint_as_float(__float_as_uint(x) + 0x1000u); }
+
+// 2^e as a double (|e| < 1022): the exact scale of the split operands
+__device__ __forceinline__ double exp2_int(int e) { return __longlong_as_double((long long)(1023 + e) << 52); }
 
 // ------------------------------------------------------------- PTX helpers
 // Warp index broadcast from lane 0: ptxas then knows role branches on it are warp-uniform.
@@ -154,6 +164,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* tm, ui
 // beyond what the shared-memory stage ring can keep in flight.
 __device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* tm, int c0, int c1) {
     asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(tm), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(tm), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* tm, int c0, int c1, int c2, int c3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global [%0, {%1, %2, %3, %4}];" ::"l"(tm), "r"(c0), "r"(c1), "r"(c2),
+                 "r"(c3) : "memory");
 }
 __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* tm, int c0, int c1, int c2) {
     asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(tm), "r"(c0), "r"(c1), "r"(c2)
@@ -270,6 +290,7 @@ struct Sched {
     int k_tiles, kps, sym, tri_x;
     unsigned int* wave_ctr;
     int a_rn;  // X1: A already rounded to TF32 (no transform)
+    int pf;    // A-tile L2 prefetch distance (stages)
 };
 // CTAs that have a tile in waves 0..w
 __device__ __forceinline__ unsigned int wave_arrivals(const Sched& sc, int w) {
@@ -308,14 +329,19 @@ __device__ __forceinline__ TileInfo tile_info(const Sched& sc, int t) {
     return ti;
 }
 
+// Scales (H3): the fp64 result of output row r, column j is multiplied by
+// 2^−(rexp[r] + cexp[j]) (either nullable) — the exact power-of-two scales of the split operands.
 template <bool A_MN, int EPI, int NT, bool X3, bool H = false>
-__global__ void __launch_bounds__(Cfg<NT, X3>::NTHREADS, 1)
+__global__ void __launch_bounds__(Cfg<NT, X3, H>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
-       const __grid_constant__ CUtensorMap tmXl, int M, int N, const Sched sc,
-       double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta) {
+       const __grid_constant__ CUtensorMap tmXl, const __grid_constant__ CUtensorMap tmAl, int M, int N,
+       const Sched sc, double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta,
+       const int* __restrict__ rexp, const int* __restrict__ cexp) {
     // instruction descriptor: fp32 accumulate, tf32 × tf32 (H: f16 × f16), B K-major,
     // N = n_cols, M = 128
-    static_assert(!H || (!X3 && EPI == EPI_ROWSQ && !A_MN), "fp16 operands: pre-converted row-sum-of-squares only");
+    static_assert(!H || (X3 ? EPI == EPI_STORE : (EPI == EPI_ROWSQ && !A_MN)),
+                  "fp16 operands: 3×FP16 products, or the pre-converted row-sum-of-squares");
+    constexpr bool H3 = H && X3;
     constexpr uint32_t FMT = H ? 0u : 2u;
     constexpr int BKE = bke<H>();
     auto idesc = [](uint32_t n_cols) -> uint32_t {
@@ -323,7 +349,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                ((uint32_t)(BM >> 4) << 24);
     };
 
-    using CF = Cfg<NT, X3>;
+    using CF = Cfg<NT, X3, H>;
     constexpr int NACC = CF::NACC;
     constexpr uint32_t BUFCOLS = CF::BUFCOLS;
     constexpr int STAGES = CF::STAGES;
@@ -371,10 +397,11 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    // per stage: [a_raw][x_hi tile 0..NT-1][x_lo tile 0..NT-1 (X3)]; then the a_lo slots
+    // per stage: [a_raw][a_lo (H3)][x_hi tile 0..NT-1][x_lo tile 0..NT-1 (X3)]; then the a_lo slots
+    constexpr uint32_t XOFF = (H3 ? 2 : 1) * A_TILE;
     auto a_raw = [&](int s) { return smem + s * STAGE; };
-    auto x_hi = [&](int s) { return smem + s * STAGE + A_TILE; };
-    auto x_lo = [&](int s) { return smem + s * STAGE + A_TILE + NT * X_TILE; };
+    auto x_hi = [&](int s) { return smem + s * STAGE + XOFF; };
+    auto x_lo = [&](int s) { return smem + s * STAGE + XOFF + NT * X_TILE; };
     auto a_lo = [&](int l) { return smem + STAGES * STAGE + l * A_TILE; };
 
     // roles: branch per warpgroup first so the register re-split (X3) is warpgroup-uniform
@@ -462,9 +489,11 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const bool plain = partial != nullptr || beta == 0.0;
             const double a_ = partial ? 1.0 : alpha;
             const int ncol = min(DC, N - col0);
+            const int re = (H3 && rexp && row < M) ? rexp[row] : 0;
 #pragma unroll
             for (int j = 0; j < DC; ++j) {
-                const double v = X3 ? (double)acc[j] + (double)cmp[X3 ? j : 0] : (double)acc[j];
+                double v = X3 ? (double)acc[j] + (double)cmp[X3 ? j : 0] : (double)acc[j];
+                if (H3) v *= exp2_int(-(re + ((cexp && j < ncol) ? cexp[col0 + j] : 0)));
                 if (j < ncol) {
                     double* o = dst + (int64_t)(col0 + j) * stride;
                     *o = plain ? a_ * v : fma(beta, *o, a_ * v);
@@ -478,7 +507,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         if (warp == 0) {
             // ------------------------------------------------------ TMA producer
             if (lane == 0) {
-                constexpr int PF = 12;  // A-tile L2 prefetch distance (stages)
+                const int PF = sc.pf;  // A-tile L2 prefetch distance (stages)
                 int gi = 0;             // stages issued so far (all tiles)
                 for (int t = blockIdx.x, w = 0; t < sc.total; t += gridDim.x, ++w) {
                     if (sc.wave_ctr && w > 0) {  // wave barrier (see Sched)
@@ -490,9 +519,22 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     }
                     const TileInfo ti = tile_info<NT>(sc, t);
                     const int kt0 = ti.kt0, nk = ti.nk, m_tile = ti.m_tile, n_tile = ti.n_tile;
+                    constexpr int MNA = H ? 64 : 32;  // MN elements per 128-byte row (A_MN)
+                    // H3: A is the interleaved hi/lo copy, a 4-D map (64, hi|lo, ...): one 256-byte
+                    // run per column and 64 rows holds both operands (see block_sumsq)
                     auto prefetch_a = [&](int i) {
                         const int k0 = (kt0 + i) * BKE;
-                        if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / 32));
+                        if (H3) {
+                            for (int hl = 0; hl < 2; ++hl) {
+                                if (A_MN) {
+                                    tma_prefetch_4d(&tmA, 0, hl, m_tile * 2, k0);
+                                    tma_prefetch_4d(&tmA, 0, hl, m_tile * 2 + 1, k0);
+                                } else {
+                                    tma_prefetch_4d(&tmA, 0, hl, k0 / 64, m_tile * BM);
+                                }
+                            }
+                        } else if (A_MN) tma_prefetch_3d(&tmA, 0, k0, m_tile * (BM / MNA));
+                        else if (H) tma_prefetch_4d(&tmA, 0, 0, k0 / 64, m_tile * BM);
                         else tma_prefetch_2d(&tmA, k0, m_tile * BM);
                     };
                     for (int i = 0; i < PF && i < nk; ++i) prefetch_a(i);
@@ -500,9 +542,20 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         const int s = gi % STAGES;
                         if (i + PF < nk) prefetch_a(i + PF);
                         mbar_wait(&empty[s], ((uint32_t)(gi / STAGES) & 1u) ^ 1u);
-                        mbar_expect_tx(&full[s], A_TILE + (X3 ? 2 : 1) * NT * X_TILE);
+                        mbar_expect_tx(&full[s], STAGE);
                         const int k0 = (kt0 + i) * BKE;
-                        if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / 32));
+                        if (H3) {
+                            for (int hl = 0; hl < 2; ++hl) {
+                                if (A_MN) {  // two 64-row chunks (8 KB MN atoms) × 64 K rows
+                                    tma_load_4d(a_raw(s) + hl * A_TILE, &tmA, &full[s], 0, hl, m_tile * 2, k0);
+                                    tma_load_4d(a_raw(s) + hl * A_TILE + A_TILE / 2, &tmA, &full[s], 0, hl,
+                                                m_tile * 2 + 1, k0);
+                                } else {
+                                    tma_load_4d(a_raw(s) + hl * A_TILE, &tmA, &full[s], 0, hl, k0 / 64, m_tile * BM);
+                                }
+                            }
+                        } else if (A_MN) tma_load_3d(a_raw(s), &tmA, &full[s], 0, k0, m_tile * (BM / MNA));
+                        else if (H) tma_load_4d(a_raw(s), &tmA, &full[s], 0, 0, k0 / 64, m_tile * BM);  // hi of the copy
                         else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
@@ -524,16 +577,20 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     const bool first = (i % CH) == 0;
                     if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
                     const uint32_t ph = (uint32_t)(gi / STAGES) & 1u;
-                    const int lr = X3 ? gi % LO_SLOTS : s;
+                    const int lr = (X3 && !H3) ? gi % (LO_SLOTS > 0 ? LO_SLOTS : 1) : s;
                     mbar_wait(&full[s], ph);
-                    mbar_wait(&lo_ready[lr], X3 ? (uint32_t)(gi / LO_SLOTS) & 1u : ph);
+                    if (!H3) mbar_wait(&lo_ready[lr], X3 ? (uint32_t)(gi / (LO_SLOTS > 0 ? LO_SLOTS : 1)) & 1u : ph);
                     tc_fence_after();
                     {  // whole warp (elect.sync inside the issue helpers)
-                        const uint32_t ar = smem_u32(a_raw(s)), al = smem_u32(a_lo(lr)), xh = smem_u32(x_hi(s));
+                        const uint32_t ar = smem_u32(a_raw(s)), xh = smem_u32(x_hi(s));
+                        const uint32_t al = H3 ? ar + A_TILE : smem_u32(a_lo(lr));
 #pragma unroll
                         for (int k8 = 0; k8 < BK / 8; ++k8) {
                             uint64_t da_r, da_l;
-                            if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
+                            if (A_MN && H) {  // [2 MN atoms of 64, 8 KB apart][64 K rows of 128 B, 8-row groups 1 KB apart]
+                                da_r = sdesc(ar + k8 * 2048, 8192, 1024, 2);
+                                da_l = sdesc(al + k8 * 2048, 8192, 1024, 2);
+                            } else if (A_MN) {  // [4 MN atoms, 4 KB apart][32 K rows of 128 B, 4-row groups 512 B apart]
                                 da_r = sdesc(ar + k8 * 1024, 4096, 512, 1);
                                 da_l = sdesc(al + k8 * 1024, 4096, 512, 1);
                             } else {     // K-major rows of 128 B, 8-row groups 1 KB apart; K step = 32 B
@@ -550,18 +607,18 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                             const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
                             if (!(dbg & 4)) {  // bit 2: skip the MMAs (timing experiments)
                                 umma_warp<H>(t_hi, da_r, dxh, idesc((X3 ? 2 : 1) * NT * BN), acc);
-                                if (X3) umma_tf32_warp(t_lo, da_l, dxh, idesc(NT * BN), 1u);
+                                if (X3) umma_warp<H>(t_lo, da_l, dxh, idesc(NT * BN), 1u);
                             }
                         }
                         umma_commit_warp(&empty[s]);
-                        if (X3) umma_commit_warp(&lo_empty[lr]);
+                        if (X3 && !H3) umma_commit_warp(&lo_empty[lr]);
                         if ((i % CH) == CH - 1 || i == nk - 1) umma_commit_warp(&tfull[b]);
                     }
                     __syncwarp();
                 }
                 gc += (nk + CH - 1) / CH;
             }
-        } else {
+        } else if (!H3) {
             // ------------------------- a_lo transform (X3) / in-place rn_tf32 (X1)
             constexpr int NTT = 32 * CF::NTRANSFORM;
             const int tid = (warp < 4 ? warp - 2 : warp - (4 + CF::NDRAIN) + 2) * 32 + lane;  // 0..NTT-1
@@ -576,9 +633,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                 }
                 if (tile >= sc.total) break;
                 const int s = gi % STAGES;
-                const int lr = X3 ? gi % LO_SLOTS : s;
+                const int lr = (X3 && !H3) ? gi % (LO_SLOTS > 0 ? LO_SLOTS : 1) : s;
                 mbar_wait(&full[s], (uint32_t)(gi / STAGES) & 1u);
-                if (X3) mbar_wait(&lo_empty[lr], ((uint32_t)(gi / LO_SLOTS) & 1u) ^ 1u);
+                if (X3) mbar_wait(&lo_empty[lr], ((uint32_t)(gi / (LO_SLOTS > 0 ? LO_SLOTS : 1)) & 1u) ^ 1u);
                 const uint32_t src = smem_u32(a_raw(s)), dst = X3 ? smem_u32(a_lo(lr)) : src;
                 if ((dbg & 1) || (!X3 && sc.a_rn)) {  // pre-rounded A (or the experiment switch)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -650,7 +707,7 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
                      const uint32_t* box, CUtensorMapSwizzle swz,
                      CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
     CUtensorMap m;
-    uint32_t es[3] = {1, 1, 1};
+    uint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = encode_fn()(&m, dt, rank, const_cast<void*>(base), dims, strides_bytes,
                              box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -661,8 +718,9 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 // Persistent launch: one CTA per SM (or fewer when there are fewer tiles).
 template <bool A_MN, int EPI, int NT, bool X3, bool H = false>
 void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
-                    int N, double* out, int64_t ldo, double* partial, double alpha, double beta) {
-    using CF = Cfg<NT, X3>;
+                    int N, double* out, int64_t ldo, double* partial, double alpha, double beta,
+                    const CUtensorMap* tal = nullptr, const int* rexp = nullptr, const int* cexp = nullptr) {
+    using CF = Cfg<NT, X3, H>;
     auto kern = k_umma<A_MN, EPI, NT, X3, H>;
     static bool attr = false;
     if (!attr) {
@@ -689,7 +747,8 @@ void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& 
     attr_c[0].val.cooperative = sc.wave_ctr ? 1 : 0;
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
-    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, th, tl, M, N, sc, out, ldo, partial, alpha, beta));
+    CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, th, tl, tal ? *tal : ta, M, N, sc, out, ldo, partial, alpha, beta,
+                                  rexp, cexp));
     LAUNCH_CHECK(c);
 }
 
@@ -717,6 +776,7 @@ Sched make_sched(int m_tiles, int n_tiles, int splits, int k_tiles, int kps, boo
     sc.total = splits * (sym ? n_tiles * (n_tiles + 1) / 2 : m_tiles * n_tiles);
     sc.wave_ctr = nullptr;
     sc.a_rn = 0;
+    sc.pf = g_pf >= 0 ? g_pf : 12;
     return sc;
 }
 
@@ -825,10 +885,16 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint32_t fb = full0 + s * 8;
                     const int k0 = i * BKE;
                     uint8_t* st = smem + s * P2_STAGE;
-                    asm volatile(
-                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(k0),
-                        "r"(m_tile * BM) : "memory");
+                    if (H)  // the interleaved hi/lo copy (4-D map; hi = part 0)
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(0),
+                            "r"(0), "r"(k0 / 64), "r"(m_tile * BM) : "memory");
+                    else
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(k0),
+                            "r"(m_tile * BM) : "memory");
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
                         asm volatile(
@@ -1308,6 +1374,61 @@ void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, 
     LAUNCH_CHECK(c);
 }
 
+
+// ------------------------------------------------ 3×FP16 operands (H3)
+// x (K × N, fp32/fp64, ldx) → fp16 hi + lo (K × N, ld K), column j scaled by 2^q[j] with
+// q[j] = f16 exponent of max_k |x[k,j]·2^−fold[k]| (fold nullable: the per-column exponents of
+// the A operand of A·X, moved onto the rows of X so that A'X' = A·X·2^q exactly).
+// One CTA per column; hi = rn16(x'), lo = rn16(x' − hi) (exact remainder in fp64).
+template <class T, bool IL>
+__global__ void __launch_bounds__(256) k_split_f16(const T* __restrict__ x, int64_t K, int64_t ldx,
+                                                   const int* __restrict__ fold, uint16_t* __restrict__ hi,
+                                                   uint16_t* __restrict__ lo, int* __restrict__ q) {
+    const int64_t j = blockIdx.x;
+    const T* col = x + j * ldx;
+    double mx = 0.0;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+        const double v = fabs((double)col[k]) * (fold ? exp2_int(-fold[k]) : 1.0);
+        mx = v > mx ? v : mx;
+    }
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+    int e = 0;
+    if (mx > 0.0 && isfinite(mx)) frexp(mx, &e);
+    const int qj = mx > 0.0 && isfinite(mx) ? 15 - e : 0;  // max·2^q < 2^15
+    if (threadIdx.x == 0) q[j] = qj;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+        const double v = (double)col[k] * exp2_int(qj - (fold ? fold[k] : 0));
+        const __half h = __double2half(v);
+        const __half l = __double2half(v - (double)__half2float(h));
+        // IL: the A-operand layout (block_sumsq's): per 64-row chunk [hi 64 | lo 64], 2K per column
+        const int64_t ih = IL ? j * 2 * K + (k >> 6) * 128 + (k & 63) : j * K + k;
+        hi[ih] = *reinterpret_cast<const uint16_t*>(&h);
+        (IL ? hi : lo)[IL ? ih + 64 : ih] = *reinterpret_cast<const uint16_t*>(&l);
+    }
+}
+
+// 3×FP16 tile counts: split K until the persistent waves are nearly full (a 3.46-wave pass
+// idles 14% of the SMs in its last wave); partials are fp64, so fewer is cheaper.
+int h3_splits(int tiles, int k_tiles, int sms) {
+    int best = 1;
+    double best_eff = 0.0;
+    for (int s = 1; s <= 8 && (s == 1 || k_tiles / s >= 16); ++s) {
+        const int64_t t = (int64_t)tiles * s;
+        const double eff = (double)t / ((double)sms * (double)((t + sms - 1) / sms));
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = s;
+        }
+        if (eff >= 0.95) break;
+    }
+    return best;
+}
 }  // namespace
 
 namespace ops {
@@ -1323,6 +1444,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         g_no_pair = np_ && np_[0] == '1';
         const char* nx = getenv("BCUR_UMMA_X3_PAIR");
         g_no_x3pair = !(nx && nx[0] == '1');
+        const char* pf = getenv("BCUR_UMMA_PF");
+        if (pf) g_pf = atoi(pf);
         const char* d = getenv("BCUR_UMMA_DEBUG");
         if (d) {
             const int f = atoi(d);
@@ -1426,14 +1549,14 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
 }
 
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
-                       const void* X, int dtx, int64_t ldx, double* rowsq) {
+                       const void* X, int dtx, int64_t ldx, double* rowsq, bool interleaved) {
     if (M <= 0) return;
     if (N <= 0 || K <= 0) {
         CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
         return;
     }
-    if (K % 8 != 0 || lda % 8 != 0 || ((uintptr_t)A16 % 16) != 0)
-        fail(BCUR_E_INVALID_ARGUMENT, "gemm_rowsumsq_f16: K and lda must be multiples of 8, A 16-byte aligned");
+    if (K % 64 != 0 || lda != K || ((uintptr_t)A16 % 16) != 0)
+        fail(BCUR_E_INVALID_ARGUMENT, "gemm_rowsumsq_f16: the fp16 copy needs K % 64 == 0 (lda = K)");
     ProfScope prof(c, "umma_atx_rowsq", 2.0 * M * N * K, 2.0 * K * M + (double)dtype_size(dtx) * K * N + 8.0 * M);
     (void)umma_ok(BCUR_F32, K, lda, A16);  // reads the environment switches once
     // X → fp16 with one power-of-two scale from its max (device-side; no host sync)
@@ -1453,11 +1576,14 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     }
     LAUNCH_CHECK(c);
     constexpr int BKH = bke<true>();
-    const uint64_t dA[2] = {(uint64_t)K, (uint64_t)M}, sA[1] = {(uint64_t)lda * 2};
-    const uint32_t bA[2] = {BKH, BM};
+    // hi of the copy as (64 rows, hi|lo, K/64 chunks, M columns), box = one chunk × 128 columns;
+    // the compact copy is the same map with one part per chunk
+    const uint64_t dA[4] = {64, interleaved ? 2u : 1u, (uint64_t)(K / 64), (uint64_t)M};
+    const uint64_t sA[3] = {128, interleaved ? 256u : 128u, (uint64_t)K * (interleaved ? 4 : 2)};
+    const uint32_t bA[4] = {64, 1, 1, BM};
     const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
     const uint32_t bX[2] = {BKH, BN};
-    CUtensorMap ta = make_map(A16, 2, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap ta = make_map(A16, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     CUtensorMap tx = make_map(x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     const int k_tiles = (int)((K + BKH - 1) / BKH);
     const int mt = (int)((M + BM - 1) / BM);
@@ -1556,5 +1682,133 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
     LAUNCH_CHECK(c);
 }
 
+
+// ---- 3×FP16 (H3) products -------------------------------------------------
+void split_f16(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, const int* fold, SplitF16* out) {
+    out->K = K;
+    out->N = N;
+    out->hi = DevBuf(c, (size_t)std::max<int64_t>(K * N, 1) * 2);
+    out->lo = DevBuf(c, (size_t)std::max<int64_t>(K * N, 1) * 2);
+    out->exps = DevBuf(c, (size_t)std::max<int64_t>(N, 1) * sizeof(int));
+    if (K <= 0 || N <= 0) return;
+    ProfScope prof(c, "split_f16", 0.0, (double)K * N * (dtype_size(dtx) + 4));
+    if (dtx == BCUR_F32)
+        k_split_f16<float, false><<<(unsigned)N, 256, 0, c->stream>>>((const float*)x, K, ldx, fold,
+                                                                     out->hi.as<uint16_t>(), out->lo.as<uint16_t>(),
+                                                                     out->exps.as<int>());
+    else
+        k_split_f16<double, false><<<(unsigned)N, 256, 0, c->stream>>>((const double*)x, K, ldx, fold,
+                                                                      out->hi.as<uint16_t>(), out->lo.as<uint16_t>(),
+                                                                      out->exps.as<int>());
+    LAUNCH_CHECK(c);
+}
+
+void split_il_into(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t lda, uint16_t* il, int* exps) {
+    if (m % 64 != 0) fail(BCUR_E_INVALID_ARGUMENT, "split_il: needs m % 64 == 0");
+    if (m <= 0 || n <= 0) return;
+    ProfScope prof(c, "split_f16", 0.0, (double)m * n * (dtype_size(dta) + 4));
+    if (dta == BCUR_F32)
+        k_split_f16<float, true><<<(unsigned)n, 256, 0, c->stream>>>((const float*)a, m, lda, nullptr, il, nullptr,
+                                                                    exps);
+    else
+        k_split_f16<double, true><<<(unsigned)n, 256, 0, c->stream>>>((const double*)a, m, lda, nullptr, il, nullptr,
+                                                                     exps);
+    LAUNCH_CHECK(c);
+}
+
+void split_il(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t lda, DevBuf* il, DevBuf* exps) {
+    *il = DevBuf(c, (size_t)std::max<int64_t>(m * n, 1) * 4);
+    *exps = DevBuf(c, (size_t)std::max<int64_t>(n, 1) * sizeof(int));
+    split_il_into(c, a, dta, m, n, lda, il->as<uint16_t>(), exps->as<int>());
+}
+
+// A split on the fly (interleaved) and X split per column; the Gram form splits A once more as
+// its own K-major X operand.
+void gemm_h3(Ctx* c, bool a_mn, const void* A, int dta, int64_t m, int64_t n, int64_t lda, const void* X, int dtx,
+             int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags) {
+    DevBuf il, ea;
+    split_il(c, A, dta, m, n, lda, &il, &ea);
+    if ((flags & GEMM_SYM_UPPER) && !a_mn) {
+        SplitF16 xs;
+        split_f16(c, A, dta, m, n, lda, nullptr, &xs);
+        umma_h3(c, false, il.as<uint16_t>(), ea.as<int>(), m, n, view(xs), alpha, beta, out, ldo, flags);
+        return;
+    }
+    umma_h3(c, a_mn, il.as<uint16_t>(), ea.as<int>(), m, n, X, dtx, N, ldx, alpha, beta, out, ldo, flags);
+}
+
+bool h3_ok(int64_t m) {
+    (void)umma_ok(BCUR_F32, 32, 8, nullptr);  // reads the environment switches once
+    static int enabled = -1;
+    if (enabled < 0) {
+        const char* e = getenv("BCUR_DISABLE_H3");
+        enabled = (e && e[0] == '1') ? 0 : 1;
+    }
+    return enabled && m > 0 && m % 64 == 0 && m < (1LL << 30);
+}
+
+void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const F16View& X,
+             double alpha, double beta, double* out, int64_t ldo, int flags) {
+    const bool sym_req = (flags & GEMM_SYM_UPPER) != 0, tri = (flags & GEMM_B_UPPER) != 0 && a_mn;
+    const int64_t M = a_mn ? m : n, K = a_mn ? n : m, N = X.N;
+    if (M <= 0 || N <= 0) return;
+    if (X.K != K) fail(BCUR_E_DIMENSION_MISMATCH, "umma_h3: X rows do not match the contraction");
+    if (!h3_ok(m)) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: needs m % 64 == 0");
+    const int NT = N > BN ? 2 : 1;
+    const bool sym = sym_req && !a_mn && NT == 2 && M == N;
+    ProfScope prof(c, a_mn ? "umma_ax_h3" : "umma_atx_h3", ((sym || tri) ? 1.0 : 2.0) * M * N * K,
+                   4.0 * m * n + 4.0 * K * N + 8.0 * M * N);
+    constexpr int BKH = bke<true>();
+    // the interleaved copy: element (row r, column j, part hl) at j·2m + (r/64)·128 + hl·64 + r%64
+    // 4-D view (64 rows, hi|lo, m/64 row chunks, n columns).  AᵀX (K = rows): box = one chunk ×
+    // 128 columns.  A·X (K = columns): box = one chunk × 64 columns, loaded twice per stage
+    // (the tile's two 64-row MN atoms).
+    const uint64_t dA[4] = {64, 2, (uint64_t)(m / 64), (uint64_t)n};
+    const uint64_t sA[3] = {128, 256, (uint64_t)m * 4};
+    const uint32_t bA[4] = {64, 1, 1, a_mn ? (uint32_t)BKH : (uint32_t)BM};
+    CUtensorMap ta = make_map(AL, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
+    const uint32_t bX[2] = {BKH, BN};
+    CUtensorMap th = make_map(X.hi, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap tl = make_map(X.lo, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    const int k_tiles = (int)((K + BKH - 1) / BKH);
+    const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
+    const int tiles = sym ? nt * (nt + 1) / 2 : mt * nt;
+    int splits = h3_splits(tiles, k_tiles, c->sm_count);
+    const int kps = (k_tiles + splits - 1) / splits;
+    splits = (k_tiles + kps - 1) / kps;
+    Sched sc = make_sched(mt, nt, splits, k_tiles, kps, sym, tri);
+    // No L2 prefetch: with the stage ring alone the 3×FP16 passes stream at 5.7-6.2 TB/s; 12
+    // stages of prefetch (57 MB of A in flight) dropped them to ~4 TB/s (L2 thrash)
+    sc.pf = g_pf >= 0 ? g_pf : 0;
+    const int* rexp = a_mn ? nullptr : ea;
+    const int* cexp = X.exps;
+    auto launch = [&](double* o, int64_t ldo_, double* prt, double al, double be) {
+        if (a_mn) {
+            if (NT == 2) launch_umma_nt<true, EPI_STORE, 2, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, prt, al, be, nullptr, rexp, cexp);
+            else launch_umma_nt<true, EPI_STORE, 1, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, prt, al, be, nullptr, rexp, cexp);
+        } else {
+            if (NT == 2) launch_umma_nt<false, EPI_STORE, 2, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, prt, al, be, nullptr, rexp, cexp);
+            else launch_umma_nt<false, EPI_STORE, 1, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, prt, al, be, nullptr, rexp, cexp);
+        }
+    };
+    if (splits == 1) {
+        launch(out, ldo, nullptr, alpha, beta);
+        return;
+    }
+    DevBuf part(c, (size_t)splits * M * N * sizeof(double));
+    if (sym || tri) CUDA_CHECK(cudaMemsetAsync(part.ptr, 0, part.bytes, c->stream));  // skipped tiles / k ranges
+    launch(nullptr, 0, part.as<double>(), 1.0, 0.0);
+    k_reduce_splits<<<(unsigned)((M * N + 255) / 256), 256, 0, c->stream>>>(M, N, splits, part.as<double>(), out, ldo,
+                                                                            alpha, beta);
+    LAUNCH_CHECK(c);
+}
+
+void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,
+             int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags) {
+    SplitF16 xs;
+    split_f16(c, X, dtx, a_mn ? n : m, N, ldx, a_mn ? ea : nullptr, &xs);
+    umma_h3(c, a_mn, AL, ea, m, n, view(xs), alpha, beta, out, ldo, flags);
+}
 }  // namespace ops
 }  // namespace bcur_b200

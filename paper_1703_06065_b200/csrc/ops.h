@@ -13,10 +13,12 @@ enum Op { OP_N = 0, OP_T = 1 };
 // out[g] = Σ_{j∈block g} Σ_i a(i,j)²  (fp64; offsets are device, relative to a's first column)
 // shadow (nullable, fp32 A only): also write the TF32-rounded copy of A (ld lds)
 // Optional copies written in the same pass (fp32 A): `shadow` = TF32-rounded fp32, or
-// `sh16` = fp16 scaled per column by 2^colexp[j] (exact; see gemm_rowsumsq_f16)
+// `sh16` = fp16 scaled per column by 2^colexp[j] (exact; see gemm_rowsumsq_f16), and with
+// it optionally `sl16` = hi and the fp16 remainder lo interleaved per 64-row chunk, 2m halves
+// per column (m % 64 == 0): the A operand of the 3×FP16 products
 void block_sumsq(Ctx* c, const void* a, int dt, int64_t m, int64_t ld, const int64_t* d_offsets, int64_t G,
                  double* d_out, float* shadow = nullptr, int64_t lds = 0, uint16_t* sh16 = nullptr,
-                 int* colexp = nullptr);
+                 int* colexp = nullptr, uint16_t* sl16 = nullptr);
 // out[j] = Σ_c v(j,c)²   then segmented into blocks: out_blocks[g]
 void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64_t ld, const int64_t* d_offsets,
                       int64_t G, double* d_rows /*nullable*/, double* d_blocks);
@@ -46,8 +48,9 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 // from its max; the tensor cores run kind::f16 (same 11-bit significand as the
 // round-to-nearest 1×TF32 pass, twice the MMA rate, half the bytes) and the scales are
 // removed exactly in fp64.
+// interleaved: A16 is the [hi 64 | lo 64]-per-chunk copy (only hi is read), else compact hi.
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
-                       const void* B, int dtb, int64_t ldb, double* rowsq);
+                       const void* B, int dtb, int64_t ldb, double* rowsq, bool interleaved = true);
 // out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
@@ -71,6 +74,41 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
 void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const void* X, int dtx, int64_t N,
              int64_t ldx, double alpha, double beta, double* out, int64_t ldo, bool x_upper_tri = false,
              bool x1 = false);
+
+// ---- 3×FP16 products (kernels_umma.cu, H3) --------------------------------
+// An fp16 hi + lo split of a K × N operand (ld K), column j scaled by 2^exps[j] (exact).
+struct SplitF16 {
+    DevBuf hi, lo, exps;
+    int64_t K = 0, N = 0;
+};
+// A non-owning view of one (e.g. block_sumsq's split of A, or a SplitF16)
+struct F16View {
+    const uint16_t* hi;
+    const uint16_t* lo;
+    const int* exps;
+    int64_t K, N;
+};
+inline F16View view(const SplitF16& s) { return {s.hi.as<uint16_t>(), s.lo.as<uint16_t>(), s.exps.as<int>(), s.K, s.N}; }
+// fold (nullable, K ints): exponents subtracted from row k first (A·X with a scaled A)
+void split_f16(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, const int* fold, SplitF16* out);
+// A (m × n, fp32/fp64, lda) → the interleaved hi/lo A operand (2m halves per column; m % 64 == 0)
+// with per-column exponents
+void split_il(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t lda, DevBuf* il, DevBuf* exps);
+void split_il_into(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t lda, uint16_t* il, int* exps);
+// umma_h3 on operands split here (a_mn: A·X, else AᵀX; GEMM_SYM_UPPER: AᵀA with X == A)
+void gemm_h3(Ctx* c, bool a_mn, const void* A, int dta, int64_t m, int64_t n, int64_t lda, const void* X, int dtx,
+             int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags = 0);
+// A (m × n) given as block_sumsq's interleaved fp16 hi/lo copy AL (2m halves per column) with
+// column exponents ea; needs m % 64 == 0.
+bool h3_ok(int64_t m);
+// a_mn: Out(m×N) = alpha·A·X + beta·Out (X: n × N); else Out(n×N) = alpha·AᵀX + beta·Out (X: m × N).
+// flags: GEMM_SYM_UPPER (AᵀA with X the split of A itself: upper tiles only), GEMM_B_UPPER (A·X, X upper).
+// Every product is hi·hi + hi·lo + lo·hi on kind::f16 tensor cores (fp32 accumulate, drained to
+// compensated fp32 every 8 MMAs), scales removed exactly in the fp64 epilogue.
+void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const F16View& X,
+             double alpha, double beta, double* out, int64_t ldo, int flags = 0);
+void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,
+             int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags = 0);
 
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
 // R upper (ld ldr, may alias g) with G = RᵀR, only g's upper triangle is read; info[0] = 0 ok / j+1 failed pivot;

@@ -339,6 +339,15 @@ struct Basis {
         CUDA_CHECK(cudaMemsetAsync(buf.ptr, 0, buf.bytes, c->stream));
     }
     void* col(int64_t j) const { return (char*)buf.ptr + (size_t)j * rows * dtype_size(dt); }
+    // optional 3×FP16 form of the fp32 basis (the interleaved hi/lo A operand, kept in step
+    // with every append): the greedy CGS2 products run on it (kernels_umma.cu, H3)
+    DevBuf il, iexps;
+    bool h3() const { return il.ptr != nullptr; }
+    void enable_h3(Ctx* c) {
+        if (dt != BCUR_F32 || !h3_ok(rows)) return;
+        il = DevBuf(c, (size_t)rows * cap * 4);
+        iexps = DevBuf(c, (size_t)cap * sizeof(int));
+    }
 };
 
 // Block CGS2 of panel P (rows × w, fp64, overwritten) against the basis; the new
@@ -348,9 +357,17 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
     if (cur > 0) {
         Mat64 X(c, cur, w);
         for (int pass = 0; pass < 2; ++pass) {
-            gemm(c, OP_T, OP_N, cur, w, rows, 1.0, B->buf.ptr, B->dt, rows, P, BCUR_F64, ldp, 0.0, X.p(), X.ld);
+            if (B->h3())
+                umma_h3(c, false, B->il.as<uint16_t>(), B->iexps.as<int>(), rows, cur, P, BCUR_F64, w, ldp, 1.0, 0.0,
+                        X.p(), X.ld);
+            else
+                gemm(c, OP_T, OP_N, cur, w, rows, 1.0, B->buf.ptr, B->dt, rows, P, BCUR_F64, ldp, 0.0, X.p(), X.ld);
             if (dist) allreduce(c, X.p(), cur * w);
-            gemm(c, OP_N, OP_N, rows, w, cur, -1.0, B->buf.ptr, B->dt, rows, X.p(), BCUR_F64, X.ld, 1.0, P, ldp);
+            if (B->h3())
+                umma_h3(c, true, B->il.as<uint16_t>(), B->iexps.as<int>(), rows, cur, X.p(), BCUR_F64, w, X.ld, -1.0,
+                        1.0, P, ldp);
+            else
+                gemm(c, OP_N, OP_N, rows, w, cur, -1.0, B->buf.ptr, B->dt, rows, X.p(), BCUR_F64, X.ld, 1.0, P, ldp);
         }
     }
     int64_t r;
@@ -360,6 +377,9 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
         Mat64 Qn(c, rows, w);
         r = orth(c, P, rows, w, ldp, ref, dt, Qn.p(), Qn.ld, dist, nullptr, nullptr);
         convert(c, Qn.p(), BCUR_F64, rows, r, Qn.ld, B->col(cur), B->dt, rows);
+        if (B->h3() && r > 0)
+            split_il_into(c, B->col(cur), B->dt, rows, r, rows, B->il.as<uint16_t>() + (size_t)cur * 2 * rows,
+                          B->iexps.as<int>() + cur);
     }
     B->rank += r;
     return r;
@@ -424,7 +444,23 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
 }
 
 // ---------------------------------------------------------- range finder
-void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out) {
+// A·X (trans = false) or AᵀX of the range finder: 3×FP16 from the norms pass's split of A
+// when present, else the fp32 A path (3×TF32 on the tensor cores / fp64)
+static void a_product(Ctx* c, const DMat* a, const RoundedA* ra, bool trans, int64_t N, const void* X, int dtx,
+                      int64_t ldx, double* out, int64_t ldo) {
+    if (ra && ra->has_lo()) {
+        umma_h3(c, !trans, ra->il.as<uint16_t>(), ra->exps.as<int>(), a->m, a->n, X, dtx, N, ldx, 1.0, 0.0, out,
+                ldo);
+        return;
+    }
+    if (trans)
+        gemm(c, OP_T, OP_N, a->n, N, a->m, 1.0, a->ptr, a->dtype, a->ld, X, dtx, ldx, 0.0, out, ldo);
+    else
+        gemm(c, OP_N, OP_N, a->m, N, a->n, 1.0, a->ptr, a->dtype, a->ld, X, dtx, ldx, 0.0, out, ldo);
+}
+
+void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
+                  const RoundedA* ra) {
     const int64_t m = a->m, nl = a->n;
     const int64_t ng = a->n_global > 0 ? a->n_global : a->n;
     if (k < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: k must be >= 1");
@@ -433,7 +469,7 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
     const int dt = a->dtype;
     Mat64 Om(c, nl, l), Y(c, m, l);
     omega(c, key, nl, a->col0, l, Om.p(), Om.ld);
-    gemm(c, OP_N, OP_N, m, l, nl, 1.0, a->ptr, dt, a->ld, Om.p(), BCUR_F64, Om.ld, 0.0, Y.p(), Y.ld);
+    a_product(c, a, ra, false, l, Om.p(), BCUR_F64, Om.ld, Y.p(), Y.ld);
     allreduce(c, Y.p(), m * l);
     Mat64 Qy(c, m, l);
     int64_t r = l;
@@ -441,17 +477,17 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
         r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
         if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
         Mat64 Z(c, nl, r), Qz(c, nl, r);
-        gemm(c, OP_T, OP_N, nl, r, m, 1.0, a->ptr, dt, a->ld, Qy.p(), BCUR_F64, Qy.ld, 0.0, Z.p(), Z.ld);
+        a_product(c, a, ra, true, r, Qy.p(), BCUR_F64, Qy.ld, Z.p(), Z.ld);
         r = orth(c, Z.p(), nl, r, Z.ld, -1.0, dt, Qz.p(), Qz.ld, true, nullptr, nullptr);
         if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
-        gemm(c, OP_N, OP_N, m, r, nl, 1.0, a->ptr, dt, a->ld, Qz.p(), BCUR_F64, Qz.ld, 0.0, Y.p(), Y.ld);
+        a_product(c, a, ra, false, r, Qz.p(), BCUR_F64, Qz.ld, Y.p(), Y.ld);
         allreduce(c, Y.p(), m * r);
     }
     r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
     if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
     // Bᵀ = Aᵀ·Q (n_local × r); B·Bᵀ = Σ_ranks Bᵀ_sᵀ Bᵀ_s
     Mat64 Bt(c, nl, r), Gb(c, r, r), lam(c, r, 1), Ut(c, r, r);
-    gemm(c, OP_T, OP_N, nl, r, m, 1.0, a->ptr, dt, a->ld, Qy.p(), BCUR_F64, Qy.ld, 0.0, Bt.p(), Bt.ld);
+    a_product(c, a, ra, true, r, Qy.p(), BCUR_F64, Qy.ld, Bt.p(), Bt.ld);
     gemm(c, OP_T, OP_N, r, r, nl, 1.0, Bt.p(), BCUR_F64, Bt.ld, Bt.p(), BCUR_F64, Bt.ld, 0.0, Gb.p(), Gb.ld);
     allreduce(c, Gb.p(), r * r);
     sym_eig(c, Gb.p(), r, Gb.ld, lam.p(), Ut.p());
@@ -543,34 +579,35 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
     }
 }
 
-// TF32-rounded copy of an fp32 A (ld m), written by the norms pass: the X1 row-Σ² passes
-// (residual, greedy scores) read it and skip their in-kernel rounding (shared-memory
-// bound).  Empty when A is fp64 or the copy does not fit in device memory.
-// block_sumsq's fp16 copy of an fp32 A for the row-Σ² passes: column j scaled by
-// 2^exps[j] (exact), rounded to nearest — the same 11-bit significands a round-to-nearest
-// TF32 copy holds, in half the bytes, for kind::f16 MMAs (twice the TF32 rate).
-struct RoundedA {
-    DevBuf buf, exps;
-};
-static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra) {
-    if (a->dtype != BCUR_F32 || a->m % 32 != 0 || a->m <= 0 || a->n <= 0 || !umma_ok(a->dtype, a->m, a->ld, a->ptr))
-        return;
-    const size_t need = (size_t)a->m * (size_t)a->n * 2;
+// block_sumsq's fp16 copy of an fp32 A (RoundedA, pipeline.h).  with_lo: the interleaved
+// hi/lo form (range finder on 3×FP16) when it fits, else the compact hi copy.
+static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra, bool with_lo) {
+    if (a->dtype != BCUR_F32 || !h3_ok(a->m) || a->n <= 0 || !umma_ok(a->dtype, a->m, a->ld, a->ptr)) return;
+    const size_t one = (size_t)a->m * (size_t)a->n * 2;
     const size_t headroom = (size_t)8 << 30;  // the rest of the pipeline's workspace
-    if (!c->cached(need)) {  // first call for this shape (cudaMemGetInfo is not free: not per step)
+    size_t need = with_lo ? 2 * one : one;
+    // a cached interleaved-size block is reused for the compact copy too (a block_css and a
+    // greedy_select on the same A alternate between the two: re-allocating ~70 GB per call
+    // at c5 cost more than every kernel of the step)
+    size_t alloc = (!with_lo && c->cached(2 * one)) ? 2 * one : need;
+    if (!c->cached(alloc)) {  // first call for this shape (cudaMemGetInfo is not free: not per step)
         size_t freeb = 0, totalb = 0;
         CUDA_CHECK(cudaMemGetInfo(&freeb, &totalb));
-        if (need + headroom > freeb + c->pooled_bytes) return;  // does not fit: in-kernel rounding
-        if (need + headroom > freeb) c->trim();                  // make room from the workspace cache
+        if (need + headroom > freeb + c->pooled_bytes) need = one;  // no room for lo
+        if (need + headroom > freeb + c->pooled_bytes) return;      // does not fit: fp32 A paths
+        if (need + headroom > freeb) c->trim();                      // make room from the workspace cache
+        alloc = need;
     }
-    ra->buf = DevBuf(c, need);
+    ra->il = DevBuf(c, alloc);
+    ra->interleaved = need > one;
     ra->exps = DevBuf(c, (size_t)a->n * sizeof(int));
 }
 // rows[j] = Σ_c (AᵀX)_jc² over the shard's columns: from the fp16 copy when present
 static void rowsq_pass(Ctx* c, const DMat* a, const RoundedA* ra, int64_t N, const void* X, int dtx, int64_t ldx,
                        double* rows) {
-    if (ra && ra->buf.ptr)
-        gemm_rowsumsq_f16(c, a->n, N, a->m, ra->buf.as<uint16_t>(), a->m, ra->exps.as<int>(), X, dtx, ldx, rows);
+    if (ra && ra->ok())
+        gemm_rowsumsq_f16(c, a->n, N, a->m, ra->il.as<uint16_t>(), a->m, ra->exps.as<int>(), X, dtx, ldx, rows,
+                          ra->interleaved);
     else
         gemm_rowsumsq(c, OP_T, OP_N, a->n, N, a->m, a->ptr, a->dtype, a->ld, X, dtx, ldx, rows);
 }
@@ -610,13 +647,14 @@ static double explicit_residual(Ctx* c, const DMat* a, const Basis& B) {
 
 // global per-block ‖A_g‖² (host copy) and ‖A‖²
 static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global,
-                          RoundedA* ra = nullptr) {
+                          RoundedA* ra = nullptr, bool with_lo = true) {
     Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     *d_global = Mat64(c, s.G, 1);
-    if (ra) make_rounded(c, a, ra);
-    const bool f16 = ra && ra->buf.ptr;
+    if (ra) make_rounded(c, a, ra, with_lo);
+    const bool f16 = ra && ra->ok();
     block_sumsq(c, a->ptr, a->dtype, a->m, a->ld, s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p(), nullptr, a->m,
-                f16 ? ra->buf.as<uint16_t>() : nullptr, f16 ? ra->exps.as<int>() : nullptr);
+                f16 && !ra->interleaved ? ra->il.as<uint16_t>() : nullptr, f16 ? ra->exps.as<int>() : nullptr,
+                f16 && ra->interleaved ? ra->il.as<uint16_t>() : nullptr);
     gather_blocks_vec(c, s, loc.p(), d_global->p());
     bn2->assign(s.G, 0.0);
     d2h(c, bn2->data(), d_global->p(), s.G);
@@ -668,7 +706,7 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
     ph.reset(new ProfScope(c, "phase:2 range_finder", 0, 0));
     Subspace sub;
-    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, &ra);
     ph.reset(new ProfScope(c, "phase:3 scores+draw", 0, 0));
     Mat64 sc(c, G, 1);
     block_scores(c, s, sub.v, a->n, sc.p());
@@ -706,7 +744,8 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     std::vector<double> bn2;
     Mat64 res;
     RoundedA ra;
-    const double a2 = block_norms(c, a, s, &bn2, &res, &ra);  // res starts as ‖A_g‖²
+    // res starts as ‖A_g‖²; the greedy scores need only hi (compact copy: half the bytes per pass)
+    const double a2 = block_norms(c, a, s, &bn2, &res, &ra, false);
     if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "greedy_select: matrix contains NaN or Inf");  // require_finite
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "greedy_select: A is identically zero");
     const int dt = a->dtype;
@@ -720,6 +759,7 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     }
     Basis B;
     B.init(c, dt == BCUR_F32 ? BCUR_F32 : BCUR_F64, m, cap);
+    B.enable_h3(c);
     DevBuf sel(c, (size_t)G);
     CUDA_CHECK(cudaMemsetAsync(sel.ptr, 0, G, c->stream));
     DevBuf didx(c, 64);
@@ -801,11 +841,12 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     Shard s = shard_of(a, coff, Gc);
     std::vector<double> bn2;
     Mat64 dbn;
-    const double a2 = block_norms(c, a, s, &bn2, &dbn);
+    RoundedA ra;
+    const double a2 = block_norms(c, a, s, &bn2, &dbn, &ra);
     if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: matrix contains NaN or Inf");  // require_finite
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_cur: A is identically zero");
     Subspace sub;
-    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, &ra);
     Mat64 csc(c, Gc, 1), rsc(c, Gr, 1);
     block_scores(c, s, sub.v, nl, csc.p());
     DevBuf droff(c, (Gr + 1) * sizeof(int64_t));
@@ -875,7 +916,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     // M = Q_Cᵀ A Q_R:  Xᵀ = A_sᵀ Q_C (n_local × rc), Mᵀ = Σ_s Q_R,sᵀ Xᵀ (rr × rc)
     Mat64 Xt(c, nl, std::max<int64_t>(rc, 1)), Mt(c, std::max<int64_t>(rr, 1), std::max<int64_t>(rc, 1));
     Mat64 M(c, std::max<int64_t>(rc, 1), std::max<int64_t>(rr, 1));
-    gemm(c, OP_T, OP_N, nl, rc, m, 1.0, a->ptr, dt, a->ld, QC.buf.ptr, QC.dt, QC.rows, 0.0, Xt.p(), Xt.ld);
+    a_product(c, a, &ra, true, rc, QC.buf.ptr, QC.dt, QC.rows, Xt.p(), Xt.ld);
     gemm(c, OP_T, OP_N, rr, rc, nl, 1.0, QR.buf.ptr, QR.dt, QR.rows, Xt.p(), BCUR_F64, Xt.ld, 0.0, Mt.p(), Mt.ld);
     allreduce(c, Mt.p(), rr * rc);
     transpose(c, Mt.p(), BCUR_F64, rr, rc, Mt.ld, M.p(), BCUR_F64, M.ld);

@@ -53,11 +53,25 @@ struct CurOut {
     bcur_report rep{};
 };
 
+// fp16 copy of an fp32 A written by the norms pass (block_sumsq): column j scaled by 2^exps[j]
+// (exact), hi = rn16(a·2^e) — the row-Σ² passes' operand (kind::f16, the same 11-bit
+// significands as a round-to-nearest TF32 copy) — either alone (compact: m halves per column)
+// or interleaved per 64-row chunk with lo = rn16(a·2^e − hi) ([hi 64 | lo 64], 2m halves per
+// column): hi + lo is the A operand of the 3×FP16 range-finder products.  Empty when A is fp64,
+// m % 64 != 0, or it does not fit.
+struct RoundedA {
+    DevBuf il, exps;
+    bool interleaved = false;
+    bool ok() const { return il.ptr != nullptr; }
+    bool has_lo() const { return ok() && interleaved; }
+};
+
 Shard shard_of(const DMat* a, const int64_t* offsets, int64_t G);
 void allreduce(Ctx* c, double* d, int64_t count);
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
              int64_t ldq, bool dist, Mat64* T_out, int* path_out);
-void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out);
+void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
+                  const RoundedA* ra = nullptr);
 void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, const double* uniforms,
                CssOut* out);
 void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, GreedyOut* out);

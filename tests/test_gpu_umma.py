@@ -112,3 +112,53 @@ def test_rowsq_f16(B, m, n, N):
     # unbiased: the per-row errors average out (column scales span 2^±40, so the plain
     # total would be one column's error)
     assert abs(rel.mean()) < 3e-6 + 4 * rel.std() / np.sqrt(n)
+
+
+# ---- 3×FP16 (fp16 hi + lo split with exact power-of-two column scales) --------------
+@pytest.mark.parametrize("m,n,N", [(512, 1024, 60), (1024, 768, 110), (256, 4096, 220), (2048, 512, 256),
+                                   (128, 1000, 17), (64, 200, 64), (4096, 2048, 60)])
+def test_h3_ax_and_atx(B, m, n, N):
+    gen = np.random.default_rng(7 * m + n + N)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    a64 = a.astype(np.float64)
+    x = np.asfortranarray(gen.standard_normal((n, N)))
+    assert rel_fro(B.structured_product(a, x, h3=True), a64 @ x) < 2e-6
+    q = np.asfortranarray(gen.standard_normal((m, N)))
+    assert rel_fro(B.structured_product(a, q, transpose=True, h3=True), a64.T @ q) < 2e-6
+
+
+def test_h3_scales_and_low_bits(B):
+    """Columns of A spanning 2^±20 and rows of X spanning 2^±12 (the exact per-column
+    scales must keep every column's own precision), with information below the fp16
+    significand (1 + k·2⁻²³)."""
+    gen = np.random.default_rng(3)
+    m, n, N = 256, 640, 64
+    base = np.float32(1.0) + gen.integers(0, 1 << 13, size=(m, n)).astype(np.float32) * np.float32(2.0 ** -23)
+    a = base * np.sign(gen.standard_normal((m, n))).astype(np.float32)
+    a = np.asfortranarray(a * np.float32(2.0) ** gen.integers(-20, 21, size=n).astype(np.float32))
+    a64 = a.astype(np.float64)
+    x = np.asfortranarray(gen.standard_normal((n, N)) * 2.0 ** gen.integers(-12, 13, size=(n, 1)))
+    ref = a64 @ x
+    got = B.structured_product(a, x, h3=True)
+    # every output column is dominated by its largest terms: compare per element against
+    # the exact sum of |terms| (the conditioning-free bound)
+    bound = np.abs(a64) @ np.abs(x)
+    assert np.max(np.abs(got - ref) / bound) < 1e-6
+    q = np.asfortranarray(gen.standard_normal((m, N)))
+    got_t = B.structured_product(a, q, transpose=True, h3=True)
+    bound_t = np.abs(a64).T @ np.abs(q)
+    assert np.max(np.abs(got_t - a64.T @ q) / bound_t) < 1e-6
+
+
+@pytest.mark.parametrize("m,n", [(1024, 384), (512, 200)])
+def test_h3_gram_and_triangular(B, m, n):
+    gen = np.random.default_rng(m + n)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    a64 = a.astype(np.float64)
+    g = B.structured_product(a, gram=True, h3=True)
+    iu = np.triu_indices(n)
+    ref = a64.T @ a64
+    assert rel_fro(g[iu], ref[iu]) < 2e-6
+    r = np.triu(gen.standard_normal((n, n)))
+    got = B.structured_product(a, r, x_upper=True, h3=True)
+    assert rel_fro(got, a64 @ r) < 2e-6
