@@ -180,6 +180,8 @@ bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
         cudaStreamDestroy(ctx->side);
+        cudaStreamSynchronize(ctx->side2);
+        cudaStreamDestroy(ctx->side2);
         for (auto e : ctx->side_ev) cudaEventDestroy(e);
     }
     delete ctx;

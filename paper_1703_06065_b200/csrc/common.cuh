@@ -131,14 +131,21 @@ struct Ctx {
     // Second stream for overlapped work (the blocked Cholesky's look-ahead).  Work on it is
     // forked from `stream` and joined back into it before any buffer it touches is released,
     // so the workspace cache's stream-order reuse rule still holds.
-    cudaStream_t side = nullptr;
-    cudaEvent_t side_ev[2] = {nullptr, nullptr};
+    // A third stream (side2) carries work nothing on the chain waits for until the end (the
+    // blocked inverse assembled alongside the factorization).
+    cudaStream_t side = nullptr, side2 = nullptr;
+    cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
     cudaStream_t side_stream() {
         if (!side) {
             CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+            CUDA_CHECK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
             for (auto& e : side_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         return side;
+    }
+    cudaStream_t side_stream2() {
+        side_stream();
+        return side2;
     }
     // make `to` wait for everything enqueued so far on `from`
     void order(cudaStream_t from, cudaStream_t to, int slot) {

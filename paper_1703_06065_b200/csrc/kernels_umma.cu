@@ -291,6 +291,7 @@ struct Sched {
     unsigned int* wave_ctr;
     int a_rn;  // X1: A already rounded to TF32 (no transform)
     int pf;    // A-tile L2 prefetch distance (stages)
+    int x_il;  // H3: x_hi/x_lo come from one interleaved split (4-D map, part = hi|lo)
 };
 // CTAs that have a tile in waves 0..w
 __device__ __forceinline__ unsigned int wave_arrivals(const Sched& sc, int w) {
@@ -559,8 +560,14 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         else tma_load_2d(a_raw(s), &tmA, &full[s], k0, m_tile * BM);
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
-                            tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, (n_tile * NT + nt) * BN);
-                            if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, (n_tile * NT + nt) * BN);
+                            const int xc = (n_tile * NT + nt) * BN;
+                            if (H3 && sc.x_il) {
+                                tma_load_4d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], 0, 0, k0 / 64, xc);
+                                tma_load_4d(x_lo(s) + nt * X_TILE, &tmXh, &full[s], 0, 1, k0 / 64, xc);
+                            } else {
+                                tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, xc);
+                                if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, xc);
+                            }
                         }
                     }
                     if (sc.wave_ctr) atomicAdd(sc.wave_ctr, 1u);
@@ -777,6 +784,7 @@ Sched make_sched(int m_tiles, int n_tiles, int splits, int k_tiles, int kps, boo
     sc.wave_ctr = nullptr;
     sc.a_rn = 0;
     sc.pf = g_pf >= 0 ? g_pf : 12;
+    sc.x_il = 0;
     return sc;
 }
 
@@ -1722,16 +1730,14 @@ void split_il(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t lda,
     split_il_into(c, a, dta, m, n, lda, il->as<uint16_t>(), exps->as<int>());
 }
 
-// A split on the fly (interleaved) and X split per column; the Gram form splits A once more as
-// its own K-major X operand.
+// A split on the fly (interleaved) and X split per column; the Gram form reads A's split as X too.
 void gemm_h3(Ctx* c, bool a_mn, const void* A, int dta, int64_t m, int64_t n, int64_t lda, const void* X, int dtx,
              int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags) {
     DevBuf il, ea;
     split_il(c, A, dta, m, n, lda, &il, &ea);
-    if ((flags & GEMM_SYM_UPPER) && !a_mn) {
-        SplitF16 xs;
-        split_f16(c, A, dta, m, n, lda, nullptr, &xs);
-        umma_h3(c, false, il.as<uint16_t>(), ea.as<int>(), m, n, view(xs), alpha, beta, out, ldo, flags);
+    if ((flags & GEMM_SYM_UPPER) && !a_mn) {  // X = A: its interleaved split serves both operands
+        const F16View xv{il.as<uint16_t>(), nullptr, ea.as<int>(), m, n};
+        umma_h3(c, false, il.as<uint16_t>(), ea.as<int>(), m, n, xv, alpha, beta, out, ldo, flags);
         return;
     }
     umma_h3(c, a_mn, il.as<uint16_t>(), ea.as<int>(), m, n, X, dtx, N, ldx, alpha, beta, out, ldo, flags);
@@ -1767,10 +1773,19 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     const uint64_t sA[3] = {128, 256, (uint64_t)m * 4};
     const uint32_t bA[4] = {64, 1, 1, a_mn ? (uint32_t)BKH : (uint32_t)BM};
     CUtensorMap ta = make_map(AL, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
-    const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
-    const uint32_t bX[2] = {BKH, BN};
-    CUtensorMap th = make_map(X.hi, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
-    CUtensorMap tl = make_map(X.lo, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap th, tl;
+    if (X.lo) {  // separate hi, lo (K × N each, ld K)
+        const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
+        const uint32_t bX[2] = {BKH, BN};
+        th = make_map(X.hi, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+        tl = make_map(X.lo, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    } else {     // interleaved (split_il layout, K % 64 == 0): one 4-D map, part 0 = hi, 1 = lo
+        if (K % 64 != 0) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: an interleaved X needs K % 64 == 0");
+        const uint64_t dX[4] = {64, 2, (uint64_t)(K / 64), (uint64_t)N}, sX[3] = {128, 256, (uint64_t)K * 4};
+        const uint32_t bX[4] = {64, 1, 1, BN};
+        th = make_map(X.hi, 4, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+        tl = th;
+    }
     const int k_tiles = (int)((K + BKH - 1) / BKH);
     const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
     const int tiles = sym ? nt * (nt + 1) / 2 : mt * nt;
@@ -1781,6 +1796,7 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     // No L2 prefetch: with the stage ring alone the 3×FP16 passes stream at 5.7-6.2 TB/s; 12
     // stages of prefetch (57 MB of A in flight) dropped them to ~4 TB/s (L2 thrash)
     sc.pf = g_pf >= 0 ? g_pf : 0;
+    sc.x_il = X.lo ? 0 : 1;
     const int* rexp = a_mn ? nullptr : ea;
     const int* cexp = X.exps;
     auto launch = [&](double* o, int64_t ldo_, double* prt, double al, double be) {

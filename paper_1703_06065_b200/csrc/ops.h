@@ -81,7 +81,8 @@ struct SplitF16 {
     DevBuf hi, lo, exps;
     int64_t K = 0, N = 0;
 };
-// A non-owning view of one (e.g. block_sumsq's split of A, or a SplitF16)
+// A non-owning view of one (a SplitF16, or — lo == nullptr — an interleaved split_il buffer
+// read as the K-major X operand, K % 64 == 0)
 struct F16View {
     const uint16_t* hi;
     const uint16_t* lo;

@@ -102,12 +102,18 @@ static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X, const dou
 // blocked right-looking (128-wide diagonal blocks + fp64 product updates) beyond.
 // dinv (nullable, 128 × w, ld 128): receives the inverses of the diagonal blocks, which
 // the panel updates need anyway and tri_inv_any can reuse.
-static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* dinv = nullptr) {
+// Rinv (nullable, w × w, ld w): also R⁻¹ (valid when info == 0).  Beyond 144 it is assembled
+// block column by block column alongside the factorization on a third stream —
+// X[:k, k] = −X[:k, :k]·R[:k, k]·R_kk⁻¹ once block row k is final — off the serial chain
+// (a blocked back-substitution afterwards added 32 dependent steps at w = 4096).
+static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* dinv = nullptr,
+                         double* Rinv = nullptr) {
     DevBuf st(c, 64);
     struct { int info; int pad; double mindiag, maxdiag; } hs;
     if (w <= 144) {
         cholesky_upper(c, G, w, ldg, R, w, st.as<int>(), st.as<double>() + 1);
         d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
+        if (Rinv && hs.info == 0) tri_inv_any(c, R, w, Rinv, nullptr);
         return {hs.info, hs.mindiag, hs.maxdiag};
     }
     constexpr int64_t B = 128;
@@ -127,16 +133,37 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     // factorization, inverse and panel product.  Step k+1's own block-row update, which
     // touches rows the side DSYRK also updates, waits for it.  T1 is double-buffered: the
     // side DSYRK of step k reads T1[k&1] while step k+1 writes T1[(k+1)&1].
-    Mat64 Rinv(c, B, B), T1a(c, B, w), T1b(c, B, w);
-    cudaStream_t main_s = c->stream, side_s = c->side_stream();
+    Mat64 Rdi(c, B, B), T1a(c, B, w), T1b(c, B, w), Tx, own_dinv;
+    if (Rinv && !dinv) {  // the inverse's side stream reads every diagonal inverse later
+        own_dinv = Mat64(c, B, w);
+        dinv = own_dinv.p();
+    }
+    cudaStream_t main_s = c->stream, side_s = c->side_stream(), inv_s = c->side_stream2();
     c->order(main_s, side_s, 0);  // the side stream starts after R's initial copy
+    if (Rinv) {
+        Tx = Mat64(c, w, B);
+        c->order(main_s, inv_s, 2);
+        c->stream = inv_s;
+        fill_f64(c, Rinv, w * w, 0.0);
+        c->stream = main_s;
+    }
     int64_t step = 0;
     for (int64_t k = 0; k < w; k += B, ++step) {
         const int64_t kb = std::min(B, w - k), rest = w - k - kb;
         double* Dk = R + k + k * w;
+        double* Ri = dinv ? dinv + k * B : Rdi.p();  // inverse of the diagonal block (ld B)
         cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
-        double* Ri = dinv ? dinv + k * B : Rinv.p();  // inverse of the diagonal block (ld B)
-        if (rest > 0 || dinv) tri_inv_upper(c, Dk, kb, w, Ri, B);
+        if (rest > 0 || dinv || Rinv) tri_inv_upper(c, Dk, kb, w, Ri, B);
+        if (Rinv) {  // block column k of R⁻¹: R[:k, k] is final once block row k−1 was written
+            c->order(main_s, inv_s, 2);
+            c->stream = inv_s;
+            copy_f64(c, Ri, kb, kb, B, Rinv + k + k * w, w);
+            if (k > 0) {
+                gemm(c, OP_N, OP_N, k, kb, k, 1.0, Rinv, BCUR_F64, w, R + k * w, BCUR_F64, w, 0.0, Tx.p(), Tx.ld);
+                gemm(c, OP_N, OP_N, k, kb, kb, -1.0, Tx.p(), BCUR_F64, Tx.ld, Ri, BCUR_F64, B, 0.0, Rinv + k * w, w);
+            }
+            c->stream = main_s;
+        }
         if (rest > 0) {
             double* T1 = (step & 1) ? T1b.p() : T1a.p();
             double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
@@ -159,6 +186,7 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         }
     }
     c->order(side_s, main_s, 1);  // join before any buffer is released
+    if (Rinv) c->order(inv_s, main_s, 3);
     zero_lower(c, R, w, w);
     d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
     out.info = hs.info;
@@ -200,14 +228,13 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w), Dv(c, 128, w);
     gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld);
     if (dist) allreduce(c, G.p(), w * w);
-    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Dv.p());
+    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Dv.p(), Ri.p());
     if (ref < 0) ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     int64_t r = w;
     const bool chol_ok = ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref;
     Mat64 Wr, sig;
     std::vector<double> sig_h;
     if (chol_ok) {
-        tri_inv_any(c, R.p(), w, Ri.p(), Dv.p());
         gemm(c, OP_N, OP_N, rows, w, w, 1.0, X, BCUR_F64, ldx, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld);
     } else {
         // σ_max(X) ≤ ‖X‖_F ≤ sqrt(w·max diag G): below the rank cut every σ is, so the
@@ -255,9 +282,8 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
             copy_f64(c, U.p(), rows, r, U.ld, Q1.p(), Q1.ld);
             Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
             gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
-            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p());
+            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p(), R2i.p());
             if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
-            tri_inv_any(c, R2.p(), r, R2i.p(), Dv.p());
             gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
             if (T_out) {  // T = R2 · (Q1ᵀ X)
                 Mat64 QX(c, r, w), T(c, r, w);
@@ -303,9 +329,8 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
     gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
     if (dist) allreduce(c, G2.p(), r * r);
-    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p());
+    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p(), R2i.p());
     if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
-    tri_inv_any(c, R2.p(), r, R2i.p(), Dv.p());
     gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
     if (T_out) {
         Mat64 T(c, r, w);
@@ -387,16 +412,57 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 
 // Whole-matrix CholQR2 of C (rows × cc; fp32 on the tensor cores, fp64 on DGEMM), written
 // to B.  Returns false (B untouched) when C is not safely full rank (oracle.cholqr2_whole).
+// fp32 C on the 3×FP16 tensor-core path: every operand split once — C (Gram and C·R⁻¹ read
+// one interleaved split), Q1 straight from fp64 (Gram and the correction) — and the products
+// issued directly (a split per gemm() call re-split C and Q1, and Q1 went through fp32 first).
+static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
+    DevBuf cil, ce;
+    split_il(c, C, BCUR_F32, rows, cc, rows, &cil, &ce);
+    const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
+    umma_h3(c, false, cil.as<uint16_t>(), ce.as<int>(), rows, cc, cx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
+    if (dist) allreduce(c, G.p(), cc * cc);
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
+    const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
+    if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
+    umma_h3(c, true, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, 0.0, Q1.p(),
+            Q1.ld, GEMM_B_UPPER);
+    cil = DevBuf();
+    DevBuf qil, qe;
+    split_il(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, &qil, &qe);
+    const F16View qx{qil.as<uint16_t>(), nullptr, qe.as<int>(), rows, cc};
+    umma_h3(c, false, qil.as<uint16_t>(), qe.as<int>(), rows, cc, qx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
+    if (dist) allreduce(c, G.p(), cc * cc);
+    // second pass as cholqr2_whole: near identity → Q = Q1 + Q1·(−F), else a full factorization
+    Mat64 dev(c, 1, 1);
+    max_dev_identity(c, G.p(), cc, G.ld, dev.p());
+    double hdev = 1.0;
+    d2h(c, &hdev, dev.p(), 1);
+    const bool near = hdev < 1e-4;
+    if (near) {
+        near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), true);
+    } else {
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
+        if (c2.info != 0) return false;
+    }
+    umma_h3(c, true, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, near ? 1.0 : 0.0,
+            Q1.p(), Q1.ld, GEMM_B_UPPER);
+    B->init(c, BCUR_F32, rows, cc);
+    convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
+    B->rank = cc;
+    return true;
+}
+
 static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
     if (cc == 0 || rows < cc) return false;
+    if (cdt == BCUR_F32 && h3_ok(rows) && cc >= 128) return cholqr2_whole_h3(c, C, rows, cc, dist, dt, B);
     Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
     gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, cdt, rows, C, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p());
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
-    tri_inv_any(c, R.p(), cc, Ri.p(), Dv.p());
     gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
          GEMM_B_UPPER);
     // Q1 in the basis dtype (fp32 → every later product with it runs on the tensor cores)
@@ -422,9 +488,8 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
         // pass is exact to ~1e-11; fp64: Q = Q1·(I − F) on DGEMM
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), cdt == BCUR_F32);
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p());
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
         if (c2.info != 0) return false;
-        tri_inv_any(c, R.p(), cc, Ri.p(), Dv.p());
     }
     B->init(c, cdt, rows, cc);
     if (cdt == BCUR_F32) {
@@ -992,9 +1057,8 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         auto pinv_rows = [&](const Mat64& T, int64_t rk, int64_t cols, Mat64* out_p) {
             Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk), Dv(c, 128, rk);
             gemm(c, OP_N, OP_T, rk, rk, cols, 1.0, T.p(), BCUR_F64, T.ld, T.p(), BCUR_F64, T.ld, 0.0, G.p(), G.ld);
-            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Dv.p());
+            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Dv.p(), Ri.p());
             if (ci.info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
-            tri_inv_any(c, R.p(), rk, Ri.p(), Dv.p());
             gemm(c, OP_N, OP_T, rk, rk, rk, 1.0, Ri.p(), BCUR_F64, Ri.ld, Ri.p(), BCUR_F64, Ri.ld, 0.0, Gi.p(), Gi.ld);
             *out_p = Mat64(c, cols, rk);
             gemm(c, OP_T, OP_N, cols, rk, rk, 1.0, T.p(), BCUR_F64, T.ld, Gi.p(), BCUR_F64, Gi.ld, 0.0, out_p->p(),
