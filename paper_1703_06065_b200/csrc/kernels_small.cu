@@ -420,6 +420,166 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
     for (int j = threadIdx.x; j < w; j += NTB) lam[j] = A[order[j] + order[j] * la];
 }
 
+// ---------------------------------------- packed two-sided Jacobi (any w ≤ 220)
+// The same rotations as k_jacobi (circle-method rounds, the same angle formula and stopping
+// rule), restructured so that a round is ONE pass over the matrix: under a round's pairing
+// the 2×2 blocks (pair P rows × pair Q columns) partition A, and each is updated from both
+// sides at once, A[P,Q] ← J_Pᵀ A[P,Q] J_Q, by one thread (blocks are disjoint: no barrier
+// between the row and the column rotation).  Only the lower triangle is stored (packed),
+// so w = 220 fits in shared memory (194 KB).  V is not accumulated here: every round's
+// rotations are logged (p, q, c, s) and k_jacobi_replay applies them to the rows of V on
+// many SMs afterwards.
+constexpr int JP_T = 1024;
+struct JRot {
+    double c, s;
+    int p, q;
+};
+__device__ __forceinline__ int tri_at(int i, int j) { return i >= j ? i * (i + 1) / 2 + j : j * (j + 1) / 2 + i; }
+__global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict__ g, int w, int64_t ldg,
+                                                        JRot* __restrict__ log, int* __restrict__ nrounds_out,
+                                                        double* __restrict__ lam, int* __restrict__ order_out,
+                                                        int max_sweeps) {
+    extern __shared__ double Ap[];  // packed lower triangle
+    __shared__ double cs[256], sn[256], np_[256], nq_[256];
+    __shared__ int pp[256], qq[256];
+    __shared__ int rotated;
+    __shared__ double floor_abs;
+    const int wp = (w + 1) & ~1, half = wp / 2, mrot = wp - 1;
+    const int NT = blockDim.x;
+    for (int i = threadIdx.x; i < w; i += NT)
+        for (int j = 0; j <= i; ++j) Ap[i * (i + 1) / 2 + j] = g[i + (int64_t)j * ldg];  // lower of a symmetric G
+    if (threadIdx.x == 0) {
+        double f = 0.0;
+        for (int j = 0; j < w; ++j) f = fmax(f, fabs(g[j + j * ldg]));
+        floor_abs = 1e-16 * f * (double)w;
+    }
+    __syncthreads();
+    const int nblk = half * (half + 1) / 2;
+    int rounds = 0;
+    for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+        if (threadIdx.x == 0) rotated = 0;
+        __syncthreads();
+        for (int round = 0; round < mrot; ++round, ++rounds) {
+            for (int i = threadIdx.x; i < half; i += NT) {
+                int p = i == 0 ? round : (round + i) % mrot;
+                int q = i == 0 ? wp - 1 : (round - i + mrot) % mrot;
+                if (p > q) { const int t = p; p = q; q = t; }
+                double c = 1.0, sv = 0.0;
+                if (q < w) {
+                    const double apq = Ap[tri_at(q, p)];
+                    const double app = Ap[tri_at(p, p)], aqq = Ap[tri_at(q, q)];
+                    if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(app * aqq)) {
+                        const double tau = (aqq - app) * fast_rcp(2.0 * apq);
+                        const double q2 = fma(tau, tau, 1.0);
+                        const double root = q2 * fast_rsqrt(q2);
+                        const double t = (tau >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(tau) + root);
+                        c = fast_rsqrt(fma(t, t, 1.0));
+                        sv = t * c;
+                        np_[i] = app - t * apq;
+                        nq_[i] = aqq + t * apq;
+                        rotated = 1;
+                    }
+                }
+                pp[i] = p;
+                qq[i] = q;
+                cs[i] = c;
+                sn[i] = sv;
+                log[(int64_t)rounds * half + i] = JRot{c, sv, p, q};
+            }
+            __syncthreads();
+            // block (P, Q), P ≥ Q, enumerated over the packed block triangle
+            for (int b = threadIdx.x; b < nblk; b += NT) {
+                int P = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+                if (P * (P + 1) / 2 > b) --P;
+                if ((P + 1) * (P + 2) / 2 <= b) ++P;
+                const int Q = b - P * (P + 1) / 2;
+                const int p1 = pp[P], q1 = qq[P], p2 = pp[Q], q2 = qq[Q];
+                const double s1 = sn[P], s2 = sn[Q];
+                if (s1 == 0.0 && s2 == 0.0) continue;
+                if (P == Q) {  // diagonal block: exact annihilation
+                    if (q1 >= w) continue;
+                    Ap[tri_at(q1, p1)] = 0.0;
+                    Ap[tri_at(p1, p1)] = np_[P];
+                    Ap[tri_at(q1, q1)] = nq_[P];
+                    continue;
+                }
+                const double c1 = cs[P], c2 = cs[Q];
+                const bool r2 = q1 < w, c2v = q2 < w;  // byes: a padding index has no row/column
+                const int i_pp = tri_at(p1, p2), i_pq = c2v ? tri_at(p1, q2) : 0;
+                const int i_qp = r2 ? tri_at(q1, p2) : 0, i_qq = (r2 && c2v) ? tri_at(q1, q2) : 0;
+                const double a_pp = Ap[i_pp], a_pq = c2v ? Ap[i_pq] : 0.0;
+                const double a_qp = r2 ? Ap[i_qp] : 0.0, a_qq = (r2 && c2v) ? Ap[i_qq] : 0.0;
+                // rows: [p1; q1] ← [c1 −s1; s1 c1]·[.]   (Jᵀ A with J = [c s; −s c] convention of k_jacobi)
+                const double b_pp = c1 * a_pp - s1 * a_qp, b_pq = c1 * a_pq - s1 * a_qq;
+                const double b_qp = s1 * a_pp + c1 * a_qp, b_qq = s1 * a_pq + c1 * a_qq;
+                // columns: [p2, q2] ← [.]·J
+                Ap[i_pp] = c2 * b_pp - s2 * b_pq;
+                if (c2v) Ap[i_pq] = s2 * b_pp + c2 * b_pq;
+                if (r2) Ap[i_qp] = c2 * b_qp - s2 * b_qq;
+                if (r2 && c2v) Ap[i_qq] = s2 * b_qp + c2 * b_qq;
+            }
+            __syncthreads();
+        }
+        if (!rotated) break;
+        __syncthreads();
+    }
+    __shared__ int order[512];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < w; ++i) order[i] = i;
+        for (int i = 0; i < w; ++i) {
+            int best = i;
+            for (int j = i + 1; j < w; ++j)
+                if (Ap[tri_at(order[j], order[j])] > Ap[tri_at(order[best], order[best])]) best = j;
+            const int t = order[i]; order[i] = order[best]; order[best] = t;
+        }
+        *nrounds_out = rounds;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < w; j += NT) {
+        lam[j] = Ap[tri_at(order[j], order[j])];
+        order_out[j] = order[j];
+    }
+}
+
+// V = the product of the logged rotations (V ← V·J per round), rows of V spread over CTAs:
+// every row goes through all rounds independently; within a round the pairs are disjoint.
+// vout[:, j] = V[:, order[j]].
+constexpr int JR_T = 256, JR_ROWS = 2, JR_CHUNK = 6144;  // log entries staged per chunk (144 KB)
+__global__ void __launch_bounds__(JR_T) k_jacobi_replay(const JRot* __restrict__ log, const int* __restrict__ nrounds,
+                                                        const int* __restrict__ order, int w, double* __restrict__ vout) {
+    __shared__ double V[JR_ROWS][512];
+    extern __shared__ JRot stage[];  // a chunk of whole rounds, loaded with one barrier
+    const int r0 = blockIdx.x * JR_ROWS;
+    const int wp = (w + 1) & ~1, half = wp / 2;
+    for (int e = threadIdx.x; e < JR_ROWS * wp; e += JR_T) {
+        const int rr = e / wp, j = e % wp;
+        V[rr][j] = (r0 + rr < w && j == r0 + rr) ? 1.0 : 0.0;
+    }
+    const int n = *nrounds, per = JR_CHUNK / half;
+    for (int t0 = 0; t0 < n; t0 += per) {
+        const int nr = min(per, n - t0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < nr * half; e += JR_T) stage[e] = log[(int64_t)t0 * half + e];
+        __syncthreads();
+        for (int t = 0; t < nr; ++t) {
+            const JRot* lr = stage + t * half;
+            for (int e = threadIdx.x; e < JR_ROWS * half; e += JR_T) {
+                const int rr = e / half, i = e - rr * half;
+                const JRot r = lr[i];
+                if (r.s == 0.0) continue;
+                const double vp = V[rr][r.p], vq = V[rr][r.q];
+                V[rr][r.p] = r.c * vp - r.s * vq;
+                V[rr][r.q] = r.s * vp + r.c * vq;
+            }
+            __syncthreads();
+        }
+    }
+    for (int e = threadIdx.x; e < JR_ROWS * w; e += JR_T) {
+        const int rr = e / w, j = e % w;
+        if (r0 + rr < w) vout[(r0 + rr) + (int64_t)j * w] = V[rr][order[j]];
+    }
+}
+
 // ------------------------------------------------ one-sided Jacobi (large w)
 // Hestenes one-sided Jacobi on a symmetric PSD G (its singular values are its
 // eigenvalues): column pairs of W = G·V are orthogonalised in the same circle-method
@@ -568,8 +728,46 @@ void tri_inv_upper(Ctx* c, const double* r, int64_t w, int64_t ldr, double* x, i
 
 void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, double* v) {
     if (w > 512) fail(BCUR_E_INVALID_ARGUMENT, "sym_eig: w > 512 not supported");
+    if (w <= 0) return;
     ensure_attrs();
     ProfScope prof(c, "sym_eig", 0.0, 8.0 * w * w);
+    const size_t packed = (size_t)w * (w + 1) / 2 * sizeof(double);
+    static const char* legacy = getenv("BCUR_JACOBI_LEGACY");
+    if (packed <= 200 * 1024 && !(legacy && legacy[0] == '1')) {
+        // packed two-sided rounds + logged rotations replayed onto V across SMs
+        static bool attr = false;
+        if (!attr) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        constexpr int max_sweeps = 40;
+        const int64_t half = (w + 1) / 2, rounds_max = (int64_t)max_sweeps * (2 * half - 1);
+        DevBuf log(c, (size_t)rounds_max * half * sizeof(JRot)), meta(c, (size_t)(w + 16) * sizeof(int));
+        int* nrounds = meta.as<int>();
+        int* order = nrounds + 16;
+        // threads: one per 2×2 block of a round (fewer warps per barrier for small w)
+        const int64_t nblk = half * (half + 1) / 2;
+        const int nt = (int)std::min<int64_t>(JP_T, std::max<int64_t>(128, (nblk + 127) / 128 * 128));
+        k_jacobi_packed<<<1, nt, packed, c->stream>>>(g, (int)w, ldg, log.as<JRot>(), nrounds, lam, order,
+                                                      max_sweeps);
+        LAUNCH_CHECK(c);
+        static bool attr_r = false;
+        if (!attr_r) {
+            CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_replay, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)(JR_CHUNK * sizeof(JRot))));
+            attr_r = true;
+        }
+        k_jacobi_replay<<<(unsigned)((w + JR_ROWS - 1) / JR_ROWS), JR_T, JR_CHUNK * sizeof(JRot), c->stream>>>(
+            log.as<JRot>(), nrounds, order, (int)w, v);
+        if (getenv("BCUR_JACOBI_DEBUG")) {
+            int hr = 0;
+            CUDA_CHECK(cudaMemcpyAsync(&hr, nrounds, sizeof hr, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_CHECK(cudaStreamSynchronize(c->stream));
+            fprintf(stderr, "sym_eig w=%d rounds=%d sweeps=%.1f threads=%d\n", (int)w, hr, hr / (double)(2 * half - 1), nt);
+        }
+        LAUNCH_CHECK(c);
+        return;
+    }
     // A and V both in shared memory when they fit (every rotation updates two rows and
     // two columns of each; a global V made a 64×64 solve take 3.4 ms)
     const size_t mat = (size_t)w * (size_t)(w | 1) * sizeof(double);
