@@ -15,19 +15,24 @@ struct Handle {
         if (h) cublasDestroy(h);
     }
 };
-thread_local std::map<int, Handle> g_handles;  // per device, per host thread
+// per device and stream, per host thread: the blocked Cholesky issues cuBLAS calls on three
+// streams concurrently, and a handle's workspace must not be shared between them
+thread_local std::map<std::pair<int, cudaStream_t>, Handle> g_handles;
+cublasHandle_t handle(Ctx* c) {
+    Handle& hd = g_handles[{c->device, c->stream}];
+    if (!hd.h) {
+        if (cublasCreate(&hd.h) != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasCreate failed");
+        cublasSetPointerMode(hd.h, CUBLAS_POINTER_MODE_HOST);
+        cublasSetStream(hd.h, c->stream);
+    }
+    return hd.h;
+}
 }  // namespace
 
 void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
-    Handle& hd = g_handles[c->device];
-    if (!hd.h) {
-        if (cublasCreate(&hd.h) != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasCreate failed");
-        cublasSetPointerMode(hd.h, CUBLAS_POINTER_MODE_HOST);
-    }
-    cublasSetStream(hd.h, c->stream);
     const cublasStatus_t st =
-        cublasDgemm(hd.h, ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, (int)M, (int)N, (int)K,
+        cublasDgemm(handle(c), ta ? CUBLAS_OP_T : CUBLAS_OP_N, tb ? CUBLAS_OP_T : CUBLAS_OP_N, (int)M, (int)N, (int)K,
                     &alpha, A, (int)lda, B, (int)ldb, &beta, C, (int)ldc);
     if (st != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasDgemm failed (" + std::to_string((int)st) + ")");
     c->launches++;
@@ -38,15 +43,19 @@ void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, dou
 // triangle is ever read)
 void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
                           double* C, int64_t ldc) {
-    Handle& hd = g_handles[c->device];
-    if (!hd.h) {
-        if (cublasCreate(&hd.h) != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasCreate failed");
-        cublasSetPointerMode(hd.h, CUBLAS_POINTER_MODE_HOST);
-    }
-    cublasSetStream(hd.h, c->stream);
-    const cublasStatus_t st = cublasDsyrk(hd.h, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, (int)n, (int)k, &alpha, A,
+    const cublasStatus_t st = cublasDsyrk(handle(c), CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T, (int)n, (int)k, &alpha, A,
                                           (int)lda, &beta, C, (int)ldc);
     if (st != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasDsyrk failed (" + std::to_string((int)st) + ")");
+    c->launches++;
+}
+
+// B ← R⁻ᵀ·B in place, R upper triangular (M×M, ld ldr), B M×N (ld ldb): the panel solve of the
+// blocked Cholesky (block row k of R = R_kk⁻ᵀ × the updated trailing row), in place in R
+void cublas_dtrsm_left_upper_t(Ctx* c, int64_t M, int64_t N, const double* R, int64_t ldr, double* B, int64_t ldb) {
+    const double one = 1.0;
+    const cublasStatus_t st = cublasDtrsm(handle(c), CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
+                                          CUBLAS_DIAG_NON_UNIT, (int)M, (int)N, &one, R, (int)ldr, B, (int)ldb);
+    if (st != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasDtrsm failed (" + std::to_string((int)st) + ")");
     c->launches++;
 }
 

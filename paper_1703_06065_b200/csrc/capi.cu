@@ -182,6 +182,8 @@ bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
         cudaStreamDestroy(ctx->side);
         cudaStreamSynchronize(ctx->side2);
         cudaStreamDestroy(ctx->side2);
+        cudaStreamSynchronize(ctx->hp);
+        cudaStreamDestroy(ctx->hp);
         for (auto e : ctx->side_ev) cudaEventDestroy(e);
     }
     delete ctx;

@@ -133,15 +133,24 @@ struct Ctx {
     // so the workspace cache's stream-order reuse rule still holds.
     // A third stream (side2) carries work nothing on the chain waits for until the end (the
     // blocked inverse assembled alongside the factorization).
-    cudaStream_t side = nullptr, side2 = nullptr;
-    cudaEvent_t side_ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // The serial chain itself runs on a high-priority stream (hp) so that the block scheduler
+    // places its small kernels ahead of the side streams' wide DSYRK/DGEMM CTAs.
+    cudaStream_t side = nullptr, side2 = nullptr, hp = nullptr;
+    cudaEvent_t side_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaStream_t side_stream() {
         if (!side) {
-            CUDA_CHECK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
-            CUDA_CHECK(cudaStreamCreateWithFlags(&side2, cudaStreamNonBlocking));
+            int lo = 0, hi = 0;
+            CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, lo));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, hi));
             for (auto& e : side_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         return side;
+    }
+    cudaStream_t hp_stream() {
+        side_stream();
+        return hp;
     }
     cudaStream_t side_stream2() {
         side_stream();

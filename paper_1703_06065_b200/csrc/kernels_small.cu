@@ -236,6 +236,59 @@ __global__ void __launch_bounds__(CP_T) k_chol_panel(const double* g, int w, int
     }
 }
 
+// ------------------------------------------------- panel solve (kb ≤ 128)
+// P ← R⁻ᵀ·P in place for an upper-triangular R (kb × kb, ld ldr) and P (kb × N, ld ldp): the
+// block-row solve of the blocked Cholesky.  One CTA per 32 columns of P; Lᵀ = R staged in
+// shared memory; four 32-row blocks: each column's 32×32 triangle solved by its own thread in
+// registers (right-looking: 2 dependent ops per row), then the 32-row block's contribution
+// subtracted from the rows below by all 8 warps.
+constexpr int TS_T = 256, TS_C = 32, TS_LD = 129;
+__global__ void __launch_bounds__(TS_T) k_trsm128(const double* __restrict__ R, int kb, int64_t ldr, double* P,
+                                                  int64_t ldp, int N) {
+    extern __shared__ double sm_ts[];
+    double* L = sm_ts;                 // L[i + k·TS_LD] = R[k][i] (lower), i ≥ k
+    double* X = L + 128 * TS_LD;       // X[r + c·TS_LD], 128 × 32 slab
+    __shared__ double dinv[128];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c0 = blockIdx.x * TS_C, nc = min(TS_C, N - c0);
+    const int kp = (kb + 31) & ~31;
+    for (int i = warp; i < kp; i += TS_T / 32)  // column i of R (contiguous) → row i of L
+        for (int k = lane; k <= i; k += 32)
+            L[i + k * TS_LD] = (i < kb) ? R[k + (int64_t)i * ldr] : (i == k ? 1.0 : 0.0);
+    for (int c = warp; c < TS_C; c += TS_T / 32)
+        for (int r = lane; r < kp; r += 32)
+            X[r + c * TS_LD] = (c < nc && r < kb) ? P[r + (int64_t)(c0 + c) * ldp] : 0.0;
+    __syncthreads();
+    for (int i = tid; i < kp; i += TS_T) dinv[i] = 1.0 / L[i + i * TS_LD];
+    __syncthreads();
+    for (int b0 = 0; b0 < kp; b0 += 32) {
+        if (warp == 0) {  // lane = column
+            double x[32];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) x[r] = X[(b0 + r) + lane * TS_LD];
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                x[r] *= dinv[b0 + r];
+#pragma unroll
+                for (int j = r + 1; j < 32; ++j) x[j] = fma(-L[(b0 + j) + (b0 + r) * TS_LD], x[r], x[j]);
+            }
+#pragma unroll
+            for (int r = 0; r < 32; ++r) X[(b0 + r) + lane * TS_LD] = x[r];
+        }
+        __syncthreads();
+        // rows below the block: X[i, c] −= Σ_r L[i, b0 + r]·X[b0 + r, c]
+        for (int i = b0 + 32 + warp; i < kp; i += TS_T / 32) {
+            double acc = X[i + lane * TS_LD];
+#pragma unroll 8
+            for (int r = 0; r < 32; ++r) acc = fma(-L[i + (b0 + r) * TS_LD], X[(b0 + r) + lane * TS_LD], acc);
+            X[i + lane * TS_LD] = acc;
+        }
+        __syncthreads();
+    }
+    for (int c = warp; c < nc; c += TS_T / 32)
+        for (int r = lane; r < kb; r += 32) P[r + (int64_t)(c0 + c) * ldp] = X[r + c * TS_LD];
+}
+
 // ------------------------------------------------------ triangular inverse
 // X = R⁻¹ for upper-triangular R, w ≤ TRI_MAX_W, one CTA, 16-wide blocks (the matrix is
 // padded with identity to a multiple of 16).  Storage: one padded square S holds R's
@@ -709,6 +762,20 @@ void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, 
     else work = DevBuf(c, bytes);
     k_cholesky<<<1, ST, smem, c->stream>>>(g, (int)w, ldg, r, ldr, work.as<double>(), info, diag, (int)info_offset,
                                            chained ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void trsm_upper_t(Ctx* c, const double* r, int64_t kb, int64_t ldr, double* p, int64_t ldp, int64_t n) {
+    if (kb > 128) fail(BCUR_E_INVALID_ARGUMENT, "trsm_upper_t: kb <= 128");
+    if (kb <= 0 || n <= 0) return;
+    ProfScope prof(c, "trsm", 1.0 * kb * kb * n, 8.0 * (kb * kb / 2.0 + 2.0 * kb * n));
+    constexpr size_t smem = (size_t)(128 + TS_C) * TS_LD * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_trsm128, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_trsm128<<<(unsigned)((n + TS_C - 1) / TS_C), TS_T, smem, c->stream>>>(r, (int)kb, ldr, p, ldp, (int)n);
     LAUNCH_CHECK(c);
 }
 

@@ -59,6 +59,8 @@ void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, con
 void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 
+// B ← R⁻ᵀ·B in place (R upper M×M; B M×N)
+void cublas_dtrsm_left_upper_t(Ctx* c, int64_t M, int64_t N, const double* R, int64_t ldr, double* B, int64_t ldb);
 // C(upper) = alpha·AᵀA + beta·C(upper)  (A k×n)
 void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
                           double* C, int64_t ldc);
@@ -122,6 +124,8 @@ void cholesky_upper(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, 
 // Cholesky factor of a near-identity Gram)
 // minus_identity: return −F instead (the correction of Q = Q1·(I − F) = Q1 + Q1·(−F))
 void near_identity_rinv(Ctx* c, const double* g, int64_t w, int64_t ldg, double* x, bool minus_identity = false);
+// P ← R⁻ᵀ·P in place (R upper kb × kb, kb ≤ 128; P kb × n): the blocked Cholesky's panel solve
+void trsm_upper_t(Ctx* c, const double* r, int64_t kb, int64_t ldr, double* p, int64_t ldp, int64_t n);
 // X = R⁻¹ (upper triangular, w ≤ 128; only R's upper triangle is read; X's lower is zeroed)
 void tri_inv_upper(Ctx* c, const double* r, int64_t w, int64_t ldr, double* x, int64_t ldx);
 // symmetric eig, eigenvalues descending in lam, eigenvectors in columns of V (w×w)

@@ -13,6 +13,8 @@
 // For fp32 inputs the factor bases are kept in fp32 so that every product with
 // A or with a basis runs on the tcgen05 3×TF32 kernels (kernels_umma.cu).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 
@@ -127,19 +129,22 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     CUDA_CHECK(cudaMemcpyAsync(st.ptr, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
     c->sync();
     for (double d : diag) out.maxdiag = std::max(out.maxdiag, d);
-    // Look-ahead: step k updates the next block row (rows of block k+1, which step k+1
-    // factors and reads as its panel) on the main stream, and the rest of the trailing
-    // matrix with DSYRK on the side stream, where it overlaps step k+1's diagonal
-    // factorization, inverse and panel product.  Step k+1's own block-row update, which
-    // touches rows the side DSYRK also updates, waits for it.  T1 is double-buffered: the
-    // side DSYRK of step k reads T1[k&1] while step k+1 writes T1[(k+1)&1].
-    Mat64 Rdi(c, B, B), T1a(c, B, w), T1b(c, B, w), Tx, own_dinv;
-    if (Rinv && !dinv) {  // the inverse's side stream reads every diagonal inverse later
+    // Look-ahead: step k factors its diagonal block, solves its block row in place (R_kk⁻ᵀ·row,
+    // k_trsm128: one CTA per 32 columns), updates the next block row (which step k+1 factors and solves) on the
+    // main stream, and the rest of the trailing matrix with DSYRK on the side stream, where it
+    // overlaps step k+1's diagonal factorization and solve.  Step k+1's own block-row update,
+    // which touches rows the side DSYRK also updates, waits for it.  The diagonal blocks'
+    // inverses (dinv) and the block columns of R⁻¹ are formed on a third stream that nothing
+    // on the chain waits for.
+    Mat64 Tx, own_dinv;
+    if (Rinv && !dinv) {  // the inverse's stream keeps every diagonal inverse
         own_dinv = Mat64(c, B, w);
         dinv = own_dinv.p();
     }
-    cudaStream_t main_s = c->stream, side_s = c->side_stream(), inv_s = c->side_stream2();
-    c->order(main_s, side_s, 0);  // the side stream starts after R's initial copy
+    cudaStream_t caller_s = c->stream, main_s = c->hp_stream(), side_s = c->side_stream(), inv_s = c->side_stream2();
+    c->order(caller_s, main_s, 4);  // the chain forks from the caller's stream (after R's initial copy)
+    c->stream = main_s;
+    c->order(main_s, side_s, 0);
     if (Rinv) {
         Tx = Mat64(c, w, B);
         c->order(main_s, inv_s, 2);
@@ -147,46 +152,69 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         fill_f64(c, Rinv, w * w, 0.0);
         c->stream = main_s;
     }
+    static const bool tdbg = getenv("BCUR_CHOL_TIMING") != nullptr;
+    cudaEvent_t te0 = nullptr, te1 = nullptr;
+    auto th0 = std::chrono::steady_clock::now();
+    if (tdbg) {
+        CUDA_CHECK(cudaEventCreate(&te0));
+        CUDA_CHECK(cudaEventCreate(&te1));
+        CUDA_CHECK(cudaEventRecord(te0, main_s));
+    }
     int64_t step = 0;
     for (int64_t k = 0; k < w; k += B, ++step) {
         const int64_t kb = std::min(B, w - k), rest = w - k - kb;
         double* Dk = R + k + k * w;
-        double* Ri = dinv ? dinv + k * B : Rdi.p();  // inverse of the diagonal block (ld B)
         cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
-        if (rest > 0 || dinv || Rinv) tri_inv_upper(c, Dk, kb, w, Ri, B);
-        if (Rinv) {  // block column k of R⁻¹: R[:k, k] is final once block row k−1 was written
+        if (dinv) {
+            // off the chain: the block's inverse, then block column k of R⁻¹ (R[:k, k] is final
+            // once block row k−1 was solved)
+            double* Ri = dinv + k * B;
             c->order(main_s, inv_s, 2);
             c->stream = inv_s;
-            copy_f64(c, Ri, kb, kb, B, Rinv + k + k * w, w);
-            if (k > 0) {
-                gemm(c, OP_N, OP_N, k, kb, k, 1.0, Rinv, BCUR_F64, w, R + k * w, BCUR_F64, w, 0.0, Tx.p(), Tx.ld);
-                gemm(c, OP_N, OP_N, k, kb, kb, -1.0, Tx.p(), BCUR_F64, Tx.ld, Ri, BCUR_F64, B, 0.0, Rinv + k * w, w);
+            tri_inv_upper(c, Dk, kb, w, Ri, B);
+            if (Rinv) {
+                copy_f64(c, Ri, kb, kb, B, Rinv + k + k * w, w);
+                if (k > 0) {
+                    gemm(c, OP_N, OP_N, k, kb, k, 1.0, Rinv, BCUR_F64, w, R + k * w, BCUR_F64, w, 0.0, Tx.p(), Tx.ld);
+                    gemm(c, OP_N, OP_N, k, kb, kb, -1.0, Tx.p(), BCUR_F64, Tx.ld, Ri, BCUR_F64, B, 0.0, Rinv + k * w,
+                         w);
+                }
             }
             c->stream = main_s;
         }
         if (rest > 0) {
-            double* T1 = (step & 1) ? T1b.p() : T1a.p();
             double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
-            gemm(c, OP_T, OP_N, kb, rest, kb, 1.0, Ri, BCUR_F64, B, Pk, BCUR_F64, w, 0.0, T1, B);
-            copy_f64(c, T1, kb, rest, B, Pk, w);
+            trsm_upper_t(c, Dk, kb, w, Pk, w, rest);
             const int64_t n1 = std::min(B, rest), k1 = k + kb;
             if (step > 0) c->order(side_s, main_s, 1);  // previous side DSYRK covered these rows
-            // next block row (upper part used downstream): R[k1:k1+n1, k1:] −= T1[:, :n1]ᵀ·T1
-            gemm(c, OP_T, OP_N, n1, rest, kb, -1.0, T1, BCUR_F64, B, T1, BCUR_F64, B, 1.0, R + k1 + k1 * w, w);
+            // next block row (upper part used downstream): R[k1:k1+n1, k1:] −= Pk[:, :n1]ᵀ·Pk
+            gemm(c, OP_T, OP_N, n1, rest, kb, -1.0, Pk, BCUR_F64, w, Pk, BCUR_F64, w, 1.0, R + k1 + k1 * w, w);
             if (rest > n1) {
                 const int64_t k2 = k1 + n1, r2 = rest - n1;
                 c->order(main_s, side_s, 0);
                 c->stream = side_s;
                 {
                     ProfScope prof(c, "dsyrk_cublas", 1.0 * r2 * r2 * kb, 8.0 * (kb * r2 + r2 * r2 / 2.0));
-                    cublas_dsyrk_upper_t(c, r2, kb, -1.0, T1 + n1 * B, B, 1.0, R + k2 + k2 * w, w);
+                    cublas_dsyrk_upper_t(c, r2, kb, -1.0, Pk + n1 * w, w, 1.0, R + k2 + k2 * w, w);
                 }
                 c->stream = main_s;
             }
         }
     }
     c->order(side_s, main_s, 1);  // join before any buffer is released
-    if (Rinv) c->order(inv_s, main_s, 3);
+    if (dinv) c->order(inv_s, main_s, 3);
+    if (tdbg) {
+        const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+        CUDA_CHECK(cudaEventRecord(te1, main_s));
+        CUDA_CHECK(cudaEventSynchronize(te1));
+        float gpu_ms = 0.f;
+        CUDA_CHECK(cudaEventElapsedTime(&gpu_ms, te0, te1));
+        fprintf(stderr, "chol_any w=%lld host enqueue %.3f ms, gpu %.3f ms\n", (long long)w, host_ms, gpu_ms);
+        cudaEventDestroy(te0);
+        cudaEventDestroy(te1);
+    }
+    c->order(main_s, caller_s, 5);
+    c->stream = caller_s;
     zero_lower(c, R, w, w);
     d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
     out.info = hs.info;
