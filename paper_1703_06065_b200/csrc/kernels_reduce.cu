@@ -151,6 +151,50 @@ __device__ double sq_col_f16(const float* __restrict__ col, int64_t m, uint16_t*
     return s0 + s1;
 }
 
+// The interleaved-copy form only (m % 64 == 0): 8 rows per thread and step, so the max pass
+// keeps two 16-byte loads in flight per thread and the write pass stores 16-byte hi and lo
+// runs (the uint2 form stored 8 bytes per instruction and ran the norms pass at 4.4 TB/s).
+__device__ double sq_col_il(const float* __restrict__ col, int64_t m, uint16_t* __restrict__ il, int* colexp_j) {
+    double s0 = 0.0, s1 = 0.0;
+    float mx = 0.0f;
+    const float4* c4 = reinterpret_cast<const float4*>(col);
+    const int64_t m8 = m >> 3;
+    for (int64_t i = threadIdx.x; i < m8; i += RT) {
+        const float4 v = c4[2 * i], u = c4[2 * i + 1];
+        s0 = fma((double)v.x, (double)v.x, s0);
+        s1 = fma((double)v.y, (double)v.y, s1);
+        s0 = fma((double)v.z, (double)v.z, s0);
+        s1 = fma((double)v.w, (double)v.w, s1);
+        s0 = fma((double)u.x, (double)u.x, s0);
+        s1 = fma((double)u.y, (double)u.y, s1);
+        s0 = fma((double)u.z, (double)u.z, s0);
+        s1 = fma((double)u.w, (double)u.w, s1);
+        mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))),
+                             fmaxf(fmaxf(fabsf(u.x), fabsf(u.y)), fmaxf(fabsf(u.z), fabsf(u.w)))));
+    }
+    const int p = f16_scale_exp(block_max_all(mx));
+    if (threadIdx.x == 0) *colexp_j = p;
+    uint4* o = reinterpret_cast<uint4*>(il);  // 16-byte units: a 64-row chunk = 8 hi + 8 lo units
+    for (int64_t i = threadIdx.x; i < m8; i += RT) {
+        const float4 v = __ldcs(c4 + 2 * i), u = __ldcs(c4 + 2 * i + 1);
+        const float x[8] = {ldexpf(v.x, p), ldexpf(v.y, p), ldexpf(v.z, p), ldexpf(v.w, p),
+                            ldexpf(u.x, p), ldexpf(u.y, p), ldexpf(u.z, p), ldexpf(u.w, p)};
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const __half2 h = __floats2half2_rn(x[2 * t], x[2 * t + 1]);
+            const float2 f = __half22float2(h);
+            const __half2 l = __floats2half2_rn(x[2 * t] - f.x, x[2 * t + 1] - f.y);
+            hw[t] = *reinterpret_cast<const uint32_t*>(&h);
+            lw[t] = *reinterpret_cast<const uint32_t*>(&l);
+        }
+        const int64_t at = (i >> 3) * 16 + (i & 7);  // row 8i: chunk i/8, 16-byte unit i%8
+        __stcs(o + at, make_uint4(hw[0], hw[1], hw[2], hw[3]));
+        __stcs(o + at + 8, make_uint4(lw[0], lw[1], lw[2], lw[3]));
+    }
+    return s0 + s1;
+}
+
 // grid (G, Z): CTA (g, z) sums columns off[g]+z, off[g]+z+Z, ...  Optional copies of the
 // column: the TF32-rounded fp32 `shadow`, or the scaled fp16 `sh16` (+ per-column exponents).
 template <class T>
@@ -163,7 +207,9 @@ __global__ void __launch_bounds__(RT) k_block_sumsq(const T* __restrict__ a, int
     const int z = blockIdx.y;
     double s = 0.0;
     for (int64_t j = off[g] + z; j < off[g + 1]; j += Z) {
-        if (sizeof(T) == 4 && (sh16 || sl16))
+        if (sizeof(T) == 4 && sl16 && !sh16 && (m & 63) == 0)
+            s += sq_col_il(reinterpret_cast<const float*>(a + j * ld), m, sl16 + 2 * j * m, colexp + j);
+        else if (sizeof(T) == 4 && (sh16 || sl16))
             s += sq_col_f16(reinterpret_cast<const float*>(a + j * ld), m, sh16 ? sh16 + j * lds : nullptr,
                             sl16 ? sl16 + 2 * j * m : nullptr, colexp + j);
         else
