@@ -5,7 +5,7 @@
 LAUNCH_CSV  `ncu --metrics gpu__time_duration.sum --clock-control none --csv` of
             `bench.py --steps 1 --warmup 1 --e2e-steps 1` (STEPS decompositions: warmup,
             timed, profiled, e2e warmup, e2e timed = 5).
-FULL_REP    `ncu --set full --import-source on --clock-control none -k regex:k_umma` of the
+FULL_REP    `ncu --set full --import-source on --clock-control none -k regex:"k_umma|k_block_sumsq"` of the
             same command.
 Writes ROUND_DIR/launches_<workload>_summary.csv (per-kernel share of one step),
 ROUND_DIR/ncu_full_<workload>.md (per-launch metrics of the UMMA kernels) and merges
@@ -19,16 +19,22 @@ import os
 import subprocess
 import sys
 
-TAG_OF = {  # k_umma<A_MN, EPI, NT, X3> → bench/ProfScope kernel class
+TAG_OF = {  # k_umma<A_MN, EPI, NT, X3, H> → bench/ProfScope kernel class
     ("0", "1"): "umma_atx_rowsq", ("0", "0"): "umma_atx_store", ("1", "0"): "umma_ax",
 }
 
 
 def tag_of(name):
+    if "k_umma2_rowsq" in name:
+        return "umma_atx_rowsq"
+    if "k_block_sumsq" in name:
+        return "block_sumsq"
     if "k_umma<" not in name:
         return None
     args = name.split("k_umma<")[1].split(">")[0].replace("(bool)", "").replace("(int)", "").split(",")
     args = [a.strip().replace("false", "0").replace("true", "1") for a in args]
+    if len(args) >= 5 and args[3] == "1" and args[4] == "1":  # 3×FP16 products
+        return "umma_ax_h3" if args[0] == "1" else "umma_atx_h3"
     return TAG_OF.get((args[0], args[1]))
 
 
@@ -99,7 +105,7 @@ def main():
         for k, (ms, n) in sorted(L.items(), key=lambda kv: -kv[1][0]):
             w.writerow([k, f"{ms:.4f}", f"{n:g}", f"{ms / total:.4f}"])
     F = full(rep)
-    md = [f"# ncu --set full, UMMA kernels of one `{workload}` bench step (cold-cache, serialised replay)", "",
+    md = [f"# ncu --set full, tensor-core and streaming kernels of one `{workload}` bench step (cold-cache, serialised replay)", "",
           "| kernel | class | ms | DRAM read MB | DRAM write MB | DRAM % | L2 % | tensor % | FMA % | XU % | grid | regs |",
           "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     per_tag = collections.defaultdict(list)

@@ -269,3 +269,15 @@ def test_two_rank_column_sharding_matches_single_rank(B):
         assert r.plan.blocks() == single.plan.blocks()
         np.testing.assert_allclose(r.scores.scores, single.scores.scores, rtol=1e-6)
         assert r.projection_error == pytest.approx(single.projection_error, rel=1e-6)
+
+
+# Blocked fp64 Cholesky (w > 144: 128-wide diagonal blocks, the block-row solve split between
+# the chain and a side stream, trailing DSYRK on a third stream, R⁻¹ assembled on a fourth)
+# inside the whole-C CholQR2: ragged last block (fp64, w = 700) and a 12-step chain (fp32,
+# w = 1536, 3×FP16 products) against the oracle's CUR error.
+@pytest.mark.parametrize("dt,m,n,s,g", [(np.float64, 1024, 4096, 100, 7), (np.float32, 2048, 8192, 128, 12)])
+def test_blocked_factorization_widths(B, dt, m, n, s, g):
+    a = lowrank(m, n, 40, "pow:1", 1e-3, 9, dt)
+    got, ref = run_css(B, a, s, 30, 10, 1, g, O.WITHOUT_REPLACEMENT, 9)
+    assert got.plan.blocks() == ref.plan.blocks()
+    assert got.rank_c == g * s
