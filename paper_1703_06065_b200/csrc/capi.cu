@@ -184,6 +184,8 @@ bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
         cudaStreamDestroy(ctx->side2);
         cudaStreamSynchronize(ctx->hp);
         cudaStreamDestroy(ctx->hp);
+        cudaStreamSynchronize(ctx->side3);
+        cudaStreamDestroy(ctx->side3);
         for (auto e : ctx->side_ev) cudaEventDestroy(e);
     }
     delete ctx;

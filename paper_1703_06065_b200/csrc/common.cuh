@@ -135,7 +135,7 @@ struct Ctx {
     // blocked inverse assembled alongside the factorization).
     // The serial chain itself runs on a high-priority stream (hp) so that the block scheduler
     // places its small kernels ahead of the side streams' wide DSYRK/DGEMM CTAs.
-    cudaStream_t side = nullptr, side2 = nullptr, hp = nullptr;
+    cudaStream_t side = nullptr, side2 = nullptr, side3 = nullptr, hp = nullptr;
     cudaEvent_t side_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaStream_t side_stream() {
         if (!side) {
@@ -143,10 +143,15 @@ struct Ctx {
             CUDA_CHECK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
             CUDA_CHECK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, lo));
             CUDA_CHECK(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, lo));
+            CUDA_CHECK(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, lo));
             CUDA_CHECK(cudaStreamCreateWithPriority(&hp, cudaStreamNonBlocking, hi));
             for (auto& e : side_ev) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
         return side;
+    }
+    cudaStream_t side_stream3() {
+        side_stream();
+        return side3;
     }
     cudaStream_t hp_stream() {
         side_stream();

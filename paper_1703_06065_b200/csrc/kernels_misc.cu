@@ -41,6 +41,13 @@ __global__ void k_scale_columns(double* x, int64_t m, int64_t n, int64_t ld, con
     x[i + j * ld] *= s[j];
 }
 
+__global__ void k_scale_rows(double* x, int64_t m, int64_t n, int64_t ld, const double* __restrict__ s) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m * n) return;
+    const int64_t i = e % m, j = e / m;
+    x[i + j * ld] *= s[i];
+}
+
 __global__ void k_axpy_neg(const double* __restrict__ x, double* __restrict__ y, int64_t n) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n) y[e] -= x[e];
@@ -122,6 +129,12 @@ void axpy_neg(Ctx* c, const double* x, double* y, int64_t n) {
 void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale) {
     if (m * n == 0) return;
     k_scale_columns<<<nblk(m * n), 256, 0, c->stream>>>(x, m, n, ld, d_scale);
+    LAUNCH_CHECK(c);
+}
+
+void scale_rows(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale) {
+    if (m <= 0 || n <= 0) return;
+    k_scale_rows<<<nblk(m * n), 256, 0, c->stream>>>(x, m, n, ld, d_scale);
     LAUNCH_CHECK(c);
 }
 

@@ -1619,6 +1619,7 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     } else {
         Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
         sc.a_rn = 1;  // converted operands: no transform
+        sc.pf = g_pf >= 0 ? g_pf : 0;  // no L2 prefetch on the fp16 copy (as the 3×FP16 passes)
         if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false, true>(c, sc, ta, tx, tx, (int)M, (int)N, nullptr, 0,
                                                              part.as<double>(), 1.0, 0.0);

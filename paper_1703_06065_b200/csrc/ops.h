@@ -139,6 +139,7 @@ void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64
 void fill_f64(Ctx* c, double* p, int64_t count, double v);
 void axpy_neg(Ctx* c, const double* x, double* y, int64_t n);  // y -= x
 void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*n*/);
+void scale_rows(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*m*/);
 void copy_f64(Ctx* c, const double* src, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
 void transpose_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
 

@@ -129,28 +129,39 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     CUDA_CHECK(cudaMemcpyAsync(st.ptr, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
     c->sync();
     for (double d : diag) out.maxdiag = std::max(out.maxdiag, d);
-    // Look-ahead: step k factors its diagonal block, solves its block row in place (R_kk⁻ᵀ·row,
-    // k_trsm128: one CTA per 32 columns), updates the next block row (which step k+1 factors and solves) on the
-    // main stream, and the rest of the trailing matrix with DSYRK on the side stream, where it
-    // overlaps step k+1's diagonal factorization and solve.  Step k+1's own block-row update,
-    // which touches rows the side DSYRK also updates, waits for it.  The diagonal blocks'
-    // inverses (dinv) and the block columns of R⁻¹ are formed on a third stream that nothing
-    // on the chain waits for.
+    // Four streams (events order them):
+    //   M (high priority, the serial chain): chol(k) → solve of block row k's first n1 columns
+    //     → update of the next diagonal block (k+1) → chol(k+1) …
+    //   S: the rest of block row k's solve, then the rest of block row k+1's update
+    //   D: the DSYRK of the trailing matrix beyond block k+1
+    //   I: the diagonal inverses and the block columns of R⁻¹ (nothing waits for it)
+    // chol(k+1) waits for the DSYRK of step k−1 (it updated block k+1), and the first-part
+    // solve of row k+1 for S's update of that row — both a step behind, so M runs at the
+    // rate of one single-CTA factor + one small solve + one small GEMM per step.
     Mat64 Tx, own_dinv;
     if (Rinv && !dinv) {  // the inverse's stream keeps every diagonal inverse
         own_dinv = Mat64(c, B, w);
         dinv = own_dinv.p();
     }
-    cudaStream_t caller_s = c->stream, main_s = c->hp_stream(), side_s = c->side_stream(), inv_s = c->side_stream2();
+    cudaStream_t caller_s = c->stream, main_s = c->hp_stream(), side_s = c->side_stream(),
+                 syrk_s = c->side_stream3(), inv_s = c->side_stream2();
     c->order(caller_s, main_s, 4);  // the chain forks from the caller's stream (after R's initial copy)
     c->stream = main_s;
+    cudaEvent_t ev[5][2];  // chol, first-part solve, rest solve, row-rest update, dsyrk  (× step parity)
+    for (auto& e2 : ev)
+        for (auto& e : e2) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    enum { E_CHOL, E_TF, E_TR, E_RR, E_DS };
+    auto rec = [&](int e, int64_t step, cudaStream_t st) { CUDA_CHECK(cudaEventRecord(ev[e][step & 1], st)); };
+    auto wait = [&](cudaStream_t st, int e, int64_t step) { CUDA_CHECK(cudaStreamWaitEvent(st, ev[e][step & 1], 0)); };
+    auto on = [&](cudaStream_t st) { c->stream = st; };
     c->order(main_s, side_s, 0);
+    c->order(main_s, syrk_s, 1);
     if (Rinv) {
         Tx = Mat64(c, w, B);
         c->order(main_s, inv_s, 2);
-        c->stream = inv_s;
+        on(inv_s);
         fill_f64(c, Rinv, w * w, 0.0);
-        c->stream = main_s;
+        on(main_s);
     }
     static const bool tdbg = getenv("BCUR_CHOL_TIMING") != nullptr;
     cudaEvent_t te0 = nullptr, te1 = nullptr;
@@ -160,17 +171,20 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         CUDA_CHECK(cudaEventCreate(&te1));
         CUDA_CHECK(cudaEventRecord(te0, main_s));
     }
-    int64_t step = 0;
-    for (int64_t k = 0; k < w; k += B, ++step) {
-        const int64_t kb = std::min(B, w - k), rest = w - k - kb;
+    const int64_t nsteps = (w + B - 1) / B;
+    for (int64_t step = 0; step < nsteps; ++step) {
+        const int64_t k = step * B, kb = std::min(B, w - k), rest = w - k - kb;
         double* Dk = R + k + k * w;
+        on(main_s);
         cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
+        rec(E_CHOL, step, main_s);
         if (dinv) {
-            // off the chain: the block's inverse, then block column k of R⁻¹ (R[:k, k] is final
-            // once block row k−1 was solved)
+            // off the chain: the block's inverse, then block column k of R⁻¹ (R[:k, k] is final:
+            // row k−1's first-part solve ran on M, earlier rows' rest solves are covered by the
+            // S event M waited for before solving row k−1)
             double* Ri = dinv + k * B;
-            c->order(main_s, inv_s, 2);
-            c->stream = inv_s;
+            wait(inv_s, E_CHOL, step);
+            on(inv_s);
             tri_inv_upper(c, Dk, kb, w, Ri, B);
             if (Rinv) {
                 copy_f64(c, Ri, kb, kb, B, Rinv + k + k * w, w);
@@ -180,28 +194,54 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
                          w);
                 }
             }
-            c->stream = main_s;
         }
-        if (rest > 0) {
-            double* Pk = R + k + (k + kb) * w;  // rows k..k+kb, columns k+kb..w
-            trsm_upper_t(c, Dk, kb, w, Pk, w, rest);
-            const int64_t n1 = std::min(B, rest), k1 = k + kb;
-            if (step > 0) c->order(side_s, main_s, 1);  // previous side DSYRK covered these rows
-            // next block row (upper part used downstream): R[k1:k1+n1, k1:] −= Pk[:, :n1]ᵀ·Pk
-            gemm(c, OP_T, OP_N, n1, rest, kb, -1.0, Pk, BCUR_F64, w, Pk, BCUR_F64, w, 1.0, R + k1 + k1 * w, w);
-            if (rest > n1) {
-                const int64_t k2 = k1 + n1, r2 = rest - n1;
-                c->order(main_s, side_s, 0);
-                c->stream = side_s;
-                {
-                    ProfScope prof(c, "dsyrk_cublas", 1.0 * r2 * r2 * kb, 8.0 * (kb * r2 + r2 * r2 / 2.0));
-                    cublas_dsyrk_upper_t(c, r2, kb, -1.0, Pk + n1 * w, w, 1.0, R + k2 + k2 * w, w);
-                }
-                c->stream = main_s;
+        if (rest <= 0) break;
+        const int64_t n1 = std::min(B, rest), k1 = k + kb, k2 = k1 + n1, r2 = rest - n1;
+        double* Pk = R + k + k1 * w;  // block row k, columns k1..w
+        // M: first n1 columns of row k (row k−1's rest update of them ran on S)
+        on(main_s);
+        if (step > 0) wait(main_s, E_RR, step - 1);
+        trsm_upper_t(c, Dk, kb, w, Pk, w, n1);
+        rec(E_TF, step, main_s);
+        // S: the rest of row k
+        if (r2 > 0) {
+            wait(side_s, E_CHOL, step);
+            on(side_s);
+            trsm_upper_t(c, Dk, kb, w, Pk + n1 * w, w, r2);
+            rec(E_TR, step, side_s);
+        }
+        // M: next diagonal block, after the DSYRK of step k−1 (which updated it)
+        on(main_s);
+        if (step > 0) wait(main_s, E_DS, step - 1);
+        gemm(c, OP_T, OP_N, n1, n1, kb, -1.0, Pk, BCUR_F64, w, Pk, BCUR_F64, w, 1.0, R + k1 + k1 * w, w);
+        if (r2 > 0) {
+            // S: the rest of row k+1: R[k1:k2, k2:] −= Pk[:, :n1]ᵀ·Pk[:, n1:]  (after the first-part
+            // solve and the DSYRK of step k−1, which also updated that region)
+            wait(side_s, E_TF, step);
+            if (step > 0) wait(side_s, E_DS, step - 1);
+            on(side_s);
+            gemm(c, OP_T, OP_N, n1, r2, kb, -1.0, Pk, BCUR_F64, w, Pk + n1 * w, BCUR_F64, w, 1.0, R + k1 + k2 * w, w);
+            rec(E_RR, step, side_s);
+            // D: the trailing matrix beyond block k+1
+            wait(syrk_s, E_TR, step);
+            on(syrk_s);
+            {
+                ProfScope prof(c, "dsyrk_cublas", 1.0 * r2 * r2 * kb, 8.0 * (kb * r2 + r2 * r2 / 2.0));
+                cublas_dsyrk_upper_t(c, r2, kb, -1.0, Pk + n1 * w, w, 1.0, R + k2 + k2 * w, w);
             }
+            rec(E_DS, step, syrk_s);
+        } else {
+            // nothing beyond block k+1: keep the event chain consistent for step k+1's waits
+            on(side_s);
+            rec(E_RR, step, side_s);
+            on(syrk_s);
+            rec(E_DS, step, syrk_s);
         }
+        on(main_s);
     }
+    on(main_s);
     c->order(side_s, main_s, 1);  // join before any buffer is released
+    c->order(syrk_s, main_s, 0);
     if (dinv) c->order(inv_s, main_s, 3);
     if (tdbg) {
         const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
@@ -215,6 +255,8 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     }
     c->order(main_s, caller_s, 5);
     c->stream = caller_s;
+    for (auto& e2 : ev)
+        for (auto& e : e2) cudaEventDestroy(e);
     zero_lower(c, R, w, w);
     d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
     out.info = hs.info;
@@ -396,6 +438,10 @@ struct Basis {
     // with every append): the greedy CGS2 products run on it (kernels_umma.cu, H3)
     DevBuf il, iexps;
     bool h3() const { return il.ptr != nullptr; }
+    // whole-C CholQR2 (fp32, 3×FP16): C = Q·R with R⁻¹ = rinv1·rinv2 (rinv1 = R1⁻¹ of the first
+    // pass, rinv2 = I − F or the full R2⁻¹ of the second), kept for U = C⁺AR⁺ (block_cur)
+    Mat64 rinv1, rinv2;
+    bool has_rinv() const { return rinv1.m > 0 && rinv1.m == rank; }
     void enable_h3(Ctx* c) {
         if (dt != BCUR_F32 || !h3_ok(rows)) return;
         il = DevBuf(c, (size_t)rows * cap * 4);
@@ -443,8 +489,9 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 // fp32 C on the 3×FP16 tensor-core path: every operand split once — C (Gram and C·R⁻¹ read
 // one interleaved split), Q1 straight from fp64 (Gram and the correction) — and the products
 // issued directly (a split per gemm() call re-split C and Q1, and Q1 went through fp32 first).
-static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
-    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
+static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B,
+                             bool keep_rinv) {
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc), R1i;
     DevBuf cil, ce;
     split_il(c, C, BCUR_F32, rows, cc, rows, &cil, &ce);
     const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
@@ -456,6 +503,10 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     umma_h3(c, true, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, 0.0, Q1.p(),
             Q1.ld, GEMM_B_UPPER);
     cil = DevBuf();
+    if (keep_rinv) {
+        R1i = Mat64(c, cc, cc);
+        copy_f64(c, Ri.p(), cc, cc, Ri.ld, R1i.p(), cc);
+    }
     DevBuf qil, qe;
     split_il(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, &qil, &qe);
     const F16View qx{qil.as<uint16_t>(), nullptr, qe.as<int>(), rows, cc};
@@ -478,12 +529,19 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     B->init(c, BCUR_F32, rows, cc);
     convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
     B->rank = cc;
+    if (keep_rinv) {
+        B->rinv1 = std::move(R1i);
+        B->rinv2 = Mat64(c, cc, cc);
+        if (near) near_identity_rinv(c, G.p(), cc, G.ld, B->rinv2.p(), false);  // I − F (Ri held −F)
+        else copy_f64(c, Ri.p(), cc, cc, Ri.ld, B->rinv2.p(), cc);
+    }
     return true;
 }
 
-static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t cc, bool dist, int dt, Basis* B) {
+static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t cc, bool dist, int dt, Basis* B,
+                          bool keep_rinv = false) {
     if (cc == 0 || rows < cc) return false;
-    if (cdt == BCUR_F32 && h3_ok(rows) && cc >= 128) return cholqr2_whole_h3(c, C, rows, cc, dist, dt, B);
+    if (cdt == BCUR_F32 && h3_ok(rows) && cc >= 128) return cholqr2_whole_h3(c, C, rows, cc, dist, dt, B, keep_rinv);
     Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
     gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, cdt, rows, C, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
@@ -639,7 +697,7 @@ static void block_panel(Ctx* c, const DMat* a, const Shard& s, int64_t b, double
 // whole-C CholQR2 on the tensor cores for fp32 when safely full rank, else block
 // CGS2 panels with per-panel rank revealing (oracle.column_basis).
 static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vector<int64_t>& blocks,
-                         const std::vector<double>& bn2, Basis* B) {
+                         const std::vector<double>& bn2, Basis* B, bool keep_rinv = false) {
     const int64_t m = a->m;
     int64_t cap = 0;
     for (int64_t b : blocks) cap += s.off_global[b + 1] - s.off_global[b];
@@ -661,7 +719,7 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
             }
             at += w;
         }
-        if (cholqr2_whole(c, cf.ptr, cdt, m, cap, false, a->dtype, B)) return;
+        if (cholqr2_whole(c, cf.ptr, cdt, m, cap, false, a->dtype, B, keep_rinv)) return;
     }
     B->init(c, a->dtype == BCUR_F32 ? BCUR_F32 : BCUR_F64, m, cap);
     for (int64_t b : blocks) {
@@ -959,7 +1017,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     rb = unique_in_order(rb);
     // Q_C (m × rc), replicated
     Basis QC;
-    column_basis(c, a, s, cb, bn2, &QC);
+    column_basis(c, a, s, cb, bn2, &QC, want_u);
     // Q_R (n_local × rr): basis of the selected row blocks of A (column blocks of Aᵀ),
     // row-distributed over ranks.  Rᵀ_u = unscaled selected rows, transposed.
     int64_t ru = 0;
@@ -993,7 +1051,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     }
     Basis QR;
     bool whole = false;
-    if (ru > 0) whole = cholqr2_whole(c, rtu.ptr, bdt, nl, ru, dist, dt, &QR);
+    if (ru > 0) whole = cholqr2_whole(c, rtu.ptr, bdt, nl, ru, dist, dt, &QR, want_u);
     if (!whole) {
         QR.init(c, bdt, nl, ru);
         for (size_t i = 0; i < rb.size(); ++i) {
@@ -1036,7 +1094,37 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         path = 1;
     }
     out->u_valid = false;
-    if (want_u && rc > 0 && rr > 0) {
+    // Fast U: with distinct draws and full-rank whole-C bases, C = Q_C·R_C·D_C and
+    // Rᵀ = Q_R·R_R·D_R (D = the draws' sampling scales), so
+    //   U = C⁺ A R⁺ = D_C⁻¹ · R_C⁻¹ · M · R_R⁻ᵀ · D_R⁻¹
+    // from the inverse factors the CholQR2 already holds (R⁻¹ = rinv1·rinv2) — four fp64
+    // products instead of gathering C and Rᵀ, forming T = QᵀC and two pseudo-inverses.
+    int64_t ccw = 0, crw = 0;
+    for (auto& d : out->col_draws) ccw += coff[d.block + 1] - coff[d.block];
+    for (auto& d : out->row_draws) crw += roff[d.block + 1] - roff[d.block];
+    if (want_u && rc > 0 && rr > 0 && cb.size() == out->col_draws.size() && rb.size() == out->row_draws.size() &&
+        QC.has_rinv() && QR.has_rinv() && rc == ccw && rr == crw) {
+        std::vector<double> sc, sr;
+        for (auto& d : out->col_draws)
+            for (int64_t j = coff[d.block]; j < coff[d.block + 1]; ++j) sc.push_back(1.0 / d.scale);
+        for (auto& d : out->row_draws)
+            for (int64_t j = roff[d.block]; j < roff[d.block + 1]; ++j) sr.push_back(1.0 / d.scale);
+        Mat64 dsc(c, ccw, 1), dsr(c, crw, 1), T1(c, ccw, crw), T2(c, ccw, crw);
+        h2d(c, dsc.p(), sc.data(), ccw);
+        h2d(c, dsr.p(), sr.data(), crw);
+        gemm(c, OP_N, OP_N, ccw, crw, ccw, 1.0, QC.rinv2.p(), BCUR_F64, QC.rinv2.ld, M.p(), BCUR_F64, M.ld, 0.0,
+             T1.p(), T1.ld);
+        gemm(c, OP_N, OP_N, ccw, crw, ccw, 1.0, QC.rinv1.p(), BCUR_F64, QC.rinv1.ld, T1.p(), BCUR_F64, T1.ld, 0.0,
+             T2.p(), T2.ld);
+        gemm(c, OP_N, OP_T, ccw, crw, crw, 1.0, T2.p(), BCUR_F64, T2.ld, QR.rinv2.p(), BCUR_F64, QR.rinv2.ld, 0.0,
+             T1.p(), T1.ld);
+        out->u = Mat64(c, ccw, crw);
+        gemm(c, OP_N, OP_T, ccw, crw, crw, 1.0, T1.p(), BCUR_F64, T1.ld, QR.rinv1.p(), BCUR_F64, QR.rinv1.ld, 0.0,
+             out->u.p(), out->u.ld);
+        scale_rows(c, out->u.p(), ccw, crw, out->u.ld, dsc.p());
+        scale_columns(c, out->u.p(), ccw, crw, out->u.ld, dsr.p());
+        out->u_valid = true;
+    } else if (want_u && rc > 0 && rr > 0) {
         // C (m × cc) and Rᵀ (n_local × cr) with their sampling scales
         int64_t cc = 0, cr = 0;
         std::vector<int64_t> dco, dro;
