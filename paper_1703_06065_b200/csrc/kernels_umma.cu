@@ -1362,12 +1362,23 @@ __global__ void k_to_f16(const T* __restrict__ x, int64_t K, int64_t N, int64_t 
 }
 // out[i] = 2^(−2(colexp[i] + q)) · Σ_t partial[t·M + i]  (removes both exact scales)
 __global__ void k_sum_tiles_scaled(int64_t M, int tiles, const double* __restrict__ partial, const int* __restrict__ colexp,
-                                   const int* __restrict__ q, double* __restrict__ out) {
+                                   const int* __restrict__ q, int qh, double* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
     double s = 0.0;
     for (int t = 0; t < tiles; ++t) s += partial[(int64_t)t * M + i];
-    out[i] = ldexp(s, -2 * (colexp[i] + *q));
+    out[i] = ldexp(s, -2 * (colexp[i] + (q ? *q : qh)));
+}
+// Q (fp64, K × N, ld ldq) → the fp32 basis and its fp16 copy for the row-Σ² passes, scaled by
+// 2^14: entries of an orthonormal basis are ≤ 1 in magnitude, so no max pass is needed
+__global__ void k_basis_out(const double* __restrict__ q, int64_t K, int64_t N, int64_t ldq, float* __restrict__ q32,
+                            uint16_t* __restrict__ q16) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= K * N) return;
+    const double v = q[e % K + (e / K) * ldq];
+    q32[e] = (float)v;
+    const __half h = __double2half(v * 16384.0);
+    q16[e] = *reinterpret_cast<const uint16_t*>(&h);
 }
 
 // x (K × N, fp32 or fp64, ldx) → hi/lo fp32 (K × N, ld K)
@@ -1556,8 +1567,15 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
     LAUNCH_CHECK(c);
 }
 
+void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float* q32, uint16_t* q16) {
+    if (K <= 0 || N <= 0) return;
+    k_basis_out<<<(unsigned)((K * N + 255) / 256), 256, 0, c->stream>>>(q, K, N, ldq, q32, q16);
+    LAUNCH_CHECK(c);
+}
+
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
-                       const void* X, int dtx, int64_t ldx, double* rowsq, bool interleaved) {
+                       const void* X, int dtx, int64_t ldx, double* rowsq, bool interleaved, const uint16_t* x16_pre,
+                       int q_pre) {
     if (M <= 0) return;
     if (N <= 0 || K <= 0) {
         CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
@@ -1567,17 +1585,23 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
         fail(BCUR_E_INVALID_ARGUMENT, "gemm_rowsumsq_f16: the fp16 copy needs K % 64 == 0 (lda = K)");
     ProfScope prof(c, "umma_atx_rowsq", 2.0 * M * N * K, 2.0 * K * M + (double)dtype_size(dtx) * K * N + 8.0 * M);
     (void)umma_ok(BCUR_F32, K, lda, A16);  // reads the environment switches once
-    // X → fp16 with one power-of-two scale from its max (device-side; no host sync)
-    DevBuf mx(c, 64), x16(c, (size_t)K * N * 2);
-    CUDA_CHECK(cudaMemsetAsync(mx.ptr, 0, 8, c->stream));
+    // X → fp16 with one power-of-two scale from its max (device-side; no host sync), unless
+    // the caller passes it pre-converted (x16_pre, scale 2^q_pre)
+    DevBuf mx(c, 64), x16;
     int* q = reinterpret_cast<int*>(mx.as<unsigned int>() + 1);
     const unsigned gx = (unsigned)std::min<int64_t>((K * N + 255) / 256, 4LL * c->sm_count);
     const unsigned gc = (unsigned)((K * N + 255) / 256);
-    if (dtx == BCUR_F32) {
+    if (x16_pre) {
+        q = nullptr;
+    } else if (dtx == BCUR_F32) {
+        x16 = DevBuf(c, (size_t)K * N * 2);
+        CUDA_CHECK(cudaMemsetAsync(mx.ptr, 0, 8, c->stream));
         k_absmax<float><<<gx, 256, 0, c->stream>>>((const float*)X, K, N, ldx, mx.as<unsigned int>());
         k_to_f16<float><<<gc, 256, 0, c->stream>>>((const float*)X, K, N, ldx, mx.as<unsigned int>(),
                                                    x16.as<uint16_t>(), q);
     } else {
+        x16 = DevBuf(c, (size_t)K * N * 2);
+        CUDA_CHECK(cudaMemsetAsync(mx.ptr, 0, 8, c->stream));
         k_absmax<double><<<gx, 256, 0, c->stream>>>((const double*)X, K, N, ldx, mx.as<unsigned int>());
         k_to_f16<double><<<gc, 256, 0, c->stream>>>((const double*)X, K, N, ldx, mx.as<unsigned int>(),
                                                     x16.as<uint16_t>(), q);
@@ -1592,7 +1616,8 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
     const uint32_t bX[2] = {BKH, BN};
     CUtensorMap ta = make_map(A16, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
-    CUtensorMap tx = make_map(x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap tx = make_map(x16_pre ? (const void*)x16_pre : x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     const int k_tiles = (int)((K + BKH - 1) / BKH);
     const int mt = (int)((M + BM - 1) / BM);
     const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
@@ -1631,7 +1656,7 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
                                                              part.as<double>(), 1.0, 0.0);
     }
     k_sum_tiles_scaled<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(M, nt * NTX, part.as<double>(), colexp, q,
-                                                                           rowsq);
+                                                                           q_pre, rowsq);
     LAUNCH_CHECK(c);
 }
 

@@ -49,8 +49,12 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 // round-to-nearest 1×TF32 pass, twice the MMA rate, half the bytes) and the scales are
 // removed exactly in fp64.
 // interleaved: A16 is the [hi 64 | lo 64]-per-chunk copy (only hi is read), else compact hi.
+// x16_pre (nullable): X already in fp16 (K × N, ld K) scaled by 2^q_pre (B is then unused)
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
-                       const void* B, int dtb, int64_t ldb, double* rowsq, bool interleaved = true);
+                       const void* B, int dtb, int64_t ldb, double* rowsq, bool interleaved = true,
+                       const uint16_t* x16_pre = nullptr, int q_pre = 0);
+// orthonormal Q (fp64) → fp32 basis + its fp16 copy scaled by 2^14 (one pass)
+void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float* q32, uint16_t* q16);
 // out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);

@@ -442,6 +442,8 @@ struct Basis {
     // pass, rinv2 = I − F or the full R2⁻¹ of the second), kept for U = C⁺AR⁺ (block_cur)
     Mat64 rinv1, rinv2;
     bool has_rinv() const { return rinv1.m > 0 && rinv1.m == rank; }
+    // fp16 copy of the basis scaled by 2^14 (entries ≤ 1): the row-Σ² passes' X operand
+    DevBuf x16;
     void enable_h3(Ctx* c) {
         if (dt != BCUR_F32 || !h3_ok(rows)) return;
         il = DevBuf(c, (size_t)rows * cap * 4);
@@ -489,11 +491,17 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 // fp32 C on the 3×FP16 tensor-core path: every operand split once — C (Gram and C·R⁻¹ read
 // one interleaved split), Q1 straight from fp64 (Gram and the correction) — and the products
 // issued directly (a split per gemm() call re-split C and Q1, and Q1 went through fp32 first).
+// cil_pre (nullable): C already split (gathered from A's interleaved copy with its exponents).
 static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B,
-                             bool keep_rinv) {
+                             bool keep_rinv, DevBuf* cil_pre = nullptr, DevBuf* ce_pre = nullptr) {
     Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc), R1i;
     DevBuf cil, ce;
-    split_il(c, C, BCUR_F32, rows, cc, rows, &cil, &ce);
+    if (cil_pre) {
+        cil = std::move(*cil_pre);
+        ce = std::move(*ce_pre);
+    } else {
+        split_il(c, C, BCUR_F32, rows, cc, rows, &cil, &ce);
+    }
     const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
     umma_h3(c, false, cil.as<uint16_t>(), ce.as<int>(), rows, cc, cx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
@@ -527,7 +535,8 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     umma_h3(c, true, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, near ? 1.0 : 0.0,
             Q1.p(), Q1.ld, GEMM_B_UPPER);
     B->init(c, BCUR_F32, rows, cc);
-    convert(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, B->buf.ptr, BCUR_F32, rows);
+    B->x16 = DevBuf(c, (size_t)rows * cc * 2);
+    basis_out(c, Q1.p(), rows, cc, Q1.ld, B->buf.as<float>(), B->x16.as<uint16_t>());
     B->rank = cc;
     if (keep_rinv) {
         B->rinv1 = std::move(R1i);
@@ -697,11 +706,29 @@ static void block_panel(Ctx* c, const DMat* a, const Shard& s, int64_t b, double
 // whole-C CholQR2 on the tensor cores for fp32 when safely full rank, else block
 // CGS2 panels with per-panel rank revealing (oracle.column_basis).
 static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vector<int64_t>& blocks,
-                         const std::vector<double>& bn2, Basis* B, bool keep_rinv = false) {
+                         const std::vector<double>& bn2, Basis* B, bool keep_rinv = false,
+                         const RoundedA* ra = nullptr) {
     const int64_t m = a->m;
     int64_t cap = 0;
     for (int64_t b : blocks) cap += s.off_global[b + 1] - s.off_global[b];
-    if (cap > 0 && cap <= m) {  // whole-C CholQR2 first (oracle.column_basis)
+    bool tried = false;
+    if (cap >= 128 && cap <= m && ra && ra->has_lo() && c->comm.world <= 1) {
+        // C's 3×FP16 split is a gather of A's interleaved copy (2m halves and one exponent per
+        // column): no fp32 C, no split pass
+        DevBuf cil(c, (size_t)m * cap * 4), ce(c, (size_t)cap * sizeof(int));
+        int64_t at = 0;
+        for (int64_t b : blocks) {
+            const int64_t w = s.off_global[b + 1] - s.off_global[b], j0 = s.off_global[b] - s.col0;
+            CUDA_CHECK(cudaMemcpyAsync(cil.as<uint16_t>() + (size_t)at * 2 * m, ra->il.as<uint16_t>() + (size_t)j0 * 2 * m,
+                                       (size_t)w * m * 4, cudaMemcpyDeviceToDevice, c->stream));
+            CUDA_CHECK(cudaMemcpyAsync(ce.as<int>() + at, ra->exps.as<int>() + j0, (size_t)w * sizeof(int),
+                                       cudaMemcpyDeviceToDevice, c->stream));
+            at += w;
+        }
+        if (cholqr2_whole_h3(c, nullptr, m, cap, false, a->dtype, B, keep_rinv, &cil, &ce)) return;
+        tried = true;
+    }
+    if (cap > 0 && cap <= m && !tried) {  // whole-C CholQR2 first (oracle.column_basis)
         const int cdt = a->dtype;
         const size_t es = dtype_size(cdt);
         DevBuf cf(c, (size_t)m * cap * es);
@@ -755,10 +782,10 @@ static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra, bool with_lo) {
 }
 // rows[j] = Σ_c (AᵀX)_jc² over the shard's columns: from the fp16 copy when present
 static void rowsq_pass(Ctx* c, const DMat* a, const RoundedA* ra, int64_t N, const void* X, int dtx, int64_t ldx,
-                       double* rows) {
+                       double* rows, const uint16_t* x16 = nullptr) {
     if (ra && ra->ok())
         gemm_rowsumsq_f16(c, a->n, N, a->m, ra->il.as<uint16_t>(), a->m, ra->exps.as<int>(), X, dtx, ldx, rows,
-                          ra->interleaved);
+                          ra->interleaved, (x16 && ldx == a->m) ? x16 : nullptr, 14);
     else
         gemm_rowsumsq(c, OP_T, OP_N, a->n, N, a->m, a->ptr, a->dtype, a->ld, X, dtx, ldx, rows);
 }
@@ -768,7 +795,7 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
                              const RoundedA* ra = nullptr) {
     const int64_t nl = a->n;
     Mat64 rows(c, nl, 1), tot(c, 1, 1);
-    rowsq_pass(c, a, ra, B.rank, B.buf.ptr, B.dt, B.rows, rows.p());
+    rowsq_pass(c, a, ra, B.rank, B.buf.ptr, B.dt, B.rows, rows.p(), B.x16.as<uint16_t>());
     Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     double* b = d_blk_local ? d_blk_local : blk.p();
     segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
@@ -869,7 +896,7 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     for (auto& d : out->draws) blocks.push_back(d.block);
     ph.reset(new ProfScope(c, "phase:4 basis", 0, 0));
     Basis B;
-    column_basis(c, a, s, unique_in_order(blocks), bn2, &B);
+    column_basis(c, a, s, unique_in_order(blocks), bn2, &B, false, &ra);
     ph.reset(new ProfScope(c, "phase:5 residual", 0, 0));
     double res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra);
     ph.reset();
@@ -1017,7 +1044,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     rb = unique_in_order(rb);
     // Q_C (m × rc), replicated
     Basis QC;
-    column_basis(c, a, s, cb, bn2, &QC, want_u);
+    column_basis(c, a, s, cb, bn2, &QC, want_u, &ra);
     // Q_R (n_local × rr): basis of the selected row blocks of A (column blocks of Aᵀ),
     // row-distributed over ranks.  Rᵀ_u = unscaled selected rows, transposed.
     int64_t ru = 0;
