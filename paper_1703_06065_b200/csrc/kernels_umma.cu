@@ -1400,7 +1400,7 @@ void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, 
 // the A operand of A·X, moved onto the rows of X so that A'X' = A·X·2^q exactly).
 // One CTA per column; hi = rn16(x'), lo = rn16(x' − hi) (exact remainder in fp64).
 template <class T, bool IL>
-__global__ void __launch_bounds__(256) k_split_f16(const T* __restrict__ x, int64_t K, int64_t ldx,
+__global__ void __launch_bounds__(1024) k_split_f16(const T* __restrict__ x, int64_t K, int64_t ldx,
                                                    const int* __restrict__ fold, uint16_t* __restrict__ hi,
                                                    uint16_t* __restrict__ lo, int* __restrict__ q) {
     const int64_t j = blockIdx.x;
@@ -1410,7 +1410,7 @@ __global__ void __launch_bounds__(256) k_split_f16(const T* __restrict__ x, int6
         const double v = fabs((double)col[k]) * (fold ? exp2_int(-fold[k]) : 1.0);
         mx = v > mx ? v : mx;
     }
-    __shared__ double red[8];
+    __shared__ double red[32];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -1718,6 +1718,11 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
 
 
 // ---- 3×FP16 (H3) products -------------------------------------------------
+// one CTA per column: few, tall columns (the range finder's 65536 × 60 operands) get 1024
+// threads so the two passes over each column keep enough loads in flight
+static unsigned split_threads(int64_t K, int64_t N, Ctx* c) {
+    return (N < 2 * c->sm_count && K >= 8192) ? 1024u : 256u;
+}
 void split_f16(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, const int* fold, SplitF16* out) {
     out->K = K;
     out->N = N;
@@ -1727,11 +1732,11 @@ void split_f16(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx
     if (K <= 0 || N <= 0) return;
     ProfScope prof(c, "split_f16", 0.0, (double)K * N * (dtype_size(dtx) + 4));
     if (dtx == BCUR_F32)
-        k_split_f16<float, false><<<(unsigned)N, 256, 0, c->stream>>>((const float*)x, K, ldx, fold,
+        k_split_f16<float, false><<<(unsigned)N, split_threads(K, N, c), 0, c->stream>>>((const float*)x, K, ldx, fold,
                                                                      out->hi.as<uint16_t>(), out->lo.as<uint16_t>(),
                                                                      out->exps.as<int>());
     else
-        k_split_f16<double, false><<<(unsigned)N, 256, 0, c->stream>>>((const double*)x, K, ldx, fold,
+        k_split_f16<double, false><<<(unsigned)N, split_threads(K, N, c), 0, c->stream>>>((const double*)x, K, ldx, fold,
                                                                       out->hi.as<uint16_t>(), out->lo.as<uint16_t>(),
                                                                       out->exps.as<int>());
     LAUNCH_CHECK(c);
@@ -1742,10 +1747,10 @@ void split_il_into(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t
     if (m <= 0 || n <= 0) return;
     ProfScope prof(c, "split_f16", 0.0, (double)m * n * (dtype_size(dta) + 4));
     if (dta == BCUR_F32)
-        k_split_f16<float, true><<<(unsigned)n, 256, 0, c->stream>>>((const float*)a, m, lda, nullptr, il, nullptr,
+        k_split_f16<float, true><<<(unsigned)n, split_threads(m, n, c), 0, c->stream>>>((const float*)a, m, lda, nullptr, il, nullptr,
                                                                     exps);
     else
-        k_split_f16<double, true><<<(unsigned)n, 256, 0, c->stream>>>((const double*)a, m, lda, nullptr, il, nullptr,
+        k_split_f16<double, true><<<(unsigned)n, split_threads(m, n, c), 0, c->stream>>>((const double*)a, m, lda, nullptr, il, nullptr,
                                                                      exps);
     LAUNCH_CHECK(c);
 }
