@@ -163,6 +163,16 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
  *                          A·X, m % 8 == 0 for AᵀX) */
 enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4, BCUR_PRODUCT_H3 = 8 };
 bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
+/* io.cpp:105-137 load_matrix_binary / save_matrix_binary: the reference's ".bcur" format
+ * (magic "BCUR", u64 rows, u64 cols, f64 row-major).  The loader streams row chunks through
+ * pinned staging into a column-major device matrix of the requested dtype; columns
+ * [col0, col0 + ncols) select a shard (ncols = -1: to the end).  Missing magic, truncated
+ * header or data, unreasonable dimensions and NaN/Inf entries return BCUR_E_PARSE.
+ * bcur_bcur_header reads only the dimensions (to plan shards). */
+bcur_status bcur_bcur_header(const char* path, int64_t* rows, int64_t* cols);
+bcur_status bcur_dmat_load_bcur(bcur_ctx ctx, const char* path, int dtype, int64_t col0, int64_t ncols,
+                                bcur_dmat* out);
+bcur_status bcur_dmat_save_bcur(bcur_ctx ctx, bcur_dmat a, const char* path);
 /* sampler.cpp:116-146 draw_blocks (probabilities on the host, one uniform per draw
  * drawn by the caller from its Rng; margins_out[t] = distance of u_t to the nearest
  * CDF edge, nullable). */

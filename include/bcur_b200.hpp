@@ -153,6 +153,17 @@ public:
         detail::check(bcur_dmat_upload(dev.handle(), h, colmajor, std::max<Index>(rows, 1)));
         return m;
     }
+    // io.cpp:105-137 load_matrix_binary, streamed into HBM: columns [col0, col0 + ncols) of a
+    // ".bcur" file (ncols = -1: to the end) as fp64 or fp32; ParseError as in the reference
+    static DeviceMatrix load_binary(const std::string& path, int dtype = BCUR_F64, Index col0 = 0, Index ncols = -1,
+                                    Device& dev = Device::current()) {
+        bcur_dmat h = nullptr;
+        detail::check(bcur_dmat_load_bcur(dev.handle(), path.c_str(), dtype, col0, ncols, &h));
+        return DeviceMatrix(h);
+    }
+    void save_binary(const std::string& path, Device& dev = Device::current()) const {
+        detail::check(bcur_dmat_save_bcur(dev.handle(), h_, path.c_str()));
+    }
     static DeviceMatrix generate(const bcur_gen_spec& spec, Device& dev = Device::current()) {
         bcur_dmat h = nullptr;
         detail::check(bcur_dmat_generate(dev.handle(), &spec, &h));

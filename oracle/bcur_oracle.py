@@ -70,6 +70,10 @@ class DegenerateR(Error):
     pass
 
 
+class ParseError(Error):
+    pass
+
+
 class DimensionMismatch(Error):
     pass
 
@@ -957,6 +961,44 @@ CONFIGS = {
                noise=1e-4, s=128, k=200, p=20, q=0, mode=WITHOUT_REPLACEMENT, select="leverage+greedy",
                g=64, seed=0),
 }
+
+
+# ------------------------------------------------------------------ .bcur files
+# io.cpp:105-137 load_matrix_binary and save_matrix_binary (io.hpp:13-14): magic "BCUR",
+# little-endian u64 rows, u64 cols, then rows·cols f64 row-major; make_dense's finiteness check
+# (matcore.cpp:26-33) surfaces as ParseError.
+BCUR_MAGIC = b"BCUR"
+
+
+def save_matrix_binary(path, a: np.ndarray) -> None:
+    a = np.asarray(a, dtype=np.float64)
+    with open(path, "wb") as f:
+        f.write(BCUR_MAGIC)
+        f.write(np.array([a.shape[0], a.shape[1]], dtype="<u8").tobytes())
+        f.write(np.ascontiguousarray(a, dtype="<f8").tobytes())
+
+
+def load_matrix_binary(path) -> np.ndarray:
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise ParseError(f"cannot open {path}")
+    with f:
+        if f.read(4) != BCUR_MAGIC:
+            raise ParseError(f"{path}: missing BCUR magic")
+        hdr = f.read(16)
+        if len(hdr) != 16:
+            raise ParseError(f"{path}: truncated header")
+        rows, cols = (int(v) for v in np.frombuffer(hdr, dtype="<u8"))
+        if rows == 0 or cols == 0 or rows >= 1 << 31 or cols >= 1 << 31:
+            raise ParseError(f"{path}: unreasonable dimensions {rows}x{cols}")
+        data = f.read(rows * cols * 8)
+        if len(data) != rows * cols * 8:
+            raise ParseError(f"{path}: truncated entry data")
+    a = np.frombuffer(data, dtype="<f8").reshape(rows, cols).astype(np.float64)
+    if not np.all(np.isfinite(a)):
+        raise ParseError(f"{path}: matrix contains NaN or Inf")
+    return np.asfortranarray(a)
 
 
 def spectrum(spec: str, r: int) -> np.ndarray:

@@ -10,6 +10,8 @@
   c2.json        config 2 (fp64 64×20000 biometric surrogate, greedy 8 of 200 blocks).
   c3s.json       config-3 structure at 2048×8192 fp32 (k=50, p=10, q=2, 8 of 64 blocks).
   c4s.json       config-4 structure at 1536×2048 fp32 (30, 4 col + 3 row blocks, U = C⁺AR⁺).
+  small.bcur     a 5×7 matrix (i − 2.5·j + 1/(1+i+j)) in the reference's binary format
+                 (io.cpp:105-137), written by the oracle's save_matrix_binary.
 
 The reference's numerical core (Eigen) cannot be built here, so everything but
 rng_ref.json is oracle output: it freezes the oracle (tests re-derive it) and gives
@@ -76,8 +78,14 @@ def css_case(a, s, k, p, q, g, mode, seed) -> dict:
             "rank_c": res.rank_c, "residual_path": res.residual_path}
 
 
+def small_bcur():
+    i, j = np.meshgrid(np.arange(5), np.arange(7), indexing="ij")
+    O.save_matrix_binary(os.path.join(OUT, "small.bcur"), i - 2.5 * j + 1.0 / (1 + i + j))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
+    small_bcur()
     files = {"rng_ref.json": rng_ref()}
     c = O.CONFIGS["c1"]
     a = lowrank(c["m"], c["n"], c["rank"], c["spectrum"], c["noise"], c["seed"], np.float64)

@@ -11,6 +11,7 @@ else fp64.  There is no CPU compute path: every numeric result comes from the GP
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence, Tuple
@@ -206,6 +207,21 @@ class DeviceMatrix:
         dm = DeviceMatrix(h, ctx)
         _check(L.lib.bcur_dmat_upload(ctx.handle, h, a.ctypes.data_as(C.c_void_p), max(a.shape[0], 1)))
         return dm
+
+    @staticmethod
+    def load_bcur(path, dtype=np.float64, col0: int = 0, ncols: int = -1,
+                  ctx: Optional[Context] = None) -> "DeviceMatrix":
+        """io.cpp:105-137 load_matrix_binary, streamed into HBM (column-major, fp32 or fp64);
+        columns [col0, col0 + ncols) select a shard.  Raises ParseError like the reference."""
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(L.lib.bcur_dmat_load_bcur(ctx.handle, os.fsencode(path), _dtype_code(np.dtype(dtype)), col0, ncols,
+                                         C.byref(h)))
+        return DeviceMatrix(h, ctx)
+
+    def save_bcur(self, path) -> None:
+        """save_matrix_binary: row-major fp64 with the BCUR header."""
+        _check(L.lib.bcur_dmat_save_bcur(self.ctx.handle, self.handle, os.fsencode(path)))
 
     @staticmethod
     def wrap(ptr: int, dtype, m: int, n: int, ld: int, ctx: Optional[Context] = None, owner=None) -> "DeviceMatrix":
@@ -440,6 +456,13 @@ def block_sq_norms(a, part: BlockPartition, ctx: Optional[Context] = None) -> np
     out = np.empty(part.num_blocks(), dtype=np.float64)
     _check(L.lib.bcur_block_sq_norms(ctx.handle, d.handle, offp, part.num_blocks(), out.ctypes.data_as(L.P_dbl)))
     return out
+
+
+def bcur_header(path):
+    """(rows, cols) of a .bcur file (plans column shards without reading the data)."""
+    r, c = L.i64(), L.i64()
+    _check(L.lib.bcur_bcur_header(os.fsencode(path), C.byref(r), C.byref(c)))
+    return r.value, c.value
 
 
 def sketch_product(a, x: np.ndarray, transpose: bool = False, row_sumsq: bool = False,

@@ -307,6 +307,150 @@ bcur_status bcur_dmat_upload(bcur_ctx ctx, bcur_dmat a, const void* host, int64_
     API_END
 }
 
+// ---------------------------------------------------------------- .bcur files
+// io.cpp:105-137 (load_matrix_binary) / save_matrix_binary: magic "BCUR", u64 rows, u64 cols
+// (little-endian), rows·cols f64 row-major.  Streamed in row chunks through two pinned
+// staging buffers (disk read of chunk i+1 overlaps the copy and device transpose of chunk
+// i) straight into a column-major device matrix of either dtype; a column range selects a
+// shard (one contiguous run per row).  Errors are ParseError as in the reference.
+namespace {
+struct BcurHeader {
+    uint64_t rows = 0, cols = 0;
+};
+BcurHeader read_bcur_header(FILE* f, const std::string& path) {
+    char magic[4] = {0, 0, 0, 0};
+    if (fread(magic, 1, 4, f) != 4 || memcmp(magic, "BCUR", 4) != 0) fail(BCUR_E_PARSE, path + ": missing BCUR magic");
+    BcurHeader h;
+    if (fread(&h.rows, 8, 1, f) != 1 || fread(&h.cols, 8, 1, f) != 1) fail(BCUR_E_PARSE, path + ": truncated header");
+    constexpr uint64_t kMaxDim = 1ull << 31;
+    if (h.rows == 0 || h.cols == 0 || h.rows >= kMaxDim || h.cols >= kMaxDim)
+        fail(BCUR_E_PARSE, path + ": unreasonable dimensions " + std::to_string(h.rows) + "x" + std::to_string(h.cols));
+    return h;
+}
+struct File {
+    FILE* f = nullptr;
+    ~File() {
+        if (f) fclose(f);
+    }
+};
+}  // namespace
+
+bcur_status bcur_bcur_header(const char* path, int64_t* rows, int64_t* cols) {
+    API_BEGIN
+    if (!path || !rows || !cols) fail(BCUR_E_INVALID_ARGUMENT, "bcur_bcur_header: null argument");
+    File fh;
+    fh.f = fopen(path, "rb");
+    if (!fh.f) fail(BCUR_E_PARSE, std::string("cannot open ") + path);
+    const BcurHeader h = read_bcur_header(fh.f, path);
+    *rows = (int64_t)h.rows;
+    *cols = (int64_t)h.cols;
+    API_END
+}
+
+bcur_status bcur_dmat_load_bcur(bcur_ctx ctx, const char* path, int dtype, int64_t col0, int64_t ncols,
+                                bcur_dmat* out) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    check_dtype(dtype);
+    if (!path || !out) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_load_bcur: null argument");
+    File fh;
+    fh.f = fopen(path, "rb");
+    if (!fh.f) fail(BCUR_E_PARSE, std::string("cannot open ") + path);
+    const BcurHeader h = read_bcur_header(fh.f, path);
+    const int64_t m = (int64_t)h.rows, n = (int64_t)h.cols;
+    if (ncols < 0) ncols = n - col0;
+    if (col0 < 0 || ncols < 1 || col0 + ncols > n)
+        fail(BCUR_E_OUT_OF_RANGE, "bcur_dmat_load_bcur: column range outside the file's " + std::to_string(n) + " columns");
+    // entry data must be complete (the reference reads all rows·cols and reports truncation)
+    const long long data0 = 4 + 16;
+    if (fseeko(fh.f, 0, SEEK_END) != 0) fail(BCUR_E_PARSE, std::string(path) + ": cannot seek");
+    const long long size = ftello(fh.f);
+    if (size < data0 + (long long)(m * n * 8)) fail(BCUR_E_PARSE, std::string(path) + ": truncated entry data");
+    bcur_dmat d = new_dmat(c, dtype, ncols, m);  // staged as its transpose's shape, fixed below
+    d->m = m;
+    d->n = ncols;
+    d->ld = std::max<int64_t>(m, 1);
+    const int64_t chunk_rows = std::max<int64_t>(1, std::min<int64_t>(m, ((int64_t)64 << 20) / (8 * ncols)));
+    const size_t chunk_bytes = (size_t)chunk_rows * ncols * 8;
+    void* pin[2] = {nullptr, nullptr};
+    cudaEvent_t done[2];
+    for (int b = 0; b < 2; ++b) {
+        CUDA_CHECK(cudaHostAlloc(&pin[b], chunk_bytes, cudaHostAllocDefault));
+        CUDA_CHECK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+    }
+    struct Cleanup {
+        void** pin;
+        cudaEvent_t* done;
+        ~Cleanup() {
+            for (int b = 0; b < 2; ++b) {
+                cudaEventSynchronize(done[b]);
+                cudaFreeHost(pin[b]);
+                cudaEventDestroy(done[b]);
+            }
+        }
+    } cleanup{pin, done};
+    try {
+        DevBuf stage(c, chunk_bytes), flag(c, 16);
+        CUDA_CHECK(cudaMemsetAsync(flag.ptr, 0, 4, c->stream));
+        int64_t r0 = 0;
+        for (int b = 0; r0 < m; r0 += chunk_rows, b ^= 1) {
+            const int64_t rr = std::min(chunk_rows, m - r0);
+            CUDA_CHECK(cudaEventSynchronize(done[b]));  // the copy that last used this staging buffer
+            char* dst = (char*)pin[b];
+            if (col0 == 0 && ncols == n) {
+                if (fseeko(fh.f, data0 + (long long)(r0 * n * 8), SEEK_SET) != 0 ||
+                    fread(dst, 8, (size_t)(rr * n), fh.f) != (size_t)(rr * n))
+                    fail(BCUR_E_PARSE, std::string(path) + ": truncated entry data");
+            } else {
+                for (int64_t i = 0; i < rr; ++i) {
+                    if (fseeko(fh.f, data0 + (long long)(((r0 + i) * n + col0) * 8), SEEK_SET) != 0 ||
+                        fread(dst + (size_t)i * ncols * 8, 8, (size_t)ncols, fh.f) != (size_t)ncols)
+                        fail(BCUR_E_PARSE, std::string(path) + ": truncated entry data");
+                }
+            }
+            CUDA_CHECK(cudaMemcpyAsync(stage.ptr, dst, (size_t)rr * ncols * 8, cudaMemcpyHostToDevice, c->stream));
+            CUDA_CHECK(cudaEventRecord(done[b], c->stream));
+            ops::flag_nonfinite(c, stage.as<double>(), rr * ncols, flag.as<unsigned int>());
+            // the chunk is row-major rr × ncols = column-major ncols × rr: transpose into rows r0.. of A
+            ops::transpose(c, stage.ptr, BCUR_F64, ncols, rr, ncols, (char*)d->ptr + (size_t)r0 * dtype_size(dtype),
+                           dtype, d->ld);
+        }
+        unsigned int bad = 0;
+        CUDA_CHECK(cudaMemcpyAsync(&bad, flag.ptr, 4, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (bad) fail(BCUR_E_PARSE, std::string(path) + ": matrix contains NaN or Inf");  // make_dense → require_finite
+    } catch (...) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(d->ptr);
+        delete d;
+        throw;
+    }
+    *out = d;
+    API_END
+}
+
+bcur_status bcur_dmat_save_bcur(bcur_ctx ctx, bcur_dmat a, const char* path) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (!path) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_save_bcur: null path");
+    if (d->m < 1 || d->n < 1) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_save_bcur: empty matrix");
+    // row-major fp64 on the device (transpose + widen), then one download
+    DevBuf rm(c, (size_t)d->m * d->n * 8);
+    ops::transpose(c, d->ptr, d->dtype, d->m, d->n, d->ld, rm.ptr, BCUR_F64, d->n);
+    std::vector<double> host((size_t)d->m * d->n);
+    CUDA_CHECK(cudaMemcpyAsync(host.data(), rm.ptr, host.size() * 8, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    File fh;
+    fh.f = fopen(path, "wb");
+    if (!fh.f) fail(BCUR_E_PARSE, std::string("cannot write ") + path);
+    const uint64_t rows = (uint64_t)d->m, cols = (uint64_t)d->n;
+    if (fwrite("BCUR", 1, 4, fh.f) != 4 || fwrite(&rows, 8, 1, fh.f) != 1 || fwrite(&cols, 8, 1, fh.f) != 1 ||
+        fwrite(host.data(), 8, host.size(), fh.f) != host.size())
+        fail(BCUR_E_PARSE, std::string("cannot write ") + path);
+    API_END
+}
+
 bcur_status bcur_dmat_download(bcur_ctx ctx, bcur_dmat a, void* host, int64_t ld_host) {
     API_BEGIN
     Ctx* c = C(ctx);

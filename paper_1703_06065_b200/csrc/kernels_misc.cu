@@ -29,6 +29,13 @@ __global__ void k_transpose(const TS* __restrict__ src, int64_t m, int64_t n, in
     }
 }
 
+__global__ void k_count_nonfinite(const double* __restrict__ x, int64_t count, unsigned int* __restrict__ flag) {
+    bool bad = false;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(x[e]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 __global__ void k_fill(double* p, int64_t count, double v) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e < count) p[e] = v;
@@ -112,6 +119,13 @@ void transpose(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t l
 
 void transpose_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd) {
     transpose(c, src, dt, m, n, lds, dst, BCUR_F64, ldd);
+}
+
+void flag_nonfinite(Ctx* c, const double* x, int64_t count, unsigned int* d_flag) {
+    if (count <= 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>((count + 255) / 256, 4LL * c->sm_count);
+    k_count_nonfinite<<<g, 256, 0, c->stream>>>(x, count, d_flag);
+    LAUNCH_CHECK(c);
 }
 
 void fill_f64(Ctx* c, double* p, int64_t count, double v) {

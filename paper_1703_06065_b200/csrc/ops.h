@@ -141,6 +141,8 @@ void transpose(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t l
 void zero_lower(Ctx* c, double* x, int64_t w, int64_t ld);
 void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
 void fill_f64(Ctx* c, double* p, int64_t count, double v);
+// *d_flag |= 1 when any of x[0..count) is NaN or Inf (the loader's require_finite)
+void flag_nonfinite(Ctx* c, const double* x, int64_t count, unsigned int* d_flag);
 void axpy_neg(Ctx* c, const double* x, double* y, int64_t n);  // y -= x
 void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*n*/);
 void scale_rows(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*m*/);

@@ -103,6 +103,26 @@ int main() {
     o.p = 5;
     o.q = 0;
     o.mode = SamplingMode::without_replacement;
+    // ---- .bcur round trip through the device (io.cpp:105-137; save_matrix_binary)
+    {
+        const std::string path = "/tmp/bcur_cpp_api_roundtrip.bcur";
+        A.save_binary(path);
+        auto B = DeviceMatrix::load_binary(path);
+        auto shard = DeviceMatrix::load_binary(path, BCUR_F64, 100, 50);
+        const Matrix ha = A.download(), hb = B.download(), hs = shard.download();
+        bool same = hb.rows() == 500 && hb.cols() == 2000 && hs.cols() == 50;
+        for (Index j = 0; j < 2000 && same; ++j)
+            for (Index i = 0; i < 500; ++i) same = same && ha(i, j) == hb(i, j) && (j < 100 || j >= 150 || hs(i, j - 100) == ha(i, j));
+        EXPECT(same);
+        bool threw = false;
+        try {
+            DeviceMatrix::load_binary("/tmp/bcur_cpp_api_absent.bcur");
+        } catch (const ParseError&) {
+            threw = true;
+        }
+        EXPECT(threw);
+        std::remove(path.c_str());
+    }
     auto res = block_css(A, BlockPartition::equal_blocks(2000, 20), 10, 10, rng, o);
     EXPECT(res.c.rows() == 500 && res.c.cols() == 200);
     std::printf("{\"blocks\": [");
