@@ -163,6 +163,30 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
  *                          A·X, m % 8 == 0 for AᵀX) */
 enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4, BCUR_PRODUCT_H3 = 8 };
 bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
+/* blockcur.cpp:54-109 block_cur — the reference's default Algorithm 1 (row_sampling =
+ * uniform): R = the caller's row draws of A (sampler.cpp:54-95, drawn from its Rng; scaled
+ * unless distinct), approximate block leverage of R (all rank(R) right singular vectors,
+ * leverage.cpp:155-164), g block draws with the caller's uniforms (one per draw, drawn after
+ * the rows), C = A·S, W = R·S, U = W⁺ (matcore.cpp:85-91), and ‖A − C·U·R‖_F for U and for
+ * its rank-k truncation (matcore.cpp:81-83).  Single device.  u_out (nullable) receives U,
+ * c × r with ld c (c = the drawn blocks' total width; size it for the g widest blocks). */
+typedef struct {
+    int64_t row;
+    double probability; /* 1/m */
+    double scale;       /* 1/sqrt(r·p) (applied when scaled_rows) */
+} bcur_row_draw;
+typedef struct {
+    double abs_err_u;   /* ‖A − C·U·R‖_F      (metrics_u) */
+    double abs_err_uk;  /* ‖A − C·U_k·R‖_F    (metrics_uk) */
+    double a_norm;      /* ‖A‖_F */
+    int64_t rank_r;     /* rank(R) = the scores' normalizer */
+    int64_t rank_w;     /* numerical rank of W */
+} bcur_alg1_report;
+bcur_status bcur_block_cur_alg1(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, int64_t k,
+                                const bcur_row_draw* rows, int64_t r, int scaled_rows, int64_t g, int block_mode,
+                                const double* uniforms, double* scores_out, double* normalizer_out,
+                                bcur_block_draw* draws_out, double* margins_out, double* u_out,
+                                bcur_alg1_report* report);
 /* io.cpp:105-137 load_matrix_binary / save_matrix_binary: the reference's ".bcur" format
  * (magic "BCUR", u64 rows, u64 cols, f64 row-major).  The loader streams row chunks through
  * pinned staging into a column-major device matrix of the requested dtype; columns

@@ -963,6 +963,101 @@ CONFIGS = {
 }
 
 
+# ------------------------------------------------------------------ Algorithm 1
+# The reference's default decomposition (blockcur.cpp:54-109): uniform rows → R, approximate
+# block leverage of R (leverage.cpp:155-164), g blocks → C = A·S and W = R·S, U = W⁺
+# (matcore.cpp:85-91), metrics for U and its rank-k truncation (matcore.cpp:81-83).
+
+@dataclass
+class RowDraw:
+    row: int
+    probability: float
+    scale: float
+
+
+def draw_rows(m: int, r: int, rng: Rng) -> List[RowDraw]:  # sampler.cpp:54-71
+    if r < 1 or m < 1:
+        raise ValueError("draw_rows: m and r must be >= 1")
+    p = 1.0 / m
+    scale = 1.0 / math.sqrt(r * p)
+    return [RowDraw(rng.below(m), p, scale) for _ in range(r)]
+
+
+def draw_rows_distinct(m: int, r: int, rng: Rng) -> List[RowDraw]:  # sampler.cpp:73-95
+    if r < 1 or m < 1 or r > m:
+        raise ValueError("draw_rows_distinct: need 1 <= r <= m")
+    pool = list(range(m))
+    p = 1.0 / m
+    scale = 1.0 / math.sqrt(r * p)
+    out = []
+    for t in range(r):
+        pick = rng.below(m - t)
+        pool[t + pick], pool[t] = pool[t], pool[t + pick]
+        out.append(RowDraw(pool[t], p, scale))
+    return out
+
+
+def svd_ranked(a: np.ndarray):
+    """matcore.cpp:39-56: thin SVD truncated at rank_tolerance."""
+    u, s, vt = np.linalg.svd(a, full_matrices=False)
+    if s.size == 0:
+        return u[:, :0], s[:0], vt[:0]
+    tol = rank_tolerance(a.shape[0], a.shape[1], s[0])
+    r = int(np.sum((s > tol) & (s > 0)))
+    return u[:, :r], s[:r], vt[:r]
+
+
+def approx_block_leverage(r: np.ndarray, part: BlockPartition) -> ScoreVector:  # leverage.cpp:155-164
+    if r.shape[1] != part.n:
+        raise DimensionMismatch("approx_block_leverage: partition size does not match R columns")
+    if not np.any(r):
+        raise ZeroMatrix("approx_block_leverage: R is identically zero")
+    _, _, vt = svd_ranked(np.asarray(r, dtype=np.float64))
+    return block_leverage(vt.T, part, check=False)
+
+
+def best_rank_k(a: np.ndarray, k: int) -> np.ndarray:  # matcore.cpp:81-83
+    u, s, vt = svd_ranked(np.asarray(a, dtype=np.float64))
+    kk = min(k, s.size)
+    return (u[:, :kk] * s[:kk]) @ vt[:kk]
+
+
+@dataclass
+class Alg1Result:
+    rows: List[RowDraw]
+    scores: ScoreVector
+    plan: SamplingPlan
+    u: np.ndarray
+    abs_err_u: float
+    abs_err_uk: float
+    a_norm: float
+
+
+def block_cur_alg1(a: np.ndarray, part: BlockPartition, k: int, r: int, g: int, rng: Rng,
+                   block_mode: str = WITH_REPLACEMENT, distinct_rows: bool = False) -> Alg1Result:
+    """blockcur.cpp:54-109 with row_sampling = uniform (the reference default)."""
+    m, n = a.shape
+    if k < 1 or k > min(m, n):
+        raise ValueError("block_cur: need 1 <= k <= min(m, n)")
+    if r < 1 or g < 1:
+        raise ValueError("block_cur: r and g must be >= 1")
+    if n != part.n:
+        raise DimensionMismatch("block_cur: partition does not match A columns")
+    a64 = np.asarray(a, dtype=np.float64)
+    rows = draw_rows_distinct(m, r, rng) if distinct_rows else draw_rows(m, r, rng)
+    rm = np.stack([a64[d.row] * (1.0 if distinct_rows else d.scale) for d in rows])  # materialize_rows
+    if not np.any(rm):
+        raise DegenerateR("block_cur: sampled row matrix R is identically zero")
+    scores = approx_block_leverage(rm, part)
+    plan = draw_blocks(scores.distribution(), g, block_mode, rng)
+    c = materialize_columns(a64, part, plan)
+    w = materialize_columns(rm, part, plan)
+    u = pinv(w)
+    err_u, _ = error_report(a64, c, u, rm)
+    err_uk, _ = error_report(a64, c, best_rank_k(u, k), rm)
+    return Alg1Result(rows, scores, plan, u, err_u, err_uk, float(np.linalg.norm(a64)))
+
+
 # ------------------------------------------------------------------ .bcur files
 # io.cpp:105-137 load_matrix_binary and save_matrix_binary (io.hpp:13-14): magic "BCUR",
 # little-endian u64 rows, u64 cols, then rows·cols f64 row-major; make_dense's finiteness check

@@ -26,6 +26,15 @@ P_i64 = C.POINTER(i64)
 P_dbl = C.POINTER(dbl)
 
 
+class RowDrawC(C.Structure):
+    _fields_ = [("row", C.c_int64), ("probability", C.c_double), ("scale", C.c_double)]
+
+
+class Alg1ReportC(C.Structure):
+    _fields_ = [("abs_err_u", C.c_double), ("abs_err_uk", C.c_double), ("a_norm", C.c_double),
+                ("rank_r", C.c_int64), ("rank_w", C.c_int64)]
+
+
 class BlockDrawC(C.Structure):
     _fields_ = [("block", i64), ("probability", dbl), ("scale", dbl)]
 
@@ -98,6 +107,9 @@ SIGNATURES = {
     "bcur_materialize_columns": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(BlockDrawC), i64, C.POINTER(vp)]),
     "bcur_materialize_row_blocks": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(BlockDrawC), i64, C.POINTER(vp)]),
     "bcur_error_report": (C.c_int, [vp, vp, vp, vp, vp, P_dbl, P_dbl]),
+    "bcur_block_cur_alg1": (C.c_int, [vp, vp, P_i64, i64, i64, C.POINTER(RowDrawC), i64, C.c_int, i64, C.c_int,
+                                      P_dbl, P_dbl, P_dbl, C.POINTER(BlockDrawC), P_dbl, P_dbl,
+                                      C.POINTER(Alg1ReportC)]),
     "bcur_block_css": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(OptionsC), P_dbl, P_dbl, P_dbl,
                                  C.POINTER(BlockDrawC), P_dbl, C.POINTER(ReportC)]),
     "bcur_greedy_select": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(OptionsC), C.POINTER(GreedyStepC), P_dbl,

@@ -714,6 +714,93 @@ def block_css(a, part: BlockPartition, k: int, g: int, rng: Rng, p: int = 5, q: 
                      "explicit" if rep.residual_path else "pythagoras", rep.orth_dev)
 
 
+# -------------------------------------------- Algorithm 1 (blockcur.cpp:54-109)
+@dataclass
+class RowDraw:
+    row: int
+    probability: float
+    scale: float
+
+
+def draw_rows(m: int, r: int, rng: Rng) -> List[RowDraw]:
+    """sampler.cpp:54-71: r uniform draws with replacement, one ``rng.below(m)`` each."""
+    if r < 1 or m < 1:
+        raise ValueError("draw_rows: m and r must be >= 1")
+    p = 1.0 / m
+    scale = 1.0 / math.sqrt(r * p)
+    return [RowDraw(rng.below(m), p, scale) for _ in range(r)]
+
+
+def draw_rows_distinct(m: int, r: int, rng: Rng) -> List[RowDraw]:
+    """sampler.cpp:73-95: partial Fisher–Yates over 0..m-1."""
+    if r < 1 or m < 1 or r > m:
+        raise ValueError("draw_rows_distinct: need 1 <= r <= m")
+    pool = list(range(m))
+    p = 1.0 / m
+    scale = 1.0 / math.sqrt(r * p)
+    out = []
+    for t in range(r):
+        pick = rng.below(m - t)
+        pool[t + pick], pool[t] = pool[t], pool[t + pick]
+        out.append(RowDraw(pool[t], p, scale))
+    return out
+
+
+@dataclass
+class CurResultAlg1:
+    rows: List[RowDraw]
+    scores: ScoreVector
+    block_plan: SamplingPlan
+    u: np.ndarray
+    abs_err_u: float
+    abs_err_uk: float
+    a_norm: float
+    rank_w: int
+
+    @property
+    def rel_to_a(self) -> float:
+        return self.abs_err_u / self.a_norm if self.a_norm > 0 else 0.0
+
+
+def block_cur_reference(a, part: BlockPartition, k: int, r: int, g: int, rng: Rng,
+                        block_mode: str = SamplingMode.with_replacement, distinct_rows: bool = False,
+                        ctx: Optional[Context] = None) -> CurResultAlg1:
+    """The reference's default block CUR (blockcur.cpp:54-109, row_sampling = uniform): the
+    rows are drawn here from ``rng`` exactly as draw_rows / draw_rows_distinct, then one
+    uniform per block draw; everything else (approximate block leverage of R, C, W,
+    U = W⁺, both error metrics) runs on the GPU."""
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    m = d.shape[0]
+    if k < 1 or k > min(d.shape):
+        raise ValueError("block_cur: need 1 <= k <= min(m, n)")
+    if r < 1 or g < 1:
+        raise ValueError("block_cur: r and g must be >= 1")
+    rows = draw_rows_distinct(m, r, rng) if distinct_rows else draw_rows(m, r, rng)
+    rc = (L.RowDrawC * r)(*[L.RowDrawC(x.row, x.probability, x.scale) for x in rows])
+    u = rng.uniforms(g)
+    off, offp = _off_ptr(part)
+    G = part.num_blocks()
+    scores = np.empty(G, dtype=np.float64)
+    norm = C.c_double()
+    draws = (L.BlockDrawC * g)()
+    marg = np.zeros(g, dtype=np.float64)
+    rep = L.Alg1ReportC()
+    # U is c × r with c = the drawn blocks' total width (≤ the g widest blocks); the library
+    # writes it contiguously (ld = c) at the start of this buffer
+    cap = sum(sorted((part.width(b) for b in range(G)), reverse=True)[:g]) * r
+    ubuf = np.empty(max(cap, 1), dtype=np.float64)
+    _check(L.lib.bcur_block_cur_alg1(ctx.handle, d.handle, offp, G, k, rc, r, 0 if distinct_rows else 1, g,
+                                     _mode_code(block_mode), u.ctypes.data_as(L.P_dbl), scores.ctypes.data_as(L.P_dbl),
+                                     C.byref(norm), draws, marg.ctypes.data_as(L.P_dbl), ubuf.ctypes.data_as(L.P_dbl),
+                                     C.byref(rep)))
+    plan = _plan_from_c(draws, g, block_mode, rng.seed(), marg)
+    cc = sum(part.width(dr.block) for dr in plan.draws)
+    um = ubuf[:cc * r].reshape((cc, r), order="F").copy(order="F")
+    return CurResultAlg1(rows, ScoreVector(scores, norm.value), plan, um, rep.abs_err_u, rep.abs_err_uk, rep.a_norm,
+                         rep.rank_w)
+
+
 @dataclass
 class GreedyStep:
     block: int

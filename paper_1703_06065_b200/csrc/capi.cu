@@ -883,6 +883,33 @@ bcur_status bcur_greedy_select(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets
     API_END
 }
 
+bcur_status bcur_block_cur_alg1(bcur_ctx ctx, bcur_dmat a, const int64_t* offsets, int64_t G, int64_t k,
+                                const bcur_row_draw* rows, int64_t r, int scaled_rows, int64_t g, int block_mode,
+                                const double* uniforms, double* scores_out, double* normalizer_out,
+                                bcur_block_draw* draws_out, double* margins_out, double* u_out,
+                                bcur_alg1_report* report) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* A = M(a);
+    if (!rows || !uniforms || !draws_out || !report) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: null argument");
+    if (block_mode != BCUR_WITH_REPLACEMENT && block_mode != BCUR_WITHOUT_REPLACEMENT)
+        fail(BCUR_E_INVALID_ARGUMENT, "bad block sampling mode");
+    check_partition(offsets, G, A->n, "block_cur");
+    Alg1Out o;
+    block_cur_alg1(c, A, offsets, G, k, rows, r, scaled_rows != 0, g, block_mode, uniforms, &o);
+    if (scores_out) std::memcpy(scores_out, o.scores.data(), G * sizeof(double));
+    if (normalizer_out) *normalizer_out = o.normalizer;
+    std::memcpy(draws_out, o.draws.data(), g * sizeof(bcur_block_draw));
+    if (margins_out) std::memcpy(margins_out, o.margins.data(), g * sizeof(double));
+    if (u_out) {
+        CUDA_CHECK(cudaMemcpyAsync(u_out, o.u.p(), (size_t)o.u.m * o.u.n * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream));
+        c->sync();
+    }
+    *report = o.rep;
+    API_END
+}
+
 bcur_status bcur_block_cur(bcur_ctx ctx, bcur_dmat a, const int64_t* col_offsets, int64_t Gc,
                            const int64_t* row_offsets, int64_t Gr, const bcur_options* opt, const double* uniforms,
                            double* col_scores, double* row_scores, bcur_block_draw* col_draws,

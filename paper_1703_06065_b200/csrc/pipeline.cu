@@ -915,6 +915,301 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     out->rep.orth_dev = sub.orth_dev;
 }
 
+// ------------------------------------------------------- Algorithm 1 (reference)
+// Thin SVD pieces of a small fp64 matrix X (rows × cols) through the Gram of its shorter
+// side (eig on the device): σ descending, the rank by rank_tolerance (matcore.cpp:35-49),
+// and the singular vectors on the Gram side.  right = true: Gram XᵀX (cols × cols), vectors
+// are V; else XXᵀ, vectors are U.
+struct SmallSvd {
+    Mat64 vec;  // side × rank
+    std::vector<double> sigma;
+    int64_t rank = 0;
+};
+static SmallSvd small_svd(Ctx* c, const double* X, int64_t rows, int64_t cols, int64_t ldx, bool right,
+                          double tol_override = -1.0) {
+    const int64_t w = right ? cols : rows;
+    if (w > 512) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: the small SVD side must be <= 512");
+    Mat64 Gm(c, w, w), lam(c, w, 1), V(c, w, w);
+    if (right)
+        gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, Gm.p(), Gm.ld);
+    else
+        gemm(c, OP_N, OP_T, w, w, cols, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, Gm.p(), Gm.ld);
+    sym_eig(c, Gm.p(), w, Gm.ld, lam.p(), V.p());
+    std::vector<double> lh(w);
+    d2h(c, lh.data(), lam.p(), w);
+    SmallSvd out;
+    for (double l : lh) out.sigma.push_back(std::sqrt(std::max(l, 0.0)));
+    const double tol = tol_override >= 0.0 ? tol_override
+                       : out.sigma.empty() ? 0.0 : 1e-12 * (double)std::max(rows, cols) * out.sigma[0];
+    while (out.rank < w && out.sigma[out.rank] > tol && out.sigma[out.rank] > 0.0) ++out.rank;
+    out.vec = Mat64(c, w, std::max<int64_t>(out.rank, 1));
+    if (out.rank > 0) copy_f64(c, V.p(), w, out.rank, V.ld, out.vec.p(), out.vec.ld);
+    return out;
+}
+
+// X⁺ (cols × rows) of a small fp64 X and its numerical rank (matcore.cpp:85-91).  Full rank
+// (the usual case): CholQR2 of X's tall orientation, tall = Q·T, so X⁺ = T⁻¹·Qᵀ (X tall) or
+// Q·T⁻ᵀ (Xᵀ tall) — forward error ~u·κ(X).  Otherwise the Gram of the shorter side with the
+// reference's rank rule (error ~u·κ(X)² on the kept range).
+// tol_scale: the rank cut is tol_scale·σ₁ (default 1e-12·max(rows, cols), matcore.cpp:35-37)
+static int64_t pinv_small(Ctx* c, const double* Xp, int64_t rows, int64_t cols, int64_t ldx, Mat64* out,
+                          double tol_scale = -1.0) {
+    *out = Mat64(c, cols, rows);
+    const bool right = cols <= rows;
+    {
+        const int64_t tall = std::max(rows, cols), wide = std::min(rows, cols);
+        Mat64 X(c, tall, wide), Q(c, tall, wide), T;
+        if (right) copy_f64(c, Xp, rows, cols, ldx, X.p(), X.ld);
+        else transpose(c, Xp, BCUR_F64, rows, cols, ldx, X.p(), BCUR_F64, X.ld);
+        int path = -1;
+        const int64_t got = orth(c, X.p(), tall, wide, X.ld, -1.0, BCUR_F64, Q.p(), Q.ld, false, &T, &path);
+        if (path == 0 && got == wide && T.m == wide && T.n == wide) {
+            Mat64 Ti(c, wide, wide);
+            tri_inv_any(c, T.p(), wide, Ti.p(), nullptr);
+            if (right)
+                gemm(c, OP_N, OP_T, cols, rows, cols, 1.0, Ti.p(), BCUR_F64, Ti.ld, Q.p(), BCUR_F64, Q.ld, 0.0,
+                     out->p(), out->ld);
+            else
+                gemm(c, OP_N, OP_T, cols, rows, rows, 1.0, Q.p(), BCUR_F64, Q.ld, Ti.p(), BCUR_F64, Ti.ld, 0.0,
+                     out->p(), out->ld);
+            return wide;
+        }
+    }
+    SmallSvd sw = small_svd(c, Xp, rows, cols, ldx, right);
+    if (tol_scale >= 0.0 && !sw.sigma.empty()) {  // re-cut with the caller's tolerance
+        const double tol = tol_scale * sw.sigma[0];
+        int64_t k = 0;
+        while (k < (int64_t)sw.sigma.size() && sw.sigma[k] > tol && sw.sigma[k] > 0.0) ++k;
+        sw.rank = std::min<int64_t>(k, sw.vec.n);
+    }
+    if (sw.rank == 0) {
+        fill_f64(c, out->p(), cols * rows, 0.0);
+        return 0;
+    }
+    const int64_t rw = sw.rank, side = right ? cols : rows;
+    std::vector<double> inv2(rw);
+    for (int64_t i = 0; i < rw; ++i) inv2[i] = 1.0 / (sw.sigma[i] * sw.sigma[i]);
+    Mat64 d2(c, rw, 1), Vs(c, side, rw), P(c, side, side);
+    h2d(c, d2.p(), inv2.data(), rw);
+    copy_f64(c, sw.vec.p(), side, rw, sw.vec.ld, Vs.p(), Vs.ld);
+    scale_columns(c, Vs.p(), side, rw, Vs.ld, d2.p());
+    gemm(c, OP_N, OP_T, side, side, rw, 1.0, Vs.p(), BCUR_F64, Vs.ld, sw.vec.p(), BCUR_F64, sw.vec.ld, 0.0, P.p(), P.ld);
+    if (right)  // X⁺ = (XᵀX)⁺ Xᵀ
+        gemm(c, OP_N, OP_T, cols, rows, cols, 1.0, P.p(), BCUR_F64, P.ld, Xp, BCUR_F64, ldx, 0.0, out->p(), out->ld);
+    else        // X⁺ = Xᵀ (XXᵀ)⁺
+        gemm(c, OP_T, OP_N, cols, rows, rows, 1.0, Xp, BCUR_F64, ldx, P.p(), BCUR_F64, P.ld, 0.0, out->p(), out->ld);
+    return rw;
+}
+
+void block_cur_alg1(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, int64_t k, const bcur_row_draw* rows,
+                    int64_t r, bool scaled_rows, int64_t g, int block_mode, const double* uniforms, Alg1Out* out) {
+    const int64_t m = a->m, n = a->n;
+    if (c->comm.world > 1) fail(BCUR_E_INVALID_ARGUMENT, "block_cur (Algorithm 1): single device");
+    if (k < 1 || k > std::min(m, n)) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: need 1 <= k <= min(m, n)");
+    if (r < 1 || g < 1) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: r and g must be >= 1");
+    Shard s = shard_of(a, offsets, G);
+    std::vector<double> bn2;
+    Mat64 dbn;
+    const double a2 = block_norms(c, a, s, &bn2, &dbn);
+    if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: matrix contains NaN or Inf");
+    // R = the drawn rows (materialize_rows, sampler.cpp:186-202): unit row blocks of A
+    for (int64_t t = 0; t < r; ++t)
+        if (rows[t].row < 0 || rows[t].row >= m) fail(BCUR_E_DIMENSION_MISMATCH, "materialize_rows: row index out of range");
+    Mat64 R(c, r, n);
+    {
+        std::vector<int64_t> unit(m + 1), dst(r);
+        for (int64_t i = 0; i <= m; ++i) unit[i] = i;
+        std::vector<bcur_block_draw> dr(r);
+        for (int64_t t = 0; t < r; ++t) {
+            dr[t] = {rows[t].row, rows[t].probability, scaled_rows ? rows[t].scale : 1.0};
+            dst[t] = t;
+        }
+        DevBuf du(c, unit.size() * sizeof(int64_t)), dd(c, dr.size() * sizeof(bcur_block_draw)), ds(c, r * sizeof(int64_t));
+        h2d(c, du.as<int64_t>(), unit.data(), unit.size());
+        h2d(c, dd.as<bcur_block_draw>(), dr.data(), dr.size());
+        h2d(c, ds.as<int64_t>(), dst.data(), dst.size());
+        gather_blocks(c, a->ptr, a->dtype, m, n, a->ld, du.as<int64_t>(), dd.as<bcur_block_draw>(), ds.as<int64_t>(), r, 1,
+                      1, R.p(), BCUR_F64, R.ld);
+    }
+    // approximate block leverage of R (leverage.cpp:155-164): all rank(R) right singular
+    // vectors.  The row space and rank of R are those of its distinct rows (a row drawn
+    // twice with replacement is an exact copy); the Gram of the distinct rows cannot show
+    // the copies' zero singular values as rounding-level ones (~1e-8·σ₁ through a Gram,
+    // above the 1e-12·max(r, n)·σ₁ rank cut).  σ₁ of the cut is R's own.
+    std::vector<int64_t> urow;
+    for (int64_t t = 0; t < r; ++t)
+        if (std::find(urow.begin(), urow.end(), rows[t].row) == urow.end()) urow.push_back(rows[t].row);
+    const int64_t ru = (int64_t)urow.size();
+    Mat64 Ru(c, ru, n);
+    {
+        std::vector<int64_t> unit(m + 1), dst(ru);
+        for (int64_t i = 0; i <= m; ++i) unit[i] = i;
+        std::vector<bcur_block_draw> dr(ru);
+        for (int64_t t = 0; t < ru; ++t) {
+            dr[t] = {urow[t], 0.0, scaled_rows ? rows[0].scale : 1.0};
+            dst[t] = t;
+        }
+        DevBuf du(c, unit.size() * sizeof(int64_t)), dd(c, dr.size() * sizeof(bcur_block_draw)), ds(c, ru * sizeof(int64_t));
+        h2d(c, du.as<int64_t>(), unit.data(), unit.size());
+        h2d(c, dd.as<bcur_block_draw>(), dr.data(), dr.size());
+        h2d(c, ds.as<int64_t>(), dst.data(), dst.size());
+        gather_blocks(c, a->ptr, a->dtype, m, n, a->ld, du.as<int64_t>(), dd.as<bcur_block_draw>(), ds.as<int64_t>(), ru,
+                      1, 1, Ru.p(), BCUR_F64, Ru.ld);
+    }
+    double sigma1 = 0.0;
+    {
+        Mat64 Gr(c, r, r), lam(c, r, 1), Vr(c, r, r);
+        gemm(c, OP_N, OP_T, r, r, n, 1.0, R.p(), BCUR_F64, R.ld, R.p(), BCUR_F64, R.ld, 0.0, Gr.p(), Gr.ld);
+        sym_eig(c, Gr.p(), r, Gr.ld, lam.p(), Vr.p());
+        double l0 = 0.0;
+        d2h(c, &l0, lam.p(), 1);
+        sigma1 = std::sqrt(std::max(l0, 0.0));
+    }
+    SmallSvd sr = small_svd(c, Ru.p(), ru, n, Ru.ld, false, 1e-12 * (double)std::max(r, n) * sigma1);
+    if (sr.rank == 0 || !(sigma1 > 0.0))  // R·Rᵀ = 0 ⇔ R = 0 (blockcur.cpp:94-96)
+        fail(BCUR_E_DEGENERATE_R, "block_cur: sampled row matrix R is identically zero");
+    const int64_t rk = sr.rank;
+    Mat64 V(c, n, rk), Vraw(c, n, rk), Ws(c, ru, rk), dinv(c, rk, 1), sc(c, G, 1);
+    {
+        std::vector<double> inv(rk);
+        for (int64_t i = 0; i < rk; ++i) inv[i] = 1.0 / sr.sigma[i];
+        h2d(c, dinv.p(), inv.data(), rk);
+        copy_f64(c, sr.vec.p(), ru, rk, sr.vec.ld, Ws.p(), Ws.ld);
+        scale_columns(c, Ws.p(), ru, rk, Ws.ld, dinv.p());
+        gemm(c, OP_T, OP_N, n, rk, ru, 1.0, Ru.p(), BCUR_F64, Ru.ld, Ws.p(), BCUR_F64, Ws.ld, 0.0, Vraw.p(), Vraw.ld);
+        // Rᵀ·Ũ·Σ⁻¹ carries the Gram's κ(R)² error in its orthonormality, not in its span (the
+        // row space): CholQR2 of it gives the right-singular subspace to fp64 accuracy, and
+        // block leverage depends on the subspace only
+        const int64_t got = orth(c, Vraw.p(), n, rk, Vraw.ld, -1.0, BCUR_F64, V.p(), V.ld, false, nullptr, nullptr);
+        if (got != rk) {
+            std::string sv;
+            for (int64_t i = 0; i < (int64_t)sr.sigma.size(); ++i) sv += " " + std::to_string(sr.sigma[i]);
+            fail(BCUR_E_ITERATION_FAILURE, "block_cur: row-space basis lost rank (" + std::to_string(got) + " of " +
+                                               std::to_string(rk) + "; sigma" + sv + ")");
+        }
+    }
+    block_scores(c, s, V, n, sc.p());
+    out->scores.resize(G);
+    d2h(c, out->scores.data(), sc.p(), G);
+    out->normalizer = (double)rk;
+    draw_on_device(c, sc.p(), G, g, block_mode, uniforms, &out->draws, &out->margins);
+    // C = A·S (m × cc), scaled (materialize_columns); W = R·S enters through its distinct part
+    int64_t cc = 0;
+    std::vector<int64_t> dst;
+    for (auto& d : out->draws) {
+        dst.push_back(cc);
+        cc += offsets[d.block + 1] - offsets[d.block];
+    }
+    Mat64 C(c, m, cc);
+    {
+        DevBuf dd(c, out->draws.size() * sizeof(bcur_block_draw)), ds(c, dst.size() * sizeof(int64_t));
+        h2d(c, dd.as<bcur_block_draw>(), out->draws.data(), out->draws.size());
+        h2d(c, ds.as<int64_t>(), dst.data(), dst.size());
+        gather_blocks(c, a->ptr, a->dtype, m, n, a->ld, s.d_local.as<int64_t>(), dd.as<bcur_block_draw>(),
+                      ds.as<int64_t>(), g, 0, 1, C.p(), BCUR_F64, C.ld);
+    }
+    // U = W⁺ (matcore.cpp:85-91).  W's repeated rows (a row drawn twice) and repeated column
+    // blocks (a block drawn twice with replacement) are exact copies: W = P·W_u·Qᵀ with P, Q
+    // 0/1 selections.  With D_r, D_c the multiplicities, P·D_r^-½ and Q·D_c^-½ have orthonormal
+    // columns, so W = (P·D_r^-½)·X·(Q·D_c^-½)ᵀ with X = D_r^½·W_u·D_c^½ and, exactly,
+    // W⁺ = Q·D_c^-½ · X⁺ · D_r^-½·Pᵀ — same singular values, same rank rule.  (A Gram of W
+    // itself would show the copies' zero singular values as ~1e-8·σ₁ ones.)
+    std::vector<int64_t> ublk;
+    for (auto& d : out->draws)
+        if (std::find(ublk.begin(), ublk.end(), d.block) == ublk.end()) ublk.push_back(d.block);
+    int64_t cu = 0;
+    std::vector<int64_t> ustart;
+    for (int64_t b : ublk) {
+        ustart.push_back(cu);
+        cu += offsets[b + 1] - offsets[b];
+    }
+    Mat64 Wu(c, ru, cu);
+    {
+        std::vector<bcur_block_draw> ud;
+        for (int64_t b : ublk)
+            for (auto& d : out->draws)
+                if (d.block == b) {
+                    ud.push_back(d);
+                    break;
+                }
+        DevBuf dd(c, ud.size() * sizeof(bcur_block_draw)), ds(c, ustart.size() * sizeof(int64_t));
+        h2d(c, dd.as<bcur_block_draw>(), ud.data(), ud.size());
+        h2d(c, ds.as<int64_t>(), ustart.data(), ustart.size());
+        gather_blocks(c, Ru.p(), BCUR_F64, ru, n, Ru.ld, s.d_local.as<int64_t>(), dd.as<bcur_block_draw>(),
+                      ds.as<int64_t>(), (int64_t)ud.size(), 0, 1, Wu.p(), BCUR_F64, Wu.ld);
+    }
+    std::vector<double> mrow(ru, 0.0), mcol(cu, 0.0);
+    for (int64_t t = 0; t < r; ++t) mrow[std::find(urow.begin(), urow.end(), rows[t].row) - urow.begin()] += 1.0;
+    for (auto& d : out->draws) {
+        const int64_t ui = std::find(ublk.begin(), ublk.end(), d.block) - ublk.begin();
+        for (int64_t x = 0; x < offsets[d.block + 1] - offsets[d.block]; ++x) mcol[ustart[ui] + x] += 1.0;
+    }
+    {
+        std::vector<double> sr_(ru), sc_(cu);
+        for (int64_t i = 0; i < ru; ++i) sr_[i] = std::sqrt(mrow[i]);
+        for (int64_t j = 0; j < cu; ++j) sc_[j] = std::sqrt(mcol[j]);
+        Mat64 dr(c, ru, 1), dc(c, cu, 1);
+        h2d(c, dr.p(), sr_.data(), ru);
+        h2d(c, dc.p(), sc_.data(), cu);
+        scale_rows(c, Wu.p(), ru, cu, Wu.ld, dr.p());
+        scale_columns(c, Wu.p(), ru, cu, Wu.ld, dc.p());
+    }
+    Mat64 Wup;  // X⁺ (cu × ru), rank cut of W's own shape
+    out->rep.rank_w = pinv_small(c, Wu.p(), ru, cu, Wu.ld, &Wup, 1e-12 * (double)std::max(r, cc));
+    out->u = Mat64(c, cc, r);
+    {
+        // Qs (cc × cu): column j of C → its distinct column, weight 1/multiplicity of its block;
+        // Ps (ru × r): distinct row u → drawn row t, weight 1/multiplicity of the row
+        std::vector<double> qs((size_t)cc * cu, 0.0), ps((size_t)ru * r, 0.0);
+        int64_t j = 0;
+        for (auto& d : out->draws) {
+            const int64_t w = offsets[d.block + 1] - offsets[d.block];
+            const int64_t ui = std::find(ublk.begin(), ublk.end(), d.block) - ublk.begin();
+            for (int64_t x = 0; x < w; ++x, ++j)
+                qs[(size_t)j + (size_t)(ustart[ui] + x) * cc] = 1.0 / std::sqrt(mcol[ustart[ui] + x]);
+        }
+        for (int64_t t = 0; t < r; ++t) {
+            const int64_t ui = std::find(urow.begin(), urow.end(), rows[t].row) - urow.begin();
+            ps[(size_t)ui + (size_t)t * ru] = 1.0 / std::sqrt(mrow[ui]);
+        }
+        Mat64 Qs(c, cc, cu), Ps(c, ru, r), T(c, cu, r);
+        h2d(c, Qs.p(), qs.data(), qs.size());
+        h2d(c, Ps.p(), ps.data(), ps.size());
+        gemm(c, OP_N, OP_N, cu, r, ru, 1.0, Wup.p(), BCUR_F64, Wup.ld, Ps.p(), BCUR_F64, Ps.ld, 0.0, T.p(), T.ld);
+        gemm(c, OP_N, OP_N, cc, r, cu, 1.0, Qs.p(), BCUR_F64, Qs.ld, T.p(), BCUR_F64, T.ld, 0.0, out->u.p(),
+             out->u.ld);
+    }
+    // ‖A − C (U R)‖_F explicitly (error_report, blockcur.cpp:33-52), for U and U_k
+    auto resid = [&](const Mat64& U) {
+        Mat64 X(c, cc, n), tot(c, 1, 1);
+        gemm(c, OP_N, OP_N, cc, n, r, 1.0, U.p(), BCUR_F64, U.ld, R.p(), BCUR_F64, R.ld, 0.0, X.p(), X.ld);
+        gemm_resid_sumsq(c, OP_N, OP_N, m, n, cc, C.p(), BCUR_F64, C.ld, X.p(), BCUR_F64, X.ld, a->ptr, a->dtype, a->ld,
+                         tot.p());
+        double h = 0.0;
+        d2h(c, &h, tot.p(), 1);
+        return std::sqrt(std::max(h, 0.0));
+    };
+    out->rep.abs_err_u = resid(out->u);
+    // U_k = best_rank_k(U, k) = U·V_k·V_kᵀ with V_k the top-k right singular vectors of U
+    {
+        SmallSvd su = small_svd(c, out->u.p(), cc, r, out->u.ld, true);
+        const int64_t kk = std::min<int64_t>(k, su.rank);
+        Mat64 Uk(c, cc, r);
+        if (kk == 0) {
+            fill_f64(c, Uk.p(), cc * r, 0.0);
+        } else {
+            Mat64 Pk(c, r, r);
+            gemm(c, OP_N, OP_T, r, r, kk, 1.0, su.vec.p(), BCUR_F64, su.vec.ld, su.vec.p(), BCUR_F64, su.vec.ld, 0.0,
+                 Pk.p(), Pk.ld);
+            gemm(c, OP_N, OP_N, cc, r, r, 1.0, out->u.p(), BCUR_F64, out->u.ld, Pk.p(), BCUR_F64, Pk.ld, 0.0, Uk.p(),
+                 Uk.ld);
+        }
+        out->rep.abs_err_uk = resid(Uk);
+    }
+    out->rep.a_norm = std::sqrt(a2);
+    out->rep.rank_r = rk;
+}
+
 // ---------------------------------------------------------------- greedy
 void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, GreedyOut* out) {
     if (o.g < 1 || o.g > G) fail(BCUR_E_INVALID_ARGUMENT, "greedy_select: need 1 <= g <= number of blocks");

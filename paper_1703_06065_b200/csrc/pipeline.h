@@ -66,6 +66,14 @@ struct RoundedA {
     bool has_lo() const { return ok() && interleaved; }
 };
 
+struct Alg1Out {
+    std::vector<double> scores, margins;
+    double normalizer = 0.0;
+    std::vector<bcur_block_draw> draws;
+    Mat64 u;  // c × r
+    bcur_alg1_report rep{};
+};
+
 Shard shard_of(const DMat* a, const int64_t* offsets, int64_t G);
 void allreduce(Ctx* c, double* d, int64_t count);
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
@@ -75,6 +83,8 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
 void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, const double* uniforms,
                CssOut* out);
 void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, GreedyOut* out);
+void block_cur_alg1(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, int64_t k, const bcur_row_draw* rows,
+                    int64_t r, bool scaled_rows, int64_t g, int block_mode, const double* uniforms, Alg1Out* out);
 void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int64_t* roff, int64_t Gr,
                const bcur_options& o, const double* uniforms, bool want_u, CurOut* out);
 
