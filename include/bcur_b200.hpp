@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstddef>
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <optional>
 #include <span>
@@ -446,6 +447,107 @@ inline ErrorReport error_report(const Matrix& a, const Matrix& c, const Matrix& 
     rep.k = k;
     rep.variant = variant;
     return rep;
+}
+
+// ------------------------------ blockcur.hpp:36-76 — the reference's Algorithm 1
+enum class RowSampling { uniform, leverage };
+struct RowDraw {
+    Index row;
+    double probability, scale;
+};
+struct RowPlan {
+    std::vector<RowDraw> draws;
+    Index source_rows = 0;
+    SamplingMode mode = SamplingMode::with_replacement;
+    std::uint64_t seed = 0;
+    Index num_draws() const { return static_cast<Index>(draws.size()); }
+};
+// sampler.cpp:54-95 — uniform row draws from the caller's Rng (one below() per draw)
+inline RowPlan draw_rows(Index m, Index r, Rng& rng) {
+    if (r < 1) throw std::invalid_argument("draw_rows: r must be >= 1");
+    if (m < 1) throw std::invalid_argument("draw_rows: m must be >= 1");
+    RowPlan plan{{}, m, SamplingMode::with_replacement, rng.seed()};
+    const double p = 1.0 / static_cast<double>(m), scale = 1.0 / std::sqrt(static_cast<double>(r) * p);
+    for (Index t = 0; t < r; ++t) plan.draws.push_back({static_cast<Index>(rng.below(static_cast<std::uint64_t>(m))), p, scale});
+    return plan;
+}
+inline RowPlan draw_rows_distinct(Index m, Index r, Rng& rng) {
+    if (r < 1 || m < 1) throw std::invalid_argument("draw_rows_distinct: m and r must be >= 1");
+    if (r > m) throw std::invalid_argument("draw_rows_distinct: r must be <= m");
+    std::vector<Index> pool(static_cast<std::size_t>(m));
+    for (Index i = 0; i < m; ++i) pool[static_cast<std::size_t>(i)] = i;
+    RowPlan plan{{}, m, SamplingMode::without_replacement, rng.seed()};
+    const double p = 1.0 / static_cast<double>(m), scale = 1.0 / std::sqrt(static_cast<double>(r) * p);
+    for (Index t = 0; t < r; ++t) {
+        const auto pick = static_cast<Index>(rng.below(static_cast<std::uint64_t>(m - t)));
+        std::swap(pool[static_cast<std::size_t>(t + pick)], pool[static_cast<std::size_t>(t)]);
+        plan.draws.push_back({pool[static_cast<std::size_t>(t)], p, scale});
+    }
+    return plan;
+}
+struct CurOptions {
+    SamplingMode block_mode = SamplingMode::with_replacement;
+    RowSampling row_sampling = RowSampling::uniform;  // leverage rows: not on this path
+    bool distinct_rows = false;
+};
+struct CurResult {  // C, R and W stay on the device: materialize_columns / rows on demand
+    Matrix u;       // c × r, U = W⁺
+    RowPlan row_plan;
+    SamplingPlan block_plan;
+    ScoreVector block_scores;  // approximate block leverage of R (normalizer = rank R)
+    ErrorReport metrics_u, metrics_uk;
+    std::vector<double> trial_errors;
+};
+// blockcur.cpp:54-109 — rows → R, approximate block leverage of R, g blocks → C, W,
+// U = W⁺, ‖A − CUR‖_F for U and U_k; everything after the row draws runs on the GPU
+inline CurResult block_cur(const DeviceMatrix& a, const BlockPartition& part, Index k, Index r, Index g,
+                           const CurOptions& opts, Rng& rng, const ErrorBaseline* baseline = nullptr) {
+    if (opts.row_sampling != RowSampling::uniform)
+        throw std::invalid_argument("block_cur: leverage row sampling needs the exact SVD of A (not on this path)");
+    if (r < 1 || g < 1) throw std::invalid_argument("block_cur: r and g must be >= 1");
+    Device& dev = Device::current();
+    const Index m = a.rows();
+    CurResult res;
+    res.row_plan = opts.distinct_rows ? draw_rows_distinct(m, r, rng) : draw_rows(m, r, rng);
+    std::vector<bcur_row_draw> rd;
+    for (const RowDraw& d : res.row_plan.draws) rd.push_back({d.row, d.probability, d.scale});
+    const std::uint64_t seed = rng.seed();
+    const auto u = detail::uniforms(rng, g);
+    const auto off = part.offsets();
+    const Index G = part.num_blocks();
+    std::vector<Index> widths;
+    for (Index b = 0; b < G; ++b) widths.push_back(off[static_cast<std::size_t>(b) + 1] - off[static_cast<std::size_t>(b)]);
+    std::sort(widths.begin(), widths.end(), std::greater<Index>());
+    Index cap = 0;
+    for (Index t = 0; t < g && t < G; ++t) cap += widths[static_cast<std::size_t>(t)];
+    std::vector<double> ubuf(static_cast<std::size_t>(std::max<Index>(cap * r, 1)));
+    res.block_scores.scores = Vector(G);
+    std::vector<bcur_block_draw> d(static_cast<std::size_t>(g));
+    std::vector<double> margins(static_cast<std::size_t>(g));
+    bcur_alg1_report rep{};
+    detail::check(bcur_block_cur_alg1(dev.handle(), a.handle(), off.data(), G, k,
+                                      rd.data(), r, opts.distinct_rows ? 0 : 1, g, detail::mode_code(opts.block_mode),
+                                      u.data(), res.block_scores.scores.data(), &res.block_scores.normalizer, d.data(),
+                                      margins.data(), ubuf.data(), &rep));
+    res.block_plan = detail::plan_from(d, margins, opts.block_mode, seed);
+    Index cc = 0;
+    for (const auto& x : d) cc += off[static_cast<std::size_t>(x.block) + 1] - off[static_cast<std::size_t>(x.block)];
+    res.u = Matrix(cc, r);
+    std::copy(ubuf.begin(), ubuf.begin() + cc * r, res.u.data());
+    for (ErrorReport* e : {&res.metrics_u, &res.metrics_uk}) {
+        e->abs_err = e == &res.metrics_u ? rep.abs_err_u : rep.abs_err_uk;
+        e->rel_to_a = rep.a_norm > 0.0 ? e->abs_err / rep.a_norm : 0.0;
+        if (baseline && baseline->k == k && baseline->best_k_residual >= 1e-12)
+            e->rel_to_best_k = e->abs_err / baseline->best_k_residual;
+        e->k = k;
+        e->variant = e == &res.metrics_u ? UVariant::full : UVariant::rank_k;
+    }
+    res.trial_errors = {res.metrics_u.abs_err};
+    return res;
+}
+inline CurResult block_cur(const Matrix& a, const BlockPartition& part, Index k, Index r, Index g,
+                           const CurOptions& opts, Rng& rng, const ErrorBaseline* baseline = nullptr) {
+    return block_cur(DeviceMatrix::upload(a), part, k, r, g, opts, rng, baseline);
 }
 
 // ----------------------------------------------------------- sketch.hpp:32-39

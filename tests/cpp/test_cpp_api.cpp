@@ -125,6 +125,15 @@ int main() {
     }
     auto res = block_css(A, BlockPartition::equal_blocks(2000, 20), 10, 10, rng, o);
     EXPECT(res.c.rows() == 500 && res.c.cols() == 200);
+    // ---- the reference's Algorithm 1 (blockcur.cpp:54-109) through the mirror
+    {
+        Rng rng2(1);
+        CurOptions co;
+        auto cur = block_cur(A, BlockPartition::equal_blocks(2000, 20), 10, 60, 10, co, rng2);
+        EXPECT(cur.u.rows() == 200 && cur.u.cols() == 60 && cur.row_plan.num_draws() == 60);
+        EXPECT(cur.metrics_u.abs_err >= 0.0 && cur.metrics_u.rel_to_a < 1.0 && cur.metrics_uk.abs_err >= 0.0);
+        EXPECT(cur.block_scores.normalizer >= 1.0 && cur.block_plan.num_draws() == 10);
+    }
     std::printf("{\"blocks\": [");
     for (Index t = 0; t < res.plan.num_draws(); ++t) std::printf("%s%td", t ? ", " : "", res.plan.draws[t].block);
     std::printf("], \"abs_err\": %.17g, \"a_norm\": %.17g, \"normalizer\": %.17g, \"scores\": [", res.projection_error,
