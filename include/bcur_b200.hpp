@@ -549,6 +549,20 @@ inline CurResult block_cur(const Matrix& a, const BlockPartition& part, Index k,
                            const CurOptions& opts, Rng& rng, const ErrorBaseline* baseline = nullptr) {
     return block_cur(DeviceMatrix::upload(a), part, k, r, g, opts, rng, baseline);
 }
+// blockcur.cpp:111-133 — t independent trials on one Rng stream, the lowest ‖A − CUR‖ kept
+inline CurResult block_cur_boosted(const DeviceMatrix& a, const BlockPartition& part, Index k, Index r, Index g,
+                                   Index t, const CurOptions& opts, Rng& rng, const ErrorBaseline* baseline = nullptr) {
+    if (t < 1) throw std::invalid_argument("block_cur_boosted: t must be >= 1");
+    CurResult best;
+    std::vector<double> errors;
+    for (Index trial = 0; trial < t; ++trial) {
+        CurResult cur = block_cur(a, part, k, r, g, opts, rng, baseline);
+        errors.push_back(cur.metrics_u.abs_err);
+        if (trial == 0 || cur.metrics_u.abs_err < best.metrics_u.abs_err) best = std::move(cur);
+    }
+    best.trial_errors = std::move(errors);
+    return best;
+}
 
 // ----------------------------------------------------------- sketch.hpp:32-39
 struct CssOptions {

@@ -1058,6 +1058,17 @@ def block_cur_alg1(a: np.ndarray, part: BlockPartition, k: int, r: int, g: int, 
     return Alg1Result(rows, scores, plan, u, err_u, err_uk, float(np.linalg.norm(a64)))
 
 
+def block_cur_alg1_boosted(a, part, k, r, g, t, rng, block_mode=WITH_REPLACEMENT, distinct_rows=False):
+    """blockcur.cpp:111-133."""
+    best, errors = None, []
+    for _ in range(t):
+        cur = block_cur_alg1(a, part, k, r, g, rng, block_mode, distinct_rows)
+        errors.append(cur.abs_err_u)
+        if best is None or cur.abs_err_u < best.abs_err_u:
+            best = cur
+    return best, errors
+
+
 # ------------------------------------------------------------------ .bcur files
 # io.cpp:105-137 load_matrix_binary and save_matrix_binary (io.hpp:13-14): magic "BCUR",
 # little-endian u64 rows, u64 cols, then rows·cols f64 row-major; make_dense's finiteness check

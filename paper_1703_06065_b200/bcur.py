@@ -801,6 +801,24 @@ def block_cur_reference(a, part: BlockPartition, k: int, r: int, g: int, rng: Rn
                          rep.rank_w)
 
 
+def block_cur_reference_boosted(a, part: BlockPartition, k: int, r: int, g: int, t: int, rng: Rng,
+                                block_mode: str = SamplingMode.with_replacement, distinct_rows: bool = False,
+                                ctx: Optional[Context] = None):
+    """blockcur.cpp:111-133: t trials on one Rng stream, the lowest ‖A − CUR‖_F kept;
+    returns (best, [abs_err of every trial])."""
+    if t < 1:
+        raise ValueError("block_cur_boosted: t must be >= 1")
+    ctx = ctx or default_context()
+    d = _dev(a, ctx)
+    best, errors = None, []
+    for _ in range(t):
+        cur = block_cur_reference(d, part, k, r, g, rng, block_mode, distinct_rows, ctx)
+        errors.append(cur.abs_err_u)
+        if best is None or cur.abs_err_u < best.abs_err_u:
+            best = cur
+    return best, errors
+
+
 @dataclass
 class GreedyStep:
     block: int

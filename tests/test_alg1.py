@@ -61,3 +61,13 @@ def test_alg1_degenerate_r(B):
     part = B.BlockPartition.equal_blocks(40, 10)
     with pytest.raises(B.DegenerateR):
         B.block_cur_reference(np.zeros((10, 40)), part, 2, 3, 2, B.Rng(0))
+
+
+@pytest.mark.gpu
+def test_alg1_boosted_matches_oracle(B):
+    a = lowrank(200, 900, 10, 11, 1e-3, np.float64)
+    pg, po = B.BlockPartition.equal_blocks(900, 30), O.BlockPartition.equal_blocks(900, 30)
+    got, ge = B.block_cur_reference_boosted(a, pg, 6, 30, 4, 3, B.Rng(12))
+    ref, re_ = O.block_cur_alg1_boosted(a, po, 6, 30, 4, 3, O.Rng(12))
+    np.testing.assert_allclose(ge, re_, rtol=1e-6, atol=1e-9 * ref.a_norm)
+    assert got.block_plan.blocks() == ref.plan.blocks()
