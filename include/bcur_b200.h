@@ -138,6 +138,12 @@ bcur_status bcur_block_sq_norms(bcur_ctx ctx, bcur_dmat a, const int64_t* offset
  * tol < 0 → 1e-8 for fp64 input, 1e-4 for fp32). */
 bcur_status bcur_block_leverage(bcur_ctx ctx, bcur_dmat v_k, const int64_t* offsets, int64_t G, double tol,
                                 double* scores, double* normalizer);
+/* leverage.cpp:123-153 score diagnostics: per-block stable ranks ‖V_g‖_F²/‖V_g‖_2² of the row
+ * blocks of V_k (k ≤ 64), their minimum (block_stable_rank) and the incoherence
+ * (m/k)·max_i ‖U_kᵀe_i‖² (u_k nullable).  Outputs are written before a zero-mass block is
+ * reported as BCUR_E_ZERO_BLOCK (its stable rank is NaN). */
+bcur_status bcur_block_diagnostics(bcur_ctx ctx, bcur_dmat v_k, bcur_dmat u_k, const int64_t* offsets, int64_t G,
+                                   double* stable_ranks, double* block_stable_rank, double* incoherence);
 /* leverage.cpp:100-106 column_leverage */
 bcur_status bcur_column_leverage(bcur_ctx ctx, bcur_dmat v_k, double tol, double* scores, double* normalizer);
 /* N1: randomized range finder replacing truncate(svd(a), k) (matcore.cpp:39-69).

@@ -1069,6 +1069,30 @@ def block_cur_alg1_boosted(a, part, k, r, g, t, rng, block_mode=WITH_REPLACEMENT
     return best, errors
 
 
+# ------------------------------------------------------------------ score diagnostics
+def column_block_stable_ranks(m_: np.ndarray, part: BlockPartition) -> np.ndarray:  # leverage.cpp:123-139
+    out = np.empty(part.num_blocks())
+    for g in range(part.num_blocks()):
+        b, e = part.offsets[g], part.offsets[g + 1]
+        slab = np.asarray(m_[:, b:e], dtype=np.float64)
+        fro2 = float(np.sum(slab * slab))
+        if not fro2 > 0.0:
+            raise ZeroBlock(f"column_block_stable_ranks: block {g} has zero Frobenius mass")
+        out[g] = fro2 / float(np.linalg.norm(slab, 2)) ** 2
+    return out
+
+
+def block_stable_rank(v_k: np.ndarray, part: BlockPartition) -> float:  # leverage.cpp:141-146
+    require_orthonormal(v_k, 1e-8, "block_stable_rank")
+    return float(column_block_stable_ranks(np.asarray(v_k).T, part).min())
+
+
+def incoherence(u_k: np.ndarray) -> float:  # leverage.cpp:148-153
+    require_orthonormal(u_k, 1e-8, "incoherence")
+    u = np.asarray(u_k, dtype=np.float64)
+    return u.shape[0] / u.shape[1] * float(np.max(np.sum(u * u, axis=1)))
+
+
 # ------------------------------------------------------------------ .bcur files
 # io.cpp:105-137 load_matrix_binary and save_matrix_binary (io.hpp:13-14): magic "BCUR",
 # little-endian u64 rows, u64 cols, then rows·cols f64 row-major; make_dense's finiteness check

@@ -110,6 +110,7 @@ SIGNATURES = {
     "bcur_block_cur_alg1": (C.c_int, [vp, vp, P_i64, i64, i64, C.POINTER(RowDrawC), i64, C.c_int, i64, C.c_int,
                                       P_dbl, P_dbl, P_dbl, C.POINTER(BlockDrawC), P_dbl, P_dbl,
                                       C.POINTER(Alg1ReportC)]),
+    "bcur_block_diagnostics": (C.c_int, [vp, vp, vp, P_i64, i64, P_dbl, P_dbl, P_dbl]),
     "bcur_block_css": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(OptionsC), P_dbl, P_dbl, P_dbl,
                                  C.POINTER(BlockDrawC), P_dbl, C.POINTER(ReportC)]),
     "bcur_greedy_select": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(OptionsC), C.POINTER(GreedyStepC), P_dbl,

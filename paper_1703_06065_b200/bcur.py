@@ -714,6 +714,22 @@ def block_css(a, part: BlockPartition, k: int, g: int, rng: Rng, p: int = 5, q: 
                      "explicit" if rep.residual_path else "pythagoras", rep.orth_dev)
 
 
+def block_diagnostics(v_k, u_k, part: BlockPartition, ctx: Optional[Context] = None):
+    """leverage.cpp:123-153 on the GPU: (per-block stable ranks of V_kᵀ, their minimum =
+    block_stable_rank, incoherence of U_k).  A zero-mass block raises ZeroBlock like the
+    reference (``bcur scores`` then reports NaN)."""
+    ctx = ctx or default_context()
+    dv = _dev(v_k, ctx)
+    du = _dev(u_k, ctx) if u_k is not None else None
+    off, offp = _off_ptr(part)
+    G = part.num_blocks()
+    sr = np.empty(G, dtype=np.float64)
+    alpha, mu = C.c_double(), C.c_double()
+    _check(L.lib.bcur_block_diagnostics(ctx.handle, dv.handle, du.handle if du is not None else None, offp, G,
+                                        sr.ctypes.data_as(L.P_dbl), C.byref(alpha), C.byref(mu)))
+    return sr, alpha.value, (mu.value if du is not None else float("nan"))
+
+
 # -------------------------------------------- Algorithm 1 (blockcur.cpp:54-109)
 @dataclass
 class RowDraw:

@@ -47,7 +47,32 @@ def _compile(src, verbose):
     return obj
 
 
+CLI_SRC = os.path.join(HERE, "..", "tools", "bcur_b200_cli.cpp")
+CLI = os.path.join(HERE, "..", "tools", "bcur_b200")
+
+
+def build_cli(verbose: bool = False) -> str:
+    """tools/bcur_b200: the reference CLI's decompose / scores (+ css) over the library."""
+    deps = [CLI_SRC, LIB, os.path.join(HERE, "..", "include", "bcur_b200.hpp")]
+    if os.path.exists(CLI) and os.path.getmtime(CLI) >= max(os.path.getmtime(d) for d in deps):
+        return CLI
+    cmd = ["g++", "-std=c++20", "-O2", "-I", os.path.join(HERE, "..", "include"), CLI_SRC, "-L", HERE, "-lbcur_b200",
+           "-Wl,-rpath,$ORIGIN/../paper_1703_06065_b200", "-o", CLI]
+    if verbose:
+        print(" ".join(cmd), flush=True)
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"CLI build failed:\n{r.stdout}\n{r.stderr}")
+    return CLI
+
+
 def build(verbose: bool = False) -> str:
+    lib = build_lib(verbose)
+    build_cli(verbose)
+    return lib
+
+
+def build_lib(verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
     srcs = sources()
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:

@@ -635,6 +635,45 @@ bcur_status bcur_block_leverage(bcur_ctx ctx, bcur_dmat v_k, const int64_t* offs
     API_END
 }
 
+bcur_status bcur_block_diagnostics(bcur_ctx ctx, bcur_dmat v_k, bcur_dmat u_k, const int64_t* offsets, int64_t G,
+                                   double* stable_ranks, double* block_stable_rank, double* incoherence) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* V = M(v_k);
+    if (V->dtype != BCUR_F64) fail(BCUR_E_INVALID_ARGUMENT, "block_stable_rank: V_k must be fp64");
+    check_partition(offsets, G, V->m, "block_stable_rank");
+    require_orthonormal(c, V, 1e-6, "block_stable_rank");  // range-finder bases of fp32 A: ~1e-7
+    DevBuf doff(c, (G + 1) * sizeof(int64_t)), fro(c, G * sizeof(double)), spec(c, G * sizeof(double));
+    CUDA_CHECK(cudaMemcpyAsync(doff.ptr, offsets, (G + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c->stream));
+    ops::block_spectral(c, (const double*)V->ptr, V->ld, V->n, doff.as<int64_t>(), G, fro.as<double>(), spec.as<double>());
+    std::vector<double> hf(G), hs(G);
+    CUDA_CHECK(cudaMemcpyAsync(hf.data(), fro.ptr, G * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(hs.data(), spec.ptr, G * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    double mn = INFINITY;
+    bool zero = false;
+    for (int64_t g = 0; g < G; ++g) {
+        const double sr = hf[g] > 0.0 ? hf[g] / hs[g] : NAN;  // leverage.cpp:128-139: ZeroBlock
+        if (!(hf[g] > 0.0)) zero = true;
+        if (stable_ranks) stable_ranks[g] = sr;
+        mn = std::min(mn, sr);
+    }
+    if (block_stable_rank) *block_stable_rank = zero ? NAN : mn;
+    if (incoherence && u_k) {  // leverage.cpp:148-153: (m/k)·max_i ‖U_kᵀ e_i‖²
+        DMat* U = M(u_k);
+        if (U->dtype != BCUR_F64) fail(BCUR_E_INVALID_ARGUMENT, "incoherence: U_k must be fp64");
+        require_orthonormal(c, U, 1e-6, "incoherence");
+        DevBuf mx(c, sizeof(double));
+        ops::max_row_sumsq(c, (const double*)U->ptr, U->m, U->ld, U->n, mx.as<double>());
+        double h = 0.0;
+        CUDA_CHECK(cudaMemcpyAsync(&h, mx.ptr, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        *incoherence = (double)U->m / (double)U->n * h;
+    }
+    if (zero) fail(BCUR_E_ZERO_BLOCK, "column_block_stable_ranks: a block has zero Frobenius mass");
+    API_END
+}
+
 bcur_status bcur_column_leverage(bcur_ctx ctx, bcur_dmat v_k, double tol, double* scores, double* normalizer) {
     API_BEGIN
     Ctx* c = C(ctx);

@@ -280,6 +280,72 @@ __global__ void k_max_dev_identity(const double* __restrict__ g, int w, int64_t 
     if (lane == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
 }
 
+// Per column block g of M (rows × n, ld): ‖M_g‖_F² and ‖M_g‖_2² (leverage.cpp:123-139
+// column_block_stable_ranks on V_kᵀ, i.e. M = V_k with blocks of rows — here M's rows are V_k's
+// rows, each block a w × k slab).  One CTA per block: the k × k Gram of the slab in shared
+// memory, then power iteration with a Rayleigh quotient (exact to rounding even when the top
+// eigenvalues cluster: the quotient error is the residual weight times the top gap).
+constexpr int BS_T = 256, BS_KMAX = 64;
+__global__ void __launch_bounds__(BS_T) k_block_spectral(const double* __restrict__ v, int64_t ld, int k,
+                                                          const int64_t* __restrict__ off, double* __restrict__ fro2,
+                                                          double* __restrict__ spec2) {
+    __shared__ double Gm[BS_KMAX * BS_KMAX];
+    __shared__ double x[BS_KMAX], y[BS_KMAX], red[BS_T / 32];
+    const int64_t g = blockIdx.x, j0 = off[g], w = off[g + 1] - off[g];
+    double f = 0.0;
+    for (int e = threadIdx.x; e < k * k; e += BS_T) {
+        const int a = e % k, b = e / k;
+        double sacc = 0.0;
+        for (int64_t i = 0; i < w; ++i) sacc = fma(v[j0 + i + a * ld], v[j0 + i + b * ld], sacc);
+        Gm[e] = sacc;
+        if (a == b) f += sacc;
+    }
+    f = block_sum(f);
+    __syncthreads();
+    if (threadIdx.x == 0) fro2[g] = f;
+    for (int a = threadIdx.x; a < k; a += BS_T) x[a] = 1.0 / sqrt((double)k) * (1.0 + 0.01 * a);  // generic start
+    __syncthreads();
+    double lam = 0.0;
+    for (int it = 0; it < 2000; ++it) {
+        for (int a = threadIdx.x; a < k; a += BS_T) {
+            double sacc = 0.0;
+            for (int b = 0; b < k; ++b) sacc = fma(Gm[a + b * k], x[b], sacc);
+            y[a] = sacc;
+        }
+        __syncthreads();
+        double num = 0.0, den = 0.0;  // Rayleigh quotient xᵀGx / xᵀx and ‖y‖
+        for (int a = 0; a < k; ++a) {
+            num = fma(x[a], y[a], num);
+            den = fma(y[a], y[a], den);
+        }
+        double xx = 0.0;
+        for (int a = 0; a < k; ++a) xx = fma(x[a], x[a], xx);
+        const double rq = xx > 0.0 ? num / xx : 0.0;
+        const double ny = sqrt(den);
+        __syncthreads();
+        for (int a = threadIdx.x; a < k; a += BS_T) x[a] = ny > 0.0 ? y[a] / ny : 0.0;
+        __syncthreads();
+        const bool done = it > 8 && fabs(rq - lam) <= 1e-16 * fabs(rq);
+        lam = rq;
+        if (done || !(ny > 0.0)) break;
+    }
+    if (threadIdx.x == 0) spec2[g] = lam;
+}
+
+// max over rows of Σ_c u(i, c)² (incoherence of U_k)
+__global__ void k_max_row_sumsq(const double* __restrict__ u, int64_t m, int64_t ld, int k,
+                                unsigned long long* __restrict__ out) {
+    double mx = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        double sacc = 0.0;
+        for (int c = 0; c < k; ++c) sacc = fma(u[i + c * ld], u[i + c * ld], sacc);
+        mx = fmax(mx, sacc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(mx));
+}
+
 }  // namespace
 
 namespace ops {
@@ -339,6 +405,22 @@ void max_dev_identity(Ctx* c, const double* g, int64_t w, int64_t ld, double* d_
     if (w <= 0) return;
     const int blocks = (int)std::min<int64_t>((w + 7) / 8, 4LL * c->sm_count);
     k_max_dev_identity<<<blocks, 256, 0, c->stream>>>(g, (int)w, ld, reinterpret_cast<unsigned long long*>(d_out));
+    LAUNCH_CHECK(c);
+}
+
+void block_spectral(Ctx* c, const double* v, int64_t ld, int64_t k, const int64_t* d_offsets, int64_t G, double* d_fro2,
+                    double* d_spec2) {
+    if (k > BS_KMAX) fail(BCUR_E_INVALID_ARGUMENT, "block_stable_rank: k <= 64 on this path");
+    if (G <= 0 || k <= 0) return;
+    k_block_spectral<<<(unsigned)G, BS_T, 0, c->stream>>>(v, ld, (int)k, d_offsets, d_fro2, d_spec2);
+    LAUNCH_CHECK(c);
+}
+
+void max_row_sumsq(Ctx* c, const double* u, int64_t m, int64_t ld, int64_t k, double* d_out) {
+    CUDA_CHECK(cudaMemsetAsync(d_out, 0, sizeof(double), c->stream));
+    if (m <= 0 || k <= 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>((m + 255) / 256, 4LL * c->sm_count);
+    k_max_row_sumsq<<<g, 256, 0, c->stream>>>(u, m, ld, (int)k, reinterpret_cast<unsigned long long*>(d_out));
     LAUNCH_CHECK(c);
 }
 

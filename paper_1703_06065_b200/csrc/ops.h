@@ -26,6 +26,11 @@ void row_sumsq_blocks(Ctx* c, const void* v, int dt, int64_t n, int64_t k, int64
 void segment_sum(Ctx* c, const double* x, const int64_t* d_offsets, int64_t G, double* d_out);
 // max |G - I| over the upper triangle of a symmetric w×w fp64 matrix → d_out[0]
 void max_dev_identity(Ctx* c, const double* g, int64_t w, int64_t ld, double* d_out);
+// per row block g of V (n × k, k ≤ 64): ‖V_g‖_F² and ‖V_g‖_2² (stable-rank diagnostics)
+void block_spectral(Ctx* c, const double* v, int64_t ld, int64_t k, const int64_t* d_offsets, int64_t G, double* d_fro2,
+                    double* d_spec2);
+// max_i Σ_c u(i, c)² → d_out[0]
+void max_row_sumsq(Ctx* c, const double* u, int64_t m, int64_t ld, int64_t k, double* d_out);
 // ordered sum of x[0..n) → d_out[0]
 void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out);
 

@@ -71,3 +71,25 @@ def test_alg1_boosted_matches_oracle(B):
     ref, re_ = O.block_cur_alg1_boosted(a, po, 6, 30, 4, 3, O.Rng(12))
     np.testing.assert_allclose(ge, re_, rtol=1e-6, atol=1e-9 * ref.a_norm)
     assert got.block_plan.blocks() == ref.plan.blocks()
+
+
+# ---- score diagnostics (leverage.cpp:123-153): block stable rank and incoherence
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,k,s", [(600, 10, 20), (2000, 50, 128), (777, 64, 100)])
+def test_block_diagnostics(B, n, k, s):
+    gen = np.random.default_rng(n + k)
+    v, _ = np.linalg.qr(gen.standard_normal((n, k)) * np.logspace(0, -1, k))
+    u, _ = np.linalg.qr(gen.standard_normal((3 * k, k)))
+    pg, po = B.BlockPartition.equal_blocks(n, s), O.BlockPartition.equal_blocks(n, s)
+    sr, alpha, mu = B.block_diagnostics(np.asfortranarray(v), np.asfortranarray(u), pg)
+    np.testing.assert_allclose(sr, O.column_block_stable_ranks(v.T, po), rtol=1e-10)
+    assert alpha == pytest.approx(O.block_stable_rank(v, po), rel=1e-10)
+    assert mu == pytest.approx(O.incoherence(u), rel=1e-12)
+
+
+@pytest.mark.gpu
+def test_block_diagnostics_zero_block(B):
+    v = np.zeros((40, 3))
+    v[:30, :] = np.linalg.qr(np.random.default_rng(0).standard_normal((30, 3)))[0]
+    with pytest.raises(B.ZeroBlock):
+        B.block_diagnostics(v, None, B.BlockPartition.equal_blocks(40, 10))
