@@ -1073,7 +1073,7 @@ def block_cur_alg1_boosted(a, part, k, r, g, t, rng, block_mode=WITH_REPLACEMENT
 def column_block_stable_ranks(m_: np.ndarray, part: BlockPartition) -> np.ndarray:  # leverage.cpp:123-139
     out = np.empty(part.num_blocks())
     for g in range(part.num_blocks()):
-        b, e = part.offsets[g], part.offsets[g + 1]
+        b, e = part.ranges[g]
         slab = np.asarray(m_[:, b:e], dtype=np.float64)
         fro2 = float(np.sum(slab * slab))
         if not fro2 > 0.0:
