@@ -710,14 +710,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// promo: L2 sector promotion.  256 B suits contiguous streams (the next K tile is adjacent);
+// reads of the hi half of the interleaved copy use 128 B, or every hi run would pull its lo
+// neighbour from DRAM as well.
 CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
                      const uint32_t* box, CUtensorMapSwizzle swz,
-                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32) {
+                     CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                     CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
     CUtensorMap m;
     uint32_t es[5] = {1, 1, 1, 1, 1};
     CUresult r = encode_fn()(&m, dt, rank, const_cast<void*>(base), dims, strides_bytes,
-                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                             box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(BCUR_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return m;
 }
@@ -1615,7 +1618,8 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     const uint32_t bA[4] = {64, 1, 1, BM};
     const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
     const uint32_t bX[2] = {BKH, BN};
-    CUtensorMap ta = make_map(A16, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap ta = make_map(A16, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                              interleaved ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
     CUtensorMap tx = make_map(x16_pre ? (const void*)x16_pre : x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     const int k_tiles = (int)((K + BKH - 1) / BKH);
