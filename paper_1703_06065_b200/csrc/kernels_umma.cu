@@ -292,6 +292,7 @@ struct Sched {
     int a_rn;  // X1: A already rounded to TF32 (no transform)
     int pf;    // A-tile L2 prefetch distance (stages)
     int x_il;  // H3: x_hi/x_lo come from one interleaved split (4-D map, part = hi|lo)
+    int bke;   // K elements per k-tile (32 tf32, 64 fp16): the triangular-X limit is in these units
 };
 // CTAs that have a tile in waves 0..w
 __device__ __forceinline__ unsigned int wave_arrivals(const Sched& sc, int w) {
@@ -322,10 +323,13 @@ __device__ __forceinline__ TileInfo tile_info(const Sched& sc, int t) {
         const int rr = r - g * gsz;
         ti.n_tile = first_n + rr % gn;
         ti.m_tile = rr / gn;
+        // triangular X: N tile j carries j + 1 diagonal blocks of K — walk the widest first so
+        // the persistent CTAs end together (longest-processing-time order)
+        if (sc.tri_x) ti.n_tile = sc.n_tiles - 1 - ti.n_tile;
     }
     ti.kt0 = ti.split * sc.kps;
     int kt1 = min(sc.k_tiles, ti.kt0 + sc.kps);
-    if (sc.tri_x) kt1 = min(kt1, ((ti.n_tile + 1) * NT * BN + BK - 1) / BK);
+    if (sc.tri_x) kt1 = min(kt1, ((ti.n_tile + 1) * NT * BN + sc.bke - 1) / sc.bke);
     ti.nk = max(kt1 - ti.kt0, 0);
     return ti;
 }
@@ -788,6 +792,7 @@ Sched make_sched(int m_tiles, int n_tiles, int splits, int k_tiles, int kps, boo
     sc.a_rn = 0;
     sc.pf = g_pf >= 0 ? g_pf : 12;
     sc.x_il = 0;
+    sc.bke = BK;
     return sc;
 }
 
@@ -1832,6 +1837,7 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     // stages of prefetch (57 MB of A in flight) dropped them to ~4 TB/s (L2 thrash)
     sc.pf = g_pf >= 0 ? g_pf : 0;
     sc.x_il = X.lo ? 0 : 1;
+    sc.bke = BKH;  // fp16 k-tiles: the diagonal limit of a triangular X in 64-row units (was 2× too far)
     const int* rexp = a_mn ? nullptr : ea;
     const int* cexp = X.exps;
     auto launch = [&](double* o, int64_t ldo_, double* prt, double al, double be) {
