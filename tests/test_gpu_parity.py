@@ -281,3 +281,12 @@ def test_blocked_factorization_widths(B, dt, m, n, s, g):
     got, ref = run_css(B, a, s, 30, 10, 1, g, O.WITHOUT_REPLACEMENT, 9)
     assert got.plan.blocks() == ref.plan.blocks()
     assert got.rank_c == g * s
+
+
+# fp32 shapes off the 64-row grid of the fp16 copy (TF32 fallbacks) and a whole-C basis whose
+# width is not a multiple of 64 with a ragged block (3×FP16 partial tiles)
+@pytest.mark.parametrize("m,n,s,g", [(1000, 3000, 100, 6), (2048, 1050, 100, 11)])
+def test_fp32_off_grid_shapes(B, m, n, s, g):
+    a = lowrank(m, n, 30, "pow:1", 1e-4, 13, np.float32)
+    got, ref = run_css(B, a, s, 20, 10, 1, g, O.WITHOUT_REPLACEMENT, 13)
+    assert got.plan.blocks() == ref.plan.blocks()
