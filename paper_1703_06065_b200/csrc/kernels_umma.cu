@@ -1410,7 +1410,7 @@ void split_x(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, 
 template <class T, bool IL>
 __global__ void __launch_bounds__(1024) k_split_f16(const T* __restrict__ x, int64_t K, int64_t ldx,
                                                    const int* __restrict__ fold, uint16_t* __restrict__ hi,
-                                                   uint16_t* __restrict__ lo, int* __restrict__ q) {
+                                                   uint16_t* __restrict__ lo, int* __restrict__ q, int64_t ldo) {
     const int64_t j = blockIdx.x;
     const T* col = x + j * ldx;
     double mx = 0.0;
@@ -1434,7 +1434,7 @@ __global__ void __launch_bounds__(1024) k_split_f16(const T* __restrict__ x, int
         const __half h = __double2half(v);
         const __half l = __double2half(v - (double)__half2float(h));
         // IL: the A-operand layout (block_sumsq's): per 64-row chunk [hi 64 | lo 64], 2K per column
-        const int64_t ih = IL ? j * 2 * K + (k >> 6) * 128 + (k & 63) : j * K + k;
+        const int64_t ih = IL ? j * 2 * K + (k >> 6) * 128 + (k & 63) : j * ldo + k;
         hi[ih] = *reinterpret_cast<const uint16_t*>(&h);
         (IL ? hi : lo)[IL ? ih + 64 : ih] = *reinterpret_cast<const uint16_t*>(&l);
     }
@@ -1735,19 +1735,20 @@ static unsigned split_threads(int64_t K, int64_t N, Ctx* c) {
 void split_f16(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, const int* fold, SplitF16* out) {
     out->K = K;
     out->N = N;
-    out->hi = DevBuf(c, (size_t)std::max<int64_t>(K * N, 1) * 2);
-    out->lo = DevBuf(c, (size_t)std::max<int64_t>(K * N, 1) * 2);
+    out->ld = (K + 7) / 8 * 8;
+    out->hi = DevBuf(c, (size_t)std::max<int64_t>(out->ld * N, 1) * 2);
+    out->lo = DevBuf(c, (size_t)std::max<int64_t>(out->ld * N, 1) * 2);
     out->exps = DevBuf(c, (size_t)std::max<int64_t>(N, 1) * sizeof(int));
     if (K <= 0 || N <= 0) return;
     ProfScope prof(c, "split_f16", 0.0, (double)K * N * (dtype_size(dtx) + 4));
     if (dtx == BCUR_F32)
         k_split_f16<float, false><<<(unsigned)N, split_threads(K, N, c), 0, c->stream>>>((const float*)x, K, ldx, fold,
                                                                      out->hi.as<uint16_t>(), out->lo.as<uint16_t>(),
-                                                                     out->exps.as<int>());
+                                                                     out->exps.as<int>(), out->ld);
     else
         k_split_f16<double, false><<<(unsigned)N, split_threads(K, N, c), 0, c->stream>>>((const double*)x, K, ldx, fold,
                                                                       out->hi.as<uint16_t>(), out->lo.as<uint16_t>(),
-                                                                      out->exps.as<int>());
+                                                                      out->exps.as<int>(), out->ld);
     LAUNCH_CHECK(c);
 }
 
@@ -1757,10 +1758,10 @@ void split_il_into(Ctx* c, const void* a, int dta, int64_t m, int64_t n, int64_t
     ProfScope prof(c, "split_f16", 0.0, (double)m * n * (dtype_size(dta) + 4));
     if (dta == BCUR_F32)
         k_split_f16<float, true><<<(unsigned)n, split_threads(m, n, c), 0, c->stream>>>((const float*)a, m, lda, nullptr, il, nullptr,
-                                                                    exps);
+                                                                    exps, 0);
     else
         k_split_f16<double, true><<<(unsigned)n, split_threads(m, n, c), 0, c->stream>>>((const double*)a, m, lda, nullptr, il, nullptr,
-                                                                     exps);
+                                                                     exps, 0);
     LAUNCH_CHECK(c);
 }
 
@@ -1814,8 +1815,10 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     const uint32_t bA[4] = {64, 1, 1, a_mn ? (uint32_t)BKH : (uint32_t)BM};
     CUtensorMap ta = make_map(AL, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     CUtensorMap th, tl;
-    if (X.lo) {  // separate hi, lo (K × N each, ld K)
-        const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)K * 2};
+    if (X.lo) {  // separate hi, lo (K × N each, ld X.ld or K)
+        const int64_t ldx = X.ld > 0 ? X.ld : K;
+        if ((ldx * 2) % 16 != 0) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: X leading dimension must be a multiple of 8");
+        const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)ldx * 2};
         const uint32_t bX[2] = {BKH, BN};
         th = make_map(X.hi, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
         tl = make_map(X.lo, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);

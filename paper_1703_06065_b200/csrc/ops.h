@@ -90,7 +90,7 @@ void umma_ax(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const vo
 // An fp16 hi + lo split of a K × N operand (ld K), column j scaled by 2^exps[j] (exact).
 struct SplitF16 {
     DevBuf hi, lo, exps;
-    int64_t K = 0, N = 0;
+    int64_t K = 0, N = 0, ld = 0;  // ld: K rounded up to 8 (TMA strides are multiples of 16 bytes)
 };
 // A non-owning view of one (a SplitF16, or — lo == nullptr — an interleaved split_il buffer
 // read as the K-major X operand, K % 64 == 0)
@@ -99,8 +99,11 @@ struct F16View {
     const uint16_t* lo;
     const int* exps;
     int64_t K, N;
+    int64_t ld = 0;  // separate hi/lo: leading dimension in halves (0: K)
 };
-inline F16View view(const SplitF16& s) { return {s.hi.as<uint16_t>(), s.lo.as<uint16_t>(), s.exps.as<int>(), s.K, s.N}; }
+inline F16View view(const SplitF16& s) {
+    return {s.hi.as<uint16_t>(), s.lo.as<uint16_t>(), s.exps.as<int>(), s.K, s.N, s.ld};
+}
 // fold (nullable, K ints): exponents subtracted from row k first (A·X with a scaled A)
 void split_f16(Ctx* c, const void* x, int dtx, int64_t K, int64_t N, int64_t ldx, const int* fold, SplitF16* out);
 // A (m × n, fp32/fp64, lda) → the interleaved hi/lo A operand (2m halves per column; m % 64 == 0)
