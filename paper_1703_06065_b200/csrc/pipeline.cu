@@ -114,8 +114,10 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     struct { int info; int pad; double mindiag, maxdiag; } hs;
     if (w <= 144) {
         cholesky_upper(c, G, w, ldg, R, w, st.as<int>(), st.as<double>() + 1);
+        // the inverse is enqueued before the status read (unused if the factorization failed),
+        // so the device does not idle through the host round trip between the two kernels
+        if (Rinv) tri_inv_any(c, R, w, Rinv, nullptr);
         d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
-        if (Rinv && hs.info == 0) tri_inv_any(c, R, w, Rinv, nullptr);
         return {hs.info, hs.mindiag, hs.maxdiag};
     }
     constexpr int64_t B = 128;
@@ -834,12 +836,14 @@ static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<dou
                 f16 && !ra->interleaved ? ra->il.as<uint16_t>() : nullptr, f16 ? ra->exps.as<int>() : nullptr,
                 f16 && ra->interleaved ? ra->il.as<uint16_t>() : nullptr);
     gather_blocks_vec(c, s, loc.p(), d_global->p());
-    bn2->assign(s.G, 0.0);
-    d2h(c, bn2->data(), d_global->p(), s.G);
     Mat64 tot(c, 1, 1);
     sum_vector(c, d_global->p(), s.G, tot.p());
+    // both reads in one round trip
+    bn2->assign(s.G, 0.0);
     double h = 0.0;
-    d2h(c, &h, tot.p(), 1);
+    CUDA_CHECK(cudaMemcpyAsync(bn2->data(), d_global->p(), s.G * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_CHECK(cudaMemcpyAsync(&h, tot.p(), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
     return h;
 }
 
