@@ -495,13 +495,24 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             const double a_ = partial ? 1.0 : alpha;
             const int ncol = min(DC, N - col0);
             const int re = (H3 && rexp && row < M) ? rexp[row] : 0;
+            // β ≠ 0: the old values are loaded 16 at a time before any store (one
+            // read-modify-write per column made each element a dependent load → store round
+            // trip through L2: the Q1 + Q1·(−F) correction ran at half the C·R⁻¹ rate)
+            constexpr int EB = 16;
 #pragma unroll
-            for (int j = 0; j < DC; ++j) {
-                double v = X3 ? (double)acc[j] + (double)cmp[X3 ? j : 0] : (double)acc[j];
-                if (H3) v *= exp2_int(-(re + ((cexp && j < ncol) ? cexp[col0 + j] : 0)));
-                if (j < ncol) {
-                    double* o = dst + (int64_t)(col0 + j) * stride;
-                    *o = plain ? a_ * v : fma(beta, *o, a_ * v);
+            for (int j0 = 0; j0 < DC; j0 += EB) {
+                double old[EB];
+#pragma unroll
+                for (int jj = 0; jj < EB; ++jj) {
+                    const int j = j0 + jj;
+                    old[jj] = (!plain && j < ncol) ? dst[(int64_t)(col0 + j) * stride] : 0.0;
+                }
+#pragma unroll
+                for (int jj = 0; jj < EB; ++jj) {
+                    const int j = j0 + jj;
+                    double v = X3 ? (double)acc[j] + (double)cmp[X3 ? j : 0] : (double)acc[j];
+                    if (H3) v *= exp2_int(-(re + ((cexp && j < ncol) ? cexp[col0 + j] : 0)));
+                    if (j < ncol) dst[(int64_t)(col0 + j) * stride] = plain ? a_ * v : fma(beta, old[jj], a_ * v);
                 }
             }
         }
