@@ -49,15 +49,5 @@ void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const doub
     c->launches++;
 }
 
-// B ← R⁻ᵀ·B in place, R upper triangular (M×M, ld ldr), B M×N (ld ldb): the panel solve of the
-// blocked Cholesky (block row k of R = R_kk⁻ᵀ × the updated trailing row), in place in R
-void cublas_dtrsm_left_upper_t(Ctx* c, int64_t M, int64_t N, const double* R, int64_t ldr, double* B, int64_t ldb) {
-    const double one = 1.0;
-    const cublasStatus_t st = cublasDtrsm(handle(c), CUBLAS_SIDE_LEFT, CUBLAS_FILL_MODE_UPPER, CUBLAS_OP_T,
-                                          CUBLAS_DIAG_NON_UNIT, (int)M, (int)N, &one, R, (int)ldr, B, (int)ldb);
-    if (st != CUBLAS_STATUS_SUCCESS) fail(BCUR_E_CUDA, "cublasDtrsm failed (" + std::to_string((int)st) + ")");
-    c->launches++;
-}
-
 }  // namespace ops
 }  // namespace bcur_b200

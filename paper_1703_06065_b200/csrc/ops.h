@@ -68,8 +68,6 @@ void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, con
 void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
                   int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 
-// B ← R⁻ᵀ·B in place (R upper M×M; B M×N)
-void cublas_dtrsm_left_upper_t(Ctx* c, int64_t M, int64_t N, const double* R, int64_t ldr, double* B, int64_t ldb);
 // C(upper) = alpha·AᵀA + beta·C(upper)  (A k×n)
 void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
                           double* C, int64_t ldc);
