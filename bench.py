@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 from paper_1703_06065_b200.configs import CONFIGS, spectrum  # noqa: E402
 
 METRIC = "Block-CUR decompositions/sec"
-TF32_MEASURED = 1094.4  # TF/s, tcgen05.mma kind::tf32 issue-rate microbenchmark (scratch/mma_rate.cu) on this pool's B200
+TF32_MEASURED = 1094.4  # TF/s, tcgen05.mma kind::tf32 issue-rate microbenchmark (microbench/mma_rate.cu) on this pool's B200
 UNIT = "decompositions/s"
 
 
@@ -104,6 +104,19 @@ def measured_peaks():
 
 
 # ------------------------------------------------------------ GPU workload
+def workload_config(name, cfg):
+    """The `config` object of both arms' lines (identical keys and values)."""
+    bytes_a = cfg["m"] * cfg["n"] * (4 if cfg["dtype"] == "f32" else 8)
+    out = {"workload": name, "m": cfg["m"], "n": cfg["n"], "dtype": cfg["dtype"], "block_width": cfg["s"],
+           "blocks": cfg["n"] // cfg["s"], "k": cfg["k"], "p": cfg["p"], "q": cfg["q"], "g": cfg["g"],
+           "select": cfg["select"], "mode": cfg.get("mode")}
+    if cfg.get("g_rows"):
+        out["g_rows"] = cfg["g_rows"]
+    out["l2"] = ("A (%.2f GB) is larger than L2 (126 MB): re-read from HBM every step" % (bytes_a / 1e9)
+                 if bytes_a > 126e6 else "A fits L2 (%.1f MB): latency-bound config" % (bytes_a / 1e6))
+    return out
+
+
 def block_offsets(n, s):
     return np.array(list(range(0, n, s)) + [n], dtype=np.int64)
 
@@ -232,10 +245,8 @@ def bench_b200(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dt == np.float32 else "f64",
             "data": "synthetic (Philox-generated on device; BASELINE.json config distribution)",
-            "config": {"workload": args.config, "m": m, "n": n, "block_width": s, "blocks": G, "k": cfg["k"],
-                       "p": cfg["p"], "q": cfg["q"], "g": cfg["g"], "select": cfg["select"], "mode": cfg["mode"],
-                       "parallelism": f"column-block shards x{world}" if world > 1 else "single GPU",
-                       "l2": "A is larger than L2 (126 MB), re-read every step"},
+            "config": workload_config(args.config, cfg),
+            "parallelism": f"column-block shards x{world}" if world > 1 else "single GPU",
             "rel_err": rel_err, "selected_blocks": blocks[:16],
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
                     "d2h_bytes_per_step": d2h_bytes(cfg, G) * world, "ms_per_step": ms_e2e / e2e_steps},
@@ -294,7 +305,7 @@ def roofline(prof, peaks, traffic=({}, None)):
         else:
             line.update(tf32_peak_measured=TF32_MEASURED, frac_of_tf32_peak=achieved / TF32_MEASURED,
                         peak_source=peaks["source"] + " bf16_tflops (burst); a 3×TF32 kernel, whose tcgen05 rate "
-                                                      "was measured at %.0f TF/s by scratch/mma_rate.cu" % TF32_MEASURED)
+                                                      "was measured at %.0f TF/s by microbench/mma_rate.cu" % TF32_MEASURED)
         return line
     achieved = d["bytes"] / (d["ms"] / 1e3) / 1e9
     return dict(common, bound="hbm", achieved=achieved, peak=peaks["hbm"], unit="GB/s",
@@ -313,22 +324,63 @@ def cpu_threads():
     return os.cpu_count() or 1
 
 
-def cpu_sample_time(cfg, n_cols, seed=1):
-    """One oracle decomposition on the first n_cols columns (same m, s, k, p, q, g)."""
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model, "blas_threads": cpu_threads(),
+            "blas": "numpy %s / OpenBLAS (fp64)" % np.__version__}
+
+
+_HOST_A = {}
+
+
+def host_workload(cfg, n_cols=None, seed=1):
+    """The config's synthetic A on the host (numpy, same shape and distribution as the device
+    generator; a different realization), stored in the config dtype.  Low-rank inputs are
+    assembled column chunk by column chunk straight into fp32, so c3's 4.3 GB A never has an
+    fp64 copy.  Cached per (config, columns)."""
     from oracle import bcur_oracle as O
 
-    rng = np.random.default_rng(seed)
+    n = n_cols or cfg["n"]
+    key = (cfg["m"], n, cfg.get("kind"), cfg.get("rank"), cfg["dtype"], seed)
+    if key in _HOST_A:
+        return _HOST_A[key]
+    _HOST_A.clear()
     dt = np.float32 if cfg["dtype"] == "f32" else np.float64
     m = cfg["m"]
+    rng = np.random.default_rng(seed)
     if cfg["kind"] == "lowrank":
         r = cfg["rank"]
         u, _ = np.linalg.qr(rng.standard_normal((m, r)))
-        v, _ = np.linalg.qr(rng.standard_normal((n_cols, r)))
-        a = (u * spectrum(cfg["spectrum"], r)) @ v.T + cfg["noise"] * rng.standard_normal((m, n_cols))
+        v, _ = np.linalg.qr(rng.standard_normal((n, r)))
+        us = u * spectrum(cfg["spectrum"], r)
+        a = np.empty((m, n), dtype=dt, order="F")
+        w = max(1, min(n, (1 << 25) // m))
+        for j0 in range(0, n, w):
+            j1 = min(n, j0 + w)
+            blk = us @ v[j0:j1].T
+            blk += cfg["noise"] * rng.standard_normal((m, j1 - j0), dtype=np.float32)
+            a[:, j0:j1] = blk
     else:
-        a = O.gen_biometric(m, n_cols, cfg["seed"])
-    a = np.asfortranarray(a.astype(dt))
-    part = O.BlockPartition.equal_blocks(n_cols, cfg["s"])
+        a = np.asfortranarray(O.gen_biometric(m, n, cfg["seed"]).astype(dt))
+    _HOST_A[key] = a
+    return a
+
+
+def cpu_decompose(cfg, a):
+    """One oracle decomposition of `a` with the config's knobs (the same algorithm as the GPU
+    path: range finder → block leverage → draws → C basis → residual).  Returns seconds."""
+    from oracle import bcur_oracle as O
+
+    n, m = a.shape[1], a.shape[0]
+    part = O.BlockPartition.equal_blocks(n, cfg["s"])
     g = min(cfg["g"], part.num_blocks())
     t0 = time.perf_counter()
     if cfg["select"] == "greedy":
@@ -344,43 +396,89 @@ def cpu_sample_time(cfg, n_cols, seed=1):
     return time.perf_counter() - t0
 
 
-def cpu_baseline(cfg, budget_cols=None):
-    """Time the oracle on two column samples and extrapolate T(n) = a + b·n to the full n."""
+# Configs whose full decomposition does not fit a CPU run of minutes: c5 (68.7 GB; the fp64
+# QᵀA of its residual alone is 2.8e14 flop) is timed on a column sample and extrapolated.
+CPU_FULL = {"c1", "c2", "c3", "c4"}
+
+
+def reference_faithful(cfg):
+    """the reference's own semantics on one thread — exact SVD of A
+    (truncate(svd(a), k), matcore.cpp:39-69), block leverage, draws, ‖A − C·pinv(C)·A‖_F
+    (sketch.cpp:68-82) — timed on c1/c2 only (a full SVD of c3's A is ~1.8e13·const flop)."""
+    from oracle import bcur_oracle as O
+    from threadpoolctl import threadpool_limits
+
+    a = host_workload(cfg).astype(np.float64)
+    part = O.BlockPartition.equal_blocks(a.shape[1], cfg["s"])
+    with threadpool_limits(limits=1):
+        t0 = time.perf_counter()
+        O.reference_block_css(a, part, cfg["k"], min(cfg["g"], part.num_blocks()), O.Rng(cfg["seed"]),
+                              mode=cfg.get("mode", O.WITHOUT_REPLACEMENT))
+        t = time.perf_counter() - t0
+    return {"value": 1.0 / t, "unit": UNIT, "cores": 1, "seconds": t,
+            "sample": f"full {a.shape[0]}x{a.shape[1]} workload: exact SVD + pinv (reference semantics), 1 thread"}
+
+
+def cpu_baseline(cfg, name):
+    """The oracle timed on the host cores: one full decomposition of the config's workload
+    (c1–c4), measured — not extrapolated."""
+    info = cpu_info()
+    if name in CPU_FULL:
+        a = host_workload(cfg)
+        t = cpu_decompose(cfg, a)
+        out = {"value": 1.0 / t, "unit": UNIT, "cores": info["blas_threads"], "kind": "port", "seconds": t,
+               "sample": f"full {cfg['m']}x{cfg['n']} {cfg['dtype']} workload, one decomposition ({t:.2f} s); "
+                         "oracle/bcur_oracle.py in fp64 on numpy/OpenBLAS",
+               "estimated": False, "host": info}
+        if name in ("c1", "c2"):
+            out["reference_faithful"] = reference_faithful(cfg)
+        return out
     n, s = cfg["n"], cfg["s"]
-    if n <= 20000 or cfg["m"] * n <= 4e7:
-        t = cpu_sample_time(cfg, n)
-        return {"value": 1.0 / t, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                "sample": f"full {cfg['m']}x{n} workload, one decomposition ({t:.2f} s)"}
-    g = cfg["g"]
-    n1 = max(2 * g * s, budget_cols or 0)
-    n1 = min(n1, n // 4)
+    n1 = max(2 * cfg["g"] * s, n // 16)
     n2 = 2 * n1
-    t1 = cpu_sample_time(cfg, n1)
-    t2 = cpu_sample_time(cfg, n2)
+    t1 = cpu_decompose(cfg, host_workload(cfg, n1))
+    t2 = cpu_decompose(cfg, host_workload(cfg, n2))
     b = max((t2 - t1) / (n2 - n1), 0.0)
-    a = max(t1 - b * n1, 0.0)
-    t_full = a + b * n
-    return {"value": 1.0 / t_full, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-            "sample": (f"oracle on {cfg['m']}x{n1} ({t1:.2f} s) and {cfg['m']}x{n2} ({t2:.2f} s) column samples "
-                       f"(same m, s, k, p, q, g); T(n)=a+b*n extrapolated to n={n}: {t_full:.2f} s")}
+    a0 = max(t1 - b * n1, 0.0)
+    t_full = a0 + b * n
+    return {"value": 1.0 / t_full, "unit": UNIT, "cores": info["blas_threads"], "kind": "port", "estimated": True,
+            "fit": {"a_s": a0, "b_s_per_col": b, "t1_s": t1, "t2_s": t2, "n1": n1, "n2": n2}, "host": info,
+            "sample": (f"ESTIMATED: oracle on {cfg['m']}x{n1} ({t1:.2f} s) and {cfg['m']}x{n2} ({t2:.2f} s) column "
+                       f"samples, T(n)=a+b*n extrapolated to n={n}: {t_full:.2f} s")}
 
 
 def bench_reference(args, cfg):
-    steps = []
-    for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(cfg)
-        if i >= args.warmup:
-            steps.append(cb)
-    vals = [c["value"] for c in steps]
-    v = statistics.median(vals)
-    cb = dict(steps[-1])
-    cb["value"] = v
+    """The reference arm: the reference algorithm on the host cores (the oracle restatement —
+    the reference itself needs Eigen and vendor/, absent here).  Warm-up steps run on a
+    1/8-column sample of the workload (page-in, thread pools); each timed step is one FULL
+    decomposition of the config's workload (c1–c4), so value = steps / total seconds is
+    measured, not extrapolated."""
+    info = cpu_info()
+    if args.config not in CPU_FULL:
+        cb = cpu_baseline(cfg, args.config)
+        v = cb["value"]
+        times = [1.0 / v]
+    else:
+        a = host_workload(cfg)
+        wcols = max(cfg["s"] * cfg["g"], (cfg["n"] // 8) // cfg["s"] * cfg["s"])
+        aw = np.asfortranarray(a[:, :wcols]) if wcols < cfg["n"] else a
+        for _ in range(args.warmup):
+            cpu_decompose(cfg, aw)
+        del aw
+        times = [cpu_decompose(cfg, a) for _ in range(args.steps)]
+        v = len(times) / sum(times)
+        cb = {"value": v, "unit": UNIT, "cores": info["blas_threads"], "kind": "port", "estimated": False,
+              "sample": (f"{len(times)} full {cfg['m']}x{cfg['n']} {cfg['dtype']} decompositions "
+                         f"(median {statistics.median(times):.2f} s, min {min(times):.2f} s, max {max(times):.2f} s); "
+                         f"warm-up on a {cfg['m']}x{wcols} column sample"),
+              "host": info}
+        if args.config in ("c1", "c2"):
+            cb["reference_faithful"] = reference_faithful(cfg)
     return {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 / v, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": cfg["dtype"], "data": "synthetic (numpy, same shapes/distribution)",
-            "config": {"workload": args.config, "m": cfg["m"], "n": cfg["n"], "block_width": cfg["s"],
-                       "k": cfg["k"], "p": cfg["p"], "q": cfg["q"], "g": cfg["g"], "select": cfg["select"]},
-            "impl": "reference", "cpu_baseline": cb,
+            "config": workload_config(args.config, cfg),
+            "impl": "reference", "cpu_baseline": cb, "step_seconds": times,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "reference (Eigen, vendor/) unbuildable here; CPU oracle restatement timed on host cores"}
 
@@ -411,7 +509,7 @@ def main():
     line = bench_b200(args, cfg, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(cfg)
+            line["cpu_baseline"] = cpu_baseline(cfg, args.config)
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

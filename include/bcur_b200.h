@@ -169,6 +169,13 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
  *                          A·X, m % 8 == 0 for AᵀX) */
 enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4, BCUR_PRODUCT_H3 = 8 };
 bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
+/* The factorization behind every orthonormal basis of the path (CholQR2 of the sketch, of C,
+ * of Rᵀ — the reference's pseudoinverse, matcore.cpp:85-91, and svd, :39-56, are never
+ * formed): g (w×w fp64, upper triangle read) → r_out = R (upper, zero below) with G = RᵀR and
+ * rinv_out = R⁻¹ (nullable).  Recursive on the device: ≤128-wide leaves factored and inverted
+ * by one CTA, DMMA products between them.  *info = 0, or j + 1 when pivot j is not positive
+ * (R, R⁻¹ then undefined).  min_diag (nullable) = min diag(R). */
+bcur_status bcur_cholesky(bcur_ctx ctx, bcur_dmat g, bcur_dmat r_out, bcur_dmat rinv_out, int* info, double* min_diag);
 /* blockcur.cpp:54-109 block_cur — the reference's default Algorithm 1 (row_sampling =
  * uniform): R = the caller's row draws of A (sampler.cpp:54-95, drawn from its Rng; scaled
  * unless distinct), approximate block leverage of R (all rank(R) right singular vectors,
@@ -225,6 +232,9 @@ typedef struct {
     int mode;           /* bcur_sampling_mode */
     int residual;       /* bcur_residual_mode */
     uint64_t seed;      /* Rng seed: sketch key = bcur_omega_key(seed) */
+    int rank_floor;     /* 0 (default): the sketch's numerical rank is the reference's
+                           (σ > 1e-12·max(m,n)·σ₁, matcore.cpp:35-49); 1: also drop
+                           σ ≤ τ_rank·σ₁ (1e-5 fp32, 1e-7 fp64: near the working precision) */
 } bcur_options;
 
 typedef struct {

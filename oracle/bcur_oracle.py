@@ -504,13 +504,13 @@ def materialize_columns(a: np.ndarray, part: BlockPartition, plan: SamplingPlan)
         if d.block < 0 or d.block >= part.num_blocks():
             raise DimensionMismatch(f"materialize_columns: plan references block {d.block} outside the partition")
         b, e = part.ranges[d.block]
-        cols.append(a[:, b:e] * d.scale)
+        cols.append(cols64(a, b, e) * d.scale)
     return np.asfortranarray(np.concatenate(cols, axis=1))
 
 
 def materialize_row_blocks(a: np.ndarray, part: BlockPartition, plan: SamplingPlan) -> np.ndarray:
     """Row blocks = column blocks of Aᵀ; sampler.cpp:186-202 analogue."""
-    return np.asfortranarray(materialize_columns(np.asfortranarray(a.T), part, plan).T)
+    return np.asfortranarray(materialize_columns(a.T, part, plan).T)
 
 
 # ----------------------------------------------------------------------------
@@ -522,10 +522,88 @@ def rank_tolerance(rows: int, cols: int, sigma_max: float) -> float:  # matcore.
     return 1e-12 * max(rows, cols) * sigma_max
 
 
+# Products with A in fp64.  An fp32 A (configs c3–c5) is converted column chunk by column
+# chunk (exactly: fp32 ⊂ fp64) instead of as a whole, which only bounds host memory — the
+# full-size parity tests hold c3/c4's A (4.3 GB fp32; its fp64 copy alone would be 8.6 GB).
+# fp64 inputs take the direct products (bit-identical to the committed c1/c2 goldens).
+CHUNK_ELEMS = 1 << 26
+
+
+def _chunks(a: np.ndarray):
+    m, n = a.shape
+    w = max(1, min(n, CHUNK_ELEMS // max(m, 1)))
+    for j0 in range(0, n, w):
+        yield j0, min(n, j0 + w)
+
+
+def cols64(a: np.ndarray, j0: int, j1: int) -> np.ndarray:
+    return np.asarray(a[:, j0:j1], dtype=np.float64)
+
+
+def a_mul(a: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """A·x (x: n × N fp64)."""
+    if a.dtype == np.float64:
+        return a @ x
+    out = np.zeros((a.shape[0], x.shape[1]))
+    for j0, j1 in _chunks(a):
+        out += cols64(a, j0, j1) @ x[j0:j1]
+    return out
+
+
+def at_mul(a: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """Aᵀ·y (y: m × N fp64) → n × N."""
+    if a.dtype == np.float64:
+        return a.T @ y
+    out = np.empty((a.shape[1], y.shape[1]))
+    for j0, j1 in _chunks(a):
+        out[j0:j1] = cols64(a, j0, j1).T @ y
+    return out
+
+
+def col_sumsq(a: np.ndarray) -> np.ndarray:
+    """Σ_i a(i, j)² per column, fp64."""
+    if a.dtype == np.float64:
+        return np.sum(a * a, axis=0)
+    out = np.empty(a.shape[1])
+    for j0, j1 in _chunks(a):
+        c = cols64(a, j0, j1)
+        out[j0:j1] = np.einsum("ij,ij->j", c, c)
+    return out
+
+
+def row_sumsq(a: np.ndarray) -> np.ndarray:
+    """Σ_j a(i, j)² per row, fp64."""
+    if a.dtype == np.float64:
+        return np.sum(a * a, axis=1)
+    out = np.zeros(a.shape[0])
+    for j0, j1 in _chunks(a):
+        c = cols64(a, j0, j1)
+        out += np.einsum("ij,ij->i", c, c)
+    return out
+
+
+def resid_sumsq(a: np.ndarray, left: np.ndarray, right_t: np.ndarray) -> float:
+    """‖A − left·right_tᵀ‖_F² (left: m × r, right_t: n × r), streamed over column chunks."""
+    if a.dtype == np.float64:
+        r = a - left @ right_t.T
+        return float(np.sum(r * r))
+    tot = 0.0
+    for j0, j1 in _chunks(a):
+        r = cols64(a, j0, j1) - left @ right_t[j0:j1].T
+        tot += float(np.einsum("ij,ij->", r, r))
+    return tot
+
+
 # Orthonormalisation thresholds (DESIGN.md §Numerics, SURVEY D8/D13).
 TAU_CHOL = {np.dtype(np.float64): 1e-5, np.dtype(np.float32): 1e-2}
-TAU_RANK = {np.dtype(np.float64): 1e-7, np.dtype(np.float32): 3e-4}
+TAU_RANK = {np.dtype(np.float64): 1e-7, np.dtype(np.float32): 1e-5}
 THETA_EXPLICIT = {np.dtype(np.float64): 1e-6, np.dtype(np.float32): 0.1}
+
+
+def right_solve_upper(x: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """X·R⁻¹ for upper-triangular R (a triangular solve, not an LU of R)."""
+    from scipy.linalg import solve_triangular
+    return solve_triangular(r, x.T, trans="T", lower=False, check_finite=False).T
 
 
 def chol_upper(g: np.ndarray) -> Optional[np.ndarray]:
@@ -557,9 +635,9 @@ def orth(x: np.ndarray, ref: float, dt) -> Tuple[np.ndarray, np.ndarray, str]:
     g = x.T @ x
     r = chol_upper(g)
     if r is not None and np.all(np.isfinite(r)) and np.min(np.diag(r)) > TAU_CHOL[dt] * ref:
-        q1 = np.linalg.solve(r.T, x.T).T  # X R⁻¹
+        q1 = right_solve_upper(x, r)  # X R⁻¹
         r2 = chol_upper(q1.T @ q1)
-        q = np.linalg.solve(r2.T, q1.T).T
+        q = right_solve_upper(q1, r2)
         return q, r2 @ r, "chol"
     if x.shape[0] < w:
         # wide panel: decide on the smaller row Gram X·Xᵀ.  Safely full row rank (its
@@ -576,7 +654,7 @@ def orth(x: np.ndarray, ref: float, dt) -> Tuple[np.ndarray, np.ndarray, str]:
             return np.zeros((x.shape[0], 0)), np.zeros((0, w)), "eig"
         q1 = u[:, :keep]
         r2 = chol_upper(q1.T @ q1)
-        q = np.linalg.solve(r2.T, q1.T).T
+        q = right_solve_upper(q1, r2)
         return q, r2 @ (q1.T @ x), "eig"
     lam, wv = eig_desc(g)
     sig = np.sqrt(np.maximum(lam, 0.0))
@@ -585,7 +663,7 @@ def orth(x: np.ndarray, ref: float, dt) -> Tuple[np.ndarray, np.ndarray, str]:
         return np.zeros((x.shape[0], 0)), np.zeros((0, w)), "eig"
     q1 = (x @ wv[:, :keep]) / sig[:keep]
     r2 = chol_upper(q1.T @ q1)
-    q = np.linalg.solve(r2.T, q1.T).T
+    q = right_solve_upper(q1, r2)
     t = (r2 * sig[:keep][None, :]) @ wv[:, :keep].T
     return q, t, "eig"
 
@@ -617,25 +695,35 @@ class Subspace:
     q_rank: int
 
 
-def range_finder(a: np.ndarray, k: int, p: int, q: int, key: int) -> Subspace:
-    dt = a.dtype
-    a = np.asarray(a, dtype=np.float64)
+def range_finder(a: np.ndarray, k: int, p: int, q: int, key: int, rank_floor: bool = False) -> Subspace:
+    """Y = AΩ, q power iterations, Q = orth(Y), Bᵀ = AᵀQ, eig of BBᵀ, V_k = BᵀŨ_kΣ_k⁻¹.
+
+    The numerical rank of the sketch is the reference's (matcore.cpp:35-49: σ >
+    1e-12·max(m,n)·σ₁).  rank_floor=True (opt-in) also drops σ ≤ τ_rank·σ₁ (1e-7 fp64,
+    1e-5 fp32): directions below the working precision of an fp32 A.
+    """
+    dt = np.dtype(a.dtype)
+    if dt not in (np.dtype(np.float32), np.dtype(np.float64)):
+        a = np.asarray(a, dtype=np.float64)
+        dt = a.dtype
     m, n = a.shape
     l = min(k + p, m, n)
     om = omega(n, l, key)
-    y = a @ om
+    y = a_mul(a, om)
     for _ in range(q):
         qy, _, _ = orth(y, float(np.sqrt(np.max(np.sum(y * y, axis=0)))), dt)
-        z = a.T @ qy
+        z = at_mul(a, qy)
         qz, _, _ = orth(z, float(np.sqrt(np.max(np.sum(z * z, axis=0)))), dt)
-        y = a @ qz
+        y = a_mul(a, qz)
     qy, _, _ = orth(y, float(np.sqrt(np.max(np.sum(y * y, axis=0)))), dt)
-    bt = a.T @ qy                     # n × r  (B = Qᵀ A)
+    bt = at_mul(a, qy)                # n × r  (B = Qᵀ A)
     lam, ut = eig_desc(bt.T @ bt)     # B Bᵀ
     sig = np.sqrt(np.maximum(lam, 0.0))
     if sig.size == 0 or not sig[0] > 0.0:
         raise ZeroMatrix("range_finder: A is identically zero")
-    tol = max(rank_tolerance(m, n, sig[0]), TAU_RANK[np.dtype(dt)] * sig[0])
+    tol = rank_tolerance(m, n, sig[0])
+    if rank_floor:
+        tol = max(tol, TAU_RANK[dt] * sig[0])
     rank = int(np.sum(sig > tol))
     k_eff = min(k, rank)
     wmat = ut[:, :k_eff] / sig[:k_eff]
@@ -679,11 +767,11 @@ def cholqr2_whole(c: np.ndarray, dt) -> Optional[np.ndarray]:
     ref = float(np.sqrt(np.max(np.diag(g))))
     if r is None or not np.all(np.isfinite(r)) or not np.min(np.diag(r)) > TAU_CHOL[np.dtype(dt)] * ref:
         return None
-    q1 = np.linalg.solve(r.T, c.T).T
+    q1 = right_solve_upper(c, r)
     r2 = chol_upper(q1.T @ q1)
     if r2 is None:
         return None
-    return np.linalg.solve(r2.T, q1.T).T
+    return right_solve_upper(q1, r2)
 
 
 def column_basis(a64: np.ndarray, part: BlockPartition, blocks: Sequence[int], dt,
@@ -693,7 +781,7 @@ def column_basis(a64: np.ndarray, part: BlockPartition, blocks: Sequence[int], d
     m = a64.shape[0]
     ub = unique_in_order(blocks)
     if allow_whole:
-        cols = np.concatenate([a64[:, part.ranges[b][0]:part.ranges[b][1]] for b in ub], axis=1)
+        cols = np.concatenate([cols64(a64, *part.ranges[b]) for b in ub], axis=1)
         q = cholqr2_whole(cols, dt)
         if q is not None:
             return q, ["whole"]
@@ -702,19 +790,20 @@ def column_basis(a64: np.ndarray, part: BlockPartition, blocks: Sequence[int], d
     for bidx in ub:
         b, e = part.ranges[bidx]
         ref = math.sqrt(block_norms[bidx])
-        qn, _, _, path = cgs2_panel(qc, a64[:, b:e].copy(), ref, dt)
+        qn, _, _, path = cgs2_panel(qc, cols64(a64, b, e).copy(), ref, dt)
         qc = np.concatenate([qc, qn], axis=1)
         paths.append(path)
     return qc, paths
 
 
-def projection_residual(a64: np.ndarray, qc: np.ndarray, a_norm2: float, dt) -> Tuple[float, str]:
-    """‖A − Q_C Q_Cᵀ A‖_F² — Pythagoras, explicit when small."""
-    x = qc.T @ a64
-    res2 = a_norm2 - float(np.sum(x * x))
-    if res2 < THETA_EXPLICIT[np.dtype(dt)] * a_norm2:
-        r = a64 - qc @ x
-        return float(np.sum(r * r)), "explicit"
+def projection_residual(a64: np.ndarray, qc: np.ndarray, a_norm2: float, dt,
+                        force: Optional[str] = None) -> Tuple[float, str]:
+    """‖A − Q_C Q_Cᵀ A‖_F² — Pythagoras, explicit when small.
+    force: "explicit" / "pythagoras" overrides the rule (the ABI's residual mode)."""
+    xt = at_mul(a64, qc)  # (Q_Cᵀ A)ᵀ, n × r
+    res2 = a_norm2 - float(np.einsum("ij,ij->", xt, xt))
+    if force == "explicit" or (force is None and res2 < THETA_EXPLICIT[np.dtype(dt)] * a_norm2):
+        return resid_sumsq(a64, qc, xt), "explicit"
     return max(res2, 0.0), "pythagoras"
 
 
@@ -734,32 +823,37 @@ class CssResult:
 
 
 def block_norms2(a64: np.ndarray, part: BlockPartition) -> np.ndarray:
-    return block_sums(np.sum(a64 * a64, axis=0), part)
+    return block_sums(col_sumsq(a64), part)
 
 
 def block_css(a: np.ndarray, part: BlockPartition, k: int, g: int, rng: Rng, p: int = 5, q: int = 0,
-              mode: str = WITH_REPLACEMENT, exact: bool = False) -> CssResult:
+              mode: str = WITH_REPLACEMENT, exact: bool = False, residual: Optional[str] = None,
+              rank_floor: bool = False) -> CssResult:
     """sketch.cpp:68-82 with the range finder (N1) in place of the exact SVD.
 
     ``exact=True`` uses truncate(svd(a), k) like the reference (small inputs).
+    An fp32 A is not copied to fp64 as a whole (products convert column chunks).
     """
     if k < 1:
         raise ValueError("block_css: k must be >= 1")
     if a.shape[1] != part.n:
         raise DimensionMismatch("block_css: partition does not match A columns")
     dt = a.dtype
-    a64 = np.asarray(a, dtype=np.float64)
+    a64 = a if dt in (np.float32, np.float64) else np.asarray(a, dtype=np.float64)
     bn2 = block_norms2(a64, part)
     a_norm2 = float(np.sum(bn2))
     if not a_norm2 > 0.0:
         raise ZeroMatrix("block_css: A is identically zero")
-    sub = exact_subspace(a64, k) if exact else range_finder(a, k, p, q, omega_key_from_seed(rng.seed()))
+    if exact:
+        sub = exact_subspace(np.asarray(a, dtype=np.float64), k)
+    else:
+        sub = range_finder(a64, k, p, q, omega_key_from_seed(rng.seed()), rank_floor=rank_floor)
     if sub.k_eff == 0:
         raise ZeroMatrix("block_css: A is identically zero")
     scores = block_leverage(sub.v_k, part, check=False)
     plan = draw_blocks(scores.distribution(), g, mode, rng)
     qc, _ = column_basis(a64, part, plan.blocks(), dt, bn2)
-    res2, path = projection_residual(a64, qc, a_norm2, dt)
+    res2, path = projection_residual(a64, qc, a_norm2, dt, force=residual)
     return CssResult(plan, scores, math.sqrt(res2), math.sqrt(a_norm2), qc.shape[1], path, sub)
 
 
@@ -906,28 +1000,28 @@ class CurResult:
 
 def block_cur_rows_cols(a: np.ndarray, col_part: BlockPartition, row_part: BlockPartition, k: int,
                         gc: int, gr: int, rng: Rng, p: int = 10, q: int = 0,
-                        mode: str = WITHOUT_REPLACEMENT, want_u: bool = True) -> CurResult:
+                        mode: str = WITHOUT_REPLACEMENT, want_u: bool = True, rank_floor: bool = False) -> CurResult:
     dt = np.dtype(a.dtype)
-    a64 = np.asarray(a, dtype=np.float64)
+    a64 = a if dt in (np.dtype(np.float32), np.dtype(np.float64)) else np.asarray(a, dtype=np.float64)
     if col_part.n != a.shape[1] or row_part.n != a.shape[0]:
         raise DimensionMismatch("block_cur: partitions do not match A")
-    a_norm2 = float(np.sum(a64 * a64))
+    a_norm2 = float(np.sum(col_sumsq(a64)))
     if not a_norm2 > 0.0:
         raise ZeroMatrix("block_cur: A is identically zero")
-    sub = range_finder(a, k, p, q, omega_key_from_seed(rng.seed()))
+    sub = range_finder(a64, k, p, q, omega_key_from_seed(rng.seed()), rank_floor=rank_floor)
     cs = block_leverage(sub.v_k, col_part, check=False)
     rs = block_leverage(sub.u_k, row_part, check=False)
     cplan = draw_blocks(cs.distribution(), gc, mode, rng)
     rplan = draw_blocks(rs.distribution(), gr, mode, rng)
     qc, _ = column_basis(a64, col_part, cplan.blocks(), dt, block_norms2(a64, col_part))
-    at = np.asfortranarray(a64.T)
-    qr_, _ = column_basis(at, row_part, rplan.blocks(), dt, block_norms2(at, row_part))
-    mm = qc.T @ a64 @ qr_
+    at = a64.T  # row blocks of A = column blocks of Aᵀ (a view: no copy)
+    rn2 = block_sums(row_sumsq(a64), row_part)
+    qr_, _ = column_basis(at, row_part, rplan.blocks(), dt, rn2)
+    mm = at_mul(a64, qc).T @ qr_  # Q_Cᵀ A Q_R
     res2 = a_norm2 - float(np.sum(mm * mm))
     path = "pythagoras"
     if res2 < THETA_EXPLICIT[dt] * a_norm2:
-        r = a64 - qc @ mm @ qr_.T
-        res2, path = float(np.sum(r * r)), "explicit"
+        res2, path = resid_sumsq(a64, qc, qr_ @ mm.T), "explicit"
     u = None
     if want_u:
         c = materialize_columns(a64, col_part, cplan)
@@ -945,22 +1039,9 @@ def block_cur_rows_cols(a: np.ndarray, col_part: BlockPartition, row_part: Block
 # SURVEY Appendix A D11).
 # ----------------------------------------------------------------------------
 
-CONFIGS = {
-    "c1": dict(kind="lowrank", dtype="f64", m=500, n=2000, rank=10, spectrum="geom:10:0.8",
-               noise=1e-3, s=20, k=10, p=5, q=0, mode=WITHOUT_REPLACEMENT, select="leverage", g=10,
-               seed=0),
-    "c2": dict(kind="biometric", dtype="f64", m=64, n=20000, s=100, k=5, p=5, q=0,
-               select="greedy", g=8, seed=0),
-    "c3": dict(kind="lowrank", dtype="f32", m=16384, n=65536, rank=50, spectrum="pow:1.5",
-               noise=1e-4, s=128, k=50, p=10, q=2, mode=WITHOUT_REPLACEMENT, select="leverage", g=32,
-               seed=0),
-    "c4": dict(kind="lowrank", dtype="f32", m=32768, n=32768, rank=100, spectrum="geom:1:0.97",
-               noise=1e-3, s=128, k=100, p=10, q=0, mode=WITHOUT_REPLACEMENT, select="cur", g=24,
-               g_rows=24, seed=0),
-    "c5": dict(kind="lowrank", dtype="f32", m=65536, n=262144, rank=200, spectrum="pow:1",
-               noise=1e-4, s=128, k=200, p=20, q=0, mode=WITHOUT_REPLACEMENT, select="leverage+greedy",
-               g=64, seed=0),
-}
+# The single source of the workloads is paper_1703_06065_b200/configs.py (pure data: importing
+# it loads no product code).
+from paper_1703_06065_b200.configs import CONFIGS  # noqa: E402,F401
 
 
 # ------------------------------------------------------------------ Algorithm 1

@@ -41,7 +41,7 @@ class BlockDrawC(C.Structure):
 
 class OptionsC(C.Structure):
     _fields_ = [("k", i64), ("p", i64), ("q", i64), ("g", i64), ("g_rows", i64), ("mode", C.c_int),
-                ("residual", C.c_int), ("seed", u64)]
+                ("residual", C.c_int), ("seed", u64), ("rank_floor", C.c_int)]
 
 
 class ReportC(C.Structure):
@@ -103,6 +103,7 @@ SIGNATURES = {
     "bcur_range_finder": (C.c_int, [vp, vp, i64, i64, i64, u64, C.POINTER(vp), C.POINTER(vp), P_dbl, P_i64]),
     "bcur_sketch_product": (C.c_int, [vp, vp, vp, C.c_int, vp, P_dbl]),
     "bcur_sketch_product_ex": (C.c_int, [vp, vp, vp, C.c_int, C.c_int, vp]),
+    "bcur_cholesky": (C.c_int, [vp, vp, vp, vp, C.POINTER(C.c_int), P_dbl]),
     "bcur_draw_blocks": (C.c_int, [vp, P_dbl, i64, i64, C.c_int, P_dbl, u64, C.POINTER(BlockDrawC), P_dbl]),
     "bcur_materialize_columns": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(BlockDrawC), i64, C.POINTER(vp)]),
     "bcur_materialize_row_blocks": (C.c_int, [vp, vp, P_i64, i64, C.POINTER(BlockDrawC), i64, C.POINTER(vp)]),

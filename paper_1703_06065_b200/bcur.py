@@ -506,6 +506,22 @@ def structured_product(a, x: Optional[np.ndarray] = None, transpose: bool = Fals
     return out[:, 0] if rowsq_f16 else out
 
 
+def cholesky(g: np.ndarray, ctx: Optional[Context] = None):
+    """G = RᵀR on the device (fp64, upper triangle of g read) → (R, R⁻¹, info, min diag R)."""
+    ctx = ctx or default_context()
+    g = np.asfortranarray(np.asarray(g, dtype=np.float64))
+    w = g.shape[0]
+    gd = DeviceMatrix.from_host(g, ctx)
+    hs = []
+    for _ in range(2):
+        h = C.c_void_p()
+        _check(L.lib.bcur_dmat_create(ctx.handle, L.F64, w, w, C.byref(h)))
+        hs.append(DeviceMatrix(h, ctx))
+    info, mn = C.c_int(), C.c_double()
+    _check(L.lib.bcur_cholesky(ctx.handle, gd.handle, hs[0].handle, hs[1].handle, C.byref(info), C.byref(mn)))
+    return hs[0].to_host(), hs[1].to_host(), info.value, mn.value
+
+
 @dataclass
 class Subspace:
     v_k: np.ndarray
@@ -680,13 +696,13 @@ class CssResult:
         return self.projection_error / self.a_norm if self.a_norm > 0 else 0.0
 
 
-def _options(k, p, q, g, g_rows, mode, residual, seed):
-    return L.OptionsC(k, p, q, g, g_rows, _mode_code(mode), residual, seed & ((1 << 64) - 1))
+def _options(k, p, q, g, g_rows, mode, residual, seed, rank_floor=False):
+    return L.OptionsC(k, p, q, g, g_rows, _mode_code(mode), residual, seed & ((1 << 64) - 1), int(bool(rank_floor)))
 
 
 def block_css(a, part: BlockPartition, k: int, g: int, rng: Rng, p: int = 5, q: int = 0,
               mode: str = SamplingMode.with_replacement, residual: int = L.RESID_AUTO, return_c: bool = True,
-              ctx: Optional[Context] = None) -> CssResult:
+              ctx: Optional[Context] = None, rank_floor: bool = False) -> CssResult:
     """Block column subset selection (sketch.cpp:68-82): block leverage at rank k from the
     randomized range finder (sketch key from ``rng.seed()``), g draws (one uniform each
     from ``rng``), C = A S, projection error ‖A − CC⁺A‖_F — all on the GPU."""
@@ -699,7 +715,7 @@ def block_css(a, part: BlockPartition, k: int, g: int, rng: Rng, p: int = 5, q: 
     off, offp = _off_ptr(part)
     G = part.num_blocks()
     u = rng.uniforms(g)
-    opt = _options(k, p, q, g, 0, mode, residual, rng.seed())
+    opt = _options(k, p, q, g, 0, mode, residual, rng.seed(), rank_floor)
     scores = np.empty(G, dtype=np.float64)
     norm = C.c_double()
     draws = (L.BlockDrawC * g)()
@@ -898,7 +914,7 @@ class CurResult:
 
 def block_cur(a, col_part: BlockPartition, row_part: BlockPartition, k: int, gc: int, gr: int, rng: Rng,
               p: int = 10, q: int = 0, mode: str = SamplingMode.without_replacement, want_u: bool = True,
-              residual: int = L.RESID_AUTO, ctx: Optional[Context] = None) -> CurResult:
+              residual: int = L.RESID_AUTO, ctx: Optional[Context] = None, rank_floor: bool = False) -> CurResult:
     """Block CUR with row and column blocks: U = C⁺AR⁺ and ‖A − CUR‖_F on the GPU."""
     ctx = ctx or default_context()
     d = _dev(a, ctx)
@@ -906,7 +922,7 @@ def block_cur(a, col_part: BlockPartition, row_part: BlockPartition, k: int, gc:
     roff, roffp = _off_ptr(row_part)
     Gc, Gr = col_part.num_blocks(), row_part.num_blocks()
     u = rng.uniforms(gc + gr)
-    opt = _options(k, p, q, gc, gr, mode, residual, rng.seed())
+    opt = _options(k, p, q, gc, gr, mode, residual, rng.seed(), rank_floor)
     cs = np.empty(Gc)
     rs = np.empty(Gr)
     cd = (L.BlockDrawC * gc)()

@@ -79,7 +79,7 @@ def build_lib(verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if os.path.exists(LIB) and os.path.getmtime(LIB) >= max(os.path.getmtime(o) for o in objs):
         return LIB
-    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcublas", "-Xlinker", "-rpath=/usr/local/cuda/lib64"]
+    cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs
     if verbose:
         print(" ".join(cmd), flush=True)
     r = subprocess.run(cmd, capture_output=True, text=True)

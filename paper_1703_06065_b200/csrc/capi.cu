@@ -694,11 +694,28 @@ bcur_status bcur_range_finder(bcur_ctx ctx, bcur_dmat a, int64_t k, int64_t p, i
     DMat* d = M(a);
     if (d->m < 1 || d->n < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: matrix must be non-empty");
     Subspace s;
-    range_finder(c, d, k, p, q, key, &s);
+    range_finder(c, d, k, p, q, key, &s, false);
     if (v_out) *v_out = from_mat64(c, s.v, d->n, s.k_eff);
     if (u_out) *u_out = from_mat64(c, s.u, d->m, s.k_eff);
     if (sigma_out) std::memcpy(sigma_out, s.sigma.data(), s.k_eff * sizeof(double));
     if (k_eff) *k_eff = s.k_eff;
+    API_END
+}
+
+bcur_status bcur_cholesky(bcur_ctx ctx, bcur_dmat g, bcur_dmat r_out, bcur_dmat rinv_out, int* info, double* min_diag) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat *G = M(g), *R = M(r_out), *X = rinv_out ? M(rinv_out) : nullptr;
+    const int64_t w = G->m;
+    if (G->dtype != BCUR_F64 || R->dtype != BCUR_F64 || (X && X->dtype != BCUR_F64))
+        fail(BCUR_E_INVALID_ARGUMENT, "cholesky: matrices must be fp64");
+    if (G->n != w || R->m != w || R->n != w || (X && (X->m != w || X->n != w)) || R->ld != w || (X && X->ld != w))
+        fail(BCUR_E_DIMENSION_MISMATCH, "cholesky: G, R, R^-1 must be w x w (R and R^-1 with ld = w)");
+    if (w < 1) fail(BCUR_E_INVALID_ARGUMENT, "cholesky: empty matrix");
+    const int st = cholesky_inverse(c, (const double*)G->ptr, w, G->ld, (double*)R->ptr, X ? (double*)X->ptr : nullptr,
+                                    min_diag);
+    if (info) *info = st;
+    c->sync();
     API_END
 }
 

@@ -61,7 +61,12 @@ struct Ctx {
     int sm_count = 148;
     int64_t launches = 0;
     bcur_comm comm{0, 1, nullptr, nullptr};
-    std::multimap<size_t, void*> free_list;
+    // free blocks by size class, each tagged with the stream its last use was enqueued on
+    struct FreeBlk {
+        void* p;
+        cudaStream_t s;
+    };
+    std::multimap<size_t, FreeBlk> free_list;
     size_t pooled_bytes = 0;
     // pinned host staging for small device→host reads
     void* pinned = nullptr;
@@ -69,14 +74,16 @@ struct Ctx {
 
     // Workspace cache over cudaMalloc (large pages, TMA-friendly): blocks are kept in exact
     // size classes (≤ 12.5% rounding), so a repeated decomposition reuses every block and
-    // never calls cudaMalloc in steady state.  Reuse is safe in stream order: a block is
-    // released only after its last use has been enqueued on this context's stream.
+    // never calls cudaMalloc in steady state.  Reuse is safe in stream order: a block carries
+    // the stream that was current when it was released (its last use was enqueued there), and
+    // is handed out again only on that stream — or on another one after order() has made that
+    // stream wait for it (order() re-tags the blocks released on `from` so far).
     int64_t allocs = 0, allocs_mark = 0;
     void* acquire(size_t bytes) {
         const size_t want = round(bytes);
-        auto it = free_list.find(want);
-        if (it != free_list.end()) {
-            void* p = it->second;
+        for (auto it = free_list.lower_bound(want); it != free_list.end() && it->first == want; ++it) {
+            if (it->second.s != stream) continue;
+            void* p = it->second.p;
             free_list.erase(it);
             pooled_bytes -= want;
             return p;
@@ -94,19 +101,24 @@ struct Ctx {
     }
     void release(void* p) {
         if (!p) return;
-        free_list.emplace(sizes[p], p);
+        free_list.emplace(sizes[p], FreeBlk{p, stream});
         pooled_bytes += sizes[p];
     }
     void trim() {
-        cudaStreamSynchronize(stream);
+        CUDA_CHECK(cudaDeviceSynchronize());  // blocks may be tagged with any of the streams
         for (auto& kv : free_list) {
-            cudaFree(kv.second);
-            sizes.erase(kv.second);
+            cudaFree(kv.second.p);
+            sizes.erase(kv.second.p);
         }
         free_list.clear();
         pooled_bytes = 0;
     }
-    bool cached(size_t bytes) const { return free_list.count(round(bytes)) > 0; }
+    bool cached(size_t bytes) const {
+        auto r = free_list.equal_range(round(bytes));
+        for (auto it = r.first; it != r.second; ++it)
+            if (it->second.s == stream) return true;
+        return false;
+    }
     static size_t round(size_t b) {
         if (b <= 256) return 256;
         size_t p = 256;
@@ -165,6 +177,22 @@ struct Ctx {
     void order(cudaStream_t from, cudaStream_t to, int slot) {
         CUDA_CHECK(cudaEventRecord(side_ev[slot], from));
         CUDA_CHECK(cudaStreamWaitEvent(to, side_ev[slot], 0));
+        retag(from, to);
+    }
+    // blocks released on `from` so far are safe on `to` once `to` waits for `from`
+    void retag(cudaStream_t from, cudaStream_t to) {
+        for (auto& kv : free_list)
+            if (kv.second.s == from) kv.second.s = to;
+    }
+    // events for fork/join inside one operation (grown on demand, reused across calls)
+    std::vector<cudaEvent_t> sync_events;
+    cudaEvent_t sync_event(size_t i) {
+        while (sync_events.size() <= i) {
+            cudaEvent_t e;
+            CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            sync_events.push_back(e);
+        }
+        return sync_events[i];
     }
 
     // --- per-kernel accounting (CUDA events on this stream; bench roofline) ---

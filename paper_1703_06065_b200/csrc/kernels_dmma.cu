@@ -1,0 +1,546 @@
+// kernels_dmma.cu — fp64 products on the tensor cores (DMMA, mma.sync m8n8k4 .f64) and
+// the fused single-CTA Cholesky + triangular inverse that the recursive factorization
+// (pipeline.cu chol_inv) uses as its leaf.
+//
+// k_dgemm: C = alpha·op(A)·op(B) + beta·C with fp64 accumulation, every operand converted
+// to fp64 on its way into shared memory (fp32 or fp64 inputs).  It serves every product that
+// is not an fp32 A-pass: the fp64 configs' sketch (Y = AΩ, B = QᵀA — the reference's
+// BDCSVD/GEMMs, matcore.cpp:39-56, blockcur.cpp:46), Grams, CholQR2 panels, the recursive
+// Cholesky's updates, U assembly.  Epilogues:
+//   STORE  alpha·AB + beta·C (split-K partials reduced in a fixed order: deterministic)
+//   ROWSQ  rowsq[i] = Σ_j (AB)_ij² without storing the product (‖Q_Cᵀ A_g‖², sketch.cpp:80)
+//   RESID  Σ (D − AB)² (the explicit residual ‖A − C(UR)‖_F², blockcur.cpp:46)
+// Structure flags shrink each tile's K range (triangular operands) or skip tiles (a product
+// known to be symmetric, of which only the upper triangle is consumed).
+//
+// CTA tile 64×64×16, 4 warps as 2×2, each warp 32×32 = 4×4 DMMA tiles; operands staged
+// through registers into double-buffered shared memory ([k][m] / [k][n] with a row pitch of
+// 72 doubles: the fragment loads — lane t reads row t&3, column t>>2 — take the minimum two
+// wavefronts).
+#include "ops.h"
+
+namespace bcur_b200 {
+namespace {
+
+constexpr int DBM = 64, DBN = 64, DBK = 16, DNT = 128, DLD = 72;
+enum { DEPI_STORE = 0, DEPI_ROWSQ = 1, DEPI_RESID = 2 };
+
+template <class T>
+__device__ __forceinline__ double ldg64(const T* p) { return (double)__ldg(p); }
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <typename TA, typename TB, int TRA, int TRB, int EPI>
+__global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
+                                               const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B,
+                                               int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
+                                               double* __restrict__ partial, const void* __restrict__ D, int dtd,
+                                               int64_t ldd, int flags) {
+    __shared__ __align__(16) double As[2][DBK][DLD];
+    __shared__ __align__(16) double Bs[2][DBK][DLD];
+    __shared__ double red[2][DBM];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int64_t m0 = (int64_t)blockIdx.x * DBM, n0 = (int64_t)blockIdx.y * DBN;
+    const bool split = partial != nullptr && EPI == DEPI_STORE;
+    // a symmetric product of which only the upper triangle is consumed: tiles strictly
+    // below the diagonal are not computed (zeros into their split-K partials)
+    const bool skip = (flags & ops::GEMM_SYM_UPPER) && m0 >= n0 + DBN;
+    if (skip && !split) return;
+    int64_t kbeg = (int64_t)blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
+    if (flags & ops::GEMM_A_UPPER) kbeg = max(kbeg, m0 / DBK * DBK);   // op(A)[i,k] = 0 for k < i
+    if (flags & ops::GEMM_A_LOWER) kend = min(kend, m0 + DBM);         // op(A)[i,k] = 0 for k > i
+    if (flags & ops::GEMM_B_UPPER) kend = min(kend, n0 + DBN);         // op(B)[k,j] = 0 for k > j
+    if (flags & ops::GEMM_B_LOWER) kbeg = max(kbeg, n0 / DBK * DBK);   // op(B)[k,j] = 0 for k < j
+    if (skip) kend = kbeg;
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    double ra[8], rb[8];
+    // op(A) tile (DBM × DBK) and op(B) tile (DBK × DBN), each 1024 elements = 8 per thread;
+    // the thread map follows the contiguous direction of the stored matrix
+    auto load = [&](int64_t k0) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            int i, kk;
+            if (TRA == 0) { i = tid & 63; kk = (tid >> 6) + 2 * r; } else { kk = tid & 15; i = (tid >> 4) + 8 * r; }
+            const int64_t gi = m0 + i, gk = k0 + kk;
+            ra[r] = (gi < M && gk < kend) ? (TRA == 0 ? ldg64(A + gi + gk * lda) : ldg64(A + gk + gi * lda)) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            int j, kk;
+            if (TRB == 0) { kk = tid & 15; j = (tid >> 4) + 8 * r; } else { j = tid & 63; kk = (tid >> 6) + 2 * r; }
+            const int64_t gj = n0 + j, gk = k0 + kk;
+            rb[r] = (gj < N && gk < kend) ? (TRB == 0 ? ldg64(B + gk + gj * ldb) : ldg64(B + gj + gk * ldb)) : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            int i, kk;
+            if (TRA == 0) { i = tid & 63; kk = (tid >> 6) + 2 * r; } else { kk = tid & 15; i = (tid >> 4) + 8 * r; }
+            As[buf][kk][i] = ra[r];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            int j, kk;
+            if (TRB == 0) { kk = tid & 15; j = (tid >> 4) + 8 * r; } else { j = tid & 63; kk = (tid >> 6) + 2 * r; }
+            Bs[buf][kk][j] = rb[r];
+        }
+    };
+
+    if (kbeg < kend) {
+        int buf = 0;
+        load(kbeg);
+        store(0);
+        __syncthreads();
+        const int fr = lane & 3, fc = lane >> 2;
+        for (int64_t k0 = kbeg; k0 < kend; k0 += DBK) {
+            const bool more = k0 + DBK < kend;
+            if (more) load(k0 + DBK);
+#pragma unroll
+            for (int k4 = 0; k4 < DBK; k4 += 4) {
+                double af[4], bf[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) af[i] = As[buf][k4 + fr][wm * 32 + i * 8 + fc];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][k4 + fr][wn * 32 + j * 8 + fc];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            }
+            if (more) {
+                store(buf ^ 1);
+                __syncthreads();
+                buf ^= 1;
+            }
+        }
+    }
+
+    // accumulator fragment: row = lane>>2, columns 2·(lane&3) + {0,1} of each 8×8 tile
+    const int er = lane >> 2, ec = 2 * (lane & 3);
+    if (EPI == DEPI_STORE) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t gi = m0 + wm * 32 + i * 8 + er;
+            if (gi >= M) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t gj = n0 + wn * 32 + j * 8 + ec + h;
+                    if (gj >= N) continue;
+                    if (split) {
+                        partial[(int64_t)blockIdx.z * M * N + gi + gj * M] = acc[i][j][h];
+                    } else {
+                        double* cp = C + gi + gj * ldc;
+                        *cp = beta == 0.0 ? alpha * acc[i][j][h] : fma(beta, *cp, alpha * acc[i][j][h]);
+                    }
+                }
+        }
+    } else if (EPI == DEPI_ROWSQ) {
+        // out-of-range columns hold exact zeros (zero-filled operands)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            double s = 0.0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) s = fma(acc[i][j][0], acc[i][j][0], fma(acc[i][j][1], acc[i][j][1], s));
+            s += __shfl_xor_sync(0xffffffffu, s, 1);
+            s += __shfl_xor_sync(0xffffffffu, s, 2);
+            if ((lane & 3) == 0) red[wn][wm * 32 + i * 8 + er] = s;
+        }
+        __syncthreads();
+        for (int i = tid; i < DBM; i += DNT) {
+            const int64_t gi = m0 + i;
+            if (gi < M) partial[(int64_t)blockIdx.y * M + gi] = red[0][i] + red[1][i];
+        }
+    } else {  // DEPI_RESID
+        double s = 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t gi = m0 + wm * 32 + i * 8 + er;
+            if (gi >= M) continue;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int64_t gj = n0 + wn * 32 + j * 8 + ec + h;
+                    if (gj >= N) continue;
+                    const double d = dtd == BCUR_F32 ? (double)((const float*)D)[gi + gj * ldd]
+                                                     : ((const double*)D)[gi + gj * ldd];
+                    const double e = d - acc[i][j][h];
+                    s = fma(e, e, s);
+                }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) red[0][warp] = s;
+        __syncthreads();
+        if (tid == 0)
+            partial[(int64_t)blockIdx.x + (int64_t)blockIdx.y * gridDim.x] = (red[0][0] + red[0][1]) + (red[0][2] + red[0][3]);
+    }
+}
+
+// C = alpha·Σ_z partial[z] + beta·C  (fixed order ⇒ deterministic)
+__global__ void k_dsplitk_reduce(int64_t M, int64_t N, int splits, const double* __restrict__ partial, double alpha,
+                                 double beta, double* __restrict__ C, int64_t ldc, int sym_upper) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= M * N) return;
+    const int64_t i = idx % M, j = idx / M;
+    if (sym_upper && i / DBM >= j / DBN + 1) return;  // tiles the product skipped
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += partial[(int64_t)z * M * N + idx];
+    double* cp = C + i + j * ldc;
+    *cp = beta == 0.0 ? alpha * s : fma(beta, *cp, alpha * s);
+}
+
+__global__ void k_dsum_rows(int64_t M, int tiles, const double* __restrict__ partial, double* __restrict__ out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= M) return;
+    double s = 0.0;
+    for (int t = 0; t < tiles; ++t) s += partial[(int64_t)t * M + i];
+    out[i] = s;
+}
+
+template <typename TA, typename TB, int EPI>
+void dlaunch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
+             const void* A, int64_t lda, const void* B, int64_t ldb, double beta, double* C, int64_t ldc,
+             double* partial, const void* D, int dtd, int64_t ldd, int flags) {
+#define BCUR_DGEMM_CASE(TRA, TRB)                                                                                  \
+    k_dgemm<TA, TB, TRA, TRB, EPI><<<grid, DNT, 0, c->stream>>>(M, N, K, kchunk, alpha, (const TA*)A, lda,          \
+                                                                 (const TB*)B, ldb, beta, C, ldc, partial, D, dtd, \
+                                                                 ldd, flags)
+    if (ta == ops::OP_N && tb == ops::OP_N) BCUR_DGEMM_CASE(0, 0);
+    else if (ta == ops::OP_N && tb == ops::OP_T) BCUR_DGEMM_CASE(0, 1);
+    else if (ta == ops::OP_T && tb == ops::OP_N) BCUR_DGEMM_CASE(1, 0);
+    else BCUR_DGEMM_CASE(1, 1);
+#undef BCUR_DGEMM_CASE
+    LAUNCH_CHECK(c);
+}
+
+template <int EPI>
+void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, int64_t K, int64_t kchunk,
+               double alpha, const void* A, int dta, int64_t lda, const void* B, int dtb, int64_t ldb, double beta,
+               double* C, int64_t ldc, double* partial, const void* D, int dtd, int64_t ldd, int flags) {
+    if (dta == BCUR_F32 && dtb == BCUR_F32)
+        dlaunch<float, float, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
+                                   dtd, ldd, flags);
+    else if (dta == BCUR_F32)
+        dlaunch<float, double, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
+                                    dtd, ldd, flags);
+    else if (dtb == BCUR_F32)
+        dlaunch<double, float, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
+                                    dtd, ldd, flags);
+    else
+        dlaunch<double, double, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial,
+                                     D, dtd, ldd, flags);
+}
+
+// ------------------------------------------- fused Cholesky + inverse (w ≤ 128)
+// G (upper triangle read) → R upper with G = RᵀR and X = R⁻¹, one CTA of 256 threads.
+// Factor: right-looking 32-column panels on the lower triangle L = Rᵀ held in shared memory
+// (warp 0 factors the 32×32 diagonal block in registers, one thread per row solves the panel,
+// all warps apply the rank-32 update).  Inverse, in the free upper triangle of the same
+// array: the diagonal 32-blocks X_bb by one warp each (lane = column, back substitution in
+// registers), then the off-diagonal blocks by superdiagonal, X_ij = −X_ii·Σ_{i<l≤j} R_il·X_lj.
+// Status: chained (part of a recursive factorization) — skip when *info != 0 on entry,
+// failures report info_offset + j + 1, diag[0] = running min diag(R).
+constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 1;
+
+__device__ __forceinline__ double lf_rsqrt(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double hx = 0.5 * x;
+    r = r * fma(-hx * r, r, 1.5);
+    r = r * fma(-hx * r, r, 1.5);
+    return r;
+}
+
+__global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict__ g, int w, int64_t ldg,
+                                                        double* __restrict__ r, int64_t ldr, double* __restrict__ x,
+                                                        int64_t ldx, int* info, double* diag, int info_offset) {
+    extern __shared__ double smlf[];
+    double* M = smlf;                       // M[i + k·LD]: i ≥ k → L = Rᵀ; i < k → X[i][k]
+    double* Tb = smlf + LF_MAX * LF_LD;     // 3 × 32 × 33 temporaries of the inverse
+    __shared__ double invd[LF_MAX];
+    __shared__ double xch[32];
+    __shared__ int stop_sh;
+    __shared__ double mn_sh;
+    if (*info != 0) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wp = (w + 31) & ~31;
+    for (int k = warp; k < wp; k += LF_T / 32)
+        for (int i = lane; i <= k; i += 32)
+            M[k + i * LF_LD] = (i < w && k < w) ? g[i + (int64_t)k * ldg] : (i == k ? 1.0 : 0.0);
+    if (tid == 0) {
+        stop_sh = 0;
+        mn_sh = INFINITY;
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < wp; c0 += 32) {
+        if (warp == 0) {
+            double a[32];
+#pragma unroll
+            for (int k = 0; k < 32; ++k) a[k] = M[(c0 + lane) + (c0 + k) * LF_LD];
+            int bad = 0;
+            double mn = INFINITY, dl = 1.0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const double d = __shfl_sync(0xffffffffu, a[j], j);
+                if (!bad && (!(d > 0.0) || !isfinite(d))) bad = c0 + j + 1;
+                if (bad) continue;
+                const double ri = lf_rsqrt(d), rj = d * ri;
+                if (c0 + j < w) mn = fmin(mn, rj);
+                if (lane == j) dl = ri;
+                const double lij = a[j] * ri;
+                a[j] = lane == j ? rj : lij;
+                xch[lane] = lij;
+                __syncwarp();
+#pragma unroll
+                for (int k = j + 1; k < 32; ++k) a[k] = fma(-lij, xch[k], a[k]);
+                __syncwarp();
+            }
+            if (!bad) {
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    if (k <= lane) M[(c0 + lane) + (c0 + k) * LF_LD] = a[k];
+                invd[c0 + lane] = dl;
+            }
+            if (lane == 0) {
+                if (bad) stop_sh = bad;
+                mn_sh = fmin(mn_sh, mn);
+            }
+        }
+        __syncthreads();
+        if (stop_sh) break;
+        const int base = c0 + 32, nr = wp - base;
+        if (nr <= 0) break;
+        if (tid < nr) {  // panel solve, right-looking (2 dependent ops per column)
+            const int i = base + tid;
+            double xr[32];
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) xr[cc] = M[i + (c0 + cc) * LF_LD];
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) {
+                xr[cc] *= invd[c0 + cc];
+#pragma unroll
+                for (int c2 = cc + 1; c2 < 32; ++c2) xr[c2] = fma(-xr[cc], M[(c0 + c2) + (c0 + cc) * LF_LD], xr[c2]);
+            }
+#pragma unroll
+            for (int cc = 0; cc < 32; ++cc) M[i + (c0 + cc) * LF_LD] = xr[cc];
+        }
+        __syncthreads();
+        {   // trailing lower-triangle update with 6×6 register tiles
+            const int ty = tid >> 4, tx = tid & 15;
+            double acc[6][6];
+#pragma unroll
+            for (int u = 0; u < 6; ++u)
+#pragma unroll
+                for (int v = 0; v < 6; ++v) acc[u][v] = 0.0;
+#pragma unroll 4
+            for (int cc = 0; cc < 32; ++cc) {
+                const double* col = M + (c0 + cc) * LF_LD + base;
+                double li[6], lk[6];
+#pragma unroll
+                for (int u = 0; u < 6; ++u) {
+                    li[u] = (ty + 16 * u) < nr ? col[ty + 16 * u] : 0.0;
+                    lk[u] = (tx + 16 * u) < nr ? col[tx + 16 * u] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 6; ++u)
+#pragma unroll
+                    for (int v = 0; v < 6; ++v) acc[u][v] = fma(li[u], lk[v], acc[u][v]);
+            }
+#pragma unroll
+            for (int u = 0; u < 6; ++u)
+#pragma unroll
+                for (int v = 0; v < 6; ++v) {
+                    const int i = ty + 16 * u, k = tx + 16 * v;
+                    if (i < nr && k <= i) M[(base + i) + (base + k) * LF_LD] -= acc[u][v];
+                }
+        }
+        __syncthreads();
+    }
+    const int stop = stop_sh;
+    if (!stop) {
+        const int nb = wp / 32;
+        // (a) diagonal blocks: warp b solves R_bb·x = e_c for lane c (back substitution)
+        if (warp < nb) {
+            const int b0 = warp * 32;
+            double xv[32];
+#pragma unroll
+            for (int t = 0; t < 32; ++t) xv[t] = t == lane ? 1.0 : 0.0;
+#pragma unroll
+            for (int t = 31; t >= 0; --t) {
+                xv[t] *= invd[b0 + t];
+#pragma unroll
+                for (int i = 0; i < t; ++i) xv[i] = fma(-M[(b0 + t) + (b0 + i) * LF_LD], xv[t], xv[i]);  // R[i][t]
+            }
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (i < lane) M[(b0 + i) + (b0 + lane) * LF_LD] = xv[i];
+        }
+        __syncthreads();
+        // (b) off-diagonal blocks, superdiagonal by superdiagonal
+        for (int d = 1; d < nb; ++d) {
+            const int nblk = nb - d;
+            // T = Σ_{l=i+1..j} R_il·X_lj for each block (i, j = i + d)
+            for (int e = tid; e < nblk * 1024; e += LF_T) {
+                const int bi = e >> 10, rr = (e >> 5) & 31, cc = e & 31;
+                const int i0 = bi * 32, j0 = (bi + d) * 32;
+                const int gr = i0 + rr, gc = j0 + cc;
+                double s = 0.0;
+                for (int t = i0 + 32; t <= gc; ++t) {
+                    const double xt = t == gc ? invd[gc] : M[t + gc * LF_LD];  // X[t][gc], t ≤ gc
+                    s = fma(M[t + gr * LF_LD], xt, s);                           // R[gr][t] = L[t][gr]
+                }
+                Tb[bi * 32 * 33 + rr * 33 + cc] = s;
+            }
+            __syncthreads();
+            // X_ij = −X_ii·T
+            for (int e = tid; e < nblk * 1024; e += LF_T) {
+                const int bi = e >> 10, rr = (e >> 5) & 31, cc = e & 31;
+                const int i0 = bi * 32, j0 = (bi + d) * 32;
+                const int gr = i0 + rr;
+                double s = invd[gr] * Tb[bi * 32 * 33 + rr * 33 + cc];
+                for (int u = rr + 1; u < 32; ++u) s = fma(M[gr + (i0 + u) * LF_LD], Tb[bi * 32 * 33 + u * 33 + cc], s);
+                M[gr + (j0 + cc) * LF_LD] = -s;
+            }
+            __syncthreads();
+        }
+    }
+    for (int k = warp; k < w; k += LF_T / 32)
+        for (int i = lane; i < w; i += 32) {
+            r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * LF_LD] : 0.0;
+            x[i + (int64_t)k * ldx] = stop ? 0.0 : (i < k ? M[i + k * LF_LD] : (i == k ? invd[i] : 0.0));
+        }
+    if (tid == 0) {
+        if (stop) *info = info_offset + stop;
+        diag[0] = stop ? 0.0 : fmin(diag[0], mn_sh);
+    }
+}
+
+// st = {info, pad, min diag(R) (running), max diag(G)}
+__global__ void k_chol_status_init(const double* __restrict__ g, int64_t w, int64_t ldg, int* st) {
+    __shared__ double red[32];
+    double mx = 0.0;
+    for (int64_t i = threadIdx.x; i < w; i += blockDim.x) mx = fmax(mx, g[i + i * ldg]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmax(mx, red[i]);
+        st[0] = 0;
+        st[1] = 0;
+        reinterpret_cast<double*>(st)[1] = INFINITY;
+        reinterpret_cast<double*>(st)[2] = mx;
+    }
+}
+
+}  // namespace
+
+namespace ops {
+
+static int dgemm_splits(const Ctx* c, int64_t tiles, int64_t K) {
+    const int64_t target = 2LL * c->sm_count;
+    if (tiles >= target || K < 8 * DBK) return 1;
+    int64_t s = std::min<int64_t>((target + tiles - 1) / tiles, K / (8 * DBK));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(s, 256));
+}
+
+void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
+           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags) {
+    if (M <= 0 || N <= 0) return;
+    ProfScope prof(c, "dgemm_dmma", 2.0 * M * N * std::max<int64_t>(K, 0),
+                   (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M * N);
+    if (K <= 0) {
+        if (beta == 0.0) {
+            CUDA_CHECK(cudaMemset2DAsync(C, ldc * sizeof(double), 0, M * sizeof(double), N, c->stream));
+            return;
+        }
+        K = 0;
+    }
+    const int64_t mt = (M + DBM - 1) / DBM, nt = (N + DBN - 1) / DBN;
+    int64_t tiles = mt * nt;
+    if (flags & GEMM_SYM_UPPER) tiles = (tiles + std::min(mt, nt)) / 2;
+    int splits = dgemm_splits(c, tiles, K);
+    int64_t kchunk = (std::max<int64_t>(K, 1) + splits - 1) / splits;
+    kchunk = (kchunk + DBK - 1) / DBK * DBK;
+    splits = (int)((std::max<int64_t>(K, 1) + kchunk - 1) / kchunk);
+    dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
+    if (splits == 1) {
+        ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, dta, lda, B, dtb, ldb, beta, C, ldc, nullptr,
+                              nullptr, 0, 0, flags);
+        return;
+    }
+    DevBuf part(c, (size_t)splits * M * N * sizeof(double));
+    ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, 1.0, A, dta, lda, B, dtb, ldb, 0.0, nullptr, 0,
+                          part.as<double>(), nullptr, 0, 0, flags);
+    const int64_t total = M * N;
+    k_dsplitk_reduce<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
+        M, N, splits, part.as<double>(), alpha, beta, C, ldc, (flags & GEMM_SYM_UPPER) ? 1 : 0);
+    LAUNCH_CHECK(c);
+}
+
+void dgemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
+                    const void* B, int dtb, int64_t ldb, double* rowsq) {
+    if (M <= 0) return;
+    ProfScope prof(c, "dgemm_rowsq_dmma", 2.0 * M * N * K,
+                   (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + 8.0 * M);
+    if (N <= 0 || K <= 0) {
+        CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
+        return;
+    }
+    const int64_t mt = (M + DBM - 1) / DBM, nt = (N + DBN - 1) / DBN;
+    DevBuf part(c, (size_t)nt * M * sizeof(double));
+    dim3 grid((unsigned)mt, (unsigned)nt, 1);
+    ddispatch<DEPI_ROWSQ>(c, ta, tb, grid, M, N, K, K, 1.0, A, dta, lda, B, dtb, ldb, 0.0, nullptr, 0,
+                          part.as<double>(), nullptr, 0, 0, 0);
+    k_dsum_rows<<<(unsigned)((M + 255) / 256), 256, 0, c->stream>>>(M, (int)nt, part.as<double>(), rowsq);
+    LAUNCH_CHECK(c);
+}
+
+void dgemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
+                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out) {
+    ProfScope prof(c, "dgemm_resid_dmma", 2.0 * M * N * K,
+                   (double)M * K * dtype_size(dta) + (double)K * N * dtype_size(dtb) + (double)M * N * dtype_size(dtd));
+    const int64_t mt = (M + DBM - 1) / DBM, nt = (N + DBN - 1) / DBN;
+    DevBuf part(c, (size_t)mt * nt * sizeof(double));
+    dim3 grid((unsigned)mt, (unsigned)nt, 1);
+    ddispatch<DEPI_RESID>(c, ta, tb, grid, M, N, std::max<int64_t>(K, 0), std::max<int64_t>(K, 1), 1.0, A, dta, lda, B,
+                          dtb, ldb, 0.0, nullptr, 0, part.as<double>(), D, dtd, ldd, 0);
+    sum_vector(c, part.as<double>(), mt * nt, out);
+}
+
+void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st) {
+    k_chol_status_init<<<1, 256, 0, c->stream>>>(g, w, ldg, st);
+    LAUNCH_CHECK(c);
+}
+
+void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int64_t ldr, double* x, int64_t ldx,
+                   int* info, double* diag, int64_t info_offset) {
+    if (w > LF_MAX || w < 1) fail(BCUR_E_INVALID_ARGUMENT, "chol_inv_leaf: 1 <= w <= 128");
+    ProfScope prof(c, "chol_inv_leaf", 2.0 * w * w * w / 3.0, 8.0 * 3 * w * w);
+    constexpr size_t smem = (size_t)(LF_MAX * LF_LD + 3 * 32 * 33) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_chol_inv_leaf<<<1, LF_T, smem, c->stream>>>(g, (int)w, ldg, r, ldr, x, ldx, info, diag, (int)info_offset);
+    LAUNCH_CHECK(c);
+}
+
+}  // namespace ops
+}  // namespace bcur_b200

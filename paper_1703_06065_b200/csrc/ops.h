@@ -41,7 +41,10 @@ void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out);
 //   GEMM_B_UPPER    op(B) is upper triangular
 //   GEMM_X1         the product is a small correction (‖op(B)‖ ≲ 1e-4): one round-to-nearest
 //                   TF32 pass suffices (errors ~1e-4 × the correction)
-enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2, GEMM_X1 = 4 };
+//   GEMM_A_UPPER / GEMM_A_LOWER / GEMM_B_LOWER   op(A) upper / lower, op(B) lower triangular
+//                   (the fp64 DMMA path skips the zero blocks)
+enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2, GEMM_X1 = 4, GEMM_A_UPPER = 8, GEMM_A_LOWER = 16,
+                 GEMM_B_LOWER = 32 };
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags = 0);
 // rowsq[i] = Σ_j (op(A)·op(B))(i,j)²   (product never stored)
@@ -64,13 +67,21 @@ void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float
 void gemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
 
-// ---- cuBLAS DGEMM for plain fp64 products (blas.cu) -----------------------
-void cublas_dgemm(Ctx* c, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
-                  int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
-
-// C(upper) = alpha·AᵀA + beta·C(upper)  (A k×n)
-void cublas_dsyrk_upper_t(Ctx* c, int64_t n, int64_t k, double alpha, const double* A, int64_t lda, double beta,
-                          double* C, int64_t ldc);
+// ---- fp64 tensor-core products (kernels_dmma.cu, mma.sync m8n8k4 .f64) -----
+// C = alpha·op(A)·op(B) + beta·C, fp32/fp64 operands, fp64 accumulation; flags as gemm()
+void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
+           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags = 0);
+void dgemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
+                    const void* B, int dtb, int64_t ldb, double* rowsq);
+void dgemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const void* A, int dta, int64_t lda,
+                       const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
+// st = {int info, int pad, double min diag(R) = +inf, double max diag(G)} before a factorization
+void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st);
+// w ≤ 128, one CTA: R (upper, lower zeroed) with G = RᵀR from G's upper triangle, and X = R⁻¹
+// (upper).  Chained status: skipped when *info != 0; failure → info = info_offset + j + 1;
+// diag[0] = running min diag(R).
+void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int64_t ldr, double* x, int64_t ldx,
+                   int* info, double* diag, int64_t info_offset);
 
 // ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
 bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);

@@ -50,7 +50,7 @@ void allreduce(Ctx* c, double* d, int64_t count) {
 }
 
 double tau_chol(int dt) { return dt == BCUR_F32 ? 1e-2 : 1e-5; }
-double tau_rank(int dt) { return dt == BCUR_F32 ? 3e-4 : 1e-7; }
+double tau_rank(int dt) { return dt == BCUR_F32 ? 1e-5 : 1e-7; }
 double theta_explicit(int dt) { return dt == BCUR_F32 ? 0.1 : 1e-6; }
 double tau_saturate(int dt) { return dt == BCUR_F32 ? 1e-6 : 1e-12; }
 
@@ -100,170 +100,95 @@ struct CholInfo {
 
 static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X, const double* dinv = nullptr);
 
-// G (w×w SPD, fp64) → R upper (w×w, ld w) with G = RᵀR.  Single CTA up to 144,
-// blocked right-looking (128-wide diagonal blocks + fp64 product updates) beyond.
-// dinv (nullable, 128 × w, ld 128): receives the inverses of the diagonal blocks, which
-// the panel updates need anyway and tri_inv_any can reuse.
-// Rinv (nullable, w × w, ld w): also R⁻¹ (valid when info == 0).  Beyond 144 it is assembled
-// block column by block column alongside the factorization on a third stream —
-// X[:k, k] = −X[:k, :k]·R[:k, k]·R_kk⁻¹ once block row k is final — off the serial chain
-// (a blocked back-substitution afterwards added 32 dependent steps at w = 4096).
-static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* dinv = nullptr,
-                         double* Rinv = nullptr) {
+// Recursive Cholesky with the inverse alongside (fp64, all on the device):
+//   chol_inv([G11 G12; · G22]) :  (R11, X11) = chol_inv(G11)
+//                                 R12 = X11ᵀ·G12                 (DMMA, op(A) lower)
+//                                 G22 −= R12ᵀ·R12                (DMMA, upper tiles only)
+//                                 (R22, X22) = chol_inv(G22)
+//                                 X12 = −(X11·R12)·X22           (X11·R12 on a side stream,
+//                                                                 overlapping the G22 branch)
+// down to ≤ 128-wide leaves factored and inverted by one CTA each (kernels_dmma.cu).  The
+// critical path is the 32 leaves of a 4096-wide Gram and the big products between them; no
+// host round trip until the final status read (the blocked right-looking chain it replaces
+// issued ~6 small dependent kernels per 128 columns).
+struct CholRec {
+    Ctx* c;
+    double *W, *R, *X;
+    int64_t w;
+    int* st;
+    cudaStream_t main_s, side_s;
+    size_t ev = 0;
+};
+
+static void chol_rec(CholRec& S, int64_t o, int64_t n) {
+    Ctx* c = S.c;
+    const int64_t w = S.w;
+    auto at = [&](double* p, int64_t i, int64_t j) { return p + i + j * w; };
+    if (n <= 128) {
+        chol_inv_leaf(c, at(S.W, o, o), n, w, at(S.R, o, o), w, at(S.X, o, o), w, S.st,
+                      reinterpret_cast<double*>(S.st) + 1, o);
+        return;
+    }
+    const int64_t nl = (n + 127) / 128, n1 = (nl + 1) / 2 * 128, n2 = n - n1, o2 = o + n1;
+    chol_rec(S, o, n1);
+    // R12 = X11ᵀ·G12
+    dgemm(c, OP_T, OP_N, n1, n2, n1, 1.0, at(S.X, o, o), BCUR_F64, w, at(S.W, o, o2), BCUR_F64, w, 0.0,
+          at(S.R, o, o2), w, GEMM_A_LOWER);
+    const cudaEvent_t e_r12 = c->sync_event(S.ev++), e_t = c->sync_event(S.ev++);
+    CUDA_CHECK(cudaEventRecord(e_r12, S.main_s));
+    CUDA_CHECK(cudaStreamWaitEvent(S.side_s, e_r12, 0));
+    c->stream = S.side_s;  // T = X11·R12 into G12's place (G12 is consumed)
+    dgemm(c, OP_N, OP_N, n1, n2, n1, 1.0, at(S.X, o, o), BCUR_F64, w, at(S.R, o, o2), BCUR_F64, w, 0.0,
+          at(S.W, o, o2), w, GEMM_A_UPPER);
+    CUDA_CHECK(cudaEventRecord(e_t, S.side_s));
+    c->stream = S.main_s;
+    // Schur complement G22 −= R12ᵀ·R12 (upper triangle)
+    dgemm(c, OP_T, OP_N, n2, n2, n1, -1.0, at(S.R, o, o2), BCUR_F64, w, at(S.R, o, o2), BCUR_F64, w, 1.0,
+          at(S.W, o2, o2), w, GEMM_SYM_UPPER);
+    chol_rec(S, o2, n2);
+    CUDA_CHECK(cudaStreamWaitEvent(S.main_s, e_t, 0));
+    c->retag(S.side_s, S.main_s);
+    // X12 = −T·X22
+    dgemm(c, OP_N, OP_N, n1, n2, n2, -1.0, at(S.W, o, o2), BCUR_F64, w, at(S.X, o2, o2), BCUR_F64, w, 0.0,
+          at(S.X, o, o2), w, GEMM_B_UPPER);
+}
+
+// G (w×w SPD, fp64, upper triangle read) → R upper (w×w, ld w, lower zero) with G = RᵀR, and
+// (Rinv nullable) X = R⁻¹ (upper, ld w).  info != 0: the pivot info − 1 failed (R, X invalid).
+static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv = nullptr) {
     DevBuf st(c, 64);
     struct { int info; int pad; double mindiag, maxdiag; } hs;
-    if (w <= 144) {
-        cholesky_upper(c, G, w, ldg, R, w, st.as<int>(), st.as<double>() + 1);
-        // the inverse is enqueued before the status read (unused if the factorization failed),
-        // so the device does not idle through the host round trip between the two kernels
-        if (Rinv) tri_inv_any(c, R, w, Rinv, nullptr);
-        d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
-        return {hs.info, hs.mindiag, hs.maxdiag};
+    chol_status_init(c, G, w, ldg, st.as<int>());
+    Mat64 Xown;
+    double* X = Rinv;
+    if (!X) {
+        Xown = Mat64(c, w, w);
+        X = Xown.p();
     }
-    constexpr int64_t B = 128;
-    copy_f64(c, G, w, w, ldg, R, w);
-    CholInfo out{0, INFINITY, 0.0};
-    std::vector<double> diag(w);
-    CUDA_CHECK(cudaMemcpy2DAsync(diag.data(), sizeof(double), G, (ldg + 1) * sizeof(double), sizeof(double), w,
-                                 cudaMemcpyDeviceToHost, c->stream));
-    // device-side chain status: {info, pad, mindiag} — checked once at the end
-    struct { int info; int pad; double mindiag, maxdiag; } init{0, 0, INFINITY, 0.0};
-    CUDA_CHECK(cudaMemcpyAsync(st.ptr, &init, sizeof init, cudaMemcpyHostToDevice, c->stream));
+    if (w <= 128) {
+        chol_inv_leaf(c, G, w, ldg, R, w, X, w, st.as<int>(), st.as<double>() + 1, 0);
+    } else {
+        ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
+        Mat64 W(c, w, w);
+        copy_f64(c, G, w, w, ldg, W.p(), w);
+        CUDA_CHECK(cudaMemsetAsync(R, 0, (size_t)w * w * sizeof(double), c->stream));
+        CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)w * w * sizeof(double), c->stream));
+        cudaStream_t main_s = c->stream, side_s = c->side_stream();
+        c->order(main_s, side_s, 0);
+        CholRec S{c, W.p(), R, X, w, st.as<int>(), main_s, side_s};
+        chol_rec(S, 0, w);
+        c->stream = main_s;
+        c->order(side_s, main_s, 1);
+    }
+    CUDA_CHECK(cudaMemcpyAsync(&hs, st.ptr, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
-    for (double d : diag) out.maxdiag = std::max(out.maxdiag, d);
-    // Four streams (events order them):
-    //   M (high priority, the serial chain): chol(k) → solve of block row k's first n1 columns
-    //     → update of the next diagonal block (k+1) → chol(k+1) …
-    //   S: the rest of block row k's solve, then the rest of block row k+1's update
-    //   D: the DSYRK of the trailing matrix beyond block k+1
-    //   I: the diagonal inverses and the block columns of R⁻¹ (nothing waits for it)
-    // chol(k+1) waits for the DSYRK of step k−1 (it updated block k+1), and the first-part
-    // solve of row k+1 for S's update of that row — both a step behind, so M runs at the
-    // rate of one single-CTA factor + one small solve + one small GEMM per step.
-    Mat64 Tx, own_dinv;
-    if (Rinv && !dinv) {  // the inverse's stream keeps every diagonal inverse
-        own_dinv = Mat64(c, B, w);
-        dinv = own_dinv.p();
-    }
-    cudaStream_t caller_s = c->stream, main_s = c->hp_stream(), side_s = c->side_stream(),
-                 syrk_s = c->side_stream3(), inv_s = c->side_stream2();
-    c->order(caller_s, main_s, 4);  // the chain forks from the caller's stream (after R's initial copy)
-    c->stream = main_s;
-    cudaEvent_t ev[5][2];  // chol, first-part solve, rest solve, row-rest update, dsyrk  (× step parity)
-    for (auto& e2 : ev)
-        for (auto& e : e2) CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    enum { E_CHOL, E_TF, E_TR, E_RR, E_DS };
-    auto rec = [&](int e, int64_t step, cudaStream_t st) { CUDA_CHECK(cudaEventRecord(ev[e][step & 1], st)); };
-    auto wait = [&](cudaStream_t st, int e, int64_t step) { CUDA_CHECK(cudaStreamWaitEvent(st, ev[e][step & 1], 0)); };
-    auto on = [&](cudaStream_t st) { c->stream = st; };
-    c->order(main_s, side_s, 0);
-    c->order(main_s, syrk_s, 1);
-    if (Rinv) {
-        Tx = Mat64(c, w, B);
-        c->order(main_s, inv_s, 2);
-        on(inv_s);
-        fill_f64(c, Rinv, w * w, 0.0);
-        on(main_s);
-    }
-    static const bool tdbg = getenv("BCUR_CHOL_TIMING") != nullptr;
-    cudaEvent_t te0 = nullptr, te1 = nullptr;
-    auto th0 = std::chrono::steady_clock::now();
-    if (tdbg) {
-        CUDA_CHECK(cudaEventCreate(&te0));
-        CUDA_CHECK(cudaEventCreate(&te1));
-        CUDA_CHECK(cudaEventRecord(te0, main_s));
-    }
-    const int64_t nsteps = (w + B - 1) / B;
-    for (int64_t step = 0; step < nsteps; ++step) {
-        const int64_t k = step * B, kb = std::min(B, w - k), rest = w - k - kb;
-        double* Dk = R + k + k * w;
-        on(main_s);
-        cholesky_upper(c, Dk, kb, w, Dk, w, st.as<int>(), st.as<double>() + 1, k, true);  // in place
-        rec(E_CHOL, step, main_s);
-        if (dinv) {
-            // off the chain: the block's inverse, then block column k of R⁻¹ (R[:k, k] is final:
-            // row k−1's first-part solve ran on M, earlier rows' rest solves are covered by the
-            // S event M waited for before solving row k−1)
-            double* Ri = dinv + k * B;
-            wait(inv_s, E_CHOL, step);
-            on(inv_s);
-            tri_inv_upper(c, Dk, kb, w, Ri, B);
-            if (Rinv) {
-                copy_f64(c, Ri, kb, kb, B, Rinv + k + k * w, w);
-                if (k > 0) {
-                    gemm(c, OP_N, OP_N, k, kb, k, 1.0, Rinv, BCUR_F64, w, R + k * w, BCUR_F64, w, 0.0, Tx.p(), Tx.ld);
-                    gemm(c, OP_N, OP_N, k, kb, kb, -1.0, Tx.p(), BCUR_F64, Tx.ld, Ri, BCUR_F64, B, 0.0, Rinv + k * w,
-                         w);
-                }
-            }
-        }
-        if (rest <= 0) break;
-        const int64_t n1 = std::min(B, rest), k1 = k + kb, k2 = k1 + n1, r2 = rest - n1;
-        double* Pk = R + k + k1 * w;  // block row k, columns k1..w
-        // M: first n1 columns of row k (row k−1's rest update of them ran on S)
-        on(main_s);
-        if (step > 0) wait(main_s, E_RR, step - 1);
-        trsm_upper_t(c, Dk, kb, w, Pk, w, n1);
-        rec(E_TF, step, main_s);
-        // S: the rest of row k
-        if (r2 > 0) {
-            wait(side_s, E_CHOL, step);
-            on(side_s);
-            trsm_upper_t(c, Dk, kb, w, Pk + n1 * w, w, r2);
-            rec(E_TR, step, side_s);
-        }
-        // M: next diagonal block, after the DSYRK of step k−1 (which updated it)
-        on(main_s);
-        if (step > 0) wait(main_s, E_DS, step - 1);
-        gemm(c, OP_T, OP_N, n1, n1, kb, -1.0, Pk, BCUR_F64, w, Pk, BCUR_F64, w, 1.0, R + k1 + k1 * w, w);
-        if (r2 > 0) {
-            // S: the rest of row k+1: R[k1:k2, k2:] −= Pk[:, :n1]ᵀ·Pk[:, n1:]  (after the first-part
-            // solve and the DSYRK of step k−1, which also updated that region)
-            wait(side_s, E_TF, step);
-            if (step > 0) wait(side_s, E_DS, step - 1);
-            on(side_s);
-            gemm(c, OP_T, OP_N, n1, r2, kb, -1.0, Pk, BCUR_F64, w, Pk + n1 * w, BCUR_F64, w, 1.0, R + k1 + k2 * w, w);
-            rec(E_RR, step, side_s);
-            // D: the trailing matrix beyond block k+1
-            wait(syrk_s, E_TR, step);
-            on(syrk_s);
-            {
-                ProfScope prof(c, "dsyrk_cublas", 1.0 * r2 * r2 * kb, 8.0 * (kb * r2 + r2 * r2 / 2.0));
-                cublas_dsyrk_upper_t(c, r2, kb, -1.0, Pk + n1 * w, w, 1.0, R + k2 + k2 * w, w);
-            }
-            rec(E_DS, step, syrk_s);
-        } else {
-            // nothing beyond block k+1: keep the event chain consistent for step k+1's waits
-            on(side_s);
-            rec(E_RR, step, side_s);
-            on(syrk_s);
-            rec(E_DS, step, syrk_s);
-        }
-        on(main_s);
-    }
-    on(main_s);
-    c->order(side_s, main_s, 1);  // join before any buffer is released
-    c->order(syrk_s, main_s, 0);
-    if (dinv) c->order(inv_s, main_s, 3);
-    if (tdbg) {
-        const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
-        CUDA_CHECK(cudaEventRecord(te1, main_s));
-        CUDA_CHECK(cudaEventSynchronize(te1));
-        float gpu_ms = 0.f;
-        CUDA_CHECK(cudaEventElapsedTime(&gpu_ms, te0, te1));
-        fprintf(stderr, "chol_any w=%lld host enqueue %.3f ms, gpu %.3f ms\n", (long long)w, host_ms, gpu_ms);
-        cudaEventDestroy(te0);
-        cudaEventDestroy(te1);
-    }
-    c->order(main_s, caller_s, 5);
-    c->stream = caller_s;
-    for (auto& e2 : ev)
-        for (auto& e : e2) cudaEventDestroy(e);
-    zero_lower(c, R, w, w);
-    d2h(c, reinterpret_cast<char*>(&hs), reinterpret_cast<const char*>(st.ptr), 24);
-    out.info = hs.info;
-    out.mindiag = hs.info ? 0.0 : hs.mindiag;
-    return out;
+    return {hs.info, hs.info ? 0.0 : hs.mindiag, hs.maxdiag};
+}
+
+int cholesky_inverse(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv, double* mindiag) {
+    const CholInfo ci = chol_any(c, G, w, ldg, R, Rinv);
+    if (mindiag) *mindiag = ci.mindiag;
+    return ci.info;
 }
 
 // X = R⁻¹ for upper-triangular R (w×w, ld w).  Blocked back-substitution by block rows.
@@ -297,10 +222,10 @@ static void tri_inv_any(Ctx* c, const double* R, int64_t w, double* X, const dou
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
              int64_t ldq, bool dist, Mat64* T_out, int* path_out) {
     if (w == 0) return 0;
-    Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w), Dv(c, 128, w);
+    Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w);
     gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld);
     if (dist) allreduce(c, G.p(), w * w);
-    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Dv.p(), Ri.p());
+    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Ri.p());
     if (ref < 0) ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     int64_t r = w;
     const bool chol_ok = ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref;
@@ -323,7 +248,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
             gemm(c, OP_N, OP_T, rows, rows, w, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, Gr.p(), Gr.ld);
             {   // safely full row rank → range(X) = ℝ^rows: Q = I, T = X (no eigensolve)
                 Mat64 Rr(c, rows, rows);
-                const CholInfo cr = chol_any(c, Gr.p(), rows, Gr.ld, Rr.p(), Dv.p());
+                const CholInfo cr = chol_any(c, Gr.p(), rows, Gr.ld, Rr.p());
                 if (cr.info == 0 && std::isfinite(cr.mindiag) && cr.mindiag > tau_chol(dt) * ref) {
                     fill_f64(c, Q1.p(), rows * rows, 0.0);
                     Mat64 one(c, rows, 1);
@@ -354,7 +279,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
             copy_f64(c, U.p(), rows, r, U.ld, Q1.p(), Q1.ld);
             Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
             gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
-            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p(), R2i.p());
+            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), R2i.p());
             if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
             gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
             if (T_out) {  // T = R2 · (Q1ᵀ X)
@@ -401,7 +326,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
     gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
     if (dist) allreduce(c, G2.p(), r * r);
-    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), Dv.p(), R2i.p());
+    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), R2i.p());
     if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
     gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
     if (T_out) {
@@ -496,7 +421,7 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 // cil_pre (nullable): C already split (gathered from A's interleaved copy with its exponents).
 static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B,
                              bool keep_rinv, DevBuf* cil_pre = nullptr, DevBuf* ce_pre = nullptr) {
-    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc), R1i;
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), R1i;
     DevBuf cil, ce;
     if (cil_pre) {
         cil = std::move(*cil_pre);
@@ -507,7 +432,7 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
     umma_h3(c, false, cil.as<uint16_t>(), ce.as<int>(), rows, cc, cx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     umma_h3(c, true, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, 0.0, Q1.p(),
@@ -531,7 +456,7 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     if (near) {
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), true);
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
         if (c2.info != 0) return false;
     }
     umma_h3(c, true, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, near ? 1.0 : 0.0,
@@ -553,11 +478,11 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
                           bool keep_rinv = false) {
     if (cc == 0 || rows < cc) return false;
     if (cdt == BCUR_F32 && h3_ok(rows) && cc >= 128) return cholqr2_whole_h3(c, C, rows, cc, dist, dt, B, keep_rinv);
-    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), Dv(c, 128, cc);
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc);
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
     gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, cdt, rows, C, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
@@ -585,7 +510,7 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
         // pass is exact to ~1e-11; fp64: Q = Q1·(I − F) on DGEMM
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), cdt == BCUR_F32);
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Dv.p(), Ri.p());
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
         if (c2.info != 0) return false;
     }
     B->init(c, cdt, rows, cc);
@@ -622,7 +547,7 @@ static void a_product(Ctx* c, const DMat* a, const RoundedA* ra, bool trans, int
 }
 
 void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
-                  const RoundedA* ra) {
+                  bool rank_floor, const RoundedA* ra) {
     const int64_t m = a->m, nl = a->n;
     const int64_t ng = a->n_global > 0 ? a->n_global : a->n;
     if (k < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: k must be >= 1");
@@ -658,7 +583,9 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
     std::vector<double> sg(r);
     for (int64_t i = 0; i < r; ++i) sg[i] = std::sqrt(std::max(lh[i], 0.0));
     if (!(sg[0] > 0.0)) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
-    const double tol = std::max(1e-12 * (double)std::max(m, ng) * sg[0], tau_rank(dt) * sg[0]);
+    // the reference's rank cut (matcore.cpp:35-49); the working-precision floor is opt-in
+    double tol = 1e-12 * (double)std::max(m, ng) * sg[0];
+    if (rank_floor) tol = std::max(tol, tau_rank(dt) * sg[0]);
     int64_t rank = 0;
     while (rank < r && sg[rank] > tol) ++rank;
     const int64_t ke = std::min(k, rank);
@@ -888,7 +815,7 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
     ph.reset(new ProfScope(c, "phase:2 range_finder", 0, 0));
     Subspace sub;
-    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, &ra);
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, o.rank_floor != 0, &ra);
     ph.reset(new ProfScope(c, "phase:3 scores+draw", 0, 0));
     Mat64 sc(c, G, 1);
     block_scores(c, s, sub.v, a->n, sc.p());
@@ -1256,7 +1183,7 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
         if (st.saturated) {
             if (!have_lev) {
                 Subspace sub;
-                range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub);
+                range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, o.rank_floor != 0);
                 lev = Mat64(c, G, 1);
                 block_scores(c, s, sub.v, a->n, lev.p());
                 have_lev = true;
@@ -1323,7 +1250,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: matrix contains NaN or Inf");  // require_finite
     if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_cur: A is identically zero");
     Subspace sub;
-    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, &ra);
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, o.rank_floor != 0, &ra);
     Mat64 csc(c, Gc, 1), rsc(c, Gr, 1);
     block_scores(c, s, sub.v, nl, csc.p());
     DevBuf droff(c, (Gr + 1) * sizeof(int64_t));
@@ -1497,9 +1424,9 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         allreduce(c, TR.p(), rr * cr);
         // T⁺ = Tᵀ (T Tᵀ)⁻¹ ; (T Tᵀ)⁻¹ = R⁻¹ R⁻ᵀ with T Tᵀ = RᵀR
         auto pinv_rows = [&](const Mat64& T, int64_t rk, int64_t cols, Mat64* out_p) {
-            Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk), Dv(c, 128, rk);
+            Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk);
             gemm(c, OP_N, OP_T, rk, rk, cols, 1.0, T.p(), BCUR_F64, T.ld, T.p(), BCUR_F64, T.ld, 0.0, G.p(), G.ld);
-            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Dv.p(), Ri.p());
+            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Ri.p());
             if (ci.info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
             gemm(c, OP_N, OP_T, rk, rk, rk, 1.0, Ri.p(), BCUR_F64, Ri.ld, Ri.p(), BCUR_F64, Ri.ld, 0.0, Gi.p(), Gi.ld);
             *out_p = Mat64(c, cols, rk);

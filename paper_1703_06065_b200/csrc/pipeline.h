@@ -75,10 +75,14 @@ struct Alg1Out {
 };
 
 Shard shard_of(const DMat* a, const int64_t* offsets, int64_t G);
+// G (w×w SPD, upper read) → R (w×w, ld w, upper) with G = RᵀR and Rinv = R⁻¹ (nullable, ld w);
+// returns 0 or the failed pivot + 1 (recursive, DMMA products, ≤128-wide fused leaves)
+int cholesky_inverse(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv, double* mindiag);
 void allreduce(Ctx* c, double* d, int64_t count);
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
              int64_t ldq, bool dist, Mat64* T_out, int* path_out);
 void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
+                  bool rank_floor,
                   const RoundedA* ra = nullptr);
 void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, const double* uniforms,
                CssOut* out);

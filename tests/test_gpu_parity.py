@@ -290,3 +290,98 @@ def test_fp32_off_grid_shapes(B, m, n, s, g):
     a = lowrank(m, n, 30, "pow:1", 1e-4, 13, np.float32)
     got, ref = run_css(B, a, s, 20, 10, 1, g, O.WITHOUT_REPLACEMENT, 13)
     assert got.plan.blocks() == ref.plan.blocks()
+
+
+def run_css_forced(B, a, s, k, p, q, g, mode, seed, residual):
+    """run_css with the ABI's residual mode forced on both sides."""
+    n = a.shape[1]
+    pg, po = B.BlockPartition.equal_blocks(n, s), O.BlockPartition.equal_blocks(n, s)
+    code = {"explicit": B.L.RESID_EXPLICIT, "pythagoras": B.L.RESID_PYTHAGORAS}[residual]
+    got = B.block_css(a, pg, k, g, B.Rng(seed), p=p, q=q, mode=mode, return_c=False, residual=code)
+    ref = O.block_css(a, po, k, g, O.Rng(seed), p=p, q=q, mode=mode, residual=residual)
+    check_scores(got.scores.scores, ref.scores.scores, a.dtype)
+    assert got.plan.blocks() == ref.plan.blocks()
+    assert got.residual_path == ref.residual_path == residual
+    check_err(got.projection_error, ref.abs_err, ref.a_norm, a.dtype)
+    return got, ref
+
+
+def test_config3_shape_pythagoras_path(B):
+    # the c3 structure at 2048 × 8192 with the noise raised so that rel_err² > θ_explicit = 0.1:
+    # the residual takes the same Pythagoras path as full-size c3 (‖A‖² − the fp16 row-Σ² pass)
+    a = lowrank(2048, 8192, 50, "pow:1.5", 3e-4, 0, np.float32)
+    got, ref = run_css(B, a, 128, 50, 10, 2, 8, O.WITHOUT_REPLACEMENT, 0)
+    assert ref.residual_path == "pythagoras" and got.residual_path == "pythagoras"
+    assert got.plan.blocks() == ref.plan.blocks()
+
+
+def planted(m, n, s, heavy, r, seed, noise, dt):
+    """Low rank with coherent right factors: the rows of V in the `heavy` column blocks are
+    scaled up before orthonormalization, so block leverage is far from uniform and a wrong
+    score would change the selection (the Philox generator's V is nearly incoherent)."""
+    gen = np.random.default_rng(seed)
+    u, _ = np.linalg.qr(gen.standard_normal((m, r)))
+    v0 = gen.standard_normal((n, r))
+    for i, b in enumerate(heavy):
+        v0[b * s:(b + 1) * s] *= 4.0 + i
+    v, _ = np.linalg.qr(v0)
+    sig = 10.0 * 0.85 ** np.arange(r)
+    a = (u * sig) @ v.T + noise * gen.standard_normal((m, n))
+    return np.asfortranarray(a.astype(dt))
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_planted_heavy_blocks_coherent_leverage(B, dt):
+    s, heavy = 64, [3, 17, 40, 41, 58]
+    a = planted(768, 64 * s, s, heavy, 24, 31, 1e-3, dt)
+    got, ref = run_css(B, a, s, 20, 8, 1, 6, O.WITHOUT_REPLACEMENT, 5)
+    sc = np.asarray(ref.scores.scores)
+    assert sc[heavy].min() > 5.0 * np.median(sc)  # the planted blocks dominate
+    assert got.plan.blocks() == ref.plan.blocks()
+    assert len(set(ref.plan.blocks()) & set(heavy)) >= 2
+
+
+def test_row_scaled_fp32_dynamic_range(B):
+    # rows spanning 2^±24 inside every column (e.g. users in different units): the per-column
+    # fp16 scaling of the 3×FP16 split cannot hold the small rows' significands
+    gen = np.random.default_rng(3)
+    a = lowrank(1024, 4096, 30, "pow:1", 1e-3, 4, np.float64)
+    a *= (2.0 ** gen.uniform(-24, 24, size=1024))[:, None]
+    a = np.asfortranarray(a.astype(np.float32))
+    got, ref = run_css(B, a, 128, 20, 10, 1, 6, O.WITHOUT_REPLACEMENT, 2)
+    assert got.plan.blocks() == ref.plan.blocks()
+    cg, rg = B.BlockPartition.equal_blocks(4096, 128), B.BlockPartition.equal_blocks(1024, 128)
+    co, ro = O.BlockPartition.equal_blocks(4096, 128), O.BlockPartition.equal_blocks(1024, 128)
+    gc = B.block_cur(a, cg, rg, 20, 4, 3, B.Rng(7), p=10)
+    rc = O.block_cur_rows_cols(a, co, ro, 20, 4, 3, O.Rng(7), p=10)
+    check_scores(gc.col_scores.scores, rc.col_scores.scores, np.float32)
+    check_scores(gc.row_scores.scores, rc.row_scores.scores, np.float32)
+    check_err(gc.abs_err, rc.abs_err, rc.a_norm, np.float32)
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_steep_spectrum_keeps_k_like_the_reference(B, dt):
+    # σ_i = 0.8^i: σ_40/σ_1 ≈ 1.3e-4 — the reference's rank cut (1e-12·max(m,n)·σ₁,
+    # matcore.cpp:35-49) keeps all k = 40; the working-precision floor is opt-in only
+    a = lowrank(1024, 4096, 60, "geom:1:0.8", 0.0, 8, dt)
+    part = B.BlockPartition.equal_blocks(4096, 128)
+    ex = O.exact_subspace(a, 40)
+    got = B.block_css(a, part, 40, 4, B.Rng(1), p=10, q=2, mode=B.SamplingMode.without_replacement,
+                      return_c=False)
+    assert got.scores.normalizer == ex.k_eff == 40
+    floor = B.block_css(a, part, 40, 4, B.Rng(1), p=10, q=2, mode=B.SamplingMode.without_replacement,
+                        return_c=False, rank_floor=True)
+    ref_floor = O.block_css(a, O.BlockPartition.equal_blocks(4096, 128), 40, 4, O.Rng(1), p=10, q=2,
+                            mode=O.WITHOUT_REPLACEMENT, rank_floor=True)
+    assert floor.scores.normalizer == ref_floor.scores.normalizer
+
+
+@pytest.mark.parametrize("dt", [np.float64, np.float32])
+def test_forced_residual_paths(B, dt):
+    # the explicit streamed residual Σ(A − Q_C X)² (and Pythagoras) forced through the ABI's
+    # residual mode, on a low-noise input (rel_err ≈ 1e-3) with n ≥ 256
+    a = lowrank(1024, 4096, 20, "geom:1:0.7", 1e-5, 21, dt)
+    for mode in ("explicit", "pythagoras"):
+        if dt == np.float32 and mode == "pythagoras":
+            continue  # ‖A‖² − ‖QᵀA‖² cancels to noise in fp32 at rel_err 1e-3 (why AUTO goes explicit)
+        run_css_forced(B, a, 128, 15, 10, 1, 6, O.WITHOUT_REPLACEMENT, 4, mode)
