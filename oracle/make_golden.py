@@ -10,6 +10,9 @@
   c2.json        config 2 (fp64 64×20000 biometric surrogate, greedy 8 of 200 blocks).
   c3s.json       config-3 structure at 2048×8192 fp32 (k=50, p=10, q=2, 8 of 64 blocks).
   c4s.json       config-4 structure at 1536×2048 fp32 (30, 4 col + 3 row blocks, U = C⁺AR⁺).
+  c3.json        the headline config 3 itself (fp32 16384×65536, 32 of 512 blocks): written on
+                 the GPU box by tests/test_gpu_zfullsize.py (the device-generated A downloaded
+                 and run through the oracle; copied from gpurun_out/golden_c3.json).
   small.bcur     a 5×7 matrix (i − 2.5·j + 1/(1+i+j)) in the reference's binary format
                  (io.cpp:105-137), written by the oracle's save_matrix_binary.
 

@@ -159,3 +159,31 @@ def test_gpu_cur_matches_c4s_golden():
     assert float(np.linalg.norm(got.u)) == pytest.approx(d(g["u_fro"]), rel=1e-4)
     ref = d(g["abs_err"])
     assert abs(got.abs_err - ref) <= ERR_TOL * ref
+
+
+@pytest.mark.gpu
+def test_gpu_css_matches_c3_full_golden():
+    """The headline workload itself (16384 × 65536 fp32, device Philox) against the committed
+    oracle result tests/golden/c3.json — written on the GPU box by
+    tests/test_gpu_zfullsize.py::test_c3_full_size_matches_oracle (the oracle run on the same
+    device-generated A)."""
+    from paper_1703_06065_b200 import bcur as B
+    g = load("c3.json")
+    a = B.DeviceMatrix.generate("lowrank", np.float32, g["m"], g["n"], seed=g["seed"],
+                                sigma=O.spectrum(g["spectrum"], g["rank"]), noise=g["noise"])
+    h = a.to_host()
+    s2 = sum(float(np.einsum("ij,ij->", c, c)) for c in
+             (O.cols64(h, j0, j1) for j0, j1 in O._chunks(h)))
+    assert s2 == pytest.approx(d(g["a"]["sumsq"]), rel=1e-12)
+    assert float(h[0, 0]) == d(g["a"]["corner"][0]) and float(h[-1, -1]) == d(g["a"]["corner"][1])
+    del h
+    part = B.BlockPartition.equal_blocks(g["n"], g["s"])
+    got = B.block_css(a, part, g["k"], g["g"], B.Rng(g["seed"]), p=g["p"], q=g["q"], mode=g["mode"],
+                      return_c=False)
+    assert rel(got.scores.scores, dv(g["scores"])) <= SCORE_TOL[g["dtype"]]
+    assert got.scores.normalizer == g["normalizer"]
+    check_plan(got.plan.blocks(), g["plan"])
+    assert got.plan.blocks() == g["plan"]["blocks"]
+    ref = d(g["abs_err"])
+    assert abs(got.projection_error - ref) <= ERR_TOL * ref
+    assert got.rank_c == g["rank_c"] and got.residual_path == g["residual_path"]
