@@ -83,6 +83,11 @@ typedef struct {
     void* user;
     /* in-place sum of `count` doubles at device pointer `buf` */
     int (*allreduce_f64)(void* user, double* buf, int64_t count, void* stream);
+    /* broadcast of `bytes` bytes at device pointer `buf` from rank `root` (nullable: the
+     * library then emulates it with a zero-padded allreduce_f64 of fp64 data).  Selected
+     * column blocks of A travel through it in their stored form — fp32, or the fp16 hi/lo
+     * split of the 3×FP16 path (4 bytes per element) — not as fp64. */
+    int (*broadcast)(void* user, void* buf, int64_t bytes, int root, void* stream);
 } bcur_comm;
 bcur_status bcur_ctx_set_comm(bcur_ctx ctx, const bcur_comm* comm); /* NULL → single rank */
 

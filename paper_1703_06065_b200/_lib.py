@@ -59,10 +59,12 @@ class GenSpecC(C.Structure):
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, vp, P_dbl, i64, vp)
+BROADCAST_FN = C.CFUNCTYPE(C.c_int, vp, vp, i64, C.c_int, vp)
 
 
 class CommC(C.Structure):
-    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("user", vp), ("allreduce_f64", ALLREDUCE_FN)]
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("user", vp), ("allreduce_f64", ALLREDUCE_FN),
+                ("broadcast", BROADCAST_FN)]
 
 
 # name: (restype, argtypes)

@@ -136,17 +136,19 @@ class Context:
         L.lib.bcur_ctx_profile_dump(self.handle, buf, len(buf))
         return json.loads(buf.value.decode())
 
-    def set_comm(self, rank: int, world: int, allreduce_fn):
-        """allreduce_fn(ptr:int, count:int, stream:int) -> None (in-place sum of fp64)."""
+    def set_comm(self, rank: int, world: int, allreduce_fn, broadcast_fn=None):
+        """allreduce_fn(ptr:int, count:int, stream:int) -> None (in-place sum of fp64);
+        broadcast_fn(ptr:int, nbytes:int, root:int, stream:int) -> None (optional)."""
         if world <= 1:
             _check(L.lib.bcur_ctx_set_comm(self.handle, None))
             self._comm = None
             return
 
         fn = make_comm_callback(allreduce_fn)
-        comm = L.CommC(rank, world, None, fn)
+        bfn = make_broadcast_callback(broadcast_fn) if broadcast_fn is not None else L.BROADCAST_FN()
+        comm = L.CommC(rank, world, None, fn, bfn)
         _check(L.lib.bcur_ctx_set_comm(self.handle, C.byref(comm)))
-        self._comm = (fn, comm)  # keep alive
+        self._comm = (fn, bfn, comm)  # keep alive
 
 
 def make_comm_callback(allreduce_fn):
@@ -163,6 +165,21 @@ def make_comm_callback(allreduce_fn):
             return 1
 
     return L.ALLREDUCE_FN(cb)
+
+
+def make_broadcast_callback(broadcast_fn):
+    """C function pointer for ``bcur_comm.broadcast`` wrapping ``broadcast_fn(ptr, nbytes,
+    root, stream)``; exceptions become a nonzero return (BCUR_E_COMM)."""
+    def cb(user, buf, nbytes, root, stream):
+        try:
+            broadcast_fn(int(buf or 0), int(nbytes), int(root), stream or 0)
+            return 0
+        except Exception:
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    return L.BROADCAST_FN(cb)
 
 
 _default_ctx: Optional[Context] = None

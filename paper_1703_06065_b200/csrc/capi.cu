@@ -274,7 +274,7 @@ bcur_status bcur_ctx_set_comm(bcur_ctx ctx, const bcur_comm* comm) {
     API_BEGIN
     Ctx* c = C(ctx);
     if (!comm) {
-        c->comm = bcur_comm{0, 1, nullptr, nullptr};
+        c->comm = bcur_comm{0, 1, nullptr, nullptr, nullptr};
     } else {
         if (comm->world < 1 || comm->rank < 0 || comm->rank >= comm->world)
             fail(BCUR_E_INVALID_ARGUMENT, "bcur_comm: invalid rank/world");

@@ -1,5 +1,6 @@
 // kernels_misc.cu — layout/elementwise helpers (dtype conversion, transposes, scaling, copies).
 #include "ops.h"
+#include <cuda_fp16.h>
 
 namespace bcur_b200 {
 namespace {
@@ -82,7 +83,18 @@ inline unsigned nblk(int64_t count) { return (unsigned)((count + 255) / 256); }
 
 }  // namespace
 
+__global__ void k_f16_to_f32(const uint16_t* __restrict__ src, int64_t count, float scale, float* __restrict__ dst) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) dst[i] = __half2float(__ushort_as_half(src[i])) * scale;
+}
+
 namespace ops {
+
+void f16_to_f32(Ctx* c, const uint16_t* src, int64_t count, float scale, float* dst) {
+    if (count <= 0) return;
+    k_f16_to_f32<<<nblk(count), 256, 0, c->stream>>>(src, count, scale, dst);
+    LAUNCH_CHECK(c);
+}
 
 void convert(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd) {
     if (m * n == 0) return;

@@ -154,6 +154,8 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
 
 // ---- elementwise / layout (kernels_misc.cu) -------------------------------
 void convert(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd);
+// dst[i] = fp32(src[i] as fp16) · scale
+void f16_to_f32(Ctx* c, const uint16_t* src, int64_t count, float scale, float* dst);
 void transpose(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd);
 void zero_lower(Ctx* c, double* x, int64_t w, int64_t ld);
 void convert_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);

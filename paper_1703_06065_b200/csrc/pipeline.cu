@@ -49,6 +49,15 @@ void allreduce(Ctx* c, double* d, int64_t count) {
     if (rc != 0) fail(BCUR_E_COMM, "allreduce callback failed with code " + std::to_string(rc));
 }
 
+// In-place broadcast of `bytes` bytes from rank `root` (the host's bcur_comm.broadcast).
+static void broadcast(Ctx* c, void* buf, int64_t bytes, int root) {
+    if (c->comm.world <= 1 || bytes <= 0) return;
+    if (!c->comm.broadcast) fail(BCUR_E_COMM, "broadcast requested but no callback installed");
+    const int rc = c->comm.broadcast(c->comm.user, buf, bytes, root, c->stream);
+    if (rc != 0) fail(BCUR_E_COMM, "broadcast callback failed with code " + std::to_string(rc));
+}
+static bool can_broadcast(const Ctx* c) { return c->comm.world > 1 && c->comm.broadcast != nullptr; }
+
 double tau_chol(int dt) { return dt == BCUR_F32 ? 1e-2 : 1e-5; }
 double tau_rank(int dt) { return dt == BCUR_F32 ? 1e-5 : 1e-7; }
 double theta_explicit(int dt) { return dt == BCUR_F32 ? 0.1 : 1e-6; }
@@ -77,6 +86,21 @@ Shard shard_of(const DMat* a, const int64_t* offsets, int64_t G) {
     for (int64_t g = s.g0; g <= s.g1; ++g) local[g - s.g0] = offsets[g] - s.col0;
     s.d_local = DevBuf(a->ctx, local.size() * sizeof(int64_t));
     h2d(a->ctx, s.d_local.as<int64_t>(), local.data(), local.size());
+    Ctx* c = a->ctx;
+    s.owner.assign(G, c->comm.rank);
+    if (c->comm.world > 1) {  // which rank holds each block (shards need not be equal)
+        std::vector<double> own(G, 0.0);
+        for (int64_t g = s.g0; g < s.g1; ++g) own[g] = c->comm.rank + 1.0;
+        DevBuf d(c, G * sizeof(double));
+        h2d(c, d.as<double>(), own.data(), G);
+        allreduce(c, d.as<double>(), G);
+        d2h(c, own.data(), d.as<double>(), G);
+        for (int64_t g = 0; g < G; ++g) {
+            s.owner[g] = (int)own[g] - 1;
+            if (s.owner[g] < 0 || s.owner[g] >= c->comm.world)
+                fail(BCUR_E_DIMENSION_MISMATCH, "column shards do not tile the partition exactly once");
+        }
+    }
     return s;
 }
 
@@ -618,10 +642,23 @@ static std::vector<int64_t> unique_in_order(const std::vector<int64_t>& v) {
     return out;
 }
 
-// Replicate column block b of A (owned by one rank) as an fp64 rows × w panel.
+// Replicate column block b of A (owned by one rank) as an fp64 rows × w panel.  The block
+// travels in its stored dtype (fp32: half the bytes of the fp64 panel) through the host's
+// broadcast; without one, as a zero-padded fp64 allreduce.
 static void block_panel(Ctx* c, const DMat* a, const Shard& s, int64_t b, double* P) {
     const int64_t w = s.off_global[b + 1] - s.off_global[b];
-    if (b >= s.g0 && b < s.g1) {
+    const bool mine = b >= s.g0 && b < s.g1;
+    if (can_broadcast(c)) {
+        const size_t es = dtype_size(a->dtype);
+        DevBuf blk(c, (size_t)a->m * w * es);
+        if (mine)
+            CUDA_CHECK(cudaMemcpy2DAsync(blk.ptr, a->m * es, (const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * es,
+                                         a->ld * es, a->m * es, w, cudaMemcpyDeviceToDevice, c->stream));
+        broadcast(c, blk.ptr, (int64_t)(a->m * w * es), s.owner[b]);
+        convert_to_f64(c, blk.ptr, a->dtype, a->m, w, a->m, P, a->m);
+        return;
+    }
+    if (mine) {
         const size_t es = dtype_size(a->dtype);
         convert_to_f64(c, (const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * es, a->dtype, a->m, w,
                        a->ld, P, a->m);
@@ -641,17 +678,35 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
     int64_t cap = 0;
     for (int64_t b : blocks) cap += s.off_global[b + 1] - s.off_global[b];
     bool tried = false;
-    if (cap >= 128 && cap <= m && ra && ra->has_lo() && c->comm.world <= 1) {
+    // every rank must take the same path: with several ranks, the split path needs the
+    // broadcast and the interleaved copy on all of them
+    bool split_ok = cap >= 128 && cap <= m && ra && ra->has_lo();
+    if (c->comm.world > 1) {
+        split_ok = split_ok && can_broadcast(c);
+        Mat64 f(c, 1, 1);
+        fill_f64(c, f.p(), 1, split_ok ? 1.0 : 0.0);
+        allreduce(c, f.p(), 1);
+        double h = 0.0;
+        d2h(c, &h, f.p(), 1);
+        split_ok = h == (double)c->comm.world;
+    }
+    if (split_ok) {
         // C's 3×FP16 split is a gather of A's interleaved copy (2m halves and one exponent per
-        // column): no fp32 C, no split pass
+        // column): no fp32 C, no split pass.  Several ranks: each block is broadcast by its
+        // owner in that form (4 bytes per element, the fp32 size) and C is replicated.
         DevBuf cil(c, (size_t)m * cap * 4), ce(c, (size_t)cap * sizeof(int));
         int64_t at = 0;
         for (int64_t b : blocks) {
             const int64_t w = s.off_global[b + 1] - s.off_global[b], j0 = s.off_global[b] - s.col0;
-            CUDA_CHECK(cudaMemcpyAsync(cil.as<uint16_t>() + (size_t)at * 2 * m, ra->il.as<uint16_t>() + (size_t)j0 * 2 * m,
-                                       (size_t)w * m * 4, cudaMemcpyDeviceToDevice, c->stream));
-            CUDA_CHECK(cudaMemcpyAsync(ce.as<int>() + at, ra->exps.as<int>() + j0, (size_t)w * sizeof(int),
-                                       cudaMemcpyDeviceToDevice, c->stream));
+            uint16_t* dst = cil.as<uint16_t>() + (size_t)at * 2 * m;
+            if (b >= s.g0 && b < s.g1) {
+                CUDA_CHECK(cudaMemcpyAsync(dst, ra->il.as<uint16_t>() + (size_t)j0 * 2 * m, (size_t)w * m * 4,
+                                           cudaMemcpyDeviceToDevice, c->stream));
+                CUDA_CHECK(cudaMemcpyAsync(ce.as<int>() + at, ra->exps.as<int>() + j0, (size_t)w * sizeof(int),
+                                           cudaMemcpyDeviceToDevice, c->stream));
+            }
+            broadcast(c, dst, (int64_t)w * m * 4, s.owner[b]);
+            broadcast(c, ce.as<int>() + at, (int64_t)w * (int64_t)sizeof(int), s.owner[b]);
             at += w;
         }
         if (cholqr2_whole_h3(c, nullptr, m, cap, false, a->dtype, B, keep_rinv, &cil, &ce)) return;
@@ -733,6 +788,36 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
     double h = 0.0;
     d2h(c, &h, tot.p(), 1);
     return h;
+}
+
+// First-order correction of the row-Σ² pass's fp16 basis copy along the sketch's top-k
+// directions.  The pass reads Q̃ = rn16(Q·2¹⁴)·2⁻¹⁴ (11 significant bits): along a direction u
+// that carries a large share of ‖A‖² (the low-rank signal), ‖Q̃ᵀu‖² differs from ‖Qᵀu‖² by a
+// random ~2⁻¹¹/√(3m) relative error that does not average out over the columns of A (measured
+// 4e-6 of ‖QᵀA‖² at 2048 × 8192; profiles/r02b/diag_rowsq.log).  With U_kΣ_k from the range
+// finder (A ≈ U_kΣ_kV_kᵀ + the rest),  Σ_k σ_k²(‖Qᵀu_k‖² − ‖Q̃ᵀu_k‖²)  restores those
+// directions; what remains is spread over many directions and averages out (~1e-7).  Two
+// thin DMMA products (r × k).
+static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub) {
+    const int64_t m = B.rows, r = B.rank, ke = sub.k_eff;
+    if (r <= 0 || ke <= 0 || !B.x16.ptr || B.dt != BCUR_F32) return 0.0;
+    Mat64 US(c, m, ke), sg(c, ke, 1), W(c, r, 2 * ke), tot(c, 2, 1);
+    copy_f64(c, sub.u.p(), m, ke, sub.u.ld, US.p(), US.ld);
+    h2d(c, sg.p(), sub.sigma.data(), ke);
+    scale_columns(c, US.p(), m, ke, US.ld, sg.p());
+    DevBuf q16(c, (size_t)m * r * sizeof(float));
+    f16_to_f32(c, B.x16.as<uint16_t>(), m * r, 1.0f / 16384.0f, q16.as<float>());
+    gemm(c, OP_T, OP_N, r, ke, m, 1.0, B.buf.ptr, BCUR_F32, m, US.p(), BCUR_F64, US.ld, 0.0, W.p(), W.ld);
+    gemm(c, OP_T, OP_N, r, ke, m, 1.0, q16.ptr, BCUR_F32, m, US.p(), BCUR_F64, US.ld, 0.0, W.p() + ke * W.ld, W.ld);
+    const int64_t off[2] = {0, r};
+    DevBuf doff(c, sizeof off);
+    h2d(c, doff.as<int64_t>(), off, 2);
+    for (int half = 0; half < 2; ++half)  // ‖W_half‖_F²: per-row sums, then one segment
+        row_sumsq_blocks(c, W.p() + half * ke * W.ld, BCUR_F64, r, ke, W.ld, doff.as<int64_t>(), 1, nullptr,
+                         tot.p() + half);
+    double h[2] = {0.0, 0.0};
+    d2h(c, h, tot.p(), 2);
+    return h[0] - h[1];
 }
 
 // ‖A − Q Qᵀ A‖² (streamed: X = QᵀA, then Σ (A − Q X)² tile by tile)
@@ -830,6 +915,7 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     column_basis(c, a, s, unique_in_order(blocks), bn2, &B, false, &ra);
     ph.reset(new ProfScope(c, "phase:5 residual", 0, 0));
     double res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra);
+    if (ra.ok() && B.x16.ptr) res2 -= sketch_correction(c, B, sub);
     ph.reset();
     int path = 0;
     if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(a->dtype) * a2)) {

@@ -21,6 +21,7 @@ struct Shard {
     int64_t G = 0, g0 = 0, g1 = 0, col0 = 0, n_global = 0;
     std::vector<int64_t> off_global;  // G+1
     DevBuf d_local;                   // (g1-g0+1) offsets relative to the shard's first column
+    std::vector<int> owner;           // G: the rank holding each block
 };
 
 struct Subspace {

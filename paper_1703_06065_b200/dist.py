@@ -65,12 +65,41 @@ def torch_allreduce(device: str = "cuda", group=None) -> Callable[[int, int, int
     return allreduce
 
 
+def torch_broadcast(device: str = "cuda", group=None) -> Callable[[int, int, int, int], None]:
+    """The ``bcur_comm.broadcast`` callback over torch.distributed: ``nbytes`` bytes at
+    ``ptr`` from rank ``root``, in place (device memory on the library's stream, or host
+    memory with a CPU/gloo group)."""
+    import torch
+    import torch.distributed as dist
+
+    if device == "cpu":
+        def broadcast(ptr: int, nbytes: int, root: int, stream: int) -> None:
+            buf = (ctypes.c_uint8 * nbytes).from_address(ptr)
+            t = torch.from_numpy(np.frombuffer(buf, dtype=np.uint8))
+            dist.broadcast(t, src=root, group=group)
+        return broadcast
+
+    dev = torch.device(device) if device != "cuda" else torch.device("cuda", torch.cuda.current_device())
+
+    class _Cai:
+        def __init__(self, ptr, nbytes):
+            self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                             "version": 3, "strides": None}
+
+    def broadcast(ptr: int, nbytes: int, root: int, stream: int) -> None:
+        t = torch.as_tensor(_Cai(ptr, nbytes), device=dev)
+        with torch.cuda.stream(torch.cuda.ExternalStream(stream, device=dev)):
+            dist.broadcast(t, src=root, group=group)
+
+    return broadcast
+
+
 def attach(ctx, rank: int, world: int, device: str = "cuda", group=None) -> None:
-    """Install the torch.distributed callback on a bcur Context (world 1 → detach)."""
+    """Install the torch.distributed callbacks on a bcur Context (world 1 → detach)."""
     if world <= 1:
         ctx.set_comm(0, 1, None)
         return
-    ctx.set_comm(rank, world, torch_allreduce(device, group))
+    ctx.set_comm(rank, world, torch_allreduce(device, group), torch_broadcast(device, group))
 
 
 def max_over_ranks(value: float, device: Optional[str] = None) -> float:

@@ -65,7 +65,16 @@ def _worker(rank, world, port, q):
         # (4) a failing collective is reported, not raised through C
         bad = bcur.make_comm_callback(lambda p, c, s: (_ for _ in ()).throw(RuntimeError("boom")))
         rc_bad = bad(None, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), 1, None)
-        q.put((rank, rc, buf.tolist(), bool(np.array_equal(gathered, full)), mx, rc_bad))
+        # (5) broadcast of a selected block in its stored form (fp32 bytes, and the int32
+        # exponents of the fp16 split) from the owning rank through the C trampoline
+        bfn = bcur.make_broadcast_callback(D.torch_broadcast("cpu"))
+        blk = (np.arange(12, dtype=np.float32) * 0.5 + 1.0) if rank == 1 else np.zeros(12, dtype=np.float32)
+        rc_b = bfn(None, blk.ctypes.data, blk.nbytes, 1, None)
+        ex = np.array([3, -7, 15], dtype=np.int32) if rank == 0 else np.zeros(3, dtype=np.int32)
+        rc_b += bfn(None, ex.ctypes.data, ex.nbytes, 0, None)
+        bcast_ok = bool(np.array_equal(blk, np.arange(12, dtype=np.float32) * 0.5 + 1.0) and
+                        np.array_equal(ex, [3, -7, 15]) and rc_b == 0)
+        q.put((rank, rc, buf.tolist(), bool(np.array_equal(gathered, full)), mx, rc_bad, bcast_ok))
     finally:
         dist.destroy_process_group()
 
@@ -84,5 +93,5 @@ def test_gloo_two_rank_allreduce_callback():
         p.join(timeout=60)
         assert p.exitcode == 0
     expect = (np.arange(5) * 2 + 10.0).tolist()
-    for rank, rc, buf, gathered_ok, mx, rc_bad in results:
-        assert rc == 0 and buf == expect and gathered_ok and mx == 2.5 and rc_bad == 1
+    for rank, rc, buf, gathered_ok, mx, rc_bad, bcast_ok in results:
+        assert rc == 0 and buf == expect and gathered_ok and mx == 2.5 and rc_bad == 1 and bcast_ok

@@ -215,21 +215,20 @@ def test_bitwise_rerun_determinism(B):
     assert np.array_equal(r1.c, r2.c)
 
 
-def test_two_rank_column_sharding_matches_single_rank(B):
-    """Two contexts on one GPU play two ranks; the collective is a host rendezvous after
-    each rank synchronises its own stream (no device-side waiting between kernels)."""
+def run_ranks(B, a, s, world, call):
+    """Run `call(dm, ctx)` on `world` contexts of one GPU, each holding a contiguous column
+    shard of `a` (blocks of width s).  The collectives are a host rendezvous after each rank
+    synchronises its own stream (no device-side waiting between kernels): allreduce (fp64 sum)
+    and broadcast (bytes from the root)."""
     import ctypes
 
-    a = lowrank(384, 4096, 20, "pow:1", 1e-4, 12, np.float32)
-    s, G = 128, 32
-    part = B.BlockPartition.equal_blocks(4096, s)
-    single = B.block_css(a, part, 16, 6, B.Rng(21), p=8, q=1, mode=B.SamplingMode.without_replacement,
-                         return_c=False)
-    world = 2
+    n = a.shape[1]
+    G = n // s
     barrier = threading.Barrier(world)
     bufs = [None] * world
     results = [None] * world
     errors = []
+    traffic = [0]
 
     def worker(rank):
         try:
@@ -237,24 +236,35 @@ def test_two_rank_column_sharding_matches_single_rank(B):
             lib = B.L.lib
 
             def allreduce(ptr, count, stream):
-                import numpy as _np
-                host = _np.empty(count, dtype=_np.float64)
-                h = B.DeviceMatrix.wrap(ptr, _np.float64, count, 1, count, ctx)
+                h = B.DeviceMatrix.wrap(ptr, np.float64, count, 1, count, ctx)
                 ctx.synchronize()
-                host[:] = h.to_host()[:, 0]
-                bufs[rank] = host
+                bufs[rank] = h.to_host()[:, 0].copy()
                 barrier.wait()
-                total = bufs[0] + bufs[1]
+                total = sum(bufs)
                 barrier.wait()
                 lib.bcur_dmat_upload(ctx.handle, h.handle, total.ctypes.data_as(ctypes.c_void_p), count)
                 h.close()
 
-            ctx.set_comm(rank, world, allreduce)
-            half = 4096 // world
-            dm = B.DeviceMatrix.from_host(np.asfortranarray(a[:, rank * half:(rank + 1) * half]), ctx)
-            dm.set_shard(rank * half, 4096)
-            results[rank] = B.block_css(dm, part, 16, 6, B.Rng(21), p=8, q=1,
-                                        mode=B.SamplingMode.without_replacement, return_c=False, ctx=ctx)
+            def broadcast(ptr, nbytes, root, stream):
+                h = B.DeviceMatrix.wrap(ptr, np.float32, nbytes // 4, 1, nbytes // 4, ctx)
+                ctx.synchronize()
+                if rank == root:
+                    bufs[root] = h.to_host()[:, 0].copy()
+                    traffic[0] += nbytes
+                barrier.wait()
+                data = bufs[root]
+                barrier.wait()
+                if rank != root:
+                    lib.bcur_dmat_upload(ctx.handle, h.handle, data.ctypes.data_as(ctypes.c_void_p), nbytes // 4)
+                ctx.synchronize()
+                h.close()
+
+            ctx.set_comm(rank, world, allreduce, broadcast)
+            g0, g1 = rank * G // world, (rank + 1) * G // world
+            dm = B.DeviceMatrix.from_host(np.asfortranarray(a[:, g0 * s:g1 * s]), ctx)
+            dm.set_shard(g0 * s, n)
+            results[rank] = call(dm, ctx)
+            ctx.synchronize()
         except Exception as e:  # pragma: no cover
             errors.append(e)
             barrier.abort()
@@ -265,10 +275,57 @@ def test_two_rank_column_sharding_matches_single_rank(B):
     for t in ts:
         t.join()
     assert not errors, errors
-    for r in results:
+    return results, traffic[0]
+
+
+def test_two_rank_column_sharding_matches_single_rank(B):
+    a = lowrank(384, 4096, 20, "pow:1", 1e-4, 12, np.float32)
+    part = B.BlockPartition.equal_blocks(4096, 128)
+    kw = dict(p=8, q=1, mode=B.SamplingMode.without_replacement, return_c=False)
+    single = B.block_css(a, part, 16, 6, B.Rng(21), **kw)
+    res, _ = run_ranks(B, a, 128, 2, lambda dm, ctx: B.block_css(dm, part, 16, 6, B.Rng(21), ctx=ctx, **kw))
+    for r in res:
         assert r.plan.blocks() == single.plan.blocks()
         np.testing.assert_allclose(r.scores.scores, single.scores.scores, rtol=1e-6)
         assert r.projection_error == pytest.approx(single.projection_error, rel=1e-6)
+
+
+def test_two_rank_pythagoras_css_ships_blocks_in_split_form(B):
+    # C narrower than m: the residual takes the Pythagoras path and C's 3×FP16 split is
+    # broadcast by each selected block's owner — 4 bytes per element, no fp64 panels
+    a = lowrank(2048, 8192, 30, "pow:1", 1e-3, 5, np.float32)
+    part = B.BlockPartition.equal_blocks(8192, 128)
+    kw = dict(p=10, q=1, mode=B.SamplingMode.without_replacement, return_c=False)
+    single = B.block_css(a, part, 20, 8, B.Rng(4), **kw)
+    assert single.residual_path == "pythagoras"
+    res, traffic = run_ranks(B, a, 128, 2, lambda dm, ctx: B.block_css(dm, part, 20, 8, B.Rng(4), ctx=ctx, **kw))
+    for r in res:
+        assert r.plan.blocks() == single.plan.blocks()
+        np.testing.assert_allclose(r.scores.scores, single.scores.scores, rtol=1e-6)
+        assert r.projection_error == pytest.approx(single.projection_error, rel=1e-6)
+    assert traffic <= 2048 * 8 * 128 * 4 + 8 * 128 * 4  # m·c·4 bytes + the exponents
+
+
+def test_two_rank_greedy_matches_single_rank(B):
+    a = lowrank(1024, 4096, 30, "pow:1", 1e-4, 3, np.float32)
+    part = B.BlockPartition.equal_blocks(4096, 128)
+    single = B.greedy_select(a, part, 16, 5, seed=2, p=10)
+    res, _ = run_ranks(B, a, 128, 2, lambda dm, ctx: B.greedy_select(dm, part, 16, 5, seed=2, p=10, ctx=ctx))
+    for r in res:
+        assert r.blocks() == single.blocks()
+        assert r.abs_err == pytest.approx(single.abs_err, rel=1e-6)
+
+
+def test_two_rank_block_cur_matches_single_rank(B):
+    a = lowrank(1536, 2048, 40, "geom:1:0.97", 1e-3, 2, np.float32)
+    cg, rg = B.BlockPartition.equal_blocks(2048, 128), B.BlockPartition.equal_blocks(1536, 128)
+    single = B.block_cur(a, cg, rg, 30, 4, 3, B.Rng(11), p=10)
+    res, _ = run_ranks(B, a, 128, 2, lambda dm, ctx: B.block_cur(dm, cg, rg, 30, 4, 3, B.Rng(11), p=10, ctx=ctx))
+    for r in res:
+        assert r.col_plan.blocks() == single.col_plan.blocks()
+        assert r.row_plan.blocks() == single.row_plan.blocks()
+        assert r.abs_err == pytest.approx(single.abs_err, rel=1e-6)
+        np.testing.assert_allclose(r.u, single.u, rtol=1e-5, atol=1e-6 * np.max(np.abs(single.u)))
 
 
 # Blocked fp64 Cholesky (w > 144: 128-wide diagonal blocks, the block-row solve split between
