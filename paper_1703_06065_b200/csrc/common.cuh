@@ -61,12 +61,22 @@ struct Ctx {
     int sm_count = 148;
     int64_t launches = 0;
     bcur_comm comm{0, 1, nullptr, nullptr};
-    // free blocks by size class, each tagged with the stream its last use was enqueued on
+    // free blocks by size class, each tagged with the stream its last use was enqueued on and
+    // a release sequence number
     struct FreeBlk {
         void* p;
         cudaStream_t s;
+        uint64_t seq;
     };
     std::multimap<size_t, FreeBlk> free_list;
+    uint64_t rel_seq = 0;
+    // seen[{to, from}] = release sequence up to which `to` has waited for `from` (order())
+    std::map<std::pair<cudaStream_t, cudaStream_t>, uint64_t> seen;
+    bool safe_on(const FreeBlk& b, cudaStream_t s) const {
+        if (b.s == s) return true;
+        auto it = seen.find({s, b.s});
+        return it != seen.end() && it->second > b.seq;
+    }
     size_t pooled_bytes = 0;
     // pinned host staging for small device→host reads
     void* pinned = nullptr;
@@ -75,14 +85,14 @@ struct Ctx {
     // Workspace cache over cudaMalloc (large pages, TMA-friendly): blocks are kept in exact
     // size classes (≤ 12.5% rounding), so a repeated decomposition reuses every block and
     // never calls cudaMalloc in steady state.  Reuse is safe in stream order: a block carries
-    // the stream that was current when it was released (its last use was enqueued there), and
-    // is handed out again only on that stream — or on another one after order() has made that
-    // stream wait for it (order() re-tags the blocks released on `from` so far).
+    // the stream that was current when it was released (its last use was enqueued there) and
+    // a release sequence number; it is handed out again on that stream, or on another stream
+    // that order() has since made wait for the releasing one.
     int64_t allocs = 0, allocs_mark = 0;
     void* acquire(size_t bytes) {
         const size_t want = round(bytes);
         for (auto it = free_list.lower_bound(want); it != free_list.end() && it->first == want; ++it) {
-            if (it->second.s != stream) continue;
+            if (!safe_on(it->second, stream)) continue;
             void* p = it->second.p;
             free_list.erase(it);
             pooled_bytes -= want;
@@ -101,7 +111,7 @@ struct Ctx {
     }
     void release(void* p) {
         if (!p) return;
-        free_list.emplace(sizes[p], FreeBlk{p, stream});
+        free_list.emplace(sizes[p], FreeBlk{p, stream, rel_seq++});
         pooled_bytes += sizes[p];
     }
     void trim() {
@@ -116,7 +126,7 @@ struct Ctx {
     bool cached(size_t bytes) const {
         auto r = free_list.equal_range(round(bytes));
         for (auto it = r.first; it != r.second; ++it)
-            if (it->second.s == stream) return true;
+            if (safe_on(it->second, stream)) return true;
         return false;
     }
     static size_t round(size_t b) {
@@ -177,13 +187,10 @@ struct Ctx {
     void order(cudaStream_t from, cudaStream_t to, int slot) {
         CUDA_CHECK(cudaEventRecord(side_ev[slot], from));
         CUDA_CHECK(cudaStreamWaitEvent(to, side_ev[slot], 0));
-        retag(from, to);
+        waited(from, to);
     }
-    // blocks released on `from` so far are safe on `to` once `to` waits for `from`
-    void retag(cudaStream_t from, cudaStream_t to) {
-        for (auto& kv : free_list)
-            if (kv.second.s == from) kv.second.s = to;
-    }
+    // `to` now waits for everything enqueued on `from` so far: blocks released there are safe on `to`
+    void waited(cudaStream_t from, cudaStream_t to) { seen[{to, from}] = rel_seq; }
     // events for fork/join inside one operation (grown on demand, reused across calls)
     std::vector<cudaEvent_t> sync_events;
     cudaEvent_t sync_event(size_t i) {

@@ -45,7 +45,11 @@ __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, 
     __shared__ double red[2][DBM];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
-    const int64_t m0 = (int64_t)blockIdx.x * DBM, n0 = (int64_t)blockIdx.y * DBN;
+    // triangular operands: the tiles with the longest K range are scheduled first (the block
+    // scheduler dispatches in blockIdx order; the last wave should hold the short tiles)
+    const int64_t bx = (flags & ops::GEMM_A_LOWER) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int64_t by = (flags & ops::GEMM_B_UPPER) ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
+    const int64_t m0 = bx * DBM, n0 = by * DBN;
     const bool split = partial != nullptr && EPI == DEPI_STORE;
     // a symmetric product of which only the upper triangle is consumed: tiles strictly
     // below the diagonal are not computed (zeros into their split-K partials)
@@ -256,6 +260,8 @@ void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, 
 // Status: chained (part of a recursive factorization) — skip when *info != 0 on entry,
 // failures report info_offset + j + 1, diag[0] = running min diag(R).
 constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 1;
+__device__ int g_leaf_timing = 0;  // BCUR_LEAF_TIMING=1: thread 0 prints the phase clocks (diagnostics)
+#define LF_CLK(i) do { if (timing && threadIdx.x == 0) clk[i] = clock64(); } while (0)
 
 __device__ __forceinline__ double lf_rsqrt(double x) {
     double r;
@@ -277,16 +283,32 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
     __shared__ int stop_sh;
     __shared__ double mn_sh;
     if (*info != 0) return;
+    const int timing = g_leaf_timing;
+    long long clk[16] = {0};
+    LF_CLK(0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wp = (w + 31) & ~31;
-    for (int k = warp; k < wp; k += LF_T / 32)
-        for (int i = lane; i <= k; i += 32)
-            M[k + i * LF_LD] = (i < w && k < w) ? g[i + (int64_t)k * ldg] : (i == k ? 1.0 : 0.0);
+    // the (padded) square in 8-deep batches of independent loads (a loop over one column at
+    // a time left each warp with ~40 dependent L2 round trips)
+    for (int q0 = 0; q0 < LF_MAX * LF_MAX / LF_T; q0 += 16) {
+        double v[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {  // 16 independent loads in flight (addresses clamped, no branches)
+            const int e = (q0 + q) * LF_T + tid, i = e & (LF_MAX - 1), k = e >> 7;
+            v[q] = __ldg(g + min(i, w - 1) + (int64_t)min(k, w - 1) * ldg);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int e = (q0 + q) * LF_T + tid, i = e & (LF_MAX - 1), k = e >> 7;
+            if (k < wp && i <= k) M[k + i * LF_LD] = (i < w && k < w) ? v[q] : (i == k ? 1.0 : 0.0);
+        }
+    }
     if (tid == 0) {
         stop_sh = 0;
         mn_sh = INFINITY;
     }
     __syncthreads();
+    LF_CLK(1);
     for (int c0 = 0; c0 < wp; c0 += 32) {
         if (warp == 0) {
             double a[32];
@@ -322,6 +344,7 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
             }
         }
         __syncthreads();
+        if (c0 == 0) LF_CLK(2);
         if (stop_sh) break;
         const int base = c0 + 32, nr = wp - base;
         if (nr <= 0) break;
@@ -340,37 +363,30 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
             for (int cc = 0; cc < 32; ++cc) M[i + (c0 + cc) * LF_LD] = xr[cc];
         }
         __syncthreads();
-        {   // trailing lower-triangle update with 6×6 register tiles
-            const int ty = tid >> 4, tx = tid & 15;
-            double acc[6][6];
+        if (c0 == 0) LF_CLK(3);
+        {   // trailing lower triangle −= P·Pᵀ (P = the solved panel, nr × 32) on DMMA: 8×8 tiles
+            // on or below the diagonal, round-robin over the warps, fragments from shared memory
+            const int t8 = nr >> 3, ntiles = t8 * (t8 + 1) / 2;
+            const int fr = lane >> 2, fk = lane & 3;
+            for (int t = warp; t < ntiles; t += LF_T / 32) {
+                int ti = 0;
+                while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+                const int tk = t - ti * (ti + 1) / 2;  // tk ≤ ti
+                const int ra = base + ti * 8 + fr, rb = base + tk * 8 + fr;
+                double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-            for (int u = 0; u < 6; ++u)
-#pragma unroll
-                for (int v = 0; v < 6; ++v) acc[u][v] = 0.0;
-#pragma unroll 4
-            for (int cc = 0; cc < 32; ++cc) {
-                const double* col = M + (c0 + cc) * LF_LD + base;
-                double li[6], lk[6];
-#pragma unroll
-                for (int u = 0; u < 6; ++u) {
-                    li[u] = (ty + 16 * u) < nr ? col[ty + 16 * u] : 0.0;
-                    lk[u] = (tx + 16 * u) < nr ? col[tx + 16 * u] : 0.0;
+                for (int k4 = 0; k4 < 32; k4 += 4) {
+                    const int kc = (c0 + k4 + fk) * LF_LD;
+                    dmma(d0, d1, M[ra + kc], M[rb + kc]);
                 }
-#pragma unroll
-                for (int u = 0; u < 6; ++u)
-#pragma unroll
-                    for (int v = 0; v < 6; ++v) acc[u][v] = fma(li[u], lk[v], acc[u][v]);
+                const int row = base + ti * 8 + fr, col = base + tk * 8 + 2 * fk;
+                if (col <= row) M[row + col * LF_LD] -= d0;
+                if (col + 1 <= row) M[row + (col + 1) * LF_LD] -= d1;
             }
-#pragma unroll
-            for (int u = 0; u < 6; ++u)
-#pragma unroll
-                for (int v = 0; v < 6; ++v) {
-                    const int i = ty + 16 * u, k = tx + 16 * v;
-                    if (i < nr && k <= i) M[(base + i) + (base + k) * LF_LD] -= acc[u][v];
-                }
         }
         __syncthreads();
     }
+    LF_CLK(4);
     const int stop = stop_sh;
     if (!stop) {
         const int nb = wp / 32;
@@ -391,43 +407,87 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
                 if (i < lane) M[(b0 + i) + (b0 + lane) * LF_LD] = xv[i];
         }
         __syncthreads();
-        // (b) off-diagonal blocks, superdiagonal by superdiagonal
+        LF_CLK(5);
+        // (b) off-diagonal blocks, superdiagonal by superdiagonal, on DMMA (8×8 output tiles,
+        // 16 per 32×32 block, round-robin over the warps):
+        //   T_ij = Σ_{i<l≤j} R_il·X_lj   (K = 32·d),   X_ij = −X_ii·T_ij   (K = 32)
+        const int fr = lane >> 2, fk = lane & 3;
+        constexpr int NW8 = LF_T / 32;
         for (int d = 1; d < nb; ++d) {
-            const int nblk = nb - d;
-            // T = Σ_{l=i+1..j} R_il·X_lj for each block (i, j = i + d)
-            for (int e = tid; e < nblk * 1024; e += LF_T) {
-                const int bi = e >> 10, rr = (e >> 5) & 31, cc = e & 31;
-                const int i0 = bi * 32, j0 = (bi + d) * 32;
-                const int gr = i0 + rr, gc = j0 + cc;
-                double s = 0.0;
-                for (int t = i0 + 32; t <= gc; ++t) {
-                    const double xt = t == gc ? invd[gc] : M[t + gc * LF_LD];  // X[t][gc], t ≤ gc
-                    s = fma(M[t + gr * LF_LD], xt, s);                           // R[gr][t] = L[t][gr]
+            const int nblk = nb - d, ntl = nblk * 16;
+            // two independent tiles per warp and pass (the K loops are equally long: 32·d)
+            for (int t0 = warp; t0 < ntl; t0 += 2 * NW8) {
+                const int t1 = t0 + NW8 < ntl ? t0 + NW8 : t0;
+                int gr[2], gc[2], i0[2];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int t = u ? t1 : t0, bi = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
+                    i0[u] = bi * 32;
+                    gr[u] = i0[u] + tr * 8 + fr;
+                    gc[u] = (bi + d) * 32 + tc * 8 + fr;
                 }
-                Tb[bi * 32 * 33 + rr * 33 + cc] = s;
+                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+                for (int k4 = 32; k4 < 32 * (d + 1); k4 += 4) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int tk = i0[u] + k4 + fk;
+                        const double av = M[tk + gr[u] * LF_LD];                                                // R[gr][tk]
+                        const double bv = tk < gc[u] ? M[tk + gc[u] * LF_LD] : (tk == gc[u] ? invd[tk] : 0.0);  // X[tk][gc]
+                        dmma(acc[u][0], acc[u][1], av, bv);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < (t1 != t0 ? 2 : 1); ++u) {
+                    const int t = u ? t1 : t0, bi = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
+                    double* T = Tb + bi * 32 * 33;
+                    T[(tr * 8 + fr) * 33 + tc * 8 + 2 * fk] = acc[u][0];
+                    T[(tr * 8 + fr) * 33 + tc * 8 + 2 * fk + 1] = acc[u][1];
+                }
             }
             __syncthreads();
-            // X_ij = −X_ii·T
-            for (int e = tid; e < nblk * 1024; e += LF_T) {
-                const int bi = e >> 10, rr = (e >> 5) & 31, cc = e & 31;
-                const int i0 = bi * 32, j0 = (bi + d) * 32;
-                const int gr = i0 + rr;
-                double s = invd[gr] * Tb[bi * 32 * 33 + rr * 33 + cc];
-                for (int u = rr + 1; u < 32; ++u) s = fma(M[gr + (i0 + u) * LF_LD], Tb[bi * 32 * 33 + u * 33 + cc], s);
-                M[gr + (j0 + cc) * LF_LD] = -s;
+            for (int t0 = warp; t0 < ntl; t0 += 2 * NW8) {
+                const int t1 = t0 + NW8 < ntl ? t0 + NW8 : t0;
+                double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                for (int k4 = 0; k4 < 32; k4 += 4) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        const int t = u ? t1 : t0, bi = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
+                        const int ii = bi * 32, r_ = tr * 8 + fr, uu = k4 + fk;
+                        const double av = uu > r_ ? M[(ii + r_) + (ii + uu) * LF_LD] : (uu == r_ ? invd[ii + r_] : 0.0);
+                        const double bv = Tb[bi * 32 * 33 + uu * 33 + tc * 8 + fr];
+                        dmma(acc[u][0], acc[u][1], av, bv);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < (t1 != t0 ? 2 : 1); ++u) {
+                    const int t = u ? t1 : t0, bi = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
+                    const int ii = bi * 32, jj = (bi + d) * 32, r_ = tr * 8 + fr, cc = tc * 8 + 2 * fk;
+                    M[(ii + r_) + (jj + cc) * LF_LD] = -acc[u][0];
+                    M[(ii + r_) + (jj + cc + 1) * LF_LD] = -acc[u][1];
+                }
             }
             __syncthreads();
         }
     }
-    for (int k = warp; k < w; k += LF_T / 32)
-        for (int i = lane; i < w; i += 32) {
+    LF_CLK(6);
+#pragma unroll 4
+    for (int q = 0; q < LF_MAX * LF_MAX / LF_T; ++q) {
+        const int e = q * LF_T + tid, i = e & (LF_MAX - 1), k = e >> 7;
+        if (i < w && k < w) {
             r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * LF_LD] : 0.0;
             x[i + (int64_t)k * ldx] = stop ? 0.0 : (i < k ? M[i + k * LF_LD] : (i == k ? invd[i] : 0.0));
         }
+    }
+    LF_CLK(7);
     if (tid == 0) {
         if (stop) *info = info_offset + stop;
         diag[0] = stop ? 0.0 : fmin(diag[0], mn_sh);
     }
+    if (timing && tid == 0)
+        printf("leaf w=%d clocks: load %lld | panel0 diag %lld | panel0 trsm %lld | panels rest %lld | inv diag %lld | "
+               "inv offdiag %lld | store %lld | total %lld\n", w, clk[1] - clk[0], clk[2] - clk[1], clk[3] - clk[2],
+               clk[4] - clk[3], clk[5] - clk[4], clk[6] - clk[5], clk[7] - clk[6], clk[7] - clk[0]);
 }
 
 // st = {info, pad, min diag(R) (running), max diag(G)}
@@ -536,6 +596,9 @@ void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, i
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(k_chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const char* t = getenv("BCUR_LEAF_TIMING");
+        const int on = (t && t[0] == '1') ? 1 : 0;
+        if (on) CUDA_CHECK(cudaMemcpyToSymbol(g_leaf_timing, &on, sizeof on));
         attr = true;
     }
     k_chol_inv_leaf<<<1, LF_T, smem, c->stream>>>(g, (int)w, ldg, r, ldr, x, ldx, info, diag, (int)info_offset);

@@ -141,8 +141,26 @@ struct CholRec {
     int64_t w;
     int* st;
     cudaStream_t main_s, side_s;
+    bool tc;  // products of ≥ 512-wide blocks on the tcgen05 3×FP16 kernels (fp32-class Grams)
     size_t ev = 0;
 };
+
+// op(A)·X product of the recursion: DMMA fp64, or — `tc`, both block sides ≥ 512 — the 3×FP16
+// tensor-core kernels (the Gram of an fp32 basis carries ~2⁻²² relative error already; the
+// first CholQR pass only needs R to ~1e-5, the second pass restores orthonormality).
+static void rec_gemm(CholRec& S, bool tc, Op ta, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+                     const double* X, double beta, double* C, int flags) {
+    Ctx* c = S.c;
+    if (tc) {
+        // gemm_h3: a_mn → Out(M×N) = A(M×K)·X(K×N); else Out(M×N) = Aᵀ·X with A K×M
+        if (ta == OP_N)
+            gemm_h3(c, true, A, BCUR_F64, M, K, S.w, X, BCUR_F64, N, S.w, alpha, beta, C, S.w, flags & GEMM_B_UPPER);
+        else
+            gemm_h3(c, false, A, BCUR_F64, K, M, S.w, X, BCUR_F64, N, S.w, alpha, beta, C, S.w, 0);
+        return;
+    }
+    dgemm(c, ta, OP_N, M, N, K, alpha, A, BCUR_F64, S.w, X, BCUR_F64, S.w, beta, C, S.w, flags);
+}
 
 static void chol_rec(CholRec& S, int64_t o, int64_t n) {
     Ctx* c = S.c;
@@ -154,32 +172,31 @@ static void chol_rec(CholRec& S, int64_t o, int64_t n) {
         return;
     }
     const int64_t nl = (n + 127) / 128, n1 = (nl + 1) / 2 * 128, n2 = n - n1, o2 = o + n1;
+    const bool tc = S.tc && n1 >= 512 && n2 >= 256;
     chol_rec(S, o, n1);
     // R12 = X11ᵀ·G12
-    dgemm(c, OP_T, OP_N, n1, n2, n1, 1.0, at(S.X, o, o), BCUR_F64, w, at(S.W, o, o2), BCUR_F64, w, 0.0,
-          at(S.R, o, o2), w, GEMM_A_LOWER);
+    rec_gemm(S, tc, OP_T, n1, n2, n1, 1.0, at(S.X, o, o), at(S.W, o, o2), 0.0, at(S.R, o, o2), GEMM_A_LOWER);
     const cudaEvent_t e_r12 = c->sync_event(S.ev++), e_t = c->sync_event(S.ev++);
     CUDA_CHECK(cudaEventRecord(e_r12, S.main_s));
     CUDA_CHECK(cudaStreamWaitEvent(S.side_s, e_r12, 0));
+    c->waited(S.main_s, S.side_s);
     c->stream = S.side_s;  // T = X11·R12 into G12's place (G12 is consumed)
-    dgemm(c, OP_N, OP_N, n1, n2, n1, 1.0, at(S.X, o, o), BCUR_F64, w, at(S.R, o, o2), BCUR_F64, w, 0.0,
-          at(S.W, o, o2), w, GEMM_A_UPPER);
+    rec_gemm(S, tc, OP_N, n1, n2, n1, 1.0, at(S.X, o, o), at(S.R, o, o2), 0.0, at(S.W, o, o2), GEMM_A_UPPER);
     CUDA_CHECK(cudaEventRecord(e_t, S.side_s));
     c->stream = S.main_s;
-    // Schur complement G22 −= R12ᵀ·R12 (upper triangle)
-    dgemm(c, OP_T, OP_N, n2, n2, n1, -1.0, at(S.R, o, o2), BCUR_F64, w, at(S.R, o, o2), BCUR_F64, w, 1.0,
-          at(S.W, o2, o2), w, GEMM_SYM_UPPER);
+    // Schur complement G22 −= R12ᵀ·R12 (upper triangle; the tensor-core form writes it whole)
+    rec_gemm(S, tc, OP_T, n2, n2, n1, -1.0, at(S.R, o, o2), at(S.R, o, o2), 1.0, at(S.W, o2, o2), GEMM_SYM_UPPER);
     chol_rec(S, o2, n2);
     CUDA_CHECK(cudaStreamWaitEvent(S.main_s, e_t, 0));
-    c->retag(S.side_s, S.main_s);
+    c->waited(S.side_s, S.main_s);
     // X12 = −T·X22
-    dgemm(c, OP_N, OP_N, n1, n2, n2, -1.0, at(S.W, o, o2), BCUR_F64, w, at(S.X, o2, o2), BCUR_F64, w, 0.0,
-          at(S.X, o, o2), w, GEMM_B_UPPER);
+    rec_gemm(S, tc, OP_N, n1, n2, n2, -1.0, at(S.W, o, o2), at(S.X, o2, o2), 0.0, at(S.X, o, o2), GEMM_B_UPPER);
 }
 
 // G (w×w SPD, fp64, upper triangle read) → R upper (w×w, ld w, lower zero) with G = RᵀR, and
 // (Rinv nullable) X = R⁻¹ (upper, ld w).  info != 0: the pivot info − 1 failed (R, X invalid).
-static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv = nullptr) {
+static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv = nullptr,
+                         bool tc = false) {
     DevBuf st(c, 64);
     struct { int info; int pad; double mindiag, maxdiag; } hs;
     chol_status_init(c, G, w, ldg, st.as<int>());
@@ -199,7 +216,7 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)w * w * sizeof(double), c->stream));
         cudaStream_t main_s = c->stream, side_s = c->side_stream();
         c->order(main_s, side_s, 0);
-        CholRec S{c, W.p(), R, X, w, st.as<int>(), main_s, side_s};
+        CholRec S{c, W.p(), R, X, w, st.as<int>(), main_s, side_s, tc};
         chol_rec(S, 0, w);
         c->stream = main_s;
         c->order(side_s, main_s, 1);
@@ -456,7 +473,7 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
     umma_h3(c, false, cil.as<uint16_t>(), ce.as<int>(), rows, cc, cx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true);
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     umma_h3(c, true, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, 0.0, Q1.p(),
@@ -480,7 +497,7 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     if (near) {
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), true);
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true);
         if (c2.info != 0) return false;
     }
     umma_h3(c, true, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, near ? 1.0 : 0.0,
