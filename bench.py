@@ -112,6 +112,10 @@ def workload_config(name, cfg):
            "select": cfg["select"], "mode": cfg.get("mode")}
     if cfg.get("g_rows"):
         out["g_rows"] = cfg["g_rows"]
+    if cfg.get("kind") == "lowrank":
+        out["noise"] = cfg["noise"]
+    if "residual" in cfg:
+        out["residual"] = {1: "explicit", 0: "pythagoras"}[cfg["residual"]]
     out["l2"] = ("A (%.2f GB) is larger than L2 (126 MB): re-read from HBM every step" % (bytes_a / 1e9)
                  if bytes_a > 126e6 else "A fits L2 (%.1f MB): latency-bound config" % (bytes_a / 1e6))
     return out
@@ -131,7 +135,7 @@ def run_step(B, cfg, dm, part, rpart, ctx):
                         q=cfg["q"], mode=cfg["mode"], want_u=True, ctx=ctx)
         return r.rel_err, r.col_plan.blocks() + r.row_plan.blocks()
     r = B.block_css(dm, part, cfg["k"], cfg["g"], B.Rng(cfg["seed"]), p=cfg["p"], q=cfg["q"], mode=cfg["mode"],
-                    return_c=False, ctx=ctx)
+                    return_c=False, ctx=ctx, residual=cfg.get("residual", B.L.RESID_AUTO))
     out = (r.rel_err, r.plan.blocks())
     if sel == "leverage+greedy":
         gr = B.greedy_select(dm, part, cfg["k"], cfg["g"], seed=cfg["seed"], p=cfg["p"], q=cfg["q"], ctx=ctx)
@@ -492,8 +496,15 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--residual", choices=["auto", "explicit", "pythagoras"], default="auto",
+                    help="residual path (diagnostics: the explicit tcgen05 residual on the headline shape)")
+    ap.add_argument("--noise", type=float, default=None, help="override the config's noise level (diagnostics)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config])
+    if args.residual != "auto":
+        cfg["residual"] = {"explicit": 1, "pythagoras": 0}[args.residual]
+    if args.noise is not None:
+        cfg["noise"] = args.noise
     rank, world, local_rank = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
 
     if args.impl == "reference":

@@ -23,6 +23,29 @@ __global__ void k_dmma(double* out, int iters, double a, double b) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// dependent chains: latency of one DMMA / DFMA / MUFU.RSQ64H-based rsqrt step (one warp)
+__global__ void k_lat(double* out, long long* cyc, double a, double b) {
+    double d0 = threadIdx.x * 1e-3, d1 = d0 + 1.0, x = d0 + 2.0, r = 1.0 + d0;
+    long long t0 = clock64();
+    for (int i = 0; i < 256; ++i) dmma(d0, d1, a, b);
+    long long t1 = clock64();
+    for (int i = 0; i < 256; ++i) x = fma(x, a, b);
+    long long t2 = clock64();
+    for (int i = 0; i < 256; ++i) {
+        double y;
+        asm volatile("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(r));
+        r = y + 1.0;
+    }
+    long long t3 = clock64();
+    double z = x;
+    for (int i = 0; i < 256; ++i) z = __shfl_sync(0xffffffffu, z, (threadIdx.x + 1) & 31) * a;
+    long long t4 = clock64();
+    out[threadIdx.x] = d0 + d1 + x + r + z;
+    if (threadIdx.x == 0) {
+        cyc[0] = (t1 - t0) / 256; cyc[1] = (t2 - t1) / 256; cyc[2] = (t3 - t2) / 256; cyc[3] = (t4 - t3) / 256;
+    }
+}
+
 __global__ void k_dfma(double* out, int iters, double a, double b) {
     double d[8];
 #pragma unroll
@@ -69,6 +92,13 @@ int main() {
         const double flops = 2.0 * 8 * (double)iters * (sms * 2) * (wpc / 2) * 32;
         printf("DFMA: %2d warps/SM: %.2f TF/s\n", wpc, flops / (ms * 1e-3) / 1e12);
     }
+    long long* cyc;
+    cudaMalloc(&cyc, 64);
+    for (int rep = 0; rep < 2; ++rep) k_lat<<<1, 32>>>(o, cyc, 1.0000001, 1e-9);
+    long long hc[4];
+    cudaMemcpy(hc, cyc, sizeof hc, cudaMemcpyDeviceToHost);
+    printf("latency (cycles, dependent chain): DMMA %lld  DFMA %lld  rsqrt.approx.f64+DADD %lld  SHFL(f64)+DMUL %lld\n",
+           hc[0], hc[1], hc[2], hc[3]);
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
 }

@@ -15,14 +15,14 @@
 //
 // CTA tile 64×64×16, 4 warps as 2×2, each warp 32×32 = 4×4 DMMA tiles; operands staged
 // through registers into double-buffered shared memory ([k][m] / [k][n] with a row pitch of
-// 72 doubles: the fragment loads — lane t reads row t&3, column t>>2 — take the minimum two
-// wavefronts).
+// 68 doubles ≡ 4 mod 16: the fragment loads — lane t reads row t&3, column t>>2 — take the
+// minimum two wavefronts; a pitch of 72 made them 2-way conflicted).
 #include "ops.h"
 
 namespace bcur_b200 {
 namespace {
 
-constexpr int DBM = 64, DBN = 64, DBK = 16, DNT = 128, DLD = 72;
+constexpr int DBM = 64, DBN = 64, DBK = 16, DNT = 128, DLD = 68;
 enum { DEPI_STORE = 0, DEPI_ROWSQ = 1, DEPI_RESID = 2 };
 
 template <class T>
@@ -208,6 +208,25 @@ __global__ void k_dsplitk_reduce(int64_t M, int64_t N, int splits, const double*
     *cp = beta == 0.0 ? alpha * s : fma(beta, *cp, alpha * s);
 }
 
+// the same with many splits (thin Grams: 60 × 60 over K = 16384): one warp per element, lanes
+// over the splits, a fixed shuffle tree (deterministic)
+__global__ void k_dsplitk_reduce_warp(int64_t M, int64_t N, int splits, const double* __restrict__ partial,
+                                      double alpha, double beta, double* __restrict__ C, int64_t ldc, int sym_upper) {
+    const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (idx >= M * N) return;
+    const int64_t i = idx % M, j = idx / M;
+    if (sym_upper && i / DBM >= j / DBN + 1) return;
+    double s = 0.0;
+    for (int z = lane; z < splits; z += 32) s += partial[(int64_t)z * M * N + idx];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+        double* cp = C + i + j * ldc;
+        *cp = beta == 0.0 ? alpha * s : fma(beta, *cp, alpha * s);
+    }
+}
+
 __global__ void k_dsum_rows(int64_t M, int tiles, const double* __restrict__ partial, double* __restrict__ out) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= M) return;
@@ -259,7 +278,10 @@ void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, 
 // registers), then the off-diagonal blocks by superdiagonal, X_ij = −X_ii·Σ_{i<l≤j} R_il·X_lj.
 // Status: chained (part of a recursive factorization) — skip when *info != 0 on entry,
 // failures report info_offset + j + 1, diag[0] = running min diag(R).
-constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 1;
+// Pitches ≡ 4 (mod 16) doubles: a DMMA fragment (8 rows × 4 consecutive k, or 8 columns × 4
+// k) then hits 16 distinct 8-byte bank pairs per half-warp — with an odd pitch it was 4-way
+// conflicted and the leaf's DMMA phases ran at the shared-memory wavefront rate
+constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 4, LF_TP = 36;
 __device__ int g_leaf_timing = 0;  // BCUR_LEAF_TIMING=1: thread 0 prints the phase clocks (diagnostics)
 #define LF_CLK(i) do { if (timing && threadIdx.x == 0) clk[i] = clock64(); } while (0)
 
@@ -277,7 +299,8 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
                                                         int64_t ldx, int* info, double* diag, int info_offset) {
     extern __shared__ double smlf[];
     double* M = smlf;                       // M[i + k·LD]: i ≥ k → L = Rᵀ; i < k → X[i][k]
-    double* Tb = smlf + LF_MAX * LF_LD;     // 3 × 32 × 33 temporaries of the inverse
+    double* Tb = smlf + LF_MAX * LF_LD;     // 3 × 32 × LF_TP temporaries of the inverse
+    double* Xd = Tb + 3 * 32 * LF_TP;       // 4 × 32 × LF_TP: the diagonal blocks of X as full squares
     __shared__ double invd[LF_MAX];
     __shared__ double xch[32];
     __shared__ int stop_sh;
@@ -290,17 +313,29 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
     const int wp = (w + 31) & ~31;
     // the (padded) square in 8-deep batches of independent loads (a loop over one column at
     // a time left each warp with ~40 dependent L2 round trips)
-    for (int q0 = 0; q0 < LF_MAX * LF_MAX / LF_T; q0 += 16) {
+    // the padded wp × wp square in 8-row × 4-column lane tiles (lane → row 8·ib + lane/4, column
+    // 4·kb + lane%4): the shared-memory side of both the load and the final store is then
+    // conflict-free at the 4-mod-16 pitch; batches of 16 independent global loads
+    const int nib = wp >> 3, total = wp * wp;
+    auto tile_ik = [&](int e, int& i, int& k) {
+        const int blk = e >> 5, ln = e & 31;
+        i = (blk % nib) * 8 + (ln >> 2);
+        k = (blk / nib) * 4 + (ln & 3);
+    };
+    for (int q0 = 0; q0 * LF_T < total; q0 += 16) {
         double v[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {  // 16 independent loads in flight (addresses clamped, no branches)
-            const int e = (q0 + q) * LF_T + tid, i = e & (LF_MAX - 1), k = e >> 7;
+        for (int q = 0; q < 16; ++q) {  // addresses clamped, no branches
+            int i, k;
+            tile_ik(min((q0 + q) * LF_T + tid, total - 1), i, k);
             v[q] = __ldg(g + min(i, w - 1) + (int64_t)min(k, w - 1) * ldg);
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const int e = (q0 + q) * LF_T + tid, i = e & (LF_MAX - 1), k = e >> 7;
-            if (k < wp && i <= k) M[k + i * LF_LD] = (i < w && k < w) ? v[q] : (i == k ? 1.0 : 0.0);
+            const int e = (q0 + q) * LF_T + tid;
+            int i, k;
+            tile_ik(e, i, k);
+            if (e < total && i <= k) M[k + i * LF_LD] = (i < w && k < w) ? v[q] : (i == k ? 1.0 : 0.0);
         }
     }
     if (tid == 0) {
@@ -314,18 +349,23 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
             double a[32];
 #pragma unroll
             for (int k = 0; k < 32; ++k) a[k] = M[(c0 + lane) + (c0 + k) * LF_LD];
+            // The next pivot is formed by its own lane (a[j+1] − l²) and shuffled right away, so
+            // the pivot chain is shuffle → rsqrt → multiply → FMA → shuffle, without the
+            // shared-memory exchange (which only feeds the rest of the row updates).  A failed
+            // pivot is recorded, not branched on: the NaNs it spreads are never stored.
             int bad = 0;
             double mn = INFINITY, dl = 1.0;
+            double dcur = __shfl_sync(0xffffffffu, a[0], 0);
 #pragma unroll
             for (int j = 0; j < 32; ++j) {
-                const double d = __shfl_sync(0xffffffffu, a[j], j);
-                if (!bad && (!(d > 0.0) || !isfinite(d))) bad = c0 + j + 1;
-                if (bad) continue;
+                const double d = dcur;
+                if (bad == 0 && (!(d > 0.0) || !isfinite(d))) bad = c0 + j + 1;
                 const double ri = lf_rsqrt(d), rj = d * ri;
                 if (c0 + j < w) mn = fmin(mn, rj);
                 if (lane == j) dl = ri;
                 const double lij = a[j] * ri;
                 a[j] = lane == j ? rj : lij;
+                if (j + 1 < 32) dcur = __shfl_sync(0xffffffffu, fma(-lij, lij, a[j + 1]), j + 1);
                 xch[lane] = lij;
                 __syncwarp();
 #pragma unroll
@@ -403,8 +443,11 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
                 for (int i = 0; i < t; ++i) xv[i] = fma(-M[(b0 + t) + (b0 + i) * LF_LD], xv[t], xv[i]);  // R[i][t]
             }
 #pragma unroll
-            for (int i = 0; i < 32; ++i)
+            for (int i = 0; i < 32; ++i) {
                 if (i < lane) M[(b0 + i) + (b0 + lane) * LF_LD] = xv[i];
+                // full square copy (zeros below, the diagonal): the DMMA operand of (b)
+                Xd[warp * 32 * LF_TP + i * LF_TP + lane] = i < lane ? xv[i] : (i == lane ? invd[b0 + lane] : 0.0);
+            }
         }
         __syncthreads();
         LF_CLK(5);
@@ -428,20 +471,23 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
                 }
                 double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
                 for (int k4 = 32; k4 < 32 * (d + 1); k4 += 4) {
+                    const bool diag_blk = k4 >= 32 * d;  // rows of X_jj (warp-uniform)
 #pragma unroll
                     for (int u = 0; u < 2; ++u) {
                         const int tk = i0[u] + k4 + fk;
-                        const double av = M[tk + gr[u] * LF_LD];                                                // R[gr][tk]
-                        const double bv = tk < gc[u] ? M[tk + gc[u] * LF_LD] : (tk == gc[u] ? invd[tk] : 0.0);  // X[tk][gc]
+                        const double av = M[tk + gr[u] * LF_LD];  // R[gr][tk]
+                        const int j0 = i0[u] + 32 * d;
+                        const double bv = diag_blk ? Xd[(j0 >> 5) * 32 * LF_TP + (tk - j0) * LF_TP + (gc[u] - j0)]
+                                                   : M[tk + gc[u] * LF_LD];  // X[tk][gc]
                         dmma(acc[u][0], acc[u][1], av, bv);
                     }
                 }
 #pragma unroll
                 for (int u = 0; u < (t1 != t0 ? 2 : 1); ++u) {
                     const int t = u ? t1 : t0, bi = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
-                    double* T = Tb + bi * 32 * 33;
-                    T[(tr * 8 + fr) * 33 + tc * 8 + 2 * fk] = acc[u][0];
-                    T[(tr * 8 + fr) * 33 + tc * 8 + 2 * fk + 1] = acc[u][1];
+                    double* T = Tb + bi * 32 * LF_TP;
+                    T[(tr * 8 + fr) * LF_TP + tc * 8 + 2 * fk] = acc[u][0];
+                    T[(tr * 8 + fr) * LF_TP + tc * 8 + 2 * fk + 1] = acc[u][1];
                 }
             }
             __syncthreads();
@@ -454,8 +500,8 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
                     for (int u = 0; u < 2; ++u) {
                         const int t = u ? t1 : t0, bi = t >> 4, tr = (t >> 2) & 3, tc = t & 3;
                         const int ii = bi * 32, r_ = tr * 8 + fr, uu = k4 + fk;
-                        const double av = uu > r_ ? M[(ii + r_) + (ii + uu) * LF_LD] : (uu == r_ ? invd[ii + r_] : 0.0);
-                        const double bv = Tb[bi * 32 * 33 + uu * 33 + tc * 8 + fr];
+                        const double av = Xd[bi * 32 * LF_TP + r_ * LF_TP + uu];  // X_ii[r_][uu]
+                        const double bv = Tb[bi * 32 * LF_TP + uu * LF_TP + tc * 8 + fr];
                         dmma(acc[u][0], acc[u][1], av, bv);
                     }
                 }
@@ -472,11 +518,13 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
     }
     LF_CLK(6);
 #pragma unroll 4
-    for (int q = 0; q < LF_MAX * LF_MAX / LF_T; ++q) {
-        const int e = q * LF_T + tid, i = e & (LF_MAX - 1), k = e >> 7;
-        if (i < w && k < w) {
-            r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * LF_LD] : 0.0;
+    for (int q = 0; q * LF_T < total; ++q) {
+        const int e = q * LF_T + tid;
+        int i, k;
+        tile_ik(e, i, k);
+        if (e < total && i < w && k < w) {
             x[i + (int64_t)k * ldx] = stop ? 0.0 : (i < k ? M[i + k * LF_LD] : (i == k ? invd[i] : 0.0));
+            r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * LF_LD] : 0.0;
         }
     }
     LF_CLK(7);
@@ -515,8 +563,8 @@ namespace ops {
 static int dgemm_splits(const Ctx* c, int64_t tiles, int64_t K) {
     const int64_t target = 2LL * c->sm_count;
     if (tiles >= target || K < 8 * DBK) return 1;
-    int64_t s = std::min<int64_t>((target + tiles - 1) / tiles, K / (8 * DBK));
-    return (int)std::max<int64_t>(1, std::min<int64_t>(s, 256));
+    int64_t s = std::min<int64_t>((target + tiles - 1) / tiles, K / (16 * DBK));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
 }
 
 void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
@@ -548,8 +596,12 @@ void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, 
     ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, 1.0, A, dta, lda, B, dtb, ldb, 0.0, nullptr, 0,
                           part.as<double>(), nullptr, 0, 0, flags);
     const int64_t total = M * N;
-    k_dsplitk_reduce<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
-        M, N, splits, part.as<double>(), alpha, beta, C, ldc, (flags & GEMM_SYM_UPPER) ? 1 : 0);
+    if (splits >= 16 && total <= (1 << 20))
+        k_dsplitk_reduce_warp<<<(unsigned)((total * 32 + 255) / 256), 256, 0, c->stream>>>(
+            M, N, splits, part.as<double>(), alpha, beta, C, ldc, (flags & GEMM_SYM_UPPER) ? 1 : 0);
+    else
+        k_dsplitk_reduce<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>(
+            M, N, splits, part.as<double>(), alpha, beta, C, ldc, (flags & GEMM_SYM_UPPER) ? 1 : 0);
     LAUNCH_CHECK(c);
 }
 
@@ -592,7 +644,7 @@ void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, i
                    int* info, double* diag, int64_t info_offset) {
     if (w > LF_MAX || w < 1) fail(BCUR_E_INVALID_ARGUMENT, "chol_inv_leaf: 1 <= w <= 128");
     ProfScope prof(c, "chol_inv_leaf", 2.0 * w * w * w / 3.0, 8.0 * 3 * w * w);
-    constexpr size_t smem = (size_t)(LF_MAX * LF_LD + 3 * 32 * 33) * sizeof(double);
+    constexpr size_t smem = (size_t)(LF_MAX * LF_LD + 7 * 32 * LF_TP) * sizeof(double);
     static bool attr = false;
     if (!attr) {
         CUDA_CHECK(cudaFuncSetAttribute(k_chol_inv_leaf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

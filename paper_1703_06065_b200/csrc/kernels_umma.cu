@@ -98,7 +98,7 @@ struct Cfg {
                   "X3 register split must fit the launch allocation");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
 };
-enum { EPI_STORE = 0, EPI_ROWSQ = 1 };
+enum { EPI_STORE = 0, EPI_ROWSQ = 1, EPI_RESID = 2 };
 
 // Round an fp32 value to the nearest TF32 (10-bit mantissa), ties to even.
 __device__ __forceinline__ float rn_tf32(float x) {
@@ -344,8 +344,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
        const int* __restrict__ rexp, const int* __restrict__ cexp) {
     // instruction descriptor: fp32 accumulate, tf32 × tf32 (H: f16 × f16), B K-major,
     // N = n_cols, M = 128
-    static_assert(!H || (X3 ? EPI == EPI_STORE : (EPI == EPI_ROWSQ && !A_MN)),
-                  "fp16 operands: 3×FP16 products, or the pre-converted row-sum-of-squares");
+    static_assert(!H || (X3 ? (EPI == EPI_STORE || (EPI == EPI_RESID && A_MN)) : (EPI == EPI_ROWSQ && !A_MN)),
+                  "fp16 operands: 3×FP16 products (stored, or the fused residual), or the pre-converted "
+                  "row-sum-of-squares");
     constexpr bool H3 = H && X3;
     constexpr uint32_t FMT = H ? 0u : 2u;
     constexpr int BKE = bke<H>();
@@ -420,6 +421,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         const int ccol = slice * DC;                  // first output column (within the tile) of this warp
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
         int gc = 0;  // chunks drained so far (all tiles)
+        double rsum = 0.0;  // EPI_RESID: this thread's Σ (D − product)² over its rows of every tile
         for (int t = blockIdx.x; t < sc.total; t += gridDim.x) {
         const TileInfo ti = tile_info<NT>(sc, t);
         const int m_tile = ti.m_tile, n_tile = ti.n_tile, split = ti.split;
@@ -478,7 +480,32 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
             mbar_arrive(&tempty[b]);
         }
         const int col0 = n_tile * NT * BN + ccol;
-        if (EPI == EPI_ROWSQ) {
+        if (EPI == EPI_RESID) {
+            // fused explicit residual: D is the fp32 A (column-major, ld = ldo) passed as `out`;
+            // lanes are consecutive rows, so each column's loads are one 128-byte line per warp
+            if (row < M) {
+                const float* D = reinterpret_cast<const float*>(out);
+                const int ncol = min(DC, N - col0);
+                const int re = (H3 && rexp) ? rexp[row] : 0;
+                constexpr int EB = 16;
+#pragma unroll
+                for (int j0 = 0; j0 < DC; j0 += EB) {
+                    float dv[EB];
+#pragma unroll
+                    for (int jj = 0; jj < EB; ++jj)
+                        dv[jj] = (j0 + jj < ncol) ? __ldg(D + row + (int64_t)(col0 + j0 + jj) * ldo) : 0.0f;
+#pragma unroll
+                    for (int jj = 0; jj < EB; ++jj) {
+                        const int j = j0 + jj;
+                        if (j >= ncol) continue;
+                        double v = X3 ? (double)acc[j] + (double)cmp[X3 ? j : 0] : (double)acc[j];
+                        if (H3) v *= exp2_int(-(re + (cexp ? cexp[col0 + j] : 0)));
+                        const double e = (double)dv[jj] - v;
+                        rsum = fma(e, e, rsum);
+                    }
+                }
+            }
+        } else if (EPI == EPI_ROWSQ) {
             double s = 0.0;
 #pragma unroll
             for (int j = 0; j < DC; ++j) {
@@ -518,6 +545,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
         }
         gc += nchunks;
         }
+        if (EPI == EPI_RESID) partial[(int64_t)blockIdx.x * (32 * CF::NDRAIN) + (warp - 4) * 32 + lane] = rsum;
     } else {
         if (CF::RESPLIT) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CF::REG_LOW));
         if (warp == 0) {
@@ -744,7 +772,8 @@ CUtensorMap make_map(const void* base, int rank, const uint64_t* dims, const uin
 template <bool A_MN, int EPI, int NT, bool X3, bool H = false>
 void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
                     int N, double* out, int64_t ldo, double* partial, double alpha, double beta,
-                    const CUtensorMap* tal = nullptr, const int* rexp = nullptr, const int* cexp = nullptr) {
+                    const CUtensorMap* tal = nullptr, const int* rexp = nullptr, const int* cexp = nullptr,
+                    bool wave_barrier = true) {
     using CF = Cfg<NT, X3, H>;
     auto kern = k_umma<A_MN, EPI, NT, X3, H>;
     static bool attr = false;
@@ -755,7 +784,7 @@ void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& 
     if (sc.total <= 0) return;
     const int grid = std::min(sc.total, c->sm_count);
     DevBuf ctr;
-    if (grid < sc.total && !(g_wave_barrier_off)) {
+    if (grid < sc.total && !(g_wave_barrier_off) && wave_barrier) {
         ctr = DevBuf(c, 64);
         CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
         sc.wave_ctr = ctr.as<unsigned int>();
@@ -1843,7 +1872,10 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     const int k_tiles = (int)((K + BKH - 1) / BKH);
     const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
     const int tiles = sym ? nt * (nt + 1) / 2 : mt * nt;
-    int splits = h3_splits(tiles, k_tiles, c->sm_count);
+    // split-K fills the last persistent wave, but its fp64 partials cost (splits + 1)·M·N·8
+    // bytes of traffic plus a reduce: for wide outputs (the 4096² Gram of C) that exceeded the
+    // wave it saved, so only outputs below 8 M elements split
+    int splits = (double)M * (double)N <= 8.0e6 ? h3_splits(tiles, k_tiles, c->sm_count) : 1;
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
     Sched sc = make_sched(mt, nt, splits, k_tiles, kps, sym, tri);
@@ -1873,6 +1905,48 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     k_reduce_splits<<<(unsigned)((M * N + 255) / 256), 256, 0, c->stream>>>(M, N, splits, part.as<double>(), out, ldo,
                                                                             alpha, beta);
     LAUNCH_CHECK(c);
+}
+
+// Σ_ij (D − A·X)_ij² with A given as its interleaved split (m × n, column exponents ea), X fp64
+// (n × N, ldx; split here with ea folded into its rows) and D fp32 (m × N, ldd) — the product
+// is never stored (EPI_RESID); one fp64 partial per drain thread of each persistent CTA, summed
+// in a fixed order (deterministic).
+void umma_h3_resid(Ctx* c, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx, int64_t N,
+                   int64_t ldx, const float* D, int64_t ldd, double* d_sum) {
+    if (m <= 0 || N <= 0) return;
+    if (!h3_ok(m)) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3_resid: needs m % 64 == 0");
+    SplitF16 xs;
+    split_f16(c, X, dtx, n, N, ldx, ea, &xs);
+    const int64_t M = m, K = n;
+    const int NT = N > BN ? 2 : 1;
+    ProfScope prof(c, "umma_resid_h3", 2.0 * M * N * K, 4.0 * m * n + 4.0 * K * N + 4.0 * M * N);
+    constexpr int BKH = bke<true>();
+    const uint64_t dA[4] = {64, 2, (uint64_t)(m / 64), (uint64_t)n};
+    const uint64_t sA[3] = {128, 256, (uint64_t)m * 4};
+    const uint32_t bA[4] = {64, 1, 1, (uint32_t)BKH};
+    CUtensorMap ta = make_map(AL, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    const int64_t lx = xs.ld > 0 ? xs.ld : K;
+    const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)lx * 2};
+    const uint32_t bX[2] = {BKH, BN};
+    CUtensorMap th = make_map(xs.hi.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    CUtensorMap tl = make_map(xs.lo.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    const int k_tiles = (int)((K + BKH - 1) / BKH);
+    const int mt = (int)((M + BM - 1) / BM), nt = (int)((N + NT * BN - 1) / (NT * BN));
+    Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
+    sc.pf = g_pf >= 0 ? g_pf : 0;
+    sc.x_il = 0;
+    sc.bke = BKH;
+    const int grid = std::min(sc.total, c->sm_count);
+    const int per = 32 * (NT == 2 ? Cfg<2, true, true>::NDRAIN : Cfg<1, true, true>::NDRAIN);
+    DevBuf part(c, (size_t)grid * per * sizeof(double));
+    double* dd = const_cast<double*>(reinterpret_cast<const double*>(D));  // read-only inside EPI_RESID
+    if (NT == 2)
+        launch_umma_nt<true, EPI_RESID, 2, true, true>(c, sc, ta, th, tl, (int)M, (int)N, dd, ldd, part.as<double>(), 1.0,
+                                                       0.0, nullptr, nullptr, xs.exps.as<int>(), k_tiles >= 8);
+    else
+        launch_umma_nt<true, EPI_RESID, 1, true, true>(c, sc, ta, th, tl, (int)M, (int)N, dd, ldd, part.as<double>(), 1.0,
+                                                       0.0, nullptr, nullptr, xs.exps.as<int>(), k_tiles >= 8);
+    sum_vector(c, part.as<double>(), (int64_t)grid * per, d_sum);
 }
 
 void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,

@@ -134,6 +134,11 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
 void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,
              int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags = 0);
 
+// Σ_ij (D − A·X)_ij² with A the interleaved split (m × n, exps ea), X fp64 (n × N, ldx), D fp32
+// (m × N, ldd): the explicit residual's second product fused with the subtraction (tcgen05 3×FP16)
+void umma_h3_resid(Ctx* c, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx, int64_t N,
+                   int64_t ldx, const float* D, int64_t ldd, double* d_sum);
+
 // ---- small dense factorizations (kernels_small.cu), single CTA, fp64 ------
 // R upper (ld ldr, may alias g) with G = RᵀR, only g's upper triangle is read; info[0] = 0 ok / j+1 failed pivot;
 // diag[0] = min diag(R), diag[1] = max diag(G) (input)

@@ -837,10 +837,33 @@ static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub) {
     return h[0] - h[1];
 }
 
-// ‖A − Q Qᵀ A‖² (streamed: X = QᵀA, then Σ (A − Q X)² tile by tile)
-static double explicit_residual(Ctx* c, const DMat* a, const Basis& B) {
+// ‖A − Q Qᵀ A‖² (streamed: X = QᵀA, then Σ (A − Q X)² tile by tile; blockcur.cpp:46's
+// ‖A − C(UR)‖ with C·U·R = P_C A).  fp32 A with its interleaved 3×FP16 copy: both products on
+// tcgen05 — X = QᵀA reads that copy as its X operand (no new split of A), the second product
+// runs with the subtraction and the square-sum fused into its epilogue (EPI_RESID: A·X never
+// stored) — over column chunks of A that bound X to ~1 GB.  Otherwise DMMA fp64.
+static double explicit_residual(Ctx* c, const DMat* a, const Basis& B, const RoundedA* ra = nullptr) {
     const int64_t m = a->m, nl = a->n, r = B.rank;
     Mat64 tot(c, 1, 1);
+    if (r > 0 && B.dt == BCUR_F32 && a->dtype == BCUR_F32 && ra && ra->has_lo() && h3_ok(m)) {
+        DevBuf qil, qe;
+        split_il(c, B.buf.ptr, BCUR_F32, m, r, B.rows, &qil, &qe);
+        const int64_t nc = std::max<int64_t>(128, std::min<int64_t>(nl, ((int64_t)1 << 30) / (8 * r) / 128 * 128));
+        const int64_t nchunks = (nl + nc - 1) / nc;
+        Mat64 X(c, r, std::min(nc, nl)), parts(c, nchunks, 1);
+        for (int64_t ci = 0; ci < nchunks; ++ci) {
+            const int64_t j0 = ci * nc, w = std::min(nc, nl - j0);
+            const F16View av{ra->il.as<uint16_t>() + (size_t)j0 * 2 * m, nullptr, ra->exps.as<int>() + j0, m, w};
+            umma_h3(c, false, qil.as<uint16_t>(), qe.as<int>(), m, r, av, 1.0, 0.0, X.p(), r);
+            umma_h3_resid(c, qil.as<uint16_t>(), qe.as<int>(), m, r, X.p(), BCUR_F64, w, r,
+                          (const float*)a->ptr + (size_t)j0 * a->ld, a->ld, parts.p() + ci);
+        }
+        sum_vector(c, parts.p(), nchunks, tot.p());
+        allreduce(c, tot.p(), 1);
+        double h = 0.0;
+        d2h(c, &h, tot.p(), 1);
+        return h;
+    }
     Mat64 X(c, std::max<int64_t>(r, 1), nl);
     if (r > 0)
         gemm(c, OP_T, OP_N, r, nl, m, 1.0, B.buf.ptr, B.dt, B.rows, a->ptr, a->dtype, a->ld, 0.0, X.p(), X.ld);
@@ -931,12 +954,15 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     Basis B;
     column_basis(c, a, s, unique_in_order(blocks), bn2, &B, false, &ra);
     ph.reset(new ProfScope(c, "phase:5 residual", 0, 0));
-    double res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra);
-    if (ra.ok() && B.x16.ptr) res2 -= sketch_correction(c, B, sub);
+    double res2 = 0.0;
+    if (o.residual != BCUR_RESID_EXPLICIT) {  // Pythagoras first (AUTO falls back to explicit when small)
+        res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra);
+        if (ra.ok() && B.x16.ptr) res2 -= sketch_correction(c, B, sub);
+    }
     ph.reset();
     int path = 0;
     if (o.residual == BCUR_RESID_EXPLICIT || (o.residual == BCUR_RESID_AUTO && res2 < theta_explicit(a->dtype) * a2)) {
-        res2 = explicit_residual(c, a, B);
+        res2 = explicit_residual(c, a, B, &ra);
         path = 1;
     }
     out->rep = bcur_report{};

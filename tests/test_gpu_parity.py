@@ -442,3 +442,14 @@ def test_forced_residual_paths(B, dt):
         if dt == np.float32 and mode == "pythagoras":
             continue  # ‖A‖² − ‖QᵀA‖² cancels to noise in fp32 at rel_err 1e-3 (why AUTO goes explicit)
         run_css_forced(B, a, 128, 15, 10, 1, 6, O.WITHOUT_REPLACEMENT, 4, mode)
+
+
+def test_config3_shape_low_noise_explicit_residual(B):
+    # c3 structure with little noise (rel_err ≈ 1e-2 < √θ_explicit): AUTO takes the explicit path —
+    # X = QᵀA and Σ(A − QX)² on tcgen05 3×FP16 with the subtraction fused into the epilogue
+    a = lowrank(2048, 8192, 50, "pow:1.5", 1e-6, 0, np.float32)
+    got, ref = run_css(B, a, 128, 50, 10, 2, 8, O.WITHOUT_REPLACEMENT, 0)
+    assert ref.residual_path == "explicit" and got.residual_path == "explicit"
+    assert got.plan.blocks() == ref.plan.blocks()
+    forced, ref_f = run_css_forced(B, a, 128, 50, 10, 2, 8, O.WITHOUT_REPLACEMENT, 0, "explicit")
+    assert forced.projection_error == pytest.approx(got.projection_error, rel=1e-9)
