@@ -1494,15 +1494,32 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         Mat64 dsc(c, ccw, 1), dsr(c, crw, 1), T1(c, ccw, crw), T2(c, ccw, crw);
         h2d(c, dsc.p(), sc.data(), ccw);
         h2d(c, dsr.p(), sr.data(), crw);
-        gemm(c, OP_N, OP_N, ccw, crw, ccw, 1.0, QC.rinv2.p(), BCUR_F64, QC.rinv2.ld, M.p(), BCUR_F64, M.ld, 0.0,
-             T1.p(), T1.ld);
-        gemm(c, OP_N, OP_N, ccw, crw, ccw, 1.0, QC.rinv1.p(), BCUR_F64, QC.rinv1.ld, T1.p(), BCUR_F64, T1.ld, 0.0,
-             T2.p(), T2.ld);
-        gemm(c, OP_N, OP_T, ccw, crw, crw, 1.0, T2.p(), BCUR_F64, T2.ld, QR.rinv2.p(), BCUR_F64, QR.rinv2.ld, 0.0,
-             T1.p(), T1.ld);
         out->u = Mat64(c, ccw, crw);
-        gemm(c, OP_N, OP_T, ccw, crw, crw, 1.0, T1.p(), BCUR_F64, T1.ld, QR.rinv1.p(), BCUR_F64, QR.rinv1.ld, 0.0,
-             out->u.p(), out->u.ld);
+        if (dt == BCUR_F32 && h3_ok(ccw) && h3_ok(crw)) {
+            // fp32 inputs: the four triangular products on the tcgen05 3×FP16 kernels (~2⁻²²
+            // relative, against U's 1e-4 bar; on DMMA they were ~9 ms of c4's step):
+            //   V = R_C⁻¹·M = rinv1·(rinv2·M),  Uᵀ = R_R⁻¹·Vᵀ = rinv1_R·(rinv2_R·Vᵀ)
+            Mat64 Vt(c, crw, ccw), W1(c, crw, ccw);
+            gemm_h3(c, true, QC.rinv2.p(), BCUR_F64, ccw, ccw, QC.rinv2.ld, M.p(), BCUR_F64, crw, M.ld, 1.0, 0.0, T1.p(),
+                    T1.ld, 0);
+            gemm_h3(c, true, QC.rinv1.p(), BCUR_F64, ccw, ccw, QC.rinv1.ld, T1.p(), BCUR_F64, crw, T1.ld, 1.0, 0.0, T2.p(),
+                    T2.ld, 0);
+            transpose(c, T2.p(), BCUR_F64, ccw, crw, T2.ld, Vt.p(), BCUR_F64, Vt.ld);
+            gemm_h3(c, true, QR.rinv2.p(), BCUR_F64, crw, crw, QR.rinv2.ld, Vt.p(), BCUR_F64, ccw, Vt.ld, 1.0, 0.0, W1.p(),
+                    W1.ld, 0);
+            gemm_h3(c, true, QR.rinv1.p(), BCUR_F64, crw, crw, QR.rinv1.ld, W1.p(), BCUR_F64, ccw, W1.ld, 1.0, 0.0, Vt.p(),
+                    Vt.ld, 0);
+            transpose(c, Vt.p(), BCUR_F64, crw, ccw, Vt.ld, out->u.p(), BCUR_F64, out->u.ld);
+        } else {
+            gemm(c, OP_N, OP_N, ccw, crw, ccw, 1.0, QC.rinv2.p(), BCUR_F64, QC.rinv2.ld, M.p(), BCUR_F64, M.ld, 0.0,
+                 T1.p(), T1.ld);
+            gemm(c, OP_N, OP_N, ccw, crw, ccw, 1.0, QC.rinv1.p(), BCUR_F64, QC.rinv1.ld, T1.p(), BCUR_F64, T1.ld, 0.0,
+                 T2.p(), T2.ld);
+            gemm(c, OP_N, OP_T, ccw, crw, crw, 1.0, T2.p(), BCUR_F64, T2.ld, QR.rinv2.p(), BCUR_F64, QR.rinv2.ld, 0.0,
+                 T1.p(), T1.ld);
+            gemm(c, OP_N, OP_T, ccw, crw, crw, 1.0, T1.p(), BCUR_F64, T1.ld, QR.rinv1.p(), BCUR_F64, QR.rinv1.ld, 0.0,
+                 out->u.p(), out->u.ld);
+        }
         scale_rows(c, out->u.p(), ccw, crw, out->u.ld, dsc.p());
         scale_columns(c, out->u.p(), ccw, crw, out->u.ld, dsr.p());
         out->u_valid = true;
