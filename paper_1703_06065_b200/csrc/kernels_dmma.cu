@@ -13,16 +13,16 @@
 // Structure flags shrink each tile's K range (triangular operands) or skip tiles (a product
 // known to be symmetric, of which only the upper triangle is consumed).
 //
-// CTA tile 64×64×16, 4 warps as 2×2, each warp 32×32 = 4×4 DMMA tiles; operands staged
-// through registers into double-buffered shared memory ([k][m] / [k][n] with a row pitch of
-// 68 doubles ≡ 4 mod 16: the fragment loads — lane t reads row t&3, column t>>2 — take the
-// minimum two wavefronts; a pitch of 72 made them 2-way conflicted).
+// CTA tile 64×64×16, 4 warps as 2×2, each warp 32×32 = 4×4 DMMA tiles; a 4-stage cp.async
+// pipeline (3 k-tiles in flight: the latency-bound small products of the factorizations and
+// orthonormalizations wait on L2 once, not once per k-tile); conflict-free fragment pitches
+// (DTile).
 #include "ops.h"
 
 namespace bcur_b200 {
 namespace {
 
-constexpr int DBM = 64, DBN = 64, DBK = 16, DNT = 128, DLD = 68;
+constexpr int DBM = 64, DBN = 64, DBK = 16, DNT = 128;
 enum { DEPI_STORE = 0, DEPI_ROWSQ = 1, DEPI_RESID = 2 };
 
 template <class T>
@@ -34,14 +34,38 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// Shared-memory tiles keep each operand's stored contiguous direction (so cp.async copies
+// elements straight from global memory): op(A) is [k][m] when A is column-major (TRA = 0) and
+// [m][k] when transposed; op(B) is [n][k] when B is K-major (TRB = 0) and [k][n] otherwise.
+// Pitches make the DMMA fragment loads conflict-free: [·][k] rows hold 16 k + 4 pad (20 ≡ 4 mod
+// 16 doubles / ≡ 20 mod 32 floats), [k][·] rows 64 + 4 doubles or 64 + 8 floats.
+template <typename T, bool KMAJOR>
+struct DTile {
+    static constexpr int P = KMAJOR ? (DBK + 4) : (64 + (sizeof(T) == 8 ? 4 : 8));
+    static constexpr int ELEMS = KMAJOR ? 64 * P : DBK * P;
+};
+constexpr int DSTAGES = 4;
+
+__device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem, int bytes, bool valid) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    const int src = valid ? bytes : 0;  // src-size 0: the destination is zero-filled
+    if (bytes == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "r"(src) : "memory");
+}
+
 template <typename TA, typename TB, int TRA, int TRB, int EPI>
 __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
                                                const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B,
                                                int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
                                                double* __restrict__ partial, const void* __restrict__ D, int dtd,
                                                int64_t ldd, int flags) {
-    __shared__ __align__(16) double As[2][DBK][DLD];
-    __shared__ __align__(16) double Bs[2][DBK][DLD];
+    using TLA = DTile<TA, TRA == 1>;
+    using TLB = DTile<TB, TRB == 0>;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    TA* As = reinterpret_cast<TA*>(dsm);
+    TB* Bs = reinterpret_cast<TB*>(dsm + (size_t)DSTAGES * TLA::ELEMS * sizeof(TA));
     __shared__ double red[2][DBM];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
@@ -68,67 +92,66 @@ __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, 
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    double ra[8], rb[8];
-    // op(A) tile (DBM × DBK) and op(B) tile (DBK × DBN), each 1024 elements = 8 per thread;
-    // the thread map follows the contiguous direction of the stored matrix
-    auto load = [&](int64_t k0) {
+    // one stage: op(A) (DBM × DBK) and op(B) (DBK × DBN), 1024 elements each = 8 cp.async per
+    // thread and operand, the thread map following the stored contiguous direction (coalesced)
+    auto issue = [&](int st, int64_t k0) {
+        TA* as = As + st * TLA::ELEMS;
+        TB* bs = Bs + st * TLB::ELEMS;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             int i, kk;
             if (TRA == 0) { i = tid & 63; kk = (tid >> 6) + 2 * r; } else { kk = tid & 15; i = (tid >> 4) + 8 * r; }
             const int64_t gi = m0 + i, gk = k0 + kk;
-            ra[r] = (gi < M && gk < kend) ? (TRA == 0 ? ldg64(A + gi + gk * lda) : ldg64(A + gk + gi * lda)) : 0.0;
+            const bool v = gi < M && gk < kend;
+            const TA* src = A + (v ? (TRA == 0 ? gi + gk * lda : gk + gi * lda) : 0);
+            cp_async_elem(TRA == 0 ? as + kk * TLA::P + i : as + i * TLA::P + kk, src, (int)sizeof(TA), v);
         }
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             int j, kk;
             if (TRB == 0) { kk = tid & 15; j = (tid >> 4) + 8 * r; } else { j = tid & 63; kk = (tid >> 6) + 2 * r; }
             const int64_t gj = n0 + j, gk = k0 + kk;
-            rb[r] = (gj < N && gk < kend) ? (TRB == 0 ? ldg64(B + gk + gj * ldb) : ldg64(B + gj + gk * ldb)) : 0.0;
-        }
-    };
-    auto store = [&](int buf) {
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int i, kk;
-            if (TRA == 0) { i = tid & 63; kk = (tid >> 6) + 2 * r; } else { kk = tid & 15; i = (tid >> 4) + 8 * r; }
-            As[buf][kk][i] = ra[r];
-        }
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            int j, kk;
-            if (TRB == 0) { kk = tid & 15; j = (tid >> 4) + 8 * r; } else { j = tid & 63; kk = (tid >> 6) + 2 * r; }
-            Bs[buf][kk][j] = rb[r];
+            const bool v = gj < N && gk < kend;
+            const TB* src = B + (v ? (TRB == 0 ? gk + gj * ldb : gj + gk * ldb) : 0);
+            cp_async_elem(TRB == 0 ? bs + j * TLB::P + kk : bs + kk * TLB::P + j, src, (int)sizeof(TB), v);
         }
     };
 
     if (kbeg < kend) {
-        int buf = 0;
-        load(kbeg);
-        store(0);
-        __syncthreads();
-        const int fr = lane & 3, fc = lane >> 2;
-        for (int64_t k0 = kbeg; k0 < kend; k0 += DBK) {
-            const bool more = k0 + DBK < kend;
-            if (more) load(k0 + DBK);
+        const int nk = (int)((kend - kbeg + DBK - 1) / DBK);
+#pragma unroll
+        for (int st = 0; st < DSTAGES - 1; ++st) {  // prologue: DSTAGES−1 stages in flight
+            if (st < nk) issue(st, kbeg + (int64_t)st * DBK);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+        const int fk = lane & 3, fm = lane >> 2;
+        for (int kt = 0; kt < nk; ++kt) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(DSTAGES - 2) : "memory");
+            __syncthreads();  // stage kt landed for every thread; stage kt−1 is free again
+            if (kt + DSTAGES - 1 < nk) issue((kt + DSTAGES - 1) % DSTAGES, kbeg + (int64_t)(kt + DSTAGES - 1) * DBK);
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            const TA* as = As + (kt % DSTAGES) * TLA::ELEMS;
+            const TB* bs = Bs + (kt % DSTAGES) * TLB::ELEMS;
 #pragma unroll
             for (int k4 = 0; k4 < DBK; k4 += 4) {
                 double af[4], bf[4];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) af[i] = As[buf][k4 + fr][wm * 32 + i * 8 + fc];
+                for (int i = 0; i < 4; ++i) {
+                    const int mm = wm * 32 + i * 8 + fm;
+                    af[i] = (double)(TRA == 0 ? as[(k4 + fk) * TLA::P + mm] : as[mm * TLA::P + k4 + fk]);
+                }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][k4 + fr][wn * 32 + j * 8 + fc];
+                for (int j = 0; j < 4; ++j) {
+                    const int nn = wn * 32 + j * 8 + fm;
+                    bf[j] = (double)(TRB == 0 ? bs[nn * TLB::P + k4 + fk] : bs[(k4 + fk) * TLB::P + nn]);
+                }
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
                     for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
-            if (more) {
-                store(buf ^ 1);
-                __syncthreads();
-                buf ^= 1;
-            }
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
 
     // accumulator fragment: row = lane>>2, columns 2·(lane&3) + {0,1} of each 8×8 tile
@@ -235,14 +258,28 @@ __global__ void k_dsum_rows(int64_t M, int tiles, const double* __restrict__ par
     out[i] = s;
 }
 
+template <typename TA, typename TB, int TRA, int TRB, int EPI>
+size_t dgemm_smem() {
+    return (size_t)DSTAGES * (DTile<TA, TRA == 1>::ELEMS * sizeof(TA) + DTile<TB, TRB == 0>::ELEMS * sizeof(TB));
+}
+
 template <typename TA, typename TB, int EPI>
 void dlaunch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
              const void* A, int64_t lda, const void* B, int64_t ldb, double beta, double* C, int64_t ldc,
              double* partial, const void* D, int dtd, int64_t ldd, int flags) {
 #define BCUR_DGEMM_CASE(TRA, TRB)                                                                                  \
-    k_dgemm<TA, TB, TRA, TRB, EPI><<<grid, DNT, 0, c->stream>>>(M, N, K, kchunk, alpha, (const TA*)A, lda,          \
-                                                                 (const TB*)B, ldb, beta, C, ldc, partial, D, dtd, \
-                                                                 ldd, flags)
+    do {                                                                                                           \
+        static bool attr = false;                                                                                  \
+        const size_t sm = dgemm_smem<TA, TB, TRA, TRB, EPI>();                                                     \
+        if (!attr) {                                                                                               \
+            CUDA_CHECK(cudaFuncSetAttribute(k_dgemm<TA, TB, TRA, TRB, EPI>,                                        \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                \
+            attr = true;                                                                                           \
+        }                                                                                                          \
+        k_dgemm<TA, TB, TRA, TRB, EPI><<<grid, DNT, sm, c->stream>>>(M, N, K, kchunk, alpha, (const TA*)A, lda,    \
+                                                                      (const TB*)B, ldb, beta, C, ldc, partial, D, \
+                                                                      dtd, ldd, flags);                            \
+    } while (0)
     if (ta == ops::OP_N && tb == ops::OP_N) BCUR_DGEMM_CASE(0, 0);
     else if (ta == ops::OP_N && tb == ops::OP_T) BCUR_DGEMM_CASE(0, 1);
     else if (ta == ops::OP_T && tb == ops::OP_N) BCUR_DGEMM_CASE(1, 0);
