@@ -319,6 +319,7 @@ void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, 
 // k) then hits 16 distinct 8-byte bank pairs per half-warp — with an odd pitch it was 4-way
 // conflicted and the leaf's DMMA phases ran at the shared-memory wavefront rate
 constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 4, LF_TP = 36;
+enum { LEAF_NO_R = 1, LEAF_ZEROED = 2 };  // chol_inv_leaf flags (ops.h)
 __device__ int g_leaf_timing = 0;  // BCUR_LEAF_TIMING=1: thread 0 prints the phase clocks (diagnostics)
 #define LF_CLK(i) do { if (timing && threadIdx.x == 0) clk[i] = clock64(); } while (0)
 
@@ -331,10 +332,12 @@ __device__ __forceinline__ double lf_rsqrt(double x) {
     return r;
 }
 
-__global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict__ g, int w, int64_t ldg,
-                                                        double* __restrict__ r, int64_t ldr, double* __restrict__ x,
-                                                        int64_t ldx, int* info, double* diag, int info_offset) {
-    extern __shared__ double smlf[];
+// The leaf as a device function of 256 threads (k_chol_inv_leaf, and the FACT step of the
+// persistent factorization k_chol_persistent); smlf: LF_SMEM bytes of dynamic shared memory.
+// g is read through L2 (ld.global.cg): inside the persistent kernel other CTAs wrote it.
+__device__ __forceinline__ void chol_leaf_dev(double* smlf, const double* __restrict__ g, int w, int64_t ldg,
+                                              double* __restrict__ r, int64_t ldr, double* __restrict__ x,
+                                              int64_t ldx, int* info, double* diag, int info_offset, int flags) {
     double* M = smlf;                       // M[i + k·LD]: i ≥ k → L = Rᵀ; i < k → X[i][k]
     double* Tb = smlf + LF_MAX * LF_LD;     // 3 × 32 × LF_TP temporaries of the inverse
     double* Xd = Tb + 3 * 32 * LF_TP;       // 4 × 32 × LF_TP: the diagonal blocks of X as full squares
@@ -342,7 +345,7 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
     __shared__ double xch[32];
     __shared__ int stop_sh;
     __shared__ double mn_sh;
-    if (*info != 0) return;
+    if (*(volatile int*)info != 0) return;
     const int timing = g_leaf_timing;
     long long clk[16] = {0};
     LF_CLK(0);
@@ -365,7 +368,7 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
         for (int q = 0; q < 16; ++q) {  // addresses clamped, no branches
             int i, k;
             tile_ik(min((q0 + q) * LF_T + tid, total - 1), i, k);
-            v[q] = __ldg(g + min(i, w - 1) + (int64_t)min(k, w - 1) * ldg);
+            v[q] = __ldcg(g + min(i, w - 1) + (int64_t)min(k, w - 1) * ldg);
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -554,14 +557,39 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
         }
     }
     LF_CLK(6);
+    // X (and R unless LEAF_NO_R): with LEAF_ZEROED the lower triangles are already zero (the
+    // recursion memsets R and X), so only the upper triangles are written — X by 16-byte stores,
+    // one column per warp, consecutive row pairs per lane (a 512-byte run per warp and column)
+    const bool zeroed = (flags & LEAF_ZEROED) != 0, want_r = !(flags & LEAF_NO_R);
+    if (zeroed && !stop && ((uintptr_t)x % 16) == 0 && (ldx % 2) == 0) {
+        for (int k = warp; k < w; k += LF_T / 32) {
+            for (int p = lane; 2 * p <= k; p += 32) {
+                const int i = 2 * p;
+                const double v0 = i < k ? M[i + k * LF_LD] : invd[k];
+                const double v1 = i + 1 < k ? M[i + 1 + k * LF_LD] : (i + 1 == k ? invd[k] : 0.0);
+                if (i + 1 < w) *reinterpret_cast<double2*>(x + i + (int64_t)k * ldx) = make_double2(v0, v1);
+                else x[i + (int64_t)k * ldx] = v0;
+            }
+        }
+        if (want_r) {
 #pragma unroll 4
-    for (int q = 0; q * LF_T < total; ++q) {
-        const int e = q * LF_T + tid;
-        int i, k;
-        tile_ik(e, i, k);
-        if (e < total && i < w && k < w) {
-            x[i + (int64_t)k * ldx] = stop ? 0.0 : (i < k ? M[i + k * LF_LD] : (i == k ? invd[i] : 0.0));
-            r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * LF_LD] : 0.0;
+            for (int q = 0; q * LF_T < total; ++q) {
+                const int e = q * LF_T + tid;
+                int i, k;
+                tile_ik(e, i, k);
+                if (e < total && i <= k && k < w) r[i + (int64_t)k * ldr] = M[k + i * LF_LD];
+            }
+        }
+    } else {
+#pragma unroll 4
+        for (int q = 0; q * LF_T < total; ++q) {
+            const int e = q * LF_T + tid;
+            int i, k;
+            tile_ik(e, i, k);
+            if (e < total && i < w && k < w && !(zeroed && i > k)) {
+                x[i + (int64_t)k * ldx] = stop ? 0.0 : (i < k ? M[i + k * LF_LD] : (i == k ? invd[i] : 0.0));
+                if (want_r) r[i + (int64_t)k * ldr] = i <= k && !stop ? M[k + i * LF_LD] : 0.0;
+            }
         }
     }
     LF_CLK(7);
@@ -573,6 +601,21 @@ __global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict
         printf("leaf w=%d clocks: load %lld | panel0 diag %lld | panel0 trsm %lld | panels rest %lld | inv diag %lld | "
                "inv offdiag %lld | store %lld | total %lld\n", w, clk[1] - clk[0], clk[2] - clk[1], clk[3] - clk[2],
                clk[4] - clk[3], clk[5] - clk[4], clk[6] - clk[5], clk[7] - clk[6], clk[7] - clk[0]);
+}
+constexpr size_t LF_SMEM = (size_t)(LF_MAX * LF_LD + 7 * 32 * LF_TP) * sizeof(double);
+// the leaf as a call of its own (register allocation independent of the caller: inlined into
+// the persistent kernel it shared that kernel's budget, spilled, and ran at half speed)
+__device__ __noinline__ void chol_leaf_call(double* smlf, const double* g, int w, int64_t ldg, double* r, int64_t ldr,
+                                            double* x, int64_t ldx, int* info, double* diag, int info_offset, int flags) {
+    chol_leaf_dev(smlf, g, w, ldg, r, ldr, x, ldx, info, diag, info_offset, flags);
+}
+
+__global__ void __launch_bounds__(LF_T) k_chol_inv_leaf(const double* __restrict__ g, int w, int64_t ldg,
+                                                        double* __restrict__ r, int64_t ldr, double* __restrict__ x,
+                                                        int64_t ldx, int* info, double* diag, int info_offset,
+                                                        int flags) {
+    extern __shared__ double smlf[];
+    chol_leaf_dev(smlf, g, w, ldg, r, ldr, x, ldx, info, diag, info_offset, flags);
 }
 
 // st = {info, pad, min diag(R) (running), max diag(G)}
@@ -593,15 +636,311 @@ __global__ void k_chol_status_init(const double* __restrict__ g, int64_t w, int6
     }
 }
 
+// *flag = 1 unless the factorization behind st succeeded with min diag(R) > tau·sqrt(max diag(G))
+// (the host-side chol_ok test of orth, decided on the device so no round trip is needed)
+__global__ void k_chol_flag(const int* __restrict__ st, double tau, int* flag) {
+    if (threadIdx.x != 0) return;
+    const double mn = reinterpret_cast<const double*>(st)[1], mx = reinterpret_cast<const double*>(st)[2];
+    const bool ok = st[0] == 0 && isfinite(mn) && mn > tau * sqrt(fmax(mx, 0.0));
+    if (!ok) *flag = 1;
+}
+
+
+// ------------------------------------- persistent blocked Cholesky + inverse (w > 128)
+// One cooperative launch (one 256-thread CTA per SM) runs the whole right-looking blocked
+// factorization of a w × w SPD G (upper triangle read) with 128-wide blocks, R and X = R⁻¹
+// together, all fp64 DMMA.  Step j (nb = ⌈w/128⌉ steps), three phases between grid barriers:
+//   1  CTA 0: FACT(j) — the leaf (chol_leaf_dev) on the updated diagonal block: R_jj, X_jj.
+//      The other CTAs meanwhile: the trailing update of step j−1 for block rows ≥ j+1
+//      (W_ik −= R_{j−1,i}ᵀ R_{j−1,k}) and T = X[0:j,0:j]·R[0:j, j] for X's block column j.
+//   2  PANEL: R_jk = X_jjᵀ W_jk for every k > j.
+//   3  lookahead: block row j+1 gets step j's update (W_{j+1,k} −= R_{j,j+1}ᵀ R_jk), so FACT(j+1)
+//      and PANEL(j+1) can start at once; X[0:j, j] = −T·X_jj.
+// Work items are 128 × 128 blocks (phase 1) or 64 × 64 sub-tiles (phases 2, 3; tile_mm),
+// dealt round-robin over CTAs 1.. — CTA 0 runs only the leaf, which keeps its long
+// straight-line code warm in that SM's instruction cache (run between tile products, each
+// FACT re-fetched it from a busy L2 and took ~2× the standalone leaf's time).  The
+// critical path per step is FACT + one sub-tile in each of phases 2 and 3 + three barriers;
+// the O(w³) updates and the inverse fill the SMs while CTA 0 factors (the launch-per-product
+// recursion it replaces spent ~5 ms of a 4096-wide factorization on small dependent launches).
+constexpr int PC_T = 256;
+constexpr int PC_KC = 16;            // k-chunk per shared-memory stage
+constexpr int PC_PK = PC_KC + 4;     // [m][k] / [n][k] pitch (≡ 4 mod 16: conflict-free fragments)
+constexpr int PC_AS = 128 * PC_PK;       // elements per operand buffer ([m][k]: 128 × 20; [k][m]: 16 × 132 fits)
+static_assert(PC_AS >= PC_KC * (128 + 4), "staging buffer");
+constexpr size_t PC_SMEM = LF_SMEM > (size_t)4 * PC_AS * 8 ? LF_SMEM : (size_t)4 * PC_AS * 8;
+
+// Grid-wide barrier of a cooperative launch (sense by generation; bar[0] = arrivals, bar[1] = generation)
+__device__ __forceinline__ void pc_grid_sync(unsigned int* bar, unsigned int& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned int g = gen;
+        if (atomicAdd(&bar[0], 1u) == gridDim.x - 1) {
+            bar[0] = 0;
+            __threadfence();
+            atomicExch(&bar[1], g + 1);
+        } else {
+            unsigned int v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 1) : "memory");
+            } while (v == g);
+        }
+    }
+    gen += 1;
+    __syncthreads();
+}
+
+// C(mv × nv ≤ TM × TN) = (accumulate ? C : 0) + alpha · Σ_{k0 ≤ k < k1} op(A)[i,k]·op(B)[k,j]
+//   op(A)[i,k] = TA ? A[k + i·lda] : A[i + k·lda],  op(B)[k,j] = TB ? B[j + k·ldb] : B[k + j·ldb]
+// (k is absolute: A and B point at k = 0).  256 threads, 8 warps of (TM/4) × (TN/2) (DMMA
+// 8×8×4); operands staged in k-chunks of 16 through registers into double-buffered shared
+// memory, stored along their contiguous global direction (pitches ≡ 4 mod 16).  Every read goes
+// through L2 (ld.global.cg): other CTAs of the same launch wrote the operands.
+template <int TM, int TN, bool TA, bool TB>
+__device__ void tile_mm(double* sm, const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                        int64_t ldb, int mv, int nv, int k0, int k1, double alpha, double* __restrict__ C,
+                        int64_t ldc, bool accumulate) {
+    constexpr int MF = TM / 32, NF = TN / 16;   // 8×8 fragments per warp along m, n
+    constexpr int PMA = TM + 4, PMB = TN + 4;   // [k][m] / [k][n] pitches
+    constexpr int LA = TM * PC_KC / PC_T, LB = TN * PC_KC / PC_T;  // staged elements per thread
+    double* As = sm;                 // [2][PC_AS]
+    double* Bs = sm + 2 * PC_AS;     // [2][PC_AS]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 3, wn = warp >> 2;
+    double acc[MF][NF][2];
+#pragma unroll
+    for (int a = 0; a < MF; ++a)
+#pragma unroll
+        for (int b = 0; b < NF; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    const int nc = k1 > k0 ? (k1 - k0 + PC_KC - 1) / PC_KC : 0;
+    double ra[LA], rb[LB];
+    // thread → (row, k) of a chunk: along the operand's contiguous global direction
+    auto a_at = [&](int r, int& i, int& kk) {
+        if (TA) { kk = tid & (PC_KC - 1); i = (tid / PC_KC) + (PC_T / PC_KC) * r; }
+        else { i = tid % TM; kk = (tid / TM) + (PC_T / TM) * r; }
+    };
+    auto b_at = [&](int r, int& j, int& kk) {
+        if (TB) { j = tid % TN; kk = (tid / TN) + (PC_T / TN) * r; }
+        else { kk = tid & (PC_KC - 1); j = (tid / PC_KC) + (PC_T / PC_KC) * r; }
+    };
+    auto load = [&](int c) {
+        const int kb = k0 + c * PC_KC;
+#pragma unroll
+        for (int r = 0; r < LA; ++r) {
+            int i, kk;
+            a_at(r, i, kk);
+            const int gk = kb + kk;
+            ra[r] = (i < mv && gk < k1) ? __ldcg(TA ? A + gk + (int64_t)i * lda : A + i + (int64_t)gk * lda) : 0.0;
+        }
+#pragma unroll
+        for (int r = 0; r < LB; ++r) {
+            int j, kk;
+            b_at(r, j, kk);
+            const int gk = kb + kk;
+            rb[r] = (j < nv && gk < k1) ? __ldcg(TB ? B + j + (int64_t)gk * ldb : B + gk + (int64_t)j * ldb) : 0.0;
+        }
+    };
+    auto store = [&](int buf) {
+        double* as = As + buf * PC_AS;
+        double* bs = Bs + buf * PC_AS;
+#pragma unroll
+        for (int r = 0; r < LA; ++r) {
+            int i, kk;
+            a_at(r, i, kk);
+            if (TA) as[i * PC_PK + kk] = ra[r];
+            else as[kk * PMA + i] = ra[r];
+        }
+#pragma unroll
+        for (int r = 0; r < LB; ++r) {
+            int j, kk;
+            b_at(r, j, kk);
+            if (TB) bs[kk * PMB + j] = rb[r];
+            else bs[j * PC_PK + kk] = rb[r];
+        }
+    };
+    if (nc > 0) {
+        load(0);
+        store(0);
+        __syncthreads();
+        const int fr = lane >> 2, fk = lane & 3;
+        for (int c = 0; c < nc; ++c) {
+            if (c + 1 < nc) load(c + 1);
+            const double* as = As + (c & 1) * PC_AS;
+            const double* bs = Bs + (c & 1) * PC_AS;
+#pragma unroll
+            for (int k4 = 0; k4 < PC_KC; k4 += 4) {
+                double af[MF], bf[NF];
+#pragma unroll
+                for (int a = 0; a < MF; ++a) {
+                    const int i = wm * (TM / 4) + a * 8 + fr, kk = k4 + fk;
+                    af[a] = TA ? as[i * PC_PK + kk] : as[kk * PMA + i];
+                }
+#pragma unroll
+                for (int b = 0; b < NF; ++b) {
+                    const int j = wn * (TN / 2) + b * 8 + fr, kk = k4 + fk;
+                    bf[b] = TB ? bs[kk * PMB + j] : bs[j * PC_PK + kk];
+                }
+#pragma unroll
+                for (int a = 0; a < MF; ++a)
+#pragma unroll
+                    for (int b = 0; b < NF; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            }
+            if (c + 1 < nc) store((c + 1) & 1);
+            __syncthreads();
+        }
+    }
+    // D fragment: row lane/4, columns 2·(lane%4) + {0, 1} of each 8 × 8 tile.  Accumulate: every
+    // old value is loaded before the first store (a load/store pair per element, which may alias,
+    // was serialized into one L2 round trip per element — ~40% of the tile's time)
+    if (accumulate) {
+#pragma unroll
+        for (int a = 0; a < MF; ++a)
+#pragma unroll
+            for (int b = 0; b < NF; ++b)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int i = wm * (TM / 4) + a * 8 + (lane >> 2), j = wn * (TN / 2) + b * 8 + 2 * (lane & 3) + e;
+                    const double old = (i < mv && j < nv) ? __ldcg(C + i + (int64_t)j * ldc) : 0.0;
+                    acc[a][b][e] = fma(alpha, acc[a][b][e], old);
+                }
+    } else {
+#pragma unroll
+        for (int a = 0; a < MF; ++a)
+#pragma unroll
+            for (int b = 0; b < NF; ++b)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) acc[a][b][e] *= alpha;
+    }
+#pragma unroll
+    for (int a = 0; a < MF; ++a)
+#pragma unroll
+        for (int b = 0; b < NF; ++b)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int i = wm * (TM / 4) + a * 8 + (lane >> 2), j = wn * (TN / 2) + b * 8 + 2 * (lane & 3) + e;
+                if (i < mv && j < nv) C[i + (int64_t)j * ldc] = acc[a][b][e];
+            }
+    __syncthreads();  // the staging buffers are reused by the next item
+}
+
+// W (w × w working copy of G, upper blocks updated in place), R and X (zeroed, ld w),
+// T (zeroed, w × w: the accumulated products X[0:j, 0:j]·R[0:j, j] of X's block columns),
+// st = chol_status_init's status, bar = 2 zeroed words.
+__global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict__ W, double* __restrict__ R,
+                                                            double* __restrict__ X, double* __restrict__ T, int w,
+                                                            int* st, unsigned int* bar) {
+    extern __shared__ double pcs[];
+    const int64_t ld = w;
+    const int nb = (w + 127) / 128;
+    const int cta = blockIdx.x, G = gridDim.x;
+    unsigned int gen = 0;
+    auto bs = [&](int b) { return min(128, w - b * 128); };
+    // BCUR_LEAF_TIMING=1: CTA 0 sums its clocks per phase (FACT, the wait for the other CTAs'
+    // phase-1 work, phases 2 and 3) and prints them at the end (diagnostics)
+    const bool timing = g_leaf_timing && cta == 0 && threadIdx.x == 0;
+    long long tf = 0, tw = 0, t2 = 0, t3 = 0, c0 = 0, c1 = 0;
+    for (int j = 0; j < nb; ++j) {
+        const int J = j * 128;
+        if (timing) c0 = clock64();
+        // ---- phase 1: FACT(j) on CTA 0 | the others: step j−1's trailing update of block rows
+        //      ≥ j+1 (W_ik −= R_{j−1,i}ᵀ R_{j−1,k}, whole 128 × 128 blocks) and X's block column
+        //      j−1 into the inverse accumulators (T[0:J, k] += X[0:J, j−1]·R[j−1, k], k ≥ j)
+        if (cta == 0) {
+            chol_leaf_call(pcs, W + J + (int64_t)J * ld, bs(j), ld, R + J + (int64_t)J * ld, ld, X + J + (int64_t)J * ld,
+                          ld, st, reinterpret_cast<double*>(st) + 1, J, LEAF_ZEROED);
+        } else if (j >= 1) {
+            const int s = j - 1, S = s * 128, n = nb - j - 1;
+            const int nupd = n * (n + 1) / 2;      // blocks (i, k), j+1 ≤ i ≤ k
+            const int ninv = j * (nb - j);         // blocks (r, k), r < j, k ≥ j
+            // items: 128 × 64 halves of those blocks (h = column half)
+            for (int t = cta - 1; t < 2 * (nupd + ninv); t += G - 1) {
+                const int h = t & 1, tb = t >> 1;
+                if (tb < nupd) {
+                    int i = j + 1, u = tb;          // row i holds nb − i blocks
+                    while (u >= nb - i) { u -= nb - i; ++i; }
+                    const int k = i + u, nv = min(64, bs(k) - h * 64);
+                    if (nv > 0)
+                        tile_mm<128, 64, true, false>(pcs, R + S + (int64_t)(i * 128) * ld, ld,
+                                                      R + S + (int64_t)(k * 128 + h * 64) * ld, ld, bs(i), nv, 0, bs(s),
+                                                      -1.0, W + i * 128 + (int64_t)(k * 128 + h * 64) * ld, ld, true);
+                } else {
+                    const int u = tb - nupd, r = u / (nb - j), k = j + u % (nb - j), nv = min(64, bs(k) - h * 64);
+                    if (nv > 0)
+                        tile_mm<128, 64, false, false>(pcs, X + r * 128 + (int64_t)S * ld, ld,
+                                                       R + S + (int64_t)(k * 128 + h * 64) * ld, ld, bs(r), nv, 0, bs(s),
+                                                       1.0, T + r * 128 + (int64_t)(k * 128 + h * 64) * ld, ld, true);
+                }
+            }
+        }
+        if (timing) { c1 = clock64(); tf += c1 - c0; c0 = c1; }
+        pc_grid_sync(bar, gen);
+        if (timing) { c1 = clock64(); tw += c1 - c0; c0 = c1; }
+        if (*(volatile int*)st != 0) return;  // a failed pivot (info) stops every CTA
+        // ---- phase 2: PANEL(j): R_jk = X_jjᵀ W_jk, k > j (64 × 64 sub-tiles: the critical path)
+        {
+            const int n2 = (nb - 1 - j) * 4;
+            for (int t = cta - 1; cta > 0 && t < n2; t += G - 1) {
+                const int k = j + 1 + t / 4, a = (t >> 1) & 1, b = t & 1;
+                const int mv = min(64, bs(j) - a * 64), nv = min(64, bs(k) - b * 64);
+                if (mv <= 0 || nv <= 0) continue;
+                // (X_jjᵀ)[a·64 + i, kk] = X[J + kk, J + a·64 + i], non-zero for kk ≤ a·64 + i
+                tile_mm<64, 64, true, false>(pcs, X + J + (int64_t)(J + a * 64) * ld, ld,
+                                             W + J + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, 0,
+                                             min(bs(j), a * 64 + 64), 1.0,
+                                             R + J + a * 64 + (int64_t)(k * 128 + b * 64) * ld, ld, false);
+            }
+        }
+        pc_grid_sync(bar, gen);
+        if (timing) { c1 = clock64(); t2 += c1 - c0; c0 = c1; }
+        // ---- phase 3: lookahead — block row j+1 gets step j's update (64 × 64 sub-tiles; the
+        //      diagonal block's upper halves); X[0:J, j] = −T[0:J, j]·X_jj
+        {
+            const int nupd = j + 1 < nb ? 3 + 4 * (nb - 2 - j) : 0;
+            const int nx = (J / 64) * 2;
+            const int i = j + 1;
+            for (int t = cta - 1; cta > 0 && t < nupd + nx; t += G - 1) {
+                if (t < nupd) {
+                    int k, a, b;
+                    if (t < 3) { k = i; a = t == 2 ? 1 : 0; b = t == 0 ? 0 : 1; }
+                    else { const int u = t - 3; k = i + 1 + u / 4; a = (u >> 1) & 1; b = u & 1; }
+                    const int mv = min(64, bs(i) - a * 64), nv = min(64, bs(k) - b * 64);
+                    if (mv <= 0 || nv <= 0) continue;
+                    tile_mm<64, 64, true, false>(pcs, R + J + (int64_t)(i * 128 + a * 64) * ld, ld,
+                                                 R + J + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, 0, bs(j), -1.0,
+                                                 W + (i * 128 + a * 64) + (int64_t)(k * 128 + b * 64) * ld, ld, true);
+                } else {
+                    const int u = t - nupd, r = u >> 1, b = u & 1;
+                    const int nv = min(64, bs(j) - b * 64);
+                    if (nv <= 0) continue;
+                    // X_jj upper: row kk of column b·64 + jj is non-zero for kk ≤ b·64 + jj
+                    tile_mm<64, 64, false, false>(pcs, T + r * 64 + (int64_t)J * ld, ld,
+                                                  X + J + (int64_t)(J + b * 64) * ld, ld, 64, nv, 0,
+                                                  min(bs(j), b * 64 + 64), -1.0,
+                                                  X + r * 64 + (int64_t)(J + b * 64) * ld, ld, false);
+                }
+            }
+        }
+        pc_grid_sync(bar, gen);
+        if (timing) { c1 = clock64(); t3 += c1 - c0; }
+    }
+    if (timing)
+        printf("chol_persistent w=%d nb=%d grid=%d clocks: fact %lld | wait phase-1 %lld | phase 2 %lld | phase 3 %lld\n", w,
+               nb, G, tf, tw, t2, t3);
+}
+
 }  // namespace
 
 namespace ops {
 
-static int dgemm_splits(const Ctx* c, int64_t tiles, int64_t K) {
+// Split-K count: about two CTAs per SM.  Thin outputs (≤ 1 M elements, reduced by a warp per
+// element) may split up to that many ways — the 60 × 60 Gram of a 65536-row panel ran 64
+// splits of K = 1024 at one SM's DMMA rate (55 µs); wider outputs stay at ≤ 64 splits.
+static int dgemm_splits(const Ctx* c, int64_t tiles, int64_t K, int64_t MN) {
     const int64_t target = 2LL * c->sm_count;
     if (tiles >= target || K < 8 * DBK) return 1;
     int64_t s = std::min<int64_t>((target + tiles - 1) / tiles, K / (16 * DBK));
-    return (int)std::max<int64_t>(1, std::min<int64_t>(s, 64));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(s, MN <= (1 << 20) ? target : 64));
 }
 
 void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
@@ -619,7 +958,7 @@ void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, 
     const int64_t mt = (M + DBM - 1) / DBM, nt = (N + DBN - 1) / DBN;
     int64_t tiles = mt * nt;
     if (flags & GEMM_SYM_UPPER) tiles = (tiles + std::min(mt, nt)) / 2;
-    int splits = dgemm_splits(c, tiles, K);
+    int splits = dgemm_splits(c, tiles, K, M * N);
     int64_t kchunk = (std::max<int64_t>(K, 1) + splits - 1) / splits;
     kchunk = (kchunk + DBK - 1) / DBK * DBK;
     splits = (int)((std::max<int64_t>(K, 1) + kchunk - 1) / kchunk);
@@ -677,8 +1016,44 @@ void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st) 
     LAUNCH_CHECK(c);
 }
 
+void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st) {
+    if (w < 1 || w > (1 << 20)) fail(BCUR_E_INVALID_ARGUMENT, "chol_persistent: bad width");
+    ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
+    static int grid = 0;
+    if (!grid) {
+        CUDA_CHECK(cudaFuncSetAttribute(k_chol_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PC_SMEM));
+        int per_sm = 0;
+        CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_persistent, PC_T, PC_SMEM));
+        grid = std::max(1, per_sm) * c->sm_count;
+        const char* t = getenv("BCUR_LEAF_TIMING");
+        const int on = (t && t[0] == '1') ? 1 : 0;
+        if (on) CUDA_CHECK(cudaMemcpyToSymbol(g_leaf_timing, &on, sizeof on));
+    }
+    if (grid < 2) fail(BCUR_E_CUDA, "chol_persistent: needs two co-resident CTAs");
+    DevBuf W(c, (size_t)w * w * sizeof(double)), T(c, (size_t)w * w * sizeof(double)), bar(c, 64);
+    CUDA_CHECK(cudaMemcpy2DAsync(W.ptr, w * sizeof(double), g, ldg * sizeof(double), w * sizeof(double), w,
+                                 cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_CHECK(cudaMemsetAsync(r, 0, (size_t)w * w * sizeof(double), c->stream));
+    CUDA_CHECK(cudaMemsetAsync(x, 0, (size_t)w * w * sizeof(double), c->stream));
+    CUDA_CHECK(cudaMemsetAsync(T.ptr, 0, T.bytes, c->stream));
+    CUDA_CHECK(cudaMemsetAsync(bar.ptr, 0, 64, c->stream));
+    double* wp = W.as<double>();
+    double* tp = T.as<double>();
+    unsigned int* bp = bar.as<unsigned int>();
+    int wi = (int)w;
+    void* args[] = {&wp, &r, &x, &tp, &wi, &st, &bp};
+    CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_chol_persistent, dim3(grid), dim3(PC_T), args, PC_SMEM,
+                                           c->stream));
+    LAUNCH_CHECK(c);
+}
+
+void chol_flag(Ctx* c, const int* st, double tau, int* flag) {
+    k_chol_flag<<<1, 32, 0, c->stream>>>(st, tau, flag);
+    LAUNCH_CHECK(c);
+}
+
 void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int64_t ldr, double* x, int64_t ldx,
-                   int* info, double* diag, int64_t info_offset) {
+                   int* info, double* diag, int64_t info_offset, int flags) {
     if (w > LF_MAX || w < 1) fail(BCUR_E_INVALID_ARGUMENT, "chol_inv_leaf: 1 <= w <= 128");
     ProfScope prof(c, "chol_inv_leaf", 2.0 * w * w * w / 3.0, 8.0 * 3 * w * w);
     constexpr size_t smem = (size_t)(LF_MAX * LF_LD + 7 * 32 * LF_TP) * sizeof(double);
@@ -690,7 +1065,7 @@ void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, i
         if (on) CUDA_CHECK(cudaMemcpyToSymbol(g_leaf_timing, &on, sizeof on));
         attr = true;
     }
-    k_chol_inv_leaf<<<1, LF_T, smem, c->stream>>>(g, (int)w, ldg, r, ldr, x, ldx, info, diag, (int)info_offset);
+    k_chol_inv_leaf<<<1, LF_T, smem, c->stream>>>(g, (int)w, ldg, r, ldr, x, ldx, info, diag, (int)info_offset, flags);
     LAUNCH_CHECK(c);
 }
 

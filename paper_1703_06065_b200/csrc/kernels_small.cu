@@ -483,6 +483,7 @@ __global__ void __launch_bounds__(ST) k_jacobi(const double* __restrict__ g, int
 // rotations are logged (p, q, c, s) and k_jacobi_replay applies them to the rows of V on
 // many SMs afterwards.
 constexpr int JP_T = 1024;
+__device__ int g_jac_timing = 0;  // BCUR_JACOBI_TIMING=1: thread 0 prints the phase clocks (diagnostics)
 struct JRot {
     double c, s;
     int p, q;
@@ -509,10 +510,13 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     __syncthreads();
     const int nblk = half * (half + 1) / 2;
     int rounds = 0;
+    const bool timing = g_jac_timing && threadIdx.x == 0;
+    long long ta = 0, tb = 0, c0 = 0, c1 = 0;
     for (int sweep = 0; sweep < max_sweeps; ++sweep) {
         if (threadIdx.x == 0) rotated = 0;
         __syncthreads();
         for (int round = 0; round < mrot; ++round, ++rounds) {
+            if (timing) c0 = clock64();
             for (int i = threadIdx.x; i < half; i += NT) {
                 int p = i == 0 ? round : (round + i) % mrot;
                 int q = i == 0 ? wp - 1 : (round - i + mrot) % mrot;
@@ -540,6 +544,7 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
                 log[(int64_t)rounds * half + i] = JRot{c, sv, p, q};
             }
             __syncthreads();
+            if (timing) { c1 = clock64(); ta += c1 - c0; c0 = c1; }
             // block (P, Q), P ≥ Q, enumerated over the packed block triangle
             for (int b = threadIdx.x; b < nblk; b += NT) {
                 int P = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
@@ -572,6 +577,7 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
                 if (r2 && c2v) Ap[i_qq] = s2 * b_qp + c2 * b_qq;
             }
             __syncthreads();
+            if (timing) tb += clock64() - c0;
         }
         if (!rotated) break;
         __syncthreads();
@@ -586,6 +592,8 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
             const int t = order[i]; order[i] = order[best]; order[best] = t;
         }
         *nrounds_out = rounds;
+        if (timing) printf("jacobi_packed w=%d threads=%d rounds=%d clocks/round: rotations %lld | updates %lld\n", w, NT,
+                           rounds, ta / (rounds ? rounds : 1), tb / (rounds ? rounds : 1));
     }
     __syncthreads();
     for (int j = threadIdx.x; j < w; j += NT) {
@@ -806,6 +814,13 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
         if (!attr) {
             CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_packed, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
             attr = true;
+        }
+        static bool timing_set = false;
+        if (!timing_set) {
+            const char* t = getenv("BCUR_JACOBI_TIMING");
+            const int on = (t && t[0] == '1') ? 1 : 0;
+            if (on) CUDA_CHECK(cudaMemcpyToSymbol(g_jac_timing, &on, sizeof on));
+            timing_set = true;
         }
         constexpr int max_sweeps = 40;
         const int64_t half = (w + 1) / 2, rounds_max = (int64_t)max_sweeps * (2 * half - 1);

@@ -38,6 +38,7 @@ __device__ int g_dbg_flags = 0;  // BCUR_UMMA_DEBUG: bit 0 skip a_lo transform, 
 bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
 bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (experiments)
 bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
+bool g_no_h3pair = false;         // BCUR_UMMA_NO_H3_PAIR=1: single-CTA 3×FP16 products (experiments)
 int g_pf = -1;                    // BCUR_UMMA_PF: A-tile L2 prefetch distance in stages (experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
@@ -98,7 +99,14 @@ struct Cfg {
                   "X3 register split must fit the launch allocation");
     static_assert(TMEM_COLS <= 512, "TMEM budget");
 };
-enum { EPI_STORE = 0, EPI_ROWSQ = 1, EPI_RESID = 2 };
+// EPI_SPLIT / EPI_BASIS (3×FP16 A·X whose output is an orthonormal-basis candidate, |v| < 2):
+//   SPLIT  the product written straight into the interleaved hi/lo layout of split_il (2M
+//          halves per column, [hi 64 | lo 64] per 64-row chunk) with the fixed column scale
+//          2^BASIS_E — the next products' A/X operand, with no fp64 copy and no split pass
+//   BASIS  v + (the aux split, read back) written as the fp32 basis and its fp16·2^BASIS_E copy
+//          (basis_out's layout): the CholQR2 correction Q = Q1 + Q1·(−F) and its output pass fused
+enum { EPI_STORE = 0, EPI_ROWSQ = 1, EPI_RESID = 2, EPI_SPLIT = 3, EPI_BASIS = 4 };
+constexpr int BASIS_E = 14;
 
 // Round an fp32 value to the nearest TF32 (10-bit mantissa), ties to even.
 __device__ __forceinline__ float rn_tf32(float x) {
@@ -341,10 +349,11 @@ __global__ void __launch_bounds__(Cfg<NT, X3, H>::NTHREADS, 1)
 k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
        const __grid_constant__ CUtensorMap tmXl, const __grid_constant__ CUtensorMap tmAl, int M, int N,
        const Sched sc, double* __restrict__ out, int64_t ldo, double* __restrict__ partial, double alpha, double beta,
-       const int* __restrict__ rexp, const int* __restrict__ cexp) {
+       const int* __restrict__ rexp, const int* __restrict__ cexp, const uint16_t* __restrict__ aux) {
     // instruction descriptor: fp32 accumulate, tf32 × tf32 (H: f16 × f16), B K-major,
     // N = n_cols, M = 128
-    static_assert(!H || (X3 ? (EPI == EPI_STORE || (EPI == EPI_RESID && A_MN)) : (EPI == EPI_ROWSQ && !A_MN)),
+    static_assert(!H || (X3 ? (EPI == EPI_STORE || (A_MN && (EPI == EPI_RESID || EPI == EPI_SPLIT || EPI == EPI_BASIS)))
+                           : (EPI == EPI_ROWSQ && !A_MN)),
                   "fp16 operands: 3×FP16 products (stored, or the fused residual), or the pre-converted "
                   "row-sum-of-squares");
     constexpr bool H3 = H && X3;
@@ -505,6 +514,44 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                     }
                 }
             }
+        } else if (EPI == EPI_SPLIT || EPI == EPI_BASIS) {
+            // lanes are consecutive rows of one 64-row chunk: each column's hi (and lo) stores are
+            // one 64-byte run per warp
+            if (row < M) {
+                const int ncol = min(DC, N - col0);
+                const int64_t r_il = (int64_t)(row >> 6) * 128 + (row & 63);
+                uint16_t* o16 = reinterpret_cast<uint16_t*>(EPI == EPI_SPLIT ? out : partial);
+                float* o32 = reinterpret_cast<float*>(out);
+#pragma unroll
+                for (int j = 0; j < DC; ++j) {
+                    if (j >= ncol) continue;
+                    const int col = col0 + j;
+                    double v = (double)acc[j] + (double)cmp[X3 ? j : 0];
+                    v *= alpha * exp2_int(-(cexp ? cexp[col] : 0));
+                    if (EPI == EPI_SPLIT) {
+                        const double sv = v * (double)(1 << BASIS_E);
+                        const __half h = __double2half(sv);
+                        const __half l = __double2half(sv - (double)__half2float(h));
+                        o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
+                        o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
+                    } else {
+                        if (aux) {
+                            const uint16_t hb = aux[(int64_t)col * 2 * M + r_il], lb = aux[(int64_t)col * 2 * M + r_il + 64];
+                            v += ((double)__half2float(*reinterpret_cast<const __half*>(&hb)) +
+                                  (double)__half2float(*reinterpret_cast<const __half*>(&lb))) *
+                                 (1.0 / (double)(1 << BASIS_E));
+                        }
+                        o32[row + (int64_t)col * ldo] = (float)v;
+                        // the fp16 copy as the interleaved split of v·2^14: hi = the row-Σ² pass's
+                        // operand, lo = its rounding error (the sketch correction's Δ)
+                        const double sv = v * (double)(1 << BASIS_E);
+                        const __half h = __double2half(sv);
+                        const __half l = __double2half(sv - (double)__half2float(h));
+                        o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
+                        o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
+                    }
+                }
+            }
         } else if (EPI == EPI_ROWSQ) {
             double s = 0.0;
 #pragma unroll
@@ -604,9 +651,9 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
 #pragma unroll
                         for (int nt = 0; nt < NT; ++nt) {
                             const int xc = (n_tile * NT + nt) * BN;
-                            if (H3 && sc.x_il) {
+                            if (H && sc.x_il) {
                                 tma_load_4d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], 0, 0, k0 / 64, xc);
-                                tma_load_4d(x_lo(s) + nt * X_TILE, &tmXh, &full[s], 0, 1, k0 / 64, xc);
+                                if (X3) tma_load_4d(x_lo(s) + nt * X_TILE, &tmXh, &full[s], 0, 1, k0 / 64, xc);
                             } else {
                                 tma_load_2d(x_hi(s) + nt * X_TILE, &tmXh, &full[s], k0, xc);
                                 if (X3) tma_load_2d(x_lo(s) + nt * X_TILE, &tmXl, &full[s], k0, xc);
@@ -773,7 +820,7 @@ template <bool A_MN, int EPI, int NT, bool X3, bool H = false>
 void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
                     int N, double* out, int64_t ldo, double* partial, double alpha, double beta,
                     const CUtensorMap* tal = nullptr, const int* rexp = nullptr, const int* cexp = nullptr,
-                    bool wave_barrier = true) {
+                    bool wave_barrier = true, const uint16_t* aux = nullptr) {
     using CF = Cfg<NT, X3, H>;
     auto kern = k_umma<A_MN, EPI, NT, X3, H>;
     static bool attr = false;
@@ -802,7 +849,7 @@ void launch_umma_nt(Ctx* c, Sched sc, const CUtensorMap& ta, const CUtensorMap& 
     cfg.attrs = attr_c;
     cfg.numAttrs = 1;
     CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, th, tl, tal ? *tal : ta, M, N, sc, out, ldo, partial, alpha, beta,
-                                  rexp, cexp));
+                                  rexp, cexp, aux));
     LAUNCH_CHECK(c);
 }
 
@@ -876,7 +923,7 @@ __device__ __forceinline__ void pair_tile(int t, int m_pairs, int n_tiles, int* 
 template <bool H>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2_THREADS, 1)
 k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int M, int m_pairs,
-              int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr) {
+              int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr, int x_il) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = (uint64_t*)(smem + P2_STAGES * P2_STAGE);
@@ -952,11 +999,18 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                             " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(k0),
                             "r"(m_tile * BM) : "memory");
 #pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        asm volatile(
-                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st + A_TILE + h * X_TILE)), "l"(&tmX),
-                            "r"(fb), "r"(k0), "r"((nt * NTP + (int)rank * 2 + h) * BN) : "memory");
+                    for (int h = 0; h < 2; ++h) {
+                        if (x_il)  // hi of an interleaved split (4-D map, part 0)
+                            asm volatile(
+                                "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(st + A_TILE + h * X_TILE)), "l"(&tmX),
+                                "r"(fb), "r"(0), "r"(0), "r"(k0 / 64), "r"((nt * NTP + (int)rank * 2 + h) * BN) : "memory");
+                        else
+                            asm volatile(
+                                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st + A_TILE + h * X_TILE)), "l"(&tmX),
+                                "r"(fb), "r"(k0), "r"((nt * NTP + (int)rank * 2 + h) * BN) : "memory");
+                    }
                 }
                 if (wave_ctr) atomicAdd(wave_ctr, 1u);
             }
@@ -1071,6 +1125,8 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 struct PSched {
     int m_pairs, n_tiles, total, k_tiles, sym, tri_x;
     unsigned int* wave_ctr;
+    int bke;   // K elements per k-tile (32 tf32, 64 fp16): the triangular-X limit is in these units
+    int x_il;  // H3: x_hi/x_lo from one interleaved split (4-D map, part = hi|lo)
 };
 constexpr int X3P_NTRANSFORM = 6, X3P_NDRAIN = 8;
 constexpr int X3P_THREADS = 32 * (2 + X3P_NTRANSFORM + X3P_NDRAIN);        // 512
@@ -1099,7 +1155,7 @@ __device__ __forceinline__ void x3p_tile(const PSched& sc, int t, int* mp, int* 
     } else {
         pair_tile(t, sc.m_pairs, sc.n_tiles, mp, nt);
     }
-    *nk = sc.tri_x ? min(sc.k_tiles, ((*nt + 1) * 2 * BN + BK - 1) / BK) : sc.k_tiles;
+    *nk = sc.tri_x ? min(sc.k_tiles, ((*nt + 1) * 2 * BN + sc.bke - 1) / sc.bke) : sc.k_tiles;
 }
 
 template <bool A_MN>
@@ -1367,6 +1423,8 @@ PSched make_psched(int mt, int nt, int k_tiles, bool sym, bool tri_x) {
     sc.sym = sym ? 1 : 0;
     sc.tri_x = tri_x ? 1 : 0;
     sc.wave_ctr = nullptr;
+    sc.bke = BK;
+    sc.x_il = 0;
     if (sym) {
         sc.total = 0;
         for (int n = 0; n < nt; ++n) sc.total += std::min(n / 2, sc.m_pairs - 1) + 1;
@@ -1374,6 +1432,313 @@ PSched make_psched(int mt, int nt, int k_tiles, bool sym, bool tri_x) {
         sc.total = sc.m_pairs * nt;
     }
     return sc;
+}
+
+
+// ------------------------------------------- CTA-pair 3×FP16 product (cta_group::2)
+// The tensor-bound 3×FP16 products (Grams of C and Q1, C·R⁻¹, the CholQR2 correction, c4's
+// Aᵀ·Q_C) on CTA pairs: one pair per 256 output rows × 128 output columns.  Each CTA stages
+// its own 128-row a_hi/a_lo tile and HALF of x_hi/x_lo (48 KB per stage; both CTAs' TMA bytes
+// land on the leader's barrier through the 2-SM TMA form), and the leader issues three M = 256
+// × N = 128 MMAs per k-step (a_hi·x_hi → hi, a_hi·x_lo → lo, a_lo·x_hi → lo) that read both
+// CTAs' shared memory.  Per SM and k-step that is 18 KB of operand reads + 12 KB of TMA writes
+// for 2·786 K flop, against 20 + 16 KB for the single-CTA N = 128 H3 tile — the single-CTA
+// kernel is bound by shared-memory bandwidth (0.67 of the f16 MMA rate measured, 0.67 modelled).
+// Epilogues as k_umma's H3 forms: STORE (α, β, exact scale removal), SPLIT, BASIS.
+constexpr int H2_NDRAIN = 8;                                  // 4 lane quarters × 2 64-column tiles
+constexpr int H2_THREADS = 32 * (4 + H2_NDRAIN);              // producer, MMA, 2 idle, drains
+constexpr uint32_t H2_STAGE = 2 * A_TILE + 2 * X_TILE;        // a_hi, a_lo, x_hi half, x_lo half
+constexpr int H2_STAGES = (int)((232448u - 1280u) / H2_STAGE);
+constexpr uint32_t H2_SMEM = H2_STAGES * H2_STAGE + 1024 + 256;
+constexpr uint32_t H2_R0 = (65536u / H2_THREADS) / 8 * 8;     // 168
+constexpr uint32_t H2_REG_LOW = 56;
+constexpr uint32_t H2_REG_DRAIN_FIT = H2_R0 + ((H2_THREADS - 32 * H2_NDRAIN) * (H2_R0 - H2_REG_LOW) / (32 * H2_NDRAIN)) / 8 * 8;
+constexpr uint32_t H2_REG_DRAIN = H2_REG_DRAIN_FIT > 232 ? 232 : H2_REG_DRAIN_FIT;
+
+template <bool A_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(H2_THREADS, 1)
+k_umma2_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
+           const __grid_constant__ CUtensorMap tmXl, int M, int N, const PSched sc, void* __restrict__ out_v,
+           int64_t ldo, double alpha, double beta, const int* __restrict__ rexp, const int* __restrict__ cexp,
+           uint16_t* __restrict__ q16, const uint16_t* __restrict__ aux) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + H2_STAGES * H2_STAGE);
+    uint64_t* full = bars;                     // [STAGES] leader: both CTAs' bytes
+    uint64_t* empty = full + H2_STAGES;        // [STAGES] each CTA: multicast MMA commit
+    uint64_t* tfull = empty + H2_STAGES;       // [2]      each CTA: multicast MMA commit
+    uint64_t* tempty = tfull + 2;              // [2]      leader: both CTAs' drain warps
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = warp_index(), lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    constexpr int NTP = 2;                     // 64-column tiles per pair tile
+    constexpr int BKH = bke<true>();
+    constexpr uint32_t IDESC = (1u << 4) | ((A_MN ? 1u : 0u) << 15) | ((uint32_t)((NTP * BN) >> 3) << 17) |
+                               ((uint32_t)(2 * BM >> 4) << 24);   // f16 × f16 → f32, M = 256, N = 128
+    constexpr uint32_t BUF = 2 * NTP * BN;     // hi + lo columns per TMEM buffer
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < H2_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * H2_NDRAIN);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXh) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXl) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    auto a_hi = [&](int s) { return smem + s * H2_STAGE; };
+    auto x_hi = [&](int s) { return smem + s * H2_STAGE + 2 * A_TILE; };
+
+    if (warp >= 4) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(H2_REG_DRAIN));
+        // ------------------------------------------- drain (both CTAs, own TMEM rows)
+        const int q = warp & 3, tile = (warp - 4) >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t tempty0 = map_to_rank(smem_u32(&tempty[0]), 0);
+        int gc = 0;
+        for (int t = pair; t < sc.total; t += npairs) {
+            int mp, nt, nk;
+            x3p_tile(sc, t, &mp, &nt, &nk);
+            const int nchunks = (nk + CH - 1) / CH;
+            const int row = (2 * mp + (int)rank) * BM + q * 32 + lane;
+            float acc[BN], cmp[BN];
+#pragma unroll
+            for (int j = 0; j < BN; ++j) acc[j] = cmp[j] = 0.0f;
+            for (int c = 0; c < nchunks; ++c) {
+                const int g = gc + c, b = g & 1;
+                mbar_wait(&tfull[b], (uint32_t)(g / 2) & 1u);
+                tc_fence_after();
+                const uint32_t t_hi = tmem + lane_off + (uint32_t)(b * BUF + tile * BN), t_lo = t_hi + NTP * BN;
+#pragma unroll
+                for (int j0 = 0; j0 < BN; j0 += 8) {
+                    uint32_t h[8], l[8];
+                    TMEM_LD8(t_hi + j0, h);
+                    TMEM_LD8(t_lo + j0, l);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {  // as k_umma's X3 drain: Fast2Sum of hi, cross terms into cmp
+                        const int e = j0 + j;
+                        const float hv = __uint_as_float(h[j]);
+                        const float sum = __fadd_rn(acc[e], hv);
+                        const float z = __fsub_rn(sum, acc[e]);
+                        cmp[e] = __fadd_rn(cmp[e], __fadd_rn(__fsub_rn(hv, z), __uint_as_float(l[j])));
+                        acc[e] = sum;
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)  // default (cta-scope) form, as k_umma2_rowsq
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+            }
+            gc += nchunks;
+            const int col0 = nt * NTP * BN + tile * BN;
+            if (row < M) {
+                const int ncol = min(BN, N - col0);
+                const int re = rexp ? rexp[row] : 0;
+                if (EPI == EPI_STORE) {
+                    double* dst = reinterpret_cast<double*>(out_v) + row;
+                    constexpr int EB = 16;  // β ≠ 0: old values loaded 16 at a time before the stores
+#pragma unroll
+                    for (int j0 = 0; j0 < BN; j0 += EB) {
+                        double old[EB];
+#pragma unroll
+                        for (int jj = 0; jj < EB; ++jj)
+                            old[jj] = (beta != 0.0 && j0 + jj < ncol) ? dst[(int64_t)(col0 + j0 + jj) * ldo] : 0.0;
+#pragma unroll
+                        for (int jj = 0; jj < EB; ++jj) {
+                            const int j = j0 + jj;
+                            if (j >= ncol) continue;
+                            double v = (double)acc[j] + (double)cmp[j];
+                            v *= exp2_int(-(re + (cexp ? cexp[col0 + j] : 0)));
+                            dst[(int64_t)(col0 + j) * ldo] = beta == 0.0 ? alpha * v : fma(beta, old[jj], alpha * v);
+                        }
+                    }
+                } else {
+                    const int64_t r_il = (int64_t)(row >> 6) * 128 + (row & 63);
+#pragma unroll
+                    for (int j = 0; j < BN; ++j) {
+                        if (j >= ncol) continue;
+                        const int col = col0 + j;
+                        double v = ((double)acc[j] + (double)cmp[j]) * (alpha * exp2_int(-(re + (cexp ? cexp[col] : 0))));
+                        if (EPI == EPI_SPLIT) {
+                            uint16_t* o16 = reinterpret_cast<uint16_t*>(out_v);
+                            const double sv = v * (double)(1 << BASIS_E);
+                            const __half h = __double2half(sv);
+                            const __half l = __double2half(sv - (double)__half2float(h));
+                            o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
+                            o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
+                        } else {
+                            if (aux) {
+                                const uint16_t hb = aux[(int64_t)col * 2 * M + r_il], lb = aux[(int64_t)col * 2 * M + r_il + 64];
+                                v += ((double)__half2float(*reinterpret_cast<const __half*>(&hb)) +
+                                      (double)__half2float(*reinterpret_cast<const __half*>(&lb))) *
+                                     (1.0 / (double)(1 << BASIS_E));
+                            }
+                            reinterpret_cast<float*>(out_v)[row + (int64_t)col * ldo] = (float)v;
+                            const double sv = v * (double)(1 << BASIS_E);  // interleaved hi/lo, as k_umma
+                            const __half h = __double2half(sv);
+                            const __half l = __double2half(sv - (double)__half2float(h));
+                            q16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
+                            q16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(H2_REG_LOW));
+        if (warp == 0) {
+            // ---------------------------------------------------------------- producer
+            if (lane == 0) {
+                const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);  // leader's barriers
+                int gi = 0;
+                for (int t = pair, w = 0; t < sc.total; t += npairs, ++w) {
+                    if (sc.wave_ctr && w > 0) {  // wave barrier (see Sched)
+                        unsigned int target = 0;
+                        for (int v = 0; v < w; ++v)
+                            target += 2u * (unsigned int)max(0, min(npairs, sc.total - v * npairs));
+                        unsigned int val;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(val) : "l"(sc.wave_ctr) : "memory");
+                        } while (val < target);
+                    }
+                    int mp, nt, nk;
+                    x3p_tile(sc, t, &mp, &nt, &nk);
+                    const int m_tile = 2 * mp + (int)rank, xc = (nt * NTP + (int)rank) * BN;
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % H2_STAGES;
+                        mbar_wait(&empty[s], ((uint32_t)(gi / H2_STAGES) & 1u) ^ 1u);
+                        if (rank == 0) mbar_expect_tx(&full[s], 2 * H2_STAGE);
+                        const uint32_t fb = full0 + s * 8;
+                        const int k0 = i * BKH;
+                        const uint32_t sa = smem_u32(a_hi(s)), sx = smem_u32(x_hi(s));
+                        auto load4 = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(tm), "r"(fb), "r"(c0), "r"(c1),
+                                "r"(c2), "r"(c3) : "memory");
+                        };
+#pragma unroll
+                        for (int hl = 0; hl < 2; ++hl) {  // A: the interleaved hi/lo copy (4-D map)
+                            if (A_MN) {  // two 64-row chunks (8 KB MN atoms) × 64 K rows
+                                load4(sa + hl * A_TILE, &tmA, 0, hl, m_tile * 2, k0);
+                                load4(sa + hl * A_TILE + A_TILE / 2, &tmA, 0, hl, m_tile * 2 + 1, k0);
+                            } else {
+                                load4(sa + hl * A_TILE, &tmA, 0, hl, k0 / 64, m_tile * BM);
+                            }
+                        }
+                        if (sc.x_il) {
+                            load4(sx, &tmXh, 0, 0, k0 / 64, xc);
+                            load4(sx + X_TILE, &tmXh, 0, 1, k0 / 64, xc);
+                        } else {
+#pragma unroll
+                            for (int hl = 0; hl < 2; ++hl)
+                                asm volatile(
+                                    "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                    " [%0], [%1, {%3, %4}], [%2];" ::"r"(sx + hl * X_TILE), "l"(hl ? &tmXl : &tmXh),
+                                    "r"(fb), "r"(k0), "r"(xc) : "memory");
+                        }
+                    }
+                    if (sc.wave_ctr) atomicAdd(sc.wave_ctr, 1u);
+                }
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------- MMA issuer (leader only)
+            if (rank == 0) {
+                int gi = 0, gc = 0;
+                for (int t = pair; t < sc.total; t += npairs) {
+                    int mp, nt, nk;
+                    x3p_tile(sc, t, &mp, &nt, &nk);
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % H2_STAGES;
+                        const int c = gc + i / CH, b = c & 1;
+                        const bool first = (i % CH) == 0;
+                        if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
+                        mbar_wait(&full[s], (uint32_t)(gi / H2_STAGES) & 1u);
+                        tc_fence_after();
+                        const uint32_t ah = smem_u32(a_hi(s)), al = ah + A_TILE;
+                        const uint32_t xh = smem_u32(x_hi(s)), xl = xh + X_TILE;
+                        const uint32_t d_hi = tmem + (uint32_t)(b * BUF), d_lo = d_hi + NTP * BN;
+#pragma unroll
+                        for (int k8 = 0; k8 < BK / 8; ++k8) {
+                            uint64_t dah, dal;
+                            if (A_MN) {  // [2 MN atoms of 64, 8 KB apart][64 K rows of 128 B, 8-row groups 1 KB apart]
+                                dah = sdesc(ah + k8 * 2048, 8192, 1024, 2);
+                                dal = sdesc(al + k8 * 2048, 8192, 1024, 2);
+                            } else {
+                                dah = sdesc(ah + k8 * 32, 16, 1024, 2);
+                                dal = sdesc(al + k8 * 32, 16, 1024, 2);
+                            }
+                            const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
+                            const uint64_t dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
+                            const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n\t.reg .pred e, p, one;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                "setp.ne.b32 p, %7, 0;\n\tsetp.eq.b32 one, %7, %7;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %2, %3, %6, p;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %2, %4, %6, p;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%1], %5, %3, %6, one;\n\t}" ::"r"(d_hi),
+                                "r"(d_lo), "l"(dah), "l"(dxh), "l"(dxl), "l"(dal), "r"(IDESC), "r"(acc));
+                        }
+                        asm volatile(
+                            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                            " [%0], %1;\n\t}" ::"r"(smem_u32(&empty[s])), "h"((uint16_t)3) : "memory");
+                        if ((i % CH) == CH - 1 || i == nk - 1)
+                            asm volatile(
+                                "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                                " [%0], %1;\n\t}" ::"r"(smem_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+                        __syncwarp();
+                    }
+                    gc += (nk + CH - 1) / CH;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <bool A_MN, int EPI>
+void launch_umma2_h3(Ctx* c, PSched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
+                     int N, void* out, int64_t ldo, double alpha, double beta, const int* rexp, const int* cexp,
+                     uint16_t* q16, const uint16_t* aux) {
+    auto kern = k_umma2_h3<A_MN, EPI>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, H2_SMEM));
+        attr = true;
+    }
+    if (sc.total <= 0) return;
+    const int pairs = std::min(sc.total, c->sm_count / 2);
+    DevBuf ctr;
+    sc.wave_ctr = nullptr;
+    if (pairs < sc.total && !g_wave_barrier_off) {  // ≤ 1 CTA per SM: all co-resident
+        ctr = DevBuf(c, 64);
+        CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
+        sc.wave_ctr = ctr.as<unsigned int>();
+    }
+    kern<<<2 * pairs, H2_THREADS, H2_SMEM, c->stream>>>(ta, th, tl, M, N, sc, out, ldo, alpha, beta, rexp, cexp, q16,
+                                                         aux);
+    LAUNCH_CHECK(c);
 }
 
 // ------------------------------------------------ fp16 operands (row-Σ² passes)
@@ -1511,6 +1876,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         g_no_pair = np_ && np_[0] == '1';
         const char* nx = getenv("BCUR_UMMA_X3_PAIR");
         g_no_x3pair = !(nx && nx[0] == '1');
+        const char* nh = getenv("BCUR_UMMA_NO_H3_PAIR");
+        g_no_h3pair = nh && nh[0] == '1';
         const char* pf = getenv("BCUR_UMMA_PF");
         if (pf) g_pf = atoi(pf);
         const char* d = getenv("BCUR_UMMA_DEBUG");
@@ -1573,7 +1940,7 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
                 wc = ctr.as<unsigned int>();
             }
             k_umma2_rowsq<false><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, th, (int)n, m_pairs, nt, k_tiles,
-                                                                         part.as<double>(), wc);
+                                                                         part.as<double>(), wc, 0);
             LAUNCH_CHECK(c);
         } else if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
@@ -1623,7 +1990,7 @@ void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float
 
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
                        const void* X, int dtx, int64_t ldx, double* rowsq, bool interleaved, const uint16_t* x16_pre,
-                       int q_pre) {
+                       int q_pre, bool x16_il) {
     if (M <= 0) return;
     if (N <= 0 || K <= 0) {
         CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
@@ -1665,8 +2032,13 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     const uint32_t bX[2] = {BKH, BN};
     CUtensorMap ta = make_map(A16, 4, dA, sA, bA, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
                               interleaved ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
-    CUtensorMap tx = make_map(x16_pre ? (const void*)x16_pre : x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B,
-                              CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+    const bool xil = x16_pre && x16_il;  // X = the hi part of an interleaved split (4-D map, part 0)
+    const uint64_t dXi[4] = {64, 2, (uint64_t)(K / 64), (uint64_t)N}, sXi[3] = {128, 256, (uint64_t)K * 4};
+    const uint32_t bXi[4] = {64, 1, 1, BN};
+    CUtensorMap tx = xil ? make_map(x16_pre, 4, dXi, sXi, bXi, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B)
+                         : make_map(x16_pre ? (const void*)x16_pre : x16.ptr, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     const int k_tiles = (int)((K + BKH - 1) / BKH);
     const int mt = (int)((M + BM - 1) / BM);
     const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
@@ -1688,12 +2060,13 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
             wc = ctr.as<unsigned int>();
         }
         k_umma2_rowsq<true><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, tx, (int)M, m_pairs, nt, k_tiles,
-                                                                           part.as<double>(), wc);
+                                                                           part.as<double>(), wc, xil ? 1 : 0);
         LAUNCH_CHECK(c);
     } else {
         Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);
         sc.a_rn = 1;  // converted operands: no transform
         sc.pf = g_pf >= 0 ? g_pf : 0;  // no L2 prefetch on the fp16 copy (as the 3×FP16 passes)
+        sc.x_il = xil ? 1 : 0;
         if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false, true>(c, sc, ta, tx, tx, (int)M, (int)N, nullptr, 0,
                                                              part.as<double>(), 1.0, 0.0);
@@ -1834,8 +2207,12 @@ bool h3_ok(int64_t m) {
     return enabled && m > 0 && m % 64 == 0 && m < (1LL << 30);
 }
 
-void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const F16View& X,
-             double alpha, double beta, double* out, int64_t ldo, int flags) {
+// epi: EPI_STORE (out fp64), EPI_SPLIT (out = the uint16 interleaved split, a_mn), EPI_BASIS (out = fp32 q32,
+// q16 = its fp16 copy, aux = the split added back, a_mn)
+static void umma_h3_epi(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const F16View& X,
+                        double alpha, double beta, void* out_v, int64_t ldo, int flags, int epi, uint16_t* q16,
+                        const uint16_t* aux) {
+    double* out = reinterpret_cast<double*>(out_v);
     const bool sym_req = (flags & GEMM_SYM_UPPER) != 0, tri = (flags & GEMM_B_UPPER) != 0 && a_mn;
     const int64_t M = a_mn ? m : n, K = a_mn ? n : m, N = X.N;
     if (M <= 0 || N <= 0) return;
@@ -1864,9 +2241,14 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
         tl = make_map(X.lo, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
     } else {     // interleaved (split_il layout, K % 64 == 0): one 4-D map, part 0 = hi, 1 = lo
         if (K % 64 != 0) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: an interleaved X needs K % 64 == 0");
-        const uint64_t dX[4] = {64, 2, (uint64_t)(K / 64), (uint64_t)N}, sX[3] = {128, 256, (uint64_t)K * 4};
+        // X.part ≥ 0: that part alone — a one-part map based at it, so the kernel's load of the
+        // other part falls outside the tensor and reads as zeros (TMA fill)
+        const bool one = X.part >= 0;
+        const uint64_t dX[4] = {64, one ? 1u : 2u, (uint64_t)(K / 64), (uint64_t)N}, sX[3] = {128, 256, (uint64_t)K * 4};
         const uint32_t bX[4] = {64, 1, 1, BN};
-        th = make_map(X.hi, 4, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+        th = make_map(one ? X.hi + 64 * X.part : X.hi, 4, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                      one ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
         tl = th;
     }
     const int k_tiles = (int)((K + BKH - 1) / BKH);
@@ -1875,7 +2257,7 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     // split-K fills the last persistent wave, but its fp64 partials cost (splits + 1)·M·N·8
     // bytes of traffic plus a reduce: for wide outputs (the 4096² Gram of C) that exceeded the
     // wave it saved, so only outputs below 8 M elements split
-    int splits = (double)M * (double)N <= 8.0e6 ? h3_splits(tiles, k_tiles, c->sm_count) : 1;
+    int splits = (epi == EPI_STORE && (double)M * (double)N <= 8.0e6) ? h3_splits(tiles, k_tiles, c->sm_count) : 1;
     const int kps = (k_tiles + splits - 1) / splits;
     splits = (k_tiles + kps - 1) / kps;
     Sched sc = make_sched(mt, nt, splits, k_tiles, kps, sym, tri);
@@ -1886,7 +2268,41 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     sc.bke = BKH;  // fp16 k-tiles: the diagonal limit of a triangular X in 64-row units (was 2× too far)
     const int* rexp = a_mn ? nullptr : ea;
     const int* cexp = X.exps;
+    if (NT == 2 && splits == 1 && M >= 2 * BM && !g_no_h3pair) {
+        // tensor-bound shapes: CTA pairs (k_umma2_h3)
+        PSched ps = make_psched(mt, nt, k_tiles, sym, tri);
+        ps.bke = BKH;
+        ps.x_il = X.lo ? 0 : 1;
+        // the A·X map's box is one 64-row chunk × 64 columns (two loads per tile), AᵀX one chunk × 128
+        if (a_mn) {
+            if (epi == EPI_SPLIT)
+                launch_umma2_h3<true, EPI_SPLIT>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, 0.0, rexp, cexp,
+                                                 nullptr, nullptr);
+            else if (epi == EPI_BASIS)
+                launch_umma2_h3<true, EPI_BASIS>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, 0.0, rexp, cexp,
+                                                 q16, aux);
+            else
+                launch_umma2_h3<true, EPI_STORE>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, beta, rexp, cexp,
+                                                 nullptr, nullptr);
+        } else {
+            if (epi != EPI_STORE) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: split/basis output needs A·X");
+            launch_umma2_h3<false, EPI_STORE>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, beta, rexp, cexp,
+                                              nullptr, nullptr);
+        }
+        return;
+    }
     auto launch = [&](double* o, int64_t ldo_, double* prt, double al, double be) {
+        if (epi == EPI_SPLIT || epi == EPI_BASIS) {
+            if (!a_mn || NT != 2 || M % 64 != 0) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: split/basis output needs A·X, N > 64, M % 64 == 0");
+            if (epi == EPI_SPLIT)
+                launch_umma_nt<true, EPI_SPLIT, 2, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, nullptr, al, 0.0,
+                                                                nullptr, nullptr, cexp);
+            else
+                launch_umma_nt<true, EPI_BASIS, 2, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_,
+                                                                reinterpret_cast<double*>(q16), al, 0.0, nullptr, nullptr,
+                                                                cexp, true, aux);
+            return;
+        }
         if (a_mn) {
             if (NT == 2) launch_umma_nt<true, EPI_STORE, 2, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, prt, al, be, nullptr, rexp, cexp);
             else launch_umma_nt<true, EPI_STORE, 1, true, true>(c, sc, ta, th, tl, (int)M, (int)N, o, ldo_, prt, al, be, nullptr, rexp, cexp);
@@ -1904,6 +2320,35 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
     launch(nullptr, 0, part.as<double>(), 1.0, 0.0);
     k_reduce_splits<<<(unsigned)((M * N + 255) / 256), 256, 0, c->stream>>>(M, N, splits, part.as<double>(), out, ldo,
                                                                             alpha, beta);
+    LAUNCH_CHECK(c);
+}
+
+void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const F16View& X,
+             double alpha, double beta, double* out, int64_t ldo, int flags) {
+    umma_h3_epi(c, a_mn, AL, ea, m, n, X, alpha, beta, out, ldo, flags, EPI_STORE, nullptr, nullptr);
+}
+
+void umma_h3_to_split(Ctx* c, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,
+                      int64_t N, int64_t ldx, double alpha, uint16_t* out_il, int flags) {
+    SplitF16 xs;
+    split_f16(c, X, dtx, n, N, ldx, ea, &xs);
+    umma_h3_epi(c, true, AL, ea, m, n, view(xs), alpha, 0.0, out_il, m, flags, EPI_SPLIT, nullptr, nullptr);
+}
+
+void umma_h3_basis(Ctx* c, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx, int64_t N,
+                   int64_t ldx, double alpha, const uint16_t* addend_il, float* q32, uint16_t* q16, int flags) {
+    SplitF16 xs;
+    split_f16(c, X, dtx, n, N, ldx, ea, &xs);
+    umma_h3_epi(c, true, AL, ea, m, n, view(xs), alpha, 0.0, q32, m, flags, EPI_BASIS, q16, addend_il);
+}
+
+__global__ void k_fill_int(int* p, int64_t count, int v) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < count) p[i] = v;
+}
+void fill_basis_exps(Ctx* c, int* exps, int64_t n) {
+    if (n <= 0) return;
+    k_fill_int<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(exps, n, BASIS_E);
     LAUNCH_CHECK(c);
 }
 

@@ -57,10 +57,11 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 // round-to-nearest 1×TF32 pass, twice the MMA rate, half the bytes) and the scales are
 // removed exactly in fp64.
 // interleaved: A16 is the [hi 64 | lo 64]-per-chunk copy (only hi is read), else compact hi.
-// x16_pre (nullable): X already in fp16 (K × N, ld K) scaled by 2^q_pre (B is then unused)
+// x16_pre (nullable): X already in fp16 (K × N, ld K) scaled by 2^q_pre (B is then unused);
+// x16_il: x16_pre is an interleaved hi/lo split (2K halves per column) whose hi part is X
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
                        const void* B, int dtb, int64_t ldb, double* rowsq, bool interleaved = true,
-                       const uint16_t* x16_pre = nullptr, int q_pre = 0);
+                       const uint16_t* x16_pre = nullptr, int q_pre = 0, bool x16_il = false);
 // orthonormal Q (fp64) → fp32 basis + its fp16 copy scaled by 2^14 (one pass)
 void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float* q32, uint16_t* q16);
 // out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
@@ -77,11 +78,18 @@ void dgemm_resid_sumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, co
                        const void* B, int dtb, int64_t ldb, const void* D, int dtd, int64_t ldd, double* out);
 // st = {int info, int pad, double min diag(R) = +inf, double max diag(G)} before a factorization
 void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st);
+// w > 128: R (upper, ld w) with G = RᵀR (G's upper triangle read, ldg) and X = R⁻¹ (upper, ld w)
+// in one cooperative persistent launch (blocked right-looking, fp64 DMMA); st as chol_status_init
+// (initialized by the caller), info = failed pivot + 1
+void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st);
+// *flag = 1 unless the factorization with status st passed min diag(R) > tau·sqrt(max diag(G))
+void chol_flag(Ctx* c, const int* st, double tau, int* flag);
 // w ≤ 128, one CTA: R (upper, lower zeroed) with G = RᵀR from G's upper triangle, and X = R⁻¹
 // (upper).  Chained status: skipped when *info != 0; failure → info = info_offset + j + 1;
-// diag[0] = running min diag(R).
+// diag[0] = running min diag(R).  flags: 1 = R not written (r may be null), 2 = the lower
+// triangles of R and X are already zero (only the upper triangles are written)
 void chol_inv_leaf(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, int64_t ldr, double* x, int64_t ldx,
-                   int* info, double* diag, int64_t info_offset);
+                   int* info, double* diag, int64_t info_offset, int flags = 0);
 
 // ---- tcgen05 3×TF32 A-passes (kernels_umma.cu), fp32 A only ----------------
 bool umma_ok(int dta, int64_t m, int64_t lda, const void* a);
@@ -109,6 +117,7 @@ struct F16View {
     const int* exps;
     int64_t K, N;
     int64_t ld = 0;  // separate hi/lo: leading dimension in halves (0: K)
+    int part = -1;   // interleaved only: 0 / 1 = read the hi / lo part alone as X (the other reads as zero)
 };
 inline F16View view(const SplitF16& s) {
     return {s.hi.as<uint16_t>(), s.lo.as<uint16_t>(), s.exps.as<int>(), s.K, s.N, s.ld};
@@ -133,6 +142,19 @@ void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, in
              double alpha, double beta, double* out, int64_t ldo, int flags = 0);
 void umma_h3(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,
              int64_t N, int64_t ldx, double alpha, double beta, double* out, int64_t ldo, int flags = 0);
+
+// Out = alpha·A·X (a_mn form; N > 64, m % 64 == 0) written straight into the interleaved split
+// layout (2m halves per column) with the fixed column exponent 14 (fill_basis_exps): for
+// outputs with |entries| < 2 (orthonormal-basis candidates, e.g. Q1 = C·R⁻¹)
+void umma_h3_to_split(Ctx* c, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx,
+                      int64_t N, int64_t ldx, double alpha, uint16_t* out_il, int flags = 0);
+// Q = alpha·A·X (+ addend_il read back from its fixed-exponent split, nullable) written as the
+// fp32 basis q32 (m × N, ld m) and its fp16 copy q16: the interleaved split of Q·2^14 (2m halves
+// per column; hi = the row-Σ² passes' operand, lo = hi's rounding error)
+void umma_h3_basis(Ctx* c, const uint16_t* AL, const int* ea, int64_t m, int64_t n, const void* X, int dtx, int64_t N,
+                   int64_t ldx, double alpha, const uint16_t* addend_il, float* q32, uint16_t* q16, int flags = 0);
+// exps[0..n) = 14, the column exponents of umma_h3_to_split's output
+void fill_basis_exps(Ctx* c, int* exps, int64_t n);
 
 // Σ_ij (D − A·X)_ij² with A the interleaved split (m × n, exps ea), X fp64 (n × N, ldx), D fp32
 // (m × N, ldd): the explicit residual's second product fused with the subtraction (tcgen05 3×FP16)

@@ -142,6 +142,7 @@ struct CholRec {
     int* st;
     cudaStream_t main_s, side_s;
     bool tc;  // products of ≥ 512-wide blocks on the tcgen05 3×FP16 kernels (fp32-class Grams)
+    bool want_r;  // the caller reads R (its diagonal blocks are never read inside the recursion)
     size_t ev = 0;
 };
 
@@ -167,8 +168,9 @@ static void chol_rec(CholRec& S, int64_t o, int64_t n) {
     const int64_t w = S.w;
     auto at = [&](double* p, int64_t i, int64_t j) { return p + i + j * w; };
     if (n <= 128) {
+        // R and X were zeroed by chol_enqueue: the leaf writes the upper triangles only
         chol_inv_leaf(c, at(S.W, o, o), n, w, at(S.R, o, o), w, at(S.X, o, o), w, S.st,
-                      reinterpret_cast<double*>(S.st) + 1, o);
+                      reinterpret_cast<double*>(S.st) + 1, o, (S.want_r ? 0 : 1) | 2);
         return;
     }
     const int64_t nl = (n + 127) / 128, n1 = (nl + 1) / 2 * 128, n2 = n - n1, o2 = o + n1;
@@ -195,32 +197,45 @@ static void chol_rec(CholRec& S, int64_t o, int64_t n) {
 
 // G (w×w SPD, fp64, upper triangle read) → R upper (w×w, ld w, lower zero) with G = RᵀR, and
 // (Rinv nullable) X = R⁻¹ (upper, ld w).  info != 0: the pivot info − 1 failed (R, X invalid).
+// Enqueue the factorization (no host round trip): st (64 bytes) receives {info, pad, min diag(R),
+// max diag(G)} (chol_status_init's layout).
+// want_r = false: R's diagonal blocks are not written (R still holds the off-diagonal blocks).
+static void chol_enqueue(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* X, bool tc, int* st,
+                         bool want_r = true) {
+    chol_status_init(c, G, w, ldg, st);
+    if (w <= 128) {
+        chol_inv_leaf(c, G, w, ldg, R, w, X, w, st, reinterpret_cast<double*>(st) + 1, 0, want_r ? 0 : 1);
+        return;
+    }
+    static const bool rec = getenv("BCUR_CHOL_REC") != nullptr;  // experiments: the launch-per-product recursion
+    if (!rec) {
+        chol_persistent(c, G, w, ldg, R, X, st);
+        return;
+    }
+    ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
+    Mat64 W(c, w, w);
+    copy_f64(c, G, w, w, ldg, W.p(), w);
+    CUDA_CHECK(cudaMemsetAsync(R, 0, (size_t)w * w * sizeof(double), c->stream));
+    CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)w * w * sizeof(double), c->stream));
+    cudaStream_t main_s = c->stream, side_s = c->side_stream();
+    c->order(main_s, side_s, 0);
+    CholRec S{c, W.p(), R, X, w, st, main_s, side_s, tc, want_r};
+    chol_rec(S, 0, w);
+    c->stream = main_s;
+    c->order(side_s, main_s, 1);
+}
+
 static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv = nullptr,
-                         bool tc = false) {
+                         bool tc = false, bool want_r = true) {
     DevBuf st(c, 64);
     struct { int info; int pad; double mindiag, maxdiag; } hs;
-    chol_status_init(c, G, w, ldg, st.as<int>());
     Mat64 Xown;
     double* X = Rinv;
     if (!X) {
         Xown = Mat64(c, w, w);
         X = Xown.p();
     }
-    if (w <= 128) {
-        chol_inv_leaf(c, G, w, ldg, R, w, X, w, st.as<int>(), st.as<double>() + 1, 0);
-    } else {
-        ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
-        Mat64 W(c, w, w);
-        copy_f64(c, G, w, w, ldg, W.p(), w);
-        CUDA_CHECK(cudaMemsetAsync(R, 0, (size_t)w * w * sizeof(double), c->stream));
-        CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)w * w * sizeof(double), c->stream));
-        cudaStream_t main_s = c->stream, side_s = c->side_stream();
-        c->order(main_s, side_s, 0);
-        CholRec S{c, W.p(), R, X, w, st.as<int>(), main_s, side_s, tc};
-        chol_rec(S, 0, w);
-        c->stream = main_s;
-        c->order(side_s, main_s, 1);
-    }
+    chol_enqueue(c, G, w, ldg, R, X, tc, st.as<int>(), want_r);
     CUDA_CHECK(cudaMemcpyAsync(&hs, st.ptr, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
     return {hs.info, hs.info ? 0.0 : hs.mindiag, hs.maxdiag};
@@ -266,7 +281,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w), Q1(c, rows, w);
     gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld);
     if (dist) allreduce(c, G.p(), w * w);
-    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Ri.p());
+    const CholInfo ci = chol_any(c, G.p(), w, G.ld, R.p(), Ri.p(), false, T_out != nullptr);
     if (ref < 0) ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     int64_t r = w;
     const bool chol_ok = ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref;
@@ -289,7 +304,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
             gemm(c, OP_N, OP_T, rows, rows, w, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, Gr.p(), Gr.ld);
             {   // safely full row rank → range(X) = ℝ^rows: Q = I, T = X (no eigensolve)
                 Mat64 Rr(c, rows, rows);
-                const CholInfo cr = chol_any(c, Gr.p(), rows, Gr.ld, Rr.p());
+                const CholInfo cr = chol_any(c, Gr.p(), rows, Gr.ld, Rr.p(), nullptr, false, false);
                 if (cr.info == 0 && std::isfinite(cr.mindiag) && cr.mindiag > tau_chol(dt) * ref) {
                     fill_f64(c, Q1.p(), rows * rows, 0.0);
                     Mat64 one(c, rows, 1);
@@ -320,7 +335,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
             copy_f64(c, U.p(), rows, r, U.ld, Q1.p(), Q1.ld);
             Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
             gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
-            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), R2i.p());
+            const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), R2i.p(), false, T_out != nullptr);
             if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
             gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
             if (T_out) {  // T = R2 · (Q1ᵀ X)
@@ -367,7 +382,7 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     Mat64 G2(c, r, r), R2(c, r, r), R2i(c, r, r);
     gemm(c, OP_T, OP_N, r, r, rows, 1.0, Q1.p(), BCUR_F64, Q1.ld, Q1.p(), BCUR_F64, Q1.ld, 0.0, G2.p(), G2.ld);
     if (dist) allreduce(c, G2.p(), r * r);
-    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), R2i.p());
+    const CholInfo c2 = chol_any(c, G2.p(), r, G2.ld, R2.p(), R2i.p(), false, T_out != nullptr);
     if (c2.info != 0) fail(BCUR_E_ITERATION_FAILURE, "orth: second CholQR pass failed");
     gemm(c, OP_N, OP_N, rows, r, r, 1.0, Q1.p(), BCUR_F64, Q1.ld, R2i.p(), BCUR_F64, R2i.ld, 0.0, Q, ldq);
     if (T_out) {
@@ -386,6 +401,22 @@ int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, doub
     return r;
 }
 
+// Power-iteration orthonormalization (range finder, q ≥ 1): only span(Q) = span(X) matters
+// there — the next product re-mixes the columns — so one CholQR pass Q = X·R⁻¹ suffices
+// whenever orth's own CholQR test passes (min R_ii > τ_chol·ref ⇒ κ(X) < 1/τ_chol and
+// ‖QᵀQ − I‖ ≲ κ²·u); the test runs on the device (*flag = 1 when it fails, and the caller
+// redoes the range finder through orth), so no host round trip is needed.
+static void orth_span(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double tau, double* Q,
+                      int64_t ldq, bool dist, int* flag) {
+    Mat64 G(c, w, w), R(c, w, w), Ri(c, w, w);
+    DevBuf st(c, 64);
+    gemm(c, OP_T, OP_N, w, w, rows, 1.0, X, BCUR_F64, ldx, X, BCUR_F64, ldx, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
+    if (dist) allreduce(c, G.p(), w * w);
+    chol_enqueue(c, G.p(), w, G.ld, R.p(), Ri.p(), false, st.as<int>(), false);
+    chol_flag(c, st.as<int>(), tau, flag);
+    gemm(c, OP_N, OP_N, rows, w, w, 1.0, X, BCUR_F64, ldx, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q, ldq, GEMM_B_UPPER);
+}
+
 // ----------------------------------------------------------------- bases
 // Orthonormal basis kept in fp32 (fp32 inputs: every product with it runs on the
 // tensor cores) or fp64 (fp64 inputs).
@@ -393,13 +424,13 @@ struct Basis {
     DevBuf buf;
     int dt = BCUR_F64;
     int64_t rows = 0, cap = 0, rank = 0;
-    void init(Ctx* c, int dt_, int64_t rows_, int64_t cap_) {
+    void init(Ctx* c, int dt_, int64_t rows_, int64_t cap_, bool zero = true) {
         dt = dt_;
         rows = rows_;
         cap = std::max<int64_t>(cap_, 1);
         rank = 0;
         buf = DevBuf(c, (size_t)std::max<int64_t>(rows, 1) * cap * dtype_size(dt));
-        CUDA_CHECK(cudaMemsetAsync(buf.ptr, 0, buf.bytes, c->stream));
+        if (zero) CUDA_CHECK(cudaMemsetAsync(buf.ptr, 0, buf.bytes, c->stream));
     }
     void* col(int64_t j) const { return (char*)buf.ptr + (size_t)j * rows * dtype_size(dt); }
     // optional 3×FP16 form of the fp32 basis (the interleaved hi/lo A operand, kept in step
@@ -410,8 +441,10 @@ struct Basis {
     // pass, rinv2 = I − F or the full R2⁻¹ of the second), kept for U = C⁺AR⁺ (block_cur)
     Mat64 rinv1, rinv2;
     bool has_rinv() const { return rinv1.m > 0 && rinv1.m == rank; }
-    // fp16 copy of the basis scaled by 2^14 (entries ≤ 1): the row-Σ² passes' X operand
-    DevBuf x16;
+    // the basis scaled by 2^14 (entries ≤ 1) as an interleaved fp16 hi/lo split (2·rows halves per
+    // column): hi is the row-Σ² passes' X operand, lo its rounding error (sketch_correction);
+    // x16e = the split's column exponents (all 14)
+    DevBuf x16, x16e;
     void enable_h3(Ctx* c) {
         if (dt != BCUR_F32 || !h3_ok(rows)) return;
         il = DevBuf(c, (size_t)rows * cap * 4);
@@ -462,7 +495,7 @@ static int64_t cgs2_append(Ctx* c, Basis* B, double* P, int64_t w, int64_t ldp, 
 // cil_pre (nullable): C already split (gathered from A's interleaved copy with its exponents).
 static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bool dist, int dt, Basis* B,
                              bool keep_rinv, DevBuf* cil_pre = nullptr, DevBuf* ce_pre = nullptr) {
-    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), Q1(c, rows, cc), R1i;
+    Mat64 G(c, cc, cc), R(c, cc, cc), Ri(c, cc, cc), R1i;
     DevBuf cil, ce;
     if (cil_pre) {
         cil = std::move(*cil_pre);
@@ -473,18 +506,21 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
     umma_h3(c, false, cil.as<uint16_t>(), ce.as<int>(), rows, cc, cx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true);
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true, false);
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
-    umma_h3(c, true, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, 0.0, Q1.p(),
-            Q1.ld, GEMM_B_UPPER);
+    // Q1 = C·R⁻¹ written straight into its interleaved split (fixed column exponent: the columns
+    // of Q1 have norm ≈ 1) — the operand of the Gram Q1ᵀQ1 and of the second-pass product, with
+    // no fp64 Q1 and no split pass
+    DevBuf qil(c, (size_t)rows * cc * 4), qe(c, (size_t)cc * sizeof(int));
+    fill_basis_exps(c, qe.as<int>(), cc);
+    umma_h3_to_split(c, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0,
+                     qil.as<uint16_t>(), GEMM_B_UPPER);
     cil = DevBuf();
     if (keep_rinv) {
         R1i = Mat64(c, cc, cc);
         copy_f64(c, Ri.p(), cc, cc, Ri.ld, R1i.p(), cc);
     }
-    DevBuf qil, qe;
-    split_il(c, Q1.p(), BCUR_F64, rows, cc, Q1.ld, &qil, &qe);
     const F16View qx{qil.as<uint16_t>(), nullptr, qe.as<int>(), rows, cc};
     umma_h3(c, false, qil.as<uint16_t>(), qe.as<int>(), rows, cc, qx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
@@ -497,14 +533,17 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     if (near) {
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), true);
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true);
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true, false);
         if (c2.info != 0) return false;
     }
-    umma_h3(c, true, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0, near ? 1.0 : 0.0,
-            Q1.p(), Q1.ld, GEMM_B_UPPER);
-    B->init(c, BCUR_F32, rows, cc);
-    B->x16 = DevBuf(c, (size_t)rows * cc * 2);
-    basis_out(c, Q1.p(), rows, cc, Q1.ld, B->buf.as<float>(), B->x16.as<uint16_t>());
+    B->init(c, BCUR_F32, rows, cc, false);  // every column is written below
+    B->x16 = DevBuf(c, (size_t)rows * cc * 4);
+    B->x16e = DevBuf(c, (size_t)cc * sizeof(int));
+    fill_basis_exps(c, B->x16e.as<int>(), cc);
+    // the second-pass product and the basis output in one pass: Q = Q1·X2 (+ Q1 read back from
+    // its split when X2 = −F), written as the fp32 basis and its fp16·2^14 copy
+    umma_h3_basis(c, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0,
+                  near ? qil.as<uint16_t>() : nullptr, B->buf.as<float>(), B->x16.as<uint16_t>(), GEMM_B_UPPER);
     B->rank = cc;
     if (keep_rinv) {
         B->rinv1 = std::move(R1i);
@@ -523,7 +562,7 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
     gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, cdt, rows, C, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
+    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), false, false);
     const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
     if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
@@ -551,7 +590,7 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
         // pass is exact to ~1e-11; fp64: Q = Q1·(I − F) on DGEMM
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), cdt == BCUR_F32);
     } else {
-        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p());
+        const CholInfo c2 = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), false, false);
         if (c2.info != 0) return false;
     }
     B->init(c, cdt, rows, cc);
@@ -587,12 +626,14 @@ static void a_product(Ctx* c, const DMat* a, const RoundedA* ra, bool trans, int
         gemm(c, OP_N, OP_N, a->m, N, a->n, 1.0, a->ptr, a->dtype, a->ld, X, dtx, ldx, 0.0, out, ldo);
 }
 
-void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
-                  bool rank_floor, const RoundedA* ra) {
+// fast: every orthonormalization is one orth_span CholQR pass (no host round trips; the power
+// iterations need only the span, the final basis passes the stricter κ < 100 test); returns
+// false when a device-side CholQR test failed — the caller then reruns with fast = false
+// (orth's CholQR2 / SVQB paths, identical to the oracle's).
+static bool range_finder_impl(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
+                              bool rank_floor, const RoundedA* ra, bool fast) {
     const int64_t m = a->m, nl = a->n;
     const int64_t ng = a->n_global > 0 ? a->n_global : a->n;
-    if (k < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: k must be >= 1");
-    if (p < 0 || q < 0) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: p and q must be >= 0");
     const int64_t l = std::min(k + p, std::min(m, ng));
     const int dt = a->dtype;
     Mat64 Om(c, nl, l), Y(c, m, l);
@@ -600,18 +641,26 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
     a_product(c, a, ra, false, l, Om.p(), BCUR_F64, Om.ld, Y.p(), Y.ld);
     allreduce(c, Y.p(), m * l);
     Mat64 Qy(c, m, l);
+    DevBuf flag(c, 64);
+    if (fast) CUDA_CHECK(cudaMemsetAsync(flag.ptr, 0, sizeof(int), c->stream));
     int64_t r = l;
     for (int64_t it = 0; it < q; ++it) {
-        r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
+        if (fast) orth_span(c, Y.p(), m, r, Y.ld, tau_chol(dt), Qy.p(), Qy.ld, false, flag.as<int>());
+        else r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
         if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
         Mat64 Z(c, nl, r), Qz(c, nl, r);
         a_product(c, a, ra, true, r, Qy.p(), BCUR_F64, Qy.ld, Z.p(), Z.ld);
-        r = orth(c, Z.p(), nl, r, Z.ld, -1.0, dt, Qz.p(), Qz.ld, true, nullptr, nullptr);
+        if (fast) orth_span(c, Z.p(), nl, r, Z.ld, tau_chol(dt), Qz.p(), Qz.ld, true, flag.as<int>());
+        else r = orth(c, Z.p(), nl, r, Z.ld, -1.0, dt, Qz.p(), Qz.ld, true, nullptr, nullptr);
         if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
         a_product(c, a, ra, false, r, Qz.p(), BCUR_F64, Qz.ld, Y.p(), Y.ld);
         allreduce(c, Y.p(), m * r);
     }
-    r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
+    // The final basis: one CholQR pass as well when κ(Y) < 100 (min R_ii > 1e-2·ref): then
+    // ‖QᵀQ − I‖ ≲ 1e4·u ≈ 1e-12 and B = QᵀA has the singular subspace of the CholQR2 basis to
+    // that accuracy.  Otherwise (the flag) the whole range finder reruns through orth.
+    if (fast) orth_span(c, Y.p(), m, r, Y.ld, std::max(tau_chol(dt), 1e-2), Qy.p(), Qy.ld, false, flag.as<int>());
+    else r = orth(c, Y.p(), m, r, Y.ld, -1.0, dt, Qy.p(), Qy.ld, false, nullptr, nullptr);
     if (r == 0) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
     // Bᵀ = Aᵀ·Q (n_local × r); B·Bᵀ = Σ_ranks Bᵀ_sᵀ Bᵀ_s
     Mat64 Bt(c, nl, r), Gb(c, r, r), lam(c, r, 1), Ut(c, r, r);
@@ -619,8 +668,11 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
     gemm(c, OP_T, OP_N, r, r, nl, 1.0, Bt.p(), BCUR_F64, Bt.ld, Bt.p(), BCUR_F64, Bt.ld, 0.0, Gb.p(), Gb.ld);
     allreduce(c, Gb.p(), r * r);
     sym_eig(c, Gb.p(), r, Gb.ld, lam.p(), Ut.p());
+    int hflag = 0;
+    if (fast) CUDA_CHECK(cudaMemcpyAsync(&hflag, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     std::vector<double> lh(r);
-    d2h(c, lh.data(), lam.p(), r);
+    d2h(c, lh.data(), lam.p(), r);  // (synchronizes the stream: hflag is valid)
+    if (hflag) return false;         // a failed CholQR test: Q (and everything after) is unusable
     std::vector<double> sg(r);
     for (int64_t i = 0; i < r; ++i) sg[i] = std::sqrt(std::max(lh[i], 0.0));
     if (!(sg[0] > 0.0)) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
@@ -649,6 +701,16 @@ void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64
     out->k_eff = ke;
     out->l = l;
     out->sigma.assign(sg.begin(), sg.begin() + rank);
+    return true;
+}
+
+void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
+                  bool rank_floor, const RoundedA* ra) {
+    if (k < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: k must be >= 1");
+    if (p < 0 || q < 0) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: p and q must be >= 0");
+    static const bool no_fast = getenv("BCUR_RF_SAFE") != nullptr;  // experiments: orth everywhere
+    if (!no_fast && range_finder_impl(c, a, k, p, q, key, out, rank_floor, ra, true)) return;
+    range_finder_impl(c, a, k, p, q, key, out, rank_floor, ra, false);
 }
 
 // ------------------------------------------------------------- helpers
@@ -786,7 +848,7 @@ static void rowsq_pass(Ctx* c, const DMat* a, const RoundedA* ra, int64_t N, con
                        double* rows, const uint16_t* x16 = nullptr) {
     if (ra && ra->ok())
         gemm_rowsumsq_f16(c, a->n, N, a->m, ra->il.as<uint16_t>(), a->m, ra->exps.as<int>(), X, dtx, ldx, rows,
-                          ra->interleaved, (x16 && ldx == a->m) ? x16 : nullptr, 14);
+                          ra->interleaved, (x16 && ldx == a->m) ? x16 : nullptr, 14, true);
     else
         gemm_rowsumsq(c, OP_T, OP_N, a->n, N, a->m, a->ptr, a->dtype, a->ld, X, dtx, ldx, rows);
 }
@@ -817,21 +879,31 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
 // thin DMMA products (r × k).
 static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub) {
     const int64_t m = B.rows, r = B.rank, ke = sub.k_eff;
-    if (r <= 0 || ke <= 0 || !B.x16.ptr || B.dt != BCUR_F32) return 0.0;
-    Mat64 US(c, m, ke), sg(c, ke, 1), W(c, r, 2 * ke), tot(c, 2, 1);
+    if (r <= 0 || ke <= 0 || !B.x16.ptr || B.dt != BCUR_F32 || !h3_ok(m)) return 0.0;
+    // W_hi = (UΣ)ᵀQ̃ and W_lo = (UΣ)ᵀΔ from the two parts of the basis's fp16 split (Q̃ = hi,
+    // Δ = lo, Q = Q̃ + Δ to 22 bits): 3×FP16 products with UΣ split once, reading only the
+    // 2-byte parts — no fp32 copy of Q̃ and no pass over the fp32 Q:
+    //   Σ_k σ_k²(‖Qᵀu_k‖² − ‖Q̃ᵀu_k‖²) = ‖W_hi + W_lo‖² − ‖W_hi‖²
+    // (W_lo is 2⁻¹¹ of W_hi: the fp64 difference keeps ~13 digits of the correction)
+    Mat64 US(c, m, ke), sg(c, ke, 1), W(c, ke, 3 * r), tot(c, 2, 1);
     copy_f64(c, sub.u.p(), m, ke, sub.u.ld, US.p(), US.ld);
     h2d(c, sg.p(), sub.sigma.data(), ke);
     scale_columns(c, US.p(), m, ke, US.ld, sg.p());
-    DevBuf q16(c, (size_t)m * r * sizeof(float));
-    f16_to_f32(c, B.x16.as<uint16_t>(), m * r, 1.0f / 16384.0f, q16.as<float>());
-    gemm(c, OP_T, OP_N, r, ke, m, 1.0, B.buf.ptr, BCUR_F32, m, US.p(), BCUR_F64, US.ld, 0.0, W.p(), W.ld);
-    gemm(c, OP_T, OP_N, r, ke, m, 1.0, q16.ptr, BCUR_F32, m, US.p(), BCUR_F64, US.ld, 0.0, W.p() + ke * W.ld, W.ld);
-    const int64_t off[2] = {0, r};
+    DevBuf uil, ue;
+    split_il(c, US.p(), BCUR_F64, m, ke, US.ld, &uil, &ue);
+    double* blk[3] = {W.p(), W.p() + r * W.ld, W.p() + 2 * r * W.ld};  // W_hi | −W_lo | W_hi + W_lo
+    for (int part = 0; part < 2; ++part) {
+        F16View xv{B.x16.as<uint16_t>(), nullptr, B.x16e.as<int>(), m, r};
+        xv.part = part;
+        umma_h3(c, false, uil.as<uint16_t>(), ue.as<int>(), m, ke, xv, part ? -1.0 : 1.0, 0.0, blk[part], W.ld);
+    }
+    copy_f64(c, blk[0], ke, r, W.ld, blk[2], W.ld);
+    axpy_neg(c, blk[1], blk[2], ke * r);
+    const int64_t off[2] = {0, r};  // one block of r columns: its Σ of squares
     DevBuf doff(c, sizeof off);
     h2d(c, doff.as<int64_t>(), off, 2);
-    for (int half = 0; half < 2; ++half)  // ‖W_half‖_F²: per-row sums, then one segment
-        row_sumsq_blocks(c, W.p() + half * ke * W.ld, BCUR_F64, r, ke, W.ld, doff.as<int64_t>(), 1, nullptr,
-                         tot.p() + half);
+    block_sumsq(c, blk[2], BCUR_F64, ke, W.ld, doff.as<int64_t>(), 1, tot.p());
+    block_sumsq(c, blk[0], BCUR_F64, ke, W.ld, doff.as<int64_t>(), 1, tot.p() + 1);
     double h[2] = {0.0, 0.0};
     d2h(c, h, tot.p(), 2);
     return h[0] - h[1];
@@ -1572,7 +1644,7 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
         auto pinv_rows = [&](const Mat64& T, int64_t rk, int64_t cols, Mat64* out_p) {
             Mat64 G(c, rk, rk), R(c, rk, rk), Ri(c, rk, rk), Gi(c, rk, rk);
             gemm(c, OP_N, OP_T, rk, rk, cols, 1.0, T.p(), BCUR_F64, T.ld, T.p(), BCUR_F64, T.ld, 0.0, G.p(), G.ld);
-            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Ri.p());
+            const CholInfo ci = chol_any(c, G.p(), rk, G.ld, R.p(), Ri.p(), false, false);
             if (ci.info != 0) fail(BCUR_E_ITERATION_FAILURE, "block_cur: factor Gram is not positive definite");
             gemm(c, OP_N, OP_T, rk, rk, rk, 1.0, Ri.p(), BCUR_F64, Ri.ld, Ri.p(), BCUR_F64, Ri.ld, 0.0, Gi.p(), Gi.ld);
             *out_p = Mat64(c, cols, rk);
