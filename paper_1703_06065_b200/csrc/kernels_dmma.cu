@@ -319,7 +319,7 @@ void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, 
 // k) then hits 16 distinct 8-byte bank pairs per half-warp — with an odd pitch it was 4-way
 // conflicted and the leaf's DMMA phases ran at the shared-memory wavefront rate
 constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 4, LF_TP = 36;
-enum { LEAF_NO_R = 1, LEAF_ZEROED = 2 };  // chol_inv_leaf flags (ops.h)
+enum { LEAF_NO_R = 1, LEAF_ZEROED = 2, LEAF_QUIET = 4 };  // chol_inv_leaf flags (ops.h); QUIET: no timing print
 __device__ int g_leaf_timing = 0;  // BCUR_LEAF_TIMING=1: thread 0 prints the phase clocks (diagnostics)
 #define LF_CLK(i) do { if (timing && threadIdx.x == 0) clk[i] = clock64(); } while (0)
 
@@ -346,7 +346,7 @@ __device__ __forceinline__ void chol_leaf_dev(double* smlf, const double* __rest
     __shared__ int stop_sh;
     __shared__ double mn_sh;
     if (*(volatile int*)info != 0) return;
-    const int timing = g_leaf_timing;
+    const int timing = g_leaf_timing && !(flags & LEAF_QUIET);
     long long clk[16] = {0};
     LF_CLK(0);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -666,9 +666,7 @@ __global__ void k_chol_flag(const int* __restrict__ st, double tau, int* flag) {
 constexpr int PC_T = 256;
 constexpr int PC_KC = 16;            // k-chunk per shared-memory stage
 constexpr int PC_PK = PC_KC + 4;     // [m][k] / [n][k] pitch (≡ 4 mod 16: conflict-free fragments)
-constexpr int PC_AS = 128 * PC_PK;       // elements per operand buffer ([m][k]: 128 × 20; [k][m]: 16 × 132 fits)
-static_assert(PC_AS >= PC_KC * (128 + 4), "staging buffer");
-constexpr size_t PC_SMEM = LF_SMEM > (size_t)4 * PC_AS * 8 ? LF_SMEM : (size_t)4 * PC_AS * 8;
+constexpr size_t PC_SMEM = LF_SMEM;       // the leaf's; the two workers' rings fit in it (static_assert below)
 
 // Grid-wide barrier of a cooperative launch (sense by generation; bar[0] = arrivals, bar[1] = generation)
 __device__ __forceinline__ void pc_grid_sync(unsigned int* bar, unsigned int& gen) {
@@ -691,142 +689,126 @@ __device__ __forceinline__ void pc_grid_sync(unsigned int* bar, unsigned int& ge
     __syncthreads();
 }
 
-// C(mv × nv ≤ TM × TN) = (accumulate ? C : 0) + alpha · Σ_{k0 ≤ k < k1} op(A)[i,k]·op(B)[k,j]
-//   op(A)[i,k] = TA ? A[k + i·lda] : A[i + k·lda],  op(B)[k,j] = TB ? B[j + k·ldb] : B[k + j·ldb]
-// (k is absolute: A and B point at k = 0).  256 threads, 8 warps of (TM/4) × (TN/2) (DMMA
-// 8×8×4); operands staged in k-chunks of 16 through registers into double-buffered shared
-// memory, stored along their contiguous global direction (pitches ≡ 4 mod 16).  Every read goes
-// through L2 (ld.global.cg): other CTAs of the same launch wrote the operands.
-template <int TM, int TN, bool TA, bool TB>
-__device__ void tile_mm(double* sm, const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
-                        int64_t ldb, int mv, int nv, int k0, int k1, double alpha, double* __restrict__ C,
-                        int64_t ldc, bool accumulate) {
-    constexpr int MF = TM / 32, NF = TN / 16;   // 8×8 fragments per warp along m, n
-    constexpr int PMA = TM + 4, PMB = TN + 4;   // [k][m] / [k][n] pitches
-    constexpr int LA = TM * PC_KC / PC_T, LB = TN * PC_KC / PC_T;  // staged elements per thread
-    double* As = sm;                 // [2][PC_AS]
-    double* Bs = sm + 2 * PC_AS;     // [2][PC_AS]
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 3, wn = warp >> 2;
+// Tile operands are streamed by cp.async.cg (16-byte pairs, L2 only — coherent with the other
+// CTAs' writes) through a PC_STAGES-deep shared-memory ring: three k-chunks in flight, no
+// register staging.  Needs even leading dimensions and 16-byte aligned bases.
+constexpr int PC_STAGES = 4;
+__device__ __forceinline__ void cp16(double* smem, const double* gmem, int bytes) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(bytes) : "memory");
+}
+// One 64 × 64 output sub-tile on a 4-warp group (two groups per CTA work independently, each
+// with its own cp.async ring and named barrier, as two co-resident CTAs would: one 8-warp
+// CTA stalled the whole SM's DMMA pipe at every chunk barrier — ncu put the persistent kernel's
+// DMMA pipe at 26 % with barrier stalls first).  Same operand conventions as tile_mm_async.
+constexpr int PG_STAGE = 2 * 64 * PC_PK;  // doubles per stage and group
+static_assert((size_t)2 * PC_STAGES * PG_STAGE * 8 <= PC_SMEM, "two group rings");
+template <int NW, bool TA, bool TB>
+__device__ void tile_mm_grp(double* sm, int gtid, int bar_id, const double* __restrict__ A, int64_t lda,
+                            const double* __restrict__ B, int64_t ldb, int mv, int nv, int k1, double alpha,
+                            double* __restrict__ C, int64_t ldc, bool accumulate) {
+    // NW = 4: a worker group (warp tile 32 × 32); NW = 8: the whole CTA (warp tile 16 × 32) for the
+    // critical-path items, which then finish in half the time
+    constexpr int TM = 64, TN = 64, PMA = TM + 4, PMB = TN + 4, NT = 32 * NW;
+    constexpr int WMN = NW == 4 ? 2 : 4;             // warps along m
+    constexpr int MF = TM / WMN / 8, NF = 4;          // 8 × 8 fragments per warp
+    constexpr int CP = 512 / NT;                      // 16-byte pairs per thread and operand
+    const int lane = gtid & 31, gw = gtid >> 5, wm = gw % WMN, wn = gw / WMN;
     double acc[MF][NF][2];
 #pragma unroll
     for (int a = 0; a < MF; ++a)
 #pragma unroll
         for (int b = 0; b < NF; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    const int nc = k1 > k0 ? (k1 - k0 + PC_KC - 1) / PC_KC : 0;
-    double ra[LA], rb[LB];
-    // thread → (row, k) of a chunk: along the operand's contiguous global direction
-    auto a_at = [&](int r, int& i, int& kk) {
-        if (TA) { kk = tid & (PC_KC - 1); i = (tid / PC_KC) + (PC_T / PC_KC) * r; }
-        else { i = tid % TM; kk = (tid / TM) + (PC_T / TM) * r; }
-    };
-    auto b_at = [&](int r, int& j, int& kk) {
-        if (TB) { j = tid % TN; kk = (tid / TN) + (PC_T / TN) * r; }
-        else { kk = tid & (PC_KC - 1); j = (tid / PC_KC) + (PC_T / PC_KC) * r; }
-    };
-    auto load = [&](int c) {
-        const int kb = k0 + c * PC_KC;
-#pragma unroll
-        for (int r = 0; r < LA; ++r) {
-            int i, kk;
-            a_at(r, i, kk);
-            const int gk = kb + kk;
-            ra[r] = (i < mv && gk < k1) ? __ldcg(TA ? A + gk + (int64_t)i * lda : A + i + (int64_t)gk * lda) : 0.0;
-        }
-#pragma unroll
-        for (int r = 0; r < LB; ++r) {
-            int j, kk;
-            b_at(r, j, kk);
-            const int gk = kb + kk;
-            rb[r] = (j < nv && gk < k1) ? __ldcg(TB ? B + j + (int64_t)gk * ldb : B + gk + (int64_t)j * ldb) : 0.0;
-        }
-    };
-    auto store = [&](int buf) {
-        double* as = As + buf * PC_AS;
-        double* bs = Bs + buf * PC_AS;
-#pragma unroll
-        for (int r = 0; r < LA; ++r) {
-            int i, kk;
-            a_at(r, i, kk);
-            if (TA) as[i * PC_PK + kk] = ra[r];
-            else as[kk * PMA + i] = ra[r];
-        }
-#pragma unroll
-        for (int r = 0; r < LB; ++r) {
-            int j, kk;
-            b_at(r, j, kk);
-            if (TB) bs[kk * PMB + j] = rb[r];
-            else bs[j * PC_PK + kk] = rb[r];
-        }
-    };
-    if (nc > 0) {
-        load(0);
-        store(0);
-        __syncthreads();
-        const int fr = lane >> 2, fk = lane & 3;
-        for (int c = 0; c < nc; ++c) {
-            if (c + 1 < nc) load(c + 1);
-            const double* as = As + (c & 1) * PC_AS;
-            const double* bs = Bs + (c & 1) * PC_AS;
-#pragma unroll
-            for (int k4 = 0; k4 < PC_KC; k4 += 4) {
-                double af[MF], bf[NF];
-#pragma unroll
-                for (int a = 0; a < MF; ++a) {
-                    const int i = wm * (TM / 4) + a * 8 + fr, kk = k4 + fk;
-                    af[a] = TA ? as[i * PC_PK + kk] : as[kk * PMA + i];
-                }
-#pragma unroll
-                for (int b = 0; b < NF; ++b) {
-                    const int j = wn * (TN / 2) + b * 8 + fr, kk = k4 + fk;
-                    bf[b] = TB ? bs[kk * PMB + j] : bs[j * PC_PK + kk];
-                }
-#pragma unroll
-                for (int a = 0; a < MF; ++a)
-#pragma unroll
-                    for (int b = 0; b < NF; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-            }
-            if (c + 1 < nc) store((c + 1) & 1);
-            __syncthreads();
-        }
-    }
-    // D fragment: row lane/4, columns 2·(lane%4) + {0, 1} of each 8 × 8 tile.  Accumulate: every
-    // old value is loaded before the first store (a load/store pair per element, which may alias,
-    // was serialized into one L2 round trip per element — ~40% of the tile's time)
-    if (accumulate) {
+    double oldv[MF][NF][2];
+    if (accumulate) {  // issued first: the latency hides behind the products
 #pragma unroll
         for (int a = 0; a < MF; ++a)
 #pragma unroll
             for (int b = 0; b < NF; ++b)
 #pragma unroll
                 for (int e = 0; e < 2; ++e) {
-                    const int i = wm * (TM / 4) + a * 8 + (lane >> 2), j = wn * (TN / 2) + b * 8 + 2 * (lane & 3) + e;
-                    const double old = (i < mv && j < nv) ? __ldcg(C + i + (int64_t)j * ldc) : 0.0;
-                    acc[a][b][e] = fma(alpha, acc[a][b][e], old);
+                    const int i = wm * (MF * 8) + a * 8 + (lane >> 2), j = wn * 32 + b * 8 + 2 * (lane & 3) + e;
+                    oldv[a][b][e] = (i < mv && j < nv) ? __ldcg(C + i + (int64_t)j * ldc) : 0.0;
                 }
-    } else {
-#pragma unroll
-        for (int a = 0; a < MF; ++a)
-#pragma unroll
-            for (int b = 0; b < NF; ++b)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) acc[a][b][e] *= alpha;
     }
+    const int nc = k1 > 0 ? (k1 + PC_KC - 1) / PC_KC : 0;
+    auto bar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "n"(NT) : "memory"); };
+    auto issue = [&](int c) {
+        double* as = sm + (c % PC_STAGES) * PG_STAGE;
+        double* bs = as + 64 * PC_PK;
+        const int kb = c * PC_KC;
+#pragma unroll
+        for (int r = 0; r < CP; ++r) {  // 512 16-byte pairs of A, then of B
+            const int t = gtid + r * NT;
+            if (TA) {
+                const int kk = 2 * (t & 7), i = t >> 3, gk = kb + kk;
+                const int n = (i < mv && gk < k1) ? (gk + 1 < k1 ? 16 : 8) : 0;
+                cp16(as + i * PC_PK + kk, n ? A + gk + (int64_t)i * lda : A, n);
+            } else {
+                const int i = 2 * (t & 31), kk = t >> 5, gk = kb + kk;
+                const int n = (i < mv && gk < k1) ? (i + 1 < mv ? 16 : 8) : 0;
+                cp16(as + kk * PMA + i, n ? A + i + (int64_t)gk * lda : A, n);
+            }
+            if (TB) {
+                const int j = 2 * (t & 31), kk = t >> 5, gk = kb + kk;
+                const int n = (j < nv && gk < k1) ? (j + 1 < nv ? 16 : 8) : 0;
+                cp16(bs + kk * PMB + j, n ? B + j + (int64_t)gk * ldb : B, n);
+            } else {
+                const int kk = 2 * (t & 7), j = t >> 3, gk = kb + kk;
+                const int n = (j < nv && gk < k1) ? (gk + 1 < k1 ? 16 : 8) : 0;
+                cp16(bs + j * PC_PK + kk, n ? B + gk + (int64_t)j * ldb : B, n);
+            }
+        }
+    };
+#pragma unroll
+    for (int c = 0; c < PC_STAGES - 1; ++c) {
+        if (c < nc) issue(c);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const int fr = lane >> 2, fk = lane & 3;
+    for (int c = 0; c < nc; ++c) {
+        asm volatile("cp.async.wait_group %0;" ::"n"(PC_STAGES - 2) : "memory");
+        bar();
+        if (c + PC_STAGES - 1 < nc) issue(c + PC_STAGES - 1);
+        asm volatile("cp.async.commit_group;" ::: "memory");
+        const double* as = sm + (c % PC_STAGES) * PG_STAGE;
+        const double* bs = as + 64 * PC_PK;
+#pragma unroll
+        for (int k4 = 0; k4 < PC_KC; k4 += 4) {
+            double af[MF], bf[NF];
+#pragma unroll
+            for (int a = 0; a < MF; ++a) {
+                const int i = wm * (MF * 8) + a * 8 + fr, kk = k4 + fk;
+                af[a] = TA ? as[i * PC_PK + kk] : as[kk * PMA + i];
+            }
+#pragma unroll
+            for (int b = 0; b < NF; ++b) {
+                const int j = wn * 32 + b * 8 + fr, kk = k4 + fk;
+                bf[b] = TB ? bs[kk * PMB + j] : bs[j * PC_PK + kk];
+            }
+#pragma unroll
+            for (int a = 0; a < MF; ++a)
+#pragma unroll
+                for (int b = 0; b < NF; ++b) dmma(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
     for (int a = 0; a < MF; ++a)
 #pragma unroll
         for (int b = 0; b < NF; ++b)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
-                const int i = wm * (TM / 4) + a * 8 + (lane >> 2), j = wn * (TN / 2) + b * 8 + 2 * (lane & 3) + e;
-                if (i < mv && j < nv) C[i + (int64_t)j * ldc] = acc[a][b][e];
+                const int i = wm * (MF * 8) + a * 8 + (lane >> 2), j = wn * 32 + b * 8 + 2 * (lane & 3) + e;
+                if (i < mv && j < nv)
+                    C[i + (int64_t)j * ldc] = accumulate ? fma(alpha, acc[a][b][e], oldv[a][b][e]) : alpha * acc[a][b][e];
             }
-    __syncthreads();  // the staging buffers are reused by the next item
+    bar();  // the ring is reused by the next item
 }
 
 // W (w × w working copy of G, upper blocks updated in place), R and X (zeroed, ld w),
 // T (zeroed, w × w: the accumulated products X[0:j, 0:j]·R[0:j, j] of X's block columns),
-// st = chol_status_init's status, bar = 2 zeroed words.
+// st = chol_status_init's status, bar = 2 zeroed words.  w even (16-byte cp.async pairs).
 __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict__ W, double* __restrict__ R,
                                                             double* __restrict__ X, double* __restrict__ T, int w,
                                                             int* st, unsigned int* bar) {
@@ -836,40 +818,66 @@ __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict_
     const int cta = blockIdx.x, G = gridDim.x;
     unsigned int gen = 0;
     auto bs = [&](int b) { return min(128, w - b * 128); };
+    // CTAs 1.. run two independent 4-warp groups ("workers"); CTA 0 runs only the leaf
+    const int grp = threadIdx.x >> 7, gtid = threadIdx.x & 127, bar_id = 1 + grp;
+    double* gsm = pcs + grp * PC_STAGES * PG_STAGE;
+    // The SM that shares CTA 0's TPC stays idle: the leaf's long straight-line code is fetched
+    // once per FACT, and tile products on the neighbouring SM evicted it from the shared
+    // instruction cache (the leaf's first panel ran at 1.5–3× its standalone time, profiles/r02s)
+    if (threadIdx.x == 0) {
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        if (cta == 0) atomicExch(&bar[2], smid + 1);
+        while (atomicAdd(&bar[2], 0u) == 0u) {}
+        if (cta != 0 && (smid >> 1) == ((atomicAdd(&bar[2], 0u) - 1) >> 1)) atomicExch(&bar[3], (unsigned int)cta);
+    }
+    pc_grid_sync(bar, gen);
+    const int quiet = (int)*(volatile unsigned int*)&bar[3];  // 0: none
+    const int nq = G - 1 - (quiet ? 1 : 0);                    // CTAs with items
+    const int crank = cta - 1 - (quiet && cta > quiet ? 1 : 0);
+    const bool busy = cta > 0 && cta != quiet;
+    const int worker = 2 * crank + grp, nwork = 2 * nq;
     // BCUR_LEAF_TIMING=1: CTA 0 sums its clocks per phase (FACT, the wait for the other CTAs'
     // phase-1 work, phases 2 and 3) and prints them at the end (diagnostics)
     const bool timing = g_leaf_timing && cta == 0 && threadIdx.x == 0;
     long long tf = 0, tw = 0, t2 = 0, t3 = 0, c0 = 0, c1 = 0;
+    // W_{i,k} sub-tile (a, b) −= R_{s,i}[:, a]ᵀ · R_{s,k}[:, b]
+    auto update = [&](int s, int i, int k, int a, int b, bool whole) {
+        const int mv = min(64, bs(i) - a * 64), nv = min(64, bs(k) - b * 64);
+        if (mv <= 0 || nv <= 0 || (i == k && a > b)) return;
+        if (whole) tile_mm_grp<8, true, false>(pcs, threadIdx.x, 1, R + s * 128 + (int64_t)(i * 128 + a * 64) * ld, ld,
+                                               R + s * 128 + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, bs(s), -1.0,
+                                               W + (i * 128 + a * 64) + (int64_t)(k * 128 + b * 64) * ld, ld, true);
+        else tile_mm_grp<4, true, false>(gsm, gtid, bar_id, R + s * 128 + (int64_t)(i * 128 + a * 64) * ld, ld,
+                                 R + s * 128 + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, bs(s), -1.0,
+                                 W + (i * 128 + a * 64) + (int64_t)(k * 128 + b * 64) * ld, ld, true);
+    };
     for (int j = 0; j < nb; ++j) {
         const int J = j * 128;
         if (timing) c0 = clock64();
-        // ---- phase 1: FACT(j) on CTA 0 | the others: step j−1's trailing update of block rows
-        //      ≥ j+1 (W_ik −= R_{j−1,i}ᵀ R_{j−1,k}, whole 128 × 128 blocks) and X's block column
-        //      j−1 into the inverse accumulators (T[0:J, k] += X[0:J, j−1]·R[j−1, k], k ≥ j)
+        // ---- phase 1: FACT(j) on CTA 0 | the workers: step j−1's trailing update of block rows
+        //      ≥ j+1 and X's block column j−1 into the inverse accumulators
+        //      (T[0:J, k] += X[0:J, j−1]·R[j−1, k], k ≥ j), as 64 × 64 sub-tiles
         if (cta == 0) {
             chol_leaf_call(pcs, W + J + (int64_t)J * ld, bs(j), ld, R + J + (int64_t)J * ld, ld, X + J + (int64_t)J * ld,
-                          ld, st, reinterpret_cast<double*>(st) + 1, J, LEAF_ZEROED);
+                           ld, st, reinterpret_cast<double*>(st) + 1, J, LEAF_ZEROED | (g_leaf_timing == 2 ? 0 : LEAF_QUIET));
         } else if (j >= 1) {
             const int s = j - 1, S = s * 128, n = nb - j - 1;
-            const int nupd = n * (n + 1) / 2;      // blocks (i, k), j+1 ≤ i ≤ k
-            const int ninv = j * (nb - j);         // blocks (r, k), r < j, k ≥ j
-            // items: 128 × 64 halves of those blocks (h = column half)
-            for (int t = cta - 1; t < 2 * (nupd + ninv); t += G - 1) {
-                const int h = t & 1, tb = t >> 1;
-                if (tb < nupd) {
-                    int i = j + 1, u = tb;          // row i holds nb − i blocks
+            const int nupd = 4 * (n * (n + 1) / 2);  // blocks (i, k), j+1 ≤ i ≤ k
+            const int ninv = 4 * (j * (nb - j));     // blocks (r, k), r < j, k ≥ j
+            for (int t = worker; busy && t < nupd + ninv; t += nwork) {
+                const int a = (t >> 1) & 1, b = t & 1, tb = t >> 2;
+                if (t < nupd) {
+                    int i = j + 1, u = tb;           // row i holds nb − i blocks
                     while (u >= nb - i) { u -= nb - i; ++i; }
-                    const int k = i + u, nv = min(64, bs(k) - h * 64);
-                    if (nv > 0)
-                        tile_mm<128, 64, true, false>(pcs, R + S + (int64_t)(i * 128) * ld, ld,
-                                                      R + S + (int64_t)(k * 128 + h * 64) * ld, ld, bs(i), nv, 0, bs(s),
-                                                      -1.0, W + i * 128 + (int64_t)(k * 128 + h * 64) * ld, ld, true);
+                    update(s, i, i + u, a, b, false);
                 } else {
-                    const int u = tb - nupd, r = u / (nb - j), k = j + u % (nb - j), nv = min(64, bs(k) - h * 64);
-                    if (nv > 0)
-                        tile_mm<128, 64, false, false>(pcs, X + r * 128 + (int64_t)S * ld, ld,
-                                                       R + S + (int64_t)(k * 128 + h * 64) * ld, ld, bs(r), nv, 0, bs(s),
-                                                       1.0, T + r * 128 + (int64_t)(k * 128 + h * 64) * ld, ld, true);
+                    const int u = tb - nupd / 4, r = u / (nb - j), k = j + u % (nb - j);
+                    const int mv = min(64, bs(r) - a * 64), nv = min(64, bs(k) - b * 64);
+                    if (mv > 0 && nv > 0)
+                        tile_mm_grp<4, false, false>(gsm, gtid, bar_id, X + r * 128 + a * 64 + (int64_t)S * ld, ld,
+                                                  R + S + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, bs(s), 1.0,
+                                                  T + r * 128 + a * 64 + (int64_t)(k * 128 + b * 64) * ld, ld, true);
                 }
             }
         }
@@ -877,47 +885,36 @@ __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict_
         pc_grid_sync(bar, gen);
         if (timing) { c1 = clock64(); tw += c1 - c0; c0 = c1; }
         if (*(volatile int*)st != 0) return;  // a failed pivot (info) stops every CTA
-        // ---- phase 2: PANEL(j): R_jk = X_jjᵀ W_jk, k > j (64 × 64 sub-tiles: the critical path)
-        {
+        // ---- phase 2: PANEL(j): R_jk = X_jjᵀ W_jk, k > j (whole-CTA items: the critical path)
+        if (cta > 0) {
             const int n2 = (nb - 1 - j) * 4;
-            for (int t = cta - 1; cta > 0 && t < n2; t += G - 1) {
+            for (int t = crank; busy && t < n2; t += nq) {
                 const int k = j + 1 + t / 4, a = (t >> 1) & 1, b = t & 1;
                 const int mv = min(64, bs(j) - a * 64), nv = min(64, bs(k) - b * 64);
                 if (mv <= 0 || nv <= 0) continue;
                 // (X_jjᵀ)[a·64 + i, kk] = X[J + kk, J + a·64 + i], non-zero for kk ≤ a·64 + i
-                tile_mm<64, 64, true, false>(pcs, X + J + (int64_t)(J + a * 64) * ld, ld,
-                                             W + J + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, 0,
-                                             min(bs(j), a * 64 + 64), 1.0,
-                                             R + J + a * 64 + (int64_t)(k * 128 + b * 64) * ld, ld, false);
+                tile_mm_grp<8, true, false>(pcs, threadIdx.x, 1, X + J + (int64_t)(J + a * 64) * ld, ld,
+                                         W + J + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, min(bs(j), a * 64 + 64),
+                                         1.0, R + J + a * 64 + (int64_t)(k * 128 + b * 64) * ld, ld, false);
             }
         }
         pc_grid_sync(bar, gen);
         if (timing) { c1 = clock64(); t2 += c1 - c0; c0 = c1; }
-        // ---- phase 3: lookahead — block row j+1 gets step j's update (64 × 64 sub-tiles; the
-        //      diagonal block's upper halves); X[0:J, j] = −T[0:J, j]·X_jj
-        {
-            const int nupd = j + 1 < nb ? 3 + 4 * (nb - 2 - j) : 0;
+        // ---- phase 3: lookahead — block row j+1 gets step j's update; X[0:J, j] = −T[0:J, j]·X_jj
+        if (cta > 0) {
+            const int nupd = j + 1 < nb ? 4 * (nb - 1 - j) : 0;
             const int nx = (J / 64) * 2;
-            const int i = j + 1;
-            for (int t = cta - 1; cta > 0 && t < nupd + nx; t += G - 1) {
+            for (int t = crank; busy && t < nupd + nx; t += nq) {
                 if (t < nupd) {
-                    int k, a, b;
-                    if (t < 3) { k = i; a = t == 2 ? 1 : 0; b = t == 0 ? 0 : 1; }
-                    else { const int u = t - 3; k = i + 1 + u / 4; a = (u >> 1) & 1; b = u & 1; }
-                    const int mv = min(64, bs(i) - a * 64), nv = min(64, bs(k) - b * 64);
-                    if (mv <= 0 || nv <= 0) continue;
-                    tile_mm<64, 64, true, false>(pcs, R + J + (int64_t)(i * 128 + a * 64) * ld, ld,
-                                                 R + J + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, 0, bs(j), -1.0,
-                                                 W + (i * 128 + a * 64) + (int64_t)(k * 128 + b * 64) * ld, ld, true);
+                    update(j, j + 1, j + 1 + t / 4, (t >> 1) & 1, t & 1, true);
                 } else {
                     const int u = t - nupd, r = u >> 1, b = u & 1;
                     const int nv = min(64, bs(j) - b * 64);
                     if (nv <= 0) continue;
                     // X_jj upper: row kk of column b·64 + jj is non-zero for kk ≤ b·64 + jj
-                    tile_mm<64, 64, false, false>(pcs, T + r * 64 + (int64_t)J * ld, ld,
-                                                  X + J + (int64_t)(J + b * 64) * ld, ld, 64, nv, 0,
-                                                  min(bs(j), b * 64 + 64), -1.0,
-                                                  X + r * 64 + (int64_t)(J + b * 64) * ld, ld, false);
+                    tile_mm_grp<8, false, false>(pcs, threadIdx.x, 1, T + r * 64 + (int64_t)J * ld, ld,
+                                              X + J + (int64_t)(J + b * 64) * ld, ld, 64, nv, min(bs(j), b * 64 + 64),
+                                              -1.0, X + r * 64 + (int64_t)(J + b * 64) * ld, ld, false);
                 }
             }
         }
@@ -1017,7 +1014,7 @@ void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st) 
 }
 
 void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st) {
-    if (w < 1 || w > (1 << 20)) fail(BCUR_E_INVALID_ARGUMENT, "chol_persistent: bad width");
+    if (w < 2 || w % 2 != 0 || w > (1 << 20)) fail(BCUR_E_INVALID_ARGUMENT, "chol_persistent: needs an even width");
     ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
     static int grid = 0;
     if (!grid) {
@@ -1025,8 +1022,8 @@ void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r,
         int per_sm = 0;
         CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_chol_persistent, PC_T, PC_SMEM));
         grid = std::max(1, per_sm) * c->sm_count;
-        const char* t = getenv("BCUR_LEAF_TIMING");
-        const int on = (t && t[0] == '1') ? 1 : 0;
+        const char* t = getenv("BCUR_LEAF_TIMING");  // 1: phase clocks; 2: also each leaf's own
+        const int on = t ? atoi(t) : 0;
         if (on) CUDA_CHECK(cudaMemcpyToSymbol(g_leaf_timing, &on, sizeof on));
     }
     if (grid < 2) fail(BCUR_E_CUDA, "chol_persistent: needs two co-resident CTAs");

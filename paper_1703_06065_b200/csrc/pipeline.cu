@@ -207,8 +207,10 @@ static void chol_enqueue(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         chol_inv_leaf(c, G, w, ldg, R, w, X, w, st, reinterpret_cast<double*>(st) + 1, 0, want_r ? 0 : 1);
         return;
     }
-    static const bool rec = getenv("BCUR_CHOL_REC") != nullptr;  // experiments: the launch-per-product recursion
-    if (!rec) {
+    // the persistent kernel streams its operands in 16-byte pairs: even widths (odd ones, and
+    // BCUR_CHOL_REC=1 for experiments, take the launch-per-product recursion below)
+    static const bool rec = getenv("BCUR_CHOL_REC") != nullptr;
+    if (!rec && w % 2 == 0) {
         chol_persistent(c, G, w, ldg, R, X, st);
         return;
     }
