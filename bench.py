@@ -222,19 +222,42 @@ def bench_b200(args, cfg, rank, world, local_rank):
     prof = {t: dict(v, ms=v["ms"] / prof_steps, scopes=v["scopes"] / prof_steps, flops=v["flops"] / prof_steps,
                     bytes=v["bytes"] / prof_steps) for t, v in (prof or {}).items()}
 
-    # e2e: the public API with host buffers — pinned A shard uploaded every step
+    # e2e: the public API with host buffers — every step's input (the pinned A shard) is uploaded
+    # inside the timed region and its result read back.  Inputs are double-buffered on the
+    # device: step k+1's upload (bcur_dmat_upload_async, the context's copy stream) runs while
+    # step k decomposes, and step k+1 waits for its copy on the device — the stream a serving
+    # loop would run.  --e2e-serial: upload, then decompose, one step at a time.
     host = torch.empty((n_local, m), dtype=torch.float32 if dt == np.float32 else torch.float64, pin_memory=True)
     import ctypes
     B._check(B.L.lib.bcur_dmat_download(ctx.handle, dm.handle, ctypes.c_void_p(host.data_ptr()), m))
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
     hptr = ctypes.c_void_p(host.data_ptr())
+    bufs = [dm]
+    # a second input buffer must fit beside A and its 3×FP16 copy (c5's 68.7 GB shard does not)
+    a_bytes = m * n_local * (4 if dt == np.float32 else 8)
+    serial = args.e2e_serial or 3 * a_bytes > 0.85 * torch.cuda.get_device_properties(local_rank).total_memory
+    if not serial:
+        bufs.append(B.DeviceMatrix.empty(dt, m, n_local, ctx=ctx))
+        if world > 1:
+            bufs[1].set_shard(col0, n)
 
-    def e2e_step():
-        B._check(B.L.lib.bcur_dmat_upload(ctx.handle, dm.handle, hptr, m))
-        return run_step(B, cfg, dm, part, rpart, ctx)
+    def e2e_run(steps):
+        if serial:
+            res = None
+            for _ in range(steps):
+                B._check(B.L.lib.bcur_dmat_upload(ctx.handle, dm.handle, hptr, m))
+                res = run_step(B, cfg, dm, part, rpart, ctx)
+            return res
+        bufs[0].upload_async(host.data_ptr(), m)
+        res = None
+        for k in range(steps):
+            if k + 1 < steps:
+                bufs[(k + 1) % 2].upload_async(host.data_ptr(), m)
+            res = run_step(B, cfg, bufs[k % 2], part, rpart, ctx)
+        return res
 
-    e2e_step()
-    ms_e2e, _, _, _ = timed(e2e_step, e2e_steps)
+    e2e_run(2)
+    ms_e2e, _, _, _ = timed(lambda: e2e_run(e2e_steps), 1)
 
     value = args.steps / (ms / 1e3)
     e2e_value = e2e_steps / (ms_e2e / 1e3)
@@ -253,7 +276,10 @@ def bench_b200(args, cfg, rank, world, local_rank):
             "parallelism": f"column-block shards x{world}" if world > 1 else "single GPU",
             "rel_err": rel_err, "selected_blocks": blocks[:16],
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d * world,
-                    "d2h_bytes_per_step": d2h_bytes(cfg, G) * world, "ms_per_step": ms_e2e / e2e_steps},
+                    "d2h_bytes_per_step": d2h_bytes(cfg, G) * world, "ms_per_step": ms_e2e / e2e_steps,
+                    "steps": e2e_steps,
+                    "pipeline": "serial upload + decomposition" if serial else
+                    "double-buffered: step k+1's upload overlaps step k's decomposition"},
             "gpu_launches": launches, "roofline": roof, "kernels_per_step": prof,
             "clocks": clk.summary(), "generate_s": gen_s,
         }
@@ -495,6 +521,7 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-serial", action="store_true", help="e2e without overlapping the next upload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--residual", choices=["auto", "explicit", "pythagoras"], default="auto",
                     help="residual path (diagnostics: the explicit tcgen05 residual on the headline shape)")

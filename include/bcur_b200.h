@@ -95,6 +95,11 @@ bcur_status bcur_ctx_set_comm(bcur_ctx ctx, const bcur_comm* comm); /* NULL → 
 bcur_status bcur_dmat_create(bcur_ctx ctx, int dtype, int64_t m, int64_t n, bcur_dmat* out);
 /* Copies m×n column-major host data (leading dimension ld_host ≥ m). */
 bcur_status bcur_dmat_upload(bcur_ctx ctx, bcur_dmat a, const void* host, int64_t ld_host);
+/* The same copy enqueued on the context's upload stream, returning at once: the next call that
+ * uses `a` waits for it on the device (so an upload of the next input overlaps the current
+ * decomposition).  The copy first waits for the uses of `a` already enqueued.  `host` must stay
+ * valid and unmodified until then (pinned memory makes the copy asynchronous). */
+bcur_status bcur_dmat_upload_async(bcur_ctx ctx, bcur_dmat a, const void* host, int64_t ld_host);
 bcur_status bcur_dmat_download(bcur_ctx ctx, bcur_dmat a, void* host, int64_t ld_host);
 /* Wraps caller-owned device memory (no copy, not freed by destroy). */
 bcur_status bcur_dmat_wrap(bcur_ctx ctx, int dtype, int64_t m, int64_t n, void* dev_ptr, int64_t ld,

@@ -80,6 +80,7 @@ SIGNATURES = {
     "bcur_ctx_set_comm": (C.c_int, [vp, C.POINTER(CommC)]),
     "bcur_dmat_create": (C.c_int, [vp, C.c_int, i64, i64, C.POINTER(vp)]),
     "bcur_dmat_upload": (C.c_int, [vp, vp, vp, i64]),
+    "bcur_dmat_upload_async": (C.c_int, [vp, vp, vp, i64]),
     "bcur_bcur_header": (C.c_int, [C.c_char_p, C.POINTER(i64), C.POINTER(i64)]),
     "bcur_dmat_load_bcur": (C.c_int, [vp, C.c_char_p, C.c_int, i64, i64, C.POINTER(vp)]),
     "bcur_dmat_save_bcur": (C.c_int, [vp, vp, C.c_char_p]),

@@ -226,6 +226,19 @@ class DeviceMatrix:
         return dm
 
     @staticmethod
+    def empty(dtype, m: int, n: int, ctx: Optional[Context] = None) -> "DeviceMatrix":
+        ctx = ctx or default_context()
+        h = C.c_void_p()
+        _check(L.lib.bcur_dmat_create(ctx.handle, _dtype_code(np.dtype(dtype)), m, n, C.byref(h)))
+        return DeviceMatrix(h, ctx)
+
+    def upload_async(self, host_ptr: int, ld_host: int) -> None:
+        """bcur_dmat_upload_async: the copy runs on the context's upload stream; the next call
+        that uses this matrix waits for it on the device.  host_ptr (column-major, pinned for an
+        asynchronous copy) must stay valid until then."""
+        _check(L.lib.bcur_dmat_upload_async(self.ctx.handle, self.handle, C.c_void_p(host_ptr), ld_host))
+
+    @staticmethod
     def load_bcur(path, dtype=np.float64, col0: int = 0, ncols: int = -1,
                   ctx: Optional[Context] = None) -> "DeviceMatrix":
         """io.cpp:105-137 load_matrix_binary, streamed into HBM (column-major, fp32 or fp64);

@@ -36,6 +36,10 @@ Ctx* C(bcur_ctx c) {
 }
 DMat* M(bcur_dmat a) {
     if (!a) fail(BCUR_E_INVALID_ARGUMENT, "null matrix");
+    if (a->pending) {  // an asynchronous upload into it: order the compute stream after the copy
+        CUDA_CHECK(cudaStreamWaitEvent(a->ctx->stream, a->ready, 0));
+        a->pending = false;
+    }
     return a;
 }
 
@@ -188,6 +192,10 @@ bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
         cudaStreamDestroy(ctx->side3);
         for (auto e : ctx->side_ev) cudaEventDestroy(e);
     }
+    if (ctx->up) {
+        cudaStreamSynchronize(ctx->up);
+        cudaStreamDestroy(ctx->up);
+    }
     delete ctx;
     API_END
 }
@@ -304,6 +312,25 @@ bcur_status bcur_dmat_upload(bcur_ctx ctx, bcur_dmat a, const void* host, int64_
         CUDA_CHECK(cudaMemcpy2DAsync(d->ptr, d->ld * es, host, ld_host * es, d->m * es, d->n, cudaMemcpyHostToDevice,
                                      c->stream));
     c->sync();
+    API_END
+}
+
+bcur_status bcur_dmat_upload_async(bcur_ctx ctx, bcur_dmat a, const void* host, int64_t ld_host) {
+    API_BEGIN
+    Ctx* c = C(ctx);
+    DMat* d = M(a);
+    if (ld_host < d->m) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_upload_async: ld_host < m");
+    if (!c->up) CUDA_CHECK(cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking));
+    if (!d->ready) CUDA_CHECK(cudaEventCreateWithFlags(&d->ready, cudaEventDisableTiming));
+    // the copy overwrites `a`: it waits for every use of `a` already enqueued on the compute stream
+    CUDA_CHECK(cudaEventRecord(d->ready, c->stream));
+    CUDA_CHECK(cudaStreamWaitEvent(c->up, d->ready, 0));
+    const size_t es = dtype_size(d->dtype);
+    if (d->m * d->n > 0)
+        CUDA_CHECK(cudaMemcpy2DAsync(d->ptr, d->ld * es, host, ld_host * es, d->m * es, d->n, cudaMemcpyHostToDevice,
+                                     c->up));
+    CUDA_CHECK(cudaEventRecord(d->ready, c->up));
+    d->pending = true;
     API_END
 }
 
@@ -504,6 +531,10 @@ bcur_status bcur_dmat_set_shard(bcur_dmat a, int64_t col0, int64_t n_global) {
 bcur_status bcur_dmat_destroy(bcur_dmat a) {
     API_BEGIN
     if (!a) return BCUR_OK;
+    if (a->ready) {
+        cudaEventSynchronize(a->ready);
+        cudaEventDestroy(a->ready);
+    }
     if (a->owned && a->ptr) {
         cudaSetDevice(a->ctx->device);
         cudaStreamSynchronize(a->ctx->stream);

@@ -158,6 +158,7 @@ struct Ctx {
     // The serial chain itself runs on a high-priority stream (hp) so that the block scheduler
     // places its small kernels ahead of the side streams' wide DSYRK/DGEMM CTAs.
     cudaStream_t side = nullptr, side2 = nullptr, side3 = nullptr, hp = nullptr;
+    cudaStream_t up = nullptr;  // host → device uploads (bcur_dmat_upload_async), created on first use
     cudaEvent_t side_ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaStream_t side_stream() {
         if (!side) {
@@ -260,6 +261,10 @@ struct DMat {
     void* ptr = nullptr;
     bool owned = false;
     int64_t col0 = 0, n_global = 0;  // column shard
+    // bcur_dmat_upload_async: the copy's completion on the context's upload stream; every API
+    // use of the matrix first makes the compute stream wait for it (capi.cu M())
+    cudaEvent_t ready = nullptr;
+    bool pending = false;
     size_t bytes() const { return (size_t)ld * (size_t)n * dtype_size(dtype); }
 };
 

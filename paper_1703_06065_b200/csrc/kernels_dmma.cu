@@ -319,7 +319,10 @@ void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, 
 // k) then hits 16 distinct 8-byte bank pairs per half-warp — with an odd pitch it was 4-way
 // conflicted and the leaf's DMMA phases ran at the shared-memory wavefront rate
 constexpr int LF_T = 256, LF_MAX = 128, LF_LD = LF_MAX + 4, LF_TP = 36;
-enum { LEAF_NO_R = 1, LEAF_ZEROED = 2, LEAF_QUIET = 4 };  // chol_inv_leaf flags (ops.h); QUIET: no timing print
+// chol_inv_leaf flags (ops.h).  QUIET: no timing print.  SYM: g holds the full symmetric block
+// (both triangles) with 16-byte aligned columns and w == 128 — it is then copied column by column
+// (M's lower triangle is g's) with cp.async instead of the transposing load
+enum { LEAF_NO_R = 1, LEAF_ZEROED = 2, LEAF_QUIET = 4, LEAF_SYM = 8 };
 __device__ int g_leaf_timing = 0;  // BCUR_LEAF_TIMING=1: thread 0 prints the phase clocks (diagnostics)
 #define LF_CLK(i) do { if (timing && threadIdx.x == 0) clk[i] = clock64(); } while (0)
 
@@ -362,7 +365,16 @@ __device__ __forceinline__ void chol_leaf_dev(double* smlf, const double* __rest
         i = (blk % nib) * 8 + (ln >> 2);
         k = (blk / nib) * 4 + (ln & 3);
     };
-    for (int q0 = 0; q0 * LF_T < total; q0 += 16) {
+    const bool sym_load = (flags & LEAF_SYM) && w == LF_MAX && (ldg % 2) == 0 && ((uintptr_t)g % 16) == 0;
+    if (sym_load) {  // 128 columns × 64 16-byte pairs, through L2 (other CTAs wrote g)
+        for (int e = tid; e < LF_MAX * (LF_MAX / 2); e += LF_T) {
+            const int c = e >> 6, r = 2 * (e & 63);
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(M + r + c * LF_LD);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g + r + (int64_t)c * ldg) : "memory");
+        }
+        asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+    }
+    for (int q0 = 0; !sym_load && q0 * LF_T < total; q0 += 16) {
         double v[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {  // addresses clamped, no branches
@@ -811,7 +823,7 @@ __device__ void tile_mm_grp(double* sm, int gtid, int bar_id, const double* __re
 // st = chol_status_init's status, bar = 2 zeroed words.  w even (16-byte cp.async pairs).
 __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict__ W, double* __restrict__ R,
                                                             double* __restrict__ X, double* __restrict__ T, int w,
-                                                            int* st, unsigned int* bar) {
+                                                            int* st, unsigned int* bar, int want_r) {
     extern __shared__ double pcs[];
     const int64_t ld = w;
     const int nb = (w + 127) / 128;
@@ -844,7 +856,7 @@ __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict_
     // W_{i,k} sub-tile (a, b) −= R_{s,i}[:, a]ᵀ · R_{s,k}[:, b]
     auto update = [&](int s, int i, int k, int a, int b, bool whole) {
         const int mv = min(64, bs(i) - a * 64), nv = min(64, bs(k) - b * 64);
-        if (mv <= 0 || nv <= 0 || (i == k && a > b)) return;
+        if (mv <= 0 || nv <= 0) return;  // diagonal blocks whole: they stay symmetric (LEAF_SYM loads)
         if (whole) tile_mm_grp<8, true, false>(pcs, threadIdx.x, 1, R + s * 128 + (int64_t)(i * 128 + a * 64) * ld, ld,
                                                R + s * 128 + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, bs(s), -1.0,
                                                W + (i * 128 + a * 64) + (int64_t)(k * 128 + b * 64) * ld, ld, true);
@@ -852,6 +864,18 @@ __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict_
                                  R + s * 128 + (int64_t)(k * 128 + b * 64) * ld, ld, mv, nv, bs(s), -1.0,
                                  W + (i * 128 + a * 64) + (int64_t)(k * 128 + b * 64) * ld, ld, true);
     };
+    // the diagonal blocks made symmetric (lower ← upper: the Gram kernels may write only the upper
+    // triangle); every later update keeps them so, and the leaf copies them column by column
+    for (int b = cta; b < nb; b += G) {
+        const int wb = bs(b);
+        double* D = W + b * 128 + (int64_t)(b * 128) * ld;
+        for (int e = threadIdx.x; e < wb * wb; e += PC_T) {
+            const int i = e % wb, k = e / wb;
+            if (i > k) D[i + (int64_t)k * ld] = D[k + (int64_t)i * ld];
+        }
+    }
+    pc_grid_sync(bar, gen);
+    const int leaf_flags = LEAF_ZEROED | LEAF_SYM | (want_r ? 0 : LEAF_NO_R) | (g_leaf_timing == 2 ? 0 : LEAF_QUIET);
     for (int j = 0; j < nb; ++j) {
         const int J = j * 128;
         if (timing) c0 = clock64();
@@ -860,7 +884,7 @@ __global__ void __launch_bounds__(PC_T, 1) k_chol_persistent(double* __restrict_
         //      (T[0:J, k] += X[0:J, j−1]·R[j−1, k], k ≥ j), as 64 × 64 sub-tiles
         if (cta == 0) {
             chol_leaf_call(pcs, W + J + (int64_t)J * ld, bs(j), ld, R + J + (int64_t)J * ld, ld, X + J + (int64_t)J * ld,
-                           ld, st, reinterpret_cast<double*>(st) + 1, J, LEAF_ZEROED | (g_leaf_timing == 2 ? 0 : LEAF_QUIET));
+                           ld, st, reinterpret_cast<double*>(st) + 1, J, leaf_flags);
         } else if (j >= 1) {
             const int s = j - 1, S = s * 128, n = nb - j - 1;
             const int nupd = 4 * (n * (n + 1) / 2);  // blocks (i, k), j+1 ≤ i ≤ k
@@ -1013,7 +1037,7 @@ void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st) 
     LAUNCH_CHECK(c);
 }
 
-void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st) {
+void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st, bool want_r) {
     if (w < 2 || w % 2 != 0 || w > (1 << 20)) fail(BCUR_E_INVALID_ARGUMENT, "chol_persistent: needs an even width");
     ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
     static int grid = 0;
@@ -1037,8 +1061,8 @@ void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r,
     double* wp = W.as<double>();
     double* tp = T.as<double>();
     unsigned int* bp = bar.as<unsigned int>();
-    int wi = (int)w;
-    void* args[] = {&wp, &r, &x, &tp, &wi, &st, &bp};
+    int wi = (int)w, wr = want_r ? 1 : 0;
+    void* args[] = {&wp, &r, &x, &tp, &wi, &st, &bp, &wr};
     CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)k_chol_persistent, dim3(grid), dim3(PC_T), args, PC_SMEM,
                                            c->stream));
     LAUNCH_CHECK(c);

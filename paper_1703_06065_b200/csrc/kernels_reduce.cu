@@ -258,6 +258,15 @@ __global__ void k_sum_vector(const double* __restrict__ x, int64_t n, double* __
     if (threadIdx.x == 0) out[0] = s;
 }
 
+// Σ x[i]² over a contiguous vector: a fixed grid of block partials (deterministic order)
+__global__ void k_sumsq_part(const double* __restrict__ x, int64_t n, double* __restrict__ part) {
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s = fma(x[i], x[i], s);
+    s = block_sum(s);
+    if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
 // max |G − I| over a w×w matrix: warp per column (lanes over rows, coalesced), block max,
 // then an integer atomicMax on the bit pattern (non-negative doubles order like their bits;
 // a NaN's pattern exceeds +inf, so NaN propagates).  *out must be zeroed first.
@@ -427,6 +436,14 @@ void max_row_sumsq(Ctx* c, const double* u, int64_t m, int64_t ld, int64_t k, do
 void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out) {
     k_sum_vector<<<1, 1024, 0, c->stream>>>(x, n, d_out);
     LAUNCH_CHECK(c);
+}
+
+void sumsq_vector(Ctx* c, const double* x, int64_t n, double* d_out) {
+    constexpr int P = 128;
+    DevBuf part(c, P * sizeof(double));
+    k_sumsq_part<<<P, 256, 0, c->stream>>>(x, n, part.as<double>());
+    LAUNCH_CHECK(c);
+    sum_vector(c, part.as<double>(), P, d_out);
 }
 
 }  // namespace ops

@@ -1154,6 +1154,9 @@ __device__ __forceinline__ void x3p_tile(const PSched& sc, int t, int* mp, int* 
         *mp = t;
     } else {
         pair_tile(t, sc.m_pairs, sc.n_tiles, mp, nt);
+        // triangular X: N tile j carries j + 1 diagonal blocks of K — the widest group first
+        // (with no wave barrier the short tiles of the last group fill the tail)
+        if (sc.tri_x) *nt = sc.n_tiles - 1 - *nt;
     }
     *nk = sc.tri_x ? min(sc.k_tiles, ((*nt + 1) * 2 * BN + sc.bke - 1) / sc.bke) : sc.k_tiles;
 }
@@ -1731,7 +1734,9 @@ void launch_umma2_h3(Ctx* c, PSched sc, const CUtensorMap& ta, const CUtensorMap
     const int pairs = std::min(sc.total, c->sm_count / 2);
     DevBuf ctr;
     sc.wave_ctr = nullptr;
-    if (pairs < sc.total && !g_wave_barrier_off) {  // ≤ 1 CTA per SM: all co-resident
+    // the wave barrier keeps a wave's pairs in lockstep along K (L2 sharing); with a triangular X
+    // the tiles of a wave differ in length and every wave would wait for its longest tile
+    if (pairs < sc.total && !g_wave_barrier_off && !sc.tri_x) {  // ≤ 1 CTA per SM: all co-resident
         ctr = DevBuf(c, 64);
         CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
         sc.wave_ctr = ctr.as<unsigned int>();

@@ -33,6 +33,8 @@ void block_spectral(Ctx* c, const double* v, int64_t ld, int64_t k, const int64_
 void max_row_sumsq(Ctx* c, const double* u, int64_t m, int64_t ld, int64_t k, double* d_out);
 // ordered sum of x[0..n) → d_out[0]
 void sum_vector(Ctx* c, const double* x, int64_t n, double* d_out);
+// Σ x[i]² over x[0..n) → d_out[0] (fixed-order, deterministic)
+void sumsq_vector(Ctx* c, const double* x, int64_t n, double* d_out);
 
 // ---- dense products (kernels_gemm.cu), fp64 accumulation ------------------
 // C(M×N fp64) = alpha·op(A)·op(B) + beta·C.  Structure hints (exploited by the tcgen05 path
@@ -81,7 +83,8 @@ void chol_status_init(Ctx* c, const double* g, int64_t w, int64_t ldg, int* st);
 // w > 128: R (upper, ld w) with G = RᵀR (G's upper triangle read, ldg) and X = R⁻¹ (upper, ld w)
 // in one cooperative persistent launch (blocked right-looking, fp64 DMMA); st as chol_status_init
 // (initialized by the caller), info = failed pivot + 1
-void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st);
+// want_r = false: R's diagonal blocks are not written (its off-diagonal blocks always are)
+void chol_persistent(Ctx* c, const double* g, int64_t w, int64_t ldg, double* r, double* x, int* st, bool want_r = true);
 // *flag = 1 unless the factorization with status st passed min diag(R) > tau·sqrt(max diag(G))
 void chol_flag(Ctx* c, const int* st, double tau, int* flag);
 // w ≤ 128, one CTA: R (upper, lower zeroed) with G = RᵀR from G's upper triangle, and X = R⁻¹

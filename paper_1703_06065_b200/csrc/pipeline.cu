@@ -211,7 +211,7 @@ static void chol_enqueue(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     // BCUR_CHOL_REC=1 for experiments, take the launch-per-product recursion below)
     static const bool rec = getenv("BCUR_CHOL_REC") != nullptr;
     if (!rec && w % 2 == 0) {
-        chol_persistent(c, G, w, ldg, R, X, st);
+        chol_persistent(c, G, w, ldg, R, X, st, want_r);
         return;
     }
     ProfScope prof(c, "chol_inv", 2.0 * w * w * w / 3.0, 8.0 * 4 * w * w);
@@ -901,11 +901,8 @@ static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub) {
     }
     copy_f64(c, blk[0], ke, r, W.ld, blk[2], W.ld);
     axpy_neg(c, blk[1], blk[2], ke * r);
-    const int64_t off[2] = {0, r};  // one block of r columns: its Σ of squares
-    DevBuf doff(c, sizeof off);
-    h2d(c, doff.as<int64_t>(), off, 2);
-    block_sumsq(c, blk[2], BCUR_F64, ke, W.ld, doff.as<int64_t>(), 1, tot.p());
-    block_sumsq(c, blk[0], BCUR_F64, ke, W.ld, doff.as<int64_t>(), 1, tot.p() + 1);
+    sumsq_vector(c, blk[2], ke * r, tot.p());  // the blocks are contiguous (ld = ke)
+    sumsq_vector(c, blk[0], ke * r, tot.p() + 1);
     double h[2] = {0.0, 0.0};
     d2h(c, h, tot.p(), 2);
     return h[0] - h[1];

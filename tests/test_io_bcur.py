@@ -108,3 +108,27 @@ def test_device_loader_errors(tmp_path, case):
         p = tmp_path / "absent.bcur"
     with pytest.raises(exc):
         B.DeviceMatrix.load_bcur(p, np.float64, 25 if case == "range" else 0, 10 if case == "range" else -1)
+
+
+@pytest.mark.gpu
+def test_upload_async_orders_the_next_use():
+    """bcur_dmat_upload_async: the copy runs on the upload stream; the next call that uses the
+    matrix (here the norms pass, then a download) sees the new data; a second upload into the
+    same matrix waits for the uses already enqueued."""
+    import torch
+
+    from paper_1703_06065_b200 import bcur as B
+
+    gen = np.random.default_rng(7)
+    m, n = 4096, 1536
+    a1 = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    a2 = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32) * 3)
+    h1 = torch.from_numpy(a1.T.copy()).pin_memory()  # (n, m) row-major = column-major m × n
+    h2 = torch.from_numpy(a2.T.copy()).pin_memory()
+    d = B.DeviceMatrix.empty(np.float32, m, n)
+    d.upload_async(h1.data_ptr(), m)
+    assert abs(B.frobenius_norm(d) - np.linalg.norm(a1.astype(np.float64))) <= 1e-6 * np.linalg.norm(a1)
+    d.upload_async(h2.data_ptr(), m)
+    d.upload_async(h1.data_ptr(), m)
+    d.upload_async(h2.data_ptr(), m)
+    np.testing.assert_array_equal(d.to_host(), a2)
