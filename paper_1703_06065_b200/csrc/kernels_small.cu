@@ -827,7 +827,9 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
         DevBuf log(c, (size_t)rounds_max * half * sizeof(JRot)), meta(c, (size_t)(w + 16) * sizeof(int));
         int* nrounds = meta.as<int>();
         int* order = nrounds + 16;
-        // threads: one per 2×2 block of a round (fewer warps per barrier for small w)
+        // threads: one per 2×2 block of a round (fewer warps per barrier for small w).  A full-square
+        // variant whose warps read contiguous runs (the circle method's r ± i pairs) measured slower:
+        // 1616 vs 1066 update cycles per round at ℓ = 60 (twice the blocks, profiles/r02y)
         const int64_t nblk = half * (half + 1) / 2;
         const int nt = (int)std::min<int64_t>(JP_T, std::max<int64_t>(128, (nblk + 127) / 128 * 128));
         k_jacobi_packed<<<1, nt, packed, c->stream>>>(g, (int)w, ldg, log.as<JRot>(), nrounds, lam, order,
@@ -845,7 +847,7 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
             int hr = 0;
             CUDA_CHECK(cudaMemcpyAsync(&hr, nrounds, sizeof hr, cudaMemcpyDeviceToHost, c->stream));
             CUDA_CHECK(cudaStreamSynchronize(c->stream));
-            fprintf(stderr, "sym_eig w=%d rounds=%d sweeps=%.1f threads=%d\n", (int)w, hr, hr / (double)(2 * half - 1), nt);
+            fprintf(stderr, "sym_eig w=%d rounds=%d sweeps=%.1f\n", (int)w, hr, hr / (double)(2 * half - 1));
         }
         LAUNCH_CHECK(c);
         return;

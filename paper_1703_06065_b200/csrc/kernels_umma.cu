@@ -39,6 +39,7 @@ bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
 bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (experiments)
 bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
 bool g_no_h3pair = false;         // BCUR_UMMA_NO_H3_PAIR=1: single-CTA 3×FP16 products (experiments)
+bool g_no_fastacc = false;        // BCUR_UMMA_NO_FAST_ACC=1: GEMM_FAST_ACC products on the split accumulators (experiments)
 int g_pf = -1;                    // BCUR_UMMA_PF: A-tile L2 prefetch distance in stages (experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
@@ -1746,6 +1747,318 @@ void launch_umma2_h3(Ctx* c, PSched sc, const CUtensorMap& ta, const CUtensorMap
     LAUNCH_CHECK(c);
 }
 
+// ---------------- CTA-pair 3×FP16 product, one accumulator (M = 256 × N = 192 per pair)
+// k_umma2_h3 with the three MMAs of a k-step (a_hi·x_hi, a_hi·x_lo, a_lo·x_hi) summed into ONE
+// fp32 TMEM accumulator, which leaves room for N = 192 double-buffered (k_umma2_h3 keeps hi
+// and cross terms apart: 2 × 128 columns per buffer).  Per SM and k-step: 21 KB of operand
+// reads + 14 KB of TMA writes for 2·1.18 M flop (122 B/clk at the MMA rate, against 156 for
+// k_umma2_h3's N = 128: the 128 B/clk shared-memory bound).  (N = 256 would need 16 drain warps
+// of 64 fp32 accumulators each in a 96-register budget: they spilled in the drain loop.)  Accuracy: each 8-k-step chunk carries
+// the tensor core's round-toward-zero bias over 24 accumulations (~7e-7 relative, systematic)
+// and the chunks sum in plain fp32 — fp32-grade, not the ~2⁻²² of the split accumulators, so
+// callers opt in (GEMM_FAST_ACC) where the product's error is corrected downstream or far
+// inside its bar: c4's Q_CᵀA (U's 1e-4), the first CholQR pass's C·R⁻¹ and the second pass's
+// small correction.
+constexpr int HM_NTP = 3;                                      // 64-column tiles per pair tile (N = 192)
+constexpr int HM_NDRAIN = 4 * HM_NTP;                          // 4 lane quarters × 3 64-column slices
+constexpr int HM_THREADS = 32 * (4 + HM_NDRAIN);               // producer, MMA, 2 idle, drains
+constexpr int HM_XR = HM_NTP * BN / 2;                         // B rows per CTA (96)
+constexpr uint32_t HM_XT = HM_XR * 128;                        // bytes of one B part per stage (12 KB)
+constexpr uint32_t HM_STAGE = 2 * A_TILE + 2 * HM_XT;          // a_hi, a_lo, x_hi part, x_lo part
+constexpr int HM_STAGES = (int)((232448u - 1280u) / HM_STAGE);
+constexpr uint32_t HM_SMEM = HM_STAGES * HM_STAGE + 1024 + 256;
+constexpr uint32_t HM_R0 = (65536u / HM_THREADS) / 8 * 8;      // 96
+constexpr uint32_t HM_REG_LOW = 56;
+constexpr uint32_t HM_REG_DRAIN_FIT = HM_R0 + ((HM_THREADS - 32 * HM_NDRAIN) * (HM_R0 - HM_REG_LOW) / (32 * HM_NDRAIN)) / 8 * 8;
+
+// pair tile t → (row pair mp, 192-column tile nt, k stages); tri_x: widest N group first
+__device__ __forceinline__ void hm_tile(const PSched& sc, int t, int* mp, int* nt, int* nk) {
+    pair_tile(t, sc.m_pairs, sc.n_tiles, mp, nt);
+    if (sc.tri_x) *nt = sc.n_tiles - 1 - *nt;
+    *nk = sc.tri_x ? min(sc.k_tiles, ((*nt + 1) * HM_NTP * BN + sc.bke - 1) / sc.bke) : sc.k_tiles;
+}
+
+template <bool A_MN, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(HM_THREADS, 1)
+k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmXh,
+            const __grid_constant__ CUtensorMap tmXl, int M, int N, const PSched sc, void* __restrict__ out_v,
+            int64_t ldo, double alpha, double beta, const int* __restrict__ rexp, const int* __restrict__ cexp,
+            uint16_t* __restrict__ q16, const uint16_t* __restrict__ aux) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + HM_STAGES * HM_STAGE);
+    uint64_t* full = bars;                     // [STAGES] leader: both CTAs' bytes
+    uint64_t* empty = full + HM_STAGES;        // [STAGES] each CTA: multicast MMA commit
+    uint64_t* tfull = empty + HM_STAGES;       // [2]      each CTA: multicast MMA commit
+    uint64_t* tempty = tfull + 2;              // [2]      leader: both CTAs' drain warps
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = warp_index(), lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    constexpr int NTP = HM_NTP;                // 64-column tiles per pair tile
+    constexpr int BKH = bke<true>();
+    constexpr uint32_t IDESC = (1u << 4) | ((A_MN ? 1u : 0u) << 15) | ((uint32_t)((NTP * BN) >> 3) << 17) |
+                               ((uint32_t)(2 * BM >> 4) << 24);   // f16 × f16 → f32, M = 256, N = 192
+    constexpr uint32_t BUF = 256;              // TMEM buffer stride (one N = 192 accumulator each)
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < HM_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 2 * HM_NDRAIN);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXh) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&tmXl) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    auto a_hi = [&](int s) { return smem + s * HM_STAGE; };
+    auto x_hi = [&](int s) { return smem + s * HM_STAGE + 2 * A_TILE; };
+
+    if (warp >= 4) {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(HM_REG_DRAIN_FIT));
+        // ------------------------------------------- drain (both CTAs, own TMEM rows)
+        const int q = warp & 3, slice = (warp - 4) >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        const uint32_t tempty0 = map_to_rank(smem_u32(&tempty[0]), 0);
+        int gc = 0;
+        for (int t = pair; t < sc.total; t += npairs) {
+            int mp, nt, nk;
+            hm_tile(sc, t, &mp, &nt, &nk);
+            const int nchunks = (nk + CH - 1) / CH;
+            const int row = (2 * mp + (int)rank) * BM + q * 32 + lane;
+            float acc[BN];
+#pragma unroll
+            for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
+            for (int c = 0; c < nchunks; ++c) {
+                const int g = gc + c, b = g & 1;
+                mbar_wait(&tfull[b], (uint32_t)(g / 2) & 1u);
+                tc_fence_after();
+                const uint32_t t0 = tmem + lane_off + (uint32_t)(b * BUF + slice * BN);
+#pragma unroll
+                for (int j0 = 0; j0 < BN; j0 += 8) {
+                    uint32_t h[8];
+                    TMEM_LD8(t0 + j0, h);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) acc[j0 + j] += __uint_as_float(h[j]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)  // default (cta-scope) form, as k_umma2_rowsq
+                    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(tempty0 + b * 8) : "memory");
+            }
+            gc += nchunks;
+            const int col0 = nt * NTP * BN + slice * BN;
+            if (row < M) {
+                const int ncol = min(BN, N - col0);
+                const int re = rexp ? rexp[row] : 0;
+                if (EPI == EPI_STORE) {
+                    double* dst = reinterpret_cast<double*>(out_v) + row;
+                    constexpr int EB = 8;  // β ≠ 0: old values loaded 8 at a time before the stores
+#pragma unroll
+                    for (int j0 = 0; j0 < BN; j0 += EB) {
+                        double old[EB];
+#pragma unroll
+                        for (int jj = 0; jj < EB; ++jj)
+                            old[jj] = (beta != 0.0 && j0 + jj < ncol) ? dst[(int64_t)(col0 + j0 + jj) * ldo] : 0.0;
+#pragma unroll
+                        for (int jj = 0; jj < EB; ++jj) {
+                            const int j = j0 + jj;
+                            if (j >= ncol) continue;
+                            const double v = (double)acc[j] * exp2_int(-(re + (cexp ? cexp[col0 + j] : 0)));
+                            dst[(int64_t)(col0 + j) * ldo] = beta == 0.0 ? alpha * v : fma(beta, old[jj], alpha * v);
+                        }
+                    }
+                } else {
+                    const int64_t r_il = (int64_t)(row >> 6) * 128 + (row & 63);
+#pragma unroll
+                    for (int j = 0; j < BN; ++j) {
+                        if (j >= ncol) continue;
+                        const int col = col0 + j;
+                        double v = (double)acc[j] * (alpha * exp2_int(-(re + (cexp ? cexp[col] : 0))));
+                        if (EPI == EPI_SPLIT) {
+                            uint16_t* o16 = reinterpret_cast<uint16_t*>(out_v);
+                            const double sv = v * (double)(1 << BASIS_E);
+                            const __half h = __double2half(sv);
+                            const __half l = __double2half(sv - (double)__half2float(h));
+                            o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
+                            o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
+                        } else {
+                            if (aux) {
+                                const uint16_t hb = aux[(int64_t)col * 2 * M + r_il], lb = aux[(int64_t)col * 2 * M + r_il + 64];
+                                v += ((double)__half2float(*reinterpret_cast<const __half*>(&hb)) +
+                                      (double)__half2float(*reinterpret_cast<const __half*>(&lb))) *
+                                     (1.0 / (double)(1 << BASIS_E));
+                            }
+                            reinterpret_cast<float*>(out_v)[row + (int64_t)col * ldo] = (float)v;
+                            const double sv = v * (double)(1 << BASIS_E);  // interleaved hi/lo, as k_umma
+                            const __half h = __double2half(sv);
+                            const __half l = __double2half(sv - (double)__half2float(h));
+                            q16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
+                            q16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
+                        }
+                    }
+                }
+            }
+        }
+    } else {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(HM_REG_LOW));
+        if (warp == 0) {
+            // ---------------------------------------------------------------- producer
+            if (lane == 0) {
+                const uint32_t full0 = map_to_rank(smem_u32(&full[0]), 0);  // leader's barriers
+                int gi = 0;
+                for (int t = pair, w = 0; t < sc.total; t += npairs, ++w) {
+                    if (sc.wave_ctr && w > 0) {  // wave barrier (see Sched)
+                        unsigned int target = 0;
+                        for (int v = 0; v < w; ++v)
+                            target += 2u * (unsigned int)max(0, min(npairs, sc.total - v * npairs));
+                        unsigned int val;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(val) : "l"(sc.wave_ctr) : "memory");
+                        } while (val < target);
+                    }
+                    int mp, nt, nk;
+                    hm_tile(sc, t, &mp, &nt, &nk);
+                    const int m_tile = 2 * mp + (int)rank, xc = nt * NTP * BN + (int)rank * HM_XR;
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % HM_STAGES;
+                        mbar_wait(&empty[s], ((uint32_t)(gi / HM_STAGES) & 1u) ^ 1u);
+                        if (rank == 0) mbar_expect_tx(&full[s], 2 * HM_STAGE);
+                        const uint32_t fb = full0 + s * 8;
+                        const int k0 = i * BKH;
+                        const uint32_t sa = smem_u32(a_hi(s)), sx = smem_u32(x_hi(s));
+                        auto load4 = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3) {
+                            asm volatile(
+                                "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(tm), "r"(fb), "r"(c0), "r"(c1),
+                                "r"(c2), "r"(c3) : "memory");
+                        };
+#pragma unroll
+                        for (int hl = 0; hl < 2; ++hl) {  // A: the interleaved hi/lo copy (4-D map)
+                            if (A_MN) {
+                                load4(sa + hl * A_TILE, &tmA, 0, hl, m_tile * 2, k0);
+                                load4(sa + hl * A_TILE + A_TILE / 2, &tmA, 0, hl, m_tile * 2 + 1, k0);
+                            } else {
+                                load4(sa + hl * A_TILE, &tmA, 0, hl, k0 / 64, m_tile * BM);
+                            }
+                        }
+                        // X: this CTA's 96 N rows, hi then lo, as three 32-row boxes each (the maps'
+                        // boxes are 32 rows for this kernel)
+#pragma unroll
+                        for (int hl = 0; hl < 2; ++hl)
+#pragma unroll
+                            for (int h3 = 0; h3 < 3; ++h3) {
+                                const uint32_t dst = sx + hl * HM_XT + h3 * (HM_XT / 3);
+                                if (sc.x_il)
+                                    load4(dst, &tmXh, 0, hl, k0 / 64, xc + h3 * 32);
+                                else
+                                    asm volatile(
+                                        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                                        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst), "l"(hl ? &tmXl : &tmXh), "r"(fb),
+                                        "r"(k0), "r"(xc + h3 * 32) : "memory");
+                            }
+                    }
+                    if (sc.wave_ctr) atomicAdd(sc.wave_ctr, 1u);
+                }
+            }
+        } else if (warp == 1) {
+            // ------------------------------------------------- MMA issuer (leader only)
+            if (rank == 0) {
+                int gi = 0, gc = 0;
+                for (int t = pair; t < sc.total; t += npairs) {
+                    int mp, nt, nk;
+                    hm_tile(sc, t, &mp, &nt, &nk);
+                    for (int i = 0; i < nk; ++i, ++gi) {
+                        const int s = gi % HM_STAGES;
+                        const int c = gc + i / CH, b = c & 1;
+                        const bool first = (i % CH) == 0;
+                        if (first) mbar_wait(&tempty[b], ((uint32_t)(c / 2) & 1u) ^ 1u);
+                        mbar_wait(&full[s], (uint32_t)(gi / HM_STAGES) & 1u);
+                        tc_fence_after();
+                        const uint32_t ah = smem_u32(a_hi(s)), al = ah + A_TILE;
+                        const uint32_t xh = smem_u32(x_hi(s)), xl = xh + HM_XT;
+                        const uint32_t d = tmem + (uint32_t)(b * BUF);
+#pragma unroll
+                        for (int k8 = 0; k8 < BK / 8; ++k8) {
+                            uint64_t dah, dal;
+                            if (A_MN) {
+                                dah = sdesc(ah + k8 * 2048, 8192, 1024, 2);
+                                dal = sdesc(al + k8 * 2048, 8192, 1024, 2);
+                            } else {
+                                dah = sdesc(ah + k8 * 32, 16, 1024, 2);
+                                dal = sdesc(al + k8 * 32, 16, 1024, 2);
+                            }
+                            const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
+                            const uint64_t dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
+                            const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n\t.reg .pred e, p, one;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                "setp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 one, %6, %6;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %5, p;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, one;\n\t"
+                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %4, %2, %5, one;\n\t}" ::"r"(d),
+                                "l"(dah), "l"(dxh), "l"(dxl), "l"(dal), "r"(IDESC), "r"(acc));
+                        }
+                        asm volatile(
+                            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                            "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                            " [%0], %1;\n\t}" ::"r"(smem_u32(&empty[s])), "h"((uint16_t)3) : "memory");
+                        if ((i % CH) == CH - 1 || i == nk - 1)
+                            asm volatile(
+                                "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+                                " [%0], %1;\n\t}" ::"r"(smem_u32(&tfull[b])), "h"((uint16_t)3) : "memory");
+                        __syncwarp();
+                    }
+                    gc += (nk + CH - 1) / CH;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    }
+}
+
+template <bool A_MN, int EPI>
+void launch_umma2_h3m(Ctx* c, PSched sc, const CUtensorMap& ta, const CUtensorMap& th, const CUtensorMap& tl, int M,
+                      int N, void* out, int64_t ldo, double alpha, double beta, const int* rexp, const int* cexp,
+                      uint16_t* q16, const uint16_t* aux) {
+    auto kern = k_umma2_h3m<A_MN, EPI>;
+    static bool attr = false;
+    if (!attr) {
+        CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, HM_SMEM));
+        attr = true;
+    }
+    if (sc.total <= 0) return;
+    const int pairs = std::min(sc.total, c->sm_count / 2);
+    DevBuf ctr;
+    sc.wave_ctr = nullptr;
+    if (pairs < sc.total && !g_wave_barrier_off && !sc.tri_x) {
+        ctr = DevBuf(c, 64);
+        CUDA_CHECK(cudaMemsetAsync(ctr.ptr, 0, 4, c->stream));
+        sc.wave_ctr = ctr.as<unsigned int>();
+    }
+    kern<<<2 * pairs, HM_THREADS, HM_SMEM, c->stream>>>(ta, th, tl, M, N, sc, out, ldo, alpha, beta, rexp, cexp, q16,
+                                                         aux);
+    LAUNCH_CHECK(c);
+}
+
 // ------------------------------------------------ fp16 operands (row-Σ² passes)
 // max |x| over a K × N matrix into *mx (float bits; non-negative floats order as integers)
 template <class T>
@@ -1883,6 +2196,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         g_no_x3pair = !(nx && nx[0] == '1');
         const char* nh = getenv("BCUR_UMMA_NO_H3_PAIR");
         g_no_h3pair = nh && nh[0] == '1';
+        const char* nf = getenv("BCUR_UMMA_NO_FAST_ACC");
+        g_no_fastacc = nf && nf[0] == '1';
         const char* pf = getenv("BCUR_UMMA_PF");
         if (pf) g_pf = atoi(pf);
         const char* d = getenv("BCUR_UMMA_DEBUG");
@@ -2273,6 +2588,43 @@ static void umma_h3_epi(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, in
     sc.bke = BKH;  // fp16 k-tiles: the diagonal limit of a triangular X in 64-row units (was 2× too far)
     const int* rexp = a_mn ? nullptr : ea;
     const int* cexp = X.exps;
+    if ((flags & GEMM_FAST_ACC) && NT == 2 && !sym && splits == 1 && M >= 2 * BM && !g_no_h3pair && !g_no_fastacc) {
+        // one accumulator per pair tile of 256 × 192 (k_umma2_h3m); its X maps load 32-row boxes
+        PSched ps = make_psched(mt, (int)((N + HM_NTP * BN - 1) / (HM_NTP * BN)), k_tiles, false, tri);
+        ps.bke = BKH;
+        ps.x_il = X.lo ? 0 : 1;
+        if (X.lo) {
+            const int64_t ldx = X.ld > 0 ? X.ld : K;
+            const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)ldx * 2};
+            const uint32_t bX[2] = {BKH, 32};
+            th = make_map(X.hi, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+            tl = make_map(X.lo, 2, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+        } else {
+            const bool one = X.part >= 0;
+            const uint64_t dX[4] = {64, one ? 1u : 2u, (uint64_t)(K / 64), (uint64_t)N}, sX[3] = {128, 256, (uint64_t)K * 4};
+            const uint32_t bX[4] = {64, 1, 1, 32};
+            th = make_map(one ? X.hi + 64 * X.part : X.hi, 4, dX, sX, bX, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_DATA_TYPE_FLOAT16,
+                          one ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B : CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+            tl = th;
+        }
+        if (a_mn) {
+            if (epi == EPI_SPLIT)
+                launch_umma2_h3m<true, EPI_SPLIT>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, 0.0, rexp, cexp,
+                                                  nullptr, nullptr);
+            else if (epi == EPI_BASIS)
+                launch_umma2_h3m<true, EPI_BASIS>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, 0.0, rexp, cexp,
+                                                  q16, aux);
+            else
+                launch_umma2_h3m<true, EPI_STORE>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, beta, rexp,
+                                                  cexp, nullptr, nullptr);
+        } else {
+            if (epi != EPI_STORE) fail(BCUR_E_INVALID_ARGUMENT, "umma_h3: split/basis output needs A·X");
+            launch_umma2_h3m<false, EPI_STORE>(c, ps, ta, th, tl, (int)M, (int)N, out_v, ldo, alpha, beta, rexp, cexp,
+                                               nullptr, nullptr);
+        }
+        return;
+    }
     if (NT == 2 && splits == 1 && M >= 2 * BM && !g_no_h3pair) {
         // tensor-bound shapes: CTA pairs (k_umma2_h3)
         PSched ps = make_psched(mt, nt, k_tiles, sym, tri);

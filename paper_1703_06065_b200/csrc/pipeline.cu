@@ -516,8 +516,10 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     // no fp64 Q1 and no split pass
     DevBuf qil(c, (size_t)rows * cc * 4), qe(c, (size_t)cc * sizeof(int));
     fill_basis_exps(c, qe.as<int>(), cc);
+    // (one-accumulator products: a ~1e-6 error in Q1 is a column scaling or a random rotation
+    // whose first-order effect on the captured mass vanishes, and the second pass measures Q1)
     umma_h3_to_split(c, cil.as<uint16_t>(), ce.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0,
-                     qil.as<uint16_t>(), GEMM_B_UPPER);
+                     qil.as<uint16_t>(), GEMM_B_UPPER | GEMM_FAST_ACC);
     cil = DevBuf();
     if (keep_rinv) {
         R1i = Mat64(c, cc, cc);
@@ -545,7 +547,8 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     // the second-pass product and the basis output in one pass: Q = Q1·X2 (+ Q1 read back from
     // its split when X2 = −F), written as the fp32 basis and its fp16·2^14 copy
     umma_h3_basis(c, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0,
-                  near ? qil.as<uint16_t>() : nullptr, B->buf.as<float>(), B->x16.as<uint16_t>(), GEMM_B_UPPER);
+                  near ? qil.as<uint16_t>() : nullptr, B->buf.as<float>(), B->x16.as<uint16_t>(),
+                  GEMM_B_UPPER | (near ? GEMM_FAST_ACC : 0));  // near: a ~1e-4-sized correction
     B->rank = cc;
     if (keep_rinv) {
         B->rinv1 = std::move(R1i);
@@ -616,10 +619,10 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
 // A·X (trans = false) or AᵀX of the range finder: 3×FP16 from the norms pass's split of A
 // when present, else the fp32 A path (3×TF32 on the tensor cores / fp64)
 static void a_product(Ctx* c, const DMat* a, const RoundedA* ra, bool trans, int64_t N, const void* X, int dtx,
-                      int64_t ldx, double* out, int64_t ldo) {
+                      int64_t ldx, double* out, int64_t ldo, int flags = 0) {
     if (ra && ra->has_lo()) {
         umma_h3(c, !trans, ra->il.as<uint16_t>(), ra->exps.as<int>(), a->m, a->n, X, dtx, N, ldx, 1.0, 0.0, out,
-                ldo);
+                ldo, flags);
         return;
     }
     if (trans)
@@ -1520,7 +1523,8 @@ void block_cur(Ctx* c, const DMat* a, const int64_t* coff, int64_t Gc, const int
     // M = Q_Cᵀ A Q_R:  Xᵀ = A_sᵀ Q_C (n_local × rc), Mᵀ = Σ_s Q_R,sᵀ Xᵀ (rr × rc)
     Mat64 Xt(c, nl, std::max<int64_t>(rc, 1)), Mt(c, std::max<int64_t>(rr, 1), std::max<int64_t>(rc, 1));
     Mat64 M(c, std::max<int64_t>(rc, 1), std::max<int64_t>(rr, 1));
-    a_product(c, a, &ra, true, rc, QC.buf.ptr, QC.dt, QC.rows, Xt.p(), Xt.ld);
+    // one-accumulator product (~1e-6 relative, against U's 1e-4 and the error's ~1e-7 here)
+    a_product(c, a, &ra, true, rc, QC.buf.ptr, QC.dt, QC.rows, Xt.p(), Xt.ld, GEMM_FAST_ACC);
     gemm(c, OP_T, OP_N, rr, rc, nl, 1.0, QR.buf.ptr, QR.dt, QR.rows, Xt.p(), BCUR_F64, Xt.ld, 0.0, Mt.p(), Mt.ld);
     allreduce(c, Mt.p(), rr * rc);
     transpose(c, Mt.p(), BCUR_F64, rr, rc, Mt.ld, M.p(), BCUR_F64, M.ld);

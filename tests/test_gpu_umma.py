@@ -162,3 +162,23 @@ def test_h3_gram_and_triangular(B, m, n):
     r = np.triu(gen.standard_normal((n, n)))
     got = B.structured_product(a, r, x_upper=True, h3=True)
     assert rel_fro(got, a64 @ r) < 2e-6
+
+
+@pytest.mark.parametrize("m,n,N,upper", [(8192, 512, 1100, False), (8192, 640, 1100, True)])
+def test_h3_fast_acc(B, m, n, N, upper):
+    """GEMM_FAST_ACC (k_umma2_h3m): the three fp16 MMAs of a k-step into one fp32 accumulator —
+    fp32-grade (the tensor core's round-toward-zero over 24 accumulations per chunk, ~1e-6)
+    instead of the split accumulators' ~2⁻²².  Shapes large enough for the CTA-pair path."""
+    gen = np.random.default_rng(m + n + N)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    x = gen.standard_normal((n, N))
+    if upper:
+        x = np.triu(x)
+    x = np.asfortranarray(x)
+    ref = a.astype(np.float64) @ x
+    fast = B.structured_product(a, x, x_upper=upper, h3=True, fast_acc=True)
+    exact = B.structured_product(a, x, x_upper=upper, h3=True)
+    assert rel_fro(exact, ref) < 2e-6
+    assert rel_fro(fast, ref) < 5e-6
+    # the bias is systematic (toward zero) but bounded by the accumulation count per chunk
+    assert abs(np.sum(fast * ref) / np.sum(ref * ref) - 1.0) < 3e-6
