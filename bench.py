@@ -294,7 +294,9 @@ def ncu_traffic(workload):
     """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of each
     kernel class from the latest committed `ncu --set full` capture, if any."""
     import glob
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json")), reverse=True):
+    # newest evidence run first: r02z < r02aa (longer names are later runs)
+    runs = glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_traffic.json"))
+    for path in sorted(runs, key=lambda p: (len(os.path.dirname(p)), p), reverse=True):
         with open(path) as f:
             d = json.load(f)
         return {t: v for t, v in d.get(workload, {}).items()}, os.path.relpath(path, ROOT)

@@ -226,14 +226,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
     return d;
 }
 
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-        "}" ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
-}
 // Whole-warp issue: every lane computes the same (uniform) descriptors and elect.sync
 // picks the issuing lane inside the asm — a lane-0-only branch makes the compiler wrap
 // each MMA in an ELECT/R2UR.BROADCAST waterfall (~56 cycles per instruction).
@@ -268,11 +260,6 @@ __device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t"
         "}" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-
 #define TMEM_LD8(taddr, r)                                                                                         \
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                            \
                  : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])     \
@@ -366,7 +353,6 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
     };
 
     using CF = Cfg<NT, X3, H>;
-    constexpr int NACC = CF::NACC;
     constexpr uint32_t BUFCOLS = CF::BUFCOLS;
     constexpr int STAGES = CF::STAGES;
     constexpr uint32_t STAGE = CF::STAGE, TMEM_COLS = CF::TMEM_COLS;
@@ -523,8 +509,23 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                 const int64_t r_il = (int64_t)(row >> 6) * 128 + (row & 63);
                 uint16_t* o16 = reinterpret_cast<uint16_t*>(EPI == EPI_SPLIT ? out : partial);
                 float* o32 = reinterpret_cast<float*>(out);
+                // BASIS: the aux values of 8 columns are loaded together (one L2 round trip per
+                // column made the epilogue, not the MMAs, bound the correction product)
+                float ax8[8];
 #pragma unroll
                 for (int j = 0; j < DC; ++j) {
+                    if (EPI == EPI_BASIS && (j & 7) == 0) {
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            ax8[jj] = 0.0f;
+                            if (aux && j + jj < ncol) {
+                                const int64_t o = (int64_t)(col0 + j + jj) * 2 * M + r_il;
+                                const uint16_t hb = aux[o], lb = aux[o + 64];
+                                ax8[jj] = __half2float(*reinterpret_cast<const __half*>(&hb)) +
+                                          __half2float(*reinterpret_cast<const __half*>(&lb));  // exact in fp32
+                            }
+                        }
+                    }
                     if (j >= ncol) continue;
                     const int col = col0 + j;
                     double v = (double)acc[j] + (double)cmp[X3 ? j : 0];
@@ -536,12 +537,7 @@ k_umma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensor
                         o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
                         o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
                     } else {
-                        if (aux) {
-                            const uint16_t hb = aux[(int64_t)col * 2 * M + r_il], lb = aux[(int64_t)col * 2 * M + r_il + 64];
-                            v += ((double)__half2float(*reinterpret_cast<const __half*>(&hb)) +
-                                  (double)__half2float(*reinterpret_cast<const __half*>(&lb))) *
-                                 (1.0 / (double)(1 << BASIS_E));
-                        }
+                        v += (double)ax8[j & 7] * (1.0 / (double)(1 << BASIS_E));
                         o32[row + (int64_t)col * ldo] = (float)v;
                         // the fp16 copy as the interleaved split of v·2^14: hi = the row-Σ² pass's
                         // operand, lo = its rounding error (the sketch correction's Δ)
@@ -1572,8 +1568,21 @@ k_umma2_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
                     }
                 } else {
                     const int64_t r_il = (int64_t)(row >> 6) * 128 + (row & 63);
+                    float ax8[8];  // BASIS: 8 columns' aux values per round trip (see k_umma)
 #pragma unroll
                     for (int j = 0; j < BN; ++j) {
+                        if (EPI == EPI_BASIS && (j & 7) == 0) {
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) {
+                                ax8[jj] = 0.0f;
+                                if (aux && j + jj < ncol) {
+                                    const int64_t o = (int64_t)(col0 + j + jj) * 2 * M + r_il;
+                                    const uint16_t hb = aux[o], lb = aux[o + 64];
+                                    ax8[jj] = __half2float(*reinterpret_cast<const __half*>(&hb)) +
+                                              __half2float(*reinterpret_cast<const __half*>(&lb));
+                                }
+                            }
+                        }
                         if (j >= ncol) continue;
                         const int col = col0 + j;
                         double v = ((double)acc[j] + (double)cmp[j]) * (alpha * exp2_int(-(re + (cexp ? cexp[col] : 0))));
@@ -1585,12 +1594,7 @@ k_umma2_h3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
                             o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
                             o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
                         } else {
-                            if (aux) {
-                                const uint16_t hb = aux[(int64_t)col * 2 * M + r_il], lb = aux[(int64_t)col * 2 * M + r_il + 64];
-                                v += ((double)__half2float(*reinterpret_cast<const __half*>(&hb)) +
-                                      (double)__half2float(*reinterpret_cast<const __half*>(&lb))) *
-                                     (1.0 / (double)(1 << BASIS_E));
-                            }
+                            v += (double)ax8[j & 7] * (1.0 / (double)(1 << BASIS_E));
                             reinterpret_cast<float*>(out_v)[row + (int64_t)col * ldo] = (float)v;
                             const double sv = v * (double)(1 << BASIS_E);  // interleaved hi/lo, as k_umma
                             const __half h = __double2half(sv);
@@ -1882,8 +1886,21 @@ k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                 } else {
                     const int64_t r_il = (int64_t)(row >> 6) * 128 + (row & 63);
+                    float ax8[8];  // BASIS: 8 columns' aux values per round trip (see k_umma)
 #pragma unroll
                     for (int j = 0; j < BN; ++j) {
+                        if (EPI == EPI_BASIS && (j & 7) == 0) {
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) {
+                                ax8[jj] = 0.0f;
+                                if (aux && j + jj < ncol) {
+                                    const int64_t o = (int64_t)(col0 + j + jj) * 2 * M + r_il;
+                                    const uint16_t hb = aux[o], lb = aux[o + 64];
+                                    ax8[jj] = __half2float(*reinterpret_cast<const __half*>(&hb)) +
+                                              __half2float(*reinterpret_cast<const __half*>(&lb));
+                                }
+                            }
+                        }
                         if (j >= ncol) continue;
                         const int col = col0 + j;
                         double v = (double)acc[j] * (alpha * exp2_int(-(re + (cexp ? cexp[col] : 0))));
@@ -1895,12 +1912,7 @@ k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
                             o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
                         } else {
-                            if (aux) {
-                                const uint16_t hb = aux[(int64_t)col * 2 * M + r_il], lb = aux[(int64_t)col * 2 * M + r_il + 64];
-                                v += ((double)__half2float(*reinterpret_cast<const __half*>(&hb)) +
-                                      (double)__half2float(*reinterpret_cast<const __half*>(&lb))) *
-                                     (1.0 / (double)(1 << BASIS_E));
-                            }
+                            v += (double)ax8[j & 7] * (1.0 / (double)(1 << BASIS_E));
                             reinterpret_cast<float*>(out_v)[row + (int64_t)col * ldo] = (float)v;
                             const double sv = v * (double)(1 << BASIS_E);  // interleaved hi/lo, as k_umma
                             const __half h = __double2half(sv);
