@@ -49,6 +49,32 @@ __global__ void k_scale_columns(double* x, int64_t m, int64_t n, int64_t ld, con
     x[i + j * ld] *= s[j];
 }
 
+// out[k] = Σ over the row ranges [r0, r1) (pairs) of v(i, k)², one block per column k
+__global__ void k_colsumsq_ranges(const double* __restrict__ v, int64_t ld, const int64_t* __restrict__ ranges, int nr,
+                                  double* __restrict__ out) {
+    const double* col = v + (int64_t)blockIdx.x * ld;
+    double s = 0.0;
+    for (int r = 0; r < nr; ++r)
+        for (int64_t i = ranges[2 * r] + threadIdx.x; i < ranges[2 * r + 1]; i += blockDim.x) s = fma(col[i], col[i], s);
+    __shared__ double red[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        out[blockIdx.x] = t;
+    }
+}
+
+// s[k] = σ[k]·sqrt(max(0, 1 − lev[k]))
+__global__ void k_sigma_weights(const double* __restrict__ sigma, const double* __restrict__ lev, int n,
+                                double* __restrict__ s) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) s[k] = sigma[k] * sqrt(fmax(0.0, 1.0 - lev[k]));
+}
+
 __global__ void k_scale_rows(double* x, int64_t m, int64_t n, int64_t ld, const double* __restrict__ s) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= m * n) return;
@@ -155,6 +181,18 @@ void axpy_neg(Ctx* c, const double* x, double* y, int64_t n) {
 void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale) {
     if (m * n == 0) return;
     k_scale_columns<<<nblk(m * n), 256, 0, c->stream>>>(x, m, n, ld, d_scale);
+    LAUNCH_CHECK(c);
+}
+
+void colsumsq_ranges(Ctx* c, const double* v, int64_t ld, int64_t k, const int64_t* d_ranges, int nr, double* d_out) {
+    if (k <= 0) return;
+    k_colsumsq_ranges<<<(unsigned)k, 256, 0, c->stream>>>(v, ld, d_ranges, nr, d_out);
+    LAUNCH_CHECK(c);
+}
+
+void sigma_weights(Ctx* c, const double* d_sigma, const double* d_lev, int64_t n, double* d_scale) {
+    if (n <= 0) return;
+    k_sigma_weights<<<(unsigned)((n + 255) / 256), 256, 0, c->stream>>>(d_sigma, d_lev, (int)n, d_scale);
     LAUNCH_CHECK(c);
 }
 

@@ -920,7 +920,11 @@ __device__ __forceinline__ void pair_tile(int t, int m_pairs, int n_tiles, int* 
 template <bool H>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2_THREADS, 1)
 k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int M, int m_pairs,
-              int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr, int x_il) {
+              int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr, int x_il,
+              const int* __restrict__ tiles, int ntiles) {
+    // tiles (nullable): the 128-column M tiles to compute, pairs taken in list order (the others'
+    // rows of `partial` are left untouched); a missing second tile reads as TMA zeros past M
+    auto m_of = [&](int mp, uint32_t r) { const int i = 2 * mp + (int)r; return tiles ? (i < ntiles ? tiles[i] : (M + BM - 1) / BM) : i; };
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t* bars = (uint64_t*)(smem + P2_STAGES * P2_STAGE);
@@ -977,7 +981,7 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                 }
                 int mp, nt;
                 pair_tile(t, m_pairs, n_tiles, &mp, &nt);
-                const int m_tile = 2 * mp + (int)rank;
+                const int m_tile = m_of(mp, rank);
                 for (int i = 0; i < k_tiles; ++i, ++gi) {
                     const int s = gi % P2_STAGES;
                     mbar_wait(&empty[s], ((uint32_t)(gi / P2_STAGES) & 1u) ^ 1u);
@@ -1066,7 +1070,7 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         for (int t = pair; t < total; t += npairs) {
             int mp, nt;
             pair_tile(t, m_pairs, n_tiles, &mp, &nt);
-            const int row = (2 * mp + (int)rank) * BM + q * 32 + lane;
+            const int row = m_of(mp, rank) * BM + q * 32 + lane;
             float acc[BN];
 #pragma unroll
             for (int j = 0; j < BN; ++j) acc[j] = 0.0f;
@@ -2272,7 +2276,7 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
                 wc = ctr.as<unsigned int>();
             }
             k_umma2_rowsq<false><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, th, (int)n, m_pairs, nt, k_tiles,
-                                                                         part.as<double>(), wc, 0);
+                                                                         part.as<double>(), wc, 0, nullptr, 0);
             LAUNCH_CHECK(c);
         } else if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
@@ -2320,9 +2324,14 @@ void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float
     LAUNCH_CHECK(c);
 }
 
+bool rowsq_tiles_ok(int64_t M, int64_t N) {
+    (void)umma_ok(BCUR_F32, 32, 8, nullptr);  // reads the environment switches once
+    return N > 2 * BN && (M + BM - 1) / BM >= 2 && !g_no_pair;
+}
+
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
                        const void* X, int dtx, int64_t ldx, double* rowsq, bool interleaved, const uint16_t* x16_pre,
-                       int q_pre, bool x16_il) {
+                       int q_pre, bool x16_il, const int* d_tiles, int ntiles) {
     if (M <= 0) return;
     if (N <= 0 || K <= 0) {
         CUDA_CHECK(cudaMemsetAsync(rowsq, 0, M * sizeof(double), c->stream));
@@ -2376,13 +2385,17 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     const int NTX = N <= BN ? 1 : N <= 2 * BN ? 2 : 4;
     const int nt = (int)((N + NTX * BN - 1) / (NTX * BN));
     DevBuf part(c, (size_t)nt * NTX * M * sizeof(double));
+    if (d_tiles) {  // only the listed tiles are computed: the rest of the row sums are zero
+        if (!(NTX == 4 && mt >= 2 && !g_no_pair)) fail(BCUR_E_INVALID_ARGUMENT, "gemm_rowsumsq_f16: tile lists need the CTA-pair path");
+        CUDA_CHECK(cudaMemsetAsync(part.ptr, 0, part.bytes, c->stream));
+    }
     if (NTX == 4 && mt >= 2 && !g_no_pair) {
         static bool attr = false;
         if (!attr) {
             CUDA_CHECK(cudaFuncSetAttribute(k_umma2_rowsq<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
             attr = true;
         }
-        const int m_pairs = (mt + 1) / 2;
+        const int m_pairs = d_tiles ? (ntiles + 1) / 2 : (mt + 1) / 2;
         const int pairs = std::min(m_pairs * nt, c->sm_count / 2);
         DevBuf ctr;
         unsigned int* wc = nullptr;
@@ -2392,7 +2405,8 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
             wc = ctr.as<unsigned int>();
         }
         k_umma2_rowsq<true><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, tx, (int)M, m_pairs, nt, k_tiles,
-                                                                           part.as<double>(), wc, xil ? 1 : 0);
+                                                                           part.as<double>(), wc, xil ? 1 : 0,
+                                                                           d_tiles, ntiles);
         LAUNCH_CHECK(c);
     } else {
         Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);

@@ -64,9 +64,13 @@ void gemm_rowsumsq(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, const 
 // interleaved: A16 is the [hi 64 | lo 64]-per-chunk copy (only hi is read), else compact hi.
 // x16_pre (nullable): X already in fp16 (K × N, ld K) scaled by 2^q_pre (B is then unused);
 // x16_il: x16_pre is an interleaved hi/lo split (2K halves per column) whose hi part is X
+// d_tiles (nullable, ntiles entries): compute only these 128-row tiles of the output (the other
+// rows are zero) — needs rowsq_tiles_ok(M, N) (the CTA-pair path)
 void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* A16, int64_t lda, const int* colexp,
                        const void* B, int dtb, int64_t ldb, double* rowsq, bool interleaved = true,
-                       const uint16_t* x16_pre = nullptr, int q_pre = 0, bool x16_il = false);
+                       const uint16_t* x16_pre = nullptr, int q_pre = 0, bool x16_il = false,
+                       const int* d_tiles = nullptr, int ntiles = 0);
+bool rowsq_tiles_ok(int64_t M, int64_t N);
 // orthonormal Q (fp64) → fp32 basis + its fp16 copy scaled by 2^14 (one pass)
 void basis_out(Ctx* c, const double* q, int64_t K, int64_t N, int64_t ldq, float* q32, uint16_t* q16);
 // out[0] = Σ_ij (D − op(A)·op(B))(i,j)²
@@ -198,6 +202,10 @@ void flag_nonfinite(Ctx* c, const double* x, int64_t count, unsigned int* d_flag
 void axpy_neg(Ctx* c, const double* x, double* y, int64_t n);  // y -= x
 void scale_columns(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*n*/);
 void scale_rows(Ctx* c, double* x, int64_t m, int64_t n, int64_t ld, const double* d_scale /*m*/);
+// out[j] = Σ_{i ∈ ranges} v(i, j)² for j < k (ranges: nr pairs [r0, r1) on the device)
+void colsumsq_ranges(Ctx* c, const double* v, int64_t ld, int64_t k, const int64_t* d_ranges, int nr, double* d_out);
+// scale[k] = σ[k]·√max(0, 1 − lev[k])
+void sigma_weights(Ctx* c, const double* d_sigma, const double* d_lev, int64_t n, double* d_scale);
 void copy_f64(Ctx* c, const double* src, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
 void transpose_to_f64(Ctx* c, const void* src, int dt, int64_t m, int64_t n, int64_t lds, double* dst, int64_t ldd);
 

@@ -850,28 +850,70 @@ static void make_rounded(Ctx* c, const DMat* a, RoundedA* ra, bool with_lo) {
 }
 // rows[j] = Σ_c (AᵀX)_jc² over the shard's columns: from the fp16 copy when present
 static void rowsq_pass(Ctx* c, const DMat* a, const RoundedA* ra, int64_t N, const void* X, int dtx, int64_t ldx,
-                       double* rows, const uint16_t* x16 = nullptr) {
+                       double* rows, const uint16_t* x16 = nullptr, const int* d_tiles = nullptr, int ntiles = 0) {
     if (ra && ra->ok())
         gemm_rowsumsq_f16(c, a->n, N, a->m, ra->il.as<uint16_t>(), a->m, ra->exps.as<int>(), X, dtx, ldx, rows,
-                          ra->interleaved, (x16 && ldx == a->m) ? x16 : nullptr, 14, true);
+                          ra->interleaved, (x16 && ldx == a->m) ? x16 : nullptr, 14, true, d_tiles, ntiles);
     else
         gemm_rowsumsq(c, OP_T, OP_N, a->n, N, a->m, a->ptr, a->dtype, a->ld, X, dtx, ldx, rows);
 }
 
-// Σ_g ‖Qᵀ A_g‖² (shard-local per-block values in d_blk_local, allreduced total)
+// Columns whose projection onto the basis is known exactly: the selected blocks themselves (A_g
+// lies in span(C) = span(Q), so ‖QᵀA_g‖² = ‖A_g‖², their norms-pass value).  The row-Σ² pass
+// skips the 128-column tiles they cover whole (c3: 32 of 512) — for full-rank whole-C bases on
+// the CTA-pair path.
+struct KnownCols {
+    std::vector<int> keep;      // tiles the pass computes
+    DevBuf d_keep;
+    std::vector<int64_t> cols;  // skipped local column ranges [c0, c1) (pairs)
+    double mass = 0.0;          // Σ ‖A_g‖² over the skipped blocks (shard-local)
+    bool active() const { return !cols.empty(); }
+};
+static KnownCols known_columns(Ctx* c, const DMat* a, const Shard& s, const Basis& B,
+                               const std::vector<int64_t>& blocks, const std::vector<double>& bn2, const RoundedA* ra) {
+    KnownCols k;
+    const int64_t nl = a->n, mt = (nl + 127) / 128;
+    int64_t width = 0;
+    for (int64_t g : blocks) width += s.off_global[g + 1] - s.off_global[g];
+    static const bool off = getenv("BCUR_NO_KNOWN_COLS") != nullptr;  // experiments
+    if (off || !ra || !ra->ok() || B.rank != width || !rowsq_tiles_ok(nl, B.rank) || !B.x16.ptr) return k;
+    std::vector<char> skip(mt, 0);
+    for (int64_t g : blocks) {
+        if (g < s.g0 || g >= s.g1) continue;
+        const int64_t c0 = s.off_global[g] - s.col0, c1 = s.off_global[g + 1] - s.col0;
+        if (c0 % 128 != 0 || (c1 - c0) % 128 != 0) continue;  // whole tiles only
+        for (int64_t t = c0 / 128; t < c1 / 128; ++t) skip[t] = 1;
+        k.cols.push_back(c0);
+        k.cols.push_back(c1);
+        k.mass += bn2[g];
+    }
+    if (k.cols.empty()) return k;
+    for (int64_t t = 0; t < mt; ++t)
+        if (!skip[t]) k.keep.push_back((int)t);
+    k.d_keep = DevBuf(c, std::max<size_t>(1, k.keep.size()) * sizeof(int));
+    if (!k.keep.empty()) h2d(c, k.d_keep.as<int>(), k.keep.data(), k.keep.size());
+    return k;
+}
+
+// Σ_g ‖Qᵀ A_g‖² (shard-local per-block values in d_blk_local, allreduced total); with `known`,
+// the skipped blocks contribute their exact ‖A_g‖² to the total (not to d_blk_local)
 static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local,
-                             const RoundedA* ra = nullptr) {
+                             const RoundedA* ra = nullptr, const KnownCols* known = nullptr) {
     const int64_t nl = a->n;
     Mat64 rows(c, nl, 1), tot(c, 1, 1);
-    rowsq_pass(c, a, ra, B.rank, B.buf.ptr, B.dt, B.rows, rows.p(), B.x16.as<uint16_t>());
-    Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
+    const bool kn = known && known->active();
+    rowsq_pass(c, a, ra, B.rank, B.buf.ptr, B.dt, B.rows, rows.p(), B.x16.as<uint16_t>(),
+               kn ? known->d_keep.as<int>() : nullptr, kn ? (int)known->keep.size() : 0);
+    Mat64 blk(c, std::max<int64_t>(1, s.g1 - s.g0), 1), tot2(c, 2, 1);
     double* b = d_blk_local ? d_blk_local : blk.p();
     segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
-    sum_vector(c, b, s.g1 - s.g0, tot.p());
-    allreduce(c, tot.p(), 1);
-    double h = 0.0;
-    d2h(c, &h, tot.p(), 1);
-    return h;
+    sum_vector(c, b, s.g1 - s.g0, tot2.p());
+    const double km = kn ? known->mass : 0.0;
+    CUDA_CHECK(cudaMemcpyAsync(tot2.p() + 1, &km, sizeof km, cudaMemcpyHostToDevice, c->stream));
+    allreduce(c, tot2.p(), 2);
+    double h[2] = {0.0, 0.0};
+    d2h(c, h, tot2.p(), 2);  // (synchronizes: km is still in scope)
+    return h[0] + h[1];
 }
 
 // First-order correction of the row-Σ² pass's fp16 basis copy along the sketch's top-k
@@ -882,7 +924,7 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
 // finder (A ≈ U_kΣ_kV_kᵀ + the rest),  Σ_k σ_k²(‖Qᵀu_k‖² − ‖Q̃ᵀu_k‖²)  restores those
 // directions; what remains is spread over many directions and averages out (~1e-7).  Two
 // thin DMMA products (r × k).
-static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub) {
+static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub, const KnownCols* known = nullptr) {
     const int64_t m = B.rows, r = B.rank, ke = sub.k_eff;
     if (r <= 0 || ke <= 0 || !B.x16.ptr || B.dt != BCUR_F32 || !h3_ok(m)) return 0.0;
     // W_hi = (UΣ)ᵀQ̃ and W_lo = (UΣ)ᵀΔ from the two parts of the basis's fp16 split (Q̃ = hi,
@@ -893,7 +935,19 @@ static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub) {
     Mat64 US(c, m, ke), sg(c, ke, 1), W(c, ke, 3 * r), tot(c, 2, 1);
     copy_f64(c, sub.u.p(), m, ke, sub.u.ld, US.p(), US.ld);
     h2d(c, sg.p(), sub.sigma.data(), ke);
-    scale_columns(c, US.p(), m, ke, US.ld, sg.p());
+    if (known && known->active()) {
+        // the pass skipped the known columns (their exact mass is used): only the share
+        // 1 − Σ_{j known} v_jk² of each component went through the fp16 basis copy
+        Mat64 lev(c, ke, 1), w(c, ke, 1);
+        DevBuf dr(c, known->cols.size() * sizeof(int64_t));
+        h2d(c, dr.as<int64_t>(), known->cols.data(), known->cols.size());
+        colsumsq_ranges(c, sub.v.p(), sub.v.ld, ke, dr.as<int64_t>(), (int)(known->cols.size() / 2), lev.p());
+        allreduce(c, lev.p(), ke);
+        sigma_weights(c, sg.p(), lev.p(), ke, w.p());
+        scale_columns(c, US.p(), m, ke, US.ld, w.p());
+    } else {
+        scale_columns(c, US.p(), m, ke, US.ld, sg.p());
+    }
     DevBuf uil, ue;
     split_il(c, US.p(), BCUR_F64, m, ke, US.ld, &uil, &ue);
     double* blk[3] = {W.p(), W.p() + r * W.ld, W.p() + 2 * r * W.ld};  // W_hi | −W_lo | W_hi + W_lo
@@ -1030,8 +1084,9 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     ph.reset(new ProfScope(c, "phase:5 residual", 0, 0));
     double res2 = 0.0;
     if (o.residual != BCUR_RESID_EXPLICIT) {  // Pythagoras first (AUTO falls back to explicit when small)
-        res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra);
-        if (ra.ok() && B.x16.ptr) res2 -= sketch_correction(c, B, sub);
+        const KnownCols known = known_columns(c, a, s, B, unique_in_order(blocks), bn2, &ra);
+        res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra, &known);
+        if (ra.ok() && B.x16.ptr) res2 -= sketch_correction(c, B, sub, &known);
     }
     ph.reset();
     int path = 0;
