@@ -580,17 +580,34 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
             if (timing) tb += clock64() - c0;
         }
         if (!rotated) break;
+        // would the next sweep rotate at all?  (The same test as the rounds' on every off-diagonal
+        // pair: none passing it means that sweep would change nothing — skipping it is exact.)
+        if (threadIdx.x == 0) rotated = 0;
+        __syncthreads();
+        for (int e = threadIdx.x; e < w * (w - 1) / 2; e += NT) {
+            int i = (int)((sqrtf(8.0f * (float)e + 1.0f) + 1.0f) * 0.5f);  // strict lower (i > j): e = i(i−1)/2 + j
+            if (i * (i - 1) / 2 > e) --i;
+            if ((i + 1) * i / 2 <= e) ++i;
+            const int j = e - i * (i - 1) / 2;
+            const double apq = Ap[tri_at(i, j)];
+            if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(Ap[tri_at(i, i)] * Ap[tri_at(j, j)])) rotated = 1;
+        }
+        __syncthreads();
+        if (!rotated) break;
         __syncthreads();
     }
+    // eigenvalues descending: rank by counting (ties keep index order), one thread per entry
     __shared__ int order[512];
-    if (threadIdx.x == 0) {
-        for (int i = 0; i < w; ++i) order[i] = i;
+    for (int j = threadIdx.x; j < w; j += NT) {
+        const double lj = Ap[tri_at(j, j)];
+        int rank = 0;
         for (int i = 0; i < w; ++i) {
-            int best = i;
-            for (int j = i + 1; j < w; ++j)
-                if (Ap[tri_at(order[j], order[j])] > Ap[tri_at(order[best], order[best])]) best = j;
-            const int t = order[i]; order[i] = order[best]; order[best] = t;
+            const double li = Ap[tri_at(i, i)];
+            rank += (li > lj || (li == lj && i < j)) ? 1 : 0;
         }
+        order[rank] = j;
+    }
+    if (threadIdx.x == 0) {
         *nrounds_out = rounds;
         if (timing) printf("jacobi_packed w=%d threads=%d rounds=%d clocks/round: rotations %lld | updates %lld\n", w, NT,
                            rounds, ta / (rounds ? rounds : 1), tb / (rounds ? rounds : 1));
@@ -602,20 +619,26 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     }
 }
 
-// V = the product of the logged rotations (V ← V·J per round), rows of V spread over CTAs:
-// every row goes through all rounds independently; within a round the pairs are disjoint.
-// vout[:, j] = V[:, order[j]].
-constexpr int JR_T = 256, JR_ROWS = 2, JR_CHUNK = 6144;  // log entries staged per chunk (144 KB)
+// V = the product of the logged rotations (V ← V·J per round), rows of V spread over warps:
+// every row goes through all rounds independently and within a round the pairs are disjoint, so
+// a warp owns JR_RW rows outright (lanes over the round's pairs) and separates rounds with
+// __syncwarp only; the CTA shares the staged log.  vout[:, j] = V[:, order[j]].
+constexpr int JR_T = 256, JR_RW = 2, JR_ROWS = JR_RW * (JR_T / 32), JR_CHUNK = 4096;  // log entries per chunk (96 KB)
+constexpr size_t JR_SMEM = JR_CHUNK * sizeof(JRot) + (size_t)JR_ROWS * 512 * sizeof(double);
 __global__ void __launch_bounds__(JR_T) k_jacobi_replay(const JRot* __restrict__ log, const int* __restrict__ nrounds,
                                                         const int* __restrict__ order, int w, double* __restrict__ vout) {
-    __shared__ double V[JR_ROWS][512];
-    extern __shared__ JRot stage[];  // a chunk of whole rounds, loaded with one barrier
+    extern __shared__ uint8_t jr_smem[];
+    JRot* stage = reinterpret_cast<JRot*>(jr_smem);                        // a chunk of whole rounds
+    double* V = reinterpret_cast<double*>(jr_smem + JR_CHUNK * sizeof(JRot));  // [JR_ROWS][512]
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r0 = blockIdx.x * JR_ROWS;
     const int wp = (w + 1) & ~1, half = wp / 2;
     for (int e = threadIdx.x; e < JR_ROWS * wp; e += JR_T) {
         const int rr = e / wp, j = e % wp;
-        V[rr][j] = (r0 + rr < w && j == r0 + rr) ? 1.0 : 0.0;
+        V[rr * 512 + j] = (r0 + rr < w && j == r0 + rr) ? 1.0 : 0.0;
     }
+    double* v0 = V + (warp * JR_RW) * 512;
+    double* v1 = v0 + 512;
     const int n = *nrounds, per = JR_CHUNK / half;
     for (int t0 = 0; t0 < n; t0 += per) {
         const int nr = min(per, n - t0);
@@ -624,20 +647,22 @@ __global__ void __launch_bounds__(JR_T) k_jacobi_replay(const JRot* __restrict__
         __syncthreads();
         for (int t = 0; t < nr; ++t) {
             const JRot* lr = stage + t * half;
-            for (int e = threadIdx.x; e < JR_ROWS * half; e += JR_T) {
-                const int rr = e / half, i = e - rr * half;
+            for (int i = lane; i < half; i += 32) {
                 const JRot r = lr[i];
                 if (r.s == 0.0) continue;
-                const double vp = V[rr][r.p], vq = V[rr][r.q];
-                V[rr][r.p] = r.c * vp - r.s * vq;
-                V[rr][r.q] = r.s * vp + r.c * vq;
+                const double a0 = v0[r.p], b0 = v0[r.q], a1 = v1[r.p], b1 = v1[r.q];
+                v0[r.p] = r.c * a0 - r.s * b0;
+                v0[r.q] = r.s * a0 + r.c * b0;
+                v1[r.p] = r.c * a1 - r.s * b1;
+                v1[r.q] = r.s * a1 + r.c * b1;
             }
-            __syncthreads();
+            __syncwarp();
         }
     }
+    __syncthreads();
     for (int e = threadIdx.x; e < JR_ROWS * w; e += JR_T) {
         const int rr = e / w, j = e % w;
-        if (r0 + rr < w) vout[(r0 + rr) + (int64_t)j * w] = V[rr][order[j]];
+        if (r0 + rr < w) vout[(r0 + rr) + (int64_t)j * w] = V[rr * 512 + order[j]];
     }
 }
 
@@ -837,11 +862,10 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
         LAUNCH_CHECK(c);
         static bool attr_r = false;
         if (!attr_r) {
-            CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_replay, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)(JR_CHUNK * sizeof(JRot))));
+            CUDA_CHECK(cudaFuncSetAttribute(k_jacobi_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)JR_SMEM));
             attr_r = true;
         }
-        k_jacobi_replay<<<(unsigned)((w + JR_ROWS - 1) / JR_ROWS), JR_T, JR_CHUNK * sizeof(JRot), c->stream>>>(
+        k_jacobi_replay<<<(unsigned)((w + JR_ROWS - 1) / JR_ROWS), JR_T, JR_SMEM, c->stream>>>(
             log.as<JRot>(), nrounds, order, (int)w, v);
         if (getenv("BCUR_JACOBI_DEBUG")) {
             int hr = 0;

@@ -40,6 +40,7 @@ bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (e
 bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
 bool g_no_h3pair = false;         // BCUR_UMMA_NO_H3_PAIR=1: single-CTA 3×FP16 products (experiments)
 bool g_no_fastacc = false;        // BCUR_UMMA_NO_FAST_ACC=1: GEMM_FAST_ACC products on the split accumulators (experiments)
+int g_l2hint = 0;                 // BCUR_ROWSQ_L2HINT: row-Σ² TMA L2 hints, 1 = X evict-last, 2 = also A evict-first (experiments)
 int g_pf = -1;                    // BCUR_UMMA_PF: A-tile L2 prefetch distance in stages (experiments)
 constexpr uint32_t A_TILE = BM * BK * 4;  // 16 KB
 constexpr uint32_t X_TILE = BN * BK * 4;  // 8 KB (one 64-column N tile)
@@ -908,6 +909,36 @@ __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// 2-SM TMA loads with an optional L2 eviction policy (the createpolicy encodings CUTLASS uses).
+// Measured on the c3 row-Σ² pass (profiles/r02ad): A evict-first + X evict-last raised its DRAM
+// reads from 7.9 to 9.8 GB (a wave's 8 X tiles share each A tile through L2), so the default is
+// no hint
+constexpr uint64_t L2_EVICT_FIRST = 0x12F0000000000000ull, L2_EVICT_LAST = 0x14F0000000000000ull;
+__device__ __forceinline__ void tma2sm_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                          uint64_t pol) {
+    if (pol)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst), "l"(map), "r"(bar), "r"(c0), "r"(c1), "l"(pol) : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c0), "r"(c1) : "memory");
+}
+__device__ __forceinline__ void tma2sm_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
+                                          int c3, uint64_t pol) {
+    if (pol)
+        asm volatile(
+            "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+            " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst), "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2),
+            "r"(c3), "l"(pol) : "memory");
+    else
+        asm volatile(
+            "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+            : "memory");
+}
+
 // pair tile t → (A column pair mp, X tile nt): groups of 8 X tiles × all pairs, so a wave
 // of pairs shares A and X bands through L2 (as make_sched's raster)
 __device__ __forceinline__ void pair_tile(int t, int m_pairs, int n_tiles, int* mp, int* nt) {
@@ -921,7 +952,7 @@ template <bool H>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(P2_THREADS, 1)
 k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmX, int M, int m_pairs,
               int n_tiles, int k_tiles, double* __restrict__ partial, unsigned int* __restrict__ wave_ctr, int x_il,
-              const int* __restrict__ tiles, int ntiles) {
+              const int* __restrict__ tiles, int ntiles, int l2hint) {
     // tiles (nullable): the 128-column M tiles to compute, pairs taken in list order (the others'
     // rows of `partial` are left untouched); a missing second tile reads as TMA zeros past M
     auto m_of = [&](int mp, uint32_t r) { const int i = 2 * mp + (int)r; return tiles ? (i < ntiles ? tiles[i] : (M + BM - 1) / BM) : i; };
@@ -989,28 +1020,18 @@ k_umma2_rowsq(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
                     const uint32_t fb = full0 + s * 8;
                     const int k0 = i * BKE;
                     uint8_t* st = smem + s * P2_STAGE;
+                    const uint64_t pa = l2hint >= 2 ? L2_EVICT_FIRST : 0, px = l2hint >= 1 ? L2_EVICT_LAST : 0;
                     if (H)  // the interleaved hi/lo copy (4-D map; hi = part 0)
-                        asm volatile(
-                            "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(0),
-                            "r"(0), "r"(k0 / 64), "r"(m_tile * BM) : "memory");
+                        tma2sm_4d(smem_u32(st), &tmA, fb, 0, 0, k0 / 64, m_tile * BM, pa);
                     else
-                        asm volatile(
-                            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                            " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st)), "l"(&tmA), "r"(fb), "r"(k0),
-                            "r"(m_tile * BM) : "memory");
+                        tma2sm_2d(smem_u32(st), &tmA, fb, k0, m_tile * BM, pa);
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
+                        const int xc = (nt * NTP + (int)rank * 2 + h) * BN;
                         if (x_il)  // hi of an interleaved split (4-D map, part 0)
-                            asm volatile(
-                                "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                                " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(st + A_TILE + h * X_TILE)), "l"(&tmX),
-                                "r"(fb), "r"(0), "r"(0), "r"(k0 / 64), "r"((nt * NTP + (int)rank * 2 + h) * BN) : "memory");
+                            tma2sm_4d(smem_u32(st + A_TILE + h * X_TILE), &tmX, fb, 0, 0, k0 / 64, xc, px);
                         else
-                            asm volatile(
-                                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                                " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(st + A_TILE + h * X_TILE)), "l"(&tmX),
-                                "r"(fb), "r"(k0), "r"((nt * NTP + (int)rank * 2 + h) * BN) : "memory");
+                            tma2sm_2d(smem_u32(st + A_TILE + h * X_TILE), &tmX, fb, k0, xc, px);
                     }
                 }
                 if (wave_ctr) atomicAdd(wave_ctr, 1u);
@@ -2214,6 +2235,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         g_no_h3pair = nh && nh[0] == '1';
         const char* nf = getenv("BCUR_UMMA_NO_FAST_ACC");
         g_no_fastacc = nf && nf[0] == '1';
+        const char* l2h = getenv("BCUR_ROWSQ_L2HINT");
+        if (l2h) g_l2hint = atoi(l2h);
         const char* pf = getenv("BCUR_UMMA_PF");
         if (pf) g_pf = atoi(pf);
         const char* d = getenv("BCUR_UMMA_DEBUG");
@@ -2276,7 +2299,7 @@ void umma_atx(Ctx* c, const float* A, int64_t m, int64_t n, int64_t lda, const v
                 wc = ctr.as<unsigned int>();
             }
             k_umma2_rowsq<false><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, th, (int)n, m_pairs, nt, k_tiles,
-                                                                         part.as<double>(), wc, 0, nullptr, 0);
+                                                                         part.as<double>(), wc, 0, nullptr, 0, g_l2hint);
             LAUNCH_CHECK(c);
         } else if (NTX == 1)
             launch_umma_nt<false, EPI_ROWSQ, 1, false>(c, sc, ta, th, th, (int)n, (int)N, nullptr, 0,
@@ -2406,7 +2429,7 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
         }
         k_umma2_rowsq<true><<<2 * pairs, P2_THREADS, P2_SMEM, c->stream>>>(ta, tx, (int)M, m_pairs, nt, k_tiles,
                                                                            part.as<double>(), wc, xil ? 1 : 0,
-                                                                           d_tiles, ntiles);
+                                                                           d_tiles, ntiles, g_l2hint);
         LAUNCH_CHECK(c);
     } else {
         Sched sc = make_sched(mt, nt, 1, k_tiles, k_tiles, false, false);

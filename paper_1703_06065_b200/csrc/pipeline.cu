@@ -208,7 +208,8 @@ static void chol_enqueue(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         return;
     }
     // the persistent kernel streams its operands in 16-byte pairs: even widths (odd ones, and
-    // BCUR_CHOL_REC=1 for experiments, take the launch-per-product recursion below)
+    // BCUR_CHOL_REC=1 for experiments, take the launch-per-product recursion below; at w = 200
+    // both take ~0.17 ms, c1's C basis, profiles/r02af)
     static const bool rec = getenv("BCUR_CHOL_REC") != nullptr;
     if (!rec && w % 2 == 0) {
         chol_persistent(c, G, w, ldg, R, X, st, want_r);

@@ -66,7 +66,7 @@ def test_cholesky_inverse(B, w):
     assert info2 == 0 and np.array_equal(r2, r)
 
 
-@pytest.mark.parametrize("w,bad", [(50, 17), (700, 300), (700, 650)])
+@pytest.mark.parametrize("w,bad", [(50, 17), (200, 150), (700, 300), (700, 650)])
 def test_cholesky_reports_failed_pivot(B, w, bad):
     gen = np.random.default_rng(bad)
     x = gen.standard_normal((w + 10, w))
