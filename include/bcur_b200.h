@@ -179,9 +179,11 @@ bcur_status bcur_sketch_product(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int tran
  *                          A·X, m % 8 == 0 for AᵀX)
  *   BCUR_PRODUCT_FAST_ACC  with H3: the three MMAs of a k-step into one fp32 accumulator (CTA pairs,
  *                          ~1e-6 relative instead of ~2⁻²²; the pipelines' C·R⁻¹ and c4's Q_CᵀA)
+ *   BCUR_PRODUCT_HI_ONLY   with FAST_ACC: the a_hi·x_hi MMA alone (2⁻¹¹ relative; the pipelines'
+ *                          CholQR2 second-pass correction Q1·(−F), ‖F‖ ≲ 1e-4)
  */
 enum { BCUR_PRODUCT_GRAM = 1, BCUR_PRODUCT_X_UPPER = 2, BCUR_PRODUCT_ROWSQ_F16 = 4, BCUR_PRODUCT_H3 = 8,
-       BCUR_PRODUCT_FAST_ACC = 16 };
+       BCUR_PRODUCT_FAST_ACC = 16, BCUR_PRODUCT_HI_ONLY = 32 };
 bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int transpose, int flags, bcur_dmat out);
 /* The factorization behind every orthonormal basis of the path (CholQR2 of the sketch, of C,
  * of Rᵀ — the reference's pseudoinverse, matcore.cpp:85-91, and svd, :39-56, are never

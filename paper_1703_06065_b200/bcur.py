@@ -516,7 +516,7 @@ def sketch_product(a, x: np.ndarray, transpose: bool = False, row_sumsq: bool = 
 
 def structured_product(a, x: Optional[np.ndarray] = None, transpose: bool = False, gram: bool = False,
                        x_upper: bool = False, rowsq_f16: bool = False, h3: bool = False,
-                       fast_acc: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
+                       fast_acc: bool = False, hi_only: bool = False, ctx: Optional[Context] = None) -> np.ndarray:
     """bcur_sketch_product_ex: ``gram`` → AᵀA (upper triangle valid, ``x`` None);
     ``x_upper`` → A·X or Aᵀ·X with an upper-triangular X (the pipelines' Q = C·R⁻¹);
     ``rowsq_f16`` → Σ_c (AᵀX)_jc² through the pipelines' fp16 row-sum path (n × 1);
@@ -524,7 +524,7 @@ def structured_product(a, x: Optional[np.ndarray] = None, transpose: bool = Fals
     ctx = ctx or default_context()
     d = _dev(a, ctx)
     flags = (1 if gram else 0) | (2 if x_upper else 0) | (4 if rowsq_f16 else 0) | (8 if h3 else 0) | \
-        (16 if fast_acc else 0)
+        (16 if fast_acc else 0) | (32 if hi_only else 0)
     xd = None if x is None else DeviceMatrix.from_host(np.asarray(x, dtype=np.float64), ctx)
     rows = d.shape[1] if (transpose or gram or rowsq_f16) else d.shape[0]
     cols = d.shape[1] if gram else (1 if rowsq_f16 else xd.shape[1])

@@ -180,6 +180,8 @@ bcur_status bcur_ctx_destroy(bcur_ctx ctx) {
     cudaStreamSynchronize(ctx->stream);
     ctx->trim();
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    if (ctx->up_ring) cudaFreeHost(ctx->up_ring);
+    if (ctx->rd_area) cudaFreeHost(ctx->rd_area);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     if (ctx->side) {
         cudaStreamSynchronize(ctx->side);
@@ -780,7 +782,7 @@ bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int t
     Ctx* c = C(ctx);
     DMat *A = M(a), *O = M(out);
     if (flags & ~(BCUR_PRODUCT_GRAM | BCUR_PRODUCT_X_UPPER | BCUR_PRODUCT_ROWSQ_F16 | BCUR_PRODUCT_H3 |
-                  BCUR_PRODUCT_FAST_ACC))
+                  BCUR_PRODUCT_FAST_ACC | BCUR_PRODUCT_HI_ONLY))
         fail(BCUR_E_INVALID_ARGUMENT, "sketch_product_ex: bad flags");
     if (flags & BCUR_PRODUCT_H3) {
         // the pipelines' 3×FP16 form: A split once by the norms pass into fp16 hi + lo
@@ -801,7 +803,8 @@ bcur_status bcur_sketch_product_ex(bcur_ctx ctx, bcur_dmat a, bcur_dmat x, int t
         ops::block_sumsq(c, A->ptr, A->dtype, A->m, A->ld, off.as<int64_t>(), 1, tot.as<double>(), nullptr, A->m,
                          nullptr, exps.as<int>(), il.as<uint16_t>());
         const int fl = (gram ? ops::GEMM_SYM_UPPER : (flags & BCUR_PRODUCT_X_UPPER) ? ops::GEMM_B_UPPER : 0) |
-                       ((flags & BCUR_PRODUCT_FAST_ACC) ? ops::GEMM_FAST_ACC : 0);
+                       ((flags & BCUR_PRODUCT_FAST_ACC) ? ops::GEMM_FAST_ACC : 0) |
+                       ((flags & BCUR_PRODUCT_HI_ONLY) ? ops::GEMM_HI_ONLY : 0);
         if (gram) {  // X = the same matrix, split on its own (K-major X operand)
             ops::SplitF16 xs;
             ops::split_f16(c, A->ptr, A->dtype, A->m, A->n, A->ld, nullptr, &xs);

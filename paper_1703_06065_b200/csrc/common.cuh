@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -149,6 +150,62 @@ struct Ctx {
     }
     void sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
     std::map<void*, size_t> sizes;
+
+    // Host → device uploads without a stream synchronization: the source is copied into a pinned
+    // ring and the asynchronous copy reads it from there, so the caller's buffer (often on its
+    // stack) may go away at once.  The ring is reused only after every stream that copied out
+    // of it since its last wrap has been synchronized.  nullptr: too large for the ring.
+    static constexpr size_t UP_RING = (size_t)4 << 20;
+    char* up_ring = nullptr;
+    size_t up_off = 0;
+    std::vector<cudaStream_t> up_streams;
+    const void* stage_upload(const void* host, size_t bytes) {
+        if (bytes > UP_RING / 4) return nullptr;
+        if (!up_ring) CUDA_CHECK(cudaMallocHost(&up_ring, UP_RING));
+        const size_t b = (bytes + 255) & ~(size_t)255;
+        if (up_off + b > UP_RING) {
+            for (cudaStream_t s : up_streams) CUDA_CHECK(cudaStreamSynchronize(s));
+            up_streams.clear();
+            up_off = 0;
+        }
+        if (std::find(up_streams.begin(), up_streams.end(), stream) == up_streams.end()) up_streams.push_back(stream);
+        char* p = up_ring + up_off;
+        up_off += b;
+        memcpy(p, host, bytes);
+        return p;
+    }
+    // Device → host reads collected into a pinned area and delivered at the next read_all(): a
+    // decomposition's small results (scores, statuses, norms) share one stream synchronization.
+    static constexpr size_t RD_AREA = (size_t)4 << 20;
+    char* rd_area = nullptr;
+    size_t rd_off = 0;
+    struct RdItem {
+        void* host;
+        size_t off, bytes;
+    };
+    std::vector<RdItem> rd_items;
+    void read_later(void* host, const void* dev, size_t bytes) {
+        if (!bytes) return;
+        if (!rd_area) CUDA_CHECK(cudaMallocHost(&rd_area, RD_AREA));
+        const size_t b = (bytes + 255) & ~(size_t)255;
+        if (bytes > RD_AREA / 2) {  // large: read it directly (synchronizes)
+            read_all();
+            CUDA_CHECK(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, stream));
+            sync();
+            return;
+        }
+        if (rd_off + b > RD_AREA) read_all();
+        CUDA_CHECK(cudaMemcpyAsync(rd_area + rd_off, dev, bytes, cudaMemcpyDeviceToHost, stream));
+        rd_items.push_back({host, rd_off, bytes});
+        rd_off += b;
+    }
+    // one stream synchronization delivers every pending read
+    void read_all() {
+        sync();
+        for (const RdItem& it : rd_items) memcpy(it.host, rd_area + it.off, it.bytes);
+        rd_items.clear();
+        rd_off = 0;
+    }
 
     // Second stream for overlapped work (the blocked Cholesky's look-ahead).  Work on it is
     // forked from `stream` and joined back into it before any buffer it touches is released,

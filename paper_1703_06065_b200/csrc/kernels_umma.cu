@@ -39,6 +39,7 @@ bool g_wave_barrier_off = false;  // BCUR_UMMA_NO_WAVE_BARRIER=1 (experiments)
 bool g_no_pair = false;           // BCUR_UMMA_NO_PAIR=1: single-CTA row-Σ² (experiments)
 bool g_no_x3pair = true;          // BCUR_UMMA_X3_PAIR=1: CTA-pair 3×TF32 products (measured slower so far)
 bool g_no_h3pair = false;         // BCUR_UMMA_NO_H3_PAIR=1: single-CTA 3×FP16 products (experiments)
+bool g_no_hi_only = false;        // BCUR_UMMA_NO_HI_ONLY=1: GEMM_HI_ONLY products with all three MMAs (experiments)
 bool g_no_fastacc = false;        // BCUR_UMMA_NO_FAST_ACC=1: GEMM_FAST_ACC products on the split accumulators (experiments)
 int g_l2hint = 0;                 // BCUR_ROWSQ_L2HINT: row-Σ² TMA L2 hints, 1 = X evict-last, 2 = also A evict-first (experiments)
 int g_pf = -1;                    // BCUR_UMMA_PF: A-tile L2 prefetch distance in stages (experiments)
@@ -1149,6 +1150,7 @@ struct PSched {
     unsigned int* wave_ctr;
     int bke;   // K elements per k-tile (32 tf32, 64 fp16): the triangular-X limit is in these units
     int x_il;  // H3: x_hi/x_lo from one interleaved split (4-D map, part = hi|lo)
+    int hi_only;  // k_umma2_h3m: a_hi·x_hi only (GEMM_HI_ONLY): the lo halves are neither loaded nor used
 };
 constexpr int X3P_NTRANSFORM = 6, X3P_NDRAIN = 8;
 constexpr int X3P_THREADS = 32 * (2 + X3P_NTRANSFORM + X3P_NDRAIN);        // 512
@@ -1450,6 +1452,7 @@ PSched make_psched(int mt, int nt, int k_tiles, bool sym, bool tri_x) {
     sc.wave_ctr = nullptr;
     sc.bke = BK;
     sc.x_il = 0;
+    sc.hi_only = 0;
     if (sym) {
         sc.total = 0;
         for (int n = 0; n < nt; ++n) sc.total += std::min(n / 2, sc.m_pairs - 1) + 1;
@@ -1972,18 +1975,18 @@ k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     for (int i = 0; i < nk; ++i, ++gi) {
                         const int s = gi % HM_STAGES;
                         mbar_wait(&empty[s], ((uint32_t)(gi / HM_STAGES) & 1u) ^ 1u);
-                        if (rank == 0) mbar_expect_tx(&full[s], 2 * HM_STAGE);
+                        if (rank == 0) mbar_expect_tx(&full[s], sc.hi_only ? 2 * (A_TILE + HM_XT) : 2 * HM_STAGE);
                         const uint32_t fb = full0 + s * 8;
                         const int k0 = i * BKH;
                         const uint32_t sa = smem_u32(a_hi(s)), sx = smem_u32(x_hi(s));
+                        const int nhl = sc.hi_only ? 1 : 2;
                         auto load4 = [&](uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3) {
                             asm volatile(
                                 "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                                 " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst), "l"(tm), "r"(fb), "r"(c0), "r"(c1),
                                 "r"(c2), "r"(c3) : "memory");
                         };
-#pragma unroll
-                        for (int hl = 0; hl < 2; ++hl) {  // A: the interleaved hi/lo copy (4-D map)
+                        for (int hl = 0; hl < nhl; ++hl) {  // A: the interleaved hi/lo copy (4-D map)
                             if (A_MN) {
                                 load4(sa + hl * A_TILE, &tmA, 0, hl, m_tile * 2, k0);
                                 load4(sa + hl * A_TILE + A_TILE / 2, &tmA, 0, hl, m_tile * 2 + 1, k0);
@@ -1993,8 +1996,7 @@ k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         }
                         // X: this CTA's 96 N rows, hi then lo, as three 32-row boxes each (the maps'
                         // boxes are 32 rows for this kernel)
-#pragma unroll
-                        for (int hl = 0; hl < 2; ++hl)
+                        for (int hl = 0; hl < nhl; ++hl)
 #pragma unroll
                             for (int h3 = 0; h3 < 3; ++h3) {
                                 const uint32_t dst = sx + hl * HM_XT + h3 * (HM_XT / 3);
@@ -2040,13 +2042,20 @@ k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             const uint64_t dxh = sdesc(xh + k8 * 32, 16, 1024, 2);
                             const uint64_t dxl = sdesc(xl + k8 * 32, 16, 1024, 2);
                             const uint32_t acc = (!first || k8 > 0) ? 1u : 0u;
-                            asm volatile(
-                                "{\n\t.reg .pred e, p, one;\n\telect.sync _|e, 0xffffffff;\n\t"
-                                "setp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 one, %6, %6;\n\t"
-                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %5, p;\n\t"
-                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, one;\n\t"
-                                "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %4, %2, %5, one;\n\t}" ::"r"(d),
-                                "l"(dah), "l"(dxh), "l"(dxl), "l"(dal), "r"(IDESC), "r"(acc));
+                            if (sc.hi_only)
+                                asm volatile(
+                                    "{\n\t.reg .pred e, p;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                    "setp.ne.b32 p, %4, 0;\n\t"
+                                    "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+                                    "l"(dah), "l"(dxh), "r"(IDESC), "r"(acc));
+                            else
+                                asm volatile(
+                                    "{\n\t.reg .pred e, p, one;\n\telect.sync _|e, 0xffffffff;\n\t"
+                                    "setp.ne.b32 p, %6, 0;\n\tsetp.eq.b32 one, %6, %6;\n\t"
+                                    "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %5, p;\n\t"
+                                    "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %3, %5, one;\n\t"
+                                    "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %4, %2, %5, one;\n\t}" ::"r"(d),
+                                    "l"(dah), "l"(dxh), "l"(dxl), "l"(dal), "r"(IDESC), "r"(acc));
                         }
                         asm volatile(
                             "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -2235,6 +2244,8 @@ bool umma_ok(int dta, int64_t m, int64_t lda, const void* a) {
         g_no_h3pair = nh && nh[0] == '1';
         const char* nf = getenv("BCUR_UMMA_NO_FAST_ACC");
         g_no_fastacc = nf && nf[0] == '1';
+        const char* nho = getenv("BCUR_UMMA_NO_HI_ONLY");
+        g_no_hi_only = nho && nho[0] == '1';
         const char* l2h = getenv("BCUR_ROWSQ_L2HINT");
         if (l2h) g_l2hint = atoi(l2h);
         const char* pf = getenv("BCUR_UMMA_PF");
@@ -2642,6 +2653,7 @@ static void umma_h3_epi(Ctx* c, bool a_mn, const uint16_t* AL, const int* ea, in
         PSched ps = make_psched(mt, (int)((N + HM_NTP * BN - 1) / (HM_NTP * BN)), k_tiles, false, tri);
         ps.bke = BKH;
         ps.x_il = X.lo ? 0 : 1;
+        ps.hi_only = (flags & GEMM_HI_ONLY) && !g_no_hi_only ? 1 : 0;
         if (X.lo) {
             const int64_t ldx = X.ld > 0 ? X.ld : K;
             const uint64_t dX[2] = {(uint64_t)K, (uint64_t)N}, sX[1] = {(uint64_t)ldx * 2};

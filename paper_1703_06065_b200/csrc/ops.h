@@ -48,8 +48,11 @@ void sumsq_vector(Ctx* c, const double* x, int64_t n, double* d_out);
 //   GEMM_FAST_ACC   3×FP16 only: the three MMAs of a k-step into one fp32 accumulator (CTA pairs,
 //                   N = 256 tiles; fp32-grade, ~1e-6 relative): for products whose error is
 //                   corrected downstream or far inside its bar
+//   GEMM_HI_ONLY    with GEMM_FAST_ACC: a_hi·x_hi alone (one of the three MMAs; the lo halves are
+//                   not loaded): 2⁻¹¹-relative, for corrections ≲ 1e-4 of the result they are
+//                   added to (the CholQR2 second pass), whose error is then ≲ 1e-7 of the result
 enum GemmFlags { GEMM_SYM_UPPER = 1, GEMM_B_UPPER = 2, GEMM_X1 = 4, GEMM_A_UPPER = 8, GEMM_A_LOWER = 16,
-                 GEMM_B_LOWER = 32, GEMM_FAST_ACC = 64 };
+                 GEMM_B_LOWER = 32, GEMM_FAST_ACC = 64, GEMM_HI_ONLY = 128 };
 void gemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, const void* A, int dta, int64_t lda,
           const void* B, int dtb, int64_t ldb, double beta, double* C, int64_t ldc, int flags = 0);
 // rowsq[i] = Σ_j (op(A)·op(B))(i,j)²   (product never stored)

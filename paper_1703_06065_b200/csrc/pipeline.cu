@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <functional>
 
 #include "pipeline.h"
 
@@ -35,12 +36,30 @@ static void d2h(Ctx* c, T* host, const T* dev, size_t count) {
     CUDA_CHECK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
     c->sync();
 }
+// host buffers may be stack-owned by the caller: small uploads go through the context's pinned
+// ring (no synchronization), large ones synchronize
 template <class T>
 static void h2d(Ctx* c, T* dev, const T* host, size_t count) {
     if (!count) return;
-    CUDA_CHECK(cudaMemcpyAsync(dev, host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
-    c->sync();  // host buffers may be stack-owned by the caller
+    const void* src = c->stage_upload(host, count * sizeof(T));
+    CUDA_CHECK(cudaMemcpyAsync(dev, src ? src : host, count * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    if (!src) c->sync();
 }
+// device → host read delivered by the next c->read_all() (one synchronization for several reads)
+template <class T>
+static void d2h_later(Ctx* c, T* host, const T* dev, size_t count) {
+    c->read_later(host, dev, count * sizeof(T));
+}
+// drops undelivered reads when an operation ends (normally none are left; after a failure their
+// host destinations may be gone)
+struct ReadScope {
+    Ctx* c;
+    explicit ReadScope(Ctx* ctx) : c(ctx) {}
+    ~ReadScope() {
+        c->rd_items.clear();
+        c->rd_off = 0;
+    }
+};
 
 void allreduce(Ctx* c, double* d, int64_t count) {
     if (c->comm.world <= 1 || count <= 0) return;
@@ -243,6 +262,20 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     c->sync();
     return {hs.info, hs.info ? 0.0 : hs.mindiag, hs.maxdiag};
 }
+
+// chol_any without the synchronization: the status is delivered into *hs by the next
+// c->read_all() (callers enqueue speculative work behind the factorization meanwhile)
+struct CholStat {
+    int info, pad;
+    double mindiag, maxdiag;
+};
+static void chol_later(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv, bool tc, bool want_r,
+                       CholStat* hs) {
+    DevBuf st(c, 64);
+    chol_enqueue(c, G, w, ldg, R, Rinv, tc, st.as<int>(), want_r);
+    c->read_later(hs, st.ptr, sizeof *hs);
+}
+static CholInfo chol_info(const CholStat& hs) { return {hs.info, hs.info ? 0.0 : hs.mindiag, hs.maxdiag}; }
 
 int cholesky_inverse(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv, double* mindiag) {
     const CholInfo ci = chol_any(c, G, w, ldg, R, Rinv);
@@ -509,9 +542,11 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     const F16View cx{cil.as<uint16_t>(), nullptr, ce.as<int>(), rows, cc};
     umma_h3(c, false, cil.as<uint16_t>(), ce.as<int>(), rows, cc, cx, 1.0, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), true, false);
-    const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
-    if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
+    // The factorization's status and the second pass's ‖Q1ᵀQ1 − I‖ come back in ONE read: Q1 and
+    // its Gram are enqueued behind the factorization before its status is known (when it failed
+    // they are garbage and discarded with the path)
+    CholStat hs1{};
+    chol_later(c, G.p(), cc, G.ld, R.p(), Ri.p(), true, false, &hs1);
     // Q1 = C·R⁻¹ written straight into its interleaved split (fixed column exponent: the columns
     // of Q1 have norm ≈ 1) — the operand of the Gram Q1ᵀQ1 and of the second-pass product, with
     // no fp64 Q1 and no split pass
@@ -533,7 +568,11 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     Mat64 dev(c, 1, 1);
     max_dev_identity(c, G.p(), cc, G.ld, dev.p());
     double hdev = 1.0;
-    d2h(c, &hdev, dev.p(), 1);
+    d2h_later(c, &hdev, dev.p(), 1);
+    c->read_all();
+    const CholInfo ci = chol_info(hs1);
+    const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
+    if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     const bool near = hdev < 1e-4;
     if (near) {
         near_identity_rinv(c, G.p(), cc, G.ld, Ri.p(), true);
@@ -549,7 +588,7 @@ static bool cholqr2_whole_h3(Ctx* c, const void* C, int64_t rows, int64_t cc, bo
     // its split when X2 = −F), written as the fp32 basis and its fp16·2^14 copy
     umma_h3_basis(c, qil.as<uint16_t>(), qe.as<int>(), rows, cc, Ri.p(), BCUR_F64, cc, Ri.ld, 1.0,
                   near ? qil.as<uint16_t>() : nullptr, B->buf.as<float>(), B->x16.as<uint16_t>(),
-                  GEMM_B_UPPER | (near ? GEMM_FAST_ACC : 0));  // near: a ~1e-4-sized correction
+                  GEMM_B_UPPER | (near ? GEMM_FAST_ACC | GEMM_HI_ONLY : 0));  // near: a ≲1e-4-sized correction
     B->rank = cc;
     if (keep_rinv) {
         B->rinv1 = std::move(R1i);
@@ -568,9 +607,10 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
     // Grams: upper triangles only (every consumer — Cholesky, max|G−I|, I−F — reads the upper)
     gemm(c, OP_T, OP_N, cc, cc, rows, 1.0, C, cdt, rows, C, cdt, rows, 0.0, G.p(), G.ld, GEMM_SYM_UPPER);
     if (dist) allreduce(c, G.p(), cc * cc);
-    const CholInfo ci = chol_any(c, G.p(), cc, G.ld, R.p(), Ri.p(), false, false);
-    const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
-    if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
+    // one read for the factorization's status and ‖Q1ᵀQ1 − I‖ (Q1 and its Gram speculative, as
+    // cholqr2_whole_h3)
+    CholStat hs1{};
+    chol_later(c, G.p(), cc, G.ld, R.p(), Ri.p(), false, false, &hs1);
     gemm(c, OP_N, OP_N, rows, cc, cc, 1.0, C, cdt, rows, Ri.p(), BCUR_F64, Ri.ld, 0.0, Q1.p(), Q1.ld,
          GEMM_B_UPPER);
     // Q1 in the basis dtype (fp32 → every later product with it runs on the tensor cores)
@@ -589,7 +629,11 @@ static bool cholqr2_whole(Ctx* c, const void* C, int cdt, int64_t rows, int64_t 
     Mat64 dev(c, 1, 1);
     max_dev_identity(c, G.p(), cc, G.ld, dev.p());
     double hdev = 1.0;
-    d2h(c, &hdev, dev.p(), 1);
+    d2h_later(c, &hdev, dev.p(), 1);
+    c->read_all();
+    const CholInfo ci = chol_info(hs1);
+    const double ref = std::sqrt(std::max(ci.maxdiag, 0.0));
+    if (!(ci.info == 0 && std::isfinite(ci.mindiag) && ci.mindiag > tau_chol(dt) * ref)) return false;
     const bool near = hdev < 1e-4;
     if (near) {
         // fp32: Q = Q1 + Q1·(−F) — the product is a ~1e-7-sized correction, so one rounded TF32
@@ -637,7 +681,7 @@ static void a_product(Ctx* c, const DMat* a, const RoundedA* ra, bool trans, int
 // false when a device-side CholQR test failed — the caller then reruns with fast = false
 // (orth's CholQR2 / SVQB paths, identical to the oracle's).
 static bool range_finder_impl(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
-                              bool rank_floor, const RoundedA* ra, bool fast) {
+                              bool rank_floor, const RoundedA* ra, bool fast, const std::function<void()>* after_read) {
     const int64_t m = a->m, nl = a->n;
     const int64_t ng = a->n_global > 0 ? a->n_global : a->n;
     const int64_t l = std::min(k + p, std::min(m, ng));
@@ -675,10 +719,12 @@ static bool range_finder_impl(Ctx* c, const DMat* a, int64_t k, int64_t p, int64
     allreduce(c, Gb.p(), r * r);
     sym_eig(c, Gb.p(), r, Gb.ld, lam.p(), Ut.p());
     int hflag = 0;
-    if (fast) CUDA_CHECK(cudaMemcpyAsync(&hflag, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     std::vector<double> lh(r);
-    d2h(c, lh.data(), lam.p(), r);  // (synchronizes the stream: hflag is valid)
-    if (hflag) return false;         // a failed CholQR test: Q (and everything after) is unusable
+    if (fast) d2h_later(c, &hflag, flag.as<int>(), 1);
+    d2h_later(c, lh.data(), lam.p(), r);
+    c->read_all();  // (also delivers the caller's earlier reads, which after_read checks)
+    if (after_read && *after_read) (*after_read)();
+    if (hflag) return false;  // a failed CholQR test: Q (and everything after) is unusable
     std::vector<double> sg(r);
     for (int64_t i = 0; i < r; ++i) sg[i] = std::sqrt(std::max(lh[i], 0.0));
     if (!(sg[0] > 0.0)) fail(BCUR_E_ZERO_MATRIX, "range_finder: A is identically zero");
@@ -703,7 +749,7 @@ static bool range_finder_impl(Ctx* c, const DMat* a, int64_t k, int64_t p, int64
     gemm(c, OP_N, OP_N, r, ke, r, 1.0, Gb.p(), BCUR_F64, Gb.ld, Wm.p(), BCUR_F64, Wm.ld, 0.0, T1.p(), T1.ld);
     gemm(c, OP_T, OP_N, ke, ke, r, 1.0, Wm.p(), BCUR_F64, Wm.ld, T1.p(), BCUR_F64, T1.ld, 0.0, Vg.p(), Vg.ld);
     max_dev_identity(c, Vg.p(), ke, Vg.ld, dev.p());
-    d2h(c, &out->orth_dev, dev.p(), 1);
+    d2h_later(c, &out->orth_dev, dev.p(), 1);  // delivered by the caller's next read_all()
     out->k_eff = ke;
     out->l = l;
     out->sigma.assign(sg.begin(), sg.begin() + rank);
@@ -711,12 +757,16 @@ static bool range_finder_impl(Ctx* c, const DMat* a, int64_t k, int64_t p, int64
 }
 
 void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
-                  bool rank_floor, const RoundedA* ra) {
+                  bool rank_floor, const RoundedA* ra, const std::function<void()>* after_read, bool defer) {
     if (k < 1) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: k must be >= 1");
     if (p < 0 || q < 0) fail(BCUR_E_INVALID_ARGUMENT, "range_finder: p and q must be >= 0");
     static const bool no_fast = getenv("BCUR_RF_SAFE") != nullptr;  // experiments: orth everywhere
-    if (!no_fast && range_finder_impl(c, a, k, p, q, key, out, rank_floor, ra, true)) return;
-    range_finder_impl(c, a, k, p, q, key, out, rank_floor, ra, false);
+    if (no_fast || !range_finder_impl(c, a, k, p, q, key, out, rank_floor, ra, true, after_read)) {
+        c->read_all();
+        if (after_read && *after_read) (*after_read)();
+        range_finder_impl(c, a, k, p, q, key, out, rank_floor, ra, false, nullptr);
+    }
+    if (!defer) c->read_all();  // out->orth_dev
 }
 
 // ------------------------------------------------------------- helpers
@@ -898,8 +948,18 @@ static KnownCols known_columns(Ctx* c, const DMat* a, const Shard& s, const Basi
 
 // Σ_g ‖Qᵀ A_g‖² (shard-local per-block values in d_blk_local, allreduced total); with `known`,
 // the skipped blocks contribute their exact ‖A_g‖² to the total (not to d_blk_local)
+static void projected_mass_later(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local,
+                                 const RoundedA* ra, const KnownCols* known, double* h2);
 static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local,
                              const RoundedA* ra = nullptr, const KnownCols* known = nullptr) {
+    double h[2] = {0.0, 0.0};
+    projected_mass_later(c, a, s, B, d_blk_local, ra, known, h);
+    c->read_all();
+    return h[0] + h[1];
+}
+// the same, its two parts {Σ‖QᵀA_g‖² computed, known mass} delivered into h2 by c->read_all()
+static void projected_mass_later(Ctx* c, const DMat* a, const Shard& s, const Basis& B, double* d_blk_local,
+                                 const RoundedA* ra, const KnownCols* known, double* h2) {
     const int64_t nl = a->n;
     Mat64 rows(c, nl, 1), tot(c, 1, 1);
     const bool kn = known && known->active();
@@ -910,11 +970,9 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
     segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, b);
     sum_vector(c, b, s.g1 - s.g0, tot2.p());
     const double km = kn ? known->mass : 0.0;
-    CUDA_CHECK(cudaMemcpyAsync(tot2.p() + 1, &km, sizeof km, cudaMemcpyHostToDevice, c->stream));
+    h2d(c, tot2.p() + 1, &km, 1);
     allreduce(c, tot2.p(), 2);
-    double h[2] = {0.0, 0.0};
-    d2h(c, h, tot2.p(), 2);  // (synchronizes: km is still in scope)
-    return h[0] + h[1];
+    d2h_later(c, h2, tot2.p(), 2);
 }
 
 // First-order correction of the row-Σ² pass's fp16 basis copy along the sketch's top-k
@@ -925,9 +983,11 @@ static double projected_mass(Ctx* c, const DMat* a, const Shard& s, const Basis&
 // finder (A ≈ U_kΣ_kV_kᵀ + the rest),  Σ_k σ_k²(‖Qᵀu_k‖² − ‖Q̃ᵀu_k‖²)  restores those
 // directions; what remains is spread over many directions and averages out (~1e-7).  Two
 // thin DMMA products (r × k).
-static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub, const KnownCols* known = nullptr) {
+// h2 (delivered by c->read_all()): {‖W_hi + W_lo‖², ‖W_hi‖²}, the correction is h2[0] − h2[1];
+// both stay 0 when there is nothing to correct
+static void sketch_correction_later(Ctx* c, const Basis& B, const Subspace& sub, const KnownCols* known, double* h2) {
     const int64_t m = B.rows, r = B.rank, ke = sub.k_eff;
-    if (r <= 0 || ke <= 0 || !B.x16.ptr || B.dt != BCUR_F32 || !h3_ok(m)) return 0.0;
+    if (r <= 0 || ke <= 0 || !B.x16.ptr || B.dt != BCUR_F32 || !h3_ok(m)) return;
     // W_hi = (UΣ)ᵀQ̃ and W_lo = (UΣ)ᵀΔ from the two parts of the basis's fp16 split (Q̃ = hi,
     // Δ = lo, Q = Q̃ + Δ to 22 bits): 3×FP16 products with UΣ split once, reading only the
     // 2-byte parts — no fp32 copy of Q̃ and no pass over the fp32 Q:
@@ -961,9 +1021,7 @@ static double sketch_correction(Ctx* c, const Basis& B, const Subspace& sub, con
     axpy_neg(c, blk[1], blk[2], ke * r);
     sumsq_vector(c, blk[2], ke * r, tot.p());  // the blocks are contiguous (ld = ke)
     sumsq_vector(c, blk[0], ke * r, tot.p() + 1);
-    double h[2] = {0.0, 0.0};
-    d2h(c, h, tot.p(), 2);
-    return h[0] - h[1];
+    d2h_later(c, h2, tot.p(), 2);
 }
 
 // ‖A − Q Qᵀ A‖² (streamed: X = QᵀA, then Σ (A − Q X)² tile by tile; blockcur.cpp:46's
@@ -1007,8 +1065,18 @@ static double explicit_residual(Ctx* c, const DMat* a, const Basis& B, const Rou
 }
 
 // global per-block ‖A_g‖² (host copy) and ‖A‖²
+static void block_norms_later(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global,
+                              double* a2, RoundedA* ra = nullptr, bool with_lo = true);
 static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global,
                           RoundedA* ra = nullptr, bool with_lo = true) {
+    double h = 0.0;
+    block_norms_later(c, a, s, bn2, d_global, &h, ra, with_lo);
+    c->read_all();
+    return h;
+}
+// the same, *bn2 and *a2 delivered by c->read_all()
+static void block_norms_later(Ctx* c, const DMat* a, const Shard& s, std::vector<double>* bn2, Mat64* d_global,
+                              double* a2, RoundedA* ra, bool with_lo) {
     Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1);
     *d_global = Mat64(c, s.G, 1);
     if (ra) make_rounded(c, a, ra, with_lo);
@@ -1019,13 +1087,9 @@ static double block_norms(Ctx* c, const DMat* a, const Shard& s, std::vector<dou
     gather_blocks_vec(c, s, loc.p(), d_global->p());
     Mat64 tot(c, 1, 1);
     sum_vector(c, d_global->p(), s.G, tot.p());
-    // both reads in one round trip
     bn2->assign(s.G, 0.0);
-    double h = 0.0;
-    CUDA_CHECK(cudaMemcpyAsync(bn2->data(), d_global->p(), s.G * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_CHECK(cudaMemcpyAsync(&h, tot.p(), sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
-    return h;
+    d2h_later(c, bn2->data(), d_global->p(), s.G);
+    d2h_later(c, a2, tot.p(), 1);
 }
 
 // scores (global G, device) from the shard-local rows of V
@@ -1042,16 +1106,17 @@ static void draw_on_device(Ctx* c, const double* d_scores, int64_t G, int64_t g,
     h2d(c, du.p(), uniforms, g);
     distribution_draw(c, d_scores, G, 1, g, mode, du.p(), dd.as<bcur_block_draw>(), dm.p(), st.as<int>());
     int status = 0;
-    d2h(c, &status, st.as<int>(), 1);
+    draws->resize(g);
+    margins->resize(g);
+    d2h_later(c, &status, st.as<int>(), 1);
+    d2h_later(c, draws->data(), dd.as<bcur_block_draw>(), g);
+    d2h_later(c, margins->data(), dm.p(), g);
+    c->read_all();  // (with the caller's pending reads)
     if (status == BCUR_E_ZERO_MATRIX) fail(BCUR_E_ZERO_MATRIX, "ScoreVector::distribution: scores sum to zero");
     if (status == BCUR_E_DISTRIBUTION_INVALID) fail(BCUR_E_DISTRIBUTION_INVALID, "draw_blocks: invalid distribution");
     if (status == BCUR_E_NOT_ENOUGH_BLOCKS)
         fail(BCUR_E_NOT_ENOUGH_BLOCKS, "draw_blocks: more distinct blocks requested than have positive probability");
     if (status != BCUR_OK) fail(BCUR_E_CUDA, "draw_blocks: kernel status " + std::to_string(status));
-    draws->resize(g);
-    margins->resize(g);
-    d2h(c, draws->data(), dd.as<bcur_block_draw>(), g);
-    d2h(c, margins->data(), dm.p(), g);
 }
 
 // ------------------------------------------------------------- block CSS
@@ -1059,22 +1124,28 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
                CssOut* out) {
     if (o.k < 1) fail(BCUR_E_INVALID_ARGUMENT, "block_css: k must be >= 1");
     if (o.g < 1) fail(BCUR_E_INVALID_ARGUMENT, "draw_blocks: g must be >= 1");
+    // Host round trips: the range finder's eigenvalues (which also deliver ‖A‖² and the block
+    // norms), the draws (with the scores and orth_dev), the basis path decision, the residual.
+    ReadScope rs(c);
     std::unique_ptr<ProfScope> ph(new ProfScope(c, "phase:1 norms", 0, 0));
     Shard s = shard_of(a, offsets, G);
     std::vector<double> bn2;
     Mat64 dbn;
     RoundedA ra;
-    const double a2 = block_norms(c, a, s, &bn2, &dbn, &ra);
-    if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_css: matrix contains NaN or Inf");  // require_finite
-    if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
+    double a2 = 0.0;
+    block_norms_later(c, a, s, &bn2, &dbn, &a2, &ra);
+    const std::function<void()> check_a = [&]() {
+        if (!std::isfinite(a2)) fail(BCUR_E_INVALID_ARGUMENT, "block_css: matrix contains NaN or Inf");  // require_finite
+        if (!(a2 > 0.0)) fail(BCUR_E_ZERO_MATRIX, "block_css: A is identically zero");
+    };
     ph.reset(new ProfScope(c, "phase:2 range_finder", 0, 0));
     Subspace sub;
-    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, o.rank_floor != 0, &ra);
+    range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, o.rank_floor != 0, &ra, &check_a, true);
     ph.reset(new ProfScope(c, "phase:3 scores+draw", 0, 0));
     Mat64 sc(c, G, 1);
     block_scores(c, s, sub.v, a->n, sc.p());
     out->scores.resize(G);
-    d2h(c, out->scores.data(), sc.p(), G);
+    d2h_later(c, out->scores.data(), sc.p(), G);
     out->normalizer = (double)sub.k_eff;
     draw_on_device(c, sc.p(), G, o.g, o.mode, uniforms, &out->draws, &out->margins);
     std::vector<int64_t> blocks;
@@ -1086,8 +1157,11 @@ void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const b
     double res2 = 0.0;
     if (o.residual != BCUR_RESID_EXPLICIT) {  // Pythagoras first (AUTO falls back to explicit when small)
         const KnownCols known = known_columns(c, a, s, B, unique_in_order(blocks), bn2, &ra);
-        res2 = a2 - projected_mass(c, a, s, B, nullptr, &ra, &known);
-        if (ra.ok() && B.x16.ptr) res2 -= sketch_correction(c, B, sub, &known);
+        double pm[2] = {0.0, 0.0}, sk[2] = {0.0, 0.0};  // one read for the pass and its correction
+        projected_mass_later(c, a, s, B, nullptr, &ra, &known, pm);
+        if (ra.ok() && B.x16.ptr) sketch_correction_later(c, B, sub, &known, sk);
+        c->read_all();
+        res2 = a2 - (pm[0] + pm[1]) - (sk[0] - sk[1]);
     }
     ph.reset();
     int path = 0;

@@ -1,5 +1,6 @@
 // pipeline.h — hot-path orchestration (pipeline.cu) used by the C ABI (capi.cu).
 #pragma once
+#include <functional>
 
 #include <vector>
 
@@ -82,9 +83,12 @@ int cholesky_inverse(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R,
 void allreduce(Ctx* c, double* d, int64_t count);
 int64_t orth(Ctx* c, const double* X, int64_t rows, int64_t w, int64_t ldx, double ref, int dt, double* Q,
              int64_t ldq, bool dist, Mat64* T_out, int* path_out);
+// after_read (nullable): run right after the first stream synchronization (the caller's
+// deferred reads — e.g. ‖A‖² — are then delivered and can be checked before any of the range
+// finder's own decisions); defer: out->orth_dev is delivered by the caller's next read_all()
 void range_finder(Ctx* c, const DMat* a, int64_t k, int64_t p, int64_t q, uint64_t key, Subspace* out,
-                  bool rank_floor,
-                  const RoundedA* ra = nullptr);
+                  bool rank_floor, const RoundedA* ra = nullptr, const std::function<void()>* after_read = nullptr,
+                  bool defer = false);
 void block_css(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, const double* uniforms,
                CssOut* out);
 void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, const bcur_options& o, GreedyOut* out);

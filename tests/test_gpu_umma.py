@@ -182,3 +182,17 @@ def test_h3_fast_acc(B, m, n, N, upper):
     assert rel_fro(fast, ref) < 5e-6
     # the bias is systematic (toward zero) but bounded by the accumulation count per chunk
     assert abs(np.sum(fast * ref) / np.sum(ref * ref) - 1.0) < 3e-6
+
+
+@pytest.mark.parametrize("m,n,N", [(8192, 640, 1100)])
+def test_h3_hi_only_correction(B, m, n, N):
+    """GEMM_HI_ONLY (k_umma2_h3m, one MMA: a_hi·x_hi): the CholQR2 second pass's correction
+    Q1·(−F) with ‖F‖ ~ 1e-4.  The product alone is 2⁻¹¹-relative; added to Q1 (the basis
+    epilogue), its error is ≲ 1e-7 of the result."""
+    gen = np.random.default_rng(m + n + N + 1)
+    a = np.asfortranarray(gen.standard_normal((m, n)).astype(np.float32))
+    x = np.asfortranarray(np.triu(gen.standard_normal((n, N))))
+    ref = a.astype(np.float64) @ x
+    hi = B.structured_product(a, x, x_upper=True, h3=True, fast_acc=True, hi_only=True)
+    err = rel_fro(hi, ref)
+    assert 1e-5 < err < 1e-3  # one fp16 MMA: well above the 3×FP16 error, below 2⁻¹⁰
