@@ -598,12 +598,17 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     }
     // eigenvalues descending: rank by counting (ties keep index order), one thread per entry
     __shared__ int order[512];
+    // (a total order even for NaN input — NaNs rank last, among themselves by index — so `order`
+    // is always a permutation: the caller's finiteness verdict arrives after this kernel ran)
     for (int j = threadIdx.x; j < w; j += NT) {
         const double lj = Ap[tri_at(j, j)];
+        const bool nj = lj != lj;
         int rank = 0;
         for (int i = 0; i < w; ++i) {
             const double li = Ap[tri_at(i, i)];
-            rank += (li > lj || (li == lj && i < j)) ? 1 : 0;
+            const bool ni = li != li;
+            const bool before = ni ? (nj && i < j) : (nj || li > lj || (li == lj && i < j));
+            rank += before ? 1 : 0;
         }
         order[rank] = j;
     }

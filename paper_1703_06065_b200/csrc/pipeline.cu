@@ -230,6 +230,51 @@ static void chol_enqueue(Ctx* c, const double* G, int64_t w, int64_t ldg, double
     // BCUR_CHOL_REC=1 for experiments, take the launch-per-product recursion below; at w = 200
     // both take ~0.17 ms, c1's C basis, profiles/r02af)
     static const bool rec = getenv("BCUR_CHOL_REC") != nullptr;
+    // Wide fp32-class Grams: one level of the recursion around two persistent launches.  The
+    // persistent kernel's cost is its serial chain (~80 µs per 128 columns up to w = 2048, ~107 µs
+    // at 4096 where the DMMA bulk outgrows the FACT window: profiles/r02x/chol_bench.log), so the
+    // two half-width chains cost what the whole one does and the off-diagonal quarter — three
+    // quarters of the bulk flops — moves to four tcgen05 3×FP16 products (~0.05 ms each).
+    static const int64_t hyb_min = getenv("BCUR_CHOL_HYBRID") ? atoll(getenv("BCUR_CHOL_HYBRID")) : 3072;
+    if (!rec && w % 2 == 0 && tc && hyb_min > 0 && w >= hyb_min) {
+        const int64_t n1 = ((w + 127) / 128 + 1) / 2 * 128, n2 = w - n1;
+        Mat64 W(c, w, w), Xs(c, n1, n1), Rs;
+        if (want_r) Rs = Mat64(c, n1, n1);
+        copy_f64(c, G, w, w, ldg, W.p(), w);
+        CUDA_CHECK(cudaMemsetAsync(R, 0, (size_t)w * w * sizeof(double), c->stream));
+        CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)w * w * sizeof(double), c->stream));
+        cudaStream_t main_s = c->stream, side_s = c->side_stream();
+        c->order(main_s, side_s, 0);
+        CholRec S{c, W.p(), R, X, w, st, main_s, side_s, true, want_r};
+        auto at = [&](double* p, int64_t i, int64_t j) { return p + i + j * w; };
+        // a diagonal half: the persistent kernel works on compact n × n outputs (ld n)
+        auto half = [&](int64_t o, int64_t n) {
+            if (!want_r) Rs = Mat64(c, n, n);  // (R's off-diagonal 128-blocks still land here; not read)
+            chol_persistent(c, at(W.p(), o, o), n, w, Rs.p(), Xs.p(), st, want_r);
+            CUDA_CHECK(cudaMemcpy2DAsync(at(X, o, o), w * sizeof(double), Xs.p(), n * sizeof(double), n * sizeof(double),
+                                         n, cudaMemcpyDeviceToDevice, c->stream));
+            if (want_r)
+                CUDA_CHECK(cudaMemcpy2DAsync(at(R, o, o), w * sizeof(double), Rs.p(), n * sizeof(double),
+                                             n * sizeof(double), n, cudaMemcpyDeviceToDevice, c->stream));
+        };
+        half(0, n1);
+        rec_gemm(S, true, OP_T, n1, n2, n1, 1.0, at(X, 0, 0), at(W.p(), 0, n1), 0.0, at(R, 0, n1), GEMM_A_LOWER);
+        const cudaEvent_t e_r12 = c->sync_event(S.ev++), e_t = c->sync_event(S.ev++);
+        CUDA_CHECK(cudaEventRecord(e_r12, main_s));
+        CUDA_CHECK(cudaStreamWaitEvent(side_s, e_r12, 0));
+        c->waited(main_s, side_s);
+        c->stream = side_s;  // T = X11·R12 into G12's place, beside the G22 branch
+        rec_gemm(S, true, OP_N, n1, n2, n1, 1.0, at(X, 0, 0), at(R, 0, n1), 0.0, at(W.p(), 0, n1), GEMM_A_UPPER);
+        CUDA_CHECK(cudaEventRecord(e_t, side_s));
+        c->stream = main_s;
+        rec_gemm(S, true, OP_T, n2, n2, n1, -1.0, at(R, 0, n1), at(R, 0, n1), 1.0, at(W.p(), n1, n1), GEMM_SYM_UPPER);
+        half(n1, n2);
+        CUDA_CHECK(cudaStreamWaitEvent(main_s, e_t, 0));
+        c->waited(side_s, main_s);
+        rec_gemm(S, true, OP_N, n1, n2, n2, -1.0, at(W.p(), 0, n1), at(X, n1, n1), 0.0, at(X, 0, n1), GEMM_B_UPPER);
+        c->order(side_s, main_s, 1);
+        return;
+    }
     if (!rec && w % 2 == 0) {
         chol_persistent(c, G, w, ldg, R, X, st, want_r);
         return;

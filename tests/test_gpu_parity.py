@@ -202,6 +202,16 @@ def test_errors(B):
             B.block_css(a, part, 2, 2, B.Rng(0))
         with pytest.raises(ValueError):
             B.greedy_select(a, part, 2, 2, seed=0)
+        # block_css reads its finiteness verdict after the range finder has run (one host round
+        # trip for both): every kernel before that read must survive NaN / Inf data — the packed
+        # Jacobi's eigenvalue ranking did not (profiles/r02al) — also on the tcgen05 fp32 path
+        big = np.random.default_rng(2).standard_normal((512, 4096)).astype(np.float32)
+        big[7, 300] = bad
+        with pytest.raises(ValueError):
+            B.block_css(big, B.BlockPartition.equal_blocks(4096, 128), 20, 6, B.Rng(0), p=10, q=1)
+    # the context is still usable afterwards
+    ok = B.block_css(np.random.default_rng(3).standard_normal((10, 40)), part, 2, 2, B.Rng(0))
+    assert np.isfinite(ok.projection_error)
 
 
 def test_bitwise_rerun_determinism(B):
