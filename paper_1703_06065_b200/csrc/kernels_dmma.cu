@@ -39,10 +39,13 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // [m][k] when transposed; op(B) is [n][k] when B is K-major (TRB = 0) and [k][n] otherwise.
 // Pitches make the DMMA fragment loads conflict-free: [·][k] rows hold 16 k + 4 pad (20 ≡ 4 mod
 // 16 doubles / ≡ 20 mod 32 floats), [k][·] rows 64 + 4 doubles or 64 + 8 floats.
-template <typename T, bool KMAJOR>
+// ROWS: the tile's extent along M (64) or N (the kernel's NB: 64, or 16 for thin outputs — an
+// N = 15 sketch product on a 64-wide tile spent three quarters of its DMMAs on zero columns,
+// and the DMMA pipe, one m8n8k4 per 4 clocks per SM, was what bound it: profiles/r02ae)
+template <typename T, bool KMAJOR, int ROWS = 64>
 struct DTile {
-    static constexpr int P = KMAJOR ? (DBK + 4) : (64 + (sizeof(T) == 8 ? 4 : 8));
-    static constexpr int ELEMS = KMAJOR ? 64 * P : DBK * P;
+    static constexpr int P = KMAJOR ? (DBK + 4) : (ROWS + (sizeof(T) == 8 ? 4 : 8));
+    static constexpr int ELEMS = KMAJOR ? ROWS * P : DBK * P;
 };
 constexpr int DSTAGES = 4;
 
@@ -55,42 +58,44 @@ __device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem, int 
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s), "l"(gmem), "r"(src) : "memory");
 }
 
-template <typename TA, typename TB, int TRA, int TRB, int EPI>
+template <typename TA, typename TB, int TRA, int TRB, int EPI, int NB = DBN>
 __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
                                                const TA* __restrict__ A, int64_t lda, const TB* __restrict__ B,
                                                int64_t ldb, double beta, double* __restrict__ C, int64_t ldc,
                                                double* __restrict__ partial, const void* __restrict__ D, int dtd,
                                                int64_t ldd, int flags) {
     using TLA = DTile<TA, TRA == 1>;
-    using TLB = DTile<TB, TRB == 0>;
+    using TLB = DTile<TB, TRB == 0, NB>;
+    // warps: 2 × 2 of 32 × 32 (NB = 64) or 4 × 1 of 16 × 16 (NB = 16)
+    constexpr int WN = NB == 64 ? 2 : 1, WM = 4 / WN, MI = DBM / WM / 8, NJ = NB / WN / 8;
     extern __shared__ __align__(16) unsigned char dsm[];
     TA* As = reinterpret_cast<TA*>(dsm);
     TB* Bs = reinterpret_cast<TB*>(dsm + (size_t)DSTAGES * TLA::ELEMS * sizeof(TA));
     __shared__ double red[2][DBM];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = warp % WM, wn = warp / WM;
     // triangular operands: the tiles with the longest K range are scheduled first (the block
     // scheduler dispatches in blockIdx order; the last wave should hold the short tiles)
     const int64_t bx = (flags & ops::GEMM_A_LOWER) ? gridDim.x - 1 - blockIdx.x : blockIdx.x;
     const int64_t by = (flags & ops::GEMM_B_UPPER) ? gridDim.y - 1 - blockIdx.y : blockIdx.y;
-    const int64_t m0 = bx * DBM, n0 = by * DBN;
+    const int64_t m0 = bx * DBM, n0 = by * NB;
     const bool split = partial != nullptr && EPI == DEPI_STORE;
     // a symmetric product of which only the upper triangle is consumed: tiles strictly
     // below the diagonal are not computed (zeros into their split-K partials)
-    const bool skip = (flags & ops::GEMM_SYM_UPPER) && m0 >= n0 + DBN;
+    const bool skip = (flags & ops::GEMM_SYM_UPPER) && m0 >= n0 + NB;
     if (skip && !split) return;
     int64_t kbeg = (int64_t)blockIdx.z * kchunk, kend = min(K, kbeg + kchunk);
     if (flags & ops::GEMM_A_UPPER) kbeg = max(kbeg, m0 / DBK * DBK);   // op(A)[i,k] = 0 for k < i
     if (flags & ops::GEMM_A_LOWER) kend = min(kend, m0 + DBM);         // op(A)[i,k] = 0 for k > i
-    if (flags & ops::GEMM_B_UPPER) kend = min(kend, n0 + DBN);         // op(B)[k,j] = 0 for k > j
+    if (flags & ops::GEMM_B_UPPER) kend = min(kend, n0 + NB);         // op(B)[k,j] = 0 for k > j
     if (flags & ops::GEMM_B_LOWER) kbeg = max(kbeg, n0 / DBK * DBK);   // op(B)[k,j] = 0 for k < j
     if (skip) kend = kbeg;
 
-    double acc[4][4][2];
+    double acc[MI][NJ][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     // one stage: op(A) (DBM × DBK) and op(B) (DBK × DBN), 1024 elements each = 8 cp.async per
     // thread and operand, the thread map following the stored contiguous direction (coalesced)
@@ -107,9 +112,9 @@ __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, 
             cp_async_elem(TRA == 0 ? as + kk * TLA::P + i : as + i * TLA::P + kk, src, (int)sizeof(TA), v);
         }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < NB / 8; ++r) {
             int j, kk;
-            if (TRB == 0) { kk = tid & 15; j = (tid >> 4) + 8 * r; } else { j = tid & 63; kk = (tid >> 6) + 2 * r; }
+            if (TRB == 0) { kk = tid & 15; j = (tid >> 4) + 8 * r; } else { j = tid & (NB - 1); kk = tid / NB + (DNT / NB) * r; }
             const int64_t gj = n0 + j, gk = k0 + kk;
             const bool v = gj < N && gk < kend;
             const TB* src = B + (v ? (TRB == 0 ? gk + gj * ldb : gj + gk * ldb) : 0);
@@ -134,21 +139,21 @@ __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, 
             const TB* bs = Bs + (kt % DSTAGES) * TLB::ELEMS;
 #pragma unroll
             for (int k4 = 0; k4 < DBK; k4 += 4) {
-                double af[4], bf[4];
+                double af[MI], bf[NJ];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const int mm = wm * 32 + i * 8 + fm;
+                for (int i = 0; i < MI; ++i) {
+                    const int mm = wm * (MI * 8) + i * 8 + fm;
                     af[i] = (double)(TRA == 0 ? as[(k4 + fk) * TLA::P + mm] : as[mm * TLA::P + k4 + fk]);
                 }
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int nn = wn * 32 + j * 8 + fm;
+                for (int j = 0; j < NJ; ++j) {
+                    const int nn = wn * (NJ * 8) + j * 8 + fm;
                     bf[j] = (double)(TRB == 0 ? bs[nn * TLB::P + k4 + fk] : bs[(k4 + fk) * TLB::P + nn]);
                 }
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+                for (int i = 0; i < MI; ++i)
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+                    for (int j = 0; j < NJ; ++j) dmma(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
             }
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -158,14 +163,14 @@ __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, 
     const int er = lane >> 2, ec = 2 * (lane & 3);
     if (EPI == DEPI_STORE) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t gi = m0 + wm * 32 + i * 8 + er;
+        for (int i = 0; i < MI; ++i) {
+            const int64_t gi = m0 + wm * (MI * 8) + i * 8 + er;
             if (gi >= M) continue;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < NJ; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int64_t gj = n0 + wn * 32 + j * 8 + ec + h;
+                    const int64_t gj = n0 + wn * (NJ * 8) + j * 8 + ec + h;
                     if (gj >= N) continue;
                     if (split) {
                         partial[(int64_t)blockIdx.z * M * N + gi + gj * M] = acc[i][j][h];
@@ -178,30 +183,30 @@ __global__ void __launch_bounds__(DNT) k_dgemm(int64_t M, int64_t N, int64_t K, 
     } else if (EPI == DEPI_ROWSQ) {
         // out-of-range columns hold exact zeros (zero-filled operands)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < MI; ++i) {
             double s = 0.0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) s = fma(acc[i][j][0], acc[i][j][0], fma(acc[i][j][1], acc[i][j][1], s));
+            for (int j = 0; j < NJ; ++j) s = fma(acc[i][j][0], acc[i][j][0], fma(acc[i][j][1], acc[i][j][1], s));
             s += __shfl_xor_sync(0xffffffffu, s, 1);
             s += __shfl_xor_sync(0xffffffffu, s, 2);
-            if ((lane & 3) == 0) red[wn][wm * 32 + i * 8 + er] = s;
+            if ((lane & 3) == 0) red[wn][wm * (MI * 8) + i * 8 + er] = s;
         }
         __syncthreads();
         for (int i = tid; i < DBM; i += DNT) {
             const int64_t gi = m0 + i;
-            if (gi < M) partial[(int64_t)blockIdx.y * M + gi] = red[0][i] + red[1][i];
+            if (gi < M) partial[(int64_t)blockIdx.y * M + gi] = WN == 2 ? red[0][i] + red[1][i] : red[0][i];
         }
     } else {  // DEPI_RESID
         double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int64_t gi = m0 + wm * 32 + i * 8 + er;
+        for (int i = 0; i < MI; ++i) {
+            const int64_t gi = m0 + wm * (MI * 8) + i * 8 + er;
             if (gi >= M) continue;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < NJ; ++j)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int64_t gj = n0 + wn * 32 + j * 8 + ec + h;
+                    const int64_t gj = n0 + wn * (NJ * 8) + j * 8 + ec + h;
                     if (gj >= N) continue;
                     const double d = dtd == BCUR_F32 ? (double)((const float*)D)[gi + gj * ldd]
                                                      : ((const double*)D)[gi + gj * ldd];
@@ -258,27 +263,26 @@ __global__ void k_dsum_rows(int64_t M, int tiles, const double* __restrict__ par
     out[i] = s;
 }
 
-template <typename TA, typename TB, int TRA, int TRB, int EPI>
+template <typename TA, typename TB, int TRA, int TRB, int NB>
 size_t dgemm_smem() {
-    return (size_t)DSTAGES * (DTile<TA, TRA == 1>::ELEMS * sizeof(TA) + DTile<TB, TRB == 0>::ELEMS * sizeof(TB));
+    return (size_t)DSTAGES * (DTile<TA, TRA == 1>::ELEMS * sizeof(TA) + DTile<TB, TRB == 0, NB>::ELEMS * sizeof(TB));
 }
 
-template <typename TA, typename TB, int EPI>
+template <typename TA, typename TB, int EPI, int NB = DBN>
 void dlaunch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, int64_t K, int64_t kchunk, double alpha,
              const void* A, int64_t lda, const void* B, int64_t ldb, double beta, double* C, int64_t ldc,
              double* partial, const void* D, int dtd, int64_t ldd, int flags) {
 #define BCUR_DGEMM_CASE(TRA, TRB)                                                                                  \
     do {                                                                                                           \
         static bool attr = false;                                                                                  \
-        const size_t sm = dgemm_smem<TA, TB, TRA, TRB, EPI>();                                                     \
+        const size_t sm = dgemm_smem<TA, TB, TRA, TRB, NB>();                                                      \
         if (!attr) {                                                                                               \
-            CUDA_CHECK(cudaFuncSetAttribute(k_dgemm<TA, TB, TRA, TRB, EPI>,                                        \
+            CUDA_CHECK(cudaFuncSetAttribute(k_dgemm<TA, TB, TRA, TRB, EPI, NB>,                                    \
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));                \
             attr = true;                                                                                           \
         }                                                                                                          \
-        k_dgemm<TA, TB, TRA, TRB, EPI><<<grid, DNT, sm, c->stream>>>(M, N, K, kchunk, alpha, (const TA*)A, lda,    \
-                                                                      (const TB*)B, ldb, beta, C, ldc, partial, D, \
-                                                                      dtd, ldd, flags);                            \
+        k_dgemm<TA, TB, TRA, TRB, EPI, NB><<<grid, DNT, sm, c->stream>>>(                                          \
+            M, N, K, kchunk, alpha, (const TA*)A, lda, (const TB*)B, ldb, beta, C, ldc, partial, D, dtd, ldd, flags); \
     } while (0)
     if (ta == ops::OP_N && tb == ops::OP_N) BCUR_DGEMM_CASE(0, 0);
     else if (ta == ops::OP_N && tb == ops::OP_T) BCUR_DGEMM_CASE(0, 1);
@@ -288,21 +292,21 @@ void dlaunch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, in
     LAUNCH_CHECK(c);
 }
 
-template <int EPI>
+template <int EPI, int NB = DBN>
 void ddispatch(Ctx* c, ops::Op ta, ops::Op tb, dim3 grid, int64_t M, int64_t N, int64_t K, int64_t kchunk,
                double alpha, const void* A, int dta, int64_t lda, const void* B, int dtb, int64_t ldb, double beta,
                double* C, int64_t ldc, double* partial, const void* D, int dtd, int64_t ldd, int flags) {
     if (dta == BCUR_F32 && dtb == BCUR_F32)
-        dlaunch<float, float, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
+        dlaunch<float, float, EPI, NB>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
                                    dtd, ldd, flags);
     else if (dta == BCUR_F32)
-        dlaunch<float, double, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
+        dlaunch<float, double, EPI, NB>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
                                     dtd, ldd, flags);
     else if (dtb == BCUR_F32)
-        dlaunch<double, float, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
+        dlaunch<double, float, EPI, NB>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial, D,
                                     dtd, ldd, flags);
     else
-        dlaunch<double, double, EPI>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial,
+        dlaunch<double, double, EPI, NB>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, partial,
                                      D, dtd, ldd, flags);
 }
 
@@ -960,7 +964,9 @@ namespace ops {
 static int dgemm_splits(const Ctx* c, int64_t tiles, int64_t K, int64_t MN) {
     const int64_t target = 2LL * c->sm_count;
     if (tiles >= target || K < 8 * DBK) return 1;
-    int64_t s = std::min<int64_t>((target + tiles - 1) / tiles, K / (16 * DBK));
+    // (under half a wave of tiles — c1's 200 × 200 Grams over K = 500 ran 10 CTAs of 32 k-tiles, 29 µs
+    // at one SM's DMMA rate each — split down to 4 k-tiles per CTA)
+    int64_t s = std::min<int64_t>((target + tiles - 1) / tiles, K / ((tiles <= 64 ? 4 : 16) * DBK));
     return (int)std::max<int64_t>(1, std::min<int64_t>(s, MN <= (1 << 20) ? target : 64));
 }
 
@@ -976,7 +982,10 @@ void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, 
         }
         K = 0;
     }
-    const int64_t mt = (M + DBM - 1) / DBM, nt = (N + DBN - 1) / DBN;
+    static const bool no_thin = getenv("BCUR_DGEMM_NO_THIN") != nullptr;  // experiments
+    const bool thin = N <= 16 && !no_thin;  // 64 × 16 tiles (the sketch's ℓ-wide products of c1/c2)
+    const int64_t nb = thin ? 16 : DBN;
+    const int64_t mt = (M + DBM - 1) / DBM, nt = (N + nb - 1) / nb;
     int64_t tiles = mt * nt;
     if (flags & GEMM_SYM_UPPER) tiles = (tiles + std::min(mt, nt)) / 2;
     int splits = dgemm_splits(c, tiles, K, M * N);
@@ -985,13 +994,21 @@ void dgemm(Ctx* c, Op ta, Op tb, int64_t M, int64_t N, int64_t K, double alpha, 
     splits = (int)((std::max<int64_t>(K, 1) + kchunk - 1) / kchunk);
     dim3 grid((unsigned)mt, (unsigned)nt, (unsigned)splits);
     if (splits == 1) {
-        ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, dta, lda, B, dtb, ldb, beta, C, ldc, nullptr,
-                              nullptr, 0, 0, flags);
+        if (thin)
+            ddispatch<DEPI_STORE, 16>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, dta, lda, B, dtb, ldb, beta, C, ldc,
+                                      nullptr, nullptr, 0, 0, flags);
+        else
+            ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, alpha, A, dta, lda, B, dtb, ldb, beta, C, ldc,
+                                  nullptr, nullptr, 0, 0, flags);
         return;
     }
     DevBuf part(c, (size_t)splits * M * N * sizeof(double));
-    ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, 1.0, A, dta, lda, B, dtb, ldb, 0.0, nullptr, 0,
-                          part.as<double>(), nullptr, 0, 0, flags);
+    if (thin)
+        ddispatch<DEPI_STORE, 16>(c, ta, tb, grid, M, N, K, kchunk, 1.0, A, dta, lda, B, dtb, ldb, 0.0, nullptr, 0,
+                                  part.as<double>(), nullptr, 0, 0, flags);
+    else
+        ddispatch<DEPI_STORE>(c, ta, tb, grid, M, N, K, kchunk, 1.0, A, dta, lda, B, dtb, ldb, 0.0, nullptr, 0,
+                              part.as<double>(), nullptr, 0, 0, flags);
     const int64_t total = M * N;
     if (splits >= 16 && total <= (1 << 20))
         k_dsplitk_reduce_warp<<<(unsigned)((total * 32 + 255) / 256), 256, 0, c->stream>>>(

@@ -30,6 +30,32 @@ __global__ void k_transpose(const TS* __restrict__ src, int64_t m, int64_t n, in
     }
 }
 
+// Several contiguous device → device copies in one launch (the selected blocks of a column
+// basis: c3 gathered its 32 blocks and their exponents with 64 dependent cudaMemcpyAsync calls,
+// 0.4 ms of a 21 ms step — profiles/r02an/step_c3.txt).  Every segment is a multiple of 4 bytes;
+// 16-byte aligned ones move as uint4.  grid = (chunks, segments).
+__global__ void __launch_bounds__(256) k_copy_segments(const ops::CopySeg* __restrict__ segs) {
+    const ops::CopySeg sg = segs[blockIdx.y];
+    const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+    const bool a16 = ((((uintptr_t)sg.src) | ((uintptr_t)sg.dst) | (uintptr_t)sg.bytes) & 15) == 0;
+    if (a16) {
+        const uint4* s = reinterpret_cast<const uint4*>(sg.src);
+        uint4* d = reinterpret_cast<uint4*>(sg.dst);
+        const size_t n = sg.bytes / 16;
+        size_t i = tid;
+        for (; i + 3 * nth < n; i += 4 * nth) {  // four independent loads in flight per thread
+            const uint4 v0 = s[i], v1 = s[i + nth], v2 = s[i + 2 * nth], v3 = s[i + 3 * nth];
+            d[i] = v0; d[i + nth] = v1; d[i + 2 * nth] = v2; d[i + 3 * nth] = v3;
+        }
+        for (; i < n; i += nth) d[i] = s[i];
+    } else {
+        const uint32_t* s = reinterpret_cast<const uint32_t*>(sg.src);
+        uint32_t* d = reinterpret_cast<uint32_t*>(sg.dst);
+        const size_t n = sg.bytes / 4;
+        for (size_t i = tid; i < n; i += nth) d[i] = s[i];
+    }
+}
+
 __global__ void k_count_nonfinite(const double* __restrict__ x, int64_t count, unsigned int* __restrict__ flag) {
     bool bad = false;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
@@ -133,6 +159,16 @@ void convert(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds
         k_convert<double, float><<<g, 256, 0, c->stream>>>((const double*)src, m, n, lds, (float*)dst, ldd);
     else
         k_convert<double, double><<<g, 256, 0, c->stream>>>((const double*)src, m, n, lds, (double*)dst, ldd);
+    LAUNCH_CHECK(c);
+}
+
+void copy_segments(Ctx* c, const CopySeg* d_segs, int nsegs, size_t max_bytes) {
+    if (nsegs <= 0 || max_bytes == 0) return;
+    // ~4 CTAs per SM in total, each thread moving at least a few 16-byte words
+    const size_t per = std::max<size_t>(1, (size_t)(4 * c->sm_count + nsegs - 1) / nsegs);
+    const size_t want = (max_bytes / 16 + 256 * 4 - 1) / (256 * 4);
+    const unsigned chunks = (unsigned)std::max<size_t>(1, std::min(per, want));
+    k_copy_segments<<<dim3(chunks, (unsigned)nsegs), 256, 0, c->stream>>>(d_segs);
     LAUNCH_CHECK(c);
 }
 

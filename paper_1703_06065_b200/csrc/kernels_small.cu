@@ -509,6 +509,10 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     }
     __syncthreads();
     const int nblk = half * (half + 1) / 2;
+    int P0 = (int)((sqrtf(8.0f * (float)threadIdx.x + 1.0f) - 1.0f) * 0.5f);  // block threadIdx.x → (P0, Q0), P0 ≥ Q0
+    if (P0 * (P0 + 1) / 2 > (int)threadIdx.x) --P0;
+    if ((P0 + 1) * (P0 + 2) / 2 <= (int)threadIdx.x) ++P0;
+    const int Q0 = (int)threadIdx.x - P0 * (P0 + 1) / 2;
     int rounds = 0;
     const bool timing = g_jac_timing && threadIdx.x == 0;
     long long ta = 0, tb = 0, c0 = 0, c1 = 0;
@@ -518,8 +522,11 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
         for (int round = 0; round < mrot; ++round, ++rounds) {
             if (timing) c0 = clock64();
             for (int i = threadIdx.x; i < half; i += NT) {
-                int p = i == 0 ? round : (round + i) % mrot;
-                int q = i == 0 ? wp - 1 : (round - i + mrot) % mrot;
+                // (round ± i) mod mrot without the integer divisions (0 ≤ round, i < mrot)
+                int p = round + i, q = round - i;
+                if (p >= mrot) p -= mrot;
+                if (q < 0) q += mrot;
+                if (i == 0) q = wp - 1;
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, sv = 0.0;
                 if (q < w) {
@@ -547,10 +554,13 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
             if (timing) { c1 = clock64(); ta += c1 - c0; c0 = c1; }
             // block (P, Q), P ≥ Q, enumerated over the packed block triangle
             for (int b = threadIdx.x; b < nblk; b += NT) {
-                int P = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
-                if (P * (P + 1) / 2 > b) --P;
-                if ((P + 1) * (P + 2) / 2 <= b) ++P;
-                const int Q = b - P * (P + 1) / 2;
+                int P = P0, Q = Q0;  // the thread's first block, decoded once before the sweeps
+                if (b != (int)threadIdx.x) {
+                    P = (int)((sqrtf(8.0f * (float)b + 1.0f) - 1.0f) * 0.5f);
+                    if (P * (P + 1) / 2 > b) --P;
+                    if ((P + 1) * (P + 2) / 2 <= b) ++P;
+                    Q = b - P * (P + 1) / 2;
+                }
                 const int p1 = pp[P], q1 = qq[P], p2 = pp[Q], q2 = qq[Q];
                 const double s1 = sn[P], s2 = sn[Q];
                 if (s1 == 0.0 && s2 == 0.0) continue;

@@ -194,6 +194,13 @@ void sym_eig(Ctx* c, const double* g, int64_t w, int64_t ldg, double* lam, doubl
 
 // ---- elementwise / layout (kernels_misc.cu) -------------------------------
 void convert(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd);
+// nsegs contiguous device → device copies in one launch (d_segs on the device; bytes % 4 == 0)
+struct CopySeg {
+    const void* src;
+    void* dst;
+    size_t bytes;
+};
+void copy_segments(Ctx* c, const CopySeg* d_segs, int nsegs, size_t max_bytes);
 // dst[i] = fp32(src[i] as fp16) · scale
 void f16_to_f32(Ctx* c, const uint16_t* src, int64_t count, float scale, float* dst);
 void transpose(Ctx* c, const void* src, int dts, int64_t m, int64_t n, int64_t lds, void* dst, int dtd, int64_t ldd);

@@ -241,8 +241,10 @@ static void chol_enqueue(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         Mat64 W(c, w, w), Xs(c, n1, n1), Rs;
         if (want_r) Rs = Mat64(c, n1, n1);
         copy_f64(c, G, w, w, ldg, W.p(), w);
-        CUDA_CHECK(cudaMemsetAsync(R, 0, (size_t)w * w * sizeof(double), c->stream));
-        CUDA_CHECK(cudaMemsetAsync(X, 0, (size_t)w * w * sizeof(double), c->stream));
+        // zeros only where nothing is written below: X's lower-left quarter (the diagonal halves
+        // arrive as full squares, X12 whole); R the same, and only when the caller reads it
+        CUDA_CHECK(cudaMemset2DAsync(X + n1, w * sizeof(double), 0, n2 * sizeof(double), n1, c->stream));
+        if (want_r) CUDA_CHECK(cudaMemset2DAsync(R + n1, w * sizeof(double), 0, n2 * sizeof(double), n1, c->stream));
         cudaStream_t main_s = c->stream, side_s = c->side_stream();
         c->order(main_s, side_s, 0);
         CholRec S{c, W.p(), R, X, w, st, main_s, side_s, true, want_r};
@@ -876,7 +878,22 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
         // owner in that form (4 bytes per element, the fp32 size) and C is replicated.
         DevBuf cil(c, (size_t)m * cap * 4), ce(c, (size_t)cap * sizeof(int));
         int64_t at = 0;
-        for (int64_t b : blocks) {
+        if (c->comm.world <= 1) {  // one launch for every block and its exponents
+            std::vector<CopySeg> segs;
+            size_t mx = 0;
+            for (int64_t b : blocks) {
+                const int64_t w = s.off_global[b + 1] - s.off_global[b], j0 = s.off_global[b] - s.col0;
+                segs.push_back({ra->il.as<uint16_t>() + (size_t)j0 * 2 * m, cil.as<uint16_t>() + (size_t)at * 2 * m,
+                                (size_t)w * m * 4});
+                segs.push_back({ra->exps.as<int>() + j0, ce.as<int>() + at, (size_t)w * sizeof(int)});
+                mx = std::max(mx, (size_t)w * m * 4);
+                at += w;
+            }
+            DevBuf dsegs(c, segs.size() * sizeof(CopySeg));
+            h2d(c, dsegs.as<CopySeg>(), segs.data(), segs.size());
+            copy_segments(c, dsegs.as<CopySeg>(), (int)segs.size(), mx);
+        }
+        else for (int64_t b : blocks) {
             const int64_t w = s.off_global[b + 1] - s.off_global[b], j0 = s.off_global[b] - s.col0;
             uint16_t* dst = cil.as<uint16_t>() + (size_t)at * 2 * m;
             if (b >= s.g0 && b < s.g1) {
@@ -897,7 +914,21 @@ static void column_basis(Ctx* c, const DMat* a, const Shard& s, const std::vecto
         const size_t es = dtype_size(cdt);
         DevBuf cf(c, (size_t)m * cap * es);
         int64_t at = 0;
-        for (int64_t b : blocks) {
+        if (c->comm.world <= 1 && a->ld == m) {  // contiguous blocks: one launch for all of them
+            std::vector<CopySeg> segs;
+            size_t mx = 0;
+            for (int64_t b : blocks) {
+                const int64_t w = s.off_global[b + 1] - s.off_global[b];
+                segs.push_back({(const char*)a->ptr + (size_t)(s.off_global[b] - s.col0) * a->ld * es,
+                                (char*)cf.ptr + (size_t)at * m * es, (size_t)w * m * es});
+                mx = std::max(mx, (size_t)w * m * es);
+                at += w;
+            }
+            DevBuf dsegs(c, segs.size() * sizeof(CopySeg));
+            h2d(c, dsegs.as<CopySeg>(), segs.data(), segs.size());
+            copy_segments(c, dsegs.as<CopySeg>(), (int)segs.size(), mx);
+        }
+        else for (int64_t b : blocks) {
             const int64_t w = s.off_global[b + 1] - s.off_global[b];
             char* dst = (char*)cf.ptr + (size_t)at * m * es;
             if (c->comm.world <= 1) {

@@ -1,0 +1,7 @@
+#!/bin/bash
+# Packed Jacobi phase clocks at c1/c2/c3 widths; split-K rule for under-half-wave DMMA products.
+cd $GRAFT_REPO_ROOT
+O=gpurun_out/r02ap; mkdir -p $O
+for c in c1 c2 c3; do BCUR_JACOBI_TIMING=1 timeout 300 python bench.py --config $c --steps 2 --warmup 1 --no-cpu-baseline 2>&1 | grep jacobi_packed | sort | uniq -c > $O/jacobi_clocks_$c.log; done
+timeout 900 python -m pytest tests/test_gpu_dmma.py tests/test_gpu_parity.py tests/test_golden.py tests/test_alg1.py -x -q -p no:cacheprovider -m gpu > $O/pytest_sel.log 2>&1; echo "rc=$?" >> $O/pytest_sel.log
+for c in c1 c2; do timeout 600 python bench.py --config $c --steps 20 --warmup 3 --no-cpu-baseline > $O/bench_$c.json 2> $O/bench_$c.err; done

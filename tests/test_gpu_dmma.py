@@ -18,7 +18,7 @@ def rel_fro(got, ref):
 
 
 @pytest.mark.parametrize("m,n,N", [(500, 2000, 15), (64, 20000, 10), (1, 7, 3), (129, 65, 1), (300, 301, 130),
-                                   (2048, 512, 256)])
+                                   (2048, 512, 256), (777, 333, 16), (1000, 64, 9), (70, 5000, 17)])
 def test_dmma_products(B, m, n, N):
     gen = np.random.default_rng(m * 7 + n + N)
     a = np.asfortranarray(gen.standard_normal((m, n)))

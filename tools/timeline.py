@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--top", type=int, default=25)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--list", default=None, help="write the last step's records (start µs, duration µs, name) here")
     args = ap.parse_args()
 
     import numpy as np
@@ -78,6 +79,14 @@ def main():
     if args.json:
         with open(args.json, "w") as f:
             json.dump(out, f, indent=1)
+    if args.list:
+        # the last step: from its norms pass (the first k_block_sumsq after the midpoint) on
+        starts = [i for i, k in enumerate(ks) if "k_block_sumsq" in k[2]]
+        i0 = starts[-1] if starts else 0
+        t0 = ks[i0][0]
+        with open(args.list, "w") as f:
+            for s0, e0, nm in ks[i0:]:
+                f.write(f"{s0 - t0:10.1f} {e0 - s0:9.1f}  {nm[:140]}\n")
 
 
 if __name__ == "__main__":
