@@ -533,12 +533,30 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
                     const double apq = Ap[tri_at(q, p)];
                     const double app = Ap[tri_at(p, p)], aqq = Ap[tri_at(q, q)];
                     if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(app * aqq)) {
-                        const double tau = (aqq - app) * fast_rcp(2.0 * apq);
-                        const double q2 = fma(tau, tau, 1.0);
-                        const double root = q2 * fast_rsqrt(q2);
-                        const double t = (tau >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(tau) + root);
-                        c = fast_rsqrt(fma(t, t, 1.0));
-                        sv = t * c;
+                        // The small-angle rotation with tan 2θ = 2a_pq/(a_qq − a_pp), from the double
+                        // angle: cos 2θ = |d|/√h, h = d² + (2a_pq)²; cos²θ = (1 + cos 2θ)/2;
+                        // |sin θ| = |2a_pq|/(2√h·cos θ); sign θ = sign(d·a_pq).  Two rsqrt chains
+                        // instead of rcp → rsqrt → rcp → rsqrt: the rotation is this phase's whole
+                        // latency (a ~33-deep dependent fp64 chain cut to ~21; profiles/r02aq →
+                        // r02as jacobi_clocks).  h outside the normal range: the tangent form.
+                        const double d = aqq - app, b2 = 2.0 * apq;
+                        const double h = fma(d, d, b2 * b2);
+                        double t;
+                        if (h > 1e-280 && h < 1e280) {
+                            const double r = fast_rsqrt(h);
+                            const double c2 = fma(0.5 * fabs(d), r, 0.5);
+                            const double rc = fast_rsqrt(c2);
+                            c = c2 * rc;
+                            sv = (d * b2 >= 0.0 ? 0.5 : -0.5) * fabs(b2) * r * rc;
+                            t = sv * rc;
+                        } else {
+                            const double tau = d * fast_rcp(b2);
+                            const double q2 = fma(tau, tau, 1.0);
+                            const double root = q2 * fast_rsqrt(q2);
+                            t = (tau >= 0.0 ? 1.0 : -1.0) * fast_rcp(fabs(tau) + root);
+                            c = fast_rsqrt(fma(t, t, 1.0));
+                            sv = t * c;
+                        }
                         np_[i] = app - t * apq;
                         nq_[i] = aqq + t * apq;
                         rotated = 1;
@@ -592,6 +610,9 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
         if (!rotated) break;
         // would the next sweep rotate at all?  (The same test as the rounds' on every off-diagonal
         // pair: none passing it means that sweep would change nothing — skipping it is exact.)
+        __syncthreads();  // every thread has read the sweep's flag before thread 0 clears it: without
+                          // this barrier a late warp could read the cleared flag and leave the loop alone
+                          // (c4's 1024-thread launches faulted in about half of 20-step runs, profiles/r02at)
         if (threadIdx.x == 0) rotated = 0;
         __syncthreads();
         for (int e = threadIdx.x; e < w * (w - 1) / 2; e += NT) {

@@ -1931,20 +1931,28 @@ k_umma2_h3m(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         }
                         if (j >= ncol) continue;
                         const int col = col0 + j;
-                        double v = (double)acc[j] * (alpha * exp2_int(-(re + (cexp ? cexp[col] : 0))));
+                        // fp32 from here on (this kernel's accumulator is one fp32 sum: GEMM_FAST_ACC).  The
+                        // fp64 form — DMULs and three F2F.F16.F64 conversions per element on the XU pipe —
+                        // left this epilogue exposed: the hi-only correction ran 19 % tensor-active, 13 % XU
+                        // (profiles/r02ar/ncu_full_c3.md).  acc × 2^e is exact, and the split of an fp32
+                        // value (hi = rn16(v·2¹⁴), lo = rn16(v·2¹⁴ − hi), the difference exact in fp32) is
+                        // the one the fp64 form gave; BASIS adds the aux term with one fp32 rounding, the
+                        // rounding of its fp32 output.
+                        const float sc = (float)(alpha * exp2_int(-(re + (cexp ? cexp[col] : 0))));
+                        float v = acc[j] * sc;
                         if (EPI == EPI_SPLIT) {
                             uint16_t* o16 = reinterpret_cast<uint16_t*>(out_v);
-                            const double sv = v * (double)(1 << BASIS_E);
-                            const __half h = __double2half(sv);
-                            const __half l = __double2half(sv - (double)__half2float(h));
+                            const float sv = v * (float)(1 << BASIS_E);
+                            const __half h = __float2half_rn(sv);
+                            const __half l = __float2half_rn(sv - __half2float(h));
                             o16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
                             o16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
                         } else {
-                            v += (double)ax8[j & 7] * (1.0 / (double)(1 << BASIS_E));
-                            reinterpret_cast<float*>(out_v)[row + (int64_t)col * ldo] = (float)v;
-                            const double sv = v * (double)(1 << BASIS_E);  // interleaved hi/lo, as k_umma
-                            const __half h = __double2half(sv);
-                            const __half l = __double2half(sv - (double)__half2float(h));
+                            v = fmaf(ax8[j & 7], 1.0f / (float)(1 << BASIS_E), v);
+                            reinterpret_cast<float*>(out_v)[row + (int64_t)col * ldo] = v;
+                            const float sv = v * (float)(1 << BASIS_E);  // interleaved hi/lo, as k_umma
+                            const __half h = __float2half_rn(sv);
+                            const __half l = __float2half_rn(sv - __half2float(h));
                             q16[(int64_t)col * 2 * M + r_il] = *reinterpret_cast<const uint16_t*>(&h);
                             q16[(int64_t)col * 2 * M + r_il + 64] = *reinterpret_cast<const uint16_t*>(&l);
                         }

@@ -29,6 +29,16 @@ def tag_of(name):
         return "umma_atx_rowsq"
     if "k_block_sumsq" in name:
         return "block_sumsq"
+    if "k_chol_persistent" in name:
+        return "chol_inv"
+    if "k_jacobi_packed" in name:
+        return "sym_eig"
+    if "k_copy_segments" in name:
+        return "copy_segments"
+    for k in ("k_umma2_h3m<", "k_umma2_h3<"):  # CTA-pair 3×FP16 products: <A_MN, EPI>
+        if k in name:
+            a = name.split(k)[1].split(">")[0].replace("(bool)", "").split(",")[0].strip()
+            return "umma_ax_h3" if a in ("1", "true") else "umma_atx_h3"
     if "k_umma<" not in name:
         return None
     args = name.split("k_umma<")[1].split(">")[0].replace("(bool)", "").replace("(int)", "").split(",")
@@ -39,11 +49,18 @@ def tag_of(name):
 
 
 def short(name):
-    return name.split("(")[0].replace("void ", "").replace("bcur_b200::<unnamed>::", "")[:90]
+    n = name.split("(")[0].replace("void ", "")
+    for pre in ("bcur_b200::<unnamed>::", "bcur_b200::(anonymous namespace)::", "bcur_b200::ops::", "unnamed>::"):
+        n = n.replace(pre, "")
+    return n[:90]
 
 
 def launches(path, steps):
-    rows = list(csv.reader(open(path)))
+    if path.endswith(".gz"):
+        import gzip
+        rows = list(csv.reader(gzip.open(path, "rt")))
+    else:
+        rows = list(csv.reader(open(path)))
     hdr = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     h = rows[hdr]
     tot, cnt = collections.defaultdict(float), collections.Counter()
@@ -61,7 +78,13 @@ def launches(path, steps):
 
 
 def full(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if path.endswith(".csv.gz"):  # an exported `ncu -i … --page raw --csv`
+        import gzip
+        out = gzip.open(path, "rt").read()
+    elif path.endswith(".csv"):
+        out = open(path).read()
+    else:
+        out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",

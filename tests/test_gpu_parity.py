@@ -225,6 +225,23 @@ def test_bitwise_rerun_determinism(B):
     assert np.array_equal(r1.c, r2.c)
 
 
+def test_wide_sketch_eigensolve_repeatable(B):
+    """The packed Jacobi at sketch widths that need 1024-thread launches (l = k + p >= 84; c4 runs
+    l = 110).  A missing barrier before its per-sweep flag reset let a late warp leave the sweep
+    loop alone — an illegal access in about half of c4's 20-step runs (profiles/r02at) — so the
+    same decomposition is repeated and must reproduce bit for bit."""
+    a = np.asfortranarray(lowrank(384, 4096, 100, "geom:1:0.97", 1e-3, 12, np.float64))
+    dm = B.DeviceMatrix.from_host(a)
+    part = B.BlockPartition.equal_blocks(4096, 128)
+    first = None
+    for _ in range(25):
+        r = B.block_css(dm, part, 100, 2, B.Rng(5), p=10, q=0)
+        key = (r.plan.blocks(), r.projection_error, r.scores.scores.tobytes())
+        if first is None:
+            first = key
+        assert key == first
+
+
 def run_ranks(B, a, s, world, call):
     """Run `call(dm, ctx)` on `world` contexts of one GPU, each holding a contiguous column
     shard of `a` (blocks of width s).  The collectives are a host rendezvous after each rank
