@@ -101,6 +101,11 @@ bcur_status bcur_dmat_upload(bcur_ctx ctx, bcur_dmat a, const void* host, int64_
  * valid and unmodified until then (pinned memory makes the copy asynchronous). */
 bcur_status bcur_dmat_upload_async(bcur_ctx ctx, bcur_dmat a, const void* host, int64_t ld_host);
 bcur_status bcur_dmat_download(bcur_ctx ctx, bcur_dmat a, void* host, int64_t ld_host);
+/* Page-locked host memory for inputs and result buffers (the reference returns its results by
+ * value, blockcur.hpp:44-58; here large ones — U of bcur_block_cur — land in caller-owned host
+ * memory, and a pinned destination takes one DMA copy where a pageable one is staged). */
+bcur_status bcur_host_alloc(size_t bytes, void** out);
+bcur_status bcur_host_free(void* p);
 /* Wraps caller-owned device memory (no copy, not freed by destroy). */
 bcur_status bcur_dmat_wrap(bcur_ctx ctx, int dtype, int64_t m, int64_t n, void* dev_ptr, int64_t ld,
                            bcur_dmat* out);

@@ -85,6 +85,8 @@ SIGNATURES = {
     "bcur_dmat_load_bcur": (C.c_int, [vp, C.c_char_p, C.c_int, i64, i64, C.POINTER(vp)]),
     "bcur_dmat_save_bcur": (C.c_int, [vp, vp, C.c_char_p]),
     "bcur_dmat_download": (C.c_int, [vp, vp, vp, i64]),
+    "bcur_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+    "bcur_host_free": (C.c_int, [vp]),
     "bcur_dmat_wrap": (C.c_int, [vp, C.c_int, i64, i64, vp, i64, C.POINTER(vp)]),
     "bcur_dmat_info": (C.c_int, [vp, C.POINTER(C.c_int), P_i64, P_i64, P_i64, C.POINTER(vp)]),
     "bcur_dmat_set_shard": (C.c_int, [vp, i64, i64]),

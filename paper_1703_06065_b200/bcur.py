@@ -943,10 +943,32 @@ class CurResult:
         return self.abs_err / self.a_norm if self.a_norm > 0 else 0.0
 
 
+def pinned_empty(shape, dtype=np.float64, order: str = "F") -> np.ndarray:
+    """An uninitialized array in page-locked host memory (bcur_host_alloc): as an upload source it
+    makes the copy asynchronous, as a result buffer (``block_cur(..., out_u=...)``) it takes one DMA
+    copy where pageable memory is staged.  Freed with the array."""
+    import weakref
+
+    shape = (shape,) if np.isscalar(shape) else tuple(int(x) for x in shape)
+    dt = np.dtype(dtype)
+    nbytes = int(np.prod(shape, dtype=np.int64)) * dt.itemsize
+    ptr = C.c_void_p()
+    _check(L.lib.bcur_host_alloc(max(nbytes, 1), C.byref(ptr)))
+    buf = (C.c_char * max(nbytes, 1)).from_address(ptr.value)
+    arr = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape, dtype=np.int64))).reshape(shape, order=order)
+    weakref.finalize(buf, L.lib.bcur_host_free, ptr)  # buf lives as long as any view of it
+    return arr
+
+
 def block_cur(a, col_part: BlockPartition, row_part: BlockPartition, k: int, gc: int, gr: int, rng: Rng,
               p: int = 10, q: int = 0, mode: str = SamplingMode.without_replacement, want_u: bool = True,
-              residual: int = L.RESID_AUTO, ctx: Optional[Context] = None, rank_floor: bool = False) -> CurResult:
-    """Block CUR with row and column blocks: U = C⁺AR⁺ and ‖A − CUR‖_F on the GPU."""
+              residual: int = L.RESID_AUTO, ctx: Optional[Context] = None, rank_floor: bool = False,
+              out_u: Optional[np.ndarray] = None) -> CurResult:
+    """Block CUR with row and column blocks: U = C⁺AR⁺ and ‖A − CUR‖_F on the GPU.
+
+    ``out_u``: a caller-owned Fortran-ordered float64 buffer of at least (gc·max col width) ×
+    (gr·max row width) that receives U (the result's ``u`` is a view of it) — a serving loop
+    reuses one ``pinned_empty`` buffer, which takes U in one DMA copy."""
     ctx = ctx or default_context()
     d = _dev(a, ctx)
     coff, coffp = _off_ptr(col_part)
@@ -964,7 +986,13 @@ def block_cur(a, col_part: BlockPartition, row_part: BlockPartition, k: int, gc:
         # upper bound on the factor sizes: every draw takes the widest block
         cmax = gc * col_part.max_width()
         rmax = gr * row_part.max_width()
-        umat = np.zeros((cmax, rmax), dtype=np.float64, order="F")
+        if out_u is not None:
+            if (out_u.dtype != np.float64 or out_u.ndim != 2 or not out_u.flags.f_contiguous
+                    or out_u.shape[0] < cmax or out_u.shape[1] < rmax):
+                raise ValueError("block_cur: out_u must be Fortran-ordered float64 of at least %d x %d" % (cmax, rmax))
+            umat = out_u
+        else:
+            umat = np.empty((cmax, rmax), dtype=np.float64, order="F")  # only [:cw, :rw] is returned
     _check(L.lib.bcur_block_cur(ctx.handle, d.handle, coffp, Gc, roffp, Gr, C.byref(opt), u.ctypes.data_as(L.P_dbl),
                                 cs.ctypes.data_as(L.P_dbl), rs.ctypes.data_as(L.P_dbl), cd, rd,
                                 umat.ctypes.data_as(L.P_dbl) if want_u else None, umat.shape[0] if want_u else 1,
@@ -974,7 +1002,7 @@ def block_cur(a, col_part: BlockPartition, row_part: BlockPartition, k: int, gc:
     if want_u:
         cw = sum(col_part.width(x.block) for x in cplan.draws)
         rw = sum(row_part.width(x.block) for x in rplan.draws)
-        umat = np.asfortranarray(umat[:cw, :rw])
+        umat = umat[:cw, :rw] if out_u is not None else np.asfortranarray(umat[:cw, :rw])
     return CurResult(cplan, rplan, ScoreVector(cs, float(rep.k_eff)), ScoreVector(rs, float(rep.k_eff)), umat,
                      rep.abs_err, rep.a_norm, rep.rank_c, rep.rank_r,
                      "explicit" if rep.residual_path else "pythagoras")

@@ -480,16 +480,77 @@ bcur_status bcur_dmat_save_bcur(bcur_ctx ctx, bcur_dmat a, const char* path) {
     API_END
 }
 
+// Device → host copy of a result matrix (width_bytes × cols, pitched on both sides), synchronous.
+// Pinned (or registered) destinations take one DMA copy.  A pageable destination made the driver
+// stage the copy itself at ~4.7 GB/s — c4's 75 MB U took 16 ms of its 55 ms step
+// (profiles/r02aw/step_c4.txt) — so it goes through two pinned staging buffers instead: the
+// DMA of chunk i + 1 runs while the host copies chunk i into the caller's memory.
+static void download_2d(Ctx* c, void* host, size_t host_pitch, const void* dev, size_t dev_pitch, size_t width_bytes,
+                        size_t cols) {
+    if (!width_bytes || !cols) return;
+    cudaPointerAttributes attr{};
+    const bool pinned = cudaPointerGetAttributes(&attr, host) == cudaSuccess && attr.type == cudaMemoryTypeHost;
+    (void)cudaGetLastError();  // (an unregistered pointer reports an error on older drivers)
+    const size_t total = width_bytes * cols;
+    if (pinned || total <= ((size_t)1 << 20)) {
+        CUDA_CHECK(cudaMemcpy2DAsync(host, host_pitch, dev, dev_pitch, width_bytes, cols, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return;
+    }
+    constexpr size_t CHUNK = (size_t)8 << 20;
+    static thread_local char* stage[2] = {nullptr, nullptr};
+    static thread_local cudaEvent_t done[2] = {nullptr, nullptr};
+    for (int b = 0; b < 2; ++b)
+        if (!stage[b]) {
+            CUDA_CHECK(cudaMallocHost(&stage[b], CHUNK));
+            CUDA_CHECK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+        }
+    const size_t cols_per = std::max<size_t>(1, CHUNK / width_bytes);
+    if (width_bytes > CHUNK) {  // one column exceeds a chunk: the plain copy
+        CUDA_CHECK(cudaMemcpy2DAsync(host, host_pitch, dev, dev_pitch, width_bytes, cols, cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        return;
+    }
+    const size_t nchunks = (cols + cols_per - 1) / cols_per;
+    auto issue = [&](size_t i) {
+        const size_t c0 = i * cols_per, nc = std::min(cols_per, cols - c0);
+        CUDA_CHECK(cudaMemcpy2DAsync(stage[i & 1], width_bytes, (const char*)dev + c0 * dev_pitch, dev_pitch, width_bytes,
+                                     nc, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_CHECK(cudaEventRecord(done[i & 1], c->stream));
+    };
+    issue(0);
+    for (size_t i = 0; i < nchunks; ++i) {
+        CUDA_CHECK(cudaEventSynchronize(done[i & 1]));
+        if (i + 1 < nchunks) issue(i + 1);  // (the other buffer: its chunk i − 1 was copied out below)
+        const size_t c0 = i * cols_per, nc = std::min(cols_per, cols - c0);
+        for (size_t j = 0; j < nc; ++j)
+            std::memcpy((char*)host + (c0 + j) * host_pitch, stage[i & 1] + j * width_bytes, width_bytes);
+    }
+    c->sync();
+}
+
+bcur_status bcur_host_alloc(size_t bytes, void** out) {
+    API_BEGIN
+    if (!out) fail(BCUR_E_INVALID_ARGUMENT, "bcur_host_alloc: null output");
+    *out = nullptr;
+    if (bytes) CUDA_CHECK(cudaMallocHost(out, bytes));
+    API_END
+}
+
+bcur_status bcur_host_free(void* p) {
+    API_BEGIN
+    if (p) CUDA_CHECK(cudaFreeHost(p));
+    API_END
+}
+
 bcur_status bcur_dmat_download(bcur_ctx ctx, bcur_dmat a, void* host, int64_t ld_host) {
     API_BEGIN
     Ctx* c = C(ctx);
     DMat* d = M(a);
     if (ld_host < d->m) fail(BCUR_E_INVALID_ARGUMENT, "bcur_dmat_download: ld_host < m");
     const size_t es = dtype_size(d->dtype);
-    if (d->m * d->n > 0)
-        CUDA_CHECK(cudaMemcpy2DAsync(host, ld_host * es, d->ptr, d->ld * es, d->m * es, d->n, cudaMemcpyDeviceToHost,
-                                     c->stream));
-    c->sync();
+    if (d->m * d->n > 0) download_2d(c, host, ld_host * es, d->ptr, d->ld * es, d->m * es, d->n);
+    else c->sync();
     API_END
 }
 
@@ -994,9 +1055,7 @@ bcur_status bcur_block_cur_alg1(bcur_ctx ctx, bcur_dmat a, const int64_t* offset
     std::memcpy(draws_out, o.draws.data(), g * sizeof(bcur_block_draw));
     if (margins_out) std::memcpy(margins_out, o.margins.data(), g * sizeof(double));
     if (u_out) {
-        CUDA_CHECK(cudaMemcpyAsync(u_out, o.u.p(), (size_t)o.u.m * o.u.n * sizeof(double), cudaMemcpyDeviceToHost,
-                                   c->stream));
-        c->sync();
+        download_2d(c, u_out, (size_t)o.u.m * 8, o.u.p(), (size_t)o.u.ld * 8, (size_t)o.u.m * 8, o.u.n);
     }
     *report = o.rep;
     API_END
@@ -1020,8 +1079,7 @@ bcur_status bcur_block_cur(bcur_ctx ctx, bcur_dmat a, const int64_t* col_offsets
     if (row_draws) std::memcpy(row_draws, o.row_draws.data(), o.row_draws.size() * sizeof(bcur_block_draw));
     if (u_out && o.u_valid) {
         if (ldu < o.u.m) fail(BCUR_E_INVALID_ARGUMENT, "block_cur: ldu < c");
-        CUDA_CHECK(cudaMemcpy2DAsync(u_out, ldu * 8, o.u.p(), o.u.ld * 8, o.u.m * 8, o.u.n, cudaMemcpyDeviceToHost, c->stream));
-        c->sync();
+        download_2d(c, u_out, ldu * 8, o.u.p(), o.u.ld * 8, o.u.m * 8, o.u.n);
     }
     if (rep) *rep = o.rep;
     API_END

@@ -23,10 +23,20 @@ __device__ __forceinline__ double wsum(double s) {
 // p (workspace, G doubles) ; active flags in `act` (G bytes)
 __global__ void __launch_bounds__(32) k_distribution_draw(const double* __restrict__ scores, int64_t G, int normalize,
                                                           int64_t g, int mode, const double* __restrict__ uniforms,
-                                                          double* __restrict__ p, unsigned char* __restrict__ act,
+                                                          double* p, unsigned char* act,
                                                           bcur_block_draw* __restrict__ draws,
                                                           double* __restrict__ margins, int* status) {
     const int lane = threadIdx.x;
+    // the working copies of p and the active flags live in shared memory when they fit: the draw
+    // loop is one serial chain, and with the global workspace every step of it paid an L2 round
+    // trip (81 µs for g = 32 draws over G = 512 blocks at c3, profiles/r02an/step_c3.txt)
+    constexpr int SG = 4096;
+    __shared__ double sp[SG];
+    __shared__ unsigned char sa[SG];
+    if (G <= SG) {
+        p = sp;
+        act = sa;
+    }
     const int64_t chunk = (G + 31) / 32;
     const int64_t lo = imin64(G, lane * chunk), hi = imin64(G, lo + chunk);
     // total of scores (fixed order)
@@ -48,6 +58,7 @@ __global__ void __launch_bounds__(32) k_distribution_draw(const double* __restri
         psum += v;
         positive += v > 0.0 ? 1 : 0;
     }
+    __syncwarp();  // p[] is read across lanes below (p[pick])
     bad = __any_sync(0xffffffffu, bad);
     psum = wsum(psum);
 #pragma unroll
@@ -65,8 +76,10 @@ __global__ void __launch_bounds__(32) k_distribution_draw(const double* __restri
     for (int64_t i = lo; i < hi; ++i)
         if (p[i] > 0.0) mass_chunk += p[i];
     double mass = 1.0;
+    double u_next = g > 0 ? uniforms[0] : 0.0;
     for (int64_t t = 0; t < g; ++t) {
-        const double u = uniforms[t] * mass;
+        const double u = u_next * mass;
+        if (t + 1 < g) u_next = uniforms[t + 1];  // (in flight during this draw)
         // inclusive scan of chunk masses
         double incl = mass_chunk;
 #pragma unroll

@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
                                                         double* __restrict__ lam, int* __restrict__ order_out,
                                                         int max_sweeps) {
     extern __shared__ double Ap[];  // packed lower triangle
+    auto at = [&](int i, int j) { return tri_at(i, j); };
     __shared__ double cs[256], sn[256], np_[256], nq_[256];
     __shared__ int pp[256], qq[256];
     __shared__ int rotated;
@@ -501,7 +502,7 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     const int wp = (w + 1) & ~1, half = wp / 2, mrot = wp - 1;
     const int NT = blockDim.x;
     for (int i = threadIdx.x; i < w; i += NT)
-        for (int j = 0; j <= i; ++j) Ap[i * (i + 1) / 2 + j] = g[i + (int64_t)j * ldg];  // lower of a symmetric G
+        for (int j = 0; j <= i; ++j) Ap[at(i, j)] = g[i + (int64_t)j * ldg];  // lower of a symmetric G
     if (threadIdx.x == 0) {
         double f = 0.0;
         for (int j = 0; j < w; ++j) f = fmax(f, fabs(g[j + j * ldg]));
@@ -530,8 +531,8 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
                 if (p > q) { const int t = p; p = q; q = t; }
                 double c = 1.0, sv = 0.0;
                 if (q < w) {
-                    const double apq = Ap[tri_at(q, p)];
-                    const double app = Ap[tri_at(p, p)], aqq = Ap[tri_at(q, q)];
+                    const double apq = Ap[at(q, p)];
+                    const double app = Ap[at(p, p)], aqq = Ap[at(q, q)];
                     if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(app * aqq)) {
                         // The small-angle rotation with tan 2θ = 2a_pq/(a_qq − a_pp), from the double
                         // angle: cos 2θ = |d|/√h, h = d² + (2a_pq)²; cos²θ = (1 + cos 2θ)/2;
@@ -584,25 +585,27 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
                 if (s1 == 0.0 && s2 == 0.0) continue;
                 if (P == Q) {  // diagonal block: exact annihilation
                     if (q1 >= w) continue;
-                    Ap[tri_at(q1, p1)] = 0.0;
-                    Ap[tri_at(p1, p1)] = np_[P];
-                    Ap[tri_at(q1, q1)] = nq_[P];
+                    Ap[at(q1, p1)] = 0.0;
+                    Ap[at(p1, p1)] = np_[P];
+                    Ap[at(q1, q1)] = nq_[P];
                     continue;
                 }
                 const double c1 = cs[P], c2 = cs[Q];
                 const bool r2 = q1 < w, c2v = q2 < w;  // byes: a padding index has no row/column
-                const int i_pp = tri_at(p1, p2), i_pq = c2v ? tri_at(p1, q2) : 0;
-                const int i_qp = r2 ? tri_at(q1, p2) : 0, i_qq = (r2 && c2v) ? tri_at(q1, q2) : 0;
+                const int i_pp = at(p1, p2), i_pq = c2v ? at(p1, q2) : 0;
+                const int i_qp = r2 ? at(q1, p2) : 0, i_qq = (r2 && c2v) ? at(q1, q2) : 0;
                 const double a_pp = Ap[i_pp], a_pq = c2v ? Ap[i_pq] : 0.0;
                 const double a_qp = r2 ? Ap[i_qp] : 0.0, a_qq = (r2 && c2v) ? Ap[i_qq] : 0.0;
                 // rows: [p1; q1] ← [c1 −s1; s1 c1]·[.]   (Jᵀ A with J = [c s; −s c] convention of k_jacobi)
                 const double b_pp = c1 * a_pp - s1 * a_qp, b_pq = c1 * a_pq - s1 * a_qq;
                 const double b_qp = s1 * a_pp + c1 * a_qp, b_qq = s1 * a_pq + c1 * a_qq;
                 // columns: [p2, q2] ← [.]·J
-                Ap[i_pp] = c2 * b_pp - s2 * b_pq;
-                if (c2v) Ap[i_pq] = s2 * b_pp + c2 * b_pq;
-                if (r2) Ap[i_qp] = c2 * b_qp - s2 * b_qq;
-                if (r2 && c2v) Ap[i_qq] = s2 * b_qp + c2 * b_qq;
+                const double o_pp = c2 * b_pp - s2 * b_pq, o_pq = s2 * b_pp + c2 * b_pq;
+                const double o_qp = c2 * b_qp - s2 * b_qq, o_qq = s2 * b_qp + c2 * b_qq;
+                Ap[i_pp] = o_pp;
+                if (c2v) Ap[i_pq] = o_pq;
+                if (r2) Ap[i_qp] = o_qp;
+                if (r2 && c2v) Ap[i_qq] = o_qq;
             }
             __syncthreads();
             if (timing) tb += clock64() - c0;
@@ -620,8 +623,8 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
             if (i * (i - 1) / 2 > e) --i;
             if ((i + 1) * i / 2 <= e) ++i;
             const int j = e - i * (i - 1) / 2;
-            const double apq = Ap[tri_at(i, j)];
-            if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(Ap[tri_at(i, i)] * Ap[tri_at(j, j)])) rotated = 1;
+            const double apq = Ap[at(i, j)];
+            if (fabs(apq) > floor_abs && apq * apq > 1e-30 * fabs(Ap[at(i, i)] * Ap[at(j, j)])) rotated = 1;
         }
         __syncthreads();
         if (!rotated) break;
@@ -632,11 +635,11 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     // (a total order even for NaN input — NaNs rank last, among themselves by index — so `order`
     // is always a permutation: the caller's finiteness verdict arrives after this kernel ran)
     for (int j = threadIdx.x; j < w; j += NT) {
-        const double lj = Ap[tri_at(j, j)];
+        const double lj = Ap[at(j, j)];
         const bool nj = lj != lj;
         int rank = 0;
         for (int i = 0; i < w; ++i) {
-            const double li = Ap[tri_at(i, i)];
+            const double li = Ap[at(i, i)];
             const bool ni = li != li;
             const bool before = ni ? (nj && i < j) : (nj || li > lj || (li == lj && i < j));
             rank += before ? 1 : 0;
@@ -650,7 +653,7 @@ __global__ void __launch_bounds__(JP_T) k_jacobi_packed(const double* __restrict
     }
     __syncthreads();
     for (int j = threadIdx.x; j < w; j += NT) {
-        lam[j] = Ap[tri_at(order[j], order[j])];
+        lam[j] = Ap[at(order[j], order[j])];
         order_out[j] = order[j];
     }
 }

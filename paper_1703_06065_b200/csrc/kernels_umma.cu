@@ -2381,7 +2381,10 @@ void gemm_rowsumsq_f16(Ctx* c, int64_t M, int64_t N, int64_t K, const uint16_t* 
     }
     if (K % 64 != 0 || lda != K || ((uintptr_t)A16 % 16) != 0)
         fail(BCUR_E_INVALID_ARGUMENT, "gemm_rowsumsq_f16: the fp16 copy needs K % 64 == 0 (lda = K)");
-    ProfScope prof(c, "umma_atx_rowsq", 2.0 * M * N * K, 2.0 * K * M + (double)dtype_size(dtx) * K * N + 8.0 * M);
+    // the work of THIS launch: with a tile list only ntiles 128-row tiles of AᵀX are computed (the
+    // selected blocks' columns are skipped by the caller, which adds their mass from the norms)
+    const double Mw = (d_tiles && ntiles > 0) ? std::min<double>((double)M, 128.0 * ntiles) : (double)M;
+    ProfScope prof(c, "umma_atx_rowsq", 2.0 * Mw * N * K, 2.0 * K * Mw + (double)dtype_size(dtx) * K * N + 8.0 * Mw);
     (void)umma_ok(BCUR_F32, K, lda, A16);  // reads the environment switches once
     // X → fp16 with one power-of-two scale from its max (device-side; no host sync), unless
     // the caller passes it pre-converted (x16_pre, scale 2^q_pre)

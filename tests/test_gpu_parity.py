@@ -225,6 +225,30 @@ def test_bitwise_rerun_determinism(B):
     assert np.array_equal(r1.c, r2.c)
 
 
+def test_result_downloads_pageable_and_pinned(B):
+    """Device → host result copies: a pageable destination above 1 MB goes through the two-buffer
+    pinned staging pipeline (ragged last chunk, pitched destination), a pinned one takes one copy;
+    block_cur's U arrives the same in a caller-owned pinned buffer (out_u) as in a fresh array."""
+    gen = np.random.default_rng(3)
+    a = np.asfortranarray(gen.standard_normal((3001, 1237)))  # 29.7 MB: four 8 MB chunks, ragged
+    dm = B.DeviceMatrix.from_host(a)
+    assert np.array_equal(dm.to_host(), a)
+    pin = B.pinned_empty((3001, 1237))
+    assert pin.flags.f_contiguous and pin.dtype == np.float64
+    B._check(B.L.lib.bcur_dmat_download(dm.ctx.handle, dm.handle, pin.ctypes.data_as(B.C.c_void_p), 3001))
+    assert np.array_equal(pin, a)
+    s = 32
+    m = lowrank(256, 512, 12, "pow:1", 1e-3, 4, np.float64)
+    cpart, rpart = B.BlockPartition.equal_blocks(512, s), B.BlockPartition.equal_blocks(256, s)
+    r0 = B.block_cur(m, cpart, rpart, 8, 3, 3, B.Rng(2), p=4, q=1)
+    buf = B.pinned_empty((3 * s, 3 * s))
+    r1 = B.block_cur(m, cpart, rpart, 8, 3, 3, B.Rng(2), p=4, q=1, out_u=buf)
+    assert np.shares_memory(r1.u, buf)
+    assert np.array_equal(r0.u, r1.u) and r0.abs_err == r1.abs_err
+    with pytest.raises(ValueError):
+        B.block_cur(m, cpart, rpart, 8, 3, 3, B.Rng(2), p=4, q=1, out_u=np.zeros((4, 4), order="F"))
+
+
 def test_wide_sketch_eigensolve_repeatable(B):
     """The packed Jacobi at sketch widths that need 1024-thread launches (l = k + p >= 84; c4 runs
     l = 110).  A missing barrier before its per-sweep flag reset let a late warp leave the sweep
