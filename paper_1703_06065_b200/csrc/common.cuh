@@ -201,7 +201,13 @@ struct Ctx {
     }
     // one stream synchronization delivers every pending read
     void read_all() {
-        sync();
+        try {
+            sync();
+        } catch (...) {  // the destinations may be gone once the failure unwinds: never deliver them
+            rd_items.clear();
+            rd_off = 0;
+            throw;
+        }
         for (const RdItem& it : rd_items) memcpy(it.host, rd_area + it.off, it.bytes);
         rd_items.clear();
         rd_off = 0;

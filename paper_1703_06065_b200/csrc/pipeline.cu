@@ -30,11 +30,13 @@ Mat64::Mat64(Ctx* c, int64_t m_, int64_t n_)
     : buf(c, (size_t)std::max<int64_t>(1, m_) * std::max<int64_t>(1, n_) * sizeof(double)),
       m(m_), n(n_), ld(std::max<int64_t>(1, m_)) {}
 
+// (through the context's pinned read area: a copy into pageable memory — usually the caller's
+// stack — is staged by the driver and costs more per read; c2's greedy makes ~40 of them)
 template <class T>
 static void d2h(Ctx* c, T* host, const T* dev, size_t count) {
     if (!count) return;
-    CUDA_CHECK(cudaMemcpyAsync(host, dev, count * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
+    c->read_later(host, dev, count * sizeof(T));
+    c->read_all();
 }
 // host buffers may be stack-owned by the caller: small uploads go through the context's pinned
 // ring (no synchronization), large ones synchronize
@@ -305,8 +307,8 @@ static CholInfo chol_any(Ctx* c, const double* G, int64_t w, int64_t ldg, double
         X = Xown.p();
     }
     chol_enqueue(c, G, w, ldg, R, X, tc, st.as<int>(), want_r);
-    CUDA_CHECK(cudaMemcpyAsync(&hs, st.ptr, sizeof hs, cudaMemcpyDeviceToHost, c->stream));
-    c->sync();
+    c->read_later(&hs, st.ptr, sizeof hs);
+    c->read_all();
     return {hs.info, hs.info ? 0.0 : hs.mindiag, hs.maxdiag};
 }
 
