@@ -530,7 +530,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=10,
+                    help="timed end-to-end steps (capped by --steps); the first upload of the double-buffered "
+                         "pipeline has nothing to overlap with, so few steps under-state the steady rate")
     ap.add_argument("--e2e-serial", action="store_true", help="e2e without overlapping the next upload")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--residual", choices=["auto", "explicit", "pythagoras"], default="auto",

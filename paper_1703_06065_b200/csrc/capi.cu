@@ -328,9 +328,13 @@ bcur_status bcur_dmat_upload_async(bcur_ctx ctx, bcur_dmat a, const void* host, 
     CUDA_CHECK(cudaEventRecord(d->ready, c->stream));
     CUDA_CHECK(cudaStreamWaitEvent(c->up, d->ready, 0));
     const size_t es = dtype_size(d->dtype);
-    if (d->m * d->n > 0)
-        CUDA_CHECK(cudaMemcpy2DAsync(d->ptr, d->ld * es, host, ld_host * es, d->m * es, d->n, cudaMemcpyHostToDevice,
-                                     c->up));
+    if (d->m * d->n > 0) {
+        if (ld_host == d->m && d->ld == d->m)  // contiguous on both sides: one linear copy
+            CUDA_CHECK(cudaMemcpyAsync(d->ptr, host, (size_t)d->m * d->n * es, cudaMemcpyHostToDevice, c->up));
+        else
+            CUDA_CHECK(cudaMemcpy2DAsync(d->ptr, d->ld * es, host, ld_host * es, d->m * es, d->n, cudaMemcpyHostToDevice,
+                                         c->up));
+    }
     CUDA_CHECK(cudaEventRecord(d->ready, c->up));
     d->pending = true;
     API_END

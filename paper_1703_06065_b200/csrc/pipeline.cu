@@ -327,7 +327,10 @@ static void chol_later(Ctx* c, const double* G, int64_t w, int64_t ldg, double* 
 static CholInfo chol_info(const CholStat& hs) { return {hs.info, hs.info ? 0.0 : hs.mindiag, hs.maxdiag}; }
 
 int cholesky_inverse(Ctx* c, const double* G, int64_t w, int64_t ldg, double* R, double* Rinv, double* mindiag) {
-    const CholInfo ci = chol_any(c, G, w, ldg, R, Rinv);
+    // BCUR_CHOL_TC=1 (tests): the path the fp32 pipelines take for their bases' Grams — off-diagonal
+    // products on tcgen05 3×FP16, and for w ≥ 3072 the hybrid around two persistent launches
+    const bool tc = getenv("BCUR_CHOL_TC") != nullptr && w % 128 == 0;
+    const CholInfo ci = chol_any(c, G, w, ldg, R, Rinv, tc);
     if (mindiag) *mindiag = ci.mindiag;
     return ci.info;
 }

@@ -66,6 +66,28 @@ def test_cholesky_inverse(B, w):
     assert info2 == 0 and np.array_equal(r2, r)
 
 
+def test_cholesky_hybrid_tensor_core_products(B, monkeypatch):
+    """The factorization path of the fp32 pipelines' basis Grams at w >= 3072: one recursion level
+    around two persistent launches, the off-diagonal quarter on tcgen05 3xFP16 products (an
+    fp32-class result by design: the Gram it factors is one).  R, R^-1 and min diag are checked,
+    with R requested (the pipelines skip it)."""
+    w = 3072
+    gen = np.random.default_rng(11)
+    x = gen.standard_normal((w + 256, w)) / np.sqrt(w + 256.0)
+    g = np.asfortranarray(x.T @ x + 0.5 * np.eye(w))  # kappa ~ 10
+    monkeypatch.setenv("BCUR_CHOL_TC", "1")
+    r, ri, info, mn = B.cholesky(g)
+    monkeypatch.delenv("BCUR_CHOL_TC")
+    assert info == 0
+    ref = np.linalg.cholesky(g).T
+    assert np.allclose(np.tril(r, -1), 0.0) and np.allclose(np.tril(ri, -1), 0.0)
+    assert rel_fro(r, ref) < 1e-5
+    assert np.max(np.abs(ri @ ref - np.eye(w))) < 1e-4
+    assert mn == pytest.approx(float(np.min(np.diag(ref))), rel=1e-4)
+    r64, ri64, _, _ = B.cholesky(g)  # the fp64 path on the same input
+    assert rel_fro(r64, ref) < 1e-12
+
+
 @pytest.mark.parametrize("w,bad", [(50, 17), (200, 150), (700, 300), (700, 650)])
 def test_cholesky_reports_failed_pivot(B, w, bad):
     gen = np.random.default_rng(bad)

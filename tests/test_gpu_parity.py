@@ -116,6 +116,14 @@ def test_config1_full(B):
     assert got.plan.blocks() == ref.plan.blocks()
 
 
+@pytest.mark.parametrize("m,n,s,dt", [(333, 420, 7, np.float64), (333, 420, 7, np.float32), (250, 600, 12, np.float64)])
+def test_block_gather_odd_shapes(B, m, n, s, dt):
+    """The one-launch block gather (k_copy_segments) on blocks whose byte size or offset is not a
+    multiple of 16 (odd m: the 4-byte path) and on 16-byte aligned ones, against the oracle."""
+    a = lowrank(m, n, 9, "pow:1", 1e-3, 5, dt)
+    run_css(B, a, s, 6, 4, 1, 5, O.WITHOUT_REPLACEMENT, 2)
+
+
 def test_config2_full_greedy(B):
     c = O.CONFIGS["c2"]
     a = O.gen_biometric(c["m"], c["n"], c["seed"])
