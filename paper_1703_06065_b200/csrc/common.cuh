@@ -8,7 +8,6 @@
 
 #include <algorithm>
 #include <cstring>
-#include <chrono>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -149,22 +148,7 @@ struct Ctx {
         }
         return pinned;
     }
-    // Host wait for the stream.  The decision reads of the latency-bound configs (c1: 4 per
-    // decomposition, c2's greedy: ~45) wait microseconds: polling the stream first avoids the
-    // blocking wait's wake-up latency; after ~150 µs of polling it blocks (BCUR_SYNC_SPIN_US, 0 = off).
-    void sync() {
-        static const long spin_us = getenv("BCUR_SYNC_SPIN_US") ? atol(getenv("BCUR_SYNC_SPIN_US")) : 150;
-        if (spin_us > 0) {
-            const auto t0 = std::chrono::steady_clock::now();
-            for (;;) {
-                const cudaError_t e = cudaStreamQuery(stream);
-                if (e == cudaSuccess) return;
-                if (e != cudaErrorNotReady) CUDA_CHECK(e);
-                if (std::chrono::steady_clock::now() - t0 > std::chrono::microseconds(spin_us)) break;
-            }
-        }
-        CUDA_CHECK(cudaStreamSynchronize(stream));
-    }
+    void sync() { CUDA_CHECK(cudaStreamSynchronize(stream)); }
     std::map<void*, size_t> sizes;
 
     // Host → device uploads without a stream synchronization: the source is copied into a pinned
