@@ -1585,16 +1585,33 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     bool have_lev = false;
     Mat64 loc(c, std::max<int64_t>(1, s.g1 - s.g0), 1), upd(c, G, 1), rows(c, a->n, 1);
     out->steps.clear();
+    // Once the basis spans all m rows nothing can be added and no residual changes: a step that is
+    // saturated then stays saturated (the maximum runs over fewer blocks), so such steps reduce to
+    // the leverage argmax — one host read each — with the frozen residuals read once.  (c2, m = 64:
+    // seven of its eight steps; each used to run the two CGS2 passes, a Gram and a 100-wide
+    // Cholesky to find rank 0, ~185 µs and three reads per step: profiles/r02ax/step_c2.txt.)
+    bool frozen = false;
+    std::vector<double> res_frozen;
     for (int64_t t = 0; t < o.g; ++t) {
-        argmax_masked(c, res.p(), sel.as<unsigned char>(), G, didx.as<int64_t>(), didx.as<double>() + 1);
         struct { int64_t idx; double v1, v2; } hm;
-        d2h(c, reinterpret_cast<char*>(&hm), reinterpret_cast<const char*>(didx.ptr), 24);
         bcur_greedy_step st{};
-        st.block = hm.idx;
-        st.score = hm.v1;
-        st.margin = hm.v1 - hm.v2;
-        st.saturated = hm.v1 <= tau_saturate(dt) * a2 ? 1 : 0;
-        if (st.saturated) {
+        if (!frozen) {
+            argmax_masked(c, res.p(), sel.as<unsigned char>(), G, didx.as<int64_t>(), didx.as<double>() + 1);
+            d2h(c, reinterpret_cast<char*>(&hm), reinterpret_cast<const char*>(didx.ptr), 24);
+            st.block = hm.idx;
+            st.score = hm.v1;
+            st.margin = hm.v1 - hm.v2;
+            st.saturated = hm.v1 <= tau_saturate(dt) * a2 ? 1 : 0;
+        } else {
+            st.saturated = 1;
+        }
+        if (frozen) {
+            argmax_masked(c, lev.p(), sel.as<unsigned char>(), G, didx.as<int64_t>(), didx.as<double>() + 1);
+            d2h(c, reinterpret_cast<char*>(&hm), reinterpret_cast<const char*>(didx.ptr), 24);
+            st.block = hm.idx;
+            st.margin = hm.v1 - hm.v2;
+            st.score = res_frozen[hm.idx];
+        } else if (st.saturated) {
             if (!have_lev) {
                 Subspace sub;
                 range_finder(c, a, o.k, o.p, o.q, bcur_omega_key(o.seed), &sub, o.rank_floor != 0);
@@ -1614,16 +1631,24 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
         const unsigned char one = 1;
         h2d(c, sel.as<unsigned char>() + b, &one, 1);
         const int64_t w = offsets[b + 1] - offsets[b];
-        Mat64 P(c, m, w);
-        block_panel(c, a, s, b, P.p());
         const int64_t cur = B.rank;
-        const int64_t r = cgs2_append(c, &B, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)), dt, false);
+        int64_t r = 0;
+        if (B.rank < m) {  // (a basis of all m rows: every further panel has rank 0 against it)
+            Mat64 P(c, m, w);
+            block_panel(c, a, s, b, P.p());
+            r = cgs2_append(c, &B, P.p(), w, P.ld, std::sqrt(std::max(bn2[b], 0.0)), dt, false);
+        }
         if (r > 0) {
             // res_g −= ‖Q_newᵀ A_g‖²
             rowsq_pass(c, a, &ra, r, B.col(cur), B.dt, B.rows, rows.p());
             segment_sum(c, rows.p(), s.d_local.as<int64_t>(), s.g1 - s.g0, loc.p());
             gather_blocks_vec(c, s, loc.p(), upd.p());
             axpy_neg(c, upd.p(), res.p(), G);
+        }
+        if (st.saturated && B.rank >= m && have_lev && !frozen) {  // (after this step's update, if any)
+            frozen = true;
+            res_frozen.resize(G);
+            d2h(c, res_frozen.data(), res.p(), G);
         }
         st.rank_added = r;
         out->steps.push_back(st);
