@@ -195,9 +195,50 @@ __global__ void k_argmax(const double* __restrict__ x, const unsigned char* __re
     }
 }
 
+// `count` successive masked argmax picks in one launch (the greedy's frozen tail: each pick only
+// masks its block): out[t] = {index, best, second best} as k_argmax reports them, sel updated.
+__global__ void k_argmax_seq(const double* __restrict__ x, unsigned char* sel, int64_t G, int count,
+                             double* __restrict__ out) {
+    const int lane = threadIdx.x;
+    for (int t = 0; t < count; ++t) {
+        double b1 = -INFINITY, b2 = -INFINITY;
+        int64_t i1 = -1;
+        for (int64_t i = lane; i < G; i += 32) {
+            if (((volatile unsigned char*)sel)[i]) continue;
+            const double v = x[i];
+            if (v > b1) { b2 = b1; b1 = v; i1 = i; }
+            else if (v > b2) { b2 = v; }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // greater value wins; equal values → lower index
+            const double ob1 = __shfl_xor_sync(0xffffffffu, b1, o);
+            const double ob2 = __shfl_xor_sync(0xffffffffu, b2, o);
+            const int64_t oi1 = __shfl_xor_sync(0xffffffffu, i1, o);
+            const bool other_wins = (ob1 > b1) || (ob1 == b1 && oi1 >= 0 && (i1 < 0 || oi1 < i1));
+            const double n2 = other_wins ? fmax(b1, ob2) : fmax(ob1, b2);
+            if (other_wins) { b1 = ob1; i1 = oi1; }
+            b2 = n2;
+        }
+        if (lane == 0) {
+            out[3 * t] = (double)i1;
+            out[3 * t + 1] = b1;
+            out[3 * t + 2] = b2;
+            if (i1 >= 0) sel[i1] = 1;
+        }
+        __threadfence_block();
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 namespace ops {
+
+void argmax_masked_seq(Ctx* c, const double* x, unsigned char* mask_selected, int64_t G, int count, double* out3) {
+    if (count <= 0) return;
+    k_argmax_seq<<<1, 32, 0, c->stream>>>(x, mask_selected, G, count, out3);
+    LAUNCH_CHECK(c);
+}
 
 void distribution_draw(Ctx* c, const double* d_scores, int64_t G, int normalize, int64_t g, int mode,
                        const double* d_uniforms, bcur_block_draw* d_draws, double* d_margins, int* d_status) {

@@ -237,6 +237,8 @@ void gather_blocks(Ctx* c, const void* a, int dt, int64_t m, int64_t n, int64_t 
                    const bcur_block_draw* d_draws, const int64_t* d_dst_off, int64_t ndraws, int rows, int scaled,
                    void* out, int dto, int64_t ldo);
 // argmax over unselected entries (ties → lowest index); out_vals = {top1, top2}
+// count successive picks, each masking its block: out3[3t..] = {index (as double), best, second best}
+void argmax_masked_seq(Ctx* c, const double* x, unsigned char* mask_selected, int64_t G, int count, double* out3);
 void argmax_masked(Ctx* c, const double* x, const unsigned char* mask_selected, int64_t G, int64_t* out_idx,
                    double* out_vals);
 

@@ -1591,7 +1591,8 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
     // seven of its eight steps; each used to run the two CGS2 passes, a Gram and a 100-wide
     // Cholesky to find rank 0, ~185 µs and three reads per step: profiles/r02ax/step_c2.txt.)
     bool frozen = false;
-    std::vector<double> res_frozen;
+    std::vector<double> res_frozen, picks;
+    int64_t pick0 = 0;
     for (int64_t t = 0; t < o.g; ++t) {
         struct { int64_t idx; double v1, v2; } hm;
         bcur_greedy_step st{};
@@ -1606,11 +1607,21 @@ void greedy_select(Ctx* c, const DMat* a, const int64_t* offsets, int64_t G, con
             st.saturated = 1;
         }
         if (frozen) {
-            argmax_masked(c, lev.p(), sel.as<unsigned char>(), G, didx.as<int64_t>(), didx.as<double>() + 1);
-            d2h(c, reinterpret_cast<char*>(&hm), reinterpret_cast<const char*>(didx.ptr), 24);
-            st.block = hm.idx;
-            st.margin = hm.v1 - hm.v2;
-            st.score = res_frozen[hm.idx];
+            if (picks.empty()) {  // every remaining pick in one launch and one read
+                const int count = (int)(o.g - t);
+                Mat64 dp(c, 3, count);
+                argmax_masked_seq(c, lev.p(), sel.as<unsigned char>(), G, count, dp.p());
+                picks.resize((size_t)3 * count);
+                d2h(c, picks.data(), dp.p(), picks.size());
+                pick0 = t;
+            }
+            const double* pk = picks.data() + 3 * (t - pick0);
+            st.block = (int64_t)pk[0];
+            st.margin = pk[1] - pk[2];
+            st.score = res_frozen[st.block];
+            st.rank_added = 0;
+            out->steps.push_back(st);
+            continue;  // (sel was updated on the device; nothing is added and no residual changes)
         } else if (st.saturated) {
             if (!have_lev) {
                 Subspace sub;
